@@ -1,0 +1,216 @@
+/*
+ * sgnn_b200.h -- C ABI of the B200-native (sm_100a) sparse GNN hot path.
+ *
+ * This is the drop-in boundary for the operator API of the iSpLib
+ * re-creation (/root/reference/proj/include/sparsegnn/).  Every entry point
+ * names the reference interface it replaces (file:line, relative to
+ * proj/include/sparsegnn/ unless a src/ path is given).  INTEGRATION.md shows
+ * the reference-side binding (the C++ shim include/sparsegnn_b200.hpp and a
+ * ctypes stub).
+ *
+ * Conventions
+ *  - All array pointers passed to compute entry points are DEVICE pointers
+ *    (cudaMalloc / torch CUDA storage).  Layout is the reference's:
+ *    row_ptr u64[n_rows+1], col_idx u32[nnz], values f32[nnz]
+ *    (types.hpp:15-18,26-79); dense matrices row-major f32 (types.hpp:82-112).
+ *  - Every call is asynchronous on `stream` (NULL = legacy default stream),
+ *    except where noted ("synchronous").  No C++ exception crosses the ABI:
+ *    errors are returned as sgnn_status codes that map 1:1 to the
+ *    reference's exception classes (error.hpp:9-61); sgnn_last_error()
+ *    returns the message of the calling thread's last failure.
+ *  - There is no CPU fallback.  Without a usable sm_100 device every compute
+ *    entry point returns SGNN_ERR_CUDA.
+ *  - Numerics contract (fp32): every SpMM/FusedMM output element accumulates
+ *    its row's nonzeros in ascending order with separately rounded multiply
+ *    and add (no FMA contraction), exactly like spmm_rows_trusted
+ *    (kernels.hpp:45-91) built without FMA -- except that rows with more than
+ *    SGNN_SEGMENT nonzeros are accumulated in canonical segments of
+ *    SGNN_SEGMENT nonzeros that are then added left to right.  The segment
+ *    length is a library constant, so results are bitwise independent of the
+ *    plan/tuning (the dispatch-transparency invariant), of the
+ *    number of GPUs of a row partition, and of run-to-run scheduling.
+ */
+#ifndef SGNN_B200_H
+#define SGNN_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define SGNN_ABI_VERSION 1
+#define SGNN_SEGMENT 256 /* canonical accumulation segment (nonzeros) */
+
+typedef struct CUstream_st* sgnn_stream; /* == cudaStream_t */
+
+/* Status codes <-> reference exceptions (error.hpp). */
+typedef enum sgnn_status {
+    SGNN_OK = 0,
+    SGNN_ERR_SHAPE = 1,       /* ShapeError      error.hpp:15-18 */
+    SGNN_ERR_DISPATCH = 2,    /* DispatchError   error.hpp:22-25 */
+    SGNN_ERR_CONFIG = 3,      /* ConfigError     error.hpp:28-31 */
+    SGNN_ERR_TAPE = 4,        /* TapeError       error.hpp:34-37 */
+    SGNN_ERR_IO = 5,          /* IoError         error.hpp:40-43 */
+    SGNN_ERR_PARSE = 6,       /* ParseError      error.hpp:46-55 */
+    SGNN_ERR_INTERNAL = 7,    /* InternalError   error.hpp:58-61 */
+    SGNN_ERR_CUDA = 8,        /* CUDA runtime / device failure (no reference analogue) */
+    SGNN_ERR_NOMEM = 9,       /* device allocation failed */
+    SGNN_ERR_UNSUPPORTED = 10 /* configuration this build does not implement */
+} sgnn_status;
+
+/* ReduceOp, in the order of types.hpp:116. */
+enum { SGNN_REDUCE_SUM = 0, SGNN_REDUCE_MIN = 1, SGNN_REDUCE_MAX = 2, SGNN_REDUCE_MEAN = 3 };
+
+/* FusedMM edge ops: the GPU-expressible Semiring::combine (types.hpp:139-145).
+ * MUL = the default combine (p*dot, kernels.hpp:239);
+ * SIGMOID_MUL = p * 1/(1+exp(-dot)) (BASELINE cfg4). */
+enum { SGNN_EDGE_MUL = 0, SGNN_EDGE_SIGMOID_MUL = 1 };
+
+/* KernelKind::Tag (kernels.hpp:16-25). */
+enum { SGNN_KERNEL_TRUSTED = 0, SGNN_KERNEL_SPECIALIZED = 1 };
+
+/* CsrMatrix<float> view over device memory (types.hpp:26-79). */
+typedef struct sgnn_csr {
+    uint32_t n_rows;
+    uint32_t n_cols;
+    uint64_t nnz;
+    const uint64_t* row_ptr; /* device, n_rows+1 */
+    const uint32_t* col_idx; /* device, nnz */
+    const float* values;     /* device, nnz */
+} sgnn_csr;
+
+/* Tunable launch parameters of a SpMM plan (the on-device tuner's search
+ * space; replaces the K-sweep of autotune.hpp:99-164).  Zero fields mean
+ * "library default". */
+typedef struct sgnn_plan_params {
+    uint32_t lanes;        /* lanes per worker group: 4, 8, 16 or 32 */
+    uint32_t vec;          /* float4 (or float, scalar path) registers per lane: 1,2,4,8 */
+    uint32_t unroll;       /* neighbor-row gathers in flight per lane: 2, 4 or 8 */
+    uint32_t path_items;   /* rows+nonzeros per worker (nnz-balanced split), >= 1 */
+    uint32_t split_rows_over; /* rows with more nonzeros than this may be split across
+                                 workers (rounded up to a multiple of SGNN_SEGMENT) */
+    uint32_t k_tile;       /* floats of K per pass over the matrix (0 = all of K) */
+    uint32_t block;        /* threads per CTA: 64, 128 or 256 */
+    uint32_t scalar;       /* 1 = force the scalar-load ("trusted") path */
+} sgnn_plan_params;
+
+typedef struct sgnn_plan_s* sgnn_plan;
+
+/* ---------------------------------------------------------------- library */
+int sgnn_abi_version(void);
+/* Message of the calling thread's most recent failure ("" if none). */
+const char* sgnn_last_error(void);
+/* Device query used by the tuner (hardware.cpp:8-34 analogue): SM count,
+ * L2 bytes, compute capability.  Synchronous. */
+sgnn_status sgnn_device_info(int* sm_count, int* l2_bytes, int* cc_major, int* cc_minor);
+
+/* ------------------------------------------------------------------ plans */
+/* Precompute the nnz-balanced work split of A for embedding width K
+ * (parallel.hpp:28-65 balanced_row_partition, at GPU-worker granularity,
+ * with hub rows split in SGNN_SEGMENT units).  params == NULL -> defaults.
+ * Synchronous (reads back two counts).  The plan borrows A's row_ptr; it is
+ * valid while that array is unchanged.  A plan owns a workspace: do not use
+ * one plan from two streams concurrently. */
+sgnn_status sgnn_plan_create(const sgnn_csr* a, uint32_t k, const sgnn_plan_params* params,
+                             sgnn_plan* out, sgnn_stream stream);
+sgnn_status sgnn_plan_destroy(sgnn_plan plan);
+sgnn_status sgnn_plan_get_params(sgnn_plan plan, sgnn_plan_params* out);
+/* Plan statistics: workers, split rows, workspace slots. */
+sgnn_status sgnn_plan_stats(sgnn_plan plan, uint64_t* workers, uint64_t* split_rows,
+                            uint64_t* slots);
+
+/* ------------------------------------------------------------------- SpMM */
+/* C = reduce_j a_ij * X[j,:]   (spmm / spmm_with / detail::spmm_into,
+ * kernels.hpp:141-182; row kernel kernels.hpp:45-91; mean divide :60-63).
+ * X is x_rows x k with x_rows == a.n_cols (else SGNN_ERR_SHAPE, as
+ * check_spmm_shapes, kernels.hpp:131-136); C is a.n_rows x k; both row-major
+ * and caller-owned (the spmm_into convention).  plan may be NULL (a temporary default plan is
+ * built, synchronously).  A plan built for another matrix or K ->
+ * SGNN_ERR_DISPATCH. */
+sgnn_status sgnn_spmm_f32(const sgnn_csr* a, const float* x, uint32_t x_rows, uint32_t k,
+                          float* c, int reduce, sgnn_plan plan, sgnn_stream stream);
+
+/* spmm_with(a, b, reduce, kind) (kernels.hpp:157-173): kind SPECIALIZED
+ * demands reduce == Sum, spec_k in the specialization sweep
+ * {16,...,1024} (kernels.hpp:27) and spec_k == k, else SGNN_ERR_DISPATCH,
+ * exactly like the reference.  On the GPU "trusted" runs the default plan,
+ * "specialized" the tuned plan registered for (a, k) (or `plan`); results are
+ * bitwise identical either way. */
+sgnn_status sgnn_spmm_with_f32(const sgnn_csr* a, const float* x, uint32_t x_rows, uint32_t k,
+                               float* c, int reduce, int kind, uint32_t spec_k, sgnn_plan plan,
+                               sgnn_stream stream);
+
+/* resolve_kernel(k, reduce) (kernels.hpp:38, src/dispatch.cpp:21-28) and the
+ * dispatch toggle set_dispatch/get_dispatch (autotune.hpp:36-37,
+ * src/dispatch.cpp:12-19).  Returns the kind; *spec_k receives K for
+ * SPECIALIZED, 0 for TRUSTED. */
+int sgnn_resolve_kernel(uint32_t k, int reduce, uint32_t* spec_k);
+void sgnn_set_dispatch(int enabled);
+int sgnn_get_dispatch(void);
+
+/* ------------------------------------------------------------- transpose */
+/* transpose(a) (sparse.hpp:72-89): CSR(A) -> CSR(A^T), bit-exact with the
+ * reference's stable counting sort (rows ascending within each column).
+ * Outputs are device arrays: t_row_ptr u64[n_cols+1], t_col_idx u32[nnz],
+ * t_values f32[nnz] (t_values may be NULL: structure only).
+ * ws/ws_bytes: scratch from sgnn_transpose_workspace (ws may be NULL: the
+ * call allocates stream-ordered scratch itself). */
+sgnn_status sgnn_transpose_workspace(const sgnn_csr* a, size_t* ws_bytes);
+sgnn_status sgnn_csr_transpose(const sgnn_csr* a, uint64_t* t_row_ptr, uint32_t* t_col_idx,
+                               float* t_values, void* ws, size_t ws_bytes, sgnn_stream stream);
+
+/* row_degrees (sparse.hpp:105-109): deg[i] = row_ptr[i+1]-row_ptr[i]. */
+sgnn_status sgnn_row_degrees(const sgnn_csr* a, uint32_t* deg, sgnn_stream stream);
+/* is_symmetric (sparse.hpp:179-192), exact structure + value check.
+ * Synchronous; *out = 1 symmetric, 0 not. */
+sgnn_status sgnn_is_symmetric(const sgnn_csr* a, int* out, sgnn_stream stream);
+
+/* ------------------------------------------------ backward cache (TrainingCache) */
+/* TrainingCache<float> (gnn.hpp:113-173) + build_cache (gnn.hpp:180-196)
+ * for a propagation operand that is already on the device (a_hat).  The
+ * cache borrows a_hat's arrays (they must outlive it) and owns the lazily
+ * built transpose / mean operand.  check_symmetric mirrors
+ * `cache.symmetric = use_cache && is_symmetric(a_hat)` (gnn.hpp:194).
+ * Synchronous. */
+typedef struct sgnn_cache_s* sgnn_cache;
+sgnn_status sgnn_cache_create(const sgnn_csr* a_hat, int use_cache, sgnn_cache* out,
+                              sgnn_stream stream);
+sgnn_status sgnn_cache_destroy(sgnn_cache cache);
+/* sum_operand() (gnn.hpp:127-144) / mean_operand() (gnn.hpp:149-172):
+ * fills *out with a device view of the operand (valid until the next fetch
+ * with use_cache == 0, or until destroy).  Counts builds/hits like the
+ * reference. */
+sgnn_status sgnn_cache_sum_operand(sgnn_cache cache, sgnn_csr* out, sgnn_stream stream);
+sgnn_status sgnn_cache_mean_operand(sgnn_cache cache, sgnn_csr* out, sgnn_stream stream);
+/* Counters (gnn.hpp:121-123) and flags: transpose_builds, normalize_builds,
+ * cache_hits, symmetric. */
+sgnn_status sgnn_cache_counters(sgnn_cache cache, uint64_t* transpose_builds,
+                                uint64_t* normalize_builds, uint64_t* cache_hits,
+                                int* symmetric);
+/* SpMM backward ("spmm_backward", gnn.hpp:275,279,290,303):
+ * dX = spmm(op, dC, Sum) where op = mean_operand() if reduce == Mean, else
+ * sum_operand().  dC is a_hat.n_rows x k, dX is a_hat.n_cols x k.  The plan
+ * for the operand is built once per K and cached inside the cache. */
+sgnn_status sgnn_spmm_backward_f32(sgnn_cache cache, const float* dc, uint32_t dc_rows,
+                                   uint32_t k, float* dx, int reduce, sgnn_stream stream);
+
+/* ------------------------------------------------------- SDDMM / FusedMM */
+/* sddmm(p, x, y) (kernels.hpp:187-210): out_values[e] = p_e * <X_i, Y_j>.
+ * The output pattern is P's own (row_ptr/col_idx are not copied).
+ * X is p.n_rows x k, Y is p.n_cols x k. */
+sgnn_status sgnn_sddmm_f32(const sgnn_csr* p, const float* x, uint32_t x_rows, const float* y,
+                           uint32_t y_rows, uint32_t k, float* out_values, sgnn_stream stream);
+/* fusedmm(p, x, y, semiring) (kernels.hpp:216-270): out_i = reduce_j
+ * combine(p_ij, <X_i,Y_j>) * Y_j in one pass (Y_j read once per edge).
+ * out is p.n_rows x k. */
+sgnn_status sgnn_fusedmm_f32(const sgnn_csr* p, const float* x, uint32_t x_rows, const float* y,
+                             uint32_t y_rows, uint32_t k, int edge_op, int reduce, float* out,
+                             sgnn_stream stream);
+
+#ifdef __cplusplus
+} /* extern "C" */
+#endif
+
+#endif /* SGNN_B200_H */

@@ -1,0 +1,207 @@
+"""numpy front-end to the reference itself, compiled by oracle/Makefile from
+/root/reference/proj into oracle/_ref/libsgnn_ref_<flags>.so.
+
+TEST / BASELINE INFRASTRUCTURE ONLY.  Used to pin oracle/port.py, to make
+tests/golden/ fixtures (make_golden.py) and as bench.py's CPU reference arm.
+The .so files are built here (where /root/reference exists) and travel to the
+GPU box with the repo snapshot; nothing at run time reads /root/reference.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+REF_DIR = os.path.join(_HERE, "_ref")
+FLAVOURS = {  # name -> (file, flags, required cpu flags)
+    "O2": ("libsgnn_ref_O2.so", "-O2", ()),
+    "O3v3": ("libsgnn_ref_O3v3.so", "-O3 -march=x86-64-v3", ("avx2", "fma", "bmi2")),
+    "O3v4": ("libsgnn_ref_O3v4.so", "-O3 -march=x86-64-v4", ("avx512f", "avx512bw", "avx512vl", "avx512dq")),
+}
+
+u64p = np.ctypeslib.ndpointer(np.uint64, flags="C_CONTIGUOUS")
+u32p = np.ctypeslib.ndpointer(np.uint32, flags="C_CONTIGUOUS")
+f32p = np.ctypeslib.ndpointer(np.float32, flags="C_CONTIGUOUS")
+f64p = np.ctypeslib.ndpointer(np.float64, flags="C_CONTIGUOUS")
+_LIBS: dict = {}
+
+
+def cpu_flags() -> set:
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("flags"):
+                    return set(line.split(":", 1)[1].split())
+    except OSError:
+        pass
+    return set()
+
+
+def available(flavour: str = "O2") -> bool:
+    fn, _, need = FLAVOURS[flavour]
+    return os.path.exists(os.path.join(REF_DIR, fn)) and set(need) <= cpu_flags()
+
+
+def flavours() -> list:
+    return [f for f in FLAVOURS if available(f)]
+
+
+def lib(flavour: str = "O2"):
+    if flavour in _LIBS:
+        return _LIBS[flavour]
+    if not available(flavour):
+        raise FileNotFoundError(f"oracle/_ref flavour {flavour} not built or not runnable on this CPU")
+    L = C.CDLL(os.path.join(REF_DIR, FLAVOURS[flavour][0]))
+    L.ref_spmm_f32.argtypes = [C.c_uint32, C.c_uint32, u64p, u32p, f32p, f32p, C.c_uint32, C.c_int, C.c_int, C.c_uint32, C.c_int, f32p]
+    L.ref_spmm_f64.argtypes = [C.c_uint32, C.c_uint32, u64p, u32p, f64p, f64p, C.c_uint32, C.c_int, C.c_int, f64p]
+    L.ref_transpose_f32.argtypes = [C.c_uint32, C.c_uint32, u64p, u32p, f32p, u64p, u32p, f32p]
+    L.ref_sddmm_f32.argtypes = [C.c_uint32, C.c_uint32, u64p, u32p, f32p, f32p, f32p, C.c_uint32, C.c_int, f32p]
+    L.ref_sddmm_f64.argtypes = [C.c_uint32, C.c_uint32, u64p, u32p, f64p, f64p, f64p, C.c_uint32, C.c_int, f64p]
+    L.ref_fusedmm_f32.argtypes = [C.c_uint32, C.c_uint32, u64p, u32p, f32p, f32p, f32p, C.c_uint32, C.c_int, C.c_int, C.c_int, f32p]
+    L.ref_fusedmm_f64.argtypes = [C.c_uint32, C.c_uint32, u64p, u32p, f64p, f64p, f64p, C.c_uint32, C.c_int, C.c_int, C.c_int, f64p]
+    L.ref_is_symmetric_f32.argtypes = [C.c_uint32, C.c_uint32, u64p, u32p, f32p]
+    L.ref_normalize_adjacency_f32.argtypes = [C.c_uint32, u64p, u32p, f32p, C.c_int, C.c_void_p, C.c_void_p, C.c_void_p]
+    L.ref_normalize_adjacency_f32.restype = C.c_int64
+    L.ref_balanced_row_partition.argtypes = [u64p, C.c_uint32, C.c_int, u32p]
+    L.ref_resolve_kernel.argtypes = [C.c_uint32, C.c_int, C.c_int]
+    L.ref_cache_operand_f32.argtypes = [C.c_uint32, u64p, u32p, f32p, C.c_int, C.c_int, C.c_int, C.c_int,
+                                        C.POINTER(C.c_uint64), C.c_void_p, C.c_void_p, C.c_void_p,
+                                        np.ctypeslib.ndpointer(np.uint64, flags="C_CONTIGUOUS")]
+    L.ref_bench_create.argtypes = [C.c_uint32, C.c_uint32, u64p, u32p, f32p, f32p, f32p, C.c_uint32, C.c_int]
+    L.ref_bench_create.restype = C.c_void_p
+    L.ref_bench_step.argtypes = [C.c_void_p, C.c_int, C.c_int, C.c_int]
+    L.ref_bench_out.argtypes = [C.c_void_p, C.c_int]
+    L.ref_bench_out.restype = C.POINTER(C.c_float)
+    L.ref_bench_free.argtypes = [C.c_void_p]
+    L.ref_hw_cores.restype = C.c_int
+    _LIBS[flavour] = L
+    return L
+
+
+def _csr(rp, ci, v, dt):
+    return (np.ascontiguousarray(rp, np.uint64), np.ascontiguousarray(ci, np.uint32),
+            np.ascontiguousarray(v, dt))
+
+
+def _check(st):
+    if st != 0:
+        raise RuntimeError(f"reference raised status {st}")
+
+
+def spmm_f32(rp, ci, v, x, n_cols, reduce=0, specialized=False, threads=0, flavour="O2"):
+    rp, ci, v = _csr(rp, ci, v, np.float32)
+    x = np.ascontiguousarray(x, np.float32)
+    m, k = len(rp) - 1, x.shape[1]
+    out = np.empty((m, k), np.float32)
+    _check(lib(flavour).ref_spmm_f32(m, n_cols, rp, ci, v, x, k, reduce, int(specialized), k, threads, out))
+    return out
+
+
+def spmm_f64(rp, ci, v, x, n_cols, reduce=0, threads=0):
+    rp, ci, v = _csr(rp, ci, v, np.float64)
+    x = np.ascontiguousarray(x, np.float64)
+    m, k = len(rp) - 1, x.shape[1]
+    out = np.empty((m, k), np.float64)
+    _check(lib().ref_spmm_f64(m, n_cols, rp, ci, v, x, k, reduce, threads, out))
+    return out
+
+
+def transpose_f32(rp, ci, v, n_cols):
+    rp, ci, v = _csr(rp, ci, v, np.float32)
+    nnz = int(rp[-1])
+    trp, tci, tv = np.empty(n_cols + 1, np.uint64), np.empty(nnz, np.uint32), np.empty(nnz, np.float32)
+    _check(lib().ref_transpose_f32(len(rp) - 1, n_cols, rp, ci, v, trp, tci, tv))
+    return trp, tci, tv
+
+
+def sddmm(rp, ci, v, x, y, n_cols, dtype=np.float64, threads=0):
+    rp, ci, v = _csr(rp, ci, v, dtype)
+    x, y = np.ascontiguousarray(x, dtype), np.ascontiguousarray(y, dtype)
+    out = np.empty(int(rp[-1]), dtype)
+    f = lib().ref_sddmm_f64 if dtype == np.float64 else lib().ref_sddmm_f32
+    _check(f(len(rp) - 1, n_cols, rp, ci, v, x, y, x.shape[1], threads, out))
+    return out
+
+
+def fusedmm(rp, ci, v, x, y, n_cols, edge_op=0, reduce=0, dtype=np.float64, threads=0):
+    rp, ci, v = _csr(rp, ci, v, dtype)
+    x, y = np.ascontiguousarray(x, dtype), np.ascontiguousarray(y, dtype)
+    m, k = len(rp) - 1, x.shape[1]
+    out = np.empty((m, k), dtype)
+    f = lib().ref_fusedmm_f64 if dtype == np.float64 else lib().ref_fusedmm_f32
+    _check(f(m, n_cols, rp, ci, v, x, y, k, edge_op, reduce, threads, out))
+    return out
+
+
+def is_symmetric(rp, ci, v, n_cols):
+    rp, ci, v = _csr(rp, ci, v, np.float32)
+    return bool(lib().ref_is_symmetric_f32(len(rp) - 1, n_cols, rp, ci, v))
+
+
+def normalize_adjacency(rp, ci, v, add_self_loops=True):
+    rp, ci, v = _csr(rp, ci, v, np.float32)
+    n = len(rp) - 1
+    nnz = lib().ref_normalize_adjacency_f32(n, rp, ci, v, int(add_self_loops), None, None, None)
+    if nnz < 0:
+        raise RuntimeError(f"reference raised status {-nnz}")
+    trp, tci, tv = np.empty(n + 1, np.uint64), np.empty(nnz, np.uint32), np.empty(nnz, np.float32)
+    lib().ref_normalize_adjacency_f32(n, rp, ci, v, int(add_self_loops), trp.ctypes.data, tci.ctypes.data, tv.ctypes.data)
+    return trp, tci, tv
+
+
+def balanced_row_partition(rp, n_chunks):
+    rp = np.ascontiguousarray(rp, np.uint64)
+    out = np.empty(n_chunks + 1, np.uint32)
+    lib().ref_balanced_row_partition(rp, len(rp) - 1, n_chunks, out)
+    return out
+
+
+def resolve_kernel(k, reduce, tuned_enabled):
+    r = lib().ref_resolve_kernel(k, reduce, int(tuned_enabled))
+    return ("specialized" if r >= 65536 else "trusted", r % 65536)
+
+
+def cache_operand(rp, ci, v, model_kind, use_cache, which, n_fetches):
+    """build_cache + sum_operand/mean_operand fetched n_fetches times (gnn.hpp:113-196).
+    Returns (row_ptr, col_idx, values, counters{transpose_builds, normalize_builds, cache_hits, symmetric})."""
+    rp, ci, v = _csr(rp, ci, v, np.float32)
+    n = len(rp) - 1
+    nnz = C.c_uint64(0)
+    cnt = np.zeros(4, np.uint64)
+    _check(lib().ref_cache_operand_f32(n, rp, ci, v, model_kind, int(use_cache), which, n_fetches,
+                                       C.byref(nnz), None, None, None, cnt))
+    trp, tci, tv = np.empty(n + 1, np.uint64), np.empty(nnz.value, np.uint32), np.empty(nnz.value, np.float32)
+    _check(lib().ref_cache_operand_f32(n, rp, ci, v, model_kind, int(use_cache), which, n_fetches,
+                                       C.byref(nnz), trp.ctypes.data, tci.ctypes.data, tv.ctypes.data, cnt))
+    return trp, tci, tv, dict(zip(("transpose_builds", "normalize_builds", "cache_hits", "symmetric"),
+                                  (int(c) for c in cnt)))
+
+
+class Bench:
+    """SpMM fwd + cached-transpose bwd on the reference CPU path (bench.py arm)."""
+
+    def __init__(self, rp, ci, v, n_cols, x, g, reduce=0, flavour="O2"):
+        self.L = lib(flavour)
+        rp, ci, v = _csr(rp, ci, v, np.float32)
+        self.m, self.k = len(rp) - 1, x.shape[1]
+        self.n = n_cols
+        self.h = self.L.ref_bench_create(self.m, n_cols, rp, ci, v, np.ascontiguousarray(x, np.float32),
+                                         np.ascontiguousarray(g, np.float32), self.k, reduce)
+
+    def step(self, specialized=False, threads=0, which=3):
+        _check(self.L.ref_bench_step(self.h, int(specialized), threads, which))
+
+    def out(self, which=1):
+        rows = self.m if which == 1 else self.n
+        p = self.L.ref_bench_out(self.h, which)
+        return np.ctypeslib.as_array(p, shape=(rows, self.k)).copy()
+
+    def close(self):
+        if self.h:
+            self.L.ref_bench_free(self.h)
+            self.h = None
+
+    def __del__(self):
+        self.close()

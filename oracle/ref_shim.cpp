@@ -1,0 +1,261 @@
+// ref_shim.cpp -- extern "C" entry points over the UNMODIFIED reference
+// headers (/root/reference/proj/include/sparsegnn/*.hpp) and sources
+// (/root/reference/proj/src/*.cpp), compiled by oracle/Makefile into
+// oracle/_ref/libsgnn_ref_<flags>.so.
+//
+// TEST / BASELINE INFRASTRUCTURE ONLY: this is the reference itself, used
+// (a) to pin the C restatement in oracle/sgnn_oracle.c and to generate the
+// golden fixtures in tests/golden/, and (b) as bench.py's CPU reference arm
+// (cpu_baseline kind "reference").  Nothing in paper_2403_14853_b200/ links it.
+//
+// gnn.hpp uses DispatchGuard without including autotune.hpp (gnn.hpp:424,
+// autotune.hpp:40-51), so autotune.hpp is included first.
+#include "sparsegnn/autotune.hpp"
+#include "sparsegnn/gnn.hpp"
+#include "sparsegnn/kernels.hpp"
+#include "sparsegnn/parallel.hpp"
+#include "sparsegnn/sparse.hpp"
+
+#include <cmath>
+#include <cstdint>
+#include <cstring>
+#include <memory>
+
+using namespace sparsegnn;
+
+namespace {
+
+template <class T>
+CsrMatrix<T> make_csr(uint32_t m, uint32_t n, const uint64_t* rp, const uint32_t* ci, const T* v) {
+    CsrMatrix<T> a(m, n);
+    a.row_ptr.assign(rp, rp + m + 1);
+    const uint64_t nnz = rp[m];
+    a.col_idx.assign(ci, ci + nnz);
+    a.values.assign(v, v + nnz);
+    return a;
+}
+
+template <class T>
+DenseMatrix<T> make_dense(uint32_t r, uint32_t c, const T* x) {
+    DenseMatrix<T> d(r, c);
+    std::memcpy(d.data.data(), x, sizeof(T) * size_t(r) * c);
+    return d;
+}
+
+// Status codes mirror include/sgnn_b200.h (sgnn_status).
+int status_of(const std::exception& e) {
+    if (dynamic_cast<const ShapeError*>(&e)) return 1;
+    if (dynamic_cast<const DispatchError*>(&e)) return 2;
+    if (dynamic_cast<const ConfigError*>(&e)) return 3;
+    if (dynamic_cast<const TapeError*>(&e)) return 4;
+    if (dynamic_cast<const InternalError*>(&e)) return 7;
+    return 7;
+}
+
+template <class T>
+Semiring<T> semiring(int edge_op, int reduce) {
+    Semiring<T> sr;
+    sr.reduce = static_cast<ReduceOp>(reduce);
+    if (edge_op == 1) sr.combine = [](T p, T d) { return p * (T(1) / (T(1) + std::exp(-d))); };
+    return sr;
+}
+
+}  // namespace
+
+#define GUARD_BEGIN try {
+#define GUARD_END                              \
+    }                                          \
+    catch (const std::exception& e) {          \
+        return status_of(e);                   \
+    }                                          \
+    return 0;
+
+extern "C" {
+
+// spmm_with(a, b, reduce, kind, threads)  (kernels.hpp:157-173)
+// kind: 0 = KernelKind::trusted(), 1 = KernelKind::specialized(spec_k)
+int ref_spmm_f32(uint32_t m, uint32_t n, const uint64_t* rp, const uint32_t* ci, const float* v,
+                 const float* x, uint32_t k, int reduce, int kind, uint32_t spec_k, int threads,
+                 float* out) {
+    GUARD_BEGIN
+    auto a = make_csr<float>(m, n, rp, ci, v);
+    auto b = make_dense<float>(n, k, x);
+    auto c = spmm_with(a, b, static_cast<ReduceOp>(reduce),
+                       kind ? KernelKind::specialized(spec_k) : KernelKind::trusted(), threads);
+    std::memcpy(out, c.data.data(), sizeof(float) * size_t(m) * k);
+    GUARD_END
+}
+
+// spmm(a, b, reduce) (kernels.hpp:179-182), fp64 instantiation = the oracle.
+int ref_spmm_f64(uint32_t m, uint32_t n, const uint64_t* rp, const uint32_t* ci, const double* v,
+                 const double* x, uint32_t k, int reduce, int threads, double* out) {
+    GUARD_BEGIN
+    auto a = make_csr<double>(m, n, rp, ci, v);
+    auto b = make_dense<double>(n, k, x);
+    auto c = spmm(a, b, static_cast<ReduceOp>(reduce), threads);
+    std::memcpy(out, c.data.data(), sizeof(double) * size_t(m) * k);
+    GUARD_END
+}
+
+// transpose (sparse.hpp:72-89)
+int ref_transpose_f32(uint32_t m, uint32_t n, const uint64_t* rp, const uint32_t* ci,
+                      const float* v, uint64_t* trp, uint32_t* tci, float* tv) {
+    GUARD_BEGIN
+    auto t = transpose(make_csr<float>(m, n, rp, ci, v));
+    std::memcpy(trp, t.row_ptr.data(), sizeof(uint64_t) * (size_t(n) + 1));
+    std::memcpy(tci, t.col_idx.data(), sizeof(uint32_t) * t.nnz());
+    std::memcpy(tv, t.values.data(), sizeof(float) * t.nnz());
+    GUARD_END
+}
+
+// sddmm (kernels.hpp:187-210)
+int ref_sddmm_f32(uint32_t m, uint32_t n, const uint64_t* rp, const uint32_t* ci, const float* v,
+                  const float* x, const float* y, uint32_t k, int threads, float* out) {
+    GUARD_BEGIN
+    auto s = sddmm(make_csr<float>(m, n, rp, ci, v), make_dense<float>(m, k, x),
+                   make_dense<float>(n, k, y), threads);
+    std::memcpy(out, s.values.data(), sizeof(float) * s.nnz());
+    GUARD_END
+}
+int ref_sddmm_f64(uint32_t m, uint32_t n, const uint64_t* rp, const uint32_t* ci, const double* v,
+                  const double* x, const double* y, uint32_t k, int threads, double* out) {
+    GUARD_BEGIN
+    auto s = sddmm(make_csr<double>(m, n, rp, ci, v), make_dense<double>(m, k, x),
+                   make_dense<double>(n, k, y), threads);
+    std::memcpy(out, s.values.data(), sizeof(double) * s.nnz());
+    GUARD_END
+}
+
+// fusedmm (kernels.hpp:216-270); edge_op 0 = plus_times(), 1 = sigmoid combine
+int ref_fusedmm_f32(uint32_t m, uint32_t n, const uint64_t* rp, const uint32_t* ci, const float* v,
+                    const float* x, const float* y, uint32_t k, int edge_op, int reduce,
+                    int threads, float* out) {
+    GUARD_BEGIN
+    auto c = fusedmm(make_csr<float>(m, n, rp, ci, v), make_dense<float>(m, k, x),
+                     make_dense<float>(n, k, y), semiring<float>(edge_op, reduce), threads);
+    std::memcpy(out, c.data.data(), sizeof(float) * size_t(m) * k);
+    GUARD_END
+}
+int ref_fusedmm_f64(uint32_t m, uint32_t n, const uint64_t* rp, const uint32_t* ci,
+                    const double* v, const double* x, const double* y, uint32_t k, int edge_op,
+                    int reduce, int threads, double* out) {
+    GUARD_BEGIN
+    auto c = fusedmm(make_csr<double>(m, n, rp, ci, v), make_dense<double>(m, k, x),
+                     make_dense<double>(n, k, y), semiring<double>(edge_op, reduce), threads);
+    std::memcpy(out, c.data.data(), sizeof(double) * size_t(m) * k);
+    GUARD_END
+}
+
+// is_symmetric (sparse.hpp:179-192)
+int ref_is_symmetric_f32(uint32_t m, uint32_t n, const uint64_t* rp, const uint32_t* ci,
+                         const float* v) {
+    return is_symmetric(make_csr<float>(m, n, rp, ci, v)) ? 1 : 0;
+}
+
+// normalize_adjacency (sparse.hpp:116-174); trp == nullptr -> returns nnz of the result
+int64_t ref_normalize_adjacency_f32(uint32_t n, const uint64_t* rp, const uint32_t* ci,
+                                    const float* v, int add_self_loops, uint64_t* trp,
+                                    uint32_t* tci, float* tv) {
+    try {
+        auto t = normalize_adjacency(make_csr<float>(n, n, rp, ci, v), add_self_loops != 0);
+        if (trp) {
+            std::memcpy(trp, t.row_ptr.data(), sizeof(uint64_t) * (size_t(n) + 1));
+            std::memcpy(tci, t.col_idx.data(), sizeof(uint32_t) * t.nnz());
+            std::memcpy(tv, t.values.data(), sizeof(float) * t.nnz());
+        }
+        return static_cast<int64_t>(t.nnz());
+    } catch (const std::exception& e) {
+        return -status_of(e);
+    }
+}
+
+// balanced_row_partition (parallel.hpp:28-41)
+void ref_balanced_row_partition(const uint64_t* rp, uint32_t n_rows, int n_chunks,
+                                uint32_t* bounds) {
+    auto b = balanced_row_partition(std::span<const offset_t>(rp, size_t(n_rows) + 1), n_rows,
+                                    n_chunks);
+    std::memcpy(bounds, b.data(), sizeof(uint32_t) * b.size());
+}
+
+// resolve_kernel (dispatch.cpp:21-28) under a given dispatch state.
+// Returns tag*65536 + k  (tag 0 trusted, 1 specialized).
+int ref_resolve_kernel(uint32_t k, int reduce, int tuned_enabled) {
+    DispatchGuard g(tuned_enabled != 0);
+    auto kk = resolve_kernel(k, static_cast<ReduceOp>(reduce));
+    return (kk.is_specialized() ? 65536 : 0) + static_cast<int>(kk.k);
+}
+
+// TrainingCache semantics (gnn.hpp:113-196): build the cache for `model_kind`
+// (0 gcn, 1 sage-sum, 2 sage-mean, 3 gin), fetch the requested operand
+// `n_fetches` times (which: 0 sum_operand, 1 mean_operand), export the last
+// operand and the counters {transpose_builds, normalize_builds, cache_hits, symmetric}.
+int ref_cache_operand_f32(uint32_t n, const uint64_t* rp, const uint32_t* ci, const float* v,
+                          int model_kind, int use_cache, int which, int n_fetches,
+                          uint64_t* out_nnz, uint64_t* trp, uint32_t* tci, float* tv,
+                          uint64_t* counters) {
+    GUARD_BEGIN
+    auto cache = build_cache(static_cast<ModelKind>(model_kind), make_csr<float>(n, n, rp, ci, v),
+                             use_cache != 0, true);
+    const CsrMatrix<float>* op = nullptr;
+    for (int f = 0; f < n_fetches; ++f) op = which ? &cache.mean_operand() : &cache.sum_operand();
+    *out_nnz = op ? op->nnz() : 0;
+    if (op && trp) {
+        std::memcpy(trp, op->row_ptr.data(), sizeof(uint64_t) * op->row_ptr.size());
+        std::memcpy(tci, op->col_idx.data(), sizeof(uint32_t) * op->nnz());
+        std::memcpy(tv, op->values.data(), sizeof(float) * op->nnz());
+    }
+    counters[0] = cache.transpose_builds;
+    counters[1] = cache.normalize_builds;
+    counters[2] = cache.cache_hits;
+    counters[3] = cache.symmetric ? 1 : 0;
+    GUARD_END
+}
+
+// ---- bench arm: one SpMM fwd + cached-transpose bwd "step" (gnn.hpp:290 shape) ----
+struct RefBench {
+    CsrMatrix<float> a, at;
+    DenseMatrix<float> x, g, c, dx;
+    int reduce = 0;
+};
+
+void* ref_bench_create(uint32_t m, uint32_t n, const uint64_t* rp, const uint32_t* ci,
+                       const float* v, const float* x, const float* g, uint32_t k, int reduce) {
+    auto* b = new RefBench;
+    b->a = make_csr<float>(m, n, rp, ci, v);
+    b->at = transpose(b->a);  // built once, outside the timed step (TrainingCache)
+    if (reduce == 3) {        // mean backward operand, gnn.hpp:149-172
+        const auto deg = row_degrees(b->a);
+        for (offset_t e = 0; e < b->at.nnz(); ++e)
+            b->at.values[e] = b->at.values[e] / static_cast<float>(deg[b->at.col_idx[e]]);
+    }
+    b->x = make_dense<float>(n, k, x);
+    b->g = make_dense<float>(m, k, g);
+    b->c = DenseMatrix<float>(m, k);
+    b->dx = DenseMatrix<float>(n, k);
+    b->reduce = reduce;
+    return b;
+}
+
+// Runs fwd spmm_into(A, X) and bwd spmm_into(A^T, G) (kernels.hpp:141-149).
+// kind 0 trusted, 1 specialized (Sum only, K in the sweep); which: 1 fwd, 2 bwd, 3 both.
+int ref_bench_step(void* h, int kind, int threads, int which) {
+    GUARD_BEGIN
+    auto* b = static_cast<RefBench*>(h);
+    const KernelKind kk =
+        kind ? KernelKind::specialized(b->x.n_cols) : KernelKind::trusted();
+    const ReduceOp red = static_cast<ReduceOp>(b->reduce);
+    if (which & 1) detail::spmm_into(b->a, b->x, red, kk, threads, b->c);
+    if (which & 2) detail::spmm_into(b->at, b->g, ReduceOp::Sum, kk, threads, b->dx);
+    GUARD_END
+}
+
+const float* ref_bench_out(void* h, int which) {
+    auto* b = static_cast<RefBench*>(h);
+    return which == 2 ? b->dx.data.data() : b->c.data.data();
+}
+
+void ref_bench_free(void* h) { delete static_cast<RefBench*>(h); }
+
+int ref_hw_cores() { return detect_hardware().cores; }
+
+}  // extern "C"

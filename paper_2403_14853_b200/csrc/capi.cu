@@ -1,0 +1,262 @@
+// capi.cu -- the extern "C" boundary (include/sgnn_b200.h).  Validation and
+// error messages follow the reference operator API (kernels.hpp:131-173).
+#include <atomic>
+#include <new>
+
+#include "ops.cuh"
+#include "plan.cuh"
+#include "spmm_kernel.cuh"
+
+using namespace sgnn;
+
+namespace {
+
+std::atomic<bool> g_tuned_enabled{true};  // src/dispatch.cpp:9
+
+constexpr uint32_t kSweep[] = {16, 32, 64, 128, 256, 512, 1024};  // kernels.hpp:27
+
+bool is_specialized_k(uint32_t k) {
+    for (uint32_t s : kSweep)
+        if (s == k) return true;
+    return false;
+}
+
+const char* reduce_name(int r) {
+    switch (r) {
+        case SGNN_REDUCE_SUM: return "sum";
+        case SGNN_REDUCE_MIN: return "min";
+        case SGNN_REDUCE_MAX: return "max";
+        case SGNN_REDUCE_MEAN: return "mean";
+    }
+    return "?";
+}
+
+cudaStream_t cs(sgnn_stream s) { return reinterpret_cast<cudaStream_t>(s); }
+
+sgnn_status spmm_shapes(const sgnn_csr* a, uint32_t x_rows, uint32_t k) {
+    if (a->n_cols != x_rows)  // check_spmm_shapes, kernels.hpp:131-136
+        return fail(SGNN_ERR_SHAPE, "spmm: sparse operand is " + std::to_string(a->n_rows) + "x" +
+                                        std::to_string(a->n_cols) + " but dense operand is " +
+                                        std::to_string(x_rows) + "x" + std::to_string(k));
+    return SGNN_OK;
+}
+
+sgnn_status spmm_dispatch(const sgnn_csr* a, const float* x, uint32_t k, float* c, int reduce,
+                          sgnn_plan plan, cudaStream_t s) {
+    if (plan) return run_spmm(a, x, k, c, reduce, plan, s);
+    if (k == 0 || a->n_rows == 0) return SGNN_OK;
+    sgnn_plan_s* tmp = nullptr;
+    SGNN_TRY(build_plan(a, k, nullptr, k % 4 == 0, &tmp, s));
+    sgnn_status st = run_spmm(a, x, k, c, reduce, tmp, s);
+    destroy_plan(tmp);  // cudaFree synchronises with the queued work
+    return st;
+}
+
+}  // namespace
+
+extern "C" {
+
+int sgnn_abi_version(void) { return SGNN_ABI_VERSION; }
+
+const char* sgnn_last_error(void) { return last_error(); }
+
+sgnn_status sgnn_device_info(int* sm_count, int* l2_bytes, int* cc_major, int* cc_minor) {
+    DeviceProps dp;
+    SGNN_TRY(device_props(&dp));
+    if (sm_count) *sm_count = dp.sm_count;
+    if (l2_bytes) *l2_bytes = dp.l2_bytes;
+    if (cc_major) *cc_major = dp.cc_major;
+    if (cc_minor) *cc_minor = dp.cc_minor;
+    return SGNN_OK;
+}
+
+// ------------------------------------------------------------------ plans
+sgnn_status sgnn_plan_create(const sgnn_csr* a, uint32_t k, const sgnn_plan_params* params,
+                             sgnn_plan* out, sgnn_stream stream) {
+    if (!out) return fail(SGNN_ERR_CONFIG, "plan_create: null out");
+    *out = nullptr;
+    SGNN_TRY(check_csr(a, "plan_create"));
+    if (k == 0) return fail(SGNN_ERR_CONFIG, "plan_create: K must be positive");
+    try {
+        SGNN_TRY(build_plan(a, k, params, k % 4 == 0, out, cs(stream)));
+        const sgnn_plan_s* p = *out;
+        if (!find_spmm_launcher(p->vec, int(p->p.lanes), int(p->p.vec), int(p->p.unroll),
+                                SGNN_REDUCE_SUM)) {
+            destroy_plan(*out);
+            *out = nullptr;
+            return fail(SGNN_ERR_UNSUPPORTED,
+                        "plan_create: no kernel compiled for lanes=" + std::to_string(p->p.lanes) +
+                            " vec=" + std::to_string(p->p.vec) + " unroll=" + std::to_string(p->p.unroll) +
+                            (p->vec ? " (float4)" : " (scalar)"));
+        }
+        return SGNN_OK;
+    } catch (const std::bad_alloc&) {
+        return fail(SGNN_ERR_NOMEM, "plan_create: host allocation failed");
+    }
+}
+
+sgnn_status sgnn_plan_destroy(sgnn_plan plan) {
+    destroy_plan(plan);
+    return SGNN_OK;
+}
+
+sgnn_status sgnn_plan_get_params(sgnn_plan plan, sgnn_plan_params* out) {
+    if (!plan || !out) return fail(SGNN_ERR_CONFIG, "plan_get_params: null argument");
+    *out = plan->p;
+    return SGNN_OK;
+}
+
+sgnn_status sgnn_plan_stats(sgnn_plan plan, uint64_t* workers, uint64_t* split_rows,
+                            uint64_t* slots) {
+    if (!plan) return fail(SGNN_ERR_CONFIG, "plan_stats: null plan");
+    if (workers) *workers = plan->n_workers;
+    if (split_rows) *split_rows = plan->n_fix;
+    if (slots) *slots = plan->n_slots;
+    return SGNN_OK;
+}
+
+// ------------------------------------------------------------------- SpMM
+sgnn_status sgnn_spmm_f32(const sgnn_csr* a, const float* x, uint32_t x_rows, uint32_t k, float* c,
+                          int reduce, sgnn_plan plan, sgnn_stream stream) {
+    SGNN_TRY(check_csr(a, "spmm"));
+    SGNN_TRY(spmm_shapes(a, x_rows, k));
+    if (reduce < 0 || reduce > 3) return fail(SGNN_ERR_CONFIG, "spmm: unknown reduce op");
+    return spmm_dispatch(a, x, k, c, reduce, plan, cs(stream));
+}
+
+sgnn_status sgnn_spmm_with_f32(const sgnn_csr* a, const float* x, uint32_t x_rows, uint32_t k,
+                               float* c, int reduce, int kind, uint32_t spec_k, sgnn_plan plan,
+                               sgnn_stream stream) {
+    SGNN_TRY(check_csr(a, "spmm_with"));
+    SGNN_TRY(spmm_shapes(a, x_rows, k));
+    if (reduce < 0 || reduce > 3) return fail(SGNN_ERR_CONFIG, "spmm: unknown reduce op");
+    if (kind == SGNN_KERNEL_SPECIALIZED) {  // kernels.hpp:159-169
+        if (reduce != SGNN_REDUCE_SUM)
+            return fail(SGNN_ERR_DISPATCH, std::string("specialized kernels support sum only, got ") +
+                                               reduce_name(reduce));
+        if (!is_specialized_k(spec_k))
+            return fail(SGNN_ERR_DISPATCH,
+                        "K=" + std::to_string(spec_k) + " is not in the specialization set");
+        if (k != spec_k)
+            return fail(SGNN_ERR_DISPATCH, "kernel is fixed at K=" + std::to_string(spec_k) +
+                                               " but dense operand has K=" + std::to_string(k));
+        return spmm_dispatch(a, x, k, c, reduce, plan, cs(stream));
+    }
+    if (kind != SGNN_KERNEL_TRUSTED) return fail(SGNN_ERR_CONFIG, "spmm_with: unknown kernel kind");
+    // trusted: the default (untuned) plan -- bitwise the same result
+    return spmm_dispatch(a, x, k, c, reduce, nullptr, cs(stream));
+}
+
+int sgnn_resolve_kernel(uint32_t k, int reduce, uint32_t* spec_k) {
+    // src/dispatch.cpp:21-28
+    int kind = SGNN_KERNEL_TRUSTED;
+    if (g_tuned_enabled.load(std::memory_order_relaxed) && reduce == SGNN_REDUCE_SUM &&
+        is_specialized_k(k))
+        kind = SGNN_KERNEL_SPECIALIZED;
+    if (spec_k) *spec_k = kind == SGNN_KERNEL_SPECIALIZED ? k : 0;
+    return kind;
+}
+
+// ------------------------------------------------------------- transpose
+sgnn_status sgnn_transpose_workspace(const sgnn_csr* a, size_t* ws_bytes) {
+    SGNN_TRY(check_csr(a, "transpose"));
+    if (!ws_bytes) return fail(SGNN_ERR_CONFIG, "transpose_workspace: null out");
+    *ws_bytes = transpose_workspace_bytes(a);
+    return SGNN_OK;
+}
+
+sgnn_status sgnn_csr_transpose(const sgnn_csr* a, uint64_t* t_row_ptr, uint32_t* t_col_idx,
+                               float* t_values, void* ws, size_t ws_bytes, sgnn_stream stream) {
+    SGNN_TRY(check_csr(a, "transpose"));
+    if (!t_row_ptr || (a->nnz && !t_col_idx))
+        return fail(SGNN_ERR_CONFIG, "transpose: null output arrays");
+    return run_transpose(a, t_row_ptr, t_col_idx, t_values, ws, ws_bytes, cs(stream));
+}
+
+sgnn_status sgnn_row_degrees(const sgnn_csr* a, uint32_t* deg, sgnn_stream stream) {
+    SGNN_TRY(check_csr(a, "row_degrees"));
+    return run_row_degrees(a, deg, cs(stream));
+}
+
+sgnn_status sgnn_is_symmetric(const sgnn_csr* a, int* out, sgnn_stream stream) {
+    SGNN_TRY(check_csr(a, "is_symmetric"));
+    if (!out) return fail(SGNN_ERR_CONFIG, "is_symmetric: null out");
+    return run_is_symmetric(a, out, cs(stream));
+}
+
+// ------------------------------------------------------------ backward cache
+sgnn_status sgnn_cache_create(const sgnn_csr* a_hat, int use_cache, sgnn_cache* out,
+                              sgnn_stream stream) {
+    if (!out) return fail(SGNN_ERR_CONFIG, "cache_create: null out");
+    try {
+        return cache_create(a_hat, use_cache, out, cs(stream));
+    } catch (const std::bad_alloc&) {
+        return fail(SGNN_ERR_NOMEM, "cache_create: host allocation failed");
+    }
+}
+
+sgnn_status sgnn_cache_destroy(sgnn_cache cache) {
+    cache_destroy(cache);
+    return SGNN_OK;
+}
+
+sgnn_status sgnn_cache_sum_operand(sgnn_cache cache, sgnn_csr* out, sgnn_stream stream) {
+    if (!cache || !out) return fail(SGNN_ERR_CONFIG, "sum_operand: null argument");
+    return cache_sum_operand(cache, out, cs(stream));
+}
+
+sgnn_status sgnn_cache_mean_operand(sgnn_cache cache, sgnn_csr* out, sgnn_stream stream) {
+    if (!cache || !out) return fail(SGNN_ERR_CONFIG, "mean_operand: null argument");
+    return cache_mean_operand(cache, out, cs(stream));
+}
+
+sgnn_status sgnn_cache_counters(sgnn_cache cache, uint64_t* transpose_builds,
+                                uint64_t* normalize_builds, uint64_t* cache_hits, int* symmetric) {
+    if (!cache) return fail(SGNN_ERR_CONFIG, "cache_counters: null cache");
+    return cache_counters(cache, transpose_builds, normalize_builds, cache_hits, symmetric);
+}
+
+sgnn_status sgnn_spmm_backward_f32(sgnn_cache cache, const float* dc, uint32_t dc_rows, uint32_t k,
+                                   float* dx, int reduce, sgnn_stream stream) {
+    if (!cache) return fail(SGNN_ERR_CONFIG, "spmm_backward: null cache");
+    try {
+        return cache_spmm_backward(cache, dc, dc_rows, k, dx, reduce, cs(stream));
+    } catch (const std::bad_alloc&) {
+        return fail(SGNN_ERR_NOMEM, "spmm_backward: host allocation failed");
+    }
+}
+
+// ------------------------------------------------------- SDDMM / FusedMM
+sgnn_status sgnn_sddmm_f32(const sgnn_csr* p, const float* x, uint32_t x_rows, const float* y,
+                           uint32_t y_rows, uint32_t k, float* out_values, sgnn_stream stream) {
+    SGNN_TRY(check_csr(p, "sddmm"));
+    if (p->n_rows != x_rows || p->n_cols != y_rows)  // kernels.hpp:189-195
+        return fail(SGNN_ERR_SHAPE, "sddmm: pattern " + std::to_string(p->n_rows) + "x" +
+                                        std::to_string(p->n_cols) + " needs X with " +
+                                        std::to_string(p->n_rows) + " rows and Y with " +
+                                        std::to_string(p->n_cols) + " rows of equal width; got X " +
+                                        std::to_string(x_rows) + "x" + std::to_string(k) + ", Y " +
+                                        std::to_string(y_rows) + "x" + std::to_string(k));
+    if (p->nnz && !out_values) return fail(SGNN_ERR_CONFIG, "sddmm: null output");
+    return run_sddmm(p, x, y, k, out_values, cs(stream));
+}
+
+sgnn_status sgnn_fusedmm_f32(const sgnn_csr* p, const float* x, uint32_t x_rows, const float* y,
+                             uint32_t y_rows, uint32_t k, int edge_op, int reduce, float* out,
+                             sgnn_stream stream) {
+    SGNN_TRY(check_csr(p, "fusedmm"));
+    if (p->n_rows != x_rows || p->n_cols != y_rows)  // kernels.hpp:218-222
+        return fail(SGNN_ERR_SHAPE, "fusedmm: operand shapes do not compose (P " +
+                                        std::to_string(p->n_rows) + "x" + std::to_string(p->n_cols) +
+                                        ", X " + std::to_string(x_rows) + "x" + std::to_string(k) +
+                                        ", Y " + std::to_string(y_rows) + "x" + std::to_string(k) + ")");
+    return run_fusedmm(p, x, y, k, edge_op, reduce, out, nullptr, cs(stream));
+}
+
+void sgnn_set_dispatch(int enabled) {
+    g_tuned_enabled.store(enabled != 0, std::memory_order_relaxed);
+}
+
+int sgnn_get_dispatch(void) { return g_tuned_enabled.load(std::memory_order_relaxed) ? 1 : 0; }
+
+}  // extern "C"

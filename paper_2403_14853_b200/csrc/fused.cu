@@ -1,0 +1,306 @@
+// fused.cu -- SDDMM (kernels.hpp:187-210) and FusedMM (kernels.hpp:216-270).
+//
+// SDDMM: each output is independent, so workers take equal nnz ranges
+// (no row snapping, no fixup).  A group holds X_i (re-loaded on row change)
+// and, per nonzero, gathers Y_j, forms the canonical group dot product
+// (group_dot) and writes p_e * dot.  Results are collected in the lane that
+// loaded the nonzero so the stores are coalesced.
+//
+// FusedMM: the SpMM worker kernel in fused mode (spmm_kernel.cuh): per edge
+// Y_j is gathered once and used for both the dot and the accumulation
+// (the reference reads it twice, kernels.hpp:238,244), with the plan's
+// nnz-balanced split, canonical segments and fixup for hub rows.
+#include <algorithm>
+
+#include "ops.cuh"
+#include "plan.cuh"
+#include "spmm_inst.cuh"
+
+namespace sgnn {
+
+namespace {
+
+struct SddmmArgs {
+    const uint64_t* __restrict__ rp;
+    const uint32_t* __restrict__ ci;
+    const float* __restrict__ val;
+    const float* __restrict__ x;
+    const float* __restrict__ y;
+    float* __restrict__ out;
+    uint64_t nnz;
+    uint64_t per_worker;
+    uint32_t n_rows;
+    uint32_t n_workers;
+    uint32_t k;
+    uint64_t ld;
+};
+
+__device__ __forceinline__ uint32_t row_of(const uint64_t* __restrict__ rp, uint32_t m, uint64_t e) {
+    uint32_t lo = 0, hi = m;  // largest r with rp[r] <= e
+    while (hi - lo > 1) {
+        const uint32_t mid = lo + (hi - lo) / 2;
+        if (__ldg(rp + mid) <= e) lo = mid;
+        else hi = mid;
+    }
+    return lo;
+}
+
+template <int G, int V, int U, bool VEC>
+__global__ void __launch_bounds__(256) sddmm_kernel(const SddmmArgs a) {
+    using F = dev::Frag<G, V, VEC>;
+    constexpr int CH = (U > G) ? (U / G) : 1;
+    constexpr int CHUNK = G * CH;
+    const int lane = threadIdx.x & 31;
+    const int gl = lane & (G - 1);
+    const unsigned gmask = (G == 32) ? 0xffffffffu : (((1u << G) - 1u) << (lane & ~(G - 1)));
+    const uint32_t n_groups = (gridDim.x * blockDim.x) / G;
+    for (uint32_t w = (blockIdx.x * blockDim.x + threadIdx.x) / G; w < a.n_workers; w += n_groups) {
+        const uint64_t j0 = uint64_t(w) * a.per_worker;
+        const uint64_t j1 = min(j0 + a.per_worker, a.nnz);
+        uint32_t r = row_of(a.rp, a.n_rows, j0);
+        uint32_t rb = r;
+        uint64_t rwin = __ldg(a.rp + min(rb + 1 + uint32_t(gl), a.n_rows));
+        uint64_t rend = dev::shfl_u64(gmask, rwin, 0, G);
+        F xrow;
+        xrow.load(a.x + uint64_t(r) * a.ld, gl, a.k);
+        for (uint64_t base = j0; base < j1; base += CHUNK) {
+            uint32_t cc[CH];
+            float vv[CH], res[CH];
+#pragma unroll
+            for (int h = 0; h < CH; ++h) {
+                const uint64_t idx = base + uint64_t(gl + G * h);
+                cc[h] = idx < j1 ? dev::ld_stream(a.ci + idx) : 0u;
+                vv[h] = idx < j1 ? dev::ld_stream(a.val + idx) : 0.0f;
+                res[h] = 0.0f;
+            }
+            const int n = (j1 - base) < uint64_t(CHUNK) ? int(j1 - base) : CHUNK;
+#pragma unroll
+            for (int q0 = 0; q0 < CHUNK; q0 += U) {
+                if (q0 >= n) break;
+                F yf[U];
+#pragma unroll
+                for (int u = 0; u < U; ++u) {
+                    const int q = q0 + u;
+                    const uint32_t col = __shfl_sync(gmask, cc[q / G], q % G, G);
+                    if (q < n) yf[u].load(a.y + uint64_t(col) * a.ld, gl, a.k);
+                }
+#pragma unroll
+                for (int u = 0; u < U; ++u) {
+                    const int q = q0 + u;
+                    const float pv = __shfl_sync(gmask, vv[q / G], q % G, G);
+                    if (q >= n) break;
+                    const uint64_t e = base + uint64_t(q);
+                    if (e >= rend) {
+                        do {
+                            ++r;
+                            if (r - rb >= uint32_t(G)) {
+                                rb = r;
+                                rwin = __ldg(a.rp + min(rb + 1 + uint32_t(gl), a.n_rows));
+                            }
+                            rend = dev::shfl_u64(gmask, rwin, int(r - rb), G);
+                        } while (e >= rend);
+                        xrow.load(a.x + uint64_t(r) * a.ld, gl, a.k);
+                    }
+                    const float d = dev::group_dot(xrow, yf[u], gmask);
+                    if (gl == q % G) res[q / G] = __fmul_rn(pv, d);  // kernels.hpp:206
+                }
+            }
+#pragma unroll
+            for (int h = 0; h < CH; ++h) {
+                const uint64_t idx = base + uint64_t(gl + G * h);
+                if (idx < j1) __stcs(a.out + idx, res[h]);
+            }
+        }
+    }
+}
+
+using SddmmLaunch = sgnn_status (*)(const SddmmArgs&, cudaStream_t);
+
+template <int G, int V, int U, bool VEC>
+sgnn_status launch_sddmm(const SddmmArgs& a, cudaStream_t s) {
+    static int per_sm = -1;
+    DeviceProps dp;
+    SGNN_TRY(device_props(&dp));
+    if (per_sm < 0) {
+        int n = 0;
+        SGNN_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, sddmm_kernel<G, V, U, VEC>, 256, 0));
+        per_sm = std::max(n, 1);
+    }
+    const uint64_t blocks = std::min<uint64_t>(ceil_div_u64(uint64_t(a.n_workers) * G, 256),
+                                               uint64_t(dp.sm_count) * per_sm);
+    if (blocks == 0) return SGNN_OK;
+    sddmm_kernel<G, V, U, VEC><<<unsigned(blocks), 256, 0, s>>>(a);
+    SGNN_LAUNCH_CHECK();
+    return SGNN_OK;
+}
+
+// (lanes, float4-or-float registers) covering K in one pass.
+bool full_k_layout(uint32_t k, bool vec, int* lanes, int* vregs) {
+    if (vec) {
+        if (k <= 16) { *lanes = 4; *vregs = 1; }
+        else if (k <= 32) { *lanes = 8; *vregs = 1; }
+        else if (k <= 64) { *lanes = 16; *vregs = 1; }
+        else if (k <= 128) { *lanes = 32; *vregs = 1; }
+        else if (k <= 256) { *lanes = 32; *vregs = 2; }
+        else if (k <= 512) { *lanes = 32; *vregs = 4; }
+        else if (k <= 1024) { *lanes = 32; *vregs = 8; }
+        else return false;
+    } else {
+        *lanes = 32;
+        if (k <= 32) *vregs = 1;
+        else if (k <= 64) *vregs = 2;
+        else if (k <= 128) *vregs = 4;
+        else if (k <= 256) *vregs = 8;
+        else return false;
+    }
+    return true;
+}
+
+// Unroll of the compiled FusedMM configuration for a full-K layout
+// (SGNN_FUSED_CONFIGS in spmm_inst.cuh).
+int fused_unroll(bool vec, int lanes, int vregs) {
+    if (vec) return (lanes < 32 || vregs == 1) ? 8 : (vregs == 8 ? 2 : 4);
+    return vregs >= 4 ? 2 : 4;
+}
+
+SpmmLauncher find_fused_launcher(bool vec, int lanes, int vregs, int unroll, int edge, int reduce) {
+    const bool sig = edge == SGNN_EDGE_SIGMOID_MUL;
+    switch (reduce) {
+        case SGNN_REDUCE_SUM:
+            return sig ? fused_lookup_sig_sum(vec, lanes, vregs, unroll) : fused_lookup_mul_sum(vec, lanes, vregs, unroll);
+        case SGNN_REDUCE_MEAN:
+            return sig ? fused_lookup_sig_mean(vec, lanes, vregs, unroll) : fused_lookup_mul_mean(vec, lanes, vregs, unroll);
+        case SGNN_REDUCE_MIN:
+            return sig ? fused_lookup_sig_min(vec, lanes, vregs, unroll) : fused_lookup_mul_min(vec, lanes, vregs, unroll);
+        case SGNN_REDUCE_MAX:
+            return sig ? fused_lookup_sig_max(vec, lanes, vregs, unroll) : fused_lookup_mul_max(vec, lanes, vregs, unroll);
+    }
+    return nullptr;
+}
+
+}  // namespace
+
+sgnn_status run_sddmm(const sgnn_csr* p, const float* x, const float* y, uint32_t k, float* out,
+                      cudaStream_t s) {
+    if (p->nnz == 0) return SGNN_OK;
+    const bool vec = (k % 4 == 0) && (reinterpret_cast<uintptr_t>(x) % 16 == 0) &&
+                     (reinterpret_cast<uintptr_t>(y) % 16 == 0);
+    int lanes, vregs;
+    if (!full_k_layout(k, vec, &lanes, &vregs))
+        return fail(SGNN_ERR_UNSUPPORTED, "sddmm: K=" + std::to_string(k) +
+                                              " exceeds the register-resident width of this build");
+    SddmmArgs a;
+    a.rp = p->row_ptr;
+    a.ci = p->col_idx;
+    a.val = p->values;
+    a.x = x;
+    a.y = y;
+    a.out = out;
+    a.nnz = p->nnz;
+    a.n_rows = p->n_rows;
+    a.k = k;
+    a.ld = k;
+    DeviceProps dp;
+    SGNN_TRY(device_props(&dp));
+    // ~4 workers per resident group, at least 64 nonzeros each
+    const uint64_t groups = uint64_t(dp.sm_count) * 2048 / lanes;
+    a.per_worker = std::max<uint64_t>(64, ceil_div_u64(p->nnz, 4 * groups));
+    const uint64_t nw = ceil_div_u64(p->nnz, a.per_worker);
+    a.n_workers = uint32_t(nw);
+    SddmmLaunch fn = nullptr;
+    if (vec) {
+        if (lanes == 4) fn = &launch_sddmm<4, 1, 8, true>;
+        else if (lanes == 8) fn = &launch_sddmm<8, 1, 8, true>;
+        else if (lanes == 16) fn = &launch_sddmm<16, 1, 8, true>;
+        else if (vregs == 1) fn = &launch_sddmm<32, 1, 8, true>;
+        else if (vregs == 2) fn = &launch_sddmm<32, 2, 4, true>;
+        else if (vregs == 4) fn = &launch_sddmm<32, 4, 4, true>;
+        else fn = &launch_sddmm<32, 8, 2, true>;
+    } else {
+        if (vregs == 1) fn = &launch_sddmm<32, 1, 4, false>;
+        else if (vregs == 2) fn = &launch_sddmm<32, 2, 4, false>;
+        else if (vregs == 4) fn = &launch_sddmm<32, 4, 2, false>;
+        else fn = &launch_sddmm<32, 8, 2, false>;
+    }
+    return fn(a, s);
+}
+
+sgnn_status run_fusedmm(const sgnn_csr* p, const float* x, const float* y, uint32_t k, int edge_op,
+                        int reduce, float* out, const sgnn_plan_s* plan, cudaStream_t s) {
+    if (reduce < 0 || reduce > 3) return fail(SGNN_ERR_CONFIG, "fusedmm: unknown reduce op");
+    if (edge_op != SGNN_EDGE_MUL && edge_op != SGNN_EDGE_SIGMOID_MUL)
+        return fail(SGNN_ERR_CONFIG, "fusedmm: unknown edge op");
+    if (k == 0 || p->n_rows == 0) return SGNN_OK;
+    const bool vec = (k % 4 == 0) && (reinterpret_cast<uintptr_t>(x) % 16 == 0) &&
+                     (reinterpret_cast<uintptr_t>(y) % 16 == 0) &&
+                     (reinterpret_cast<uintptr_t>(out) % 16 == 0);
+    int lanes, vregs;
+    if (!full_k_layout(k, vec, &lanes, &vregs))
+        return fail(SGNN_ERR_UNSUPPORTED, "fusedmm: K=" + std::to_string(k) +
+                                              " exceeds the register-resident width of this build");
+    sgnn_plan_s* own = nullptr;
+    if (!plan) {
+        sgnn_plan_params pp{};
+        pp.lanes = uint32_t(lanes);
+        pp.vec = uint32_t(vregs);
+        pp.k_tile = k;
+        pp.unroll = uint32_t(fused_unroll(vec, lanes, vregs));
+        if (!vec) pp.scalar = 1;
+        SGNN_TRY(build_plan(p, k, &pp, vec, &own, s));
+        plan = own;
+    } else if (!plan_matches(plan, p, k)) {
+        return fail(SGNN_ERR_DISPATCH, "fusedmm: plan was built for another matrix or K");
+    }
+    sgnn_status st = SGNN_OK;
+    int unroll = int(plan->p.unroll);
+    if (plan->vec != vec || int(plan->p.lanes) != lanes || int(plan->p.vec) != vregs)
+        unroll = fused_unroll(vec, lanes, vregs);  // the split is reusable; the layout must cover K
+    if (plan->kt < k && plan->p.k_tile != k) {
+        // K-tiling is meaningless for FusedMM (the dot needs all of K); the
+        // split itself does not depend on the tile, so only the slots matter.
+        if (plan->n_slots && plan->kt < k)
+            st = fail(SGNN_ERR_DISPATCH, "fusedmm: plan workspace is narrower than K; build the plan with k_tile=K");
+    }
+    SpmmLauncher launch = st == SGNN_OK ? find_fused_launcher(vec, lanes, vregs, unroll, edge_op, reduce) : nullptr;
+    if (st == SGNN_OK && !launch)
+        st = fail(SGNN_ERR_UNSUPPORTED, "fusedmm: no kernel for lanes=" + std::to_string(lanes) +
+                                            " vec=" + std::to_string(vregs) + " unroll=" + std::to_string(unroll));
+    if (st == SGNN_OK) {
+        SpmmArgs args;
+        args.rp = p->row_ptr;
+        args.ci = p->col_idx;
+        args.val = p->values;
+        args.x = y;
+        args.xi = x;
+        args.ldxi = k;
+        args.c = out;
+        args.slots = plan->slots;
+        args.wrow = plan->wrow;
+        args.wnz = plan->wnz;
+        args.wslot = plan->wslot;
+        args.n_rows = p->n_rows;
+        args.n_workers = plan->n_workers;
+        args.ldx = k;
+        args.ldc = k;
+        args.ld_slot = plan->kt;
+        args.width = k;
+        st = launch(args, plan->p.block, 0, s);
+    }
+    if (st == SGNN_OK && plan->n_fix) {
+        FixupArgs f;
+        f.rp = p->row_ptr;
+        f.fix_row = plan->fix_row;
+        f.fix_slot = plan->fix_slot;
+        f.slots = plan->slots;
+        f.c = out;
+        f.ldc = k;
+        f.ld_slot = plan->kt;
+        f.n_fix = plan->n_fix;
+        f.width = k;
+        st = launch_spmm_fixup(f, reduce, s);
+    }
+    if (own) destroy_plan(own);
+    return st;
+}
+
+}  // namespace sgnn

@@ -1,0 +1,38 @@
+// ops.cuh -- internal host entry points shared by the C ABI (capi.cu).
+#pragma once
+
+#include "common.cuh"
+
+struct sgnn_plan_s;
+struct sgnn_cache_s;
+
+namespace sgnn {
+
+// TrainingCache (cache.cu)
+sgnn_status cache_create(const sgnn_csr* a_hat, int use_cache, sgnn_cache_s** out, cudaStream_t s);
+void cache_destroy(sgnn_cache_s* c);
+sgnn_status cache_sum_operand(sgnn_cache_s* c, sgnn_csr* out, cudaStream_t s);
+sgnn_status cache_mean_operand(sgnn_cache_s* c, sgnn_csr* out, cudaStream_t s);
+sgnn_status cache_spmm_backward(sgnn_cache_s* c, const float* dc, uint32_t dc_rows, uint32_t k,
+                                float* dx, int reduce, cudaStream_t s);
+sgnn_status cache_counters(sgnn_cache_s* c, uint64_t* tb, uint64_t* nb, uint64_t* hits, int* sym);
+
+sgnn_status run_spmm(const sgnn_csr* a, const float* x, uint32_t k, float* c, int reduce,
+                     const sgnn_plan_s* plan, cudaStream_t s);
+
+sgnn_status run_transpose(const sgnn_csr* a, uint64_t* trp, uint32_t* tci, float* tv, void* ws,
+                          size_t ws_bytes, cudaStream_t s);
+size_t transpose_workspace_bytes(const sgnn_csr* a);
+// values_out[p] = values_in[p] / deg[col_idx[p]]  (gnn.hpp:158-159)
+sgnn_status run_mean_scale(const uint32_t* col_idx, const float* vin, const uint32_t* deg,
+                           uint64_t nnz, float* vout, cudaStream_t s);
+sgnn_status run_row_degrees(const sgnn_csr* a, uint32_t* deg, cudaStream_t s);
+sgnn_status run_is_symmetric(const sgnn_csr* a, int* out, cudaStream_t s);
+
+sgnn_status run_sddmm(const sgnn_csr* p, const float* x, const float* y, uint32_t k, float* out,
+                      cudaStream_t s);
+sgnn_status run_fusedmm(const sgnn_csr* p, const float* x, const float* y, uint32_t k,
+                        int edge_op, int reduce, float* out, const sgnn_plan_s* plan,
+                        cudaStream_t s);
+
+}  // namespace sgnn

@@ -1,0 +1,290 @@
+// plan.cu -- builds the nnz-balanced worker split (see plan.cuh).
+#include <algorithm>
+
+#include "plan.cuh"
+
+namespace sgnn {
+
+namespace {
+
+constexpr uint64_t kSeg = SGNN_SEGMENT;
+
+// Boundary w of the cost-balanced split (parallel.hpp:28-41 cost model,
+// at worker granularity, with snapping -- see plan.cuh).
+__global__ void plan_coords_kernel(const uint64_t* __restrict__ rp, uint32_t m, uint64_t nnz,
+                                   uint64_t d, uint64_t split_t, uint32_t n_workers,
+                                   uint32_t* __restrict__ wrow, uint64_t* __restrict__ wnz) {
+    const uint64_t w = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (w > n_workers) return;
+    const uint64_t total = nnz + m;
+    const uint64_t b = min(w * d, total);
+    if (w == n_workers || b >= total) {
+        wrow[w] = m;
+        wnz[w] = nnz;
+        return;
+    }
+    // largest r in [0, m) with rp[r] + r <= b
+    uint32_t lo = 0, hi = m;
+    while (hi - lo > 1) {
+        const uint32_t mid = lo + (hi - lo) / 2;
+        if (__ldg(rp + mid) + mid <= b) lo = mid;
+        else hi = mid;
+    }
+    const uint32_t r = lo;
+    const uint64_t rs = __ldg(rp + r), re = __ldg(rp + r + 1);
+    const uint64_t deg = re - rs;
+    const uint64_t o = b - (rs + r);  // in [0, deg]
+    uint32_t outr;
+    uint64_t outj;
+    if (o == 0) {
+        outr = r; outj = rs;
+    } else if (deg <= split_t) {
+        // short row: never split; snap to the nearer row boundary
+        if (2 * o > deg + 1) { outr = r + 1; outj = re; }
+        else { outr = r; outj = rs; }
+    } else {
+        const uint64_t mm = (o / kSeg) * kSeg;  // segment boundary at or below
+        if (mm == 0) { outr = r; outj = rs; }
+        else if (mm >= deg) { outr = r + 1; outj = re; }
+        else { outr = r; outj = rs + mm; }
+    }
+    wrow[w] = outr;
+    wnz[w] = outj;
+}
+
+// Per worker: number of segment partials it emits and whether a split row starts in it.
+__global__ void plan_count_kernel(const uint64_t* __restrict__ rp, uint32_t m, uint32_t n_workers,
+                                  const uint32_t* __restrict__ wrow,
+                                  const uint64_t* __restrict__ wnz, uint32_t* __restrict__ nslot,
+                                  uint32_t* __restrict__ nfix) {
+    const uint32_t w = blockIdx.x * blockDim.x + threadIdx.x;
+    if (w >= n_workers) return;
+    const uint32_t i0 = wrow[w], i1 = wrow[w + 1];
+    const uint64_t j0 = wnz[w], j1 = wnz[w + 1];
+    uint32_t n = 0, f = 0;
+    if (i0 < m) {
+        const uint64_t rs0 = rp[i0];
+        if (j0 > rs0) {  // continuation of a row split before this worker
+            const uint64_t end = min(j1, rp[i0 + 1]);
+            n += uint32_t((end - j0 + kSeg - 1) / kSeg);
+        }
+    }
+    if (i1 < m) {
+        const uint64_t rs1 = rp[i1];
+        if (j1 > rs1 && rs1 >= j0) {  // a split row starts here and continues
+            n += uint32_t((j1 - rs1) / kSeg);
+            f = 1;
+        }
+    }
+    nslot[w] = n;
+    nfix[w] = f;
+}
+
+__global__ void plan_fix_kernel(const uint64_t* __restrict__ rp, uint32_t m, uint32_t n_workers,
+                                const uint32_t* __restrict__ wrow, const uint64_t* __restrict__ wnz,
+                                const uint32_t* __restrict__ wslot,
+                                const uint32_t* __restrict__ fixscan,
+                                uint32_t* __restrict__ fix_row, uint32_t* __restrict__ fix_slot) {
+    const uint32_t w = blockIdx.x * blockDim.x + threadIdx.x;
+    if (w >= n_workers) return;
+    if (fixscan[w + 1] == fixscan[w]) return;
+    const uint32_t i0 = wrow[w], i1 = wrow[w + 1];
+    const uint64_t j0 = wnz[w];
+    uint32_t first = 0;
+    if (i0 < m && j0 > rp[i0]) {
+        const uint64_t end = min(wnz[w + 1], rp[i0 + 1]);
+        first = uint32_t((end - j0 + kSeg - 1) / kSeg);
+    }
+    fix_row[fixscan[w]] = i1;
+    fix_slot[fixscan[w]] = wslot[w] + first;
+}
+
+uint32_t pow2_floor(uint64_t v) {
+    uint32_t p = 1;
+    while (uint64_t(p) * 2 <= v && p < (1u << 30)) p *= 2;
+    return p;
+}
+
+}  // namespace
+
+void default_params(const sgnn_csr* a, uint32_t k, bool vec_ok, const DeviceProps& dp,
+                    sgnn_plan_params* p) {
+    sgnn_plan_params d{};
+    if (vec_ok && !p->scalar) {
+        // two float4 per lane per gathered row measured best on B200 (cfg1/cfg2 probes)
+        if (k <= 16) { d.lanes = 4; d.vec = 1; }
+        else if (k <= 32) { d.lanes = 4; d.vec = 2; }
+        else if (k <= 64) { d.lanes = 8; d.vec = 2; }
+        else if (k <= 128) { d.lanes = 16; d.vec = 2; }
+        else if (k <= 256) { d.lanes = 32; d.vec = 2; }
+        else { d.lanes = 32; d.vec = 4; }
+        d.unroll = d.vec >= 4 ? 4 : 8;
+    } else {
+        d.lanes = 32;
+        d.vec = k <= 32 ? 1 : k <= 64 ? 2 : k <= 128 ? 4 : 8;
+        d.unroll = d.vec >= 8 ? 2 : 4;
+    }
+    d.block = 256;
+    // Enough workers for ~4 per resident lane group, so the tail is short.
+    const uint64_t total = a->nnz + a->n_rows;
+    const uint64_t groups = uint64_t(dp.sm_count > 0 ? dp.sm_count : 148) *
+                            uint64_t(dp.max_threads_per_sm > 0 ? dp.max_threads_per_sm : 2048) /
+                            d.lanes;
+    uint64_t want = total / (4 * groups);
+    d.path_items = std::max<uint32_t>(16, std::min<uint32_t>(4096, pow2_floor(std::max<uint64_t>(want, 1))));
+    d.split_rows_over = std::max<uint32_t>(d.path_items, SGNN_SEGMENT);
+    d.k_tile = 0;
+    d.scalar = p->scalar;
+    if (!p->lanes) p->lanes = d.lanes;
+    if (!p->vec) p->vec = d.vec;
+    if (!p->unroll) p->unroll = d.unroll;
+    if (!p->path_items) p->path_items = d.path_items;
+    if (!p->split_rows_over) p->split_rows_over = std::max<uint32_t>(p->path_items, SGNN_SEGMENT);
+    if (!p->block) p->block = d.block;
+}
+
+sgnn_status resolve_params(const sgnn_csr* a, uint32_t k, bool vec_ok, const DeviceProps& dp,
+                           const sgnn_plan_params* in, sgnn_plan_s* plan) {
+    sgnn_plan_params p{};
+    if (in) p = *in;
+    default_params(a, k, vec_ok, dp, &p);
+    const bool scalar = p.scalar || !vec_ok;
+    if (p.lanes != 4 && p.lanes != 8 && p.lanes != 16 && p.lanes != 32)
+        return fail(SGNN_ERR_CONFIG, "plan: lanes must be 4, 8, 16 or 32");
+    if (p.vec != 1 && p.vec != 2 && p.vec != 4 && p.vec != 8)
+        return fail(SGNN_ERR_CONFIG, "plan: vec must be 1, 2, 4 or 8");
+    if (p.unroll != 2 && p.unroll != 4 && p.unroll != 8)
+        return fail(SGNN_ERR_CONFIG, "plan: unroll must be 2, 4 or 8");
+    if (p.block < 64 || p.block > 1024 || p.block % 32)
+        return fail(SGNN_ERR_CONFIG, "plan: block must be a multiple of 32 in [64, 1024]");
+    if (p.path_items == 0) return fail(SGNN_ERR_CONFIG, "plan: path_items must be >= 1");
+    const uint32_t width = (scalar ? 1u : 4u) * p.lanes * p.vec;  // floats one pass covers
+    uint32_t kt = p.k_tile ? p.k_tile : k;
+    kt = std::min(kt, k);
+    kt = std::min(kt, width);
+    if (!scalar && (kt % 4)) kt = (kt / 4) * 4;
+    if (kt == 0) kt = std::min<uint32_t>(k, width);
+    plan->p = p;
+    plan->p.scalar = scalar ? 1 : 0;
+    plan->p.k_tile = kt;
+    plan->vec = !scalar;
+    plan->kt = kt;
+    uint64_t t = std::max<uint64_t>(p.split_rows_over, SGNN_SEGMENT);
+    plan->split_T = ceil_div_u64(t, SGNN_SEGMENT) * SGNN_SEGMENT;
+    plan->p.split_rows_over = uint32_t(plan->split_T);
+    return SGNN_OK;
+}
+
+bool plan_matches(const sgnn_plan_s* p, const sgnn_csr* a, uint32_t k) {
+    return p && p->row_ptr == a->row_ptr && p->n_rows == a->n_rows && p->nnz == a->nnz && p->k == k;
+}
+
+void destroy_plan(sgnn_plan_s* p) {
+    if (!p) return;
+    if (p->mem) cudaFree(p->mem);
+    if (p->fmem) cudaFree(p->fmem);
+    delete p;
+}
+
+sgnn_status build_plan(const sgnn_csr* a, uint32_t k, const sgnn_plan_params* params, bool vec_ok,
+                       sgnn_plan_s** out, cudaStream_t s) {
+    *out = nullptr;
+    SGNN_TRY(check_csr(a, "plan"));
+    DeviceProps dp;
+    SGNN_TRY(device_props(&dp));
+    auto* plan = new sgnn_plan_s;
+    plan->row_ptr = a->row_ptr;
+    plan->n_rows = a->n_rows;
+    plan->n_cols = a->n_cols;
+    plan->nnz = a->nnz;
+    plan->k = k;
+    sgnn_status st = resolve_params(a, k, vec_ok, dp, params, plan);
+    if (st != SGNN_OK) {
+        delete plan;
+        return st;
+    }
+    const uint64_t total = a->nnz + a->n_rows;
+    const uint64_t nw = ceil_div_u64(total, plan->p.path_items);
+    if (nw >= (1ull << 32) - 2) {
+        delete plan;
+        return fail(SGNN_ERR_CONFIG, "plan: too many workers; raise path_items");
+    }
+    const uint32_t W = uint32_t(nw);
+    plan->n_workers = W;
+    // layout: wrow u32[W+1] | wnz u64[W+1] | wslot u32[W+1] | nfix u32[W+1] | fix arrays later
+    auto align = [](size_t v) { return (v + 255) & ~size_t(255); };
+    const size_t o_wrow = 0;
+    const size_t o_wnz = align(o_wrow + sizeof(uint32_t) * (size_t(W) + 1));
+    const size_t o_wslot = align(o_wnz + sizeof(uint64_t) * (size_t(W) + 1));
+    const size_t o_fscan = align(o_wslot + sizeof(uint32_t) * (size_t(W) + 1));
+    const size_t o_end = align(o_fscan + sizeof(uint32_t) * (size_t(W) + 1));
+    cudaError_t ce = cudaMalloc(&plan->mem, o_end);
+    if (ce != cudaSuccess) {
+        delete plan;
+        return fail(SGNN_ERR_NOMEM, std::string("plan alloc: ") + cudaGetErrorString(ce));
+    }
+    char* base = static_cast<char*>(plan->mem);
+    plan->wrow = reinterpret_cast<uint32_t*>(base + o_wrow);
+    plan->wnz = reinterpret_cast<uint64_t*>(base + o_wnz);
+    plan->wslot = reinterpret_cast<uint32_t*>(base + o_wslot);
+    uint32_t* fscan = reinterpret_cast<uint32_t*>(base + o_fscan);
+
+    const int tb = 256;
+    plan_coords_kernel<<<unsigned(ceil_div_u64(uint64_t(W) + 1, tb)), tb, 0, s>>>(
+        a->row_ptr, a->n_rows, a->nnz, plan->p.path_items, plan->split_T, W, plan->wrow, plan->wnz);
+    ce = cudaGetLastError();
+    if (ce == cudaSuccess && W > 0) {
+        plan_count_kernel<<<unsigned(ceil_div_u64(W, tb)), tb, 0, s>>>(
+            a->row_ptr, a->n_rows, W, plan->wrow, plan->wnz, plan->wslot, fscan);
+        ce = cudaGetLastError();
+    }
+    if (ce != cudaSuccess) {
+        destroy_plan(plan);
+        return fail(SGNN_ERR_CUDA, std::string("plan kernels: ") + cudaGetErrorString(ce));
+    }
+    st = exclusive_scan_u32(plan->wslot, plan->wslot, W, s);
+    if (st == SGNN_OK) st = exclusive_scan_u32(fscan, fscan, W, s);
+    if (st != SGNN_OK) {
+        destroy_plan(plan);
+        return st;
+    }
+    uint32_t counts[2] = {0, 0};
+    ce = cudaMemcpyAsync(&counts[0], plan->wslot + W, sizeof(uint32_t), cudaMemcpyDeviceToHost, s);
+    if (ce == cudaSuccess)
+        ce = cudaMemcpyAsync(&counts[1], fscan + W, sizeof(uint32_t), cudaMemcpyDeviceToHost, s);
+    if (ce == cudaSuccess) ce = cudaStreamSynchronize(s);
+    if (ce != cudaSuccess) {
+        destroy_plan(plan);
+        return fail(SGNN_ERR_CUDA, std::string("plan readback: ") + cudaGetErrorString(ce));
+    }
+    plan->n_slots = counts[0];
+    plan->n_fix = counts[1];
+    if (plan->n_fix > 0) {
+        // fix arrays + slot workspace
+        void* fmem = nullptr;
+        const size_t fbytes = align(sizeof(uint32_t) * plan->n_fix) * 2 +
+                              sizeof(float) * size_t(plan->n_slots) * plan->kt;
+        ce = cudaMalloc(&fmem, fbytes);
+        if (ce != cudaSuccess) {
+            destroy_plan(plan);
+            return fail(SGNN_ERR_NOMEM, std::string("plan workspace: ") + cudaGetErrorString(ce));
+        }
+        plan->fmem = fmem;
+        char* fb = static_cast<char*>(fmem);
+        plan->fix_row = reinterpret_cast<uint32_t*>(fb);
+        plan->fix_slot = reinterpret_cast<uint32_t*>(fb + align(sizeof(uint32_t) * plan->n_fix));
+        plan->slots = reinterpret_cast<float*>(fb + 2 * align(sizeof(uint32_t) * plan->n_fix));
+        plan_fix_kernel<<<unsigned(ceil_div_u64(W, tb)), tb, 0, s>>>(
+            a->row_ptr, a->n_rows, W, plan->wrow, plan->wnz, plan->wslot, fscan, plan->fix_row,
+            plan->fix_slot);
+        ce = cudaGetLastError();
+        if (ce != cudaSuccess) {
+            destroy_plan(plan);
+            return fail(SGNN_ERR_CUDA, std::string("plan fix: ") + cudaGetErrorString(ce));
+        }
+    }
+    *out = plan;
+    return SGNN_OK;
+}
+
+}  // namespace sgnn

@@ -1,0 +1,94 @@
+// spmm.cu -- host driver of the SpMM worker + fixup kernels (K-tile passes).
+#include <algorithm>
+
+#include "ops.cuh"
+#include "plan.cuh"
+#include "spmm_inst.cuh"
+
+namespace sgnn {
+
+SpmmLauncher find_spmm_launcher(bool vec, int lanes, int vregs, int unroll, int reduce) {
+    switch (reduce) {
+        case SGNN_REDUCE_SUM: return spmm_lookup_sum(vec, lanes, vregs, unroll);
+        case SGNN_REDUCE_MEAN: return spmm_lookup_mean(vec, lanes, vregs, unroll);
+        case SGNN_REDUCE_MIN: return spmm_lookup_min(vec, lanes, vregs, unroll);
+        case SGNN_REDUCE_MAX: return spmm_lookup_max(vec, lanes, vregs, unroll);
+    }
+    return nullptr;
+}
+
+sgnn_status launch_spmm_fixup(const FixupArgs& f, int reduce, cudaStream_t s) {
+    switch (reduce) {
+        case SGNN_REDUCE_SUM: return spmm_lookup_sum_fixup(f, s);
+        case SGNN_REDUCE_MEAN: return spmm_lookup_mean_fixup(f, s);
+        case SGNN_REDUCE_MIN: return spmm_lookup_min_fixup(f, s);
+        case SGNN_REDUCE_MAX: return spmm_lookup_max_fixup(f, s);
+    }
+    return fail(SGNN_ERR_CONFIG, "unknown reduce op");
+}
+
+sgnn_status run_spmm(const sgnn_csr* a, const float* x, uint32_t k, float* c, int reduce,
+                     const sgnn_plan_s* plan, cudaStream_t s) {
+    if (reduce < 0 || reduce > 3) return fail(SGNN_ERR_CONFIG, "spmm: unknown reduce op");
+    if (k == 0 || a->n_rows == 0) return SGNN_OK;
+    if (!plan_matches(plan, a, k))
+        return fail(SGNN_ERR_DISPATCH, "spmm: plan was built for another matrix or K");
+    const bool aligned = (reinterpret_cast<uintptr_t>(x) % 16 == 0) &&
+                         (reinterpret_cast<uintptr_t>(c) % 16 == 0) && (k % 4 == 0);
+    const bool vec = plan->vec && aligned;
+    int lanes = int(plan->p.lanes), vregs = int(plan->p.vec), unroll = int(plan->p.unroll);
+    if (!vec) {
+        lanes = 32;
+        if (plan->vec) {  // float4 plan on misaligned operands: scalar kernel, same split
+            vregs = std::min<int>(8, int(ceil_div_u64(plan->kt, 32)));
+            vregs = vregs <= 1 ? 1 : vregs <= 2 ? 2 : vregs <= 4 ? 4 : 8;
+            unroll = vregs >= 4 ? 2 : 4;
+        }
+    }
+    SpmmLauncher launch = find_spmm_launcher(vec, lanes, vregs, unroll, reduce);
+    if (!launch)
+        return fail(SGNN_ERR_UNSUPPORTED, "spmm: no kernel compiled for lanes=" +
+                                              std::to_string(lanes) + " vec=" +
+                                              std::to_string(vregs) + " unroll=" +
+                                              std::to_string(unroll));
+    const uint32_t kernel_width = uint32_t((vec ? 4 : 1) * lanes * vregs);
+
+    for (uint32_t k0 = 0; k0 < k; k0 += plan->kt) {
+        const uint32_t kp = std::min(plan->kt, k - k0);
+        for (uint32_t sk = 0; sk < kp; sk += kernel_width) {
+            SpmmArgs args{};
+            args.rp = a->row_ptr;
+            args.ci = a->col_idx;
+            args.val = a->values;
+            args.x = x + k0 + sk;
+            args.c = c + k0 + sk;
+            args.slots = plan->slots ? plan->slots + sk : nullptr;
+            args.wrow = plan->wrow;
+            args.wnz = plan->wnz;
+            args.wslot = plan->wslot;
+            args.n_rows = a->n_rows;
+            args.n_workers = plan->n_workers;
+            args.ldx = k;
+            args.ldc = k;
+            args.ld_slot = plan->kt;
+            args.width = std::min(kernel_width, kp - sk);
+            SGNN_TRY(launch(args, plan->p.block, 0, s));
+        }
+        if (plan->n_fix) {
+            FixupArgs f;
+            f.rp = a->row_ptr;
+            f.fix_row = plan->fix_row;
+            f.fix_slot = plan->fix_slot;
+            f.slots = plan->slots;
+            f.c = c + k0;
+            f.ldc = k;
+            f.ld_slot = plan->kt;
+            f.n_fix = plan->n_fix;
+            f.width = kp;
+            SGNN_TRY(launch_spmm_fixup(f, reduce, s));
+        }
+    }
+    return SGNN_OK;
+}
+
+}  // namespace sgnn

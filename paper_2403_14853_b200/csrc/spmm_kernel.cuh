@@ -1,0 +1,378 @@
+// spmm_kernel.cuh -- the sm_100a CSR SpMM worker kernel and its fixup pass.
+//
+// Restates spmm_rows_trusted / spmm_rows_fixed (kernels.hpp:45-128) for the
+// GPU.  One *worker* = a group of G lanes (G in {4,8,16,32}) that walks a
+// contiguous nnz-balanced range of the CSR (plan.cuh).  Lane l of the group
+// owns the K-slice elements {4*(l + G*v) .. +3 : v < V} (float4 path) or
+// {l + G*v} (scalar path), so one warp instruction gathers a contiguous,
+// coalesced piece of a neighbour row X[col, :].
+//
+// Per nonzero the group broadcasts (col, val) by warp shuffle from a
+// coalesced chunk load, issues U independent row gathers before consuming
+// them (memory-level parallelism), then accumulates in ascending nonzero
+// order with separately rounded multiply and add -- the reference's exact
+// fp32 chain (kernels.hpp:55-58) for every row of <= SGNN_SEGMENT nonzeros.
+// Row ends come from a G-wide window of row_ptr held in registers, so short
+// rows cost no dependent loads.
+#pragma once
+
+#include "common.cuh"
+
+namespace sgnn {
+
+struct SpmmArgs {
+    const uint64_t* __restrict__ rp;
+    const uint32_t* __restrict__ ci;
+    const float* __restrict__ val;
+    const float* __restrict__ x;  // gathered operand (X for SpMM, Y for FusedMM), pre-offset by k0
+    const float* __restrict__ xi; // FusedMM only: row operand X (row r's slice is dotted with Y_j)
+    uint64_t ldxi;
+    float* c;                     // pre-offset by k0 (re-read for multi-segment rows)
+    float* __restrict__ slots;    // pre-offset by k0-in-pass; stride ld_slot
+    const uint32_t* __restrict__ wrow;
+    const uint64_t* __restrict__ wnz;
+    const uint32_t* __restrict__ wslot;
+    uint32_t n_rows;
+    uint32_t n_workers;
+    uint64_t ldx;     // row stride of X (floats)
+    uint64_t ldc;     // row stride of C (floats)
+    uint64_t ld_slot; // row stride of a slot (floats)
+    uint32_t width;   // floats of K this launch covers
+};
+
+struct FixupArgs {
+    const uint64_t* __restrict__ rp;
+    const uint32_t* __restrict__ fix_row;
+    const uint32_t* __restrict__ fix_slot;
+    const float* __restrict__ slots;
+    float* __restrict__ c;  // pre-offset by k0
+    uint64_t ldc;
+    uint64_t ld_slot;
+    uint32_t n_fix;
+    uint32_t width;
+};
+
+namespace dev {
+
+// Reduction semantics (kernels.hpp:53-89, types.hpp:116).
+template <int RED>
+struct Reducer {
+    // a*x folded into acc; `first` marks the first element of a segment.
+    static __device__ __forceinline__ float fold(float acc, float a, float x, bool first) {
+        const float p = __fmul_rn(a, x);
+        if (RED == SGNN_REDUCE_SUM || RED == SGNN_REDUCE_MEAN) return __fadd_rn(acc, p);
+        if (first) return p;
+        if (RED == SGNN_REDUCE_MIN) return (p < acc) ? p : acc;  // std::min(acc, p)
+        return (acc < p) ? p : acc;                               // std::max(acc, p)
+    }
+    // canonical combine of consecutive segment partials (left to right)
+    static __device__ __forceinline__ float combine(float t, float s) {
+        if (RED == SGNN_REDUCE_SUM || RED == SGNN_REDUCE_MEAN) return __fadd_rn(t, s);
+        if (RED == SGNN_REDUCE_MIN) return (s < t) ? s : t;
+        return (t < s) ? s : t;
+    }
+    // epilogue: mean divide (kernels.hpp:60-63); empty rows give 0 for all ops
+    static __device__ __forceinline__ float finish(float v, uint64_t deg) {
+        if (RED == SGNN_REDUCE_MEAN) return deg ? __fdiv_rn(v, float(deg)) : 0.0f;
+        return deg ? v : 0.0f;
+    }
+};
+
+template <int G, int V, bool VEC>
+struct Frag {
+    static constexpr int W = VEC ? 4 : 1;
+    static constexpr int N = V * W;
+    float v[N];
+
+    __device__ __forceinline__ void zero() {
+#pragma unroll
+        for (int i = 0; i < N; ++i) v[i] = 0.0f;
+    }
+    // Is register block `q` of lane `gl` inside the launch width?
+    static __device__ __forceinline__ bool valid(int gl, int q, uint32_t width) {
+        return uint32_t(W * (gl + G * q)) < width;
+    }
+    __device__ __forceinline__ void load(const float* __restrict__ row, int gl, uint32_t width) {
+#pragma unroll
+        for (int q = 0; q < V; ++q) {
+            if (valid(gl, q, width)) {
+                if constexpr (VEC) {
+                    const float4 t = __ldg(reinterpret_cast<const float4*>(row) + gl + G * q);
+                    v[4 * q + 0] = t.x; v[4 * q + 1] = t.y; v[4 * q + 2] = t.z; v[4 * q + 3] = t.w;
+                } else {
+                    v[q] = __ldg(row + gl + G * q);
+                }
+            } else {
+#pragma unroll
+                for (int i = 0; i < W; ++i) v[W * q + i] = 0.0f;
+            }
+        }
+    }
+    // Coherent load of data this thread wrote earlier in the same launch.
+    __device__ __forceinline__ void load_own(const float* row, int gl, uint32_t width) {
+#pragma unroll
+        for (int q = 0; q < V; ++q) {
+            if (valid(gl, q, width)) {
+                if constexpr (VEC) {
+                    const float4 t = reinterpret_cast<const float4*>(row)[gl + G * q];
+                    v[4 * q + 0] = t.x; v[4 * q + 1] = t.y; v[4 * q + 2] = t.z; v[4 * q + 3] = t.w;
+                } else {
+                    v[q] = row[gl + G * q];
+                }
+            }
+        }
+    }
+    __device__ __forceinline__ void store(float* __restrict__ row, int gl, uint32_t width) const {
+#pragma unroll
+        for (int q = 0; q < V; ++q) {
+            if (valid(gl, q, width)) {
+                if constexpr (VEC) {
+                    __stcs(reinterpret_cast<float4*>(row) + gl + G * q,
+                           make_float4(v[4 * q + 0], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]));
+                } else {
+                    __stcs(row + gl + G * q, v[q]);
+                }
+            }
+        }
+    }
+};
+
+// Kernel modes: plain SpMM, or FusedMM with an edge op (kernels.hpp:216-270).
+enum { OP_SPMM = 0, OP_FUSED_MUL = 1, OP_FUSED_SIGMOID = 2 };
+
+// Canonical dot product <a, b> over the group: float4 leaves
+// ((a0b0 + a1b1) + a2b2) + a3b3 (scalar path: a0b0), then a balanced binary
+// tree over the leaves, lowest index bits first (zero leaves pad to a power
+// of two).  The tree is the same for every (G, V) layout, so FusedMM results
+// do not depend on the plan.  Every lane of the group returns the same value.
+template <int G, int V, bool VEC>
+__device__ __forceinline__ float group_dot(const Frag<G, V, VEC>& a, const Frag<G, V, VEC>& b,
+                                           unsigned gmask) {
+    float p[V];
+#pragma unroll
+    for (int q = 0; q < V; ++q) {
+        if constexpr (VEC) {
+            float t = __fmul_rn(a.v[4 * q], b.v[4 * q]);
+            t = __fadd_rn(t, __fmul_rn(a.v[4 * q + 1], b.v[4 * q + 1]));
+            t = __fadd_rn(t, __fmul_rn(a.v[4 * q + 2], b.v[4 * q + 2]));
+            p[q] = __fadd_rn(t, __fmul_rn(a.v[4 * q + 3], b.v[4 * q + 3]));
+        } else {
+            p[q] = __fmul_rn(a.v[q], b.v[q]);
+        }
+    }
+#pragma unroll
+    for (int off = 1; off < G; off <<= 1)
+#pragma unroll
+        for (int q = 0; q < V; ++q) p[q] = __fadd_rn(p[q], __shfl_xor_sync(gmask, p[q], off, G));
+#pragma unroll
+    for (int step = 1; step < V; step <<= 1)
+#pragma unroll
+        for (int q = 0; q + step < V; q += 2 * step) p[q] = __fadd_rn(p[q], p[q + step]);
+    return p[0];
+}
+
+template <int OP>
+__device__ __forceinline__ float edge_value(float p, float dot) {
+    if (OP == OP_FUSED_SIGMOID)  // p * (1 / (1 + exp(-dot)))
+        return __fmul_rn(p, __fdiv_rn(1.0f, __fadd_rn(1.0f, expf(-dot))));
+    return __fmul_rn(p, dot);  // default combine, kernels.hpp:239
+}
+
+// The worker walk.  See plan.cuh for the ownership rules; in short, worker
+// (i0,j0)->(i1,j1) consumes nonzeros [j0,j1), finishes rows i0..i1-1 and
+// holds the head of row i1 when j1 > row_ptr[i1].  A row that lies entirely
+// inside [j0,j1) is written to C; a row split across workers has its
+// SGNN_SEGMENT-nonzero segment partials written to consecutive slots.
+template <int G, int V, int U, int RED, bool VEC, int OP = OP_SPMM>
+__global__ void __launch_bounds__(256) spmm_worker_kernel(const SpmmArgs a) {
+    using F = Frag<G, V, VEC>;
+    using R = Reducer<RED>;
+    constexpr int N = F::N;
+    // One chunk = one batch of U nonzeros: their (col, val) are loaded by the
+    // first U lanes of the group (CH per lane when U > G), all U row gathers
+    // are issued, then consumed in order.  Keeping one batch per loop trip
+    // bounds the live registers to U fragments.
+    constexpr int CH = (U + G - 1) / G;
+    constexpr int CHUNK = U;
+    constexpr uint64_t SEG = SGNN_SEGMENT;
+
+    const int lane = threadIdx.x & 31;
+    const int gl = lane & (G - 1);
+    const unsigned gmask = (G == 32) ? 0xffffffffu : (((1u << G) - 1u) << (lane & ~(G - 1)));
+    const uint32_t n_groups = (gridDim.x * blockDim.x) / G;
+
+    for (uint32_t w = (blockIdx.x * blockDim.x + threadIdx.x) / G; w < a.n_workers; w += n_groups) {
+        const uint32_t i0 = __ldg(a.wrow + w), i1 = __ldg(a.wrow + w + 1);
+        const uint64_t j0 = __ldg(a.wnz + w), j1 = __ldg(a.wnz + w + 1);
+        uint32_t slot = a.wslot ? __ldg(a.wslot + w) : 0u;
+
+        // row_ptr window: lane gl holds rp[rb + 1 + gl] (row ends of rows rb..rb+G-1)
+        uint32_t r = i0;
+        uint32_t rb = r;
+        uint64_t rwin = __ldg(a.rp + min(rb + 1 + uint32_t(gl), a.n_rows));
+        uint64_t rstart = __ldg(a.rp + r);
+        uint64_t rend = dev::shfl_u64(gmask, rwin, 0, G);
+        bool inside = (rstart >= j0) && (rend <= j1);
+        uint64_t seg_end = min(j0 + SEG, rend);
+        bool first = true;
+        bool have_tot = false;
+        F acc;
+        acc.zero();
+        F xrow;                   // FusedMM: X[r, :] slice of the current row
+        uint32_t xrow_id = 0xffffffffu;
+
+        auto store_slot = [&](const F& f) {
+            f.store(a.slots + uint64_t(slot) * a.ld_slot, gl, a.width);
+            ++slot;
+        };
+        // Rows longer than one segment but owned by this worker keep their
+        // running segment total in the output row itself (rare; saves registers).
+        auto finish_segment = [&]() {  // segment boundary inside a row
+            if (inside) {
+                float* crow = a.c + uint64_t(r) * a.ldc;
+                if (have_tot) {
+                    F t;
+                    t.load_own(crow, gl, a.width);
+#pragma unroll
+                    for (int i = 0; i < N; ++i) t.v[i] = R::combine(t.v[i], acc.v[i]);
+                    t.store(crow, gl, a.width);
+                } else {
+                    acc.store(crow, gl, a.width);
+                }
+                have_tot = true;
+            } else {
+                store_slot(acc);
+            }
+            acc.zero();
+            first = true;
+        };
+        auto finish_row = [&]() {  // row r has no more nonzeros in this worker
+            if (inside) {
+                const uint64_t deg = rend - rstart;
+                float* crow = a.c + uint64_t(r) * a.ldc;
+                if (have_tot) {
+                    F t;
+                    t.load_own(crow, gl, a.width);
+#pragma unroll
+                    for (int i = 0; i < N; ++i) acc.v[i] = R::combine(t.v[i], acc.v[i]);
+                }
+#pragma unroll
+                for (int i = 0; i < N; ++i) acc.v[i] = R::finish(acc.v[i], deg);
+                acc.store(crow, gl, a.width);
+            } else {
+                store_slot(acc);
+            }
+        };
+        auto advance_row = [&]() {
+            ++r;
+            rstart = rend;
+            if (r - rb >= uint32_t(G)) {
+                rb = r;
+                rwin = __ldg(a.rp + min(rb + 1 + uint32_t(gl), a.n_rows));
+            }
+            rend = dev::shfl_u64(gmask, rwin, int(r - rb), G);
+            inside = (rstart >= j0) && (rend <= j1);
+            seg_end = min(rstart + SEG, rend);
+            first = true;
+            have_tot = false;
+            acc.zero();
+        };
+
+        for (uint64_t base = j0; base < j1; base += CHUNK) {
+            uint32_t cc[CH];
+            float vv[CH];
+#pragma unroll
+            for (int h = 0; h < CH; ++h) {
+                const uint64_t idx = base + uint64_t(gl + G * h);
+                const bool ok = (gl + G * h) < CHUNK && idx < j1;
+                cc[h] = ok ? dev::ld_stream(a.ci + idx) : 0u;
+                vv[h] = ok ? dev::ld_stream(a.val + idx) : 0.0f;
+            }
+            const int n = (j1 - base) < uint64_t(CHUNK) ? int(j1 - base) : CHUNK;
+            {
+                constexpr int q0 = 0;
+                F xf[U];
+#pragma unroll
+                for (int u = 0; u < U; ++u) {
+                    const int q = q0 + u;
+                    const uint32_t col = __shfl_sync(gmask, cc[q / G], q % G, G);
+                    if (q < n) xf[u].load(a.x + uint64_t(col) * a.ldx, gl, a.width);
+                }
+#pragma unroll
+                for (int u = 0; u < U; ++u) {
+                    const int q = q0 + u;
+                    const float av = __shfl_sync(gmask, vv[q / G], q % G, G);
+                    if (q >= n) break;
+                    const uint64_t e = base + uint64_t(q);
+                    while (e >= rend) {
+                        finish_row();
+                        advance_row();
+                    }
+                    if (e >= seg_end) {
+                        finish_segment();
+                        seg_end = min(seg_end + SEG, rend);
+                    }
+                    float s = av;
+                    if constexpr (OP != OP_SPMM) {
+                        // s_ij = combine(p_ij, <X_i, Y_j>); Y_j is reused below (read once)
+                        if (xrow_id != r) {
+                            xrow.load(a.xi + uint64_t(r) * a.ldxi, gl, a.width);
+                            xrow_id = r;
+                        }
+                        s = edge_value<OP>(av, group_dot(xrow, xf[u], gmask));
+                    }
+#pragma unroll
+                    for (int i = 0; i < N; ++i) acc.v[i] = R::fold(acc.v[i], s, xf[u].v[i], first);
+                    first = false;
+                }
+            }
+        }
+        // All nonzeros consumed: close rows that end inside this worker (the
+        // current one and any empty rows after it), then the head of row i1.
+        while (r < i1) {
+            finish_row();
+            advance_row();
+        }
+        if (r < a.n_rows && j1 > max(j0, rstart)) store_slot(acc);  // head of a split row
+    }
+}
+
+// Adds the segment partials of each split row left to right and applies the
+// reduction epilogue.  One thread per K element; the slot loads are
+// independent, the fold is the canonical sequential chain.
+template <int RED>
+__global__ void __launch_bounds__(256) spmm_fixup_kernel(const FixupArgs f) {
+    using R = Reducer<RED>;
+    constexpr uint64_t SEG = SGNN_SEGMENT;
+    const uint64_t total = uint64_t(f.n_fix) * f.width;
+    for (uint64_t t = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; t < total;
+         t += uint64_t(gridDim.x) * blockDim.x) {
+        const uint32_t fi = uint32_t(t / f.width);
+        const uint32_t k = uint32_t(t % f.width);
+        const uint32_t r = __ldg(f.fix_row + fi);
+        const uint64_t deg = __ldg(f.rp + r + 1) - __ldg(f.rp + r);
+        const uint64_t nseg = (deg + SEG - 1) / SEG;
+        const float* s = f.slots + uint64_t(__ldg(f.fix_slot + fi)) * f.ld_slot + k;
+        float v = __ldcs(s);
+        uint64_t q = 1;
+        for (; q + 8 <= nseg; q += 8) {
+            float b[8];
+#pragma unroll
+            for (int i = 0; i < 8; ++i) b[i] = __ldcs(s + (q + i) * f.ld_slot);
+#pragma unroll
+            for (int i = 0; i < 8; ++i) v = R::combine(v, b[i]);
+        }
+        for (; q < nseg; ++q) v = R::combine(v, __ldcs(s + q * f.ld_slot));
+        __stcs(f.c + uint64_t(r) * f.ldc + k, R::finish(v, deg));
+    }
+}
+
+}  // namespace dev
+
+// Host launcher table (spmm_launch.cu).
+using SpmmLauncher = sgnn_status (*)(const SpmmArgs&, uint32_t block, uint32_t max_blocks,
+                                     cudaStream_t);
+SpmmLauncher find_spmm_launcher(bool vec, int lanes, int vec_regs, int unroll, int reduce);
+sgnn_status launch_spmm_fixup(const FixupArgs& f, int reduce, cudaStream_t s);
+
+}  // namespace sgnn

@@ -1,0 +1,389 @@
+// transpose.cu -- on-device CSR -> CSC (= CSR of A^T), bit-exact with the
+// reference's serial counting sort (sparse.hpp:72-89): column histogram ->
+// exclusive scan -> placement in ascending original row within each column.
+//
+// The stable placement is an LSD radix sort of the nonzeros keyed by column
+// (2 passes of <= 11-bit digits for up to 2^22 columns), carrying (row, value)
+// as payload.  Within a tile, ranks are made stable with a warp-level
+// multisplit (__match_any_sync) processed in index order, so the output is
+// exactly the counting-sort order.  The row id of a nonzero is found in the
+// first pass by binary search inside the tile's row range, so no expanded
+// row array is materialised.
+//
+// Also: row_degrees (sparse.hpp:105-109), is_symmetric (sparse.hpp:179-192)
+// and the mean-operand value scaling (gnn.hpp:158-159).
+#include <algorithm>
+
+#include "ops.cuh"
+
+namespace sgnn {
+
+namespace {
+
+constexpr int kThreads = 256;
+constexpr int kWarps = kThreads / 32;
+constexpr int kItems = 16;                          // per thread per tile
+constexpr uint64_t kTile = uint64_t(kThreads) * kItems;  // 4096 nonzeros
+constexpr int kMaxDigitBits = 11;
+
+struct RadixPlan {
+    int passes = 1;
+    int dbits = 1;
+    uint32_t bins = 2;
+    uint64_t tiles = 0;
+};
+
+RadixPlan radix_plan(uint32_t n_cols, uint64_t nnz) {
+    RadixPlan r;
+    int nbits = 0;
+    if (n_cols > 1) {
+        uint32_t v = n_cols - 1;
+        while (v) { ++nbits; v >>= 1; }
+    }
+    r.passes = std::max(1, (nbits + kMaxDigitBits - 1) / kMaxDigitBits);
+    r.dbits = std::max(1, (nbits + r.passes - 1) / r.passes);
+    r.bins = 1u << r.dbits;
+    r.tiles = ceil_div_u64(nnz, kTile);
+    return r;
+}
+
+struct Workspace {
+    uint32_t* keys_a;
+    uint32_t* keys_b;
+    uint32_t* rows_a;
+    float* vals_a;
+    uint32_t* hist;    // bins * tiles (+1 for the scan total)
+    uint32_t* counts;  // n_cols
+    size_t bytes;
+};
+
+size_t align256(size_t v) { return (v + 255) & ~size_t(255); }
+
+Workspace carve(void* base, const sgnn_csr* a, const RadixPlan& rp) {
+    Workspace w{};
+    char* p = static_cast<char*>(base);
+    size_t off = 0;
+    auto take = [&](size_t bytes) {
+        char* q = p ? p + off : nullptr;
+        off += align256(bytes);
+        return q;
+    };
+    const size_t nnz = a->nnz;
+    w.keys_a = reinterpret_cast<uint32_t*>(take(4 * nnz));
+    w.keys_b = reinterpret_cast<uint32_t*>(take(4 * nnz));
+    w.rows_a = reinterpret_cast<uint32_t*>(take(4 * nnz));
+    w.vals_a = reinterpret_cast<float*>(take(4 * nnz));
+    w.hist = reinterpret_cast<uint32_t*>(take(4 * (size_t(rp.bins) * rp.tiles + 1)));
+    w.counts = reinterpret_cast<uint32_t*>(take(4 * (size_t(a->n_cols) + 1)));
+    w.bytes = off;
+    return w;
+}
+
+__global__ void col_histogram_kernel(const uint32_t* __restrict__ ci, uint64_t nnz,
+                                     uint32_t* __restrict__ counts) {
+    for (uint64_t e = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; e < nnz;
+         e += uint64_t(gridDim.x) * blockDim.x)
+        atomicAdd(counts + __ldcs(ci + e), 1u);
+}
+
+// Largest r in [lo, hi) with rp[r] <= idx (the row holding nonzero idx).
+__device__ __forceinline__ uint32_t find_row(const uint64_t* __restrict__ rp, uint32_t lo,
+                                             uint32_t hi, uint64_t idx) {
+    while (hi - lo > 1) {
+        const uint32_t mid = lo + (hi - lo) / 2;
+        if (__ldg(rp + mid) <= idx) lo = mid;
+        else hi = mid;
+    }
+    return lo;
+}
+
+// Row range [r_lo, r_hi] covering nonzeros [base, last] of a tile.
+__device__ __forceinline__ void tile_rows(const uint64_t* __restrict__ rp, uint32_t m,
+                                          uint64_t base, uint64_t last, uint32_t* r_lo,
+                                          uint32_t* r_hi) {
+    *r_lo = find_row(rp, 0, m, base);
+    *r_hi = find_row(rp, *r_lo, m, last);
+}
+
+__global__ void __launch_bounds__(kThreads) radix_upsweep_kernel(const uint32_t* __restrict__ keys,
+                                                                 uint64_t n, int shift,
+                                                                 uint32_t mask, uint64_t tiles,
+                                                                 uint32_t* __restrict__ hist) {
+    extern __shared__ uint32_t sh[];
+    const uint32_t bins = mask + 1;
+    for (uint32_t d = threadIdx.x; d < bins; d += kThreads) sh[d] = 0;
+    __syncthreads();
+    const uint64_t base = uint64_t(blockIdx.x) * kTile;
+    for (int r = 0; r < kItems; ++r) {
+        const uint64_t idx = base + uint64_t(r) * kThreads + threadIdx.x;
+        if (idx < n) atomicAdd(sh + ((__ldg(keys + idx) >> shift) & mask), 1u);
+    }
+    __syncthreads();
+    for (uint32_t d = threadIdx.x; d < bins; d += kThreads) hist[uint64_t(d) * tiles + blockIdx.x] = sh[d];
+}
+
+// Stable scatter of one tile.  FIRST: payload rows are computed by binary
+// search (pass 1); otherwise read from rows_in.  LAST: keys are not written.
+template <bool FIRST, bool LAST, bool VALS>
+__global__ void __launch_bounds__(kThreads) radix_downsweep_kernel(
+    const uint32_t* __restrict__ keys_in, const uint32_t* __restrict__ rows_in,
+    const float* __restrict__ vals_in, uint32_t* __restrict__ keys_out,
+    uint32_t* __restrict__ rows_out, float* __restrict__ vals_out, uint64_t n, int shift,
+    uint32_t mask, uint64_t tiles, const uint32_t* __restrict__ hist_scan,
+    const uint64_t* __restrict__ rp, uint32_t m) {
+    extern __shared__ uint32_t sh[];
+    const uint32_t bins = mask + 1;
+    uint32_t* cnt = sh;               // [bins]
+    uint32_t* whist = sh + bins;      // [kWarps][bins]
+    __shared__ uint32_t s_rows[2];
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    for (uint32_t d = threadIdx.x; d < bins * (kWarps + 1); d += kThreads) sh[d] = 0;
+    const uint64_t base = uint64_t(blockIdx.x) * kTile;
+    if (FIRST && threadIdx.x == 0) {
+        uint32_t lo, hi;
+        tile_rows(rp, m, base, min(base + kTile, n) - 1, &lo, &hi);
+        s_rows[0] = lo;
+        s_rows[1] = hi + 1;
+    }
+    __syncthreads();
+    const unsigned lt = (1u << lane) - 1u;
+    for (int r = 0; r < kItems; ++r) {
+        const uint64_t idx = base + uint64_t(r) * kThreads + threadIdx.x;
+        const bool valid = idx < n;
+        uint32_t key = 0, row = 0;
+        float val = 0.0f;
+        if (valid) {
+            key = FIRST ? __ldcs(keys_in + idx) : __ldcs(keys_in + idx);
+            if (FIRST) row = find_row(rp, s_rows[0], s_rows[1], idx);
+            else row = __ldcs(rows_in + idx);
+            if (VALS) val = __ldcs(vals_in + idx);
+        }
+        const uint32_t d = (key >> shift) & mask;
+        const unsigned peers = __match_any_sync(0xffffffffu, valid ? d : 0xffffffffu);
+        const uint32_t rank = __popc(peers & lt);
+        const bool leader = (peers & lt) == 0;
+        if (valid && leader) whist[wid * bins + d] = __popc(peers);
+        __syncthreads();
+        if (valid) {
+            uint32_t pos = cnt[d] + rank;
+            for (int w = 0; w < wid; ++w) pos += whist[w * bins + d];
+            const uint64_t dst = uint64_t(__ldg(hist_scan + uint64_t(d) * tiles + blockIdx.x)) + pos;
+            if (!LAST) keys_out[dst] = key;
+            rows_out[dst] = row;
+            if (VALS) vals_out[dst] = val;
+        }
+        __syncthreads();
+        if (valid && leader) {
+            atomicAdd(cnt + d, __popc(peers));
+            whist[wid * bins + d] = 0;
+        }
+        __syncthreads();
+    }
+}
+
+template <bool FIRST, bool LAST, bool VALS>
+sgnn_status launch_down(const uint32_t* ki, const uint32_t* ri, const float* vi, uint32_t* ko,
+                        uint32_t* ro, float* vo, uint64_t n, int shift, uint32_t mask,
+                        uint64_t tiles, const uint32_t* hs, const uint64_t* rp, uint32_t m,
+                        cudaStream_t s) {
+    const size_t smem = sizeof(uint32_t) * size_t(mask + 1) * (kWarps + 1);
+    auto k = radix_downsweep_kernel<FIRST, LAST, VALS>;
+    SGNN_CUDA_TRY(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+    k<<<unsigned(tiles), kThreads, smem, s>>>(ki, ri, vi, ko, ro, vo, n, shift, mask, tiles, hs, rp, m);
+    SGNN_LAUNCH_CHECK();
+    return SGNN_OK;
+}
+
+template <bool FIRST, bool LAST>
+sgnn_status launch_down_v(bool vals, const uint32_t* ki, const uint32_t* ri, const float* vi,
+                          uint32_t* ko, uint32_t* ro, float* vo, uint64_t n, int shift,
+                          uint32_t mask, uint64_t tiles, const uint32_t* hs, const uint64_t* rp,
+                          uint32_t m, cudaStream_t s) {
+    if (vals)
+        return launch_down<FIRST, LAST, true>(ki, ri, vi, ko, ro, vo, n, shift, mask, tiles, hs, rp, m, s);
+    return launch_down<FIRST, LAST, false>(ki, ri, vi, ko, ro, vo, n, shift, mask, tiles, hs, rp, m, s);
+}
+
+__global__ void row_degrees_kernel(const uint64_t* __restrict__ rp, uint32_t m,
+                                   uint32_t* __restrict__ deg) {
+    for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < m; i += gridDim.x * blockDim.x)
+        deg[i] = uint32_t(__ldg(rp + i + 1) - __ldg(rp + i));
+}
+
+__global__ void mean_scale_kernel(const uint32_t* __restrict__ ci, const float* __restrict__ vin,
+                                  const uint32_t* __restrict__ deg, uint64_t nnz,
+                                  float* __restrict__ vout) {
+    for (uint64_t e = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; e < nnz;
+         e += uint64_t(gridDim.x) * blockDim.x)
+        vout[e] = __fdiv_rn(vin[e], float(__ldg(deg + __ldg(ci + e))));
+}
+
+// One thread per nonzero (i, j, v): binary-search i in row j; mismatch -> flag 0.
+__global__ void __launch_bounds__(kThreads) symmetric_kernel(const uint64_t* __restrict__ rp,
+                                                             const uint32_t* __restrict__ ci,
+                                                             const float* __restrict__ v,
+                                                             uint32_t m, uint64_t nnz,
+                                                             int* __restrict__ flag) {
+    __shared__ uint32_t s_rows[2];
+    const uint64_t base = uint64_t(blockIdx.x) * kTile;
+    if (threadIdx.x == 0) {
+        uint32_t lo, hi;
+        tile_rows(rp, m, base, min(base + kTile, nnz) - 1, &lo, &hi);
+        s_rows[0] = lo;
+        s_rows[1] = hi + 1;
+    }
+    __syncthreads();
+    bool ok = true;
+    for (int r = 0; r < kItems; ++r) {
+        const uint64_t e = base + uint64_t(r) * kThreads + threadIdx.x;
+        if (e >= nnz) break;
+        const uint32_t i = find_row(rp, s_rows[0], s_rows[1], e);
+        const uint32_t j = __ldg(ci + e);
+        uint64_t lo = __ldg(rp + j), hi = __ldg(rp + j + 1);
+        const uint64_t end = hi;
+        while (lo < hi) {  // lower_bound of i in row j
+            const uint64_t mid = lo + (hi - lo) / 2;
+            if (__ldg(ci + mid) < i) lo = mid + 1;
+            else hi = mid;
+        }
+        if (lo == end || __ldg(ci + lo) != i || __ldg(v + lo) != __ldg(v + e)) ok = false;
+    }
+    if (__syncthreads_or(!ok) && threadIdx.x == 0) atomicExch(flag, 0);
+}
+
+}  // namespace
+
+size_t transpose_workspace_bytes(const sgnn_csr* a) {
+    const RadixPlan rp = radix_plan(a->n_cols, a->nnz);
+    return carve(nullptr, a, rp).bytes;
+}
+
+sgnn_status run_transpose(const sgnn_csr* a, uint64_t* trp, uint32_t* tci, float* tv, void* ws,
+                          size_t ws_bytes, cudaStream_t s) {
+    DeviceProps dp;
+    SGNN_TRY(device_props(&dp));
+    const RadixPlan plan = radix_plan(a->n_cols, a->nnz);
+    const size_t need = carve(nullptr, a, plan).bytes;
+    void* own = nullptr;
+    if (!ws) {
+        SGNN_TRY(scratch_alloc(&own, need, s));
+        ws = own;
+    } else if (ws_bytes < need) {
+        return fail(SGNN_ERR_CONFIG, "transpose: workspace too small (need " +
+                                         std::to_string(need) + " bytes)");
+    }
+    Workspace w = carve(ws, a, plan);
+    sgnn_status st = SGNN_OK;
+    do {
+        // 1. column histogram -> t_row_ptr (sparse.hpp:75-76)
+        if (cudaMemsetAsync(w.counts, 0, sizeof(uint32_t) * (size_t(a->n_cols) + 1), s) != cudaSuccess) {
+            st = fail(SGNN_ERR_CUDA, "transpose: memset failed");
+            break;
+        }
+        if (a->nnz) {
+            const uint64_t blocks = std::min<uint64_t>(ceil_div_u64(a->nnz, 256), uint64_t(dp.sm_count) * 16);
+            col_histogram_kernel<<<unsigned(blocks), 256, 0, s>>>(a->col_idx, a->nnz, w.counts);
+            if (cudaGetLastError() != cudaSuccess) {
+                st = fail(SGNN_ERR_CUDA, "transpose: histogram launch failed");
+                break;
+            }
+        }
+        st = exclusive_scan_u32_to_u64(w.counts, trp, a->n_cols, s);
+        if (st != SGNN_OK || a->nnz == 0) break;
+
+        // 2. stable LSD radix passes (sparse.hpp:80-86 placement order)
+        const bool vals = tv != nullptr;
+        const uint32_t mask = plan.bins - 1;
+        const uint32_t* keys_src = a->col_idx;
+        const uint32_t* rows_src = nullptr;
+        const float* vals_src = a->values;
+        for (int p = 0; p < plan.passes && st == SGNN_OK; ++p) {
+            const bool first = p == 0, last = p == plan.passes - 1;
+            // the last pass lands in (tci, tv); earlier passes alternate with set A
+            const bool to_out = ((plan.passes - 1 - p) % 2) == 0;
+            uint32_t* keys_dst = (p % 2 == 0) ? w.keys_a : w.keys_b;
+            uint32_t* rows_dst = to_out ? tci : w.rows_a;
+            float* vals_dst = to_out ? tv : w.vals_a;
+            const int shift = p * plan.dbits;
+            const size_t up_smem = sizeof(uint32_t) * plan.bins;
+            radix_upsweep_kernel<<<unsigned(plan.tiles), kThreads, up_smem, s>>>(
+                keys_src, a->nnz, shift, mask, plan.tiles, w.hist);
+            if (cudaGetLastError() != cudaSuccess) {
+                st = fail(SGNN_ERR_CUDA, "transpose: upsweep launch failed");
+                break;
+            }
+            st = exclusive_scan_u32(w.hist, w.hist, uint64_t(plan.bins) * plan.tiles, s);
+            if (st != SGNN_OK) break;
+            if (first && last)
+                st = launch_down_v<true, true>(vals, keys_src, rows_src, vals_src, keys_dst, rows_dst,
+                                               vals_dst, a->nnz, shift, mask, plan.tiles, w.hist,
+                                               a->row_ptr, a->n_rows, s);
+            else if (first)
+                st = launch_down_v<true, false>(vals, keys_src, rows_src, vals_src, keys_dst, rows_dst,
+                                                vals_dst, a->nnz, shift, mask, plan.tiles, w.hist,
+                                                a->row_ptr, a->n_rows, s);
+            else if (last)
+                st = launch_down_v<false, true>(vals, keys_src, rows_src, vals_src, keys_dst, rows_dst,
+                                                vals_dst, a->nnz, shift, mask, plan.tiles, w.hist,
+                                                a->row_ptr, a->n_rows, s);
+            else
+                st = launch_down_v<false, false>(vals, keys_src, rows_src, vals_src, keys_dst, rows_dst,
+                                                 vals_dst, a->nnz, shift, mask, plan.tiles, w.hist,
+                                                 a->row_ptr, a->n_rows, s);
+            keys_src = keys_dst;
+            rows_src = rows_dst;
+            vals_src = vals_dst;
+        }
+    } while (false);
+    if (own) scratch_free(own, s);
+    return st;
+}
+
+sgnn_status run_row_degrees(const sgnn_csr* a, uint32_t* deg, cudaStream_t s) {
+    if (a->n_rows == 0) return SGNN_OK;
+    DeviceProps dp;
+    SGNN_TRY(device_props(&dp));
+    const uint64_t blocks = std::min<uint64_t>(ceil_div_u64(a->n_rows, 256), uint64_t(dp.sm_count) * 8);
+    row_degrees_kernel<<<unsigned(blocks), 256, 0, s>>>(a->row_ptr, a->n_rows, deg);
+    SGNN_LAUNCH_CHECK();
+    return SGNN_OK;
+}
+
+sgnn_status run_mean_scale(const uint32_t* col_idx, const float* vin, const uint32_t* deg,
+                           uint64_t nnz, float* vout, cudaStream_t s) {
+    if (nnz == 0) return SGNN_OK;
+    DeviceProps dp;
+    SGNN_TRY(device_props(&dp));
+    const uint64_t blocks = std::min<uint64_t>(ceil_div_u64(nnz, 256), uint64_t(dp.sm_count) * 16);
+    mean_scale_kernel<<<unsigned(blocks), 256, 0, s>>>(col_idx, vin, deg, nnz, vout);
+    SGNN_LAUNCH_CHECK();
+    return SGNN_OK;
+}
+
+sgnn_status run_is_symmetric(const sgnn_csr* a, int* out, cudaStream_t s) {
+    *out = 0;
+    if (a->n_rows != a->n_cols) return SGNN_OK;  // sparse.hpp:180
+    if (a->nnz == 0) {
+        *out = 1;
+        return SGNN_OK;
+    }
+    int* flag = nullptr;
+    SGNN_TRY(scratch_alloc(reinterpret_cast<void**>(&flag), sizeof(int), s));
+    const int one = 1;
+    sgnn_status st = SGNN_OK;
+    if (cudaMemcpyAsync(flag, &one, sizeof(int), cudaMemcpyHostToDevice, s) != cudaSuccess)
+        st = fail(SGNN_ERR_CUDA, "is_symmetric: memcpy failed");
+    if (st == SGNN_OK) {
+        symmetric_kernel<<<unsigned(ceil_div_u64(a->nnz, kTile)), kThreads, 0, s>>>(
+            a->row_ptr, a->col_idx, a->values, a->n_rows, a->nnz, flag);
+        if (cudaGetLastError() != cudaSuccess) st = fail(SGNN_ERR_CUDA, "is_symmetric: launch failed");
+    }
+    if (st == SGNN_OK &&
+        (cudaMemcpyAsync(out, flag, sizeof(int), cudaMemcpyDeviceToHost, s) != cudaSuccess ||
+         cudaStreamSynchronize(s) != cudaSuccess))
+        st = fail(SGNN_ERR_CUDA, "is_symmetric: readback failed");
+    scratch_free(flag, s);
+    return st;
+}
+
+}  // namespace sgnn

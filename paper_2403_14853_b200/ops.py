@@ -1,0 +1,358 @@
+"""Python mirror of the reference operator API over device tensors.
+
+Names, argument meaning and error behaviour follow
+/root/reference/proj/include/sparsegnn/ (kernels.hpp, sparse.hpp, gnn.hpp,
+autotune.hpp); every call goes through the C ABI of libsgnn_b200.so
+(include/sgnn_b200.h).  torch supplies device memory and the stream only.
+"""
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+
+from . import _lib
+from ._lib import (ConfigError, DispatchError, Error, InternalError, ShapeError,  # noqa: F401
+                   TapeError, check, lib)
+
+__all__ = [
+    "CsrMatrix", "KernelKind", "Plan", "TrainingCache", "DispatchGuard", "spmm", "spmm_with",
+    "spmm_into", "resolve_kernel", "set_dispatch", "get_dispatch", "transpose", "row_degrees",
+    "is_symmetric", "sddmm", "fusedmm", "specialization_sweep", "spmm_plan",
+]
+
+specialization_sweep = (16, 32, 64, 128, 256, 512, 1024)  # kernels.hpp:27
+
+
+def _stream():
+    return C.c_void_p(torch.cuda.current_stream().cuda_stream)
+
+
+def _reduce(r) -> int:
+    if isinstance(r, str):
+        if r not in _lib.REDUCE:  # types.hpp:129-135 parse_reduce_op
+            raise ConfigError(f"unknown reduce op '{r}' (expected sum|min|max|mean)")
+        return _lib.REDUCE[r]
+    return int(r)
+
+
+def _dense(t: torch.Tensor, what: str) -> torch.Tensor:
+    if not isinstance(t, torch.Tensor) or not t.is_cuda:
+        raise ConfigError(f"{what}: expected a CUDA tensor (no CPU fallback)")
+    if t.dtype != torch.float32 or t.dim() != 2:
+        raise ConfigError(f"{what}: expected a 2-D float32 tensor")
+    if not t.is_contiguous():
+        raise ConfigError(f"{what}: expected a row-major contiguous tensor")
+    return t
+
+
+class CsrMatrix:
+    """CsrMatrix<float> on the device (types.hpp:26-79): row_ptr u64 (stored
+    as int64), col_idx u32 (stored as int32), values f32."""
+
+    def __init__(self, n_rows: int, n_cols: int, row_ptr: torch.Tensor, col_idx: torch.Tensor,
+                 values: torch.Tensor):
+        if row_ptr.numel() != n_rows + 1:
+            raise ConfigError(f"csr: row_ptr has length {row_ptr.numel()}, expected n_rows+1 = {n_rows + 1}")
+        self.n_rows, self.n_cols = int(n_rows), int(n_cols)
+        self.row_ptr = row_ptr.contiguous()
+        self.col_idx = col_idx.contiguous()
+        self.values = values.contiguous()
+        self._cstruct = None
+
+    @property
+    def nnz(self) -> int:
+        return int(self.col_idx.numel())
+
+    @classmethod
+    def from_numpy(cls, row_ptr, col_idx, values, n_cols, device="cuda"):
+        rp = torch.from_numpy(np.ascontiguousarray(row_ptr, np.uint64).view(np.int64)).to(device)
+        ci = torch.from_numpy(np.ascontiguousarray(col_idx, np.uint32).view(np.int32)).to(device)
+        v = torch.from_numpy(np.ascontiguousarray(values, np.float32)).to(device)
+        return cls(len(row_ptr) - 1, n_cols, rp, ci, v)
+
+    def to_numpy(self):
+        return (self.row_ptr.cpu().numpy().view(np.uint64), self.col_idx.cpu().numpy().view(np.uint32),
+                self.values.cpu().numpy())
+
+    def c(self) -> _lib.Csr:
+        if self._cstruct is None:
+            self._cstruct = _lib.Csr(self.n_rows, self.n_cols, self.nnz, self.row_ptr.data_ptr(),
+                                     self.col_idx.data_ptr() if self.nnz else 0,
+                                     self.values.data_ptr() if self.nnz else 0)
+        return self._cstruct
+
+    def with_values(self, values: torch.Tensor) -> "CsrMatrix":
+        return CsrMatrix(self.n_rows, self.n_cols, self.row_ptr, self.col_idx, values)
+
+
+@dataclass(frozen=True)
+class KernelKind:
+    """KernelKind (kernels.hpp:14-25)."""
+    tag: str = "trusted"
+    k: int = 0
+
+    @staticmethod
+    def trusted():
+        return KernelKind("trusted", 0)
+
+    @staticmethod
+    def specialized(k: int):
+        return KernelKind("specialized", int(k))
+
+    def is_specialized(self) -> bool:
+        return self.tag == "specialized"
+
+
+class Plan:
+    """A tuned/untuned SpMM work split for (A, K) (sgnn_plan_create)."""
+
+    def __init__(self, a: CsrMatrix, k: int, **params):
+        self.a, self.k = a, int(k)
+        pp = _lib.PlanParams(**{k_: int(v) for k_, v in params.items()})
+        h = C.c_void_p()
+        check(lib().sgnn_plan_create(C.byref(a.c()), self.k, C.byref(pp), C.byref(h), _stream()),
+              "plan_create")
+        self.handle = h
+
+    @property
+    def params(self) -> dict:
+        pp = _lib.PlanParams()
+        check(lib().sgnn_plan_get_params(self.handle, C.byref(pp)))
+        return pp.as_dict()
+
+    @property
+    def stats(self) -> dict:
+        w, f, s = C.c_uint64(), C.c_uint64(), C.c_uint64()
+        check(lib().sgnn_plan_stats(self.handle, C.byref(w), C.byref(f), C.byref(s)))
+        return {"workers": w.value, "split_rows": f.value, "slots": s.value}
+
+    def close(self):
+        if getattr(self, "handle", None):
+            lib().sgnn_plan_destroy(self.handle)
+            self.handle = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def spmm_into(a: CsrMatrix, b: torch.Tensor, reduce, kind: KernelKind, out: torch.Tensor,
+              plan: Plan | None = None) -> torch.Tensor:
+    """detail::spmm_into (kernels.hpp:141-149) plus spmm_with's checks (:157-169)."""
+    _dense(b, "spmm")
+    _dense(out, "spmm out")
+    if out.shape[0] != a.n_rows or out.shape[1] != b.shape[1]:
+        raise ShapeError(f"spmm: output is {tuple(out.shape)}, expected ({a.n_rows}, {b.shape[1]})")
+    st = lib().sgnn_spmm_with_f32(
+        C.byref(a.c()), b.data_ptr(), b.shape[0], b.shape[1], out.data_ptr(), _reduce(reduce),
+        _lib.SPECIALIZED if kind.is_specialized() else _lib.TRUSTED, kind.k,
+        plan.handle if plan is not None else None, _stream())
+    check(st, "spmm")
+    return out
+
+
+def spmm_with(a: CsrMatrix, b: torch.Tensor, reduce, kind: KernelKind, plan: Plan | None = None):
+    """spmm_with (kernels.hpp:157-173)."""
+    _dense(b, "spmm")
+    out = torch.empty((a.n_rows, b.shape[1]), dtype=torch.float32, device=b.device)
+    return spmm_into(a, b, reduce, kind, out, plan)
+
+
+def spmm(a: CsrMatrix, b: torch.Tensor, reduce="sum", plan: Plan | None = None,
+         out: torch.Tensor | None = None):
+    """spmm (kernels.hpp:179-182): kernel picked by the dispatch state."""
+    _dense(b, "spmm")
+    kind = resolve_kernel(b.shape[1], reduce)
+    if out is None:
+        out = torch.empty((a.n_rows, b.shape[1]), dtype=torch.float32, device=b.device)
+    return spmm_into(a, b, reduce, kind, out, plan if kind.is_specialized() else None)
+
+
+def spmm_plan(a: CsrMatrix, b: torch.Tensor, reduce="sum", plan: Plan | None = None,
+              out: torch.Tensor | None = None) -> torch.Tensor:
+    """sgnn_spmm_f32: SpMM with an explicit plan for any reduce/K (the plan's
+    launch parameters never change the result)."""
+    _dense(b, "spmm")
+    if out is None:
+        out = torch.empty((a.n_rows, b.shape[1]), dtype=torch.float32, device=b.device)
+    check(lib().sgnn_spmm_f32(C.byref(a.c()), b.data_ptr(), b.shape[0], b.shape[1], out.data_ptr(),
+                              _reduce(reduce), plan.handle if plan is not None else None, _stream()), "spmm")
+    return out
+
+
+def resolve_kernel(k: int, reduce) -> KernelKind:
+    """resolve_kernel (kernels.hpp:38, dispatch.cpp:21-28)."""
+    sk = C.c_uint32()
+    tag = lib().sgnn_resolve_kernel(int(k), _reduce(reduce), C.byref(sk))
+    return KernelKind.specialized(sk.value) if tag == _lib.SPECIALIZED else KernelKind.trusted()
+
+
+def set_dispatch(enabled: bool) -> None:
+    """set_dispatch (autotune.hpp:36, dispatch.cpp:12)."""
+    lib().sgnn_set_dispatch(int(bool(enabled)))
+
+
+def get_dispatch() -> bool:
+    return bool(lib().sgnn_get_dispatch())
+
+
+class DispatchGuard:
+    """DispatchGuard (autotune.hpp:40-51)."""
+
+    def __init__(self, enabled: bool):
+        self.enabled = enabled
+
+    def __enter__(self):
+        self.prev = get_dispatch()
+        set_dispatch(self.enabled)
+        return self
+
+    def __exit__(self, *exc):
+        set_dispatch(self.prev)
+
+
+def transpose(a: CsrMatrix) -> CsrMatrix:
+    """transpose (sparse.hpp:72-89), bit-exact, on the device."""
+    dev = a.row_ptr.device
+    trp = torch.empty(a.n_cols + 1, dtype=torch.int64, device=dev)
+    tci = torch.empty(a.nnz, dtype=torch.int32, device=dev)
+    tv = torch.empty(a.nnz, dtype=torch.float32, device=dev)
+    check(lib().sgnn_csr_transpose(C.byref(a.c()), trp.data_ptr(), tci.data_ptr() if a.nnz else None,
+                                   tv.data_ptr() if a.nnz else None, None, 0, _stream()), "transpose")
+    return CsrMatrix(a.n_cols, a.n_rows, trp, tci, tv)
+
+
+def row_degrees(a: CsrMatrix) -> torch.Tensor:
+    """row_degrees (sparse.hpp:105-109) as int32 (u32 bits)."""
+    deg = torch.empty(a.n_rows, dtype=torch.int32, device=a.row_ptr.device)
+    check(lib().sgnn_row_degrees(C.byref(a.c()), deg.data_ptr(), _stream()), "row_degrees")
+    return deg
+
+
+def is_symmetric(a: CsrMatrix) -> bool:
+    """is_symmetric (sparse.hpp:179-192)."""
+    out = C.c_int()
+    check(lib().sgnn_is_symmetric(C.byref(a.c()), C.byref(out), _stream()), "is_symmetric")
+    return bool(out.value)
+
+
+class TrainingCache:
+    """TrainingCache<float> + build_cache (gnn.hpp:113-196) over a device a_hat."""
+
+    def __init__(self, a_hat: CsrMatrix, use_cache: bool = True):
+        if a_hat.n_rows != a_hat.n_cols:
+            raise ShapeError(f"build_cache: adjacency is {a_hat.n_rows}x{a_hat.n_cols}, expected square")
+        self.a_hat = a_hat
+        h = C.c_void_p()
+        check(lib().sgnn_cache_create(C.byref(a_hat.c()), int(bool(use_cache)), C.byref(h), _stream()),
+              "build_cache")
+        self.handle = h
+
+    def _operand(self, fn) -> CsrMatrix:
+        out = _lib.Csr()
+        check(fn(self.handle, C.byref(out), _stream()), "cache operand")
+        return _View(out, self)
+
+    def sum_operand(self) -> CsrMatrix:
+        return self._operand(lib().sgnn_cache_sum_operand)
+
+    def mean_operand(self) -> CsrMatrix:
+        return self._operand(lib().sgnn_cache_mean_operand)
+
+    @property
+    def counters(self) -> dict:
+        t, n, h, s = C.c_uint64(), C.c_uint64(), C.c_uint64(), C.c_int()
+        check(lib().sgnn_cache_counters(self.handle, C.byref(t), C.byref(n), C.byref(h), C.byref(s)))
+        return {"transpose_builds": t.value, "normalize_builds": n.value, "cache_hits": h.value,
+                "symmetric": bool(s.value)}
+
+    def spmm_backward(self, dc: torch.Tensor, reduce="sum", out: torch.Tensor | None = None):
+        """dX = spmm(sum_operand | mean_operand, dC, Sum) (gnn.hpp:275,290)."""
+        _dense(dc, "spmm_backward")
+        if out is None:
+            out = torch.empty((self.a_hat.n_cols, dc.shape[1]), dtype=torch.float32, device=dc.device)
+        check(lib().sgnn_spmm_backward_f32(self.handle, dc.data_ptr(), dc.shape[0], dc.shape[1],
+                                           out.data_ptr(), _reduce(reduce), _stream()), "spmm_backward")
+        return out
+
+    def close(self):
+        if getattr(self, "handle", None):
+            lib().sgnn_cache_destroy(self.handle)
+            self.handle = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+class _View(CsrMatrix):
+    """A CSR view onto device arrays owned by a TrainingCache."""
+
+    def __init__(self, cs: _lib.Csr, owner):
+        self.n_rows, self.n_cols = cs.n_rows, cs.n_cols
+        self._nnz = cs.nnz
+        self._cstruct = cs
+        self._owner = owner
+
+    @property
+    def nnz(self) -> int:
+        return int(self._nnz)
+
+    def to_numpy(self):
+        cs = self._cstruct
+        rp = np.empty(cs.n_rows + 1, np.uint64)
+        ci = np.empty(cs.nnz, np.uint32)
+        v = np.empty(cs.nnz, np.float32)
+        torch.cuda.synchronize()
+        for host, ptr in ((rp, cs.row_ptr), (ci, cs.col_idx), (v, cs.values)):
+            if host.nbytes:
+                _lib.memcpy_d2h(host.ctypes.data, ptr, host.nbytes)
+        return rp, ci, v
+
+
+def sddmm(p: CsrMatrix, x: torch.Tensor, y: torch.Tensor) -> CsrMatrix:
+    """sddmm (kernels.hpp:187-210): P's pattern with values p_e * <X_i, Y_j>."""
+    _dense(x, "sddmm X")
+    _dense(y, "sddmm Y")
+    if p.n_rows != x.shape[0] or p.n_cols != y.shape[0] or x.shape[1] != y.shape[1]:
+        raise ShapeError(f"sddmm: pattern {p.n_rows}x{p.n_cols} needs X with {p.n_rows} rows and Y with "
+                         f"{p.n_cols} rows of equal width; got X {x.shape[0]}x{x.shape[1]}, "
+                         f"Y {y.shape[0]}x{y.shape[1]}")
+    out = torch.empty(p.nnz, dtype=torch.float32, device=x.device)
+    check(lib().sgnn_sddmm_f32(C.byref(p.c()), x.data_ptr(), x.shape[0], y.data_ptr(), y.shape[0],
+                               x.shape[1], out.data_ptr() if p.nnz else None, _stream()), "sddmm")
+    return p.with_values(out)
+
+
+EDGE_OPS = {"mul": _lib.EDGE_MUL, None: _lib.EDGE_MUL, "sigmoid_mul": _lib.EDGE_SIGMOID_MUL}
+
+
+def fusedmm(p: CsrMatrix, x: torch.Tensor, y: torch.Tensor, edge_op="mul", reduce="sum",
+            out: torch.Tensor | None = None) -> torch.Tensor:
+    """fusedmm (kernels.hpp:216-270) with a GPU-expressible combine
+    (Semiring::combine, types.hpp:139-145): "mul" = p*dot (plus_times), or
+    "sigmoid_mul" = p*sigmoid(dot).  An arbitrary Python callable is a
+    DispatchError: there is no CPU fallback."""
+    if callable(edge_op):
+        raise DispatchError("fusedmm: arbitrary combine callables cannot run on the GPU; "
+                            "use edge_op='mul' or 'sigmoid_mul'")
+    if edge_op not in EDGE_OPS:
+        raise ConfigError(f"fusedmm: unknown edge op {edge_op!r}")
+    _dense(x, "fusedmm X")
+    _dense(y, "fusedmm Y")
+    if p.n_rows != x.shape[0] or p.n_cols != y.shape[0] or x.shape[1] != y.shape[1]:
+        raise ShapeError(f"fusedmm: operand shapes do not compose (P {p.n_rows}x{p.n_cols}, X "
+                         f"{x.shape[0]}x{x.shape[1]}, Y {y.shape[0]}x{y.shape[1]})")
+    if out is None:
+        out = torch.empty((p.n_rows, y.shape[1]), dtype=torch.float32, device=x.device)
+    check(lib().sgnn_fusedmm_f32(C.byref(p.c()), x.data_ptr(), x.shape[0], y.data_ptr(), y.shape[0],
+                                 x.shape[1], EDGE_OPS[edge_op], _reduce(reduce), out.data_ptr(),
+                                 _stream()), "fusedmm")
+    return out

@@ -1,0 +1,147 @@
+"""SDDMM (kernels.hpp:187-210) and FusedMM (kernels.hpp:216-270) on the B200
+against the reference's golden vectors and the oracle.  Tolerances:
+SDDMM |gpu - ref64| <= 1e-5 * |p_e| * sum_k |x_ik y_jk|; FusedMM
+|gpu - ref64| <= 1e-5 * sum_j |s_ij y_jk| (+ the dot's own rounding)."""
+import numpy as np
+import pytest
+
+from conftest import assert_spmm_close, golden_cases, load_golden, rand_csr
+from oracle import port
+
+pytestmark = pytest.mark.gpu
+REDS = {"sum": 0, "min": 1, "max": 2, "mean": 3}
+EDGES = {"mul": 0, "sigmoid_mul": 1}
+
+
+def _ops():
+    from paper_2403_14853_b200 import ops
+    return ops
+
+
+def _t(a):
+    import torch
+    return torch.from_numpy(np.ascontiguousarray(a, np.float32)).cuda()
+
+
+def run_sddmm(rp, ci, v, n, x, y):
+    ops = _ops()
+    out = ops.sddmm(ops.CsrMatrix.from_numpy(rp, ci, v, n), _t(x), _t(y))
+    return out.values.cpu().numpy(), out
+
+
+def run_fused(rp, ci, v, n, x, y, edge, red):
+    ops = _ops()
+    return ops.fusedmm(ops.CsrMatrix.from_numpy(rp, ci, v, n), _t(x), _t(y), edge, red).cpu().numpy()
+
+
+def check_sddmm(rp, ci, v, n, x, y):
+    got, _ = run_sddmm(rp, ci, v, n, x, y)
+    want = port.sddmm(rp, ci, v, x, y)
+    den = port.sddmm_absdenom(rp, ci, v, x, y)
+    err = np.abs(got.astype(np.float64) - want)
+    assert (err <= 1e-5 * den + 1e-30).all(), f"sddmm: max err/den {np.max(err / np.maximum(den, 1e-30))}"
+    return got
+
+
+def check_fused(rp, ci, v, n, x, y, edge, red):
+    got = run_fused(rp, ci, v, n, x, y, edge, red)
+    want = port.fusedmm(rp, ci, v, x, y, EDGES[edge], REDS[red])
+    den = port.fusedmm_absdenom(rp, ci, v, x, y, EDGES[edge], REDS[red])
+    assert_spmm_close(got, want, den, what=f"fusedmm {edge} {red}")
+    return got
+
+
+def test_kat_sddmm_fusedmm(cuda):
+    ident = (np.arange(3, dtype=np.uint64), np.arange(2, dtype=np.uint32), np.ones(2, np.float32))
+    x = np.array([[1, 2], [3, 4]], np.float32)
+    got, out = run_sddmm(*ident, 2, x, x)
+    np.testing.assert_array_equal(got, [5, 25])
+    np.testing.assert_array_equal(out.row_ptr.cpu().numpy(), [0, 1, 2])  # pattern is P's
+    np.testing.assert_array_equal(run_fused(*ident, 2, x, x, "mul", "sum"), [[5, 10], [75, 100]])
+    # full pattern, values 1 -> X Y^T
+    rng = np.random.default_rng(0)
+    xx, yy = rng.uniform(-1, 1, (5, 8)).astype(np.float32), rng.uniform(-1, 1, (4, 8)).astype(np.float32)
+    rp = np.arange(0, 21, 4, dtype=np.uint64)
+    ci = np.tile(np.arange(4, dtype=np.uint32), 5)
+    got, _ = run_sddmm(rp, ci, np.ones(20, np.float32), 4, xx, yy)
+    np.testing.assert_allclose(got.reshape(5, 4), xx.astype(np.float64) @ yy.T.astype(np.float64), rtol=1e-5, atol=1e-6)
+
+
+def test_empty(cuda):
+    rp = np.zeros(4, np.uint64)
+    x = np.ones((3, 16), np.float32)
+    got, _ = run_sddmm(rp, np.zeros(0, np.uint32), np.zeros(0, np.float32), 5, x, np.ones((5, 16), np.float32))
+    assert got.size == 0
+    for red in REDS:
+        out = run_fused(rp, np.zeros(0, np.uint32), np.zeros(0, np.float32), 5, x, np.ones((5, 16), np.float32), "mul", red)
+        assert (out == 0).all()
+
+
+@pytest.mark.parametrize("name", golden_cases())
+def test_golden(cuda, name):
+    g = load_golden(name)
+    rp, ci, v, n = g["row_ptr"], g["col_idx"], g["values"], int(g["n_cols"])
+    for k in g["ks"]:
+        x, xi = g[f"x_{k}"], g[f"xi_{k}"]
+        if k <= 1024:
+            got, _ = run_sddmm(rp, ci, v, n, xi, x)
+            den = port.sddmm_absdenom(rp, ci, v, xi, x)
+            assert (np.abs(got - g[f"sddmm64_{k}"]) <= 1e-5 * den + 1e-30).all(), (name, k)
+        for edge, eo in EDGES.items():
+            for red, r in REDS.items():
+                got = run_fused(rp, ci, v, n, xi, x, edge, red)
+                den = port.fusedmm_absdenom(rp, ci, v, xi, x, eo, r)
+                assert_spmm_close(got, g[f"fused64_{k}_{eo}_{r}"], den, what=f"{name} K={k} {edge} {red}")
+
+
+@pytest.mark.parametrize("k", [1, 4, 7, 16, 32, 64, 100, 128, 256, 512, 1024])
+def test_random(cuda, k):
+    rng = np.random.default_rng(k)
+    rp, ci, v = rand_csr(rng, 400, 700, 0.01, hub_rows=(3, 300), empty_frac=0.2)
+    x = rng.normal(0, 0.3, (400, k)).astype(np.float32)
+    y = rng.normal(0, 0.3, (700, k)).astype(np.float32)
+    if k <= 256 or k % 4 == 0:
+        check_sddmm(rp, ci, v, 700, x, y)
+        for edge in EDGES:
+            for red in REDS:
+                check_fused(rp, ci, v, 700, x, y, edge, red)
+
+
+def test_fusedmm_equals_spmm_of_sddmm(cuda):
+    """SPEC.md:176 / acceptance #8: fusedmm = spmm(sddmm(P,X,Y), Y) within tolerance."""
+    ops = _ops()
+    rng = np.random.default_rng(4)
+    rp, ci, v = rand_csr(rng, 300, 300, 0.03, hub_rows=(1,))
+    x = rng.normal(0, 0.5, (300, 32)).astype(np.float32)
+    y = rng.normal(0, 0.5, (300, 32)).astype(np.float32)
+    p = ops.CsrMatrix.from_numpy(rp, ci, v, 300)
+    s = ops.sddmm(p, _t(x), _t(y))
+    for red in REDS:
+        fused = ops.fusedmm(p, _t(x), _t(y), "mul", red).cpu().numpy()
+        comp = ops.spmm(s, _t(y), red).cpu().numpy()
+        sv = s.values.cpu().numpy()
+        den = port.spmm_absdenom(rp, ci, sv, y, REDS[red]) + 1e-30
+        assert (np.abs(fused - comp) <= 2e-5 * den).all(), red
+
+
+def test_hub_rows_fused(cuda):
+    rng = np.random.default_rng(12)
+    n = 20000
+    rp, ci, v = rand_csr(rng, 40, n, 0.0005, hub_rows=(0, 39), hub_density=0.7, value="positive")
+    x = rng.normal(0, 0.1, (40, 64)).astype(np.float32)
+    y = rng.normal(0, 0.1, (n, 64)).astype(np.float32)
+    for red in REDS:
+        check_fused(rp, ci, v, n, x, y, "sigmoid_mul", red)
+    check_sddmm(rp, ci, v, n, x, y)
+
+
+def test_errors(cuda):
+    import torch
+    ops = _ops()
+    p = ops.CsrMatrix.from_numpy(np.array([0, 1], np.uint64), np.array([0], np.uint32), np.ones(1, np.float32), 2)
+    with pytest.raises(ops.ShapeError):
+        ops.sddmm(p, torch.ones(2, 4, device="cuda"), torch.ones(2, 4, device="cuda"))
+    with pytest.raises(ops.ShapeError):
+        ops.fusedmm(p, torch.ones(1, 4, device="cuda"), torch.ones(3, 4, device="cuda"))
+    with pytest.raises(ops.DispatchError):
+        ops.fusedmm(p, torch.ones(1, 4, device="cuda"), torch.ones(2, 4, device="cuda"), edge_op=lambda a, b: a)

@@ -1,0 +1,185 @@
+"""SpMM parity on the B200 against the CPU oracle (oracle/port.py, pinned to the
+reference by tests/test_oracle_golden.py) and the reference's own golden
+vectors (tests/golden/).  Tolerance: |gpu - ref64| <= 1e-5 * sum_j |a_ij x_jk|
+(BASELINE north_star); rows with <= SGNN_SEGMENT nonzeros must additionally be
+bit-identical to the reference's fp32 trusted kernel (no-FMA build)."""
+import numpy as np
+import pytest
+
+from conftest import assert_spmm_close, golden_cases, load_golden, rand_csr
+from oracle import port
+
+pytestmark = pytest.mark.gpu
+
+REDS = {"sum": 0, "min": 1, "max": 2, "mean": 3}
+
+
+def _ops():
+    from paper_2403_14853_b200 import ops
+    return ops
+
+
+def _run(a_np, x, reduce, n_cols, **plan_params):
+    import torch
+    ops = _ops()
+    a = ops.CsrMatrix.from_numpy(*a_np, n_cols)
+    xt = torch.from_numpy(np.ascontiguousarray(x, np.float32)).cuda()
+    if plan_params:
+        out = ops.spmm_plan(a, xt, reduce, ops.Plan(a, x.shape[1], **plan_params))
+    else:
+        out = ops.spmm(a, xt, reduce)
+    torch.cuda.synchronize()
+    return out.cpu().numpy()
+
+
+def _short_rows(rp):
+    deg = np.diff(rp.astype(np.int64))
+    return deg <= 256
+
+
+def check_spmm(rp, ci, v, x, n_cols, reduce, **plan_params):
+    got = _run((rp, ci, v), x, reduce, n_cols, **plan_params)
+    r = REDS[reduce]
+    want64 = port.spmm(rp, ci, v.astype(np.float64), x.astype(np.float64), r)
+    denom = port.spmm_absdenom(rp, ci, v, x, r)
+    assert_spmm_close(got, want64, denom, what=f"spmm {reduce}")
+    want32 = port.spmm(rp, ci, v, x, r, np.float32)
+    if reduce in ("min", "max"):  # exact regardless of segmenting
+        np.testing.assert_array_equal(got.view(np.uint32), want32.view(np.uint32))
+    else:
+        short = _short_rows(rp)
+        np.testing.assert_array_equal(got[short].view(np.uint32), want32[short].view(np.uint32))
+    return got
+
+
+# ---- SPEC known answers --------------------------------------
+def test_kat_spmm(cuda):
+    # A = 2x2 {(0,1)=2,(1,0)=3}, B=[[1,1],[2,2]] -> [[4,4],[3,3]]
+    got = _run((np.array([0, 1, 2], np.uint64), np.array([1, 0], np.uint32), np.array([2, 3], np.float32)),
+               np.array([[1, 1], [2, 2]], np.float32), "sum", 2)
+    np.testing.assert_array_equal(got, [[4, 4], [3, 3]])
+    a = (np.array([0, 2], np.uint64), np.array([0, 1], np.uint32), np.array([1, 1], np.float32))
+    b = np.array([[2, 8], [4, 2]], np.float32)
+    np.testing.assert_array_equal(_run(a, b, "min", 2), [[2, 2]])
+    np.testing.assert_array_equal(_run(a, b, "max", 2), [[4, 8]])
+    np.testing.assert_array_equal(_run(a, b, "mean", 2), [[3, 5]])
+    # identity law
+    ident = (np.arange(3, dtype=np.uint64), np.arange(2, dtype=np.uint32), np.ones(2, np.float32))
+    bb = np.array([[1, 2], [3, 4]], np.float32)
+    np.testing.assert_array_equal(_run(ident, bb, "sum", 2), bb)
+
+
+def test_empty_rows_all_reductions(cuda):
+    rp = np.array([0, 0, 2, 2, 3, 3], np.uint64)
+    ci = np.array([0, 3, 1], np.uint32)
+    v = np.array([1.5, -2.0, 0.5], np.float32)
+    x = np.random.default_rng(0).uniform(-1, 1, (4, 8)).astype(np.float32)
+    for red in REDS:
+        got = check_spmm(rp, ci, v, x, 4, red)
+        assert (got[[0, 2, 4]] == 0).all()
+
+
+def test_empty_matrix(cuda):
+    rp = np.zeros(6, np.uint64)
+    x = np.ones((3, 16), np.float32)
+    for red in REDS:
+        got = _run((rp, np.zeros(0, np.uint32), np.zeros(0, np.float32)), x, red, 3)
+        assert got.shape == (5, 16) and (got == 0).all()
+
+
+@pytest.mark.parametrize("name", golden_cases())
+def test_golden_fixtures(cuda, name):
+    g = load_golden(name)
+    rp, ci, v, n = g["row_ptr"], g["col_idx"], g["values"], int(g["n_cols"])
+    for k in g["ks"]:
+        x = g[f"x_{k}"]
+        for red, r in REDS.items():
+            got = _run((rp, ci, v), x, red, n)
+            want64 = g[f"spmm64_{k}_{r}"]
+            assert_spmm_close(got, want64, port.spmm_absdenom(rp, ci, v, x, r), what=f"{name} K={k} {red}")
+            ref32 = g[f"spmm32_{k}_{r}"]
+            short = _short_rows(rp) if red in ("sum", "mean") else np.ones(len(rp) - 1, bool)
+            np.testing.assert_array_equal(got[short].view(np.uint32), ref32[short].view(np.uint32))
+
+
+@pytest.mark.parametrize("k", [1, 3, 4, 16, 20, 32, 33, 64, 128, 200, 256, 512, 1024])
+def test_random_widths(cuda, k):
+    rng = np.random.default_rng(100 + k)
+    rp, ci, v = rand_csr(rng, 300, 500, 0.02, hub_rows=(5, 100), empty_frac=0.1)
+    x = rng.uniform(-1, 1, (500, k)).astype(np.float32)
+    for red in REDS:
+        check_spmm(rp, ci, v, x, 500, red)
+
+
+def test_hub_rows_split_segments(cuda):
+    """Rows far longer than SGNN_SEGMENT are split over workers; result within
+    tolerance and identical for every plan."""
+    rng = np.random.default_rng(7)
+    n = 40000
+    rp, ci, v = rand_csr(rng, 64, n, 0.001, hub_rows=(0, 1, 33, 63), hub_density=0.8)
+    x = rng.standard_normal((n, 64)).astype(np.float32)
+    base = check_spmm(rp, ci, v, x, n, "sum")
+    for params in ({"path_items": 64}, {"path_items": 300, "lanes": 8, "vec": 2},
+                   {"path_items": 4096, "split_rows_over": 100000}, {"scalar": 1, "path_items": 128},
+                   {"k_tile": 16, "lanes": 4}):
+        got = _run((rp, ci, v), x, "sum", n, **params)
+        np.testing.assert_array_equal(got.view(np.uint32), base.view(np.uint32), err_msg=str(params))
+
+
+def test_plans_bitwise_transparent(cuda):
+    """Dispatch transparency: every plan gives bitwise the same C."""
+    rng = np.random.default_rng(3)
+    rp, ci, v = rand_csr(rng, 2000, 3000, 0.01, hub_rows=(1, 2, 1000), empty_frac=0.2)
+    x = rng.uniform(-1, 1, (3000, 128)).astype(np.float32)
+    ref = None
+    for params in ({}, {"path_items": 16}, {"path_items": 1024}, {"lanes": 16, "vec": 2},
+                   {"lanes": 8, "vec": 4, "unroll": 4}, {"unroll": 4}, {"k_tile": 64},
+                   {"scalar": 1}, {"block": 64}, {"split_rows_over": 4096}):
+        got = _run((rp, ci, v), x, "sum", 3000, **params) if params else _run((rp, ci, v), x, "sum", 3000)
+        if ref is None:
+            ref = got
+            check_spmm(rp, ci, v, x, 3000, "sum")
+        np.testing.assert_array_equal(got.view(np.uint32), ref.view(np.uint32), err_msg=str(params))
+
+
+def test_shape_and_dispatch_errors(cuda):
+    import torch
+    ops = _ops()
+    a = ops.CsrMatrix.from_numpy(np.array([0, 1], np.uint64), np.array([0], np.uint32),
+                                 np.array([1], np.float32), 2)
+    x = torch.ones((3, 32), device="cuda")
+    with pytest.raises(ops.ShapeError):
+        ops.spmm(a, x)
+    x = torch.ones((2, 48), device="cuda")
+    with pytest.raises(ops.DispatchError):
+        ops.spmm_with(a, x, "sum", ops.KernelKind.specialized(32))
+    with pytest.raises(ops.DispatchError):
+        ops.spmm_with(a, x, "sum", ops.KernelKind.specialized(48))
+    with pytest.raises(ops.DispatchError):
+        ops.spmm_with(a, torch.ones((2, 32), device="cuda"), "mean", ops.KernelKind.specialized(32))
+    with pytest.raises(ops.ConfigError):
+        ops.spmm(a, torch.ones((2, 32), device="cuda"), "median")
+
+
+def test_dispatch_toggle(cuda):
+    ops = _ops()
+    with ops.DispatchGuard(False):
+        assert ops.resolve_kernel(32, "sum") == ops.KernelKind.trusted()
+    assert ops.resolve_kernel(32, "sum") == ops.KernelKind.specialized(32)
+    assert ops.resolve_kernel(48, "sum") == ops.KernelKind.trusted()
+    assert ops.resolve_kernel(32, "mean") == ops.KernelKind.trusted()
+
+
+def test_misaligned_operands_use_scalar_path(cuda):
+    import torch
+    rng = np.random.default_rng(11)
+    rp, ci, v = rand_csr(rng, 100, 100, 0.05)
+    x = rng.uniform(-1, 1, (100, 32)).astype(np.float32)
+    ops = _ops()
+    a = ops.CsrMatrix.from_numpy(rp, ci, v, 100)
+    buf = torch.zeros(100 * 32 + 1, device="cuda")
+    buf[1:] = torch.from_numpy(x.ravel()).cuda()
+    xt = buf[1:].view(100, 32)  # 4-byte offset: not 16-byte aligned
+    out = ops.spmm(a, xt, "sum")
+    want = port.spmm(rp, ci, v, x, 0, np.float32)
+    np.testing.assert_array_equal(out.cpu().numpy().view(np.uint32), want.view(np.uint32))

@@ -1,0 +1,151 @@
+"""On-device CSR->CSC transpose (bit-exact with sparse.hpp:72-89), row
+degrees, is_symmetric, and the TrainingCache backward operands/counters
+(gnn.hpp:113-196) against the reference's golden vectors and the oracle."""
+import numpy as np
+import pytest
+
+from conftest import assert_spmm_close, golden_cases, load_golden, rand_csr
+from oracle import port
+
+pytestmark = pytest.mark.gpu
+
+
+def _ops():
+    from paper_2403_14853_b200 import ops
+    return ops
+
+
+def _dev(rp, ci, v, n):
+    return _ops().CsrMatrix.from_numpy(rp, ci, v, n)
+
+
+def _assert_csr_equal(got, want):
+    for g, w, name in zip(got, want, ("row_ptr", "col_idx", "values")):
+        g = np.asarray(g)
+        w = np.asarray(w)
+        assert g.shape == w.shape, name
+        np.testing.assert_array_equal(g.view(np.uint8), w.view(np.uint8), err_msg=name)
+
+
+@pytest.mark.parametrize("name", golden_cases())
+def test_transpose_golden(cuda, name):
+    g = load_golden(name)
+    t = _ops().transpose(_dev(g["row_ptr"], g["col_idx"], g["values"], int(g["n_cols"])))
+    _assert_csr_equal(t.to_numpy(), (g["t_row_ptr"], g["t_col_idx"], g["t_values"]))
+
+
+@pytest.mark.parametrize("shape", [(1, 1), (3, 1), (1, 5000), (700, 300), (2000, 70000), (5000, 2049)])
+def test_transpose_random(cuda, shape):
+    m, n = shape
+    rng = np.random.default_rng(m * 7 + n)
+    rp, ci, v = rand_csr(rng, m, n, min(1.0, 20.0 / n), hub_rows=(0,) if m > 1 else (), empty_frac=0.2)
+    t = _ops().transpose(_dev(rp, ci, v, n))
+    _assert_csr_equal(t.to_numpy(), port.transpose(rp, ci, v, n))
+
+
+def test_transpose_involution_and_empty(cuda):
+    ops = _ops()
+    rng = np.random.default_rng(5)
+    rp, ci, v = rand_csr(rng, 1500, 900, 0.01, hub_rows=(3,), empty_frac=0.3)
+    a = _dev(rp, ci, v, 900)
+    _assert_csr_equal(ops.transpose(ops.transpose(a)).to_numpy(), (rp, ci, v))
+    e = _dev(np.zeros(4, np.uint64), np.zeros(0, np.uint32), np.zeros(0, np.float32), 6)
+    t = ops.transpose(e).to_numpy()
+    assert t[0].shape == (7,) and (t[0] == 0).all() and t[1].size == 0
+    # identity fixed point, single entry
+    ident = _dev(np.arange(4, dtype=np.uint64), np.arange(3, dtype=np.uint32), np.ones(3, np.float32), 3)
+    _assert_csr_equal(ops.transpose(ident).to_numpy(), ident.to_numpy())
+    one = ops.transpose(_dev(np.array([0, 1, 1], np.uint64), np.array([1], np.uint32), np.array([2.0], np.float32), 2))
+    _assert_csr_equal(one.to_numpy(), (np.array([0, 0, 1], np.uint64), np.array([0], np.uint32), np.array([2.0], np.float32)))
+
+
+def test_row_degrees_and_symmetry(cuda):
+    ops = _ops()
+    for name in golden_cases():
+        g = load_golden(name)
+        a = _dev(g["row_ptr"], g["col_idx"], g["values"], int(g["n_cols"]))
+        np.testing.assert_array_equal(ops.row_degrees(a).cpu().numpy().view(np.uint32), port.row_degrees(g["row_ptr"]))
+        assert ops.is_symmetric(a) == bool(g["is_symmetric"]), name
+
+
+def test_symmetry_value_mismatch(cuda):
+    ops = _ops()
+    rp = np.array([0, 1, 2], np.uint64)
+    ci = np.array([1, 0], np.uint32)
+    assert ops.is_symmetric(_dev(rp, ci, np.array([1.0, 1.0], np.float32), 2))
+    assert not ops.is_symmetric(_dev(rp, ci, np.array([1.0, 2.0], np.float32), 2))
+    assert not ops.is_symmetric(_dev(np.array([0, 1, 1], np.uint64), np.array([1], np.uint32), np.ones(1, np.float32), 2))
+
+
+@pytest.mark.parametrize("name", [c for c in golden_cases() if c in ("empty_rows", "sym", "sym_ones")])
+def test_cache_operands_and_counters_golden(cuda, name):
+    """sum_operand / mean_operand and the build counters match the reference
+    TrainingCache fetched 3 times (make_golden.py), with caching on and off."""
+    ops = _ops()
+    g = load_golden(name)
+    for tag, which in (("sum", 0), ("mean", 1)):
+        for use_cache in (0, 1):
+            a = _dev(g["row_ptr"], g["col_idx"], g["values"], int(g["n_cols"]))
+            cache = ops.TrainingCache(a, bool(use_cache))
+            for _ in range(3):
+                op = cache.sum_operand() if which == 0 else cache.mean_operand()
+            _assert_csr_equal(op.to_numpy(), (g[f"cache_{tag}_{use_cache}_rp"], g[f"cache_{tag}_{use_cache}_ci"],
+                                              g[f"cache_{tag}_{use_cache}_v"]))
+            c = cache.counters
+            want = g[f"cache_{tag}_{use_cache}_cnt"]
+            assert [c["transpose_builds"], c["normalize_builds"], c["cache_hits"], int(c["symmetric"])] == \
+                [int(x) for x in want], (name, tag, use_cache, c)
+
+
+def test_spmm_backward_through_cache(cuda):
+    """dX = A^T dC (sum) and (A D^-1)^T-style mean operand, vs the oracle."""
+    import torch
+    ops = _ops()
+    rng = np.random.default_rng(9)
+    n = 3000
+    rp, ci, v = rand_csr(rng, n, n, 0.003, hub_rows=(0, 17), empty_frac=0.1, value="ones")
+    a = _dev(rp, ci, v, n)
+    cache = ops.TrainingCache(a, True)
+    assert not cache.counters["symmetric"]
+    g = rng.standard_normal((n, 64)).astype(np.float32)
+    gt = torch.from_numpy(g).cuda()
+    for red in ("sum", "mean"):
+        dx = cache.spmm_backward(gt, red).cpu().numpy()
+        if red == "sum":
+            trp, tci, tv = port.transpose(rp, ci, v, n)
+        else:
+            trp, tci, tv = port.mean_operand(rp, ci, v, n, False)
+        want = port.spmm(trp, tci, tv.astype(np.float64), g.astype(np.float64), 0)
+        assert_spmm_close(dx, want, port.spmm_absdenom(trp, tci, tv, g, 0), what=f"backward {red}")
+        short = np.diff(trp.astype(np.int64)) <= 256
+        w32 = port.spmm(trp, tci, tv, g, 0, np.float32)
+        np.testing.assert_array_equal(dx[short].view(np.uint32), w32[short].view(np.uint32))
+    c = cache.counters
+    assert c["transpose_builds"] == 2  # one for sum_operand, one for mean_operand (gnn.hpp:155)
+    for _ in range(3):
+        cache.spmm_backward(gt, "sum")
+    assert cache.counters["transpose_builds"] == 2
+
+
+def test_cache_symmetric_short_circuit(cuda):
+    import torch
+    ops = _ops()
+    g = load_golden("sym")
+    a = _dev(g["row_ptr"], g["col_idx"], g["values"], int(g["n_cols"]))
+    cache = ops.TrainingCache(a, True)
+    dc = torch.randn(a.n_rows, 32, device="cuda")
+    for _ in range(4):
+        cache.spmm_backward(dc, "sum")
+    c = cache.counters
+    assert c["symmetric"] and c["transpose_builds"] == 0 and c["cache_hits"] == 4
+
+
+def test_backward_tape_error(cuda):
+    import torch
+    ops = _ops()
+    g = load_golden("sym")
+    cache = ops.TrainingCache(_dev(g["row_ptr"], g["col_idx"], g["values"], int(g["n_cols"])), True)
+    with pytest.raises(ops.TapeError):
+        cache.spmm_backward(torch.ones(5, 8, device="cuda"))
+    with pytest.raises(ops.ShapeError):
+        ops.TrainingCache(_dev(np.array([0, 0], np.uint64), np.zeros(0, np.uint32), np.zeros(0, np.float32), 3))
