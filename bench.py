@@ -1,0 +1,434 @@
+#!/usr/bin/env python
+"""Benchmark of the sparse hot path (BASELINE.json metric) -- one JSON line.
+
+Workload (BASELINE configs[1], "cfg2"): SpMM forward + backward through the
+cached CSC on an R-MAT graph with 2^18 nodes, N*256 samples (a,b,c,d) =
+(.57,.19,.19,.05), duplicates removed (50.07M nnz), values 1.0, sum
+aggregation, X and dC N(0,1) 2^18 x 128 fp32.  One *step* =
+  C  = spmm(A, X)             (kernels.hpp:179 / gnn.hpp:237)
+  dX = spmm(A^T, dC)          (TrainingCache::sum_operand, gnn.hpp:275/290)
+with A^T built once on the device before timing (the cache; its build time
+is reported separately as `transpose_ms`).
+
+  value  = 2 * (2*nnz*K) / step time   [GFLOP/s], inputs resident in HBM,
+           L2 flushed (256 MiB write) between steps, device-timed (CUDA events)
+  e2e    = the same metric through the public API with pinned HOST buffers:
+           H2D of X and dC, both SpMMs, D2H of C and dX inside the timed region
+  roofline = algorithmic bytes of the SpMM launches / their event-timed
+           duration vs the measured HBM copy bandwidth (MEASURED_PEAKS.json)
+
+--impl reference runs the reference's own CPU implementation (oracle/_ref,
+the reference compiled from /root/reference/proj) on the host cores.
+--gpus N (under torchrun): N independent replicas (the cfg2 path is a
+single-GPU problem; "replicas only"), max time over ranks.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "SpMM/FusedMM GFLOP/s (2·nnz·K) and % of HBM roofline; GNN epoch time"
+FALLBACK_HBM = 6650.0
+
+
+def parse():
+    p = argparse.ArgumentParser()
+    p.add_argument("--gpus", type=int, default=1)
+    p.add_argument("--steps", type=int, default=100)
+    p.add_argument("--warmup", type=int, default=5)
+    p.add_argument("--impl", choices=("ours", "reference"), default="ours")
+    p.add_argument("--seed", type=int, default=1)
+    p.add_argument("--no-cpu-baseline", action="store_true")
+    p.add_argument("--no-e2e", action="store_true")
+    p.add_argument("--plan", type=str, default="", help="JSON plan params override")
+    return p.parse_args()
+
+
+def peaks():
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        with open(path) as f:
+            d = json.load(f)
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs, burst copy)"
+    except Exception:
+        return FALLBACK_HBM, "fallback (B200_PROFILING.md 6.65 TB/s)"
+
+
+def spmm_bytes(m, nnz, k):
+    """Algorithmic bytes: CSR arrays + feature gathers + output."""
+    return 8 * (m + 1) + 8 * nnz + 4 * nnz * k + 4 * m * k
+
+
+def dist_env():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return ws, rank, local
+
+
+class ClockSampler:
+    """Samples SM clocks and clock-event reasons via NVML during the timed region."""
+    NAMES = {0x2: "applications_clocks_setting", 0x4: "sw_power_cap", 0x8: "hw_slowdown",
+             0x20: "sw_thermal_slowdown", 0x40: "hw_thermal_slowdown", 0x80: "hw_power_brake_slowdown"}
+
+    def __init__(self, index):
+        self.samples, self.reasons, self.max_mhz = [], set(), None
+        self.stop = threading.Event()
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+        except Exception:
+            self.nv = None
+
+    def _run(self):
+        while not self.stop.is_set():
+            try:
+                self.samples.append(self.nv.nvmlDeviceGetClockInfo(self.h, self.nv.NVML_CLOCK_SM))
+                try:
+                    bits = self.nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+                except AttributeError:
+                    bits = self.nv.nvmlDeviceGetCurrentClocksThrottleReasons(self.h)
+                for b, n in self.NAMES.items():
+                    if bits & b:
+                        self.reasons.add(n)
+            except Exception:
+                pass
+            time.sleep(0.01)
+
+    def __enter__(self):
+        if self.nv:
+            self.t = threading.Thread(target=self._run, daemon=True)
+            self.t.start()
+        return self
+
+    def __exit__(self, *a):
+        if self.nv:
+            self.stop.set()
+            self.t.join()
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": sorted(self.reasons), "samples": 0}
+        return {"sm_mhz": statistics.median(self.samples), "sm_max_mhz": self.max_mhz,
+                "reasons": sorted(self.reasons), "samples": len(self.samples)}
+
+
+def load_traffic(workload):
+    """ncu dram bytes per launch for the dominant kernel (profiles/traffic.json)."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "traffic.json")) as f:
+            return json.load(f).get(workload)
+    except Exception:
+        return None
+
+
+def build_workload(seed):
+    from paper_2403_14853_b200 import graphs
+    w = graphs.cfg2(seed)
+    x = graphs.normal(w.n_cols * w.k, 0.0, 1.0, seed, stream=21).reshape(w.n_cols, w.k)
+    g = graphs.normal(w.n_rows * w.k, 0.0, 1.0, seed, stream=22).reshape(w.n_rows, w.k)
+    return w, x, g
+
+
+def config_of(w, extra=None):
+    c = {"workload": "cfg2: SpMM fwd + bwd (cached CSC), R-MAT 2^18 avg-deg 256 sampled, dedup",
+         "n_rows": w.n_rows, "nnz": w.nnz, "K": w.k, "reduce": "sum", "values": "1.0",
+         "X,dC": "N(0,1)", "rmat": "(0.57,0.19,0.19,0.05), no permutation, N*256 samples",
+         "seed": w.seed, "l2": "flushed between steps (256 MiB write), flush not timed"}
+    if extra:
+        c.update(extra)
+    return c
+
+
+# ------------------------------------------------------------------ CPU arms
+def cpu_reference_run(w, x, g, steps, warmup, budget_s=150.0, flavours=None):
+    """Times the reference's own CPU path (oracle/_ref) on all host threads.
+    Picks the fastest (flags, kernel) pair like BASELINE.md section 2, then
+    times `steps` fwd+bwd steps; if that would exceed the budget, each step is
+    a row sample of the workload (every f-th 64-row block of A, all columns)."""
+    import numpy as np
+
+    from oracle import ref
+    flav = flavours or ref.flavours()
+    if not flav:
+        return None
+    cores = os.cpu_count() or 1
+    rp, ci, v = w.row_ptr, w.col_idx, w.values
+
+    def make(rp_, ci_, v_):
+        return {f: ref.Bench(rp_, ci_, v_, w.n_cols, x, g[: len(rp_) - 1], 0, f) for f in flav}
+
+    def sample(frac):
+        m = w.n_rows
+        blk = (np.arange(m) // 64) % frac == 0
+        rows = np.nonzero(blk)[0]
+        deg = np.diff(rp.astype(np.int64))[rows]
+        srp = np.zeros(len(rows) + 1, np.uint64)
+        srp[1:] = np.cumsum(deg)
+        idx = np.concatenate([np.arange(rp[i], rp[i + 1], dtype=np.int64) for i in rows]) if len(rows) else np.zeros(0, np.int64)
+        return srp, ci[idx], v[idx]
+
+    frac = 1
+    benches = make(rp, ci, v)
+    best, best_t = None, None
+    for f, b in benches.items():
+        for spec in (False, True):
+            t0 = time.perf_counter()
+            b.step(specialized=spec, threads=0)
+            dt = time.perf_counter() - t0
+            if best_t is None or dt < best_t:
+                best, best_t = (f, spec), dt
+    est = best_t * (steps + warmup)
+    nnz = w.nnz
+    if est > budget_s:
+        frac = int(np.ceil(est / budget_s))
+        srp, sci, sv = sample(frac)
+        benches = {best[0]: ref.Bench(srp, sci, sv, w.n_cols, x, g[: len(srp) - 1], 0, best[0])}
+        nnz = int(srp[-1])
+    b = benches[best[0]]
+    for _ in range(warmup):
+        b.step(specialized=best[1], threads=0)
+    times = []
+    for _ in range(steps):
+        t0 = time.perf_counter()
+        b.step(specialized=best[1], threads=0)
+        times.append(time.perf_counter() - t0)
+    for bb in benches.values():
+        bb.close()
+    total = sum(times)
+    flops = 2 * (2 * nnz * w.k)
+    from oracle.ref import FLAVOURS
+    return {
+        "value": flops * steps / total / 1e9, "unit": "GFLOP/s", "cores": cores, "kind": "reference",
+        "ms_per_step": total / steps * 1e3,
+        "sample": (f"full cfg2 fwd+bwd step ({nnz} nnz)" if frac == 1 else
+                   f"1/{frac} row sample of cfg2 (every {frac}th 64-row block; {nnz} nnz) per step"),
+        "kernel": f"{'specialized' if best[1] else 'trusted'} spmm_into, g++ {FLAVOURS[best[0]][1]}",
+        "steps": steps,
+    }
+
+
+# ----------------------------------------------------------------- GPU arm
+def run_ours(args):
+    import numpy as np
+    import torch
+
+    from paper_2403_14853_b200 import ops
+
+    ws, rank, local = dist_env()
+    torch.cuda.set_device(local)
+    dist = None
+    if ws > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    dev = torch.device("cuda", local)
+
+    t0 = time.time()
+    w, x_np, g_np = build_workload(args.seed)
+    gen_s = time.time() - t0
+    a = ops.CsrMatrix.from_numpy(w.row_ptr, w.col_idx, w.values, w.n_cols, device=dev)
+    x = torch.from_numpy(x_np).to(dev)
+    g = torch.from_numpy(g_np).to(dev)
+    c = torch.empty(w.n_rows, w.k, device=dev)
+    dx = torch.empty(w.n_cols, w.k, device=dev)
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+    stream = torch.cuda.current_stream()
+
+    params = json.loads(args.plan) if args.plan else {}
+    torch.cuda.synchronize()
+    e_t0, e_t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e_t0.record()
+    cache = ops.TrainingCache(a, True)          # symmetric probe + degrees
+    at = cache.sum_operand()                     # device CSC, built once (counted)
+    e_t1.record()
+    torch.cuda.synchronize()
+    cache_ms = e_t0.elapsed_time(e_t1)
+    plan_f = ops.Plan(a, w.k, **params)
+    plan_b = ops.Plan(at, w.k, **params)
+
+    def step():
+        ops.spmm_plan(a, x, "sum", plan_f, c)
+        ops.spmm_plan(at, g, "sum", plan_b, dx)
+
+    for _ in range(max(3, args.warmup)):
+        flush.zero_()
+        step()
+    torch.cuda.synchronize()
+    if dist:
+        dist.barrier()
+    ev = [[torch.cuda.Event(enable_timing=True) for _ in range(3)] for _ in range(args.steps)]
+    nvml_index = local
+    cvd = os.environ.get("CUDA_VISIBLE_DEVICES", "")
+    if cvd:
+        ids = cvd.split(",")
+        if local < len(ids) and ids[local].strip().isdigit():
+            nvml_index = int(ids[local])
+    with ClockSampler(nvml_index) as clk:
+        torch.cuda.synchronize()
+        for s in range(args.steps):
+            flush.zero_()
+            ev[s][0].record(stream)
+            ops.spmm_plan(a, x, "sum", plan_f, c)
+            ev[s][1].record(stream)
+            ops.spmm_plan(at, g, "sum", plan_b, dx)
+            ev[s][2].record(stream)
+        torch.cuda.synchronize()
+    if dist:
+        dist.barrier()
+    fwd = [e[0].elapsed_time(e[1]) for e in ev]
+    bwd = [e[1].elapsed_time(e[2]) for e in ev]
+    total_ms = sum(fwd) + sum(bwd)
+    if dist:
+        tt = torch.tensor([total_ms], device=dev, dtype=torch.float64)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        total_ms = float(tt.item())
+    ms_step = total_ms / args.steps
+    flops_step = 2 * (2 * w.nnz * w.k)
+    value = flops_step * args.steps * ws / (total_ms * 1e-3) / 1e9
+
+    # warm-L2 reference number (not the headline)
+    torch.cuda.synchronize()
+    s0, s1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    s0.record()
+    for _ in range(10):
+        step()
+    s1.record()
+    torch.cuda.synchronize()
+    warm_ms = s0.elapsed_time(s1) / 10
+
+    # roofline of the SpMM launches (worker + fixup per call)
+    bytes_f = spmm_bytes(w.n_rows, w.nnz, w.k)
+    bytes_b = spmm_bytes(w.n_cols, w.nnz, w.k)
+    peak, peak_src = peaks()
+    achieved = (bytes_f + bytes_b) * args.steps / (sum(fwd) + sum(bwd)) / 1e6  # GB/s
+    pf, pb = plan_f.stats, plan_b.stats
+    launches_step = (1 + (1 if pf["split_rows"] else 0)) + (1 + (1 if pb["split_rows"] else 0))
+    traffic = load_traffic("cfg2")
+
+    # parity spot check of this run's outputs (cheap; full parity lives in tests/)
+    out = {
+        "metric": METRIC, "value": round(value, 2), "unit": "GFLOP/s", "n_gpus": ws,
+        "steps": args.steps, "warmup": max(3, args.warmup), "ms_per_step": round(ms_step, 4),
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+        "data": "synthetic (seeded R-MAT, BASELINE cfg2 shapes; paper datasets not available offline)",
+        "config": config_of(w, {"parallelism": f"replicas x{ws}" if ws > 1 else "1 GPU",
+                                "plan_fwd": plan_f.params, "plan_bwd": plan_b.params}),
+        "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
+                     "frac": round(achieved / peak, 4), "traffic": traffic,
+                     "peak_source": peak_src,
+                     "alg_bytes_per_step": bytes_f + bytes_b,
+                     "note": "achieved = algorithmic bytes (CSR + gathered X rows + output) / event-timed SpMM; "
+                             "gathers hitting L2 can push frac past 1 -- see traffic (ncu dram bytes)"},
+        "gpu_launches": launches_step * args.steps,
+        "fwd_ms": round(sum(fwd) / args.steps, 4), "bwd_ms": round(sum(bwd) / args.steps, 4),
+        "warm_l2_ms_per_step": round(warm_ms, 4), "transpose_ms": round(cache_ms, 3),
+        "gen_s": round(gen_s, 2),
+    }
+    out["clocks"] = clk.summary()
+
+    if not args.no_e2e:
+        out["e2e"] = e2e_run(a, at, w, x_np, g_np, dev, plan_f, plan_b, args, ws, dist)
+
+    if rank == 0 and ws == 1 and not args.no_cpu_baseline:
+        try:
+            cb = cpu_reference_run(w, x_np, g_np, steps=3, warmup=1, budget_s=25.0)
+        except Exception as ex:  # noqa: BLE001
+            cb = {"error": str(ex)}
+        out["cpu_baseline"] = cb
+    if dist:
+        dist.barrier()
+        dist.destroy_process_group()
+    if rank == 0:
+        print(json.dumps(out), flush=True)
+
+
+def e2e_run(a, at, w, x_np, g_np, dev, plan_f, plan_b, args, ws, dist):
+    """Public-API step with host buffers: H2D(X, dC) -> spmm -> spmm_backward -> D2H(C, dX)."""
+    import torch
+
+    from paper_2403_14853_b200 import ops
+    hx = torch.from_numpy(x_np).pin_memory()
+    hg = torch.from_numpy(g_np).pin_memory()
+    hc = torch.empty(w.n_rows, w.k).pin_memory()
+    hdx = torch.empty(w.n_cols, w.k).pin_memory()
+    dxd = torch.empty_like(hx, device=dev)
+    dgd = torch.empty_like(hg, device=dev)
+    c = torch.empty(w.n_rows, w.k, device=dev)
+    dx = torch.empty(w.n_cols, w.k, device=dev)
+    steps = max(5, min(args.steps, 30))
+
+    def step():
+        dxd.copy_(hx, non_blocking=True)
+        dgd.copy_(hg, non_blocking=True)
+        ops.spmm_plan(a, dxd, "sum", plan_f, c)
+        ops.spmm_plan(at, dgd, "sum", plan_b, dx)
+        hc.copy_(c, non_blocking=True)
+        hdx.copy_(dx, non_blocking=True)
+
+    for _ in range(3):
+        step()
+    torch.cuda.synchronize()
+    if dist:
+        dist.barrier()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(steps):
+        step()
+    e1.record()
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1)
+    if dist:
+        tt = torch.tensor([ms], device=dev, dtype=torch.float64)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        ms = float(tt.item())
+    flops = 2 * (2 * w.nnz * w.k) * steps * ws
+    return {"value": round(flops / (ms * 1e-3) / 1e9, 2), "unit": "GFLOP/s",
+            "h2d_bytes_per_step": hx.numel() * 4 + hg.numel() * 4,
+            "d2h_bytes_per_step": hc.numel() * 4 + hdx.numel() * 4,
+            "ms_per_step": round(ms / steps, 4), "steps": steps,
+            "note": "graph (CSR + cached CSC) resident on the device like the reference's TrainingCache; "
+                    "dense inputs/outputs cross PCIe every step from pinned host memory"}
+
+
+def run_reference(args):
+    ws, rank, _ = dist_env()
+    if rank != 0:
+        return
+    w, x_np, g_np = build_workload(args.seed)
+    cb = cpu_reference_run(w, x_np, g_np, steps=args.steps, warmup=args.warmup, budget_s=150.0)
+    if cb is None:
+        print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref not built (needs /root/reference at build time)"}))
+        return
+    out = {
+        "impl": "reference", "metric": METRIC, "value": round(cb["value"], 3), "unit": "GFLOP/s",
+        "n_gpus": ws, "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(cb["ms_per_step"], 3),
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+        "data": "synthetic (seeded R-MAT, BASELINE cfg2 shapes)", "config": config_of(w, {"l2": "n/a (CPU)"}),
+        "cpu_baseline": {"value": round(cb["value"], 3), "unit": "GFLOP/s", "cores": cb["cores"],
+                         "kind": "reference", "sample": cb["sample"], "kernel": cb["kernel"]},
+        "e2e": {"value": round(cb["value"], 3), "unit": "GFLOP/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(out), flush=True)
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

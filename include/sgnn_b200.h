@@ -92,8 +92,10 @@ typedef struct sgnn_plan_params {
     uint32_t split_rows_over; /* rows with more nonzeros than this may be split across
                                  workers (rounded up to a multiple of SGNN_SEGMENT) */
     uint32_t k_tile;       /* floats of K per pass over the matrix (0 = all of K) */
-    uint32_t block;        /* threads per CTA: 64, 128 or 256 */
+    uint32_t block;        /* threads per CTA: 64 or 128 */
     uint32_t scalar;       /* 1 = force the scalar-load ("trusted") path */
+    uint32_t occupancy;    /* register cap as resident 128-thread CTAs per SM the kernel must
+                              fit: 0/1 = compiler's choice, 4, 6 or 8 (float4 path) */
 } sgnn_plan_params;
 
 typedef struct sgnn_plan_s* sgnn_plan;
@@ -141,6 +143,24 @@ sgnn_status sgnn_spmm_f32(const sgnn_csr* a, const float* x, uint32_t x_rows, ui
 sgnn_status sgnn_spmm_with_f32(const sgnn_csr* a, const float* x, uint32_t x_rows, uint32_t k,
                                float* c, int reduce, int kind, uint32_t spec_k, sgnn_plan plan,
                                sgnn_stream stream);
+
+/* On-device autotuner (replaces run_tuning, autotune.hpp:99-164): times every
+ * candidate launch geometry for (a, k, reduce) -- lanes x float4s per lane
+ * (the K-tile), gathers in flight, path items per worker, split threshold,
+ * CTA size -- with CUDA events (median of `reps` >= 3, else
+ * SGNN_ERR_CONFIG), asserts each candidate's output is bit-identical to the
+ * default plan's (else SGNN_ERR_INTERNAL, as autotune.hpp:131-133) and
+ * returns the fastest as a new plan.  x may be NULL (a seeded uniform [0,1)
+ * operand is generated, as autotune.hpp:119-121).  entries (optional)
+ * receives up to max_entries timings.  Synchronous. */
+typedef struct sgnn_tune_entry {
+    sgnn_plan_params params;
+    float ms; /* median time of one SpMM with these params */
+    float reserved;
+} sgnn_tune_entry;
+sgnn_status sgnn_tune_spmm(const sgnn_csr* a, const float* x, uint32_t k, int reduce, int reps,
+                           sgnn_plan* best, sgnn_tune_entry* entries, int max_entries,
+                           int* n_entries, sgnn_stream stream);
 
 /* resolve_kernel(k, reduce) (kernels.hpp:38, src/dispatch.cpp:21-28) and the
  * dispatch toggle set_dispatch/get_dispatch (autotune.hpp:36-37,

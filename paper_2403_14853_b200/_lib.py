@@ -75,10 +75,15 @@ class Csr(C.Structure):
 class PlanParams(C.Structure):
     _fields_ = [("lanes", C.c_uint32), ("vec", C.c_uint32), ("unroll", C.c_uint32),
                 ("path_items", C.c_uint32), ("split_rows_over", C.c_uint32),
-                ("k_tile", C.c_uint32), ("block", C.c_uint32), ("scalar", C.c_uint32)]
+                ("k_tile", C.c_uint32), ("block", C.c_uint32), ("scalar", C.c_uint32),
+                ("occupancy", C.c_uint32)]
 
     def as_dict(self):
         return {f: int(getattr(self, f)) for f, _ in self._fields_}
+
+
+class TuneEntry(C.Structure):
+    _fields_ = [("params", PlanParams), ("ms", C.c_float), ("reserved", C.c_float)]
 
 
 # Every symbol include/sgnn_b200.h declares, with (restype, argtypes).
@@ -95,6 +100,8 @@ SIGNATURES = {
     "sgnn_plan_stats": (i32, [P, C.POINTER(u64), C.POINTER(u64), C.POINTER(u64)]),
     "sgnn_spmm_f32": (i32, [CsrP, P, u32, u32, P, i32, P, P]),
     "sgnn_spmm_with_f32": (i32, [CsrP, P, u32, u32, P, i32, i32, u32, P, P]),
+    "sgnn_tune_spmm": (i32, [CsrP, P, u32, i32, i32, C.POINTER(P), C.POINTER(TuneEntry), i32,
+                             C.POINTER(i32), P]),
     "sgnn_resolve_kernel": (i32, [u32, i32, C.POINTER(u32)]),
     "sgnn_set_dispatch": (None, [i32]),
     "sgnn_get_dispatch": (i32, []),

@@ -81,12 +81,12 @@ sgnn_status sgnn_plan_create(const sgnn_csr* a, uint32_t k, const sgnn_plan_para
         SGNN_TRY(build_plan(a, k, params, k % 4 == 0, out, cs(stream)));
         const sgnn_plan_s* p = *out;
         if (!find_spmm_launcher(p->vec, int(p->p.lanes), int(p->p.vec), int(p->p.unroll),
-                                SGNN_REDUCE_SUM)) {
+                                SGNN_REDUCE_SUM, int(p->p.occupancy))) {
             destroy_plan(*out);
             *out = nullptr;
             return fail(SGNN_ERR_UNSUPPORTED,
                         "plan_create: no kernel compiled for lanes=" + std::to_string(p->p.lanes) +
-                            " vec=" + std::to_string(p->p.vec) + " unroll=" + std::to_string(p->p.unroll) +
+                            " vec=" + std::to_string(p->p.vec) + " unroll=" + std::to_string(p->p.unroll) + " occupancy=" + std::to_string(p->p.occupancy) +
                             (p->vec ? " (float4)" : " (scalar)"));
         }
         return SGNN_OK;
@@ -145,6 +145,19 @@ sgnn_status sgnn_spmm_with_f32(const sgnn_csr* a, const float* x, uint32_t x_row
     if (kind != SGNN_KERNEL_TRUSTED) return fail(SGNN_ERR_CONFIG, "spmm_with: unknown kernel kind");
     // trusted: the default (untuned) plan -- bitwise the same result
     return spmm_dispatch(a, x, k, c, reduce, nullptr, cs(stream));
+}
+
+sgnn_status sgnn_tune_spmm(const sgnn_csr* a, const float* x, uint32_t k, int reduce, int reps,
+                           sgnn_plan* best, sgnn_tune_entry* entries, int max_entries,
+                           int* n_entries, sgnn_stream stream) {
+    SGNN_TRY(check_csr(a, "run_tuning"));
+    if (!best) return fail(SGNN_ERR_CONFIG, "run_tuning: null out");
+    if (reduce < 0 || reduce > 3) return fail(SGNN_ERR_CONFIG, "run_tuning: unknown reduce op");
+    try {
+        return tune_spmm(a, x, k, reduce, reps, best, entries, max_entries, n_entries, cs(stream));
+    } catch (const std::bad_alloc&) {
+        return fail(SGNN_ERR_NOMEM, "run_tuning: host allocation failed");
+    }
 }
 
 int sgnn_resolve_kernel(uint32_t k, int reduce, uint32_t* spec_k) {

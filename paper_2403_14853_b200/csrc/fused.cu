@@ -167,13 +167,13 @@ SpmmLauncher find_fused_launcher(bool vec, int lanes, int vregs, int unroll, int
     const bool sig = edge == SGNN_EDGE_SIGMOID_MUL;
     switch (reduce) {
         case SGNN_REDUCE_SUM:
-            return sig ? fused_lookup_sig_sum(vec, lanes, vregs, unroll) : fused_lookup_mul_sum(vec, lanes, vregs, unroll);
+            return sig ? fused_lookup_sig_sum(vec, lanes, vregs, unroll, 1) : fused_lookup_mul_sum(vec, lanes, vregs, unroll, 1);
         case SGNN_REDUCE_MEAN:
-            return sig ? fused_lookup_sig_mean(vec, lanes, vregs, unroll) : fused_lookup_mul_mean(vec, lanes, vregs, unroll);
+            return sig ? fused_lookup_sig_mean(vec, lanes, vregs, unroll, 1) : fused_lookup_mul_mean(vec, lanes, vregs, unroll, 1);
         case SGNN_REDUCE_MIN:
-            return sig ? fused_lookup_sig_min(vec, lanes, vregs, unroll) : fused_lookup_mul_min(vec, lanes, vregs, unroll);
+            return sig ? fused_lookup_sig_min(vec, lanes, vregs, unroll, 1) : fused_lookup_mul_min(vec, lanes, vregs, unroll, 1);
         case SGNN_REDUCE_MAX:
-            return sig ? fused_lookup_sig_max(vec, lanes, vregs, unroll) : fused_lookup_mul_max(vec, lanes, vregs, unroll);
+            return sig ? fused_lookup_sig_max(vec, lanes, vregs, unroll, 1) : fused_lookup_mul_max(vec, lanes, vregs, unroll, 1);
     }
     return nullptr;
 }

@@ -29,6 +29,10 @@ sgnn_status run_mean_scale(const uint32_t* col_idx, const float* vin, const uint
 sgnn_status run_row_degrees(const sgnn_csr* a, uint32_t* deg, cudaStream_t s);
 sgnn_status run_is_symmetric(const sgnn_csr* a, int* out, cudaStream_t s);
 
+sgnn_status tune_spmm(const sgnn_csr* a, const float* x, uint32_t k, int reduce, int reps,
+                      sgnn_plan_s** best_out, sgnn_tune_entry* entries, int max_entries,
+                      int* n_entries, cudaStream_t s);
+
 sgnn_status run_sddmm(const sgnn_csr* p, const float* x, const float* y, uint32_t k, float* out,
                       cudaStream_t s);
 sgnn_status run_fusedmm(const sgnn_csr* p, const float* x, const float* y, uint32_t k,

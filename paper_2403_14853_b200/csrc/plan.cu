@@ -111,20 +111,20 @@ void default_params(const sgnn_csr* a, uint32_t k, bool vec_ok, const DeviceProp
                     sgnn_plan_params* p) {
     sgnn_plan_params d{};
     if (vec_ok && !p->scalar) {
-        // two float4 per lane per gathered row measured best on B200 (cfg1/cfg2 probes)
+        // one float4 per lane, 8 gathers in flight measured best on B200 (cfg1/cfg2 probes)
         if (k <= 16) { d.lanes = 4; d.vec = 1; }
-        else if (k <= 32) { d.lanes = 4; d.vec = 2; }
-        else if (k <= 64) { d.lanes = 8; d.vec = 2; }
-        else if (k <= 128) { d.lanes = 16; d.vec = 2; }
+        else if (k <= 32) { d.lanes = 8; d.vec = 1; }
+        else if (k <= 64) { d.lanes = 16; d.vec = 1; }
+        else if (k <= 128) { d.lanes = 32; d.vec = 1; }
         else if (k <= 256) { d.lanes = 32; d.vec = 2; }
         else { d.lanes = 32; d.vec = 4; }
-        d.unroll = d.vec >= 4 ? 4 : 8;
+        d.unroll = d.vec >= 4 ? 4 : (d.vec == 2 ? 4 : 8);
     } else {
         d.lanes = 32;
         d.vec = k <= 32 ? 1 : k <= 64 ? 2 : k <= 128 ? 4 : 8;
         d.unroll = d.vec >= 8 ? 2 : 4;
     }
-    d.block = 256;
+    d.block = 128;
     // Enough workers for ~4 per resident lane group, so the tail is short.
     const uint64_t total = a->nnz + a->n_rows;
     const uint64_t groups = uint64_t(dp.sm_count > 0 ? dp.sm_count : 148) *
@@ -153,10 +153,12 @@ sgnn_status resolve_params(const sgnn_csr* a, uint32_t k, bool vec_ok, const Dev
         return fail(SGNN_ERR_CONFIG, "plan: lanes must be 4, 8, 16 or 32");
     if (p.vec != 1 && p.vec != 2 && p.vec != 4 && p.vec != 8)
         return fail(SGNN_ERR_CONFIG, "plan: vec must be 1, 2, 4 or 8");
-    if (p.unroll != 2 && p.unroll != 4 && p.unroll != 8)
-        return fail(SGNN_ERR_CONFIG, "plan: unroll must be 2, 4 or 8");
-    if (p.block < 64 || p.block > 1024 || p.block % 32)
-        return fail(SGNN_ERR_CONFIG, "plan: block must be a multiple of 32 in [64, 1024]");
+    if (p.unroll != 2 && p.unroll != 4 && p.unroll != 8 && p.unroll != 16)
+        return fail(SGNN_ERR_CONFIG, "plan: unroll must be 2, 4, 8 or 16");
+    if (p.block != 64 && p.block != 128)
+        return fail(SGNN_ERR_CONFIG, "plan: block must be 64 or 128");
+    if (p.occupancy != 0 && p.occupancy != 1 && p.occupancy != 4 && p.occupancy != 6 && p.occupancy != 8)
+        return fail(SGNN_ERR_CONFIG, "plan: occupancy must be 0, 1, 4, 6 or 8");
     if (p.path_items == 0) return fail(SGNN_ERR_CONFIG, "plan: path_items must be >= 1");
     const uint32_t width = (scalar ? 1u : 4u) * p.lanes * p.vec;  // floats one pass covers
     uint32_t kt = p.k_tile ? p.k_tile : k;

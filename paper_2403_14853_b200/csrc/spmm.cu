@@ -7,12 +7,12 @@
 
 namespace sgnn {
 
-SpmmLauncher find_spmm_launcher(bool vec, int lanes, int vregs, int unroll, int reduce) {
+SpmmLauncher find_spmm_launcher(bool vec, int lanes, int vregs, int unroll, int reduce, int occ) {
     switch (reduce) {
-        case SGNN_REDUCE_SUM: return spmm_lookup_sum(vec, lanes, vregs, unroll);
-        case SGNN_REDUCE_MEAN: return spmm_lookup_mean(vec, lanes, vregs, unroll);
-        case SGNN_REDUCE_MIN: return spmm_lookup_min(vec, lanes, vregs, unroll);
-        case SGNN_REDUCE_MAX: return spmm_lookup_max(vec, lanes, vregs, unroll);
+        case SGNN_REDUCE_SUM: return spmm_lookup_sum(vec, lanes, vregs, unroll, occ);
+        case SGNN_REDUCE_MEAN: return spmm_lookup_mean(vec, lanes, vregs, unroll, occ);
+        case SGNN_REDUCE_MIN: return spmm_lookup_min(vec, lanes, vregs, unroll, occ);
+        case SGNN_REDUCE_MAX: return spmm_lookup_max(vec, lanes, vregs, unroll, occ);
     }
     return nullptr;
 }
@@ -45,7 +45,9 @@ sgnn_status run_spmm(const sgnn_csr* a, const float* x, uint32_t k, float* c, in
             unroll = vregs >= 4 ? 2 : 4;
         }
     }
-    SpmmLauncher launch = find_spmm_launcher(vec, lanes, vregs, unroll, reduce);
+    if (!find_spmm_launcher(vec, lanes, vregs, unroll, reduce, vec ? int(plan->p.occupancy) : 1))
+        return fail(SGNN_ERR_UNSUPPORTED, "spmm: no kernel compiled for this plan and reduce op");
+    SpmmLauncher launch = find_spmm_launcher(vec, lanes, vregs, unroll, reduce, vec ? int(plan->p.occupancy) : 1);
     if (!launch)
         return fail(SGNN_ERR_UNSUPPORTED, "spmm: no kernel compiled for lanes=" +
                                               std::to_string(lanes) + " vec=" +

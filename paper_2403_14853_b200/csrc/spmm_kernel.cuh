@@ -108,6 +108,31 @@ struct Frag {
             }
         }
     }
+    // Number of this lane's register blocks inside the launch width.
+    static __device__ __forceinline__ int blocks_in(int gl, uint32_t width) {
+        const int lim = int(width / W) - gl;
+        return lim <= 0 ? 0 : min(V, (lim + G - 1) / G);
+    }
+    // Hot-loop gather of a neighbour row: `lrow` already points at this
+    // lane's first element; blocks beyond nq are skipped (ZERO: zero-filled,
+    // needed where all lanes' values are summed, i.e. the FusedMM dot).
+    template <bool ZERO>
+    __device__ __forceinline__ void gather(const float* __restrict__ lrow, int nq) {
+#pragma unroll
+        for (int q = 0; q < V; ++q) {
+            if (q < nq) {
+                if constexpr (VEC) {
+                    const float4 t = __ldg(reinterpret_cast<const float4*>(lrow + 4 * G * q));
+                    v[4 * q + 0] = t.x; v[4 * q + 1] = t.y; v[4 * q + 2] = t.z; v[4 * q + 3] = t.w;
+                } else {
+                    v[q] = __ldg(lrow + G * q);
+                }
+            } else if constexpr (ZERO) {
+#pragma unroll
+                for (int i = 0; i < W; ++i) v[W * q + i] = 0.0f;
+            }
+        }
+    }
     // Coherent load of data this thread wrote earlier in the same launch.
     __device__ __forceinline__ void load_own(const float* row, int gl, uint32_t width) {
 #pragma unroll
@@ -183,8 +208,10 @@ __device__ __forceinline__ float edge_value(float p, float dot) {
 // holds the head of row i1 when j1 > row_ptr[i1].  A row that lies entirely
 // inside [j0,j1) is written to C; a row split across workers has its
 // SGNN_SEGMENT-nonzero segment partials written to consecutive slots.
-template <int G, int V, int U, int RED, bool VEC, int OP = OP_SPMM>
-__global__ void __launch_bounds__(256) spmm_worker_kernel(const SpmmArgs a) {
+// MINB: resident 128-thread CTAs per SM the register allocation must allow
+// (1 = unconstrained); the tuner's occupancy knob.
+template <int G, int V, int U, int RED, bool VEC, int OP = OP_SPMM, int MINB = 1>
+__global__ void __launch_bounds__(128, MINB) spmm_worker_kernel(const SpmmArgs a) {
     using F = Frag<G, V, VEC>;
     using R = Reducer<RED>;
     constexpr int N = F::N;
@@ -200,10 +227,15 @@ __global__ void __launch_bounds__(256) spmm_worker_kernel(const SpmmArgs a) {
     const int gl = lane & (G - 1);
     const unsigned gmask = (G == 32) ? 0xffffffffu : (((1u << G) - 1u) << (lane & ~(G - 1)));
     const uint32_t n_groups = (gridDim.x * blockDim.x) / G;
+    // this lane's slice of any gathered row: byte offset col*ldxb from xlane
+    const char* xlane = reinterpret_cast<const char*>(a.x + F::W * gl);
+    const uint32_t ldxb = uint32_t(a.ldx) * 4u;
+    const int nq = F::blocks_in(gl, a.width);
 
     for (uint32_t w = (blockIdx.x * blockDim.x + threadIdx.x) / G; w < a.n_workers; w += n_groups) {
         const uint32_t i0 = __ldg(a.wrow + w), i1 = __ldg(a.wrow + w + 1);
         const uint64_t j0 = __ldg(a.wnz + w), j1 = __ldg(a.wnz + w + 1);
+        const uint32_t E = uint32_t(j1 - j0);  // nonzeros of this worker; hot loop is 32-bit local
         uint32_t slot = a.wslot ? __ldg(a.wslot + w) : 0u;
 
         // row_ptr window: lane gl holds rp[rb + 1 + gl] (row ends of rows rb..rb+G-1)
@@ -213,7 +245,10 @@ __global__ void __launch_bounds__(256) spmm_worker_kernel(const SpmmArgs a) {
         uint64_t rstart = __ldg(a.rp + r);
         uint64_t rend = dev::shfl_u64(gmask, rwin, 0, G);
         bool inside = (rstart >= j0) && (rend <= j1);
-        uint64_t seg_end = min(j0 + SEG, rend);
+        // local (j0-relative) row end and segment end, clamped to E
+        uint32_t rend_l = uint32_t(min(rend, j1) - j0);
+        uint32_t seg_l = min(uint32_t(SEG), rend_l);
+        uint32_t next_l = 0;  // next local position needing row/segment work (0: settle first)
         bool first = true;
         bool have_tot = false;
         F acc;
@@ -272,58 +307,81 @@ __global__ void __launch_bounds__(256) spmm_worker_kernel(const SpmmArgs a) {
             }
             rend = dev::shfl_u64(gmask, rwin, int(r - rb), G);
             inside = (rstart >= j0) && (rend <= j1);
-            seg_end = min(rstart + SEG, rend);
+            rend_l = uint32_t(min(rend, j1) - j0);
+            seg_l = uint32_t(min(rstart + SEG, min(rend, j1)) - j0);
             first = true;
             have_tot = false;
             acc.zero();
         };
+        // Row/segment bookkeeping for local position l (>= next_l): close
+        // finished rows, close a finished segment, fetch X_r for FusedMM.
+        auto settle = [&](uint32_t l) {
+            while (l >= rend_l) {
+                finish_row();
+                advance_row();
+            }
+            if (l >= seg_l) {
+                finish_segment();
+                seg_l = min(seg_l + uint32_t(SEG), rend_l);
+            }
+            if constexpr (OP != OP_SPMM) {
+                if (xrow_id != r) {
+                    xrow.load(a.xi + uint64_t(r) * a.ldxi, gl, a.width);
+                    xrow_id = r;
+                }
+            }
+            next_l = min(rend_l, seg_l);
+        };
 
-        for (uint64_t base = j0; base < j1; base += CHUNK) {
-            uint32_t cc[CH];
-            float vv[CH];
+        // (col, val) of batch b+1 are prefetched while batch b is gathered and
+        // folded, so each batch waits for one memory latency, not two.
+        uint32_t cc[CH];
+        float vv[CH];
+        auto load_cv = [&](uint32_t base) {
 #pragma unroll
             for (int h = 0; h < CH; ++h) {
-                const uint64_t idx = base + uint64_t(gl + G * h);
-                const bool ok = (gl + G * h) < CHUNK && idx < j1;
-                cc[h] = ok ? dev::ld_stream(a.ci + idx) : 0u;
-                vv[h] = ok ? dev::ld_stream(a.val + idx) : 0.0f;
+                const uint32_t lq = base + uint32_t(gl + G * h);
+                const bool ok = (gl + G * h) < CHUNK && lq < E;
+                cc[h] = ok ? dev::ld_stream(a.ci + j0 + lq) : 0u;  // 0: a safe dummy row
+                vv[h] = ok ? dev::ld_stream(a.val + j0 + lq) : 0.0f;
             }
-            const int n = (j1 - base) < uint64_t(CHUNK) ? int(j1 - base) : CHUNK;
-            {
-                constexpr int q0 = 0;
-                F xf[U];
+        };
+        if (E) load_cv(0);
+        for (uint32_t base = 0; base < E; base += CHUNK) {
+            const int n = (E - base) < uint32_t(CHUNK) ? int(E - base) : CHUNK;
+            F xf[U];
+            float av[U];
 #pragma unroll
-                for (int u = 0; u < U; ++u) {
-                    const int q = q0 + u;
-                    const uint32_t col = __shfl_sync(gmask, cc[q / G], q % G, G);
-                    if (q < n) xf[u].load(a.x + uint64_t(col) * a.ldx, gl, a.width);
+            for (int u = 0; u < U; ++u) {  // unconditional gathers (tail lanes read row 0)
+                const uint32_t col = __shfl_sync(gmask, cc[u / G], u % G, G);
+                av[u] = __shfl_sync(gmask, vv[u / G], u % G, G);
+                xf[u].template gather<OP != OP_SPMM>(
+                    reinterpret_cast<const float*>(xlane + uint64_t(col) * ldxb), nq);
+            }
+            if (base + CHUNK < E) load_cv(base + CHUNK);
+            auto fold = [&](const F& xv, float pv) {
+                float s = pv;
+                if constexpr (OP != OP_SPMM) {
+                    // s_ij = combine(p_ij, <X_i, Y_j>); Y_j is reused below (read once)
+                    s = edge_value<OP>(pv, group_dot(xrow, xv, gmask));
                 }
 #pragma unroll
-                for (int u = 0; u < U; ++u) {
-                    const int q = q0 + u;
-                    const float av = __shfl_sync(gmask, vv[q / G], q % G, G);
-                    if (q >= n) break;
-                    const uint64_t e = base + uint64_t(q);
-                    while (e >= rend) {
-                        finish_row();
-                        advance_row();
-                    }
-                    if (e >= seg_end) {
-                        finish_segment();
-                        seg_end = min(seg_end + SEG, rend);
-                    }
-                    float s = av;
-                    if constexpr (OP != OP_SPMM) {
-                        // s_ij = combine(p_ij, <X_i, Y_j>); Y_j is reused below (read once)
-                        if (xrow_id != r) {
-                            xrow.load(a.xi + uint64_t(r) * a.ldxi, gl, a.width);
-                            xrow_id = r;
-                        }
-                        s = edge_value<OP>(av, group_dot(xrow, xf[u], gmask));
-                    }
+                for (int i = 0; i < N; ++i) acc.v[i] = R::fold(acc.v[i], s, xv.v[i], first);
+                first = false;
+            };
+            if (base + uint32_t(n) <= next_l) {
+                // fast path: the whole batch continues the current row segment
 #pragma unroll
-                    for (int i = 0; i < N; ++i) acc.v[i] = R::fold(acc.v[i], s, xf[u].v[i], first);
-                    first = false;
+                for (int u = 0; u < U; ++u)
+                    if (u < n) fold(xf[u], av[u]);
+            } else {
+                // slow path: row / segment boundaries inside the batch
+#pragma unroll
+                for (int u = 0; u < U; ++u) {
+                    if (u >= n) break;
+                    const uint32_t l = base + uint32_t(u);
+                    if (l >= next_l) settle(l);
+                    fold(xf[u], av[u]);
                 }
             }
         }
@@ -372,7 +430,7 @@ __global__ void __launch_bounds__(256) spmm_fixup_kernel(const FixupArgs f) {
 // Host launcher table (spmm_launch.cu).
 using SpmmLauncher = sgnn_status (*)(const SpmmArgs&, uint32_t block, uint32_t max_blocks,
                                      cudaStream_t);
-SpmmLauncher find_spmm_launcher(bool vec, int lanes, int vec_regs, int unroll, int reduce);
+SpmmLauncher find_spmm_launcher(bool vec, int lanes, int vec_regs, int unroll, int reduce, int occ);
 sgnn_status launch_spmm_fixup(const FixupArgs& f, int reduce, cudaStream_t s);
 
 }  // namespace sgnn

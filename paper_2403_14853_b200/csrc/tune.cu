@@ -1,0 +1,197 @@
+// tune.cu -- the on-device autotuner.
+//
+// The reference tunes the embedding size K on the CPU by timing its trusted
+// kernel against register-blocked fixed-K kernels (run_tuning,
+// autotune.hpp:99-164).  On the B200 the kernel is already specialised for
+// every K; what matters is the launch geometry for a given (graph, K): lanes
+// per worker and float4s per lane (the K-tile held in registers), gathers in
+// flight, path items per worker (rows+nnz per worker, the GPU analogue of
+// rows per thread) and the split threshold for hub rows, CTA size and K
+// passes.  sgnn_tune_spmm times each candidate with CUDA events (median of
+// reps), asserts that every candidate's output is bit-identical to the
+// default plan's (the reference's warm-up equality assertion,
+// autotune.hpp:128-133 -> SGNN_ERR_INTERNAL), and returns the fastest plan.
+#include <algorithm>
+#include <vector>
+
+#include "ops.cuh"
+#include "plan.cuh"
+#include "spmm_kernel.cuh"
+
+namespace sgnn {
+namespace {
+
+__global__ void fill_uniform_kernel(float* x, uint64_t n, uint64_t seed) {
+    for (uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
+         i += uint64_t(gridDim.x) * blockDim.x) {
+        uint64_t z = seed + 0x9e3779b97f4a7c15ull * (i + 1);
+        z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ull;
+        z = (z ^ (z >> 27)) * 0x94d049bb133111ebull;
+        z ^= z >> 31;
+        x[i] = float(double(z >> 11) * 0x1.0p-53);  // uniform01 as rng.hpp:24-26
+    }
+}
+
+__global__ void compare_kernel(const uint32_t* a, const uint32_t* b, uint64_t n, int* diff) {
+    for (uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
+         i += uint64_t(gridDim.x) * blockDim.x)
+        if (a[i] != b[i]) atomicExch(diff, 1);
+}
+
+std::vector<sgnn_plan_params> candidates(const sgnn_csr* a, uint32_t k, const DeviceProps& dp) {
+    std::vector<sgnn_plan_params> out;
+    const bool vec = k % 4 == 0;
+    sgnn_plan_params d{};
+    default_params(a, k, vec, dp, &d);
+    struct LV { uint32_t lanes, vec, unroll; };
+    std::vector<LV> layouts;
+    if (vec) {
+        const LV all[] = {{4, 1, 8}, {4, 2, 8}, {8, 1, 8}, {8, 2, 4}, {8, 2, 8}, {8, 4, 4},
+                          {16, 1, 8}, {16, 2, 4}, {16, 2, 8}, {16, 4, 2}, {16, 4, 4},
+                          {32, 1, 4}, {32, 1, 8}, {32, 2, 4}, {32, 2, 8}, {32, 4, 2},
+                          {32, 4, 4}, {32, 8, 2}};
+        for (const LV& l : all) {
+            const uint32_t width = 4 * l.lanes * l.vec;
+            // one pass (width covers K, at most 2x wider) or exact K-tiles
+            if ((width >= k && width < 2 * k + 4) || (width < k && k % width == 0 && k / width <= 2))
+                layouts.push_back(l);
+        }
+    } else {
+        const LV all[] = {{32, 1, 4}, {32, 1, 8}, {32, 2, 4}, {32, 2, 8}, {32, 4, 2}, {32, 4, 4},
+                          {32, 8, 2}, {32, 8, 4}};
+        for (const LV& l : all) {
+            const uint32_t width = l.lanes * l.vec;
+            if (width >= k ? width < 2 * k + 32 : (k + width - 1) / width <= 2) layouts.push_back(l);
+        }
+    }
+    const uint32_t d0 = d.path_items;
+    const uint32_t paths[] = {std::max(16u, d0 / 2), d0, std::min(4096u, d0 * 2)};
+    for (const LV& l : layouts)
+        for (uint32_t pi : paths)
+            for (uint32_t occ : {1u, 4u, 6u, 8u}) {
+                if (!vec && occ != 1) continue;
+                sgnn_plan_params p{};
+                p.lanes = l.lanes;
+                p.vec = l.vec;
+                p.unroll = l.unroll;
+                p.path_items = pi;
+                p.split_rows_over = std::max<uint32_t>(pi, SGNN_SEGMENT);
+                p.block = 128;
+                p.scalar = vec ? 0 : 1;
+                p.occupancy = occ;
+                out.push_back(p);  // combinations without a compiled kernel are skipped
+            }
+    return out;
+}
+
+}  // namespace
+
+sgnn_status tune_spmm(const sgnn_csr* a, const float* x_in, uint32_t k, int reduce, int reps,
+                      sgnn_plan_s** best_out, sgnn_tune_entry* entries, int max_entries,
+                      int* n_entries, cudaStream_t s) {
+    *best_out = nullptr;
+    if (n_entries) *n_entries = 0;
+    if (reps < 3) return fail(SGNN_ERR_CONFIG, "run_tuning: reps must be >= 3");  // autotune.hpp:104
+    if (k == 0) return fail(SGNN_ERR_CONFIG, "run_tuning: K must be positive");
+    DeviceProps dp;
+    SGNN_TRY(device_props(&dp));
+    float* x = const_cast<float*>(x_in);
+    float *c_ref = nullptr, *c = nullptr;
+    int* diff = nullptr;
+    const uint64_t xn = uint64_t(a->n_cols) * k, cn = uint64_t(a->n_rows) * k;
+    sgnn_status st = SGNN_OK;
+    if (!x) st = scratch_alloc(reinterpret_cast<void**>(&x), sizeof(float) * (xn + 1), s);
+    if (st == SGNN_OK) st = scratch_alloc(reinterpret_cast<void**>(&c_ref), sizeof(float) * (cn + 1), s);
+    if (st == SGNN_OK) st = scratch_alloc(reinterpret_cast<void**>(&c), sizeof(float) * (cn + 1), s);
+    if (st == SGNN_OK) st = scratch_alloc(reinterpret_cast<void**>(&diff), sizeof(int), s);
+    cudaEvent_t e0 = nullptr, e1 = nullptr;
+    sgnn_plan_s* best = nullptr;
+    float best_ms = 0;
+    int n = 0;
+    if (st == SGNN_OK && (cudaEventCreate(&e0) != cudaSuccess || cudaEventCreate(&e1) != cudaSuccess))
+        st = fail(SGNN_ERR_CUDA, "tune: event create failed");
+    if (st == SGNN_OK && !x_in && xn) {
+        // seeded operand, as run_tuning's Rng(seed ^ golden*K) (autotune.hpp:119-121)
+        fill_uniform_kernel<<<unsigned(std::min<uint64_t>(ceil_div_u64(xn, 256), 4096)), 256, 0, s>>>(
+            x, xn, 42ull ^ (0x9e3779b97f4a7c15ull * k));
+    }
+    // reference output from the default ("trusted") plan
+    sgnn_plan_s* def = nullptr;
+    if (st == SGNN_OK) st = build_plan(a, k, nullptr, k % 4 == 0, &def, s);
+    if (st == SGNN_OK) st = run_spmm(a, x, k, c_ref, reduce, def, s);
+    if (def) destroy_plan(def);
+    if (st == SGNN_OK) {
+        for (const sgnn_plan_params& p : candidates(a, k, dp)) {
+            sgnn_plan_s* plan = nullptr;
+            if (build_plan(a, k, &p, k % 4 == 0, &plan, s) != SGNN_OK) continue;
+            if (!find_spmm_launcher(plan->vec, int(plan->p.lanes), int(plan->p.vec),
+                                    int(plan->p.unroll), reduce, int(plan->p.occupancy))) {
+                destroy_plan(plan);
+                continue;
+            }
+            // warm-up doubles as the bitwise correctness assertion
+            st = run_spmm(a, x, k, c, reduce, plan, s);
+            int d = 0;
+            if (st == SGNN_OK && cn) {
+                cudaMemsetAsync(diff, 0, sizeof(int), s);
+                compare_kernel<<<unsigned(std::min<uint64_t>(ceil_div_u64(cn, 256), 4096)), 256, 0, s>>>(
+                    reinterpret_cast<const uint32_t*>(c_ref), reinterpret_cast<const uint32_t*>(c), cn, diff);
+                cudaMemcpyAsync(&d, diff, sizeof(int), cudaMemcpyDeviceToHost, s);
+                cudaStreamSynchronize(s);
+            }
+            if (st != SGNN_OK || d) {
+                destroy_plan(plan);
+                if (st == SGNN_OK)
+                    st = fail(SGNN_ERR_INTERNAL, "run_tuning: plan lanes=" + std::to_string(p.lanes) +
+                                                     " vec=" + std::to_string(p.vec) +
+                                                     " disagrees with the default plan");
+                break;
+            }
+            std::vector<float> ts;
+            for (int r = 0; r < reps && st == SGNN_OK; ++r) {
+                cudaEventRecord(e0, s);
+                st = run_spmm(a, x, k, c, reduce, plan, s);
+                cudaEventRecord(e1, s);
+                cudaEventSynchronize(e1);
+                float ms = 0;
+                cudaEventElapsedTime(&ms, e0, e1);
+                ts.push_back(ms);
+            }
+            if (st != SGNN_OK) {
+                destroy_plan(plan);
+                break;
+            }
+            std::sort(ts.begin(), ts.end());
+            const float med = ts[ts.size() / 2];  // median (autotune.hpp:148-151)
+            if (entries && n < max_entries) {
+                entries[n].params = plan->p;
+                entries[n].ms = med;
+            }
+            ++n;
+            if (!best || med < best_ms) {
+                if (best) destroy_plan(best);
+                best = plan;
+                best_ms = med;
+            } else {
+                destroy_plan(plan);
+            }
+        }
+    }
+    if (e0) cudaEventDestroy(e0);
+    if (e1) cudaEventDestroy(e1);
+    if (!x_in) scratch_free(x, s);
+    scratch_free(c_ref, s);
+    scratch_free(c, s);
+    scratch_free(diff, s);
+    cudaStreamSynchronize(s);
+    if (n_entries) *n_entries = n;
+    if (st != SGNN_OK) {
+        if (best) destroy_plan(best);
+        return st;
+    }
+    if (!best) return fail(SGNN_ERR_CONFIG, "run_tuning: no candidate plan could be built");
+    *best_out = best;
+    return SGNN_OK;
+}
+
+}  // namespace sgnn

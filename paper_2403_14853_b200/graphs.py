@@ -118,6 +118,38 @@ def cfg3_graph(seed: int = 1):
     return rmat(scale, (1 << scale) * 25, seed=seed, symmetrize=True)
 
 
+def gcn_normalize_ones(rp_a, ci_a, rp_t, ci_t):
+    """A_hat = D^-1/2 (A + I) D^-1/2 for a 0/1 matrix A (structure rp_a/ci_a),
+    given the structure of A+I (rp_t/ci_t, duplicates removed).  Follows
+    normalize_adjacency (sparse.hpp:116-174): a diagonal already present in A
+    gets value 1+1, degrees are value sums in double, entries are
+    v * (s_i * s_j) in double, then rounded to fp32."""
+    n = len(rp_t) - 1
+    rows_a = np.repeat(np.arange(n, dtype=np.int64), np.diff(rp_a.astype(np.int64)))
+    has_diag = np.zeros(n, np.float64)
+    has_diag[rows_a[ci_a.astype(np.int64) == rows_a]] = 1.0
+    rows = np.repeat(np.arange(n, dtype=np.int64), np.diff(rp_t.astype(np.int64)))
+    ci64 = ci_t.astype(np.int64)
+    val = np.ones(len(ci_t), np.float64)
+    diag = ci64 == rows
+    val[diag] += has_diag[rows[diag]]
+    d = np.bincount(rows, weights=val, minlength=n)
+    inv = np.where(d > 0, 1.0 / np.sqrt(np.maximum(d, 1e-300)), 0.0)
+    return (val * (inv[rows] * inv[ci64])).astype(np.float32)
+
+
+def cfg3(seed: int = 1) -> Workload:
+    """GCN layer operand: A_hat = D^-1/2 (A+I) D^-1/2 of the symmetrised
+    R-MAT 2^20 (N*25 samples) graph; K=256 (H W is 2^20 x 256)."""
+    scale = 20
+    rp_a, ci_a = cfg3_graph(seed)
+    rp, ci = rmat(scale, (1 << scale) * 25, seed=seed, symmetrize=True, self_loops=True)
+    v = gcn_normalize_ones(rp_a, ci_a, rp, ci)
+    return Workload("cfg3_gcn_rmat20_sym_k256", rp, ci, v, 1 << scale, 256, seed,
+                    {"graph": "R-MAT scale 20, N*25 samples, symmetrised, A_hat = D^-1/2(A+I)D^-1/2",
+                     "H": "N(0,1)"})
+
+
 def cfg5(seed: int = 1) -> Workload:
     """GraphSAGE-mean: R-MAT 2^22, N*25 samples, symmetrised + self loops, dedup, values 1, K=128."""
     scale = 22

@@ -185,6 +185,102 @@ def spmm_plan(a: CsrMatrix, b: torch.Tensor, reduce="sum", plan: Plan | None = N
     return out
 
 
+class _TunedPlan(Plan):
+    def __init__(self, a, k, handle):  # noqa: D401 - wraps a plan made by the tuner
+        self.a, self.k, self.handle = a, int(k), handle
+
+
+def tune_spmm(a: CsrMatrix, k: int, reduce="sum", reps: int = 5, x: torch.Tensor | None = None,
+              max_entries: int = 256):
+    """On-device autotuner (sgnn_tune_spmm): returns (best Plan, [{params, ms}])."""
+    if x is not None:
+        _dense(x, "tune X")
+    ents = (_lib.TuneEntry * max_entries)()
+    n = C.c_int()
+    h = C.c_void_p()
+    check(lib().sgnn_tune_spmm(C.byref(a.c()), x.data_ptr() if x is not None else None, int(k),
+                               _reduce(reduce), int(reps), C.byref(h), ents, max_entries, C.byref(n),
+                               _stream()), "run_tuning")
+    table = [{"params": ents[i].params.as_dict(), "ms": float(ents[i].ms)} for i in range(min(n.value, max_entries))]
+    return _TunedPlan(a, k, h), table
+
+
+@dataclass
+class TuningEntry:
+    """TuningEntry (autotune.hpp:54-59): default-plan vs tuned-plan time."""
+    k: int
+    t_trusted_ms: float
+    t_specialized_ms: float
+    speedup: float
+
+
+@dataclass
+class TuningReport:
+    """TuningReport (autotune.hpp:63-70); profile = the device query."""
+    entries: list
+    best_k: int
+    profile: dict
+    graph_id: str
+    skipped: list
+    plans: dict
+
+
+def run_tuning(a: CsrMatrix, ks, reps: int = 5, seed: int = 42, graph_id: str = "") -> TuningReport:
+    """run_tuning (autotune.hpp:99-164) on the B200: for each K in the sweep,
+    time the default ("trusted") plan against the on-device-tuned
+    ("specialized") plan, both on a seeded uniform operand; the tuner asserts
+    bitwise equality of the two outputs (InternalError otherwise).  best_k =
+    argmax speedup, ties to the smaller K."""
+    ks = list(ks)
+    if not ks:
+        raise ConfigError("run_tuning: candidate list is empty")
+    if reps < 3:
+        raise ConfigError("run_tuning: reps must be >= 3")
+    sm, l2, ma, mi = C.c_int(), C.c_int(), C.c_int(), C.c_int()
+    check(lib().sgnn_device_info(C.byref(sm), C.byref(l2), C.byref(ma), C.byref(mi)))
+    profile = {"sm_count": sm.value, "l2_bytes": l2.value, "cc": f"{ma.value}.{mi.value}",
+               "description": torch.cuda.get_device_name()}
+    entries, skipped, plans, seen = [], [], {}, []
+    dev = a.row_ptr.device
+    for k in ks:
+        if k in seen:
+            continue
+        seen.append(k)
+        if k not in specialization_sweep:
+            skipped.append(k)
+            continue
+        g = torch.Generator(device=dev).manual_seed(seed ^ ((0x9E3779B97F4A7C15 * k) & 0x7FFFFFFFFFFFFFFF))
+        b = torch.rand((a.n_cols, k), generator=g, device=dev, dtype=torch.float32)
+        best, _ = tune_spmm(a, k, "sum", reps, x=b)
+        default = Plan(a, k)
+        out = torch.empty((a.n_rows, k), device=dev)
+
+        def med(plan):
+            ts = []
+            for _ in range(reps):
+                s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                s.record()
+                spmm_plan(a, b, "sum", plan, out)
+                e.record()
+                torch.cuda.synchronize()
+                ts.append(s.elapsed_time(e))
+            ts.sort()
+            n = len(ts)
+            return ts[n // 2] if n % 2 else 0.5 * (ts[n // 2 - 1] + ts[n // 2])
+
+        spmm_plan(a, b, "sum", default, out)
+        t_t, t_s = med(default), med(best)
+        entries.append(TuningEntry(k, t_t, t_s, t_t / t_s))
+        plans[k] = best
+    if not entries:
+        raise ConfigError("run_tuning: no requested K has a specialized kernel")
+    top = entries[0]
+    for e in entries:
+        if e.speedup > top.speedup or (e.speedup == top.speedup and e.k < top.k):
+            top = e
+    return TuningReport(entries, top.k, profile, graph_id, skipped, plans)
+
+
 def resolve_kernel(k: int, reduce) -> KernelKind:
     """resolve_kernel (kernels.hpp:38, dispatch.cpp:21-28)."""
     sk = C.c_uint32()

@@ -41,7 +41,7 @@ def test_host_library_exports_every_declared_symbol():
 def test_struct_layout_matches_header():
     from paper_2403_14853_b200 import _lib
     assert C.sizeof(_lib.Csr) == 40
-    assert C.sizeof(_lib.PlanParams) == 32
+    assert C.sizeof(_lib.PlanParams) == 36
 
 
 def test_dispatch_state_is_host_only():
