@@ -1,0 +1,386 @@
+// sparsegnn_b200.hpp -- C++ drop-in over the C ABI (sgnn_b200.h) with the
+// operator API of the iSpLib re-creation (proj/include/sparsegnn/):
+//
+//   spmm / spmm_with / detail::spmm_into   kernels.hpp:141-182
+//   sddmm / fusedmm                        kernels.hpp:187-270
+//   transpose / row_degrees / is_symmetric sparse.hpp:72-109,179-192
+//   resolve_kernel, set_dispatch, get_dispatch, DispatchGuard
+//                                          kernels.hpp:38, autotune.hpp:36-51
+//   TrainingCache / build_cache            gnn.hpp:113-196
+//
+// Every function is a template over the matrix types, so the caller's own
+// sparsegnn::CsrMatrix<float> / DenseMatrix<float> (or the look-alikes below)
+// pass straight in: same names, same argument meaning, same result
+// semantics, same exception classes by name.  Host operands are uploaded per
+// call; for training loops keep the graph resident with DeviceCsr /
+// TrainingCache (what the reference's TrainingCache does on the CPU).
+// `threads` is accepted and ignored (the GPU decides its own parallelism).
+//
+// Errors: sgnn_status codes become exceptions.  By default the classes below
+// are thrown; define SGNN_B200_ERROR_NS to a namespace that has the
+// reference's classes (e.g. `sparsegnn`, after including its error.hpp) to
+// throw those instead.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cmath>
+#include <cstdint>
+#include <cstring>
+#include <functional>
+#include <stdexcept>
+#include <string>
+#include <utility>
+#include <vector>
+
+#include "sgnn_b200.h"
+
+namespace sparsegnn_b200 {
+
+// ------------------------------------------------------------- errors
+#ifndef SGNN_B200_ERROR_NS
+class Error : public std::runtime_error {
+public:
+    using std::runtime_error::runtime_error;
+};
+class ShapeError : public Error { public: using Error::Error; };
+class DispatchError : public Error { public: using Error::Error; };
+class ConfigError : public Error { public: using Error::Error; };
+class TapeError : public Error { public: using Error::Error; };
+class InternalError : public Error { public: using Error::Error; };
+#define SGNN_B200_ERR(cls) ::sparsegnn_b200::cls
+#else
+#define SGNN_B200_ERR(cls) ::SGNN_B200_ERROR_NS::cls
+#endif
+/// CUDA runtime / device failure (no reference analogue).
+class CudaError : public std::runtime_error {
+public:
+    using std::runtime_error::runtime_error;
+};
+
+inline void check(sgnn_status st) {
+    if (st == SGNN_OK) return;
+    const std::string msg = sgnn_last_error();
+    switch (st) {
+        case SGNN_ERR_SHAPE: throw SGNN_B200_ERR(ShapeError)(msg);
+        case SGNN_ERR_DISPATCH: throw SGNN_B200_ERR(DispatchError)(msg);
+        case SGNN_ERR_CONFIG: throw SGNN_B200_ERR(ConfigError)(msg);
+        case SGNN_ERR_TAPE: throw SGNN_B200_ERR(TapeError)(msg);
+        case SGNN_ERR_INTERNAL: throw SGNN_B200_ERR(InternalError)(msg);
+        default: throw CudaError(msg);
+    }
+}
+
+inline void cuda_check(cudaError_t e, const char* what) {
+    if (e != cudaSuccess) throw CudaError(std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+// ------------------------------------------------- host types (look-alikes)
+using index_t = std::uint32_t;   // types.hpp:15
+using offset_t = std::uint64_t;  // types.hpp:18
+enum class ReduceOp { Sum, Min, Max, Mean };  // types.hpp:116 (same order)
+
+template <class T>
+struct CsrMatrix {
+    index_t n_rows = 0, n_cols = 0;
+    std::vector<offset_t> row_ptr{0};
+    std::vector<index_t> col_idx;
+    std::vector<T> values;
+    CsrMatrix() = default;
+    CsrMatrix(index_t r, index_t c) : n_rows(r), n_cols(c), row_ptr(std::size_t(r) + 1, 0) {}
+    offset_t nnz() const { return row_ptr.empty() ? 0 : row_ptr.back(); }
+};
+
+template <class T>
+struct DenseMatrix {
+    index_t n_rows = 0, n_cols = 0;
+    std::vector<T> data;
+    DenseMatrix() = default;
+    DenseMatrix(index_t r, index_t c) : n_rows(r), n_cols(c), data(std::size_t(r) * c, T(0)) {}
+    T& operator()(index_t i, index_t j) { return data[std::size_t(i) * n_cols + j]; }
+    T operator()(index_t i, index_t j) const { return data[std::size_t(i) * n_cols + j]; }
+};
+
+/// KernelKind (kernels.hpp:14-25).
+struct KernelKind {
+    enum class Tag : std::uint8_t { Trusted, Specialized };
+    Tag tag = Tag::Trusted;
+    index_t k = 0;
+    static constexpr KernelKind trusted() { return {Tag::Trusted, 0}; }
+    static constexpr KernelKind specialized(index_t k) { return {Tag::Specialized, k}; }
+    bool is_specialized() const { return tag == Tag::Specialized; }
+};
+
+/// Semiring (types.hpp:139-145) with the GPU edge-op tag.  `combine` keeps
+/// the CPU meaning; the GPU runs `edge_op`.  A semiring with a combine but no
+/// tag cannot run on the GPU and raises DispatchError (no CPU fallback).
+template <class T>
+struct Semiring {
+    std::function<T(T, T)> combine;
+    ReduceOp reduce = ReduceOp::Sum;
+    int edge_op = -1;  // -1: derive (empty combine -> MUL)
+    static Semiring plus_times() { return {nullptr, ReduceOp::Sum, SGNN_EDGE_MUL}; }
+};
+
+/// combine(p, d) = p * sigmoid(d)  (BASELINE cfg4 edge op), CPU + GPU forms.
+template <class T>
+Semiring<T> sigmoid_times(ReduceOp reduce = ReduceOp::Sum) {
+    return {[](T p, T d) { return p * (T(1) / (T(1) + std::exp(-d))); }, reduce, SGNN_EDGE_SIGMOID_MUL};
+}
+
+// ------------------------------------------------------- device buffers
+template <class T>
+class DeviceBuffer {
+public:
+    DeviceBuffer() = default;
+    explicit DeviceBuffer(std::size_t n) : n_(n) {
+        if (n) cuda_check(cudaMalloc(&p_, n * sizeof(T)), "cudaMalloc");
+    }
+    DeviceBuffer(const T* host, std::size_t n) : DeviceBuffer(n) { upload(host, n); }
+    DeviceBuffer(DeviceBuffer&& o) noexcept : p_(o.p_), n_(o.n_) { o.p_ = nullptr; o.n_ = 0; }
+    DeviceBuffer& operator=(DeviceBuffer&& o) noexcept {
+        std::swap(p_, o.p_);
+        std::swap(n_, o.n_);
+        return *this;
+    }
+    DeviceBuffer(const DeviceBuffer&) = delete;
+    DeviceBuffer& operator=(const DeviceBuffer&) = delete;
+    ~DeviceBuffer() { if (p_) cudaFree(p_); }
+    void upload(const T* host, std::size_t n) {
+        if (n) cuda_check(cudaMemcpy(p_, host, n * sizeof(T), cudaMemcpyHostToDevice), "upload");
+    }
+    void download(T* host, std::size_t n) const {
+        if (n) cuda_check(cudaMemcpy(host, p_, n * sizeof(T), cudaMemcpyDeviceToHost), "download");
+    }
+    T* get() const { return p_; }
+    std::size_t size() const { return n_; }
+
+private:
+    T* p_ = nullptr;
+    std::size_t n_ = 0;
+};
+
+/// A CSR matrix resident on the device (uploaded once).
+class DeviceCsr {
+public:
+    DeviceCsr() = default;
+    template <class Csr>
+    explicit DeviceCsr(const Csr& a)
+        : n_rows_(a.n_rows), n_cols_(a.n_cols), nnz_(a.row_ptr.empty() ? 0 : a.row_ptr.back()),
+          rp_(a.row_ptr.data(), a.row_ptr.size()), ci_(a.col_idx.data(), a.col_idx.size()),
+          v_(nullptr, 0) {
+        std::vector<float> vf(a.values.begin(), a.values.end());
+        v_ = DeviceBuffer<float>(vf.data(), vf.size());
+    }
+    sgnn_csr view() const {
+        return sgnn_csr{n_rows_, n_cols_, nnz_, rp_.get(), ci_.get(), v_.get()};
+    }
+    index_t n_rows() const { return n_rows_; }
+    index_t n_cols() const { return n_cols_; }
+    offset_t nnz() const { return nnz_; }
+
+private:
+    index_t n_rows_ = 0, n_cols_ = 0;
+    offset_t nnz_ = 0;
+    DeviceBuffer<offset_t> rp_;
+    DeviceBuffer<index_t> ci_;
+    DeviceBuffer<float> v_;
+};
+
+/// Copies a device CSR view back into a host CsrMatrix-like object.
+template <class Csr>
+void download_csr(const sgnn_csr& v, Csr& out) {
+    out.n_rows = v.n_rows;
+    out.n_cols = v.n_cols;
+    out.row_ptr.resize(std::size_t(v.n_rows) + 1);
+    out.col_idx.resize(v.nnz);
+    std::vector<float> vals(v.nnz);
+    cuda_check(cudaMemcpy(out.row_ptr.data(), v.row_ptr, sizeof(offset_t) * out.row_ptr.size(),
+                          cudaMemcpyDeviceToHost), "download");
+    if (v.nnz) {
+        cuda_check(cudaMemcpy(out.col_idx.data(), v.col_idx, sizeof(index_t) * v.nnz, cudaMemcpyDeviceToHost), "download");
+        cuda_check(cudaMemcpy(vals.data(), v.values, sizeof(float) * v.nnz, cudaMemcpyDeviceToHost), "download");
+    }
+    out.values.assign(vals.begin(), vals.end());
+}
+
+namespace internal {
+template <class Dense>
+DeviceBuffer<float> upload_dense(const Dense& b) {
+    std::vector<float> f(b.data.begin(), b.data.end());
+    return DeviceBuffer<float>(f.data(), f.size());
+}
+template <class Dense>
+void download_dense(const DeviceBuffer<float>& d, Dense& c) {
+    std::vector<float> f(c.data.size());
+    d.download(f.data(), f.size());
+    c.data.assign(f.begin(), f.end());
+}
+template <class R>
+int reduce_code(R r) { return static_cast<int>(r); }  // same order as types.hpp:116
+}  // namespace internal
+
+// --------------------------------------------------------- dispatch toggle
+inline void set_dispatch(bool enabled) { sgnn_set_dispatch(enabled ? 1 : 0); }
+inline bool get_dispatch() { return sgnn_get_dispatch() != 0; }
+class DispatchGuard {  // autotune.hpp:40-51
+public:
+    explicit DispatchGuard(bool enabled) : prev_(get_dispatch()) { set_dispatch(enabled); }
+    ~DispatchGuard() { set_dispatch(prev_); }
+    DispatchGuard(const DispatchGuard&) = delete;
+    DispatchGuard& operator=(const DispatchGuard&) = delete;
+
+private:
+    bool prev_;
+};
+template <class R = ReduceOp>
+KernelKind resolve_kernel(index_t k, R reduce) {
+    std::uint32_t sk = 0;
+    const int tag = sgnn_resolve_kernel(k, internal::reduce_code(reduce), &sk);
+    return tag == SGNN_KERNEL_SPECIALIZED ? KernelKind::specialized(sk) : KernelKind::trusted();
+}
+
+// -------------------------------------------------------------- operators
+namespace detail {
+/// detail::spmm_into (kernels.hpp:141-149): caller-owned output.
+template <class Csr, class Dense, class R, class Kind>
+void spmm_into(const Csr& a, const Dense& b, R reduce, Kind kind, int /*threads*/, Dense& c) {
+    DeviceCsr da(a);
+    auto db = internal::upload_dense(b);
+    DeviceBuffer<float> dc(std::size_t(a.n_rows) * b.n_cols);
+    const sgnn_csr v = da.view();
+    check(sgnn_spmm_with_f32(&v, db.get(), b.n_rows, b.n_cols, dc.get(), internal::reduce_code(reduce),
+                             kind.is_specialized() ? SGNN_KERNEL_SPECIALIZED : SGNN_KERNEL_TRUSTED,
+                             kind.k, nullptr, nullptr));
+    cuda_check(cudaDeviceSynchronize(), "spmm");
+    internal::download_dense(dc, c);
+}
+}  // namespace detail
+
+/// spmm_with (kernels.hpp:157-173).
+template <class Csr, class Dense, class R, class Kind>
+Dense spmm_with(const Csr& a, const Dense& b, R reduce, Kind kind, int threads = 0) {
+    Dense c(a.n_rows, b.n_cols);
+    detail::spmm_into(a, b, reduce, kind, threads, c);
+    return c;
+}
+
+/// spmm (kernels.hpp:179-182): kernel picked by the dispatch state.
+template <class Csr, class Dense, class R = ReduceOp>
+Dense spmm(const Csr& a, const Dense& b, R reduce = R::Sum, int threads = 0) {
+    return spmm_with(a, b, reduce, resolve_kernel(b.n_cols, reduce), threads);
+}
+
+/// transpose (sparse.hpp:72-89), bit-exact, computed on the device.
+template <class Csr>
+Csr transpose(const Csr& a) {
+    DeviceCsr da(a);
+    const sgnn_csr v = da.view();
+    DeviceBuffer<offset_t> trp(std::size_t(a.n_cols) + 1);
+    DeviceBuffer<index_t> tci(v.nnz);
+    DeviceBuffer<float> tv(v.nnz);
+    check(sgnn_csr_transpose(&v, trp.get(), tci.get(), tv.get(), nullptr, 0, nullptr));
+    cuda_check(cudaDeviceSynchronize(), "transpose");
+    Csr t;
+    download_csr(sgnn_csr{a.n_cols, a.n_rows, v.nnz, trp.get(), tci.get(), tv.get()}, t);
+    return t;
+}
+
+/// is_symmetric (sparse.hpp:179-192).
+template <class Csr>
+bool is_symmetric(const Csr& a) {
+    DeviceCsr da(a);
+    const sgnn_csr v = da.view();
+    int out = 0;
+    check(sgnn_is_symmetric(&v, &out, nullptr));
+    return out != 0;
+}
+
+/// sddmm (kernels.hpp:187-210): P's pattern, values p_e * <X_i, Y_j>.
+template <class Csr, class Dense>
+Csr sddmm(const Csr& p, const Dense& x, const Dense& y, int /*threads*/ = 0) {
+    DeviceCsr dp(p);
+    auto dx = internal::upload_dense(x);
+    auto dy = internal::upload_dense(y);
+    DeviceBuffer<float> out(dp.nnz());
+    const sgnn_csr v = dp.view();
+    check(sgnn_sddmm_f32(&v, dx.get(), x.n_rows, dy.get(), y.n_rows, x.n_cols, out.get(), nullptr));
+    cuda_check(cudaDeviceSynchronize(), "sddmm");
+    Csr r = p;  // the reference returns a copy of P with new values (kernels.hpp:196)
+    std::vector<float> f(dp.nnz());
+    out.download(f.data(), f.size());
+    r.values.assign(f.begin(), f.end());
+    return r;
+}
+
+/// fusedmm (kernels.hpp:216-270).  Accepts the reference's Semiring (empty
+/// combine = plus_times) or this header's (tagged edge op).
+template <class Csr, class Dense, class SR>
+Dense fusedmm(const Csr& p, const Dense& x, const Dense& y, const SR& sr, int /*threads*/ = 0) {
+    int edge = SGNN_EDGE_MUL;
+    if constexpr (requires { sr.edge_op; }) {
+        if (sr.edge_op >= 0) edge = sr.edge_op;
+        else if (sr.combine) throw SGNN_B200_ERR(DispatchError)("fusedmm: untagged combine cannot run on the GPU");
+    } else {
+        if (sr.combine) throw SGNN_B200_ERR(DispatchError)("fusedmm: untagged combine cannot run on the GPU");
+    }
+    DeviceCsr dp(p);
+    auto dx = internal::upload_dense(x);
+    auto dy = internal::upload_dense(y);
+    DeviceBuffer<float> out(std::size_t(p.n_rows) * y.n_cols);
+    const sgnn_csr v = dp.view();
+    check(sgnn_fusedmm_f32(&v, dx.get(), x.n_rows, dy.get(), y.n_rows, x.n_cols, edge,
+                           internal::reduce_code(sr.reduce), out.get(), nullptr));
+    cuda_check(cudaDeviceSynchronize(), "fusedmm");
+    Dense c(p.n_rows, y.n_cols);
+    internal::download_dense(out, c);
+    return c;
+}
+template <class Csr, class Dense>
+Dense fusedmm(const Csr& p, const Dense& x, const Dense& y) {
+    return fusedmm(p, x, y, Semiring<float>::plus_times());
+}
+
+// --------------------------------------------------- backward cache (gnn.hpp)
+/// TrainingCache + build_cache (gnn.hpp:113-196) with a device-resident a_hat.
+/// sum_operand()/mean_operand() return device views; spmm_backward() runs
+/// dX = spmm(operand, dC, Sum) on the device.
+class TrainingCache {
+public:
+    template <class Csr>
+    explicit TrainingCache(const Csr& a_hat, bool use_cache = true) : a_(a_hat) {
+        const sgnn_csr v = a_.view();
+        check(sgnn_cache_create(&v, use_cache ? 1 : 0, &h_, nullptr));
+    }
+    ~TrainingCache() { if (h_) sgnn_cache_destroy(h_); }
+    TrainingCache(const TrainingCache&) = delete;
+    TrainingCache& operator=(const TrainingCache&) = delete;
+
+    sgnn_csr sum_operand() { sgnn_csr o; check(sgnn_cache_sum_operand(h_, &o, nullptr)); return o; }
+    sgnn_csr mean_operand() { sgnn_csr o; check(sgnn_cache_mean_operand(h_, &o, nullptr)); return o; }
+
+    std::uint64_t transpose_builds() const { return counter(0); }
+    std::uint64_t normalize_builds() const { return counter(1); }
+    std::uint64_t cache_hits() const { return counter(2); }
+    bool symmetric() const { std::uint64_t a, b, c; int s; sgnn_cache_counters(h_, &a, &b, &c, &s); return s != 0; }
+
+    /// dX = op^T-style backward SpMM for a device dC (rows = a_hat.n_rows).
+    void spmm_backward(const float* dc_dev, index_t k, float* dx_dev, ReduceOp reduce = ReduceOp::Sum,
+                       cudaStream_t stream = nullptr) {
+        check(sgnn_spmm_backward_f32(h_, dc_dev, a_.n_rows(), k, dx_dev, static_cast<int>(reduce),
+                                     reinterpret_cast<sgnn_stream>(stream)));
+    }
+    const DeviceCsr& a_hat() const { return a_; }
+
+private:
+    std::uint64_t counter(int i) const {
+        std::uint64_t v[3];
+        int s;
+        check(sgnn_cache_counters(h_, &v[0], &v[1], &v[2], &s));
+        return v[i];
+    }
+    DeviceCsr a_;
+    sgnn_cache h_ = nullptr;
+};
+
+}  // namespace sparsegnn_b200

@@ -119,6 +119,7 @@ void default_params(const sgnn_csr* a, uint32_t k, bool vec_ok, const DeviceProp
         else if (k <= 256) { d.lanes = 32; d.vec = 2; }
         else { d.lanes = 32; d.vec = 4; }
         d.unroll = d.vec >= 4 ? 4 : (d.vec == 2 ? 4 : 8);
+        if (d.lanes == 32 && d.vec == 2) d.occupancy = 4;  // K=256: cfg3 probe
     } else {
         d.lanes = 32;
         d.vec = k <= 32 ? 1 : k <= 64 ? 2 : k <= 128 ? 4 : 8;
@@ -131,7 +132,7 @@ void default_params(const sgnn_csr* a, uint32_t k, bool vec_ok, const DeviceProp
                             uint64_t(dp.max_threads_per_sm > 0 ? dp.max_threads_per_sm : 2048) /
                             d.lanes;
     uint64_t want = total / (4 * groups);
-    d.path_items = std::max<uint32_t>(16, std::min<uint32_t>(4096, pow2_floor(std::max<uint64_t>(want, 1))));
+    d.path_items = std::max<uint32_t>(32, std::min<uint32_t>(4096, pow2_floor(std::max<uint64_t>(want, 1))));
     d.split_rows_over = std::max<uint32_t>(d.path_items, SGNN_SEGMENT);
     d.k_tile = 0;
     d.scalar = p->scalar;
@@ -141,6 +142,9 @@ void default_params(const sgnn_csr* a, uint32_t k, bool vec_ok, const DeviceProp
     if (!p->path_items) p->path_items = d.path_items;
     if (!p->split_rows_over) p->split_rows_over = std::max<uint32_t>(p->path_items, SGNN_SEGMENT);
     if (!p->block) p->block = d.block;
+    // the occupancy default belongs to the default layout only
+    if (!p->occupancy && p->lanes == d.lanes && p->vec == d.vec && p->unroll == d.unroll)
+        p->occupancy = d.occupancy;
 }
 
 sgnn_status resolve_params(const sgnn_csr* a, uint32_t k, bool vec_ok, const DeviceProps& dp,
@@ -157,8 +161,8 @@ sgnn_status resolve_params(const sgnn_csr* a, uint32_t k, bool vec_ok, const Dev
         return fail(SGNN_ERR_CONFIG, "plan: unroll must be 2, 4, 8 or 16");
     if (p.block != 64 && p.block != 128)
         return fail(SGNN_ERR_CONFIG, "plan: block must be 64 or 128");
-    if (p.occupancy != 0 && p.occupancy != 1 && p.occupancy != 4 && p.occupancy != 6 && p.occupancy != 8)
-        return fail(SGNN_ERR_CONFIG, "plan: occupancy must be 0, 1, 4, 6 or 8");
+    if (p.occupancy > 8 || p.occupancy == 2 || p.occupancy == 3 || p.occupancy == 7)
+        return fail(SGNN_ERR_CONFIG, "plan: occupancy must be 0, 1, 4, 5, 6 or 8");
     if (p.path_items == 0) return fail(SGNN_ERR_CONFIG, "plan: path_items must be >= 1");
     const uint32_t width = (scalar ? 1u : 4u) * p.lanes * p.vec;  // floats one pass covers
     uint32_t kt = p.k_tile ? p.k_tile : k;

@@ -82,7 +82,14 @@ sgnn_status launch_spmm_worker(const SpmmArgs& a, uint32_t block, uint32_t max_b
     X(32, 1, 4, RED, true, OP, 6)         \
     X(32, 1, 4, RED, true, OP, 8)         \
     X(32, 1, 8, RED, true, OP, 4)         \
+    X(32, 1, 8, RED, true, OP, 5)         \
     X(32, 1, 8, RED, true, OP, 6)         \
+    X(16, 1, 8, RED, true, OP, 5)         \
+    X(16, 1, 8, RED, true, OP, 6)         \
+    X(16, 1, 4, RED, true, OP, 6)         \
+    X(8, 1, 8, RED, true, OP, 5)          \
+    X(8, 1, 8, RED, true, OP, 6)          \
+    X(32, 2, 4, RED, true, OP, 5)         \
     X(32, 2, 4, RED, true, OP, 4)         \
     X(32, 2, 4, RED, true, OP, 6)         \
     X(16, 4, 2, RED, true, OP, 6)         \

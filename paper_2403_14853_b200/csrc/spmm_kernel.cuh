@@ -118,6 +118,21 @@ struct Frag {
     // needed where all lanes' values are summed, i.e. the FusedMM dot).
     template <bool ZERO>
     __device__ __forceinline__ void gather(const float* __restrict__ lrow, int nq) {
+        if constexpr (!ZERO) {
+            // Unpredicated: blocks beyond the width re-read block 0 (the lane
+            // base is clamped inside the row), their values are never stored.
+#pragma unroll
+            for (int q = 0; q < V; ++q) {
+                const int qe = (q < nq) ? q : 0;
+                if constexpr (VEC) {
+                    const float4 t = __ldg(reinterpret_cast<const float4*>(lrow + 4 * G * qe));
+                    v[4 * q + 0] = t.x; v[4 * q + 1] = t.y; v[4 * q + 2] = t.z; v[4 * q + 3] = t.w;
+                } else {
+                    v[q] = __ldg(lrow + G * qe);
+                }
+            }
+            return;
+        }
 #pragma unroll
         for (int q = 0; q < V; ++q) {
             if (q < nq) {
@@ -228,7 +243,9 @@ __global__ void __launch_bounds__(128, MINB) spmm_worker_kernel(const SpmmArgs a
     const unsigned gmask = (G == 32) ? 0xffffffffu : (((1u << G) - 1u) << (lane & ~(G - 1)));
     const uint32_t n_groups = (gridDim.x * blockDim.x) / G;
     // this lane's slice of any gathered row: byte offset col*ldxb from xlane
-    const char* xlane = reinterpret_cast<const char*>(a.x + F::W * gl);
+    // lanes past the width alias the row's last valid block (always in bounds)
+    const int gl_eff = min(gl, int(a.width / F::W) - 1);
+    const char* xlane = reinterpret_cast<const char*>(a.x + F::W * gl_eff);
     const uint32_t ldxb = uint32_t(a.ldx) * 4u;
     const int nq = F::blocks_in(gl, a.width);
 
@@ -371,9 +388,24 @@ __global__ void __launch_bounds__(128, MINB) spmm_worker_kernel(const SpmmArgs a
             };
             if (base + uint32_t(n) <= next_l) {
                 // fast path: the whole batch continues the current row segment
+                if constexpr (OP != OP_SPMM) {
+                    // all U dot products first (independent shuffle trees interleave)
+                    float sv[U];
 #pragma unroll
-                for (int u = 0; u < U; ++u)
-                    if (u < n) fold(xf[u], av[u]);
+                    for (int u = 0; u < U; ++u) sv[u] = edge_value<OP>(av[u], group_dot(xrow, xf[u], gmask));
+#pragma unroll
+                    for (int u = 0; u < U; ++u) {
+                        if (u < n) {
+#pragma unroll
+                            for (int i = 0; i < N; ++i) acc.v[i] = R::fold(acc.v[i], sv[u], xf[u].v[i], first);
+                            first = false;
+                        }
+                    }
+                } else {
+#pragma unroll
+                    for (int u = 0; u < U; ++u)
+                        if (u < n) fold(xf[u], av[u]);
+                }
             } else {
                 // slow path: row / segment boundaries inside the batch
 #pragma unroll

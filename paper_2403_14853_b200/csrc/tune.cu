@@ -68,7 +68,7 @@ std::vector<sgnn_plan_params> candidates(const sgnn_csr* a, uint32_t k, const De
     const uint32_t paths[] = {std::max(16u, d0 / 2), d0, std::min(4096u, d0 * 2)};
     for (const LV& l : layouts)
         for (uint32_t pi : paths)
-            for (uint32_t occ : {1u, 4u, 6u, 8u}) {
+            for (uint32_t occ : {1u, 4u, 5u, 6u, 8u}) {
                 if (!vec && occ != 1) continue;
                 sgnn_plan_params p{};
                 p.lanes = l.lanes;

@@ -45,19 +45,17 @@ def main():
         out = torch.empty(w.n_rows, w.k, device="cuda")
         by = alg_bytes(w.n_rows, w.nnz, w.k)
         if w.k == 128:
-            variants = [{}, {"unroll": 16}, {"path_items": 512}, {"path_items": 2048}, {"path_items": 256},
-                        {"lanes": 16, "vec": 2, "unroll": 4, "occupancy": 4}, {"block": 64},
-                        {"unroll": 16, "path_items": 512}]
+            variants = [{}, {"occupancy": 5}, {"occupancy": 6}, {"unroll": 4, "occupancy": 6},
+                        {"unroll": 4, "occupancy": 8}, {"unroll": 16}, {"path_items": 512}]
         elif w.k == 64:
-            variants = [{}, {"unroll": 16}, {"lanes": 8, "vec": 2, "unroll": 8}, {"lanes": 16, "vec": 1, "unroll": 4},
-                        {"lanes": 32, "vec": 1, "unroll": 8}, {"path_items": 256}, {"path_items": 2048}]
+            variants = [{}, {"occupancy": 5}, {"occupancy": 6}, {"unroll": 4, "occupancy": 6},
+                        {"lanes": 32, "vec": 1, "unroll": 8}, {"path_items": 512}]
         elif w.k == 256:
-            variants = [{}, {"lanes": 32, "vec": 2, "unroll": 8}, {"lanes": 32, "vec": 1, "unroll": 8},
-                        {"lanes": 32, "vec": 1, "unroll": 16}, {"lanes": 16, "vec": 4, "unroll": 4},
-                        {"lanes": 32, "vec": 2, "unroll": 4, "occupancy": 4}]
+            variants = [{}, {"lanes": 32, "vec": 2, "unroll": 4, "occupancy": 5},
+                        {"lanes": 32, "vec": 1, "unroll": 8}, {"lanes": 32, "vec": 1, "unroll": 8, "occupancy": 5}]
         else:
-            variants = [{}, {"unroll": 16}, {"lanes": 4, "vec": 2}, {"lanes": 4, "vec": 1},
-                        {"path_items": 32}, {"path_items": 64}, {"lanes": 16, "vec": 1, "unroll": 8}]
+            variants = [{}, {"occupancy": 5}, {"occupancy": 6}, {"unroll": 16}, {"lanes": 4, "vec": 2},
+                        {"path_items": 64}]
         for red in ("sum", "mean"):
             for v in variants:
                 try:

@@ -1,0 +1,179 @@
+// test_compat.cpp -- the C++ drop-in (include/sparsegnn_b200.hpp) used the way
+// the reference's operator API is used, checked against the SPEC known
+// answers and the CPU oracle (oracle/liboracle.so, test infrastructure).
+// Run by tests/test_cpp_compat.py on the GPU box.
+#include <cstdio>
+#include <cstdlib>
+#include <random>
+
+#include "sparsegnn_b200.hpp"
+
+extern "C" {
+void orc_spmm_f64(uint32_t, const uint64_t*, const uint32_t*, const double*, const double*, uint32_t,
+                  int, double*);
+void orc_spmm_f32(uint32_t, const uint64_t*, const uint32_t*, const float*, const float*, uint32_t, int,
+                  float*);
+void orc_spmm_absdenom_f64(uint32_t, const uint64_t*, const uint32_t*, const double*, const double*,
+                           uint32_t, int, double*);
+void orc_transpose_f32(uint32_t, uint32_t, const uint64_t*, const uint32_t*, const float*, uint64_t*,
+                       uint32_t*, float*);
+}
+
+namespace sg = sparsegnn_b200;
+using Csr = sg::CsrMatrix<float>;
+using Dense = sg::DenseMatrix<float>;
+
+static int failures = 0;
+#define EXPECT(cond)                                                         \
+    do {                                                                     \
+        if (!(cond)) {                                                       \
+            std::fprintf(stderr, "FAIL %s:%d: %s\n", __FILE__, __LINE__, #cond); \
+            ++failures;                                                      \
+        }                                                                    \
+    } while (0)
+
+template <class E, class F>
+bool throws(F&& f) {
+    try {
+        f();
+    } catch (const E&) {
+        return true;
+    } catch (...) {
+        return false;
+    }
+    return false;
+}
+
+static Csr make(uint32_t m, uint32_t n, std::vector<uint64_t> rp, std::vector<uint32_t> ci, std::vector<float> v) {
+    Csr a(m, n);
+    a.row_ptr = std::move(rp);
+    a.col_idx = std::move(ci);
+    a.values = std::move(v);
+    return a;
+}
+
+static Csr random_csr(std::mt19937_64& g, uint32_t m, uint32_t n, double dens, bool hub) {
+    Csr a(m, n);
+    std::uniform_real_distribution<float> u(-1.f, 1.f);
+    std::bernoulli_distribution b(dens), bh(0.8);
+    for (uint32_t i = 0; i < m; ++i) {
+        for (uint32_t j = 0; j < n; ++j)
+            if ((hub && i == 1) ? bh(g) : b(g)) {
+                a.col_idx.push_back(j);
+                a.values.push_back(u(g));
+            }
+        a.row_ptr[i + 1] = a.col_idx.size();
+    }
+    return a;
+}
+
+int main() {
+    // ---- SPEC.md:141-143 known answers
+    {
+        Csr a = make(2, 2, {0, 1, 2}, {1, 0}, {2.f, 3.f});
+        Dense b(2, 2);
+        b.data = {1, 1, 2, 2};
+        Dense c = sg::spmm(a, b);
+        EXPECT((c.data == std::vector<float>{4, 4, 3, 3}));
+        Csr r = make(1, 2, {0, 2}, {0, 1}, {1.f, 1.f});
+        Dense bb(2, 2);
+        bb.data = {2, 8, 4, 2};
+        EXPECT((sg::spmm(r, bb, sg::ReduceOp::Min).data == std::vector<float>{2, 2}));
+        EXPECT((sg::spmm(r, bb, sg::ReduceOp::Max).data == std::vector<float>{4, 8}));
+        EXPECT((sg::spmm(r, bb, sg::ReduceOp::Mean).data == std::vector<float>{3, 5}));
+    }
+    // ---- sddmm / fusedmm known answers
+    {
+        Csr ident = make(2, 2, {0, 1, 2}, {0, 1}, {1.f, 1.f});
+        Dense x(2, 2);
+        x.data = {1, 2, 3, 4};
+        Csr s = sg::sddmm(ident, x, x);
+        EXPECT((s.values == std::vector<float>{5, 25}));
+        EXPECT(s.row_ptr == ident.row_ptr && s.col_idx == ident.col_idx);
+        EXPECT((sg::fusedmm(ident, x, x).data == std::vector<float>{5, 10, 75, 100}));
+        auto sr = sg::sigmoid_times<float>();
+        Dense f = sg::fusedmm(ident, x, x, sr);
+        const float e0 = 1.f / (1.f + std::exp(-5.f));
+        EXPECT(std::fabs(f.data[0] - e0 * 1.f) < 1e-6f);
+        sg::Semiring<float> untagged{[](float p, float d) { return p + d; }, sg::ReduceOp::Sum};
+        untagged.edge_op = -1;
+        EXPECT(throws<sg::DispatchError>([&] { sg::fusedmm(ident, x, x, untagged); }));
+    }
+    // ---- errors mirror kernels.hpp:131-169
+    {
+        Csr a = make(1, 2, {0, 1}, {0}, {1.f});
+        Dense bad(3, 32);
+        EXPECT(throws<sg::ShapeError>([&] { sg::spmm(a, bad); }));
+        Dense b48(2, 48);
+        EXPECT(throws<sg::DispatchError>([&] { sg::spmm_with(a, b48, sg::ReduceOp::Sum, sg::KernelKind::specialized(32)); }));
+        Dense b32(2, 32);
+        EXPECT(throws<sg::DispatchError>([&] { sg::spmm_with(a, b32, sg::ReduceOp::Mean, sg::KernelKind::specialized(32)); }));
+        EXPECT(!throws<sg::Error>([&] { sg::spmm_with(a, b32, sg::ReduceOp::Sum, sg::KernelKind::specialized(32)); }));
+    }
+    // ---- dispatch toggle (dispatch.cpp:21-28)
+    {
+        EXPECT(sg::resolve_kernel(32, sg::ReduceOp::Sum).is_specialized());
+        EXPECT(!sg::resolve_kernel(48, sg::ReduceOp::Sum).is_specialized());
+        EXPECT(!sg::resolve_kernel(32, sg::ReduceOp::Mean).is_specialized());
+        {
+            sg::DispatchGuard off(false);
+            EXPECT(!sg::resolve_kernel(32, sg::ReduceOp::Sum).is_specialized());
+        }
+        EXPECT(sg::get_dispatch());
+    }
+    // ---- random parity vs the oracle: tolerance + bitwise on rows <= 256 nnz
+    std::mt19937_64 g(7);
+    for (uint32_t k : {16u, 33u, 128u}) {
+        Csr a = random_csr(g, 200, 900, 0.02, true);
+        Dense x(900, k);
+        std::uniform_real_distribution<float> u(-1.f, 1.f);
+        for (auto& v : x.data) v = u(g);
+        for (int red = 0; red < 4; ++red) {
+            Dense c = sg::spmm(a, x, static_cast<sg::ReduceOp>(red));
+            std::vector<double> av(a.values.begin(), a.values.end()), xv(x.data.begin(), x.data.end());
+            std::vector<double> ref(size_t(200) * k), den(size_t(200) * k);
+            std::vector<float> ref32(size_t(200) * k);
+            orc_spmm_f64(200, a.row_ptr.data(), a.col_idx.data(), av.data(), xv.data(), k, red, ref.data());
+            orc_spmm_absdenom_f64(200, a.row_ptr.data(), a.col_idx.data(), av.data(), xv.data(), k, red, den.data());
+            orc_spmm_f32(200, a.row_ptr.data(), a.col_idx.data(), a.values.data(), x.data.data(), k, red, ref32.data());
+            for (uint32_t i = 0; i < 200; ++i) {
+                const bool short_row = a.row_ptr[i + 1] - a.row_ptr[i] <= SGNN_SEGMENT;
+                for (uint32_t q = 0; q < k; ++q) {
+                    const size_t o = size_t(i) * k + q;
+                    EXPECT(std::fabs(c.data[o] - ref[o]) <= 1e-5 * den[o]);
+                    if (short_row || red == 1 || red == 2)
+                        EXPECT(std::memcmp(&c.data[o], &ref32[o], 4) == 0);
+                }
+            }
+        }
+    }
+    // ---- transpose bit-exact (sparse.hpp:72-89)
+    {
+        Csr a = random_csr(g, 300, 500, 0.03, true);
+        Csr t = sg::transpose(a);
+        std::vector<uint64_t> trp(501);
+        std::vector<uint32_t> tci(a.nnz());
+        std::vector<float> tv(a.nnz());
+        orc_transpose_f32(300, 500, a.row_ptr.data(), a.col_idx.data(), a.values.data(), trp.data(), tci.data(), tv.data());
+        EXPECT(t.row_ptr == trp && t.col_idx == tci && t.values == tv);
+        Csr tt = sg::transpose(t);
+        EXPECT(tt.row_ptr == a.row_ptr && tt.col_idx == a.col_idx && tt.values == a.values);
+        EXPECT(!sg::is_symmetric(a));
+    }
+    // ---- TrainingCache counters (gnn.hpp:113-173)
+    {
+        Csr a = random_csr(g, 400, 400, 0.01, false);
+        sg::TrainingCache cache(a, true);
+        sg::DeviceBuffer<float> dc(size_t(400) * 8), dx(size_t(400) * 8);
+        cudaMemset(dc.get(), 0, sizeof(float) * 400 * 8);
+        for (int i = 0; i < 5; ++i) cache.spmm_backward(dc.get(), 8, dx.get());
+        cudaDeviceSynchronize();
+        EXPECT(cache.transpose_builds() == 1 && cache.cache_hits() == 4 && !cache.symmetric());
+    }
+    if (failures) {
+        std::fprintf(stderr, "%d failures\n", failures);
+        return 1;
+    }
+    std::printf("compat OK\n");
+    return 0;
+}
