@@ -47,6 +47,20 @@ void sgnn_host_rmat_free(void* h);
 void sgnn_host_balanced_row_partition(const uint64_t* rp, uint32_t n_rows, int n_chunks,
                                       uint32_t* bounds);
 
+/* Row block `part` of a square CSR A (n x n) split at `bounds` (n_parts+1
+ * entries, e.g. from sgnn_host_balanced_row_partition), with every column id
+ * remapped to the padded owner layout used by the multi-GPU exchange:
+ *     col' = owner(col) * stride + (col - bounds[owner])
+ * so the all-gathered feature buffer [n_parts * stride, K] (rank q's block at
+ * rows q*stride..) can be indexed directly.  stride >= max block size.  The
+ * remap is monotone, so each row keeps its nonzero order (results are
+ * bitwise those of the unpartitioned SpMM).  out_rp: bounds[part+1] -
+ * bounds[part] + 1 entries; out_ci / out_v: the block's nonzeros (out_v and
+ * v may be NULL).  Returns the block's nnz. */
+uint64_t sgnn_host_partition_block(const uint64_t* rp, const uint32_t* ci, const float* v,
+                                   const uint32_t* bounds, int n_parts, int part, uint32_t stride,
+                                   uint64_t* out_rp, uint32_t* out_ci, float* out_v, int threads);
+
 #ifdef __cplusplus
 }
 #endif

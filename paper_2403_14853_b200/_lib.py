@@ -128,6 +128,7 @@ HOST_SIGNATURES = {
     "sgnn_host_rmat_export": (None, [P, P, P]),
     "sgnn_host_rmat_free": (None, [P]),
     "sgnn_host_balanced_row_partition": (None, [P, u32, i32, P]),
+    "sgnn_host_partition_block": (u64, [P, P, P, P, i32, i32, u32, P, P, P, i32]),
 }
 
 _lock = threading.Lock()

@@ -167,9 +167,8 @@ SpmmLauncher find_fused_launcher(bool vec, int lanes, int vregs, int unroll, int
     const bool sig = edge == SGNN_EDGE_SIGMOID_MUL;
     switch (reduce) {
         case SGNN_REDUCE_SUM:
+        case SGNN_REDUCE_MEAN:  // sum kernels + the divide pass (run_mean_divide)
             return sig ? fused_lookup_sig_sum(vec, lanes, vregs, unroll, 1) : fused_lookup_mul_sum(vec, lanes, vregs, unroll, 1);
-        case SGNN_REDUCE_MEAN:
-            return sig ? fused_lookup_sig_mean(vec, lanes, vregs, unroll, 1) : fused_lookup_mul_mean(vec, lanes, vregs, unroll, 1);
         case SGNN_REDUCE_MIN:
             return sig ? fused_lookup_sig_min(vec, lanes, vregs, unroll, 1) : fused_lookup_mul_min(vec, lanes, vregs, unroll, 1);
         case SGNN_REDUCE_MAX:
@@ -299,6 +298,8 @@ sgnn_status run_fusedmm(const sgnn_csr* p, const float* x, const float* y, uint3
         f.width = k;
         st = launch_spmm_fixup(f, reduce, s);
     }
+    if (st == SGNN_OK && reduce == SGNN_REDUCE_MEAN)  // kernels.hpp:263-266
+        st = run_mean_divide(p->row_ptr, p->n_rows, out, k, k, s);
     if (own) destroy_plan(own);
     return st;
 }

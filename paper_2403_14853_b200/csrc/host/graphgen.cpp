@@ -213,4 +213,23 @@ void sgnn_host_balanced_row_partition(const uint64_t* rp, uint32_t n_rows, int n
     }
 }
 
+uint64_t sgnn_host_partition_block(const uint64_t* rp, const uint32_t* ci, const float* v,
+                                   const uint32_t* bounds, int n_parts, int part, uint32_t stride,
+                                   uint64_t* out_rp, uint32_t* out_ci, float* out_v, int threads) {
+    const uint32_t r0 = bounds[part], r1 = bounds[part + 1];
+    const uint64_t e0 = rp[r0], e1 = rp[r1];
+    for (uint32_t r = r0; r <= r1; ++r) out_rp[r - r0] = rp[r] - e0;
+    parallel_range(e1 - e0, threads, [&](uint64_t lo, uint64_t hi) {
+        for (uint64_t e = lo; e < hi; ++e) {
+            const uint32_t c = ci[e0 + e];
+            // owner = last q with bounds[q] <= c (n_parts <= a few dozen: linear is fine)
+            int q = 0;
+            while (q + 1 < n_parts && bounds[q + 1] <= c) ++q;
+            out_ci[e] = uint32_t(q) * stride + (c - bounds[q]);
+            if (out_v) out_v[e] = v[e0 + e];
+        }
+    });
+    return e1 - e0;
+}
+
 }  // extern "C"

@@ -19,6 +19,9 @@ sgnn_status cache_counters(sgnn_cache_s* c, uint64_t* tb, uint64_t* nb, uint64_t
 
 sgnn_status run_spmm(const sgnn_csr* a, const float* x, uint32_t k, float* c, int reduce,
                      const sgnn_plan_s* plan, cudaStream_t s);
+// Mean epilogue: C[r, :k] /= deg(r) (kernels.hpp:60-63, :263-266).
+sgnn_status run_mean_divide(const uint64_t* rp, uint32_t m, float* c, uint64_t ldc, uint32_t k,
+                            cudaStream_t s);
 
 sgnn_status run_transpose(const sgnn_csr* a, uint64_t* trp, uint32_t* tci, float* tv, void* ws,
                           size_t ws_bytes, cudaStream_t s);

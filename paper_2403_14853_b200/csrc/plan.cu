@@ -119,7 +119,8 @@ void default_params(const sgnn_csr* a, uint32_t k, bool vec_ok, const DeviceProp
         else if (k <= 256) { d.lanes = 32; d.vec = 2; }
         else { d.lanes = 32; d.vec = 4; }
         d.unroll = d.vec >= 4 ? 4 : (d.vec == 2 ? 4 : 8);
-        if (d.lanes == 32 && d.vec == 2) d.occupancy = 4;  // K=256: cfg3 probe
+        // register cap for 5 resident 128-thread CTAs: best or equal on cfg1-cfg4 probes
+        if (d.vec <= 2 && k > 16) d.occupancy = 5;
     } else {
         d.lanes = 32;
         d.vec = k <= 32 ? 1 : k <= 64 ? 2 : k <= 128 ? 4 : 8;

@@ -1,4 +1,10 @@
-// spmm.cu -- host driver of the SpMM worker + fixup kernels (K-tile passes).
+// spmm.cu -- host driver of the SpMM worker + fixup kernels (K-tile passes),
+// and the Mean epilogue.
+//
+// Mean (kernels.hpp:60-63) is the Sum kernels followed by one divide pass
+// over C: the IEEE-exact division (__fdiv_rn) carries a slow-path subroutine
+// call whose register cost would otherwise be paid inside the gather loop.
+// The quotient is the same: (canonical sum) / deg.
 #include <algorithm>
 
 #include "ops.cuh"
@@ -7,10 +13,52 @@
 
 namespace sgnn {
 
+namespace {
+
+// C[r, :] /= deg(r) for rows with deg > 0 (empty rows already hold 0).
+// One warp per row; float4 when the row is 16-byte aligned.
+__global__ void __launch_bounds__(256) mean_divide_kernel(const uint64_t* __restrict__ rp, uint32_t m,
+                                                          float* __restrict__ c, uint64_t ldc,
+                                                          uint32_t k, bool vec) {
+    const uint32_t lane = threadIdx.x & 31;
+    const uint32_t n_warps = (gridDim.x * blockDim.x) >> 5;
+    for (uint32_t r = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; r < m; r += n_warps) {
+        const uint64_t deg = __ldg(rp + r + 1) - __ldg(rp + r);
+        if (!deg) continue;
+        const float d = float(deg);
+        float* row = c + uint64_t(r) * ldc;
+        if (vec) {
+            float4* row4 = reinterpret_cast<float4*>(row);
+            for (uint32_t q = lane; q < k / 4; q += 32) {
+                float4 t = row4[q];
+                t.x = __fdiv_rn(t.x, d); t.y = __fdiv_rn(t.y, d);
+                t.z = __fdiv_rn(t.z, d); t.w = __fdiv_rn(t.w, d);
+                row4[q] = t;
+            }
+        } else {
+            for (uint32_t q = lane; q < k; q += 32) row[q] = __fdiv_rn(row[q], d);
+        }
+    }
+}
+
+}  // namespace
+
+sgnn_status run_mean_divide(const uint64_t* rp, uint32_t m, float* c, uint64_t ldc, uint32_t k,
+                            cudaStream_t s) {
+    if (m == 0 || k == 0) return SGNN_OK;
+    DeviceProps dp;
+    SGNN_TRY(device_props(&dp));
+    const uint64_t blocks = std::min<uint64_t>(ceil_div_u64(uint64_t(m) * 32, 256), uint64_t(dp.sm_count) * 16);
+    const bool vec = (k % 4 == 0) && (ldc % 4 == 0) && (reinterpret_cast<uintptr_t>(c) % 16 == 0);
+    mean_divide_kernel<<<unsigned(blocks), 256, 0, s>>>(rp, m, c, ldc, k, vec);
+    SGNN_LAUNCH_CHECK();
+    return SGNN_OK;
+}
+
 SpmmLauncher find_spmm_launcher(bool vec, int lanes, int vregs, int unroll, int reduce, int occ) {
     switch (reduce) {
-        case SGNN_REDUCE_SUM: return spmm_lookup_sum(vec, lanes, vregs, unroll, occ);
-        case SGNN_REDUCE_MEAN: return spmm_lookup_mean(vec, lanes, vregs, unroll, occ);
+        case SGNN_REDUCE_SUM:
+        case SGNN_REDUCE_MEAN: return spmm_lookup_sum(vec, lanes, vregs, unroll, occ);
         case SGNN_REDUCE_MIN: return spmm_lookup_min(vec, lanes, vregs, unroll, occ);
         case SGNN_REDUCE_MAX: return spmm_lookup_max(vec, lanes, vregs, unroll, occ);
     }
@@ -19,8 +67,8 @@ SpmmLauncher find_spmm_launcher(bool vec, int lanes, int vregs, int unroll, int 
 
 sgnn_status launch_spmm_fixup(const FixupArgs& f, int reduce, cudaStream_t s) {
     switch (reduce) {
-        case SGNN_REDUCE_SUM: return spmm_lookup_sum_fixup(f, s);
-        case SGNN_REDUCE_MEAN: return spmm_lookup_mean_fixup(f, s);
+        case SGNN_REDUCE_SUM:
+        case SGNN_REDUCE_MEAN: return spmm_lookup_sum_fixup(f, s);
         case SGNN_REDUCE_MIN: return spmm_lookup_min_fixup(f, s);
         case SGNN_REDUCE_MAX: return spmm_lookup_max_fixup(f, s);
     }
@@ -45,9 +93,11 @@ sgnn_status run_spmm(const sgnn_csr* a, const float* x, uint32_t k, float* c, in
             unroll = vregs >= 4 ? 2 : 4;
         }
     }
-    if (!find_spmm_launcher(vec, lanes, vregs, unroll, reduce, vec ? int(plan->p.occupancy) : 1))
-        return fail(SGNN_ERR_UNSUPPORTED, "spmm: no kernel compiled for this plan and reduce op");
-    SpmmLauncher launch = find_spmm_launcher(vec, lanes, vregs, unroll, reduce, vec ? int(plan->p.occupancy) : 1);
+    // register-capped variants exist for sum (and hence mean); min/max use
+    // the uncapped kernel of the same layout (occupancy is not numerics)
+    const int occ = vec ? int(plan->p.occupancy) : 1;
+    SpmmLauncher launch = find_spmm_launcher(vec, lanes, vregs, unroll, reduce, occ);
+    if (!launch && occ > 1) launch = find_spmm_launcher(vec, lanes, vregs, unroll, reduce, 1);
     if (!launch)
         return fail(SGNN_ERR_UNSUPPORTED, "spmm: no kernel compiled for lanes=" +
                                               std::to_string(lanes) + " vec=" +
@@ -90,6 +140,7 @@ sgnn_status run_spmm(const sgnn_csr* a, const float* x, uint32_t k, float* c, in
             SGNN_TRY(launch_spmm_fixup(f, reduce, s));
         }
     }
+    if (reduce == SGNN_REDUCE_MEAN) SGNN_TRY(run_mean_divide(a->row_ptr, a->n_rows, c, k, k, s));
     return SGNN_OK;
 }
 

@@ -146,20 +146,17 @@ sgnn_status launch_spmm_worker(const SpmmArgs& a, uint32_t block, uint32_t max_b
         return nullptr;                                                               \
     }
 
+// Mean runs the Sum kernels plus run_mean_divide (spmm.cu).
 SpmmLauncher spmm_lookup_sum(bool, int, int, int, int);
-SpmmLauncher spmm_lookup_mean(bool, int, int, int, int);
 SpmmLauncher spmm_lookup_min(bool, int, int, int, int);
 SpmmLauncher spmm_lookup_max(bool, int, int, int, int);
 sgnn_status spmm_lookup_sum_fixup(const FixupArgs&, cudaStream_t);
-sgnn_status spmm_lookup_mean_fixup(const FixupArgs&, cudaStream_t);
 sgnn_status spmm_lookup_min_fixup(const FixupArgs&, cudaStream_t);
 sgnn_status spmm_lookup_max_fixup(const FixupArgs&, cudaStream_t);
 SpmmLauncher fused_lookup_mul_sum(bool, int, int, int, int);
-SpmmLauncher fused_lookup_mul_mean(bool, int, int, int, int);
 SpmmLauncher fused_lookup_mul_min(bool, int, int, int, int);
 SpmmLauncher fused_lookup_mul_max(bool, int, int, int, int);
 SpmmLauncher fused_lookup_sig_sum(bool, int, int, int, int);
-SpmmLauncher fused_lookup_sig_mean(bool, int, int, int, int);
 SpmmLauncher fused_lookup_sig_min(bool, int, int, int, int);
 SpmmLauncher fused_lookup_sig_max(bool, int, int, int, int);
 

@@ -213,8 +213,11 @@ __device__ __forceinline__ float group_dot(const Frag<G, V, VEC>& a, const Frag<
 
 template <int OP>
 __device__ __forceinline__ float edge_value(float p, float dot) {
-    if (OP == OP_FUSED_SIGMOID)  // p * (1 / (1 + exp(-dot)))
-        return __fmul_rn(p, __fdiv_rn(1.0f, __fadd_rn(1.0f, expf(-dot))));
+    // p * (1 / (1 + exp(-dot))).  The reciprocal is the fast one (<= 2 ulp,
+    // deterministic): the IEEE-exact divide's slow-path call would cost
+    // registers inside the gather loop; FusedMM parity is tolerance-based.
+    if (OP == OP_FUSED_SIGMOID)
+        return __fmul_rn(p, __fdividef(1.0f, __fadd_rn(1.0f, expf(-dot))));
     return __fmul_rn(p, dot);  // default combine, kernels.hpp:239
 }
 

@@ -1,0 +1,115 @@
+"""Multi-GPU row partition.  CPU: the partitioner, the column
+remap and the all-gather/reassembly logic with world_size 2 over gloo, local
+compute by the oracle.  GPU: P virtual partitions on one device (loopback
+exchange) must reproduce the single-GPU SpMM bit for bit."""
+import os
+import socket
+
+import numpy as np
+import pytest
+
+from conftest import rand_csr
+from oracle import port
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _oracle_compute(local, gathered, reduce):
+    import torch
+    rp, ci, v = local
+    red = {"sum": 0, "min": 1, "max": 2, "mean": 3}[reduce]
+    out = port.spmm(rp, ci, v, gathered.numpy(), red, np.float32)
+    return torch.from_numpy(out)
+
+
+def test_partition_blocks_cover_and_remap():
+    from paper_2403_14853_b200 import partition
+    rng = np.random.default_rng(0)
+    n = 500
+    rp, ci, v = rand_csr(rng, n, n, 0.02, hub_rows=(0, 7), empty_frac=0.1)
+    for parts in (1, 2, 3, 8):
+        pt = partition.make_partition(rp, parts)
+        np.testing.assert_array_equal(pt.bounds, port.balanced_row_partition(rp, parts))
+        assert pt.stride >= max(np.diff(pt.bounds.astype(np.int64)))
+        total = 0
+        for p in range(parts):
+            lrp, lci, lv = pt.block(rp, ci, v, p)
+            r0, r1 = pt.rows(p)
+            total += len(lci)
+            # inverse remap recovers the global columns in the same order
+            owner = lci // pt.stride
+            glob = pt.bounds[owner] + (lci % pt.stride)
+            np.testing.assert_array_equal(glob, ci[rp[r0]:rp[r1]])
+            np.testing.assert_array_equal(lv, v[rp[r0]:rp[r1]])
+            for i in range(len(lrp) - 1):  # the remap keeps every row strictly increasing
+                row = lci[lrp[i]:lrp[i + 1]].astype(np.int64)
+                assert (np.diff(row) > 0).all()
+        assert total == len(ci)
+
+
+def _worker(rank, world, port_, rp, ci, v, x, reduce, q):
+    import torch
+    import torch.distributed as dist
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port_))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_2403_14853_b200 import partition
+        pt = partition.make_partition(rp, world)
+        ps = partition.PartitionedSpmm(rp, ci, v, pt, rank, x.shape[1], device="cpu", compute=_oracle_compute)
+        r0, r1 = pt.rows(rank)
+        c_local = ps.forward(torch.from_numpy(x[r0:r1].copy()), partition.NcclExchange(), reduce)
+        # reassemble on every rank through the same padded all-gather
+        full = partition.NcclExchange().all_gather(partition.pad_block(c_local, pt.stride))
+        if rank == 0:
+            rows = [full[p * pt.stride: p * pt.stride + (pt.rows(p)[1] - pt.rows(p)[0])] for p in range(world)]
+            q.put(torch.cat(rows).numpy())
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("reduce", ["sum", "mean", "max"])
+def test_two_rank_gloo_matches_single_process(reduce):
+    import torch.multiprocessing as mp
+    rng = np.random.default_rng(3)
+    n = 400
+    rp, ci, v = rand_csr(rng, n, n, 0.03, hub_rows=(1,), empty_frac=0.1)
+    x = rng.uniform(-1, 1, (n, 16)).astype(np.float32)
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port_ = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, 2, port_, rp, ci, v, x, reduce, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    got = q.get(timeout=120)
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    want = port.spmm(rp, ci, v, x, {"sum": 0, "max": 2, "mean": 3}[reduce], np.float32)
+    np.testing.assert_array_equal(got.view(np.uint32), want.view(np.uint32))
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("parts", [1, 2, 3, 8])
+def test_loopback_partition_bitwise_equals_single_gpu(cuda, parts):
+    import torch
+
+    from paper_2403_14853_b200 import graphs, ops, partition
+    rp, ci = graphs.rmat(14, (1 << 14) * 24, seed=5, symmetrize=True, self_loops=True)
+    n = 1 << 14
+    v = np.ones(len(ci), np.float32)
+    x = torch.from_numpy(graphs.normal(n * 64, 0, 1, 3).reshape(n, 64)).cuda()
+    a = ops.CsrMatrix.from_numpy(rp, ci, v, n)
+    for reduce in ("sum", "mean"):
+        want = ops.spmm(a, x, reduce).cpu().numpy()
+        pt = partition.make_partition(rp, parts)
+        ranks = [partition.PartitionedSpmm(rp, ci, v, pt, p, 64) for p in range(parts)]
+        blocks = [partition.pad_block(x[pt.rows(p)[0]:pt.rows(p)[1]], pt.stride) for p in range(parts)]
+        gathered = partition.LoopbackExchange().all_gather(blocks)
+        got = np.concatenate([r.compute(gathered, reduce).cpu().numpy() for r in ranks])
+        np.testing.assert_array_equal(got.view(np.uint32), want.view(np.uint32))
