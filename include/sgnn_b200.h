@@ -228,6 +228,12 @@ sgnn_status sgnn_sddmm_f32(const sgnn_csr* p, const float* x, uint32_t x_rows, c
 sgnn_status sgnn_fusedmm_f32(const sgnn_csr* p, const float* x, uint32_t x_rows, const float* y,
                              uint32_t y_rows, uint32_t k, int edge_op, int reduce, float* out,
                              sgnn_stream stream);
+/* fusedmm with a caller-owned plan of P (reused work split; its lanes x vec
+ * register layout is used when it holds all of K and a fused kernel exists
+ * for it).  The plan must be built with k_tile = 0 (all of K). */
+sgnn_status sgnn_fusedmm_plan_f32(const sgnn_csr* p, const float* x, uint32_t x_rows,
+                                  const float* y, uint32_t y_rows, uint32_t k, int edge_op,
+                                  int reduce, float* out, sgnn_plan plan, sgnn_stream stream);
 
 #ifdef __cplusplus
 } /* extern "C" */

@@ -12,6 +12,7 @@
 // autotune.hpp:40-51), so autotune.hpp is included first.
 #include "sparsegnn/autotune.hpp"
 #include "sparsegnn/gnn.hpp"
+#include "sparsegnn/io.hpp"
 #include "sparsegnn/kernels.hpp"
 #include "sparsegnn/parallel.hpp"
 #include "sparsegnn/sparse.hpp"
@@ -257,5 +258,98 @@ const float* ref_bench_out(void* h, int which) {
 void ref_bench_free(void* h) { delete static_cast<RefBench*>(h); }
 
 int ref_hw_cores() { return detect_hardware().cores; }
+
+// ---- GNN training (gnn.hpp:75-438), the callers of the hot path --------------
+// init_model (gnn.hpp:75-99): writes w1, w2 (and w1_self, w2_self for SAGE) in
+// that order into `out` (sizes in*h, h*c, in*h, h*c).
+int ref_init_model(int kind, uint32_t in, uint32_t hidden, uint32_t classes, uint64_t seed, float* out) {
+    GUARD_BEGIN
+    auto m = init_model<float>(static_cast<ModelKind>(kind), in, hidden, classes, seed);
+    size_t o = 0;
+    auto put = [&](const DenseMatrix<float>& w) {
+        std::memcpy(out + o, w.data.data(), sizeof(float) * w.data.size());
+        o += w.data.size();
+    };
+    put(m.w1);
+    put(m.w2);
+    if (m.has_self_weights()) {
+        put(m.w1_self);
+        put(m.w2_self);
+    }
+    GUARD_END
+}
+
+// train (gnn.hpp:414-438) from the given initial weights; returns per-epoch
+// loss/accuracy, the final weights (same packing as ref_init_model) and the
+// cache counters {transpose_builds, normalize_builds, cache_hits}.
+int ref_train(int kind, uint32_t n, const uint64_t* rp, const uint32_t* ci, const float* v,
+              uint32_t in, const float* x, const uint32_t* labels, const uint8_t* mask,
+              uint32_t hidden, uint32_t classes, const float* w_init, int epochs, double lr,
+              int use_cache, int threads, double* losses, double* accs, float* w_out,
+              uint64_t* counters) {
+    GUARD_BEGIN
+    GnnModel<float> m = init_model<float>(static_cast<ModelKind>(kind), in, hidden, classes, 1);
+    size_t o = 0;
+    auto get = [&](DenseMatrix<float>& w) {
+        std::memcpy(w.data.data(), w_init + o, sizeof(float) * w.data.size());
+        o += w.data.size();
+    };
+    get(m.w1);
+    get(m.w2);
+    if (m.has_self_weights()) {
+        get(m.w1_self);
+        get(m.w2_self);
+    }
+    TrainOptions opts;
+    opts.epochs = epochs;
+    opts.lr = lr;
+    opts.threads = threads;
+    opts.use_cache = use_cache != 0;
+    std::vector<index_t> lab(labels, labels + n);
+    std::vector<std::uint8_t> msk(mask, mask + n);
+    auto res = train(m, make_csr<float>(n, n, rp, ci, v), make_dense<float>(n, in, x), lab, msk, opts);
+    for (int e = 0; e < epochs; ++e) {
+        losses[e] = res.stats[e].loss;
+        accs[e] = res.stats[e].train_accuracy;
+    }
+    o = 0;
+    auto put = [&](const DenseMatrix<float>& w) {
+        std::memcpy(w_out + o, w.data.data(), sizeof(float) * w.data.size());
+        o += w.data.size();
+    };
+    put(m.w1);
+    put(m.w2);
+    if (m.has_self_weights()) {
+        put(m.w1_self);
+        put(m.w2_self);
+    }
+    counters[0] = res.cache.transpose_builds;
+    counters[1] = res.cache.normalize_builds;
+    counters[2] = res.cache.cache_hits;
+    GUARD_END
+}
+
+// synth_planted (io.hpp:315-378): the reference's seeded node-classification set.
+// Two calls: features/labels/mask sized by n/feat_dim; the graph via out_nnz + arrays.
+void* ref_synth_planted(uint32_t n, uint32_t classes, double p_intra, double p_inter, uint32_t feat_dim,
+                        double noise, uint64_t seed) {
+    try {
+        return new Dataset<float>(synth_planted<float>(n, classes, p_intra, p_inter, feat_dim, noise, seed));
+    } catch (...) {
+        return nullptr;
+    }
+}
+uint64_t ref_dataset_nnz(void* h) { return static_cast<Dataset<float>*>(h)->adjacency.nnz(); }
+void ref_dataset_export(void* h, uint64_t* rp, uint32_t* ci, float* v, float* x, uint32_t* labels,
+                        uint8_t* mask) {
+    auto* d = static_cast<Dataset<float>*>(h);
+    std::memcpy(rp, d->adjacency.row_ptr.data(), sizeof(uint64_t) * d->adjacency.row_ptr.size());
+    std::memcpy(ci, d->adjacency.col_idx.data(), sizeof(uint32_t) * d->adjacency.nnz());
+    std::memcpy(v, d->adjacency.values.data(), sizeof(float) * d->adjacency.nnz());
+    std::memcpy(x, d->features.data.data(), sizeof(float) * d->features.data.size());
+    std::memcpy(labels, d->labels.data(), sizeof(uint32_t) * d->labels.size());
+    std::memcpy(mask, d->train_mask.data(), d->train_mask.size());
+}
+void ref_dataset_free(void* h) { delete static_cast<Dataset<float>*>(h); }
 
 }  // extern "C"

@@ -117,6 +117,7 @@ SIGNATURES = {
     "sgnn_spmm_backward_f32": (i32, [P, P, u32, u32, P, i32, P]),
     "sgnn_sddmm_f32": (i32, [CsrP, P, u32, P, u32, u32, P, P]),
     "sgnn_fusedmm_f32": (i32, [CsrP, P, u32, P, u32, u32, i32, i32, P, P]),
+    "sgnn_fusedmm_plan_f32": (i32, [CsrP, P, u32, P, u32, u32, i32, i32, P, P, P]),
 }
 
 HOST_SIGNATURES = {

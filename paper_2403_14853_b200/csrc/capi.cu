@@ -266,6 +266,19 @@ sgnn_status sgnn_fusedmm_f32(const sgnn_csr* p, const float* x, uint32_t x_rows,
     return run_fusedmm(p, x, y, k, edge_op, reduce, out, nullptr, cs(stream));
 }
 
+sgnn_status sgnn_fusedmm_plan_f32(const sgnn_csr* p, const float* x, uint32_t x_rows,
+                                  const float* y, uint32_t y_rows, uint32_t k, int edge_op,
+                                  int reduce, float* out, sgnn_plan plan, sgnn_stream stream) {
+    SGNN_TRY(check_csr(p, "fusedmm"));
+    if (p->n_rows != x_rows || p->n_cols != y_rows)
+        return fail(SGNN_ERR_SHAPE, "fusedmm: operand shapes do not compose (P " +
+                                        std::to_string(p->n_rows) + "x" + std::to_string(p->n_cols) +
+                                        ", X " + std::to_string(x_rows) + "x" + std::to_string(k) +
+                                        ", Y " + std::to_string(y_rows) + "x" + std::to_string(k) + ")");
+    if (!plan) return fail(SGNN_ERR_CONFIG, "fusedmm_plan: null plan");
+    return run_fusedmm(p, x, y, k, edge_op, reduce, out, plan, cs(stream));
+}
+
 void sgnn_set_dispatch(int enabled) {
     g_tuned_enabled.store(enabled != 0, std::memory_order_relaxed);
 }

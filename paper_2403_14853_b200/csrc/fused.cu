@@ -45,70 +45,92 @@ __device__ __forceinline__ uint32_t row_of(const uint64_t* __restrict__ rp, uint
     return lo;
 }
 
+// Same hot-loop shape as the SpMM worker: 32-bit worker-local positions,
+// (col, val) of the next batch prefetched, one IMAD per gather address, and
+// the U dot products of a batch formed together when the batch stays in one
+// row (independent shuffle trees interleave).
 template <int G, int V, int U, bool VEC>
-__global__ void __launch_bounds__(256) sddmm_kernel(const SddmmArgs a) {
+__global__ void __launch_bounds__(128) sddmm_kernel(const SddmmArgs a) {
     using F = dev::Frag<G, V, VEC>;
-    constexpr int CH = (U > G) ? (U / G) : 1;
-    constexpr int CHUNK = G * CH;
+    constexpr int CH = (U + G - 1) / G;
     const int lane = threadIdx.x & 31;
     const int gl = lane & (G - 1);
     const unsigned gmask = (G == 32) ? 0xffffffffu : (((1u << G) - 1u) << (lane & ~(G - 1)));
     const uint32_t n_groups = (gridDim.x * blockDim.x) / G;
+    const int gl_eff = min(gl, int(a.k / F::W) - 1);
+    const char* ylane = reinterpret_cast<const char*>(a.y + F::W * gl_eff);
+    const uint32_t ldb = uint32_t(a.ld) * 4u;
+    const int nq = F::blocks_in(gl, a.k);
+    const bool full = a.k == uint32_t(F::W * G * V);
     for (uint32_t w = (blockIdx.x * blockDim.x + threadIdx.x) / G; w < a.n_workers; w += n_groups) {
         const uint64_t j0 = uint64_t(w) * a.per_worker;
-        const uint64_t j1 = min(j0 + a.per_worker, a.nnz);
+        const uint32_t E = uint32_t(min(a.per_worker, a.nnz - j0));
         uint32_t r = row_of(a.rp, a.n_rows, j0);
         uint32_t rb = r;
         uint64_t rwin = __ldg(a.rp + min(rb + 1 + uint32_t(gl), a.n_rows));
-        uint64_t rend = dev::shfl_u64(gmask, rwin, 0, G);
+        uint32_t rend_l = uint32_t(min(dev::shfl_u64(gmask, rwin, 0, G), j0 + E) - j0);
         F xrow;
-        xrow.load(a.x + uint64_t(r) * a.ld, gl, a.k);
-        for (uint64_t base = j0; base < j1; base += CHUNK) {
-            uint32_t cc[CH];
-            float vv[CH], res[CH];
+        xrow.load(a.x + uint64_t(r) * a.ld, gl, a.k);  // zero-filled past K
+        uint32_t cc[CH];
+        float vv[CH];
+        auto load_cv = [&](uint32_t base) {
 #pragma unroll
             for (int h = 0; h < CH; ++h) {
-                const uint64_t idx = base + uint64_t(gl + G * h);
-                cc[h] = idx < j1 ? dev::ld_stream(a.ci + idx) : 0u;
-                vv[h] = idx < j1 ? dev::ld_stream(a.val + idx) : 0.0f;
-                res[h] = 0.0f;
+                const uint32_t lq = base + uint32_t(gl + G * h);
+                const bool ok = (gl + G * h) < U && lq < E;
+                cc[h] = ok ? dev::ld_stream(a.ci + j0 + lq) : 0u;
+                vv[h] = ok ? dev::ld_stream(a.val + j0 + lq) : 0.0f;
             }
-            const int n = (j1 - base) < uint64_t(CHUNK) ? int(j1 - base) : CHUNK;
-#pragma unroll
-            for (int q0 = 0; q0 < CHUNK; q0 += U) {
-                if (q0 >= n) break;
-                F yf[U];
-#pragma unroll
-                for (int u = 0; u < U; ++u) {
-                    const int q = q0 + u;
-                    const uint32_t col = __shfl_sync(gmask, cc[q / G], q % G, G);
-                    if (q < n) yf[u].load(a.y + uint64_t(col) * a.ld, gl, a.k);
+        };
+        auto next_row = [&](uint32_t l) {  // advance to the row holding local position l
+            do {
+                ++r;
+                if (r - rb >= uint32_t(G)) {
+                    rb = r;
+                    rwin = __ldg(a.rp + min(rb + 1 + uint32_t(gl), a.n_rows));
                 }
+                rend_l = uint32_t(min(dev::shfl_u64(gmask, rwin, int(r - rb), G), j0 + E) - j0);
+            } while (l >= rend_l);
+            xrow.load(a.x + uint64_t(r) * a.ld, gl, a.k);
+        };
+        if (E) load_cv(0);
+        for (uint32_t base = 0; base < E; base += U) {
+            const int n = (E - base) < uint32_t(U) ? int(E - base) : U;
+            F yf[U];
+            float pv[U];
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+                const uint32_t col = __shfl_sync(gmask, cc[u / G], u % G, G);
+                pv[u] = __shfl_sync(gmask, vv[u / G], u % G, G);
+                const float* lrow = reinterpret_cast<const float*>(ylane + uint64_t(col) * ldb);
+                if (full) yf[u].template gather<false>(lrow, nq);
+                else yf[u].template gather<true>(lrow, nq);
+            }
+            if (base + U < E) load_cv(base + U);
+            float res[CH];
+#pragma unroll
+            for (int h = 0; h < CH; ++h) res[h] = 0.0f;
+            if (base >= rend_l) next_row(base);
+            if (base + uint32_t(n) <= rend_l) {
+                float d[U];
+#pragma unroll
+                for (int u = 0; u < U; ++u) d[u] = dev::group_dot(xrow, yf[u], gmask);
+#pragma unroll
+                for (int u = 0; u < U; ++u)
+                    if (gl == u % G) res[u / G] = __fmul_rn(pv[u], d[u]);  // kernels.hpp:206
+            } else {
 #pragma unroll
                 for (int u = 0; u < U; ++u) {
-                    const int q = q0 + u;
-                    const float pv = __shfl_sync(gmask, vv[q / G], q % G, G);
-                    if (q >= n) break;
-                    const uint64_t e = base + uint64_t(q);
-                    if (e >= rend) {
-                        do {
-                            ++r;
-                            if (r - rb >= uint32_t(G)) {
-                                rb = r;
-                                rwin = __ldg(a.rp + min(rb + 1 + uint32_t(gl), a.n_rows));
-                            }
-                            rend = dev::shfl_u64(gmask, rwin, int(r - rb), G);
-                        } while (e >= rend);
-                        xrow.load(a.x + uint64_t(r) * a.ld, gl, a.k);
-                    }
+                    if (u >= n) break;
+                    if (base + uint32_t(u) >= rend_l) next_row(base + uint32_t(u));
                     const float d = dev::group_dot(xrow, yf[u], gmask);
-                    if (gl == q % G) res[q / G] = __fmul_rn(pv, d);  // kernels.hpp:206
+                    if (gl == u % G) res[u / G] = __fmul_rn(pv[u], d);
                 }
             }
 #pragma unroll
             for (int h = 0; h < CH; ++h) {
-                const uint64_t idx = base + uint64_t(gl + G * h);
-                if (idx < j1) __stcs(a.out + idx, res[h]);
+                const uint32_t lq = base + uint32_t(gl + G * h);
+                if ((gl + G * h) < U && lq < E) __stcs(a.out + j0 + lq, res[h]);
             }
         }
     }
@@ -123,13 +145,13 @@ sgnn_status launch_sddmm(const SddmmArgs& a, cudaStream_t s) {
     SGNN_TRY(device_props(&dp));
     if (per_sm < 0) {
         int n = 0;
-        SGNN_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, sddmm_kernel<G, V, U, VEC>, 256, 0));
+        SGNN_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, sddmm_kernel<G, V, U, VEC>, 128, 0));
         per_sm = std::max(n, 1);
     }
-    const uint64_t blocks = std::min<uint64_t>(ceil_div_u64(uint64_t(a.n_workers) * G, 256),
+    const uint64_t blocks = std::min<uint64_t>(ceil_div_u64(uint64_t(a.n_workers) * G, 128),
                                                uint64_t(dp.sm_count) * per_sm);
     if (blocks == 0) return SGNN_OK;
-    sddmm_kernel<G, V, U, VEC><<<unsigned(blocks), 256, 0, s>>>(a);
+    sddmm_kernel<G, V, U, VEC><<<unsigned(blocks), 128, 0, s>>>(a);
     SGNN_LAUNCH_CHECK();
     return SGNN_OK;
 }
@@ -163,18 +185,25 @@ int fused_unroll(bool vec, int lanes, int vregs) {
     return vregs >= 4 ? 2 : 4;
 }
 
-SpmmLauncher find_fused_launcher(bool vec, int lanes, int vregs, int unroll, int edge, int reduce) {
+SpmmLauncher find_fused_launcher_occ(bool vec, int lanes, int vregs, int unroll, int edge, int reduce,
+                                     int occ) {
     const bool sig = edge == SGNN_EDGE_SIGMOID_MUL;
     switch (reduce) {
         case SGNN_REDUCE_SUM:
         case SGNN_REDUCE_MEAN:  // sum kernels + the divide pass (run_mean_divide)
-            return sig ? fused_lookup_sig_sum(vec, lanes, vregs, unroll, 1) : fused_lookup_mul_sum(vec, lanes, vregs, unroll, 1);
+            return sig ? fused_lookup_sig_sum(vec, lanes, vregs, unroll, occ) : fused_lookup_mul_sum(vec, lanes, vregs, unroll, occ);
         case SGNN_REDUCE_MIN:
-            return sig ? fused_lookup_sig_min(vec, lanes, vregs, unroll, 1) : fused_lookup_mul_min(vec, lanes, vregs, unroll, 1);
+            return sig ? fused_lookup_sig_min(vec, lanes, vregs, unroll, occ) : fused_lookup_mul_min(vec, lanes, vregs, unroll, occ);
         case SGNN_REDUCE_MAX:
-            return sig ? fused_lookup_sig_max(vec, lanes, vregs, unroll, 1) : fused_lookup_mul_max(vec, lanes, vregs, unroll, 1);
+            return sig ? fused_lookup_sig_max(vec, lanes, vregs, unroll, occ) : fused_lookup_mul_max(vec, lanes, vregs, unroll, occ);
     }
     return nullptr;
+}
+
+// Prefers the register-capped (5 CTAs/SM) variant when one is compiled.
+SpmmLauncher find_fused_launcher(bool vec, int lanes, int vregs, int unroll, int edge, int reduce) {
+    SpmmLauncher l = find_fused_launcher_occ(vec, lanes, vregs, unroll, edge, reduce, 5);
+    return l ? l : find_fused_launcher_occ(vec, lanes, vregs, unroll, edge, reduce, 1);
 }
 
 }  // namespace
@@ -251,15 +280,19 @@ sgnn_status run_fusedmm(const sgnn_csr* p, const float* x, const float* y, uint3
         return fail(SGNN_ERR_DISPATCH, "fusedmm: plan was built for another matrix or K");
     }
     sgnn_status st = SGNN_OK;
-    int unroll = int(plan->p.unroll);
-    if (plan->vec != vec || int(plan->p.lanes) != lanes || int(plan->p.vec) != vregs)
-        unroll = fused_unroll(vec, lanes, vregs);  // the split is reusable; the layout must cover K
-    if (plan->kt < k && plan->p.k_tile != k) {
-        // K-tiling is meaningless for FusedMM (the dot needs all of K); the
-        // split itself does not depend on the tile, so only the slots matter.
-        if (plan->n_slots && plan->kt < k)
-            st = fail(SGNN_ERR_DISPATCH, "fusedmm: plan workspace is narrower than K; build the plan with k_tile=K");
+    int unroll = fused_unroll(vec, lanes, vregs);
+    // A caller's plan may choose the register layout if it holds all of K and
+    // a fused kernel is compiled for it (the split is reusable either way).
+    if (!own && plan->vec == vec) {
+        const int pl = int(plan->p.lanes), pv = int(plan->p.vec), pu = int(plan->p.unroll);
+        if (uint32_t((vec ? 4 : 1) * pl * pv) >= k && find_fused_launcher(vec, pl, pv, pu, edge_op, reduce)) {
+            lanes = pl;
+            vregs = pv;
+            unroll = pu;
+        }
     }
+    if (plan->n_slots && plan->kt < k)  // the dot needs all of K: slots must be K wide
+        st = fail(SGNN_ERR_DISPATCH, "fusedmm: plan workspace is narrower than K; build the plan with k_tile=K");
     SpmmLauncher launch = st == SGNN_OK ? find_fused_launcher(vec, lanes, vregs, unroll, edge_op, reduce) : nullptr;
     if (st == SGNN_OK && !launch)
         st = fail(SGNN_ERR_UNSUPPORTED, "fusedmm: no kernel for lanes=" + std::to_string(lanes) +

@@ -36,6 +36,7 @@ sgnn_status launch_spmm_worker(const SpmmArgs& a, uint32_t block, uint32_t max_b
     X(4, 1, 4, RED, true, OP, 1)      \
     X(4, 1, 8, RED, true, OP, 1)      \
     X(4, 2, 8, RED, true, OP, 1)      \
+    X(4, 4, 4, RED, true, OP, 1)      \
     X(8, 4, 4, RED, true, OP, 1)      \
     X(8, 1, 4, RED, true, OP, 1)      \
     X(8, 1, 8, RED, true, OP, 1)      \
@@ -101,7 +102,15 @@ sgnn_status launch_spmm_worker(const SpmmArgs& a, uint32_t block, uint32_t max_b
 
 // FusedMM needs all of K in registers (the dot); a smaller set suffices.
 #define SGNN_FUSED_CONFIGS(X, RED, OP) \
+    X(16, 1, 8, RED, true, OP, 5)      \
+    X(8, 1, 8, RED, true, OP, 5)       \
+    X(32, 1, 8, RED, true, OP, 5)      \
     X(4, 1, 8, RED, true, OP, 1)       \
+    X(4, 2, 8, RED, true, OP, 1)       \
+    X(4, 4, 4, RED, true, OP, 1)       \
+    X(8, 2, 4, RED, true, OP, 1)       \
+    X(8, 4, 4, RED, true, OP, 1)       \
+    X(16, 2, 4, RED, true, OP, 1)      \
     X(8, 1, 8, RED, true, OP, 1)       \
     X(16, 1, 8, RED, true, OP, 1)      \
     X(32, 1, 4, RED, true, OP, 1)      \

@@ -65,6 +65,13 @@ struct Reducer {
         if (RED == SGNN_REDUCE_MIN) return (p < acc) ? p : acc;  // std::min(acc, p)
         return (acc < p) ? p : acc;                               // std::max(acc, p)
     }
+    // FusedMM fold: the sum accumulates with fma (FusedMM parity is
+    // tolerance-based -- its dot already differs from the reference's chain --
+    // and every plan uses the same fold, so results stay plan-independent).
+    static __device__ __forceinline__ float fold_fused(float acc, float s, float y, bool first) {
+        if (RED == SGNN_REDUCE_SUM || RED == SGNN_REDUCE_MEAN) return __fmaf_rn(s, y, acc);
+        return fold(acc, s, y, first);
+    }
     // canonical combine of consecutive segment partials (left to right)
     static __device__ __forceinline__ float combine(float t, float s) {
         if (RED == SGNN_REDUCE_SUM || RED == SGNN_REDUCE_MEAN) return __fadd_rn(t, s);
@@ -191,11 +198,11 @@ __device__ __forceinline__ float group_dot(const Frag<G, V, VEC>& a, const Frag<
     float p[V];
 #pragma unroll
     for (int q = 0; q < V; ++q) {
-        if constexpr (VEC) {
+        if constexpr (VEC) {  // leaf: fma chain over the float4
             float t = __fmul_rn(a.v[4 * q], b.v[4 * q]);
-            t = __fadd_rn(t, __fmul_rn(a.v[4 * q + 1], b.v[4 * q + 1]));
-            t = __fadd_rn(t, __fmul_rn(a.v[4 * q + 2], b.v[4 * q + 2]));
-            p[q] = __fadd_rn(t, __fmul_rn(a.v[4 * q + 3], b.v[4 * q + 3]));
+            t = __fmaf_rn(a.v[4 * q + 1], b.v[4 * q + 1], t);
+            t = __fmaf_rn(a.v[4 * q + 2], b.v[4 * q + 2], t);
+            p[q] = __fmaf_rn(a.v[4 * q + 3], b.v[4 * q + 3], t);
         } else {
             p[q] = __fmul_rn(a.v[q], b.v[q]);
         }
@@ -213,11 +220,11 @@ __device__ __forceinline__ float group_dot(const Frag<G, V, VEC>& a, const Frag<
 
 template <int OP>
 __device__ __forceinline__ float edge_value(float p, float dot) {
-    // p * (1 / (1 + exp(-dot))).  The reciprocal is the fast one (<= 2 ulp,
+    // p * (1 / (1 + exp(-dot))) with the hardware exp2/reciprocal (a few ulp,
     // deterministic): the IEEE-exact divide's slow-path call would cost
     // registers inside the gather loop; FusedMM parity is tolerance-based.
     if (OP == OP_FUSED_SIGMOID)
-        return __fmul_rn(p, __fdividef(1.0f, __fadd_rn(1.0f, expf(-dot))));
+        return __fmul_rn(p, __fdividef(1.0f, __fadd_rn(1.0f, __expf(-dot))));
     return __fmul_rn(p, dot);  // default combine, kernels.hpp:239
 }
 
@@ -251,6 +258,7 @@ __global__ void __launch_bounds__(128, MINB) spmm_worker_kernel(const SpmmArgs a
     const char* xlane = reinterpret_cast<const char*>(a.x + F::W * gl_eff);
     const uint32_t ldxb = uint32_t(a.ldx) * 4u;
     const int nq = F::blocks_in(gl, a.width);
+    const bool full = a.width == uint32_t(F::W * G * V);  // every lane's blocks are in range
 
     for (uint32_t w = (blockIdx.x * blockDim.x + threadIdx.x) / G; w < a.n_workers; w += n_groups) {
         const uint32_t i0 = __ldg(a.wrow + w), i1 = __ldg(a.wrow + w + 1);
@@ -375,8 +383,10 @@ __global__ void __launch_bounds__(128, MINB) spmm_worker_kernel(const SpmmArgs a
             for (int u = 0; u < U; ++u) {  // unconditional gathers (tail lanes read row 0)
                 const uint32_t col = __shfl_sync(gmask, cc[u / G], u % G, G);
                 av[u] = __shfl_sync(gmask, vv[u / G], u % G, G);
-                xf[u].template gather<OP != OP_SPMM>(
-                    reinterpret_cast<const float*>(xlane + uint64_t(col) * ldxb), nq);
+                const float* lrow = reinterpret_cast<const float*>(xlane + uint64_t(col) * ldxb);
+                // the FusedMM dot sums all lanes: zero-fill blocks past a partial width
+                if (OP == OP_SPMM || full) xf[u].template gather<false>(lrow, nq);
+                else xf[u].template gather<true>(lrow, nq);
             }
             if (base + CHUNK < E) load_cv(base + CHUNK);
             auto fold = [&](const F& xv, float pv) {
@@ -386,7 +396,9 @@ __global__ void __launch_bounds__(128, MINB) spmm_worker_kernel(const SpmmArgs a
                     s = edge_value<OP>(pv, group_dot(xrow, xv, gmask));
                 }
 #pragma unroll
-                for (int i = 0; i < N; ++i) acc.v[i] = R::fold(acc.v[i], s, xv.v[i], first);
+                for (int i = 0; i < N; ++i)
+                    acc.v[i] = (OP != OP_SPMM) ? R::fold_fused(acc.v[i], s, xv.v[i], first)
+                                               : R::fold(acc.v[i], s, xv.v[i], first);
                 first = false;
             };
             if (base + uint32_t(n) <= next_l) {
@@ -400,7 +412,7 @@ __global__ void __launch_bounds__(128, MINB) spmm_worker_kernel(const SpmmArgs a
                     for (int u = 0; u < U; ++u) {
                         if (u < n) {
 #pragma unroll
-                            for (int i = 0; i < N; ++i) acc.v[i] = R::fold(acc.v[i], sv[u], xf[u].v[i], first);
+                            for (int i = 0; i < N; ++i) acc.v[i] = R::fold_fused(acc.v[i], sv[u], xf[u].v[i], first);
                             first = false;
                         }
                     }

@@ -30,6 +30,9 @@ def _stream():
     return C.c_void_p(torch.cuda.current_stream().cuda_stream)
 
 
+_NAMES = {0: "sum", 1: "min", 2: "max", 3: "mean"}
+
+
 def _reduce(r) -> int:
     if isinstance(r, str):
         if r not in _lib.REDUCE:  # types.hpp:129-135 parse_reduce_op
@@ -61,6 +64,24 @@ class CsrMatrix:
         self.col_idx = col_idx.contiguous()
         self.values = values.contiguous()
         self._cstruct = None
+        self._plans = {}  # (kind, K) -> Plan; the structure is immutable once wrapped
+
+    def plan(self, k: int, kind: str = "default") -> "Plan":
+        """Cached work split for this matrix: "default" (trusted), "tuned"
+        (registered by run_tuning / register_plan, else default) or "fused"
+        (register layout holding all of K, for FusedMM)."""
+        if kind == "tuned":
+            return self._plans.get(("tuned", int(k))) or self.plan(k)
+        key = (kind, int(k))
+        if key not in self._plans:
+            if kind == "fused":
+                self._plans[key] = Plan(self, k, **_fused_layout(int(k)))
+            else:
+                self._plans[key] = Plan(self, k)
+        return self._plans[key]
+
+    def register_plan(self, k: int, plan: "Plan") -> None:
+        self._plans[("tuned", int(k))] = plan
 
     @property
     def nnz(self) -> int:
@@ -86,6 +107,18 @@ class CsrMatrix:
 
     def with_values(self, values: torch.Tensor) -> "CsrMatrix":
         return CsrMatrix(self.n_rows, self.n_cols, self.row_ptr, self.col_idx, values)
+
+
+def _fused_layout(k: int) -> dict:
+    """Register layout holding all of K (csrc/fused.cu full_k_layout)."""
+    if k % 4:
+        v = 1 if k <= 32 else 2 if k <= 64 else 4 if k <= 128 else 8
+        return {"lanes": 32, "vec": v, "unroll": 4 if v <= 2 else 2, "scalar": 1}
+    for lim, lanes, vec, unroll in ((16, 4, 1, 8), (32, 8, 1, 8), (64, 16, 1, 8), (128, 32, 1, 8),
+                                    (256, 32, 2, 4), (512, 32, 4, 4), (1024, 32, 8, 2)):
+        if k <= lim:
+            return {"lanes": lanes, "vec": vec, "unroll": unroll}
+    raise _lib.UnsupportedError(f"fusedmm: K={k} exceeds the register-resident width")
 
 
 @dataclass(frozen=True)
@@ -148,12 +181,22 @@ def spmm_into(a: CsrMatrix, b: torch.Tensor, reduce, kind: KernelKind, out: torc
     _dense(out, "spmm out")
     if out.shape[0] != a.n_rows or out.shape[1] != b.shape[1]:
         raise ShapeError(f"spmm: output is {tuple(out.shape)}, expected ({a.n_rows}, {b.shape[1]})")
-    st = lib().sgnn_spmm_with_f32(
-        C.byref(a.c()), b.data_ptr(), b.shape[0], b.shape[1], out.data_ptr(), _reduce(reduce),
-        _lib.SPECIALIZED if kind.is_specialized() else _lib.TRUSTED, kind.k,
-        plan.handle if plan is not None else None, _stream())
-    check(st, "spmm")
-    return out
+    red = _reduce(reduce)
+    if a.n_cols != b.shape[0]:  # check_spmm_shapes, kernels.hpp:131-136
+        raise ShapeError(f"spmm: sparse operand is {a.n_rows}x{a.n_cols} but dense operand is "
+                         f"{b.shape[0]}x{b.shape[1]}")
+    if kind.is_specialized():  # kernels.hpp:159-169 (same rule as sgnn_spmm_with_f32)
+        if red != _lib.SUM:
+            raise DispatchError(f"specialized kernels support sum only, got {_NAMES[red]}")
+        if kind.k not in specialization_sweep:
+            raise DispatchError(f"K={kind.k} is not in the specialization set")
+        if b.shape[1] != kind.k:
+            raise DispatchError(f"kernel is fixed at K={kind.k} but dense operand has K={b.shape[1]}")
+    if b.shape[1] == 0 or a.n_rows == 0:
+        return out
+    if plan is None:
+        plan = a.plan(b.shape[1], "tuned" if kind.is_specialized() else "default")
+    return spmm_plan(a, b, red, plan, out)
 
 
 def spmm_with(a: CsrMatrix, b: torch.Tensor, reduce, kind: KernelKind, plan: Plan | None = None):
@@ -396,6 +439,7 @@ class _View(CsrMatrix):
         self._nnz = cs.nnz
         self._cstruct = cs
         self._owner = owner
+        self._plans = {}
 
     @property
     def nnz(self) -> int:
@@ -431,7 +475,7 @@ EDGE_OPS = {"mul": _lib.EDGE_MUL, None: _lib.EDGE_MUL, "sigmoid_mul": _lib.EDGE_
 
 
 def fusedmm(p: CsrMatrix, x: torch.Tensor, y: torch.Tensor, edge_op="mul", reduce="sum",
-            out: torch.Tensor | None = None) -> torch.Tensor:
+            out: torch.Tensor | None = None, plan: Plan | None = None) -> torch.Tensor:
     """fusedmm (kernels.hpp:216-270) with a GPU-expressible combine
     (Semiring::combine, types.hpp:139-145): "mul" = p*dot (plus_times), or
     "sigmoid_mul" = p*sigmoid(dot).  An arbitrary Python callable is a
@@ -448,6 +492,13 @@ def fusedmm(p: CsrMatrix, x: torch.Tensor, y: torch.Tensor, edge_op="mul", reduc
                          f"{x.shape[0]}x{x.shape[1]}, Y {y.shape[0]}x{y.shape[1]})")
     if out is None:
         out = torch.empty((p.n_rows, y.shape[1]), dtype=torch.float32, device=x.device)
+    if plan is None and p.n_rows and x.shape[1] and x.shape[1] <= 1024 and (x.shape[1] % 4 == 0 or x.shape[1] <= 256):
+        plan = p.plan(x.shape[1], "fused")  # cached split (built once per matrix and K)
+    if plan is not None:
+        check(lib().sgnn_fusedmm_plan_f32(C.byref(p.c()), x.data_ptr(), x.shape[0], y.data_ptr(), y.shape[0],
+                                          x.shape[1], EDGE_OPS[edge_op], _reduce(reduce), out.data_ptr(),
+                                          plan.handle, _stream()), "fusedmm")
+        return out
     check(lib().sgnn_fusedmm_f32(C.byref(p.c()), x.data_ptr(), x.shape[0], y.data_ptr(), y.shape[0],
                                  x.shape[1], EDGE_OPS[edge_op], _reduce(reduce), out.data_ptr(),
                                  _stream()), "fusedmm")

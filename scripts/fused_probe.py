@@ -46,6 +46,16 @@ def main():
             print(json.dumps({"op": f"fusedmm {edge} {red}", "ms": round(ms, 4),
                               "GFLOPs(2nnzK)": round(2 * nnz * k / ms / 1e6, 1),
                               "frac": round(fu_bytes / ms / 1e6 / PEAK, 3)}))
+    for lv in ((16, 1, 8), (8, 2, 4), (16, 2, 4)):
+        for pi in (64, 128, 256):
+            try:
+                plan = ops.Plan(p, k, lanes=lv[0], vec=lv[1], unroll=lv[2], path_items=pi)
+            except Exception as ex:  # noqa: BLE001
+                print("plan", lv, ex)
+                continue
+            ms = t(lambda: ops.fusedmm(p, x, y, "sigmoid_mul", "sum", out, plan=plan), flush)
+            print(json.dumps({"op": "fusedmm sigmoid sum (plan)", "layout": lv, "path": pi, "ms": round(ms, 4),
+                              "frac": round(fu_bytes / ms / 1e6 / PEAK, 3)}))
     # SpMM on the same graph (K=64)
     plan = ops.Plan(p, k)
     ms = t(lambda: ops.spmm_plan(p, y, "sum", plan, out), flush)
