@@ -187,6 +187,15 @@ sgnn_status sgnn_row_degrees(const sgnn_csr* a, uint32_t* deg, sgnn_stream strea
  * Synchronous; *out = 1 symmetric, 0 not. */
 sgnn_status sgnn_is_symmetric(const sgnn_csr* a, int* out, sgnn_stream stream);
 
+/* normalize_adjacency(a, add_self_loops) (sparse.hpp:116-174) on the device,
+ * bit-exact: A_hat = D^-1/2 (A [+ I]) D^-1/2 with degrees and scaling in
+ * double.  Two calls: with t_row_ptr == NULL only *out_nnz is computed;
+ * then pass arrays of n+1 / out_nnz / out_nnz entries.  Non-square ->
+ * SGNN_ERR_SHAPE, a negative value -> SGNN_ERR_CONFIG.  Synchronous. */
+sgnn_status sgnn_normalize_adjacency(const sgnn_csr* a, int add_self_loops, uint64_t* out_nnz,
+                                     uint64_t* t_row_ptr, uint32_t* t_col_idx, float* t_values,
+                                     sgnn_stream stream);
+
 /* ------------------------------------------------ backward cache (TrainingCache) */
 /* TrainingCache<float> (gnn.hpp:113-173) + build_cache (gnn.hpp:180-196)
  * for a propagation operand that is already on the device (a_hat).  The
@@ -197,6 +206,14 @@ sgnn_status sgnn_is_symmetric(const sgnn_csr* a, int* out, sgnn_stream stream);
 typedef struct sgnn_cache_s* sgnn_cache;
 sgnn_status sgnn_cache_create(const sgnn_csr* a_hat, int use_cache, sgnn_cache* out,
                               sgnn_stream stream);
+/* build_cache(kind, a, use_cache, add_self_loops) (gnn.hpp:180-196) proper:
+ * model_kind 0 = GCN normalizes A on the device into a cache-owned A_hat
+ * (normalize_builds = 1); 1 = SAGE-sum, 2 = SAGE-mean, 3 = GIN propagate
+ * over A itself (borrowed).  Synchronous. */
+sgnn_status sgnn_cache_create_model(const sgnn_csr* a, int model_kind, int use_cache,
+                                    int add_self_loops, sgnn_cache* out, sgnn_stream stream);
+/* The cache's propagation operand a_hat (for the forward SpMMs). */
+sgnn_status sgnn_cache_a_hat(sgnn_cache cache, sgnn_csr* out);
 sgnn_status sgnn_cache_destroy(sgnn_cache cache);
 /* sum_operand() (gnn.hpp:127-144) / mean_operand() (gnn.hpp:149-172):
  * fills *out with a device view of the operand (valid until the next fetch

@@ -179,6 +179,75 @@ def cache_operand(rp, ci, v, model_kind, use_cache, which, n_fetches):
                                   (int(c) for c in cnt)))
 
 
+MODEL_KINDS = {"gcn": 0, "sage-sum": 1, "sage-mean": 2, "gin": 3}
+
+
+def _gnn_sigs(L):
+    if getattr(L, "_gnn_bound", False):
+        return
+    L.ref_init_model.argtypes = [C.c_int, C.c_uint32, C.c_uint32, C.c_uint32, C.c_uint64, f32p]
+    L.ref_train.argtypes = [C.c_int, C.c_uint32, u64p, u32p, f32p, C.c_uint32, f32p, u32p,
+                            np.ctypeslib.ndpointer(np.uint8, flags="C_CONTIGUOUS"), C.c_uint32, C.c_uint32,
+                            f32p, C.c_int, C.c_double, C.c_int, C.c_int, f64p, f64p, f32p,
+                            np.ctypeslib.ndpointer(np.uint64, flags="C_CONTIGUOUS")]
+    L.ref_synth_planted.argtypes = [C.c_uint32, C.c_uint32, C.c_double, C.c_double, C.c_uint32, C.c_double, C.c_uint64]
+    L.ref_synth_planted.restype = C.c_void_p
+    L.ref_dataset_nnz.argtypes = [C.c_void_p]
+    L.ref_dataset_nnz.restype = C.c_uint64
+    L.ref_dataset_export.argtypes = [C.c_void_p, u64p, u32p, f32p, f32p, u32p,
+                                     np.ctypeslib.ndpointer(np.uint8, flags="C_CONTIGUOUS")]
+    L.ref_dataset_free.argtypes = [C.c_void_p]
+    L._gnn_bound = True
+
+
+def _n_weights(kind, in_f, hidden, classes):
+    n = in_f * hidden + hidden * classes
+    return 2 * n if kind in ("sage-sum", "sage-mean") else n
+
+
+def init_model(kind, in_f, hidden, classes, seed):
+    """init_model (gnn.hpp:75-99): packed w1|w2|(w1_self|w2_self)."""
+    L = lib()
+    _gnn_sigs(L)
+    out = np.empty(_n_weights(kind, in_f, hidden, classes), np.float32)
+    _check(L.ref_init_model(MODEL_KINDS[kind], in_f, hidden, classes, seed, out))
+    return out
+
+
+def synth_planted(n, classes, p_intra, p_inter, feat_dim, noise, seed):
+    """synth_planted (io.hpp:315-378) -> (rp, ci, v, x, labels, mask)."""
+    L = lib()
+    _gnn_sigs(L)
+    h = L.ref_synth_planted(n, classes, p_intra, p_inter, feat_dim, noise, seed)
+    if not h:
+        raise RuntimeError("synth_planted failed")
+    try:
+        nnz = L.ref_dataset_nnz(h)
+        rp, ci, v = np.empty(n + 1, np.uint64), np.empty(nnz, np.uint32), np.empty(nnz, np.float32)
+        x, lab, mask = np.empty((n, feat_dim), np.float32), np.empty(n, np.uint32), np.empty(n, np.uint8)
+        L.ref_dataset_export(h, rp, ci, v, x, lab, mask)
+    finally:
+        L.ref_dataset_free(h)
+    return rp, ci, v, x, lab, mask
+
+
+def train(kind, rp, ci, v, x, labels, mask, hidden, classes, w_init, epochs, lr, use_cache=True,
+          threads=0):
+    """train (gnn.hpp:414-438) from w_init; returns (losses, accs, w_final, counters)."""
+    L = lib()
+    _gnn_sigs(L)
+    rp, ci, v = _csr(rp, ci, v, np.float32)
+    n, in_f = x.shape
+    losses, accs = np.empty(epochs), np.empty(epochs)
+    w_out = np.empty_like(np.asarray(w_init, np.float32))
+    cnt = np.zeros(3, np.uint64)
+    _check(L.ref_train(MODEL_KINDS[kind], n, rp, ci, v, in_f, np.ascontiguousarray(x, np.float32),
+                       np.ascontiguousarray(labels, np.uint32), np.ascontiguousarray(mask, np.uint8),
+                       hidden, classes, np.ascontiguousarray(w_init, np.float32), epochs, lr,
+                       int(use_cache), threads, losses, accs, w_out, cnt))
+    return losses, accs, w_out, dict(zip(("transpose_builds", "normalize_builds", "cache_hits"), (int(c) for c in cnt)))
+
+
 class Bench:
     """SpMM fwd + cached-transpose bwd on the reference CPU path (bench.py arm)."""
 

@@ -110,6 +110,9 @@ SIGNATURES = {
     "sgnn_row_degrees": (i32, [CsrP, P, P]),
     "sgnn_is_symmetric": (i32, [CsrP, C.POINTER(i32), P]),
     "sgnn_cache_create": (i32, [CsrP, i32, C.POINTER(P), P]),
+    "sgnn_cache_create_model": (i32, [CsrP, i32, i32, i32, C.POINTER(P), P]),
+    "sgnn_cache_a_hat": (i32, [P, CsrP]),
+    "sgnn_normalize_adjacency": (i32, [CsrP, i32, C.POINTER(u64), P, P, P, P]),
     "sgnn_cache_destroy": (i32, [P]),
     "sgnn_cache_sum_operand": (i32, [P, CsrP, P]),
     "sgnn_cache_mean_operand": (i32, [P, CsrP, P]),

@@ -45,7 +45,8 @@ struct DevCsr {
 }  // namespace
 
 struct sgnn_cache_s {
-    sgnn_csr a_hat{};  // borrowed
+    sgnn_csr a_hat{};  // borrowed, or a view of `own` (GCN: normalized on the device)
+    DevCsr own;
     bool use_cache = true;
     bool symmetric = false;
     uint64_t transpose_builds = 0, normalize_builds = 0, cache_hits = 0;
@@ -57,6 +58,7 @@ struct sgnn_cache_s {
     std::map<std::pair<const uint64_t*, uint32_t>, sgnn_plan_s*> plans;
 
     ~sgnn_cache_s() {
+        own.release();
         at.release();
         mean.release();
         if (deg) cudaFree(deg);
@@ -115,6 +117,42 @@ sgnn_status cache_create(const sgnn_csr* a_hat, int use_cache, sgnn_cache_s** ou
 }
 
 void cache_destroy(sgnn_cache_s* c) { delete c; }
+
+// build_cache (gnn.hpp:180-196): GCN normalizes (counted), others borrow A.
+sgnn_status cache_create_model(const sgnn_csr* a, int model_kind, int use_cache, int add_loops,
+                               sgnn_cache_s** out, cudaStream_t s) {
+    *out = nullptr;
+    SGNN_TRY(check_csr(a, "build_cache"));
+    if (a->n_rows != a->n_cols)
+        return fail(SGNN_ERR_SHAPE, "build_cache: adjacency is " + std::to_string(a->n_rows) + "x" +
+                                        std::to_string(a->n_cols) + ", expected square");
+    if (model_kind < 0 || model_kind > 3) return fail(SGNN_ERR_CONFIG, "build_cache: unknown model kind");
+    if (model_kind != 0) return cache_create(a, use_cache, out, s);
+    DevCsr norm;
+    uint64_t nnz = 0;
+    SGNN_TRY(run_normalize(a, add_loops, &nnz, nullptr, nullptr, nullptr, s));
+    SGNN_TRY(norm.alloc(a->n_rows, nnz, true));
+    sgnn_status st = run_normalize(a, add_loops, &nnz, norm.rp, norm.ci, norm.v, s);
+    if (st != SGNN_OK) {
+        norm.release();
+        return st;
+    }
+    sgnn_csr ah = view(a->n_rows, a->n_cols, nnz, norm.rp, norm.ci, norm.v);
+    st = cache_create(&ah, use_cache, out, s);
+    if (st != SGNN_OK) {
+        norm.release();
+        return st;
+    }
+    (*out)->own = norm;  // the cache owns A_hat from here on
+    norm.mem = nullptr;
+    (*out)->normalize_builds = 1;  // gnn.hpp:189
+    return SGNN_OK;
+}
+
+sgnn_status cache_a_hat(sgnn_cache_s* c, sgnn_csr* out) {
+    *out = c->a_hat;
+    return SGNN_OK;
+}
 
 // gnn.hpp:127-144
 sgnn_status cache_sum_operand(sgnn_cache_s* c, sgnn_csr* out, cudaStream_t s) {

@@ -208,6 +208,29 @@ sgnn_status sgnn_cache_create(const sgnn_csr* a_hat, int use_cache, sgnn_cache* 
     }
 }
 
+sgnn_status sgnn_normalize_adjacency(const sgnn_csr* a, int add_self_loops, uint64_t* out_nnz,
+                                     uint64_t* t_row_ptr, uint32_t* t_col_idx, float* t_values,
+                                     sgnn_stream stream) {
+    SGNN_TRY(check_csr(a, "normalize_adjacency"));
+    if (!out_nnz) return fail(SGNN_ERR_CONFIG, "normalize_adjacency: null out_nnz");
+    return run_normalize(a, add_self_loops, out_nnz, t_row_ptr, t_col_idx, t_values, cs(stream));
+}
+
+sgnn_status sgnn_cache_create_model(const sgnn_csr* a, int model_kind, int use_cache,
+                                    int add_self_loops, sgnn_cache* out, sgnn_stream stream) {
+    if (!out) return fail(SGNN_ERR_CONFIG, "build_cache: null out");
+    try {
+        return cache_create_model(a, model_kind, use_cache, add_self_loops, out, cs(stream));
+    } catch (const std::bad_alloc&) {
+        return fail(SGNN_ERR_NOMEM, "build_cache: host allocation failed");
+    }
+}
+
+sgnn_status sgnn_cache_a_hat(sgnn_cache cache, sgnn_csr* out) {
+    if (!cache || !out) return fail(SGNN_ERR_CONFIG, "cache_a_hat: null argument");
+    return cache_a_hat(cache, out);
+}
+
 sgnn_status sgnn_cache_destroy(sgnn_cache cache) {
     cache_destroy(cache);
     return SGNN_OK;

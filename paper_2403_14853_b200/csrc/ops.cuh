@@ -16,6 +16,13 @@ sgnn_status cache_mean_operand(sgnn_cache_s* c, sgnn_csr* out, cudaStream_t s);
 sgnn_status cache_spmm_backward(sgnn_cache_s* c, const float* dc, uint32_t dc_rows, uint32_t k,
                                 float* dx, int reduce, cudaStream_t s);
 sgnn_status cache_counters(sgnn_cache_s* c, uint64_t* tb, uint64_t* nb, uint64_t* hits, int* sym);
+sgnn_status cache_create_model(const sgnn_csr* a, int model_kind, int use_cache, int add_loops,
+                               sgnn_cache_s** out, cudaStream_t s);
+sgnn_status cache_a_hat(sgnn_cache_s* c, sgnn_csr* out);
+
+// normalize_adjacency (normalize.cu); trp == nullptr -> count only.
+sgnn_status run_normalize(const sgnn_csr* a, int add_loops, uint64_t* out_nnz, uint64_t* trp,
+                          uint32_t* tci, float* tv, cudaStream_t s);
 
 sgnn_status run_spmm(const sgnn_csr* a, const float* x, uint32_t k, float* c, int reduce,
                      const sgnn_plan_s* plan, cudaStream_t s);

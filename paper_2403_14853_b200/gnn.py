@@ -1,0 +1,257 @@
+"""GNN layer glue on the device -- the callers of the hot path
+(gnn.hpp:75-438: init_model, forward, backward, softmax_xent, masked_accuracy,
+sgd_step, train).  Every propagation is the B200 SpMM; every backward
+propagation goes through the device TrainingCache (cached CSC / symmetric
+short-circuit / 1/deg-scaled mean operand).  Dense products use torch
+(cuBLAS SGEMM, TF32 disabled) and are outside the sparse hot path (north_star:
+"any dense X·W ... is timed separately").
+"""
+from __future__ import annotations
+
+import time
+from dataclasses import dataclass, field
+
+import numpy as np
+import torch
+
+from . import ops
+
+torch.backends.cuda.matmul.allow_tf32 = False
+torch.backends.cudnn.allow_tf32 = False
+
+KINDS = ("gcn", "sage-sum", "sage-mean", "gin")
+
+
+@dataclass
+class GnnModel:
+    """GnnModel (gnn.hpp:40-63)."""
+    kind: str
+    in_features: int
+    hidden: int
+    classes: int
+    w1: torch.Tensor
+    w2: torch.Tensor
+    w1_self: torch.Tensor | None = None
+    w2_self: torch.Tensor | None = None
+    epsilon: float = 0.0
+
+    @property
+    def has_self_weights(self):
+        return self.kind in ("sage-sum", "sage-mean")
+
+    @property
+    def reduce(self):
+        return "mean" if self.kind == "sage-mean" else "sum"
+
+    def params(self):
+        out = [self.w1, self.w2]
+        if self.has_self_weights:
+            out += [self.w1_self, self.w2_self]
+        return out
+
+
+@dataclass
+class Gradients:
+    w1: torch.Tensor
+    w2: torch.Tensor
+    w1_self: torch.Tensor | None = None
+    w2_self: torch.Tensor | None = None
+    epsilon: float = 0.0
+
+
+def init_model(kind, in_features, hidden, classes, seed=1, device="cuda") -> GnnModel:
+    """Glorot-uniform init (gnn.hpp:75-99 fill order w1, w2, w1_self, w2_self)."""
+    if kind not in KINDS:
+        raise ops.ConfigError(f"unknown model '{kind}' (expected gcn|sage-sum|sage-mean|gin)")
+    if not (in_features and hidden and classes):
+        raise ops.ConfigError("init_model: in_features, hidden, and classes must be positive")
+    g = torch.Generator(device="cpu").manual_seed(seed)
+
+    def glorot(r, c):
+        lim = float(np.sqrt(6.0 / (r + c)))
+        return ((torch.rand((r, c), generator=g, dtype=torch.float64) * 2 - 1) * lim).float().to(device)
+
+    m = GnnModel(kind, in_features, hidden, classes, glorot(in_features, hidden), glorot(hidden, classes))
+    if m.has_self_weights:
+        m.w1_self, m.w2_self = glorot(in_features, hidden), glorot(hidden, classes)
+    return m
+
+
+def model_from_flat(kind, in_features, hidden, classes, flat, device="cuda") -> GnnModel:
+    """Weights packed w1|w2|(w1_self|w2_self) (the reference's init order)."""
+    flat = np.asarray(flat, np.float32)
+    o = 0
+
+    def take(r, c):
+        nonlocal o
+        t = torch.from_numpy(flat[o:o + r * c].reshape(r, c).copy()).to(device)
+        o += r * c
+        return t
+
+    m = GnnModel(kind, in_features, hidden, classes, take(in_features, hidden), take(hidden, classes))
+    if m.has_self_weights:
+        m.w1_self, m.w2_self = take(in_features, hidden), take(hidden, classes)
+    return m
+
+
+def flat_weights(m: GnnModel) -> np.ndarray:
+    return np.concatenate([p.detach().cpu().numpy().ravel() for p in m.params()])
+
+
+@dataclass
+class Tape:
+    """Tape (gnn.hpp:199-207)."""
+    n_nodes: int
+    x: torch.Tensor
+    h1: torch.Tensor | None = None
+    a1: torch.Tensor | None = None
+    a2: torch.Tensor | None = None
+
+
+def build_cache(kind, a: ops.CsrMatrix, use_cache=True, add_self_loops=True) -> ops.TrainingCache:
+    """build_cache (gnn.hpp:180-196) on the device."""
+    return ops.TrainingCache(a, use_cache, model_kind=kind, add_self_loops=add_self_loops)
+
+
+def _relu_backward(grad, act):
+    return torch.where(act <= 0, torch.zeros_like(grad), grad)
+
+
+def forward(model: GnnModel, cache: ops.TrainingCache, x: torch.Tensor):
+    """forward (gnn.hpp:212-256)."""
+    a_hat = cache.a_hat
+    if x.shape[0] != a_hat.n_rows:
+        raise ops.ShapeError(f"forward: features have {x.shape[0]} rows but graph has {a_hat.n_rows} nodes")
+    if x.shape[1] != model.in_features:
+        raise ops.ShapeError(f"forward: features have {x.shape[1]} columns but model expects {model.in_features}")
+    tape = Tape(x.shape[0], x)
+    if model.kind == "gcn":
+        z1 = x @ model.w1
+        tape.h1 = torch.relu(ops.spmm(a_hat, z1, "sum"))
+        logits = ops.spmm(a_hat, tape.h1 @ model.w2, "sum")
+    elif model.kind in ("sage-sum", "sage-mean"):
+        red = model.reduce
+        tape.a1 = ops.spmm(a_hat, x, red)
+        z1 = tape.a1 @ model.w1 + x @ model.w1_self
+        tape.h1 = torch.relu(z1)
+        tape.a2 = ops.spmm(a_hat, tape.h1, red)
+        logits = tape.a2 @ model.w2 + tape.h1 @ model.w2_self
+    else:  # gin
+        scale = 1.0 + model.epsilon
+        tape.a1 = scale * x + ops.spmm(a_hat, x, "sum")
+        tape.h1 = torch.relu(tape.a1 @ model.w1)
+        tape.a2 = scale * tape.h1 + ops.spmm(a_hat, tape.h1, "sum")
+        logits = tape.a2 @ model.w2
+    return logits, tape
+
+
+def backward(model: GnnModel, cache: ops.TrainingCache, tape: Tape, grad: torch.Tensor) -> Gradients:
+    """backward (gnn.hpp:261-313); propagation transposes come from the cache."""
+    if tape.n_nodes != cache.a_hat.n_rows or grad.shape[0] != tape.n_nodes:
+        raise ops.TapeError(f"backward: tape covers {tape.n_nodes} nodes but graph/gradient expects "
+                            f"{cache.a_hat.n_rows}/{grad.shape[0]}")
+    if grad.shape[1] != model.classes:
+        raise ops.TapeError(f"backward: grad_logits has {grad.shape[1]} columns, model has {model.classes} classes")
+    if model.kind == "gcn":
+        at = cache.sum_operand()  # fetched once per backward, used twice (gnn.hpp:274-279)
+        dz2 = ops.spmm(at, grad.contiguous(), "sum")
+        g = Gradients(None, tape.h1.T @ dz2)
+        dp1 = _relu_backward(dz2 @ model.w2.T, tape.h1)
+        dz1 = ops.spmm(at, dp1.contiguous(), "sum")
+        g.w1 = tape.x.T @ dz1
+        return g
+    if model.kind in ("sage-sum", "sage-mean"):
+        g = Gradients(None, tape.a2.T @ grad, None, tape.h1.T @ grad)
+        ds2 = (grad @ model.w2.T).contiguous()
+        dh1 = cache.spmm_backward(ds2, model.reduce) + grad @ model.w2_self.T
+        dz1 = _relu_backward(dh1, tape.h1)
+        g.w1 = tape.a1.T @ dz1
+        g.w1_self = tape.x.T @ dz1
+        return g
+    scale = 1.0 + model.epsilon
+    g = Gradients(None, tape.a2.T @ grad)
+    dm2 = (grad @ model.w2.T).contiguous()
+    deps = float((dm2.double() * tape.h1.double()).sum())
+    dh1 = scale * dm2 + cache.spmm_backward(dm2, "sum")
+    dz1 = _relu_backward(dh1, tape.h1)
+    g.w1 = tape.a1.T @ dz1
+    dm1 = dz1 @ model.w1.T
+    deps += float((dm1.double() * tape.x.double()).sum())
+    g.epsilon = deps
+    return g
+
+
+def softmax_xent(logits: torch.Tensor, labels: torch.Tensor, mask: torch.Tensor):
+    """softmax_xent (gnn.hpp:318-349): mean -log softmax over masked rows, in double."""
+    m = mask.bool()
+    n_masked = int(m.sum())
+    if n_masked == 0:
+        raise ops.ConfigError("softmax_xent: mask selects no rows")
+    if int(labels[m].max()) >= logits.shape[1]:
+        raise ops.ConfigError("softmax_xent: label out of range")
+    ld = logits.double()
+    row_max = ld.max(dim=1, keepdim=True).values
+    ex = torch.exp(ld - row_max)
+    denom = ex.sum(dim=1, keepdim=True)
+    lab = labels.long()
+    loss_rows = (row_max.squeeze(1) + torch.log(denom.squeeze(1))) - ld.gather(1, lab[:, None]).squeeze(1)
+    loss = float(loss_rows[m].sum()) / n_masked
+    p = ex / denom
+    onehot = torch.zeros_like(p)
+    onehot.scatter_(1, lab[:, None], 1.0)
+    grad = ((p - onehot) * (1.0 / n_masked)).float()
+    grad[~m] = 0
+    return loss, grad
+
+
+def masked_accuracy(logits, labels, mask) -> float:
+    """masked_accuracy (gnn.hpp:353-370); ties take the smallest class."""
+    m = mask.bool()
+    if int(m.sum()) == 0:
+        return 0.0
+    pred = logits.argmax(dim=1)
+    return float((pred[m] == labels.long()[m]).double().mean())
+
+
+def sgd_step(model: GnnModel, g: Gradients, lr: float) -> None:
+    """sgd_step (gnn.hpp:374-386)."""
+    model.w1 -= lr * g.w1
+    model.w2 -= lr * g.w2
+    if model.has_self_weights:
+        model.w1_self -= lr * g.w1_self
+        model.w2_self -= lr * g.w2_self
+    if model.kind == "gin":
+        model.epsilon -= lr * g.epsilon
+
+
+@dataclass
+class EpochStats:
+    epoch: int
+    loss: float
+    train_accuracy: float
+    epoch_seconds: float
+
+
+@dataclass
+class TrainOutput:
+    stats: list = field(default_factory=list)
+    cache: ops.TrainingCache | None = None
+
+
+def train(model: GnnModel, a: ops.CsrMatrix, x: torch.Tensor, labels: torch.Tensor, mask: torch.Tensor,
+          epochs=100, lr=0.05, use_tuned=True, use_cache=True, add_self_loops=True) -> TrainOutput:
+    """train (gnn.hpp:414-438): the adjacency is prepared once (build_cache)."""
+    if epochs < 1:
+        raise ops.ConfigError("train: epochs must be >= 1")
+    out = TrainOutput(cache=build_cache(model.kind, a, use_cache, add_self_loops))
+    with ops.DispatchGuard(use_tuned):
+        for epoch in range(1, epochs + 1):
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            logits, tape = forward(model, out.cache, x)
+            loss, grad = softmax_xent(logits, labels, mask)
+            acc = masked_accuracy(logits, labels, mask)
+            sgd_step(model, backward(model, out.cache, tape, grad), lr)
+            torch.cuda.synchronize()
+            out.stats.append(EpochStats(epoch, loss, acc, time.perf_counter() - t0))
+    return out

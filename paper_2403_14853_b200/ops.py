@@ -383,19 +383,45 @@ def is_symmetric(a: CsrMatrix) -> bool:
 class TrainingCache:
     """TrainingCache<float> + build_cache (gnn.hpp:113-196) over a device a_hat."""
 
-    def __init__(self, a_hat: CsrMatrix, use_cache: bool = True):
-        if a_hat.n_rows != a_hat.n_cols:
-            raise ShapeError(f"build_cache: adjacency is {a_hat.n_rows}x{a_hat.n_cols}, expected square")
-        self.a_hat = a_hat
+    MODEL_KINDS = {"gcn": 0, "sage-sum": 1, "sage-mean": 2, "gin": 3}  # gnn.hpp:17-35
+
+    def __init__(self, a: CsrMatrix, use_cache: bool = True, model_kind: str | None = None,
+                 add_self_loops: bool = True):
+        """model_kind None: `a` is already the propagation operand a_hat.
+        Otherwise build_cache(kind, a, ...) (gnn.hpp:180-196): "gcn"
+        normalizes A on the device (normalize_builds = 1)."""
+        if a.n_rows != a.n_cols:
+            raise ShapeError(f"build_cache: adjacency is {a.n_rows}x{a.n_cols}, expected square")
+        self._a = a
         h = C.c_void_p()
-        check(lib().sgnn_cache_create(C.byref(a_hat.c()), int(bool(use_cache)), C.byref(h), _stream()),
-              "build_cache")
+        if model_kind is None:
+            check(lib().sgnn_cache_create(C.byref(a.c()), int(bool(use_cache)), C.byref(h), _stream()),
+                  "build_cache")
+        else:
+            if model_kind not in self.MODEL_KINDS:
+                raise ConfigError(f"unknown model '{model_kind}' (expected gcn|sage-sum|sage-mean|gin)")
+            check(lib().sgnn_cache_create_model(C.byref(a.c()), self.MODEL_KINDS[model_kind], int(bool(use_cache)),
+                                                int(bool(add_self_loops)), C.byref(h), _stream()), "build_cache")
         self.handle = h
+        if model_kind == "gcn":
+            cs = _lib.Csr()
+            check(lib().sgnn_cache_a_hat(self.handle, C.byref(cs)))
+            self.a_hat = _View(cs, self)
+        else:
+            self.a_hat = a
 
     def _operand(self, fn) -> CsrMatrix:
         out = _lib.Csr()
         check(fn(self.handle, C.byref(out), _stream()), "cache operand")
-        return _View(out, self)
+        # one view per device operand, so its cached plans survive across epochs
+        key = (out.row_ptr, out.col_idx, out.values, out.n_rows, out.nnz)
+        views = self.__dict__.setdefault("_views", {})
+        if key not in views:
+            if out.row_ptr == self.a_hat.c().row_ptr and out.values == self.a_hat.c().values:
+                views[key] = self.a_hat  # symmetric short-circuit: the operand is a_hat itself
+            else:
+                views[key] = _View(out, self)
+        return views[key]
 
     def sum_operand(self) -> CsrMatrix:
         return self._operand(lib().sgnn_cache_sum_operand)
@@ -455,6 +481,21 @@ class _View(CsrMatrix):
             if host.nbytes:
                 _lib.memcpy_d2h(host.ctypes.data, ptr, host.nbytes)
         return rp, ci, v
+
+
+def normalize_adjacency(a: CsrMatrix, add_self_loops: bool = True) -> CsrMatrix:
+    """normalize_adjacency (sparse.hpp:116-174) on the device, bit-exact."""
+    nnz = C.c_uint64()
+    check(lib().sgnn_normalize_adjacency(C.byref(a.c()), int(bool(add_self_loops)), C.byref(nnz),
+                                         None, None, None, _stream()), "normalize_adjacency")
+    dev = a.row_ptr.device
+    trp = torch.empty(a.n_rows + 1, dtype=torch.int64, device=dev)
+    tci = torch.empty(nnz.value, dtype=torch.int32, device=dev)
+    tv = torch.empty(nnz.value, dtype=torch.float32, device=dev)
+    check(lib().sgnn_normalize_adjacency(C.byref(a.c()), int(bool(add_self_loops)), C.byref(nnz),
+                                         trp.data_ptr(), tci.data_ptr() if nnz.value else None,
+                                         tv.data_ptr() if nnz.value else None, _stream()), "normalize_adjacency")
+    return CsrMatrix(a.n_rows, a.n_cols, trp, tci, tv)
 
 
 def sddmm(p: CsrMatrix, x: torch.Tensor, y: torch.Tensor) -> CsrMatrix:

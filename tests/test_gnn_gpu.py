@@ -1,0 +1,94 @@
+"""GNN layer glue on the device (gnn.hpp:180-438) vs the reference's own
+training runs (tests/golden/gnn_planted.npz, make_golden_gnn.py): per-epoch
+losses, cache counters, cache/dispatch transparency, device
+normalize_adjacency bit-exactness."""
+import numpy as np
+import pytest
+
+from conftest import load_golden, rand_csr
+from oracle import port
+
+pytestmark = pytest.mark.gpu
+
+HIDDEN, CLASSES, LR, EPOCHS = 32, 4, 0.05, 30
+
+
+def _setup(kind):
+    import torch
+
+    from paper_2403_14853_b200 import gnn, ops
+    g = load_golden("gnn_planted")
+    a = ops.CsrMatrix.from_numpy(g["row_ptr"], g["col_idx"], g["values"], len(g["row_ptr"]) - 1)
+    x = torch.from_numpy(g["x"]).cuda()
+    lab = torch.from_numpy(g["labels"].astype(np.int64)).cuda()
+    mask = torch.from_numpy(g["mask"]).cuda()
+    m = gnn.model_from_flat(kind, x.shape[1], HIDDEN, CLASSES, g[f"{kind}_w0"])
+    return g, a, x, lab, mask, m
+
+
+@pytest.mark.parametrize("kind", ["gcn", "sage-sum", "sage-mean", "gin"])
+def test_training_matches_reference(cuda, kind):
+    from paper_2403_14853_b200 import gnn
+    g, a, x, lab, mask, m = _setup(kind)
+    out = gnn.train(m, a, x, lab, mask, epochs=EPOCHS, lr=LR)
+    losses = np.array([s.loss for s in out.stats])
+    want = g[f"{kind}_losses"]
+    np.testing.assert_allclose(losses, want, rtol=2e-3, atol=1e-4)
+    c = out.cache.counters
+    assert [c["transpose_builds"], c["normalize_builds"], c["cache_hits"]] == [int(v) for v in g[f"{kind}_counters"]]
+    assert abs(out.stats[-1].train_accuracy - g[f"{kind}_accs"][-1]) <= 0.02
+
+
+@pytest.mark.parametrize("kind", ["gcn", "sage-mean"])
+def test_cache_and_dispatch_transparency(cuda, kind):
+    """use_cache / use_tuned on vs off give bitwise-identical losses."""
+    from paper_2403_14853_b200 import gnn
+    g, a, x, lab, mask, m0 = _setup(kind)
+    runs = {}
+    for use_cache, use_tuned in ((True, True), (False, True), (True, False)):
+        m = gnn.model_from_flat(kind, x.shape[1], HIDDEN, CLASSES, g[f"{kind}_w0"])
+        out = gnn.train(m, a, x, lab, mask, epochs=10, lr=LR, use_cache=use_cache, use_tuned=use_tuned)
+        runs[(use_cache, use_tuned)] = ([s.loss for s in out.stats], out.cache.counters)
+    base = runs[(True, True)][0]
+    assert runs[(False, True)][0] == base and runs[(True, False)][0] == base
+    assert runs[(False, True)][1]["transpose_builds"] == int(g[f"{kind}_counters_nocache"][0]) * 10 // EPOCHS
+
+
+def test_device_normalize_adjacency_bitexact(cuda):
+    from paper_2403_14853_b200 import graphs, ops
+    g = load_golden("gnn_planted")
+    for rp, ci, v in ((g["row_ptr"], g["col_idx"], g["values"]),):
+        a = ops.CsrMatrix.from_numpy(rp, ci, v, len(rp) - 1)
+        for loops in (True, False):
+            got = ops.normalize_adjacency(a, loops).to_numpy()
+            want = port.normalize_adjacency(rp, ci, v, loops)
+            for p, q in zip(got, want):
+                np.testing.assert_array_equal(np.asarray(p).view(np.uint8), np.asarray(q).view(np.uint8))
+    # weighted, with existing diagonals and empty rows; R-MAT with hubs
+    rng = np.random.default_rng(2)
+    rp, ci, v = rand_csr(rng, 700, 700, 0.01, hub_rows=(3,), empty_frac=0.2, value="positive")
+    a = ops.CsrMatrix.from_numpy(rp, ci, v, 700)
+    got = ops.normalize_adjacency(a, True).to_numpy()
+    for p, q in zip(got, port.normalize_adjacency(rp, ci, v, True)):
+        np.testing.assert_array_equal(np.asarray(p).view(np.uint8), np.asarray(q).view(np.uint8))
+    rp, ci = graphs.rmat(12, 4096 * 12, seed=9, symmetrize=True)
+    v = np.ones(len(ci), np.float32)
+    got = ops.normalize_adjacency(ops.CsrMatrix.from_numpy(rp, ci, v, 4096), True).to_numpy()
+    for p, q in zip(got, port.normalize_adjacency(rp, ci, v, True)):
+        np.testing.assert_array_equal(np.asarray(p).view(np.uint8), np.asarray(q).view(np.uint8))
+    with pytest.raises(ops.ConfigError):
+        ops.normalize_adjacency(ops.CsrMatrix.from_numpy(np.array([0, 1], np.uint64), np.array([0], np.uint32),
+                                                         np.array([-1.0], np.float32), 1))
+
+
+def test_tape_and_shape_errors(cuda):
+    import torch
+
+    from paper_2403_14853_b200 import gnn, ops
+    g, a, x, lab, mask, m = _setup("gcn")
+    cache = gnn.build_cache("gcn", a)
+    with pytest.raises(ops.ShapeError):
+        gnn.forward(m, cache, x[:10])
+    logits, tape = gnn.forward(m, cache, x)
+    with pytest.raises(ops.TapeError):
+        gnn.backward(m, cache, tape, torch.zeros(10, CLASSES, device="cuda"))
