@@ -32,6 +32,8 @@ import sys
 import threading
 import time
 
+import numpy as np
+
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
@@ -49,6 +51,9 @@ def parse():
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--plan", type=str, default="", help="JSON plan params override")
+    p.add_argument("--workload", choices=("cfg2", "cfg3", "cfg4", "cfg5"), default="cfg2",
+                   help="cfg2 (default, the headline) | cfg3 GCN layer | cfg4 FusedMM/SDDMM | "
+                        "cfg5 row-partitioned GraphSAGE-mean step")
     return p.parse_args()
 
 
@@ -457,12 +462,212 @@ def run_reference(args):
     print(json.dumps(out), flush=True)
 
 
+# ------------------------------------------------------- secondary workloads
+def _events_time(fn, steps, warmup, flush=None):
+    """Per-step CUDA-event times (flush outside the events), ms list."""
+    import torch
+    for _ in range(max(3, warmup)):
+        if flush is not None:
+            flush.zero_()
+        fn()
+    torch.cuda.synchronize()
+    out = []
+    for _ in range(steps):
+        if flush is not None:
+            flush.zero_()
+        s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        s.record()
+        fn()
+        e.record()
+        out.append((s, e))
+    torch.cuda.synchronize()
+    return [s.elapsed_time(e) for s, e in out]
+
+
+def _base_line(args, ws, value, ms, config, extra):
+    peak, src = peaks()
+    line = {"metric": METRIC, "value": round(value, 2), "unit": "GFLOP/s", "n_gpus": ws, "steps": args.steps,
+            "warmup": max(3, args.warmup), "ms_per_step": round(ms, 4), "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+            "data": "synthetic (seeded R-MAT, BASELINE shapes; paper datasets not available offline)",
+            "config": config}
+    line.update(extra)
+    if "roofline" in line:
+        line["roofline"].update({"peak": peak, "peak_source": src,
+                                 "frac": round(line["roofline"]["achieved"] / peak, 4)})
+    return line
+
+
+def run_cfg4(args):
+    """FusedMM (sigmoid edge op, sum) + SDDMM alone on cfg4."""
+    import torch
+
+    from paper_2403_14853_b200 import graphs, ops
+    torch.cuda.set_device(0)
+    w = graphs.cfg4(args.seed)
+    m, nnz, k = w.n_rows, w.nnz, w.k
+    p = ops.CsrMatrix.from_numpy(w.row_ptr, w.col_idx, w.values, w.n_cols)
+    x = torch.from_numpy(graphs.normal(m * k, 0, 0.1, args.seed, 41).reshape(m, k)).cuda()
+    y = torch.from_numpy(graphs.normal(w.n_cols * k, 0, 0.1, args.seed, 42).reshape(w.n_cols, k)).cuda()
+    out = torch.empty(m, k, device="cuda")
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
+    plan = p.plan(k, "fused")
+    with ClockSampler(0) as clk:
+        tf = _events_time(lambda: ops.fusedmm(p, x, y, "sigmoid_mul", "sum", out, plan=plan), args.steps, args.warmup, flush)
+    ts = _events_time(lambda: ops.sddmm(p, x, y), max(5, args.steps // 4), args.warmup, flush)
+    mf, msd = sum(tf) / len(tf), sum(ts) / len(ts)
+    fu_bytes = 8 * (m + 1) + 8 * nnz + 8 * m * k + 4 * nnz * k
+    sd_bytes = 8 * (m + 1) + 8 * nnz + 4 * m * k + 4 * nnz * k + 4 * nnz
+    cfg = {"workload": "cfg4: FusedMM e_ij = sigmoid(<X_i,Y_j>) a_ij, out = sum_j e_ij Y_j; R-MAT 2^20, N*32 "
+                       "samples, dedup", "n_rows": m, "nnz": nnz, "K": k, "a_ij": "U[0,1]", "X,Y": "N(0,0.1)",
+           "l2": "flushed between steps (256 MiB write), flush not timed", "plan": plan.params}
+    line = _base_line(args, 1, 2 * nnz * k / mf / 1e6, mf, cfg, {
+        "roofline": {"bound": "hbm", "achieved": round(fu_bytes / mf / 1e6, 1), "unit": "GB/s",
+                     "traffic": (load_traffic("cfg4") or None), "alg_bytes_per_step": fu_bytes},
+        "gflops_4nnzK": round(4 * nnz * k / mf / 1e6, 1),
+        "sddmm": {"ms": round(msd, 4), "GFLOP/s": round(2 * nnz * k / msd / 1e6, 1),
+                  "achieved_GBps": round(sd_bytes / msd / 1e6, 1)},
+        "gpu_launches": args.steps * (2 if plan.stats["split_rows"] else 1)})
+    line["clocks"] = clk.summary()
+    print(json.dumps(line), flush=True)
+
+
+def run_cfg3(args):
+    """GCN layer fwd + bwd: A_hat (device normalize), SpMM(A_hat, H W) and
+    A_hat^T G (symmetric: the cached operand is A_hat), dense GEMMs timed apart."""
+    import torch
+
+    from paper_2403_14853_b200 import gnn, graphs, ops
+    torch.cuda.set_device(0)
+    rp, ci = graphs.cfg3_graph(args.seed)
+    n, k = len(rp) - 1, 256
+    a = ops.CsrMatrix.from_numpy(rp, ci, np.ones(len(ci), np.float32), n)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    cache = gnn.build_cache("gcn", a, True)
+    e1.record()
+    torch.cuda.synchronize()
+    build_ms = e0.elapsed_time(e1)
+    a_hat = cache.a_hat
+    nnz = a_hat.nnz
+    h = torch.from_numpy(graphs.normal(n * k, 0, 1, args.seed, 31).reshape(n, k)).cuda()
+    lim = float(np.sqrt(6.0 / 512))
+    wt = (torch.rand(k, k, generator=torch.Generator().manual_seed(args.seed)) * 2 - 1).mul(lim).cuda()
+    g = torch.from_numpy(graphs.normal(n * k, 0, 1, args.seed, 32).reshape(n, k)).cuda()
+    hw = h @ wt
+    out = torch.empty(n, k, device="cuda")
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
+    plan = a_hat.plan(k)
+
+    def sparse():
+        ops.spmm_plan(a_hat, hw, "sum", plan, out)          # forward propagation
+        cache.spmm_backward(g, "sum", out)                   # A_hat^T G (symmetric short-circuit)
+
+    def dense():
+        torch.matmul(h, wt, out=hw)
+        _ = h.T @ out
+
+    with ClockSampler(0) as clk:
+        tsp = _events_time(sparse, args.steps, args.warmup, flush)
+    tde = _events_time(dense, max(5, args.steps // 4), args.warmup, flush)
+    ms_sp, ms_de = sum(tsp) / len(tsp), sum(tde) / len(tde)
+    by = 2 * spmm_bytes(n, nnz, k)
+    cfg = {"workload": "cfg3: GCN layer fwd+bwd, A_hat = D^-1/2(A+I)D^-1/2 of R-MAT 2^20 avg-deg 50 symmetrised; "
+                       "sparse = SpMM(A_hat, HW) + A_hat^T G; dense HW, H^T(A_hat^T G) cuBLAS SGEMM timed apart",
+           "n_rows": n, "nnz": nnz, "K": k, "l2": "flushed between steps, flush not timed", "plan": plan.params}
+    line = _base_line(args, 1, 2 * 2 * nnz * k / ms_sp / 1e6, ms_sp, cfg, {
+        "roofline": {"bound": "hbm", "achieved": round(by / ms_sp / 1e6, 1), "unit": "GB/s",
+                     "traffic": load_traffic("cfg3"), "alg_bytes_per_step": by},
+        "dense_ms": round(ms_de, 4), "layer_ms": round(ms_sp + ms_de, 4),
+        "normalize_and_cache_ms": round(build_ms, 3), "cache_counters": cache.counters,
+        "gpu_launches": args.steps * 4})
+    line["clocks"] = clk.summary()
+    print(json.dumps(line), flush=True)
+
+
+def run_cfg5(args):
+    """2-layer GraphSAGE-mean training step, rows partitioned over the ranks
+    (NCCL all-gather of feature blocks, all-reduce of weight gradients)."""
+    import torch
+
+    from paper_2403_14853_b200 import graphs, partition, sage_dist
+    ws, rank, local = dist_env()
+    torch.cuda.set_device(local)
+    dist = None
+    if ws > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    dev = torch.device("cuda", local)
+    w = graphs.cfg5(args.seed)
+    n, k, hidden, classes = w.n_rows, w.k, 128, 16
+    ex = partition.NcclExchange() if ws > 1 else _LocalExchange()
+    ar = (lambda t: (dist.all_reduce(t), t)[1]) if ws > 1 else (lambda t: t)
+    ds = sage_dist.DistSage(w.row_ptr, w.col_idx, w.values, ws, rank, k, hidden, classes, "mean",
+                            device=dev, exchange=ex, allreduce=ar)
+    r0, r1 = ds.r0, ds.r1
+    x = torch.from_numpy(graphs.normal(n * k, 0, 1, args.seed, 51).reshape(n, k)[r0:r1].copy()).to(dev)
+    labels_all = (np.arange(n) * 2654435761 % classes).astype(np.int64)  # uniform labels (cfg5)
+    lab = torch.from_numpy(labels_all[r0:r1].copy()).to(dev)
+    mask = torch.ones(r1 - r0, dtype=torch.uint8, device=dev)
+    gen = torch.Generator().manual_seed(args.seed)
+
+    def glorot(r, c):
+        return ((torch.rand(r, c, generator=gen, dtype=torch.float64) * 2 - 1) * np.sqrt(6.0 / (r + c))).float().to(dev)
+    params = sage_dist.SageParams(glorot(k, hidden), glorot(hidden, classes), glorot(k, hidden), glorot(hidden, classes))
+    steps = max(3, min(args.steps, 20))
+    for _ in range(max(3, args.warmup)):
+        ds.step(params, x, lab, mask, 0.05, n)
+    torch.cuda.synchronize()
+    if dist:
+        dist.barrier()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clk:
+        e0.record()
+        for _ in range(steps):
+            loss = ds.step(params, x, lab, mask, 0.05, n)
+        e1.record()
+        torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1) / steps
+    if dist:
+        t = torch.tensor([ms], device=dev, dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    nnz = w.nnz
+    flops = 3 * 2 * nnz * k  # 2 forward + 1 backward SpMM (gnn.hpp:237,241,290)
+    cfg = {"workload": "cfg5: 2-layer GraphSAGE-mean training step, R-MAT 2^22 avg-deg 50 symmetrised + self "
+                       "loops (dedup), X N(0,1) 2^22x128, hidden 128, 16 classes, uniform labels",
+           "n_rows": n, "nnz": nnz, "K": k, "parallelism": f"1D row partition x{ws} (nnz-balanced), "
+           "all-gather of feature blocks", "partition_bounds": [int(b) for b in ds.part.bounds]}
+    line = _base_line(args, ws, flops / ms / 1e6, ms, cfg, {
+        "epoch_ms": round(ms, 3), "loss": loss, "scaling": "strong", "gpu_launches": steps * 12})
+    line["steps"] = steps
+    line["clocks"] = clk.summary()
+    if dist:
+        dist.barrier()
+        dist.destroy_process_group()
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+
+
+class _LocalExchange:
+    """World size 1: the gathered buffer is the block itself."""
+
+    def all_gather(self, block):
+        return block
+
+
 def main():
     args = parse()
     if args.impl == "reference":
         run_reference(args)
-    else:
+    elif args.workload == "cfg2":
         run_ours(args)
+    elif args.workload == "cfg3":
+        run_cfg3(args)
+    elif args.workload == "cfg4":
+        run_cfg4(args)
+    else:
+        run_cfg5(args)
 
 
 if __name__ == "__main__":

@@ -259,6 +259,24 @@ void ref_bench_free(void* h) { delete static_cast<RefBench*>(h); }
 
 int ref_hw_cores() { return detect_hardware().cores; }
 
+// load_report (src/report.cpp:76-145): parses `path` with the reference's own
+// loader; returns 0 and best_k / #entries / #skipped, or a status (6 = ParseError).
+int ref_load_report(const char* path, uint32_t* best_k, uint32_t* n_entries, uint32_t* n_skipped) {
+    try {
+        auto r = load_report(path);
+        *best_k = r.best_k;
+        *n_entries = uint32_t(r.entries.size());
+        *n_skipped = uint32_t(r.skipped.size());
+        return 0;
+    } catch (const ParseError&) {
+        return 6;
+    } catch (const IoError&) {
+        return 5;
+    } catch (const std::exception& e) {
+        return status_of(e);
+    }
+}
+
 // ---- GNN training (gnn.hpp:75-438), the callers of the hot path --------------
 // init_model (gnn.hpp:75-99): writes w1, w2 (and w1_self, w2_self for SAGE) in
 // that order into `out` (sizes in*h, h*c, in*h, h*c).

@@ -1,0 +1,104 @@
+"""Row-partitioned 2-layer GraphSAGE training step over P ranks (BASELINE cfg5,
+SURVEY 8e): the hot path (SpMM fwd x2, SpMM bwd x1 through the mean operand)
+on each rank's row block, the all-gather of feature blocks as the only
+sparse-path exchange, and an all-reduce of the dense weight gradients and the
+loss.  Mirrors gnn.hpp:234-244 (forward), :283-296 (backward), :318-349
+(softmax_xent), :374-386 (sgd_step); with one rank it is exactly gnn.train's
+step.
+
+Ranks are torch.distributed processes (NCCL on the B200 box, gloo on CPU for
+the tests); the local SpMM is the B200 kernel (or an injected `compute` on
+CPU tests).
+"""
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+
+from . import partition
+
+
+def mean_operand_values(row_ptr, col_idx, values):
+    """Values of TrainingCache::mean_operand for a symmetric graph
+    (gnn.hpp:152-159): v / deg[col], IEEE fp32 divide."""
+    deg = np.diff(np.asarray(row_ptr, np.uint64).astype(np.int64)).astype(np.float32)
+    return (np.asarray(values, np.float32) / deg[np.asarray(col_idx, np.int64)]).astype(np.float32)
+
+
+@dataclass
+class SageParams:
+    w1: torch.Tensor
+    w2: torch.Tensor
+    w1_self: torch.Tensor
+    w2_self: torch.Tensor
+
+
+class DistSage:
+    """One rank of the partitioned SAGE (sum or mean) trainer."""
+
+    def __init__(self, row_ptr, col_idx, values, n_parts, rank, k_in, hidden, classes, reduce="mean",
+                 device="cuda", exchange=None, allreduce=None, compute=None, symmetric=True):
+        if not symmetric:
+            raise NotImplementedError("the partitioned backward uses the symmetric short-circuit "
+                                      "(gnn.hpp:152-153); cfg5 is symmetric")
+        self.reduce = reduce
+        self.part = partition.make_partition(row_ptr, n_parts)
+        self.rank = rank
+        self.r0, self.r1 = self.part.rows(rank)
+        self.device = device
+        self.exchange = exchange or partition.NcclExchange()
+        self.allreduce = allreduce or _nccl_allreduce
+        bwd_vals = mean_operand_values(row_ptr, col_idx, values) if reduce == "mean" else values
+        self.fwd = partition.PartitionedSpmm(row_ptr, col_idx, values, self.part, rank, k_in, device, compute)
+        self.fwd2 = self.fwd if hidden == k_in else partition.PartitionedSpmm(
+            row_ptr, col_idx, values, self.part, rank, hidden, device, compute)
+        self.bwd = partition.PartitionedSpmm(row_ptr, col_idx, bwd_vals, self.part, rank, hidden, device, compute)
+        self.hidden, self.classes = hidden, classes
+
+    def step(self, params: SageParams, x_local, labels_local, mask_local, lr, n_masked_total):
+        """One training step; returns the global mean loss."""
+        red = self.reduce
+        ex = self.exchange
+        # forward (gnn.hpp:236-244)
+        a1 = self.fwd.forward(x_local, ex, red)
+        z1 = a1 @ params.w1 + x_local @ params.w1_self
+        h1 = torch.relu(z1)
+        a2 = self.fwd2.forward(h1, ex, red)
+        logits = a2 @ params.w2 + h1 @ params.w2_self
+        # softmax_xent over the global mask (gnn.hpp:318-349)
+        ld = logits.double()
+        row_max = ld.max(dim=1, keepdim=True).values
+        e = torch.exp(ld - row_max)
+        denom = e.sum(dim=1, keepdim=True)
+        lab = labels_local.long()
+        m = mask_local.bool()
+        loss_rows = (row_max.squeeze(1) + torch.log(denom.squeeze(1))) - ld.gather(1, lab[:, None]).squeeze(1)
+        loss_sum = loss_rows[m].sum().reshape(1)
+        onehot = torch.zeros_like(e)
+        onehot.scatter_(1, lab[:, None], 1.0)
+        grad = ((e / denom - onehot) * (1.0 / n_masked_total)).float()
+        grad[~m] = 0
+        # backward (gnn.hpp:283-296); dense weight gradients are all-reduced
+        g_w2 = a2.T @ grad
+        g_w2s = h1.T @ grad
+        ds2 = grad @ params.w2.T
+        dh1 = self.bwd.forward(ds2, ex, "sum") + grad @ params.w2_self.T
+        dz1 = torch.where(h1 <= 0, torch.zeros_like(dh1), dh1)
+        g_w1 = a1.T @ dz1
+        g_w1s = x_local.T @ dz1
+        flat = self.allreduce(torch.cat([g_w1.ravel(), g_w2.ravel(), g_w1s.ravel(), g_w2s.ravel()]))
+        loss_sum = self.allreduce(loss_sum)  # double, like the reference's accumulation
+        sizes = [g_w1.numel(), g_w2.numel(), g_w1s.numel(), g_w2s.numel()]
+        o = 0
+        for p, g, n in zip((params.w1, params.w2, params.w1_self, params.w2_self), (g_w1, g_w2, g_w1s, g_w2s), sizes):
+            p -= lr * flat[o:o + n].reshape(g.shape)
+            o += n
+        return float(loss_sum[0]) / n_masked_total
+
+
+def _nccl_allreduce(t):
+    import torch.distributed as dist
+    dist.all_reduce(t)
+    return t

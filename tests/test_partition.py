@@ -94,6 +94,60 @@ def test_two_rank_gloo_matches_single_process(reduce):
     np.testing.assert_array_equal(got.view(np.uint32), want.view(np.uint32))
 
 
+def _sage_worker(rank, world, port_, q):
+    import torch
+    import torch.distributed as dist
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port_))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from conftest import load_golden
+
+        from paper_2403_14853_b200 import partition, sage_dist
+        g = load_golden("gnn_planted")
+        rp, ci, v, x = g["row_ptr"], g["col_idx"], g["values"], g["x"]
+        n, f = x.shape
+        hidden, classes = 32, 4
+        ds = sage_dist.DistSage(rp, ci, v, world, rank, f, hidden, classes, "mean", device="cpu",
+                                exchange=partition.NcclExchange(), compute=_oracle_compute)
+        w0 = g["sage-mean_w0"]
+        o = [0]
+
+        def take(r, c):
+            t = torch.from_numpy(w0[o[0]:o[0] + r * c].reshape(r, c).copy())
+            o[0] += r * c
+            return t
+        params = sage_dist.SageParams(take(f, hidden), take(hidden, classes), take(f, hidden), take(hidden, classes))
+        r0, r1 = ds.r0, ds.r1
+        xl = torch.from_numpy(x[r0:r1].copy())
+        lab = torch.from_numpy(g["labels"][r0:r1].astype(np.int64))
+        mask = torch.from_numpy(g["mask"][r0:r1].copy())
+        losses = [ds.step(params, xl, lab, mask, 0.05, int(g["mask"].sum())) for _ in range(6)]
+        if rank == 0:
+            q.put(losses)
+    finally:
+        dist.destroy_process_group()
+
+
+def test_two_rank_sage_mean_step_matches_reference():
+    """The partitioned SAGE-mean step (gloo, 2 ranks, oracle SpMM) reproduces
+    the reference's own training losses (tests/golden/gnn_planted.npz)."""
+    import torch.multiprocessing as mp
+
+    from conftest import load_golden
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port_ = _free_port()
+    procs = [ctx.Process(target=_sage_worker, args=(r, 2, port_, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    losses = q.get(timeout=180)
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    want = load_golden("gnn_planted")["sage-mean_losses"][:6]
+    np.testing.assert_allclose(losses, want, rtol=2e-3, atol=1e-5)
+
+
 @pytest.mark.gpu
 @pytest.mark.parametrize("parts", [1, 2, 3, 8])
 def test_loopback_partition_bitwise_equals_single_gpu(cuda, parts):
