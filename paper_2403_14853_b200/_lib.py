@@ -11,7 +11,7 @@ import os
 import threading
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libsgnn_b200.so")
+LIB_PATH = os.environ.get("SGNN_B200_LIB") or os.path.join(_HERE, "libsgnn_b200.so")
 HOST_LIB_PATH = os.path.join(_HERE, "libsgnn_host.so")
 
 # ---- status codes <-> reference exception classes (error.hpp:9-61) ----------

@@ -59,6 +59,9 @@ template <int RED>
 struct Reducer {
     // a*x folded into acc; `first` marks the first element of a segment.
     static __device__ __forceinline__ float fold(float acc, float a, float x, bool first) {
+#ifdef SGNN_EXPERIMENT_FMA_FOLD
+        if (RED == SGNN_REDUCE_SUM || RED == SGNN_REDUCE_MEAN) return __fmaf_rn(a, x, acc);
+#endif
         const float p = __fmul_rn(a, x);
         if (RED == SGNN_REDUCE_SUM || RED == SGNN_REDUCE_MEAN) return __fadd_rn(acc, p);
         if (first) return p;

@@ -1,0 +1,118 @@
+"""Parity at BASELINE sizes (cfg2 / cfg4): full outputs are checked on a
+deterministic row sample that includes every hub row (the oracle runs on the
+sampled rows only), the transpose is checked bit-exact in full, and
+size-independent properties (involution, linearity, plan transparency) are
+checked on the whole matrices."""
+import numpy as np
+import pytest
+
+from conftest import assert_spmm_close
+from oracle import port
+
+pytestmark = [pytest.mark.gpu, pytest.mark.slow]
+
+
+def _sample_rows(rp, n_sample=3000, seed=0):
+    deg = np.diff(rp.astype(np.int64))
+    hubs = np.argsort(deg)[::-1][:200]
+    rng = np.random.default_rng(seed)
+    rest = rng.choice(len(deg), size=n_sample, replace=False)
+    empties = np.nonzero(deg == 0)[0][:50]
+    return np.unique(np.concatenate([hubs, rest, empties]))
+
+
+def _sub(rp, ci, v, rows):
+    deg = np.diff(rp.astype(np.int64))[rows]
+    srp = np.zeros(len(rows) + 1, np.uint64)
+    srp[1:] = np.cumsum(deg)
+    idx = np.concatenate([np.arange(rp[r], rp[r + 1], dtype=np.int64) for r in rows])
+    return srp, ci[idx], v[idx]
+
+
+@pytest.fixture(scope="module")
+def cfg2():
+    from paper_2403_14853_b200 import graphs
+    w = graphs.cfg2()
+    x = graphs.normal(w.n_cols * w.k, 0, 1, 1, 21).reshape(w.n_cols, w.k)
+    return w, x
+
+
+def test_cfg2_spmm_sampled_rows(cuda, cfg2):
+    import torch
+
+    from paper_2403_14853_b200 import ops
+    w, x = cfg2
+    a = ops.CsrMatrix.from_numpy(w.row_ptr, w.col_idx, w.values, w.n_cols)
+    xt = torch.from_numpy(x).cuda()
+    rows = _sample_rows(w.row_ptr)
+    srp, sci, sv = _sub(w.row_ptr, w.col_idx, w.values, rows)
+    for red, r in (("sum", 0), ("mean", 3), ("max", 2)):
+        got = ops.spmm(a, xt, red).cpu().numpy()[rows]
+        want = port.spmm(srp, sci, sv.astype(np.float64), x.astype(np.float64), r)
+        assert_spmm_close(got, want, port.spmm_absdenom(srp, sci, sv, x, r), what=f"cfg2 {red}")
+        w32 = port.spmm(srp, sci, sv, x, r, np.float32)
+        short = np.diff(srp.astype(np.int64)) <= 256 if red != "max" else np.ones(len(rows), bool)
+        np.testing.assert_array_equal(got[short].view(np.uint32), w32[short].view(np.uint32))
+
+
+def test_cfg2_transpose_full_bitexact_and_backward(cuda, cfg2):
+    import torch
+
+    from paper_2403_14853_b200 import ops
+    w, x = cfg2
+    a = ops.CsrMatrix.from_numpy(w.row_ptr, w.col_idx, w.values, w.n_cols)
+    t = ops.transpose(a)
+    got = t.to_numpy()
+    want = port.transpose(w.row_ptr, w.col_idx, w.values, w.n_cols)
+    for p, q in zip(got, want):
+        np.testing.assert_array_equal(p, q)
+    tt = ops.transpose(t).to_numpy()  # involution
+    for p, q in zip(tt, (w.row_ptr, w.col_idx, w.values)):
+        np.testing.assert_array_equal(p, q)
+    cache = ops.TrainingCache(a, True)
+    g = torch.from_numpy(x).cuda()  # square graph: reuse X as dC
+    dx = cache.spmm_backward(g, "sum").cpu().numpy()
+    rows = _sample_rows(want[0], seed=1)
+    srp, sci, sv = _sub(want[0], want[1], want[2], rows)
+    ref = port.spmm(srp, sci, sv.astype(np.float64), x.astype(np.float64), 0)
+    assert_spmm_close(dx[rows], ref, port.spmm_absdenom(srp, sci, sv, x, 0), what="cfg2 backward")
+
+
+def test_cfg2_linearity_and_plan_transparency(cuda, cfg2):
+    import torch
+
+    from paper_2403_14853_b200 import ops
+    w, x = cfg2
+    a = ops.CsrMatrix.from_numpy(w.row_ptr, w.col_idx, w.values, w.n_cols)
+    x1 = torch.from_numpy(x).cuda()
+    x2 = torch.roll(x1, 7, dims=1)
+    c1, c2, c12 = ops.spmm(a, x1), ops.spmm(a, x2), ops.spmm(a, x1 + x2)
+    den = ops.spmm(a, x1.abs()) + ops.spmm(a, x2.abs())
+    assert bool(((c12 - (c1 + c2)).abs() <= 2e-5 * den + 1e-30).all())
+    base = c1.cpu().numpy()
+    for params in ({"lanes": 16, "vec": 2, "unroll": 4}, {"path_items": 256}, {"lanes": 32, "vec": 1, "unroll": 4,
+                                                                                 "occupancy": 8}):
+        got = ops.spmm_plan(a, x1, "sum", ops.Plan(a, w.k, **params)).cpu().numpy()
+        np.testing.assert_array_equal(got.view(np.uint32), base.view(np.uint32), err_msg=str(params))
+
+
+def test_cfg4_fused_and_sddmm_sampled_rows(cuda):
+    import torch
+
+    from paper_2403_14853_b200 import graphs, ops
+    w = graphs.cfg4()
+    m, k = w.n_rows, w.k
+    x = graphs.normal(m * k, 0, 0.1, 1, 41).reshape(m, k)
+    y = graphs.normal(w.n_cols * k, 0, 0.1, 1, 42).reshape(w.n_cols, k)
+    p = ops.CsrMatrix.from_numpy(w.row_ptr, w.col_idx, w.values, w.n_cols)
+    xt, yt = torch.from_numpy(x).cuda(), torch.from_numpy(y).cuda()
+    rows = _sample_rows(w.row_ptr, 2000)
+    srp, sci, sv = _sub(w.row_ptr, w.col_idx, w.values, rows)
+    got = ops.fusedmm(p, xt, yt, "sigmoid_mul", "sum").cpu().numpy()[rows]
+    want = port.fusedmm(srp, sci, sv, x[rows], y, 1, 0)
+    assert_spmm_close(got, want, port.fusedmm_absdenom(srp, sci, sv, x[rows], y, 1, 0), what="cfg4 fusedmm")
+    s = ops.sddmm(p, xt, yt).values.cpu().numpy()
+    idx = np.concatenate([np.arange(w.row_ptr[r], w.row_ptr[r + 1], dtype=np.int64) for r in rows])
+    want_s = port.sddmm(srp, sci, sv, x[rows], y)
+    den = port.sddmm_absdenom(srp, sci, sv, x[rows], y)
+    assert (np.abs(s[idx] - want_s) <= 1e-5 * den + 1e-30).all()
