@@ -112,12 +112,24 @@ __global__ void __launch_bounds__(128) sddmm_kernel(const SddmmArgs a) {
             for (int h = 0; h < CH; ++h) res[h] = 0.0f;
             if (base >= rend_l) next_row(base);
             if (base + uint32_t(n) <= rend_l) {
-                float d[U];
+                if constexpr (U <= G) {
+                    // transpose-reduce: lane gl owns nonzero gl/(G/U); lane u stores nonzero u
+                    constexpr int PER = G / U;
+                    const int u_own = gl / PER;
+                    float pv_own = pv[0];
 #pragma unroll
-                for (int u = 0; u < U; ++u) d[u] = dev::group_dot(xrow, yf[u], gmask);
+                    for (int u = 1; u < U; ++u)
+                        if (u == u_own) pv_own = pv[u];
+                    const float r_own = __fmul_rn(pv_own, dev::batch_dots(xrow, yf, gmask, gl));  // kernels.hpp:206
+                    res[0] = __shfl_sync(gmask, r_own, (gl * PER) & (G - 1), G);
+                } else {
+                    float d[U];
 #pragma unroll
-                for (int u = 0; u < U; ++u)
-                    if (gl == u % G) res[u / G] = __fmul_rn(pv[u], d[u]);  // kernels.hpp:206
+                    for (int u = 0; u < U; ++u) d[u] = dev::group_dot(xrow, yf[u], gmask);
+#pragma unroll
+                    for (int u = 0; u < U; ++u)
+                        if (gl == u % G) res[u / G] = __fmul_rn(pv[u], d[u]);  // kernels.hpp:206
+                }
             } else {
 #pragma unroll
                 for (int u = 0; u < U; ++u) {

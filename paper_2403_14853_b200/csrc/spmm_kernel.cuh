@@ -190,18 +190,20 @@ struct Frag {
 // Kernel modes: plain SpMM, or FusedMM with an edge op (kernels.hpp:216-270).
 enum { OP_SPMM = 0, OP_FUSED_MUL = 1, OP_FUSED_SIGMOID = 2 };
 
-// Canonical dot product <a, b> over the group: float4 leaves
-// ((a0b0 + a1b1) + a2b2) + a3b3 (scalar path: a0b0), then a balanced binary
-// tree over the leaves, lowest index bits first (zero leaves pad to a power
-// of two).  The tree is the same for every (G, V) layout, so FusedMM results
-// do not depend on the plan.  Every lane of the group returns the same value.
+// Canonical dot product <a, b> over the group.  Leaves are float4 blocks
+// q = lane + G*v: x0*y0 then fma of the next three (scalar path: x0*y0);
+// the leaves are summed by a balanced binary tree over q, HIGHEST index bit
+// first (zero leaves pad to a power of two).  q's high bits are the
+// register index v and its low bits the lane, so the tree is: within-lane
+// over v (high v bit first), then across lanes xor G/2, G/4, ..., 1.  It is
+// the same tree for every (G, V) layout, so FusedMM/SDDMM results do not
+// depend on the plan.
 template <int G, int V, bool VEC>
-__device__ __forceinline__ float group_dot(const Frag<G, V, VEC>& a, const Frag<G, V, VEC>& b,
-                                           unsigned gmask) {
+__device__ __forceinline__ float lane_leaf(const Frag<G, V, VEC>& a, const Frag<G, V, VEC>& b) {
     float p[V];
 #pragma unroll
     for (int q = 0; q < V; ++q) {
-        if constexpr (VEC) {  // leaf: fma chain over the float4
+        if constexpr (VEC) {
             float t = __fmul_rn(a.v[4 * q], b.v[4 * q]);
             t = __fmaf_rn(a.v[4 * q + 1], b.v[4 * q + 1], t);
             t = __fmaf_rn(a.v[4 * q + 2], b.v[4 * q + 2], t);
@@ -211,13 +213,47 @@ __device__ __forceinline__ float group_dot(const Frag<G, V, VEC>& a, const Frag<
         }
     }
 #pragma unroll
-    for (int off = 1; off < G; off <<= 1)
+    for (int half = V / 2; half >= 1; half >>= 1)  // v tree, high bit first
 #pragma unroll
-        for (int q = 0; q < V; ++q) p[q] = __fadd_rn(p[q], __shfl_xor_sync(gmask, p[q], off, G));
+        for (int q = 0; q < half; ++q) p[q] = __fadd_rn(p[q], p[q + half]);
+    return p[0];
+}
+
+// One dot, every lane of the group gets it.
+template <int G, int V, bool VEC>
+__device__ __forceinline__ float group_dot(const Frag<G, V, VEC>& a, const Frag<G, V, VEC>& b,
+                                           unsigned gmask) {
+    float p = lane_leaf(a, b);
 #pragma unroll
-    for (int step = 1; step < V; step <<= 1)
+    for (int s = G / 2; s >= 1; s >>= 1) p = __fadd_rn(p, __shfl_xor_sync(gmask, p, s, G));
+    return p;
+}
+
+// U dots at once (U <= G) by a transpose-reduce: each halving step exchanges
+// half of the remaining partials with lane ^ s (s = G/2, G/4, ...), then a
+// butterfly finishes the lanes below.  Same tree as group_dot (lane bits high
+// first), U-1 + log2(G/U) shuffles for U dots instead of U*log2(G).  Lane gl
+// returns the dot of nonzero gl / (G/U).
+template <int G, int V, int U, bool VEC>
+__device__ __forceinline__ float batch_dots(const Frag<G, V, VEC>& a, const Frag<G, V, VEC> (&b)[U],
+                                            unsigned gmask, int gl) {
+    static_assert(U <= G, "batch_dots needs U <= G");
+    float p[U];
 #pragma unroll
-        for (int q = 0; q + step < V; q += 2 * step) p[q] = __fadd_rn(p[q], p[q + step]);
+    for (int u = 0; u < U; ++u) p[u] = lane_leaf(a, b[u]);
+    int s = G / 2;
+#pragma unroll
+    for (int h = U / 2; h >= 1; h >>= 1, s >>= 1) {
+        const bool up = (gl & s) != 0;
+#pragma unroll
+        for (int i = 0; i < h; ++i) {
+            const float send = up ? p[i] : p[h + i];
+            const float keep = up ? p[h + i] : p[i];
+            p[i] = __fadd_rn(keep, __shfl_xor_sync(gmask, send, s, G));
+        }
+    }
+#pragma unroll
+    for (; s >= 1; s >>= 1) p[0] = __fadd_rn(p[0], __shfl_xor_sync(gmask, p[0], s, G));
     return p[0];
 }
 
@@ -407,10 +443,23 @@ __global__ void __launch_bounds__(128, MINB) spmm_worker_kernel(const SpmmArgs a
             if (base + uint32_t(n) <= next_l) {
                 // fast path: the whole batch continues the current row segment
                 if constexpr (OP != OP_SPMM) {
-                    // all U dot products first (independent shuffle trees interleave)
                     float sv[U];
+                    if constexpr (U <= G) {
+                        // transpose-reduce: lane gl owns the dot of nonzero gl/(G/U);
+                        // the edge op runs once per nonzero, then s is broadcast
+                        constexpr int PER = G / U;
+                        const int u_own = gl / PER;
+                        float pv_own = av[0];
 #pragma unroll
-                    for (int u = 0; u < U; ++u) sv[u] = edge_value<OP>(av[u], group_dot(xrow, xf[u], gmask));
+                        for (int u = 1; u < U; ++u)
+                            if (u == u_own) pv_own = av[u];
+                        const float s_own = edge_value<OP>(pv_own, batch_dots(xrow, xf, gmask, gl));
+#pragma unroll
+                        for (int u = 0; u < U; ++u) sv[u] = __shfl_sync(gmask, s_own, u * PER, G);
+                    } else {
+#pragma unroll
+                        for (int u = 0; u < U; ++u) sv[u] = edge_value<OP>(av[u], group_dot(xrow, xf[u], gmask));
+                    }
 #pragma unroll
                     for (int u = 0; u < U; ++u) {
                         if (u < n) {

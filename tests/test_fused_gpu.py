@@ -135,6 +135,25 @@ def test_hub_rows_fused(cuda):
     check_sddmm(rp, ci, v, n, x, y)
 
 
+def test_fused_plan_transparency(cuda):
+    """FusedMM/SDDMM results are bitwise independent of the register layout
+    and work split (canonical high-bit-first dot tree, canonical segments)."""
+    ops = _ops()
+    rng = np.random.default_rng(21)
+    rp, ci, v = rand_csr(rng, 600, 3000, 0.01, hub_rows=(0, 5), hub_density=0.3, empty_frac=0.1)
+    x = rng.normal(0, 0.3, (600, 64)).astype(np.float32)
+    y = rng.normal(0, 0.3, (3000, 64)).astype(np.float32)
+    p = ops.CsrMatrix.from_numpy(rp, ci, v, 3000)
+    for edge in ("sigmoid_mul", "mul"):
+        base = ops.fusedmm(p, _t(x), _t(y), edge, "sum").cpu().numpy()
+        for lv in ((16, 1, 8), (8, 2, 4), (4, 4, 4), (16, 2, 4), (32, 1, 8)):
+            for pi in (32, 300):
+                plan = ops.Plan(p, 64, lanes=lv[0], vec=lv[1], unroll=lv[2], path_items=pi)
+                got = ops.fusedmm(p, _t(x), _t(y), edge, "sum", plan=plan).cpu().numpy()
+                np.testing.assert_array_equal(got.view(np.uint32), base.view(np.uint32), err_msg=f"{edge} {lv} {pi}")
+    check_fused(rp, ci, v, 3000, x, y, "sigmoid_mul", "sum")
+
+
 def test_errors(cuda):
     import torch
     ops = _ops()
