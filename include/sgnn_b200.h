@@ -239,6 +239,11 @@ sgnn_status sgnn_spmm_backward_f32(sgnn_cache cache, const float* dc, uint32_t d
  * X is p.n_rows x k, Y is p.n_cols x k. */
 sgnn_status sgnn_sddmm_f32(const sgnn_csr* p, const float* x, uint32_t x_rows, const float* y,
                            uint32_t y_rows, uint32_t k, float* out_values, sgnn_stream stream);
+/* sddmm reusing a plan of P for its nnz-balanced work split (no per-worker
+ * row search); results are identical to sgnn_sddmm_f32. */
+sgnn_status sgnn_sddmm_plan_f32(const sgnn_csr* p, const float* x, uint32_t x_rows, const float* y,
+                                uint32_t y_rows, uint32_t k, float* out_values, sgnn_plan plan,
+                                sgnn_stream stream);
 /* fusedmm(p, x, y, semiring) (kernels.hpp:216-270): out_i = reduce_j
  * combine(p_ij, <X_i,Y_j>) * Y_j in one pass (Y_j read once per edge).
  * out is p.n_rows x k. */

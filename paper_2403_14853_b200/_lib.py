@@ -119,6 +119,7 @@ SIGNATURES = {
     "sgnn_cache_counters": (i32, [P, C.POINTER(u64), C.POINTER(u64), C.POINTER(u64), C.POINTER(i32)]),
     "sgnn_spmm_backward_f32": (i32, [P, P, u32, u32, P, i32, P]),
     "sgnn_sddmm_f32": (i32, [CsrP, P, u32, P, u32, u32, P, P]),
+    "sgnn_sddmm_plan_f32": (i32, [CsrP, P, u32, P, u32, u32, P, P, P]),
     "sgnn_fusedmm_f32": (i32, [CsrP, P, u32, P, u32, u32, i32, i32, P, P]),
     "sgnn_fusedmm_plan_f32": (i32, [CsrP, P, u32, P, u32, u32, i32, i32, P, P, P]),
 }

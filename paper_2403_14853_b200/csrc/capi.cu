@@ -274,7 +274,23 @@ sgnn_status sgnn_sddmm_f32(const sgnn_csr* p, const float* x, uint32_t x_rows, c
                                         std::to_string(x_rows) + "x" + std::to_string(k) + ", Y " +
                                         std::to_string(y_rows) + "x" + std::to_string(k));
     if (p->nnz && !out_values) return fail(SGNN_ERR_CONFIG, "sddmm: null output");
-    return run_sddmm(p, x, y, k, out_values, cs(stream));
+    return run_sddmm(p, x, y, k, out_values, nullptr, cs(stream));
+}
+
+sgnn_status sgnn_sddmm_plan_f32(const sgnn_csr* p, const float* x, uint32_t x_rows, const float* y,
+                                uint32_t y_rows, uint32_t k, float* out_values, sgnn_plan plan,
+                                sgnn_stream stream) {
+    SGNN_TRY(check_csr(p, "sddmm"));
+    if (p->n_rows != x_rows || p->n_cols != y_rows)
+        return fail(SGNN_ERR_SHAPE, "sddmm: pattern " + std::to_string(p->n_rows) + "x" +
+                                        std::to_string(p->n_cols) + " needs X with " +
+                                        std::to_string(p->n_rows) + " rows and Y with " +
+                                        std::to_string(p->n_cols) + " rows of equal width; got X " +
+                                        std::to_string(x_rows) + "x" + std::to_string(k) + ", Y " +
+                                        std::to_string(y_rows) + "x" + std::to_string(k));
+    if (p->nnz && !out_values) return fail(SGNN_ERR_CONFIG, "sddmm: null output");
+    if (!plan) return fail(SGNN_ERR_CONFIG, "sddmm_plan: null plan");
+    return run_sddmm(p, x, y, k, out_values, plan, cs(stream));
 }
 
 sgnn_status sgnn_fusedmm_f32(const sgnn_csr* p, const float* x, uint32_t x_rows, const float* y,

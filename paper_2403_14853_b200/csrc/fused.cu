@@ -29,6 +29,8 @@ struct SddmmArgs {
     float* __restrict__ out;
     uint64_t nnz;
     uint64_t per_worker;
+    const uint32_t* __restrict__ wrow;  // optional plan split (row of each worker start)
+    const uint64_t* __restrict__ wnz;
     uint32_t n_rows;
     uint32_t n_workers;
     uint32_t k;
@@ -63,9 +65,10 @@ __global__ void __launch_bounds__(128) sddmm_kernel(const SddmmArgs a) {
     const int nq = F::blocks_in(gl, a.k);
     const bool full = a.k == uint32_t(F::W * G * V);
     for (uint32_t w = (blockIdx.x * blockDim.x + threadIdx.x) / G; w < a.n_workers; w += n_groups) {
-        const uint64_t j0 = uint64_t(w) * a.per_worker;
-        const uint32_t E = uint32_t(min(a.per_worker, a.nnz - j0));
-        uint32_t r = row_of(a.rp, a.n_rows, j0);
+        // a plan's split (no search) or an even nnz split (binary search)
+        const uint64_t j0 = a.wnz ? __ldg(a.wnz + w) : uint64_t(w) * a.per_worker;
+        const uint32_t E = a.wnz ? uint32_t(__ldg(a.wnz + w + 1) - j0) : uint32_t(min(a.per_worker, a.nnz - j0));
+        uint32_t r = a.wrow ? __ldg(a.wrow + w) : row_of(a.rp, a.n_rows, j0);
         uint32_t rb = r;
         uint64_t rwin = __ldg(a.rp + min(rb + 1 + uint32_t(gl), a.n_rows));
         uint32_t rend_l = uint32_t(min(dev::shfl_u64(gmask, rwin, 0, G), j0 + E) - j0);
@@ -221,8 +224,10 @@ SpmmLauncher find_fused_launcher(bool vec, int lanes, int vregs, int unroll, int
 }  // namespace
 
 sgnn_status run_sddmm(const sgnn_csr* p, const float* x, const float* y, uint32_t k, float* out,
-                      cudaStream_t s) {
+                      const sgnn_plan_s* plan, cudaStream_t s) {
     if (p->nnz == 0) return SGNN_OK;
+    if (plan && !plan_matches(plan, p, plan->k))
+        return fail(SGNN_ERR_DISPATCH, "sddmm: plan was built for another matrix");
     const bool vec = (k % 4 == 0) && (reinterpret_cast<uintptr_t>(x) % 16 == 0) &&
                      (reinterpret_cast<uintptr_t>(y) % 16 == 0);
     int lanes, vregs;
@@ -245,8 +250,14 @@ sgnn_status run_sddmm(const sgnn_csr* p, const float* x, const float* y, uint32_
     // ~4 workers per resident group, at least 64 nonzeros each
     const uint64_t groups = uint64_t(dp.sm_count) * 2048 / lanes;
     a.per_worker = std::max<uint64_t>(64, ceil_div_u64(p->nnz, 4 * groups));
-    const uint64_t nw = ceil_div_u64(p->nnz, a.per_worker);
-    a.n_workers = uint32_t(nw);
+    a.n_workers = uint32_t(ceil_div_u64(p->nnz, a.per_worker));
+    a.wrow = nullptr;
+    a.wnz = nullptr;
+    if (plan) {  // reuse the plan's nnz-balanced split: worker starts need no row search
+        a.wrow = plan->wrow;
+        a.wnz = plan->wnz;
+        a.n_workers = plan->n_workers;
+    }
     SddmmLaunch fn = nullptr;
     if (vec) {
         if (lanes == 4) fn = &launch_sddmm<4, 1, 8, true>;

@@ -44,7 +44,7 @@ sgnn_status tune_spmm(const sgnn_csr* a, const float* x, uint32_t k, int reduce,
                       int* n_entries, cudaStream_t s);
 
 sgnn_status run_sddmm(const sgnn_csr* p, const float* x, const float* y, uint32_t k, float* out,
-                      cudaStream_t s);
+                      const sgnn_plan_s* plan, cudaStream_t s);
 sgnn_status run_fusedmm(const sgnn_csr* p, const float* x, const float* y, uint32_t k,
                         int edge_op, int reduce, float* out, const sgnn_plan_s* plan,
                         cudaStream_t s);

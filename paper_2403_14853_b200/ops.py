@@ -507,8 +507,14 @@ def sddmm(p: CsrMatrix, x: torch.Tensor, y: torch.Tensor) -> CsrMatrix:
                          f"{p.n_cols} rows of equal width; got X {x.shape[0]}x{x.shape[1]}, "
                          f"Y {y.shape[0]}x{y.shape[1]}")
     out = torch.empty(p.nnz, dtype=torch.float32, device=x.device)
-    check(lib().sgnn_sddmm_f32(C.byref(p.c()), x.data_ptr(), x.shape[0], y.data_ptr(), y.shape[0],
-                               x.shape[1], out.data_ptr() if p.nnz else None, _stream()), "sddmm")
+    k = x.shape[1]
+    if p.nnz and p.n_rows and k and k <= 1024 and (k % 4 == 0 or k <= 256):
+        plan = p.plan(k, "fused")  # cached nnz-balanced split shared with fusedmm
+        check(lib().sgnn_sddmm_plan_f32(C.byref(p.c()), x.data_ptr(), x.shape[0], y.data_ptr(), y.shape[0],
+                                        k, out.data_ptr(), plan.handle, _stream()), "sddmm")
+    else:
+        check(lib().sgnn_sddmm_f32(C.byref(p.c()), x.data_ptr(), x.shape[0], y.data_ptr(), y.shape[0],
+                                   k, out.data_ptr() if p.nnz else None, _stream()), "sddmm")
     return p.with_values(out)
 
 
