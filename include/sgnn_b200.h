@@ -170,6 +170,28 @@ int sgnn_resolve_kernel(uint32_t k, int reduce, uint32_t* spec_k);
 void sgnn_set_dispatch(int enabled);
 int sgnn_get_dispatch(void);
 
+/* ------------------------------------------------- row-partitioned SpMM */
+/* The multi-GPU row partition's SpMM with the feature exchange fused in:
+ * the gathered operand X is NOT materialised -- it is the union of the
+ * n_parts row blocks `parts[q]` (each [2^part_shift, k] row-major, e.g. the
+ * ranks' own feature blocks mapped over NVLink peer access / CUDA IPC), and
+ * A's column ids are in the padded owner layout col' = q << part_shift |
+ * local (sgnn_host_partition_block with stride = 2^part_shift).  Each gather
+ * reads the owner block directly, replacing all-gather + SpMM.  Sum and Mean;
+ * n_parts <= 8; results are bitwise those of sgnn_spmm_f32 on the gathered
+ * matrix.  plan: a plan of A (required). */
+sgnn_status sgnn_spmm_peer_f32(const sgnn_csr* a, const float* const* parts, uint32_t n_parts,
+                               uint32_t part_shift, uint32_t k, float* c, int reduce,
+                               sgnn_plan plan, sgnn_stream stream);
+/* CUDA IPC plumbing for the peer mappings (cudaIpcGetMemHandle /
+ * cudaIpcOpenMemHandle with peer access enabled / cudaIpcCloseMemHandle).
+ * handle is 64 bytes. */
+sgnn_status sgnn_peer_alloc(size_t bytes, void** dev_ptr); /* own cudaMalloc: IPC handle == pointer */
+sgnn_status sgnn_peer_free(void* dev_ptr);
+sgnn_status sgnn_ipc_get_handle(void* dev_ptr, void* handle64);
+sgnn_status sgnn_ipc_open_handle(const void* handle64, void** dev_ptr);
+sgnn_status sgnn_ipc_close_handle(void* dev_ptr);
+
 /* ------------------------------------------------------------- transpose */
 /* transpose(a) (sparse.hpp:72-89): CSR(A) -> CSR(A^T), bit-exact with the
  * reference's stable counting sort (rows ascending within each column).

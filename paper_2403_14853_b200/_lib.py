@@ -102,6 +102,12 @@ SIGNATURES = {
     "sgnn_spmm_with_f32": (i32, [CsrP, P, u32, u32, P, i32, i32, u32, P, P]),
     "sgnn_tune_spmm": (i32, [CsrP, P, u32, i32, i32, C.POINTER(P), C.POINTER(TuneEntry), i32,
                              C.POINTER(i32), P]),
+    "sgnn_spmm_peer_f32": (i32, [CsrP, C.POINTER(P), u32, u32, u32, P, i32, P, P]),
+    "sgnn_peer_alloc": (i32, [C.c_size_t, C.POINTER(P)]),
+    "sgnn_peer_free": (i32, [P]),
+    "sgnn_ipc_get_handle": (i32, [P, P]),
+    "sgnn_ipc_open_handle": (i32, [P, C.POINTER(P)]),
+    "sgnn_ipc_close_handle": (i32, [P]),
     "sgnn_resolve_kernel": (i32, [u32, i32, C.POINTER(u32)]),
     "sgnn_set_dispatch": (None, [i32]),
     "sgnn_get_dispatch": (i32, []),

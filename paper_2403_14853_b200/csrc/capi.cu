@@ -1,6 +1,7 @@
 // capi.cu -- the extern "C" boundary (include/sgnn_b200.h).  Validation and
 // error messages follow the reference operator API (kernels.hpp:131-173).
 #include <atomic>
+#include <cstring>
 #include <new>
 
 #include "ops.cuh"
@@ -168,6 +169,51 @@ int sgnn_resolve_kernel(uint32_t k, int reduce, uint32_t* spec_k) {
         kind = SGNN_KERNEL_SPECIALIZED;
     if (spec_k) *spec_k = kind == SGNN_KERNEL_SPECIALIZED ? k : 0;
     return kind;
+}
+
+// ------------------------------------------------- row-partitioned SpMM
+sgnn_status sgnn_spmm_peer_f32(const sgnn_csr* a, const float* const* parts, uint32_t n_parts,
+                               uint32_t part_shift, uint32_t k, float* c, int reduce,
+                               sgnn_plan plan, sgnn_stream stream) {
+    SGNN_TRY(check_csr(a, "spmm_peer"));
+    if (!parts || !plan) return fail(SGNN_ERR_CONFIG, "spmm_peer: null parts or plan");
+    for (uint32_t i = 0; i < n_parts && i < SGNN_MAX_PEERS; ++i)
+        if (!parts[i]) return fail(SGNN_ERR_CONFIG, "spmm_peer: null part pointer");
+    return run_spmm_peer(a, parts, n_parts, part_shift, k, c, reduce, plan, cs(stream));
+}
+
+sgnn_status sgnn_peer_alloc(size_t bytes, void** dev_ptr) {
+    if (!dev_ptr) return fail(SGNN_ERR_CONFIG, "peer_alloc: null out");
+    SGNN_CUDA_TRY(cudaMalloc(dev_ptr, bytes ? bytes : 16));
+    return SGNN_OK;
+}
+
+sgnn_status sgnn_peer_free(void* dev_ptr) {
+    if (dev_ptr) SGNN_CUDA_TRY(cudaFree(dev_ptr));
+    return SGNN_OK;
+}
+
+sgnn_status sgnn_ipc_get_handle(void* dev_ptr, void* handle64) {
+    static_assert(sizeof(cudaIpcMemHandle_t) == 64, "cudaIpcMemHandle_t is 64 bytes");
+    if (!dev_ptr || !handle64) return fail(SGNN_ERR_CONFIG, "ipc_get_handle: null argument");
+    cudaIpcMemHandle_t h;
+    SGNN_CUDA_TRY(cudaIpcGetMemHandle(&h, dev_ptr));
+    std::memcpy(handle64, &h, sizeof(h));
+    return SGNN_OK;
+}
+
+sgnn_status sgnn_ipc_open_handle(const void* handle64, void** dev_ptr) {
+    if (!dev_ptr || !handle64) return fail(SGNN_ERR_CONFIG, "ipc_open_handle: null argument");
+    cudaIpcMemHandle_t h;
+    std::memcpy(&h, handle64, sizeof(h));
+    SGNN_CUDA_TRY(cudaIpcOpenMemHandle(dev_ptr, h, cudaIpcMemLazyEnablePeerAccess));
+    return SGNN_OK;
+}
+
+sgnn_status sgnn_ipc_close_handle(void* dev_ptr) {
+    if (!dev_ptr) return fail(SGNN_ERR_CONFIG, "ipc_close_handle: null argument");
+    SGNN_CUDA_TRY(cudaIpcCloseMemHandle(dev_ptr));
+    return SGNN_OK;
 }
 
 // ------------------------------------------------------------- transpose

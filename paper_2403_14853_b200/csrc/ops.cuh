@@ -26,6 +26,10 @@ sgnn_status run_normalize(const sgnn_csr* a, int add_loops, uint64_t* out_nnz, u
 
 sgnn_status run_spmm(const sgnn_csr* a, const float* x, uint32_t k, float* c, int reduce,
                      const sgnn_plan_s* plan, cudaStream_t s);
+// SpMM reading X from the row blocks `parts` of a partition (peer memory).
+sgnn_status run_spmm_peer(const sgnn_csr* a, const float* const* parts, uint32_t n_parts,
+                          uint32_t part_shift, uint32_t k, float* c, int reduce,
+                          const sgnn_plan_s* plan, cudaStream_t s);
 // Mean epilogue: C[r, :k] /= deg(r) (kernels.hpp:60-63, :263-266).
 sgnn_status run_mean_divide(const uint64_t* rp, uint32_t m, float* c, uint64_t ldc, uint32_t k,
                             cudaStream_t s);

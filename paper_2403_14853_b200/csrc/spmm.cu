@@ -144,4 +144,75 @@ sgnn_status run_spmm(const sgnn_csr* a, const float* x, uint32_t k, float* c, in
     return SGNN_OK;
 }
 
+sgnn_status run_spmm_peer(const sgnn_csr* a, const float* const* parts, uint32_t n_parts,
+                          uint32_t part_shift, uint32_t k, float* c, int reduce,
+                          const sgnn_plan_s* plan, cudaStream_t s) {
+    if (reduce != SGNN_REDUCE_SUM && reduce != SGNN_REDUCE_MEAN)
+        return fail(SGNN_ERR_UNSUPPORTED, "spmm_peer: sum and mean only");
+    if (n_parts == 0 || n_parts > SGNN_MAX_PEERS)
+        return fail(SGNN_ERR_CONFIG, "spmm_peer: 1.." + std::to_string(SGNN_MAX_PEERS) + " parts");
+    if (part_shift > 31 || (uint64_t(n_parts) << part_shift) < a->n_cols)
+        return fail(SGNN_ERR_SHAPE, "spmm_peer: n_parts << part_shift must cover the remapped columns");
+    if (k == 0 || a->n_rows == 0) return SGNN_OK;
+    if (!plan_matches(plan, a, k))
+        return fail(SGNN_ERR_DISPATCH, "spmm_peer: plan was built for another matrix or K");
+    bool aligned = (reinterpret_cast<uintptr_t>(c) % 16 == 0) && (k % 4 == 0);
+    for (uint32_t i = 0; i < n_parts; ++i) aligned &= reinterpret_cast<uintptr_t>(parts[i]) % 16 == 0;
+    const bool vec = plan->vec && aligned;
+    int lanes = int(plan->p.lanes), vregs = int(plan->p.vec), unroll = int(plan->p.unroll);
+    if (!vec) {
+        lanes = 32;
+        vregs = std::min<int>(8, int(ceil_div_u64(plan->kt, 32)));
+        vregs = vregs <= 1 ? 1 : vregs <= 2 ? 2 : vregs <= 4 ? 4 : 8;
+        unroll = vregs >= 4 ? 2 : 4;
+    }
+    SpmmLauncher launch = spmm_peer_lookup_sum(vec, lanes, vregs, unroll, vec ? int(plan->p.occupancy) : 1);
+    // peer kernels carry the part table: they are compiled at occupancy 4 / 1
+    if (!launch && vec) launch = spmm_peer_lookup_sum(vec, lanes, vregs, unroll, 4);
+    if (!launch && vec) launch = spmm_peer_lookup_sum(vec, lanes, vregs, unroll, 1);
+    if (!launch)
+        return fail(SGNN_ERR_UNSUPPORTED, "spmm_peer: no peer kernel for lanes=" + std::to_string(lanes) +
+                                              " vec=" + std::to_string(vregs) + " unroll=" + std::to_string(unroll));
+    const uint32_t kernel_width = uint32_t((vec ? 4 : 1) * lanes * vregs);
+    for (uint32_t k0 = 0; k0 < k; k0 += plan->kt) {
+        const uint32_t kp = std::min(plan->kt, k - k0);
+        for (uint32_t sk = 0; sk < kp; sk += kernel_width) {
+            SpmmArgs args{};
+            args.rp = a->row_ptr;
+            args.ci = a->col_idx;
+            args.val = a->values;
+            args.x = parts[0] + k0 + sk;  // (unused base for the lane clamp)
+            for (uint32_t i = 0; i < n_parts; ++i) args.xparts[i] = parts[i] + k0 + sk;
+            args.part_shift = part_shift;
+            args.c = c + k0 + sk;
+            args.slots = plan->slots ? plan->slots + sk : nullptr;
+            args.wrow = plan->wrow;
+            args.wnz = plan->wnz;
+            args.wslot = plan->wslot;
+            args.n_rows = a->n_rows;
+            args.n_workers = plan->n_workers;
+            args.ldx = k;
+            args.ldc = k;
+            args.ld_slot = plan->kt;
+            args.width = std::min(kernel_width, kp - sk);
+            SGNN_TRY(launch(args, plan->p.block, 0, s));
+        }
+        if (plan->n_fix) {
+            FixupArgs f;
+            f.rp = a->row_ptr;
+            f.fix_row = plan->fix_row;
+            f.fix_slot = plan->fix_slot;
+            f.slots = plan->slots;
+            f.c = c + k0;
+            f.ldc = k;
+            f.ld_slot = plan->kt;
+            f.n_fix = plan->n_fix;
+            f.width = kp;
+            SGNN_TRY(launch_spmm_fixup(f, SGNN_REDUCE_SUM, s));
+        }
+    }
+    if (reduce == SGNN_REDUCE_MEAN) SGNN_TRY(run_mean_divide(a->row_ptr, a->n_rows, c, k, k, s));
+    return SGNN_OK;
+}
+
 }  // namespace sgnn

@@ -148,6 +148,26 @@ sgnn_status launch_spmm_worker(const SpmmArgs& a, uint32_t block, uint32_t max_b
         return SGNN_OK;                                                               \
     }
 
+// Peer-partitioned SpMM (OP_SPMM_PEER): the default layouts per K, sum (and mean).
+#define SGNN_PEER_CONFIGS(X, RED, OP) \
+    X(4, 1, 8, RED, true, OP, 1)      \
+    X(8, 1, 8, RED, true, OP, 4)      \
+    X(16, 1, 8, RED, true, OP, 4)     \
+    X(32, 1, 8, RED, true, OP, 4)     \
+    X(32, 2, 4, RED, true, OP, 4)     \
+    X(32, 4, 4, RED, true, OP, 1)     \
+    X(32, 1, 4, RED, false, OP, 1)    \
+    X(32, 2, 4, RED, false, OP, 1)    \
+    X(32, 4, 2, RED, false, OP, 1)    \
+    X(32, 8, 2, RED, false, OP, 1)
+
+#define SGNN_DEFINE_PEER_LOOKUP(NAME, RED)                                            \
+    SpmmLauncher NAME(bool vec, int lanes, int vregs, int unroll, int occ) {         \
+        if (occ == 0) occ = 1;                                                        \
+        SGNN_PEER_CONFIGS(SGNN_WORKER_CASE, RED, dev::OP_SPMM_PEER)                   \
+        return nullptr;                                                               \
+    }
+
 #define SGNN_DEFINE_FUSED_LOOKUP(NAME, RED, OP)                                       \
     SpmmLauncher NAME(bool vec, int lanes, int vregs, int unroll, int occ) {         \
         if (occ == 0) occ = 1;                                                        \
@@ -157,6 +177,7 @@ sgnn_status launch_spmm_worker(const SpmmArgs& a, uint32_t block, uint32_t max_b
 
 // Mean runs the Sum kernels plus run_mean_divide (spmm.cu).
 SpmmLauncher spmm_lookup_sum(bool, int, int, int, int);
+SpmmLauncher spmm_peer_lookup_sum(bool, int, int, int, int);
 SpmmLauncher spmm_lookup_min(bool, int, int, int, int);
 SpmmLauncher spmm_lookup_max(bool, int, int, int, int);
 sgnn_status spmm_lookup_sum_fixup(const FixupArgs&, cudaStream_t);

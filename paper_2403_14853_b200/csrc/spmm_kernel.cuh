@@ -20,6 +20,8 @@
 
 namespace sgnn {
 
+#define SGNN_MAX_PEERS 8
+
 struct SpmmArgs {
     const uint64_t* __restrict__ rp;
     const uint32_t* __restrict__ ci;
@@ -38,6 +40,10 @@ struct SpmmArgs {
     uint64_t ldc;     // row stride of C (floats)
     uint64_t ld_slot; // row stride of a slot (floats)
     uint32_t width;   // floats of K this launch covers
+    // OP_SPMM_PEER: column c lives in block c >> part_shift at row
+    // c & ((1 << part_shift) - 1); block base pointers pre-offset by k0
+    const float* xparts[SGNN_MAX_PEERS];
+    uint32_t part_shift;
 };
 
 struct FixupArgs {
@@ -188,7 +194,12 @@ struct Frag {
 };
 
 // Kernel modes: plain SpMM, or FusedMM with an edge op (kernels.hpp:216-270).
-enum { OP_SPMM = 0, OP_FUSED_MUL = 1, OP_FUSED_SIGMOID = 2 };
+// OP_SPMM_PEER: SpMM whose gathered operand is split in row blocks that live
+// in different allocations -- the feature blocks of the ranks of a row
+// partition, read directly over NVLink peer mappings (no all-gather copy).
+enum { OP_SPMM = 0, OP_FUSED_MUL = 1, OP_FUSED_SIGMOID = 2, OP_SPMM_PEER = 3 };
+template <int OP>
+constexpr bool is_fused() { return OP == OP_FUSED_MUL || OP == OP_FUSED_SIGMOID; }
 
 // Canonical dot product <a, b> over the group.  Leaves are float4 blocks
 // q = lane + G*v: x0*y0 then fma of the next three (scalar path: x0*y0);
@@ -296,6 +307,17 @@ __global__ void __launch_bounds__(128, MINB) spmm_worker_kernel(const SpmmArgs a
     const int gl_eff = min(gl, int(a.width / F::W) - 1);
     const char* xlane = reinterpret_cast<const char*>(a.x + F::W * gl_eff);
     const uint32_t ldxb = uint32_t(a.ldx) * 4u;
+    const uint32_t lane_off = uint32_t(F::W * gl_eff) * 4u;  // OP_SPMM_PEER
+    const uint32_t part_mask = (1u << a.part_shift) - 1u;
+    // address of this lane's slice of gathered row `col`
+    auto row_addr = [&](uint32_t col) -> const float* {
+        if constexpr (OP == OP_SPMM_PEER) {
+            const char* base = reinterpret_cast<const char*>(a.xparts[col >> a.part_shift]);
+            return reinterpret_cast<const float*>(base + lane_off + uint64_t(col & part_mask) * ldxb);
+        } else {
+            return reinterpret_cast<const float*>(xlane + uint64_t(col) * ldxb);
+        }
+    };
     const int nq = F::blocks_in(gl, a.width);
     const bool full = a.width == uint32_t(F::W * G * V);  // every lane's blocks are in range
 
@@ -391,7 +413,7 @@ __global__ void __launch_bounds__(128, MINB) spmm_worker_kernel(const SpmmArgs a
                 finish_segment();
                 seg_l = min(seg_l + uint32_t(SEG), rend_l);
             }
-            if constexpr (OP != OP_SPMM) {
+            if constexpr (is_fused<OP>()) {
                 if (xrow_id != r) {
                     xrow.load(a.xi + uint64_t(r) * a.ldxi, gl, a.width);
                     xrow_id = r;
@@ -422,27 +444,27 @@ __global__ void __launch_bounds__(128, MINB) spmm_worker_kernel(const SpmmArgs a
             for (int u = 0; u < U; ++u) {  // unconditional gathers (tail lanes read row 0)
                 const uint32_t col = __shfl_sync(gmask, cc[u / G], u % G, G);
                 av[u] = __shfl_sync(gmask, vv[u / G], u % G, G);
-                const float* lrow = reinterpret_cast<const float*>(xlane + uint64_t(col) * ldxb);
+                const float* lrow = row_addr(col);
                 // the FusedMM dot sums all lanes: zero-fill blocks past a partial width
-                if (OP == OP_SPMM || full) xf[u].template gather<false>(lrow, nq);
+                if (!is_fused<OP>() || full) xf[u].template gather<false>(lrow, nq);
                 else xf[u].template gather<true>(lrow, nq);
             }
             if (base + CHUNK < E) load_cv(base + CHUNK);
             auto fold = [&](const F& xv, float pv) {
                 float s = pv;
-                if constexpr (OP != OP_SPMM) {
+                if constexpr (is_fused<OP>()) {
                     // s_ij = combine(p_ij, <X_i, Y_j>); Y_j is reused below (read once)
                     s = edge_value<OP>(pv, group_dot(xrow, xv, gmask));
                 }
 #pragma unroll
                 for (int i = 0; i < N; ++i)
-                    acc.v[i] = (OP != OP_SPMM) ? R::fold_fused(acc.v[i], s, xv.v[i], first)
-                                               : R::fold(acc.v[i], s, xv.v[i], first);
+                    acc.v[i] = is_fused<OP>() ? R::fold_fused(acc.v[i], s, xv.v[i], first)
+                                              : R::fold(acc.v[i], s, xv.v[i], first);
                 first = false;
             };
             if (base + uint32_t(n) <= next_l) {
                 // fast path: the whole batch continues the current row segment
-                if constexpr (OP != OP_SPMM) {
+                if constexpr (is_fused<OP>()) {
                     float sv[U];
                     if constexpr (U <= G) {
                         // transpose-reduce: lane gl owns the dot of nonzero gl/(G/U);

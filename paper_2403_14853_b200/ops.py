@@ -228,6 +228,33 @@ def spmm_plan(a: CsrMatrix, b: torch.Tensor, reduce="sum", plan: Plan | None = N
     return out
 
 
+def spmm_peer(a: CsrMatrix, parts, part_shift: int, k: int, reduce="sum", plan: Plan | None = None,
+              out: torch.Tensor | None = None, device=None) -> torch.Tensor:
+    """sgnn_spmm_peer_f32: SpMM whose X is the row partition's blocks, read in
+    place.  `parts` are device pointers (ints) or [2**part_shift, k] tensors,
+    one per partition, possibly mapped from peer GPUs; column c of `a` is row
+    (c & (2**part_shift - 1)) of block c >> part_shift.  Sum and mean only."""
+    ptrs = []
+    for p in parts:
+        if isinstance(p, torch.Tensor):
+            _dense(p, "spmm_peer block")
+            if p.shape[1] != k:
+                raise _lib.ShapeError(f"spmm_peer: block has {p.shape[1]} columns, K={k}")
+            if p.shape[0] < (1 << part_shift):
+                raise _lib.ShapeError("spmm_peer: block shorter than 2**part_shift rows")
+            ptrs.append(p.data_ptr())
+        else:
+            ptrs.append(int(p))
+    arr = (C.c_void_p * max(1, len(ptrs)))(*ptrs)
+    if out is None:
+        dev = device if device is not None else a.row_ptr.device
+        out = torch.empty((a.n_rows, k), dtype=torch.float32, device=dev)
+    check(lib().sgnn_spmm_peer_f32(C.byref(a.c()), arr, len(ptrs), int(part_shift), int(k), out.data_ptr(),
+                                   _reduce(reduce), plan.handle if plan is not None else None, _stream()),
+          "spmm_peer")
+    return out
+
+
 class _TunedPlan(Plan):
     def __init__(self, a, k, handle):  # noqa: D401 - wraps a plan made by the tuner
         self.a, self.k, self.handle = a, int(k), handle

@@ -12,6 +12,13 @@ row is accumulated in the same order as on one GPU: the P-GPU result is
 bitwise the 1-GPU result.
 
 Exchanges:
+  PeerBlocks        no copy at all: every rank's padded block lives in its own
+                    cudaMalloc allocation, mapped into every other rank with
+                    CUDA IPC (NVLink/NVSwitch peer memory on the B200 box); the
+                    SpMM kernel (sgnn_spmm_peer_f32) gathers X rows straight
+                    from the owner's HBM, so the all-gather is fused into the
+                    SpMM's own gather loop.  A pow2 stride turns the owner
+                    lookup into a shift and a mask.
   NcclExchange      torch.distributed all_gather_into_tensor (NCCL over NVLink
                     on the B200 box; gloo on CPU for tests)
   LoopbackExchange  P virtual partitions in one process (device copies) -- the
@@ -36,6 +43,13 @@ class RowPartition:
     def parts(self) -> int:
         return len(self.bounds) - 1
 
+    @property
+    def shift(self) -> int:
+        """log2(stride) for a pow2 partition (the peer path's part_shift)."""
+        if self.stride & (self.stride - 1):
+            raise ValueError("peer SpMM needs a power-of-two stride: make_partition(..., pow2=True)")
+        return self.stride.bit_length() - 1
+
     def rows(self, p: int):
         return int(self.bounds[p]), int(self.bounds[p + 1])
 
@@ -58,13 +72,17 @@ class RowPartition:
         return out_rp, out_ci, out_v
 
 
-def make_partition(row_ptr, n_parts: int, align: int = 1) -> RowPartition:
-    """balanced_row_partition (parallel.hpp:28-41) at GPU granularity."""
+def make_partition(row_ptr, n_parts: int, align: int = 1, pow2: bool = False) -> RowPartition:
+    """balanced_row_partition (parallel.hpp:28-41) at GPU granularity.
+    pow2=True rounds the block stride up to a power of two (the peer path
+    splits a remapped column into (owner, row) with a shift and a mask)."""
     rp = np.ascontiguousarray(row_ptr, np.uint64)
     bounds = graphs.balanced_row_partition(rp, n_parts)
     sizes = np.diff(bounds.astype(np.int64))
     stride = int(max(1, sizes.max() if len(sizes) else 1))
     stride = (stride + align - 1) // align * align
+    if pow2:
+        stride = 1 << (stride - 1).bit_length()
     return RowPartition(bounds, stride, len(rp) - 1)
 
 
@@ -130,3 +148,113 @@ class PartitionedSpmm:
         """x_local: this rank's feature rows [r1-r0, K]."""
         gathered = exchange.all_gather(pad_block(x_local, self.part.stride))
         return self.compute(gathered, reduce, out)
+
+    def compute_peer(self, parts, reduce="sum", out=None):
+        """The local SpMM reading the partition's blocks in place (pointer
+        table or tensors, one per rank): bitwise the gathered-buffer result."""
+        from . import ops
+        return ops.spmm_peer(self._a, parts, self.part.shift, self.k, reduce, self._plan, out)
+
+    def forward_peer(self, x_local, blocks: "PeerBlocks", reduce="sum", out=None):
+        """Fused all-gather + SpMM over peer memory."""
+        return self.compute_peer(blocks.publish(x_local), reduce, out)
+
+
+class _DeviceArray:
+    """__cuda_array_interface__ over a library-owned device allocation."""
+
+    def __init__(self, ptr: int, shape):
+        self.__cuda_array_interface__ = {"shape": tuple(shape), "typestr": "<f4", "data": (int(ptr), False),
+                                         "version": 3, "strides": None}
+
+
+class PeerBlocks:
+    """Feature blocks shared through peer memory (fused all-gather).
+
+    Each rank owns `buffers` blocks of [stride, K] f32 in its own cudaMalloc
+    allocation (sgnn_peer_alloc) and maps every other rank's blocks through
+    CUDA IPC (sgnn_ipc_get_handle / sgnn_ipc_open_handle; handles travel by
+    torch.distributed.all_gather_object).  publish(x_local) writes this rank's
+    rows into the next block and runs one fence; after it every rank's block is
+    readable by the SpMM.  With two buffers the fence of step t also orders the
+    reads of step t-1 before the overwrite at step t+1, so one fence per step
+    suffices.
+
+    fence="device": an all_reduce of one element on the current stream (NCCL)
+    -- stream-ordered, no host sync.  fence="host": synchronize + barrier
+    (gloo; used where NCCL cannot run, e.g. two processes sharing one GPU)."""
+
+    def __init__(self, stride: int, k: int, group=None, fence: str = "device", buffers: int = 2):
+        import torch
+        import torch.distributed as dist
+        if fence not in ("device", "host"):
+            raise ValueError("fence must be 'device' or 'host'")
+        self.dist, self.group, self.fence = dist, group, fence
+        self.rank, self.world = dist.get_rank(group), dist.get_world_size(group)
+        if self.world > 8:
+            raise ValueError("peer SpMM maps at most 8 partitions")
+        self.stride, self.k, self.buffers = int(stride), int(k), int(buffers)
+        self.step = 0
+        lib = _lib.lib()
+        nbytes = self.stride * self.k * 4
+        dev = torch.device("cuda", torch.cuda.current_device())
+        self._own, self.views, handles = [], [], []
+        for _ in range(self.buffers):
+            p = _lib.C.c_void_p()
+            _lib.check(lib.sgnn_peer_alloc(nbytes, _lib.C.byref(p)), "peer_alloc")
+            self._own.append(p.value)
+            v = torch.as_tensor(_DeviceArray(p.value, (self.stride, self.k)), device=dev)
+            v.zero_()
+            self.views.append(v)
+            h = (_lib.C.c_char * 64)()
+            _lib.check(lib.sgnn_ipc_get_handle(p.value, h), "ipc_get_handle")
+            handles.append(bytes(h))
+        torch.cuda.synchronize()
+        gathered = [None] * self.world
+        dist.all_gather_object(gathered, handles, group=group)
+        self._opened = []
+        self.ptrs = [[0] * self.world for _ in range(self.buffers)]
+        for b in range(self.buffers):
+            for q in range(self.world):
+                if q == self.rank:
+                    self.ptrs[b][q] = self._own[b]
+                    continue
+                out = _lib.C.c_void_p()
+                h = (_lib.C.c_char * 64).from_buffer_copy(gathered[q][b])
+                _lib.check(lib.sgnn_ipc_open_handle(h, _lib.C.byref(out)), "ipc_open_handle")
+                self._opened.append(out.value)
+                self.ptrs[b][q] = out.value
+        if fence == "device":
+            self._token = torch.zeros(1, device=dev)
+        self._fence()
+
+    def _fence(self):
+        import torch
+        if self.fence == "device":
+            self.dist.all_reduce(self._token, group=self.group)
+        else:
+            torch.cuda.synchronize()
+            self.dist.barrier(group=self.group)
+
+    def publish(self, x_local):
+        """Write this rank's rows; returns the part pointer table to read."""
+        b = self.step % self.buffers
+        self.step += 1
+        self.views[b][: x_local.shape[0]].copy_(x_local)
+        self._fence()
+        return self.ptrs[b]
+
+    def close(self):
+        import torch
+        if self._own is None:
+            return
+        torch.cuda.synchronize()
+        self.dist.barrier(group=self.group)
+        lib = _lib.lib()
+        for p in self._opened:
+            lib.sgnn_ipc_close_handle(p)
+        self.dist.barrier(group=self.group)
+        self.views = []
+        for p in self._own:
+            lib.sgnn_peer_free(p)
+        self._own = None

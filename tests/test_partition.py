@@ -167,3 +167,103 @@ def test_loopback_partition_bitwise_equals_single_gpu(cuda, parts):
         gathered = partition.LoopbackExchange().all_gather(blocks)
         got = np.concatenate([r.compute(gathered, reduce).cpu().numpy() for r in ranks])
         np.testing.assert_array_equal(got.view(np.uint32), want.view(np.uint32))
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("parts", [1, 2, 3, 8])
+@pytest.mark.parametrize("k", [64, 128, 30])
+def test_peer_spmm_bitwise_equals_single_gpu(cuda, parts, k):
+    """sgnn_spmm_peer_f32 reading P separately allocated blocks (stand-ins for
+    the peers' HBM) reproduces the single-GPU SpMM bit for bit."""
+    import torch
+
+    from paper_2403_14853_b200 import graphs, ops, partition
+    n = 1 << 13
+    rp, ci = graphs.rmat(13, n * 24, seed=9, symmetrize=True, self_loops=True)
+    v = graphs.uniform(len(ci), 0.1, 1.0, 4)
+    x = torch.from_numpy(graphs.normal(n * k, 0, 1, 3).reshape(n, k)).cuda()
+    a = ops.CsrMatrix.from_numpy(rp, ci, v, n)
+    pt = partition.make_partition(rp, parts, pow2=True)
+    ranks = [partition.PartitionedSpmm(rp, ci, v, pt, p, k) for p in range(parts)]
+    blocks = [partition.pad_block(x[pt.rows(p)[0]:pt.rows(p)[1]], pt.stride) for p in range(parts)]
+    for reduce in ("sum", "mean"):
+        want = ops.spmm(a, x, reduce).cpu().numpy()
+        got = np.concatenate([r.compute_peer(blocks, reduce).cpu().numpy() for r in ranks])
+        np.testing.assert_array_equal(got.view(np.uint32), want.view(np.uint32))
+    # raw pointer table form
+    got0 = ranks[0].compute_peer([b.data_ptr() for b in blocks], "sum").cpu().numpy()
+    np.testing.assert_array_equal(got0.view(np.uint32), ops.spmm(a, x, "sum")[: pt.rows(0)[1]].cpu().numpy().view(np.uint32))
+
+
+@pytest.mark.gpu
+def test_peer_spmm_rejects_bad_arguments(cuda):
+    import torch
+
+    from paper_2403_14853_b200 import _lib, graphs, ops, partition
+    n = 1000
+    rp, ci = graphs.er(n, n, 8, seed=1)
+    v = np.ones(len(ci), np.float32)
+    pt = partition.make_partition(rp, 2, pow2=True)
+    r = partition.PartitionedSpmm(rp, ci, v, pt, 0, 32)
+    blocks = [torch.zeros((pt.stride, 32), device="cuda") for _ in range(2)]
+    with pytest.raises(_lib.UnsupportedError):
+        r.compute_peer(blocks, "max")
+    with pytest.raises(_lib.ShapeError):  # 1 part cannot cover 2*stride columns
+        ops.spmm_peer(r._a, blocks[:1], pt.shift, 32, "sum", r._plan)
+    with pytest.raises(ValueError):  # the peer path needs a pow2 stride
+        partition.RowPartition(pt.bounds, pt.stride - 1, n).shift
+
+
+def _ipc_worker(rank, world, port_, rp, ci, v, x, q):
+    import torch
+    import torch.distributed as dist
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port_))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_2403_14853_b200 import partition
+        torch.cuda.set_device(0)
+        k = x.shape[1]
+        pt = partition.make_partition(rp, world, pow2=True)
+        r = partition.PartitionedSpmm(rp, ci, v, pt, rank, k)
+        r0, r1 = pt.rows(rank)
+        blocks = partition.PeerBlocks(pt.stride, k, fence="host")
+        outs = []
+        for step in range(3):  # exercises both buffers and the reuse fence
+            xl = torch.from_numpy(x[r0:r1] * (step + 1)).cuda()
+            outs.append(r.forward_peer(xl, blocks, "sum").cpu().numpy())
+        blocks.close()
+        gathered = [None] * world
+        dist.all_gather_object(gathered, outs)
+        if rank == 0:
+            q.put([np.concatenate([g[s] for g in gathered]) for s in range(3)])
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.gpu
+def test_peer_blocks_ipc_two_processes(cuda):
+    """The IPC handshake of PeerBlocks: two processes share the one GPU (host
+    fences over gloo, so no kernel waits on another), each SpMM reads the
+    other's block through an IPC mapping; bitwise the single-process result."""
+    import torch
+    import torch.multiprocessing as mp
+
+    from paper_2403_14853_b200 import graphs, ops
+    n = 3000
+    rp, ci = graphs.er(n, n, 12, seed=2)
+    v = graphs.uniform(len(ci), -1.0, 1.0, 5)
+    x = graphs.normal(n * 64, 0, 1, 6).reshape(n, 64)
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port_ = _free_port()
+    procs = [ctx.Process(target=_ipc_worker, args=(r, 2, port_, rp, ci, v, x, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    got = q.get(timeout=240)
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    a = ops.CsrMatrix.from_numpy(rp, ci, v, n)
+    for s in range(3):
+        want = ops.spmm(a, torch.from_numpy(x * (s + 1)).cuda(), "sum").cpu().numpy()
+        np.testing.assert_array_equal(got[s].view(np.uint32), want.view(np.uint32))
