@@ -54,6 +54,8 @@ def parse():
     p.add_argument("--workload", choices=("cfg2", "cfg3", "cfg4", "cfg5"), default="cfg2",
                    help="cfg2 (default, the headline) | cfg3 GCN layer | cfg4 FusedMM/SDDMM | "
                         "cfg5 row-partitioned GraphSAGE-mean step")
+    p.add_argument("--exchange", choices=("peer", "nccl"), default="peer",
+                   help="cfg5 at N>1: SpMM reads peer feature blocks in place (peer) or NCCL all-gather")
     return p.parse_args()
 
 
@@ -604,7 +606,12 @@ def run_cfg5(args):
     dev = torch.device("cuda", local)
     w = graphs.cfg5(args.seed)
     n, k, hidden, classes = w.n_rows, w.k, 128, 16
-    ex = partition.NcclExchange() if ws > 1 else _LocalExchange()
+    if ws == 1:
+        ex = _LocalExchange()
+    elif args.exchange == "peer":
+        ex = partition.PeerExchange()
+    else:
+        ex = partition.NcclExchange()
     ar = (lambda t: (dist.all_reduce(t), t)[1]) if ws > 1 else (lambda t: t)
     ds = sage_dist.DistSage(w.row_ptr, w.col_idx, w.values, ws, rank, k, hidden, classes, "mean",
                             device=dev, exchange=ex, allreduce=ar)
@@ -641,7 +648,8 @@ def run_cfg5(args):
     cfg = {"workload": "cfg5: 2-layer GraphSAGE-mean training step, R-MAT 2^22 avg-deg 50 symmetrised + self "
                        "loops (dedup), X N(0,1) 2^22x128, hidden 128, 16 classes, uniform labels",
            "n_rows": n, "nnz": nnz, "K": k, "parallelism": f"1D row partition x{ws} (nnz-balanced), "
-           "all-gather of feature blocks", "partition_bounds": [int(b) for b in ds.part.bounds]}
+           ("SpMM reads peer feature blocks in place (CUDA IPC over NVLink)" if ws > 1 and args.exchange == "peer"
+            else "all-gather of feature blocks"), "partition_bounds": [int(b) for b in ds.part.bounds]}
     line = _base_line(args, ws, flops / ms / 1e6, ms, cfg, {
         "epoch_ms": round(ms, 3), "loss": loss, "scaling": "strong", "gpu_launches": steps * 12})
     line["steps"] = steps

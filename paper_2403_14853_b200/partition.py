@@ -146,6 +146,8 @@ class PartitionedSpmm:
 
     def forward(self, x_local, exchange, reduce="sum", out=None):
         """x_local: this rank's feature rows [r1-r0, K]."""
+        if isinstance(exchange, PeerExchange):
+            return self.forward_peer(x_local, exchange.blocks_for(self.part.stride, x_local.shape[1]), reduce, out)
         gathered = exchange.all_gather(pad_block(x_local, self.part.stride))
         return self.compute(gathered, reduce, out)
 
@@ -258,3 +260,24 @@ class PeerBlocks:
         for p in self._own:
             lib.sgnn_peer_free(p)
         self._own = None
+
+
+class PeerExchange:
+    """Exchange object for PartitionedSpmm.forward that selects the fused
+    peer-memory path: one PeerBlocks per (stride, K), created on first use
+    (collectively: every rank runs the same forward sequence)."""
+
+    def __init__(self, group=None, fence: str = "device"):
+        self.group, self.fence = group, fence
+        self._blocks = {}
+
+    def blocks_for(self, stride: int, k: int) -> PeerBlocks:
+        key = (int(stride), int(k))
+        if key not in self._blocks:
+            self._blocks[key] = PeerBlocks(stride, k, self.group, self.fence)
+        return self._blocks[key]
+
+    def close(self):
+        for b in self._blocks.values():
+            b.close()
+        self._blocks = {}

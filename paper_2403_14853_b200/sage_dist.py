@@ -1,8 +1,9 @@
 """Row-partitioned 2-layer GraphSAGE training step over P ranks (BASELINE cfg5,
 SURVEY 8e): the hot path (SpMM fwd x2, SpMM bwd x1 through the mean operand)
 on each rank's row block, the all-gather of feature blocks as the only
-sparse-path exchange, and an all-reduce of the dense weight gradients and the
-loss.  Mirrors gnn.hpp:234-244 (forward), :283-296 (backward), :318-349
+sparse-path exchange (NCCL all-gather, or partition.PeerExchange: the SpMM
+reads the other ranks' blocks in place over NVLink), and an all-reduce of the
+dense weight gradients and the loss.  Mirrors gnn.hpp:234-244 (forward), :283-296 (backward), :318-349
 (softmax_xent), :374-386 (sgd_step); with one rank it is exactly gnn.train's
 step.
 
@@ -44,11 +45,13 @@ class DistSage:
             raise NotImplementedError("the partitioned backward uses the symmetric short-circuit "
                                       "(gnn.hpp:152-153); cfg5 is symmetric")
         self.reduce = reduce
-        self.part = partition.make_partition(row_ptr, n_parts)
+        self.exchange = exchange or partition.NcclExchange()
+        # the peer path splits remapped columns with a shift: pow2 block stride
+        self.part = partition.make_partition(row_ptr, n_parts,
+                                             pow2=isinstance(self.exchange, partition.PeerExchange))
         self.rank = rank
         self.r0, self.r1 = self.part.rows(rank)
         self.device = device
-        self.exchange = exchange or partition.NcclExchange()
         self.allreduce = allreduce or _nccl_allreduce
         bwd_vals = mean_operand_values(row_ptr, col_idx, values) if reduce == "mean" else values
         self.fwd = partition.PartitionedSpmm(row_ptr, col_idx, values, self.part, rank, k_in, device, compute)

@@ -267,3 +267,67 @@ def test_peer_blocks_ipc_two_processes(cuda):
     for s in range(3):
         want = ops.spmm(a, torch.from_numpy(x * (s + 1)).cuda(), "sum").cpu().numpy()
         np.testing.assert_array_equal(got[s].view(np.uint32), want.view(np.uint32))
+
+
+def _sage_peer_worker(rank, world, port_, q):
+    import torch
+    import torch.distributed as dist
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port_))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from conftest import load_golden
+
+        from paper_2403_14853_b200 import partition, sage_dist
+        torch.cuda.set_device(0)
+        g = load_golden("gnn_planted")
+        rp, ci, v, x = g["row_ptr"], g["col_idx"], g["values"], g["x"]
+        n, f = x.shape
+        hidden, classes = 32, 4
+
+        def allreduce(t):  # gloo reduces host tensors
+            h = t.cpu()
+            dist.all_reduce(h)
+            return h.to(t.device)
+        ex = partition.PeerExchange(fence="host")
+        ds = sage_dist.DistSage(rp, ci, v, world, rank, f, hidden, classes, "mean", device="cuda",
+                                exchange=ex, allreduce=allreduce)
+        assert ds.part.stride & (ds.part.stride - 1) == 0
+        w0 = g["sage-mean_w0"]
+        o = [0]
+
+        def take(r, c):
+            t = torch.from_numpy(w0[o[0]:o[0] + r * c].reshape(r, c).copy()).cuda()
+            o[0] += r * c
+            return t
+        params = sage_dist.SageParams(take(f, hidden), take(hidden, classes), take(f, hidden), take(hidden, classes))
+        r0, r1 = ds.r0, ds.r1
+        xl = torch.from_numpy(x[r0:r1].copy()).cuda()
+        lab = torch.from_numpy(g["labels"][r0:r1].astype(np.int64)).cuda()
+        mask = torch.from_numpy(g["mask"][r0:r1].copy()).cuda()
+        losses = [ds.step(params, xl, lab, mask, 0.05, int(g["mask"].sum())) for _ in range(6)]
+        ex.close()
+        if rank == 0:
+            q.put(losses)
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.gpu
+def test_two_rank_sage_peer_exchange_matches_reference(cuda):
+    """cfg5's step with the fused peer exchange (two processes on one GPU,
+    IPC-mapped blocks, host fences): losses track the reference's train()."""
+    import torch.multiprocessing as mp
+
+    from conftest import load_golden
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port_ = _free_port()
+    procs = [ctx.Process(target=_sage_peer_worker, args=(r, 2, port_, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    losses = q.get(timeout=240)
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    want = load_golden("gnn_planted")["sage-mean_losses"][:6]
+    np.testing.assert_allclose(losses, want, rtol=2e-3, atol=1e-5)
