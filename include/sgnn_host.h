@@ -61,6 +61,39 @@ uint64_t sgnn_host_partition_block(const uint64_t* rp, const uint32_t* ci, const
                                    const uint32_t* bounds, int n_parts, int part, uint32_t stride,
                                    uint64_t* out_rp, uint32_t* out_ci, float* out_v, int threads);
 
+/* ---- on-disk formats either side of the path (io.hpp:80-262) ------------
+ * Status: 0 ok, 3 config (dimensions / memory), 5 IoError, 6 ParseError.
+ * On failure `err` receives the reference's message (without the "line N: "
+ * prefix ParseError adds) and *err_line the 1-based line (0 when none). */
+
+/* load_mtx (io.hpp:80-165): coordinate real|integer|pattern,
+ * general|symmetric; 1-based -> 0-based, pattern values 1, symmetric files
+ * expanded to both triangles, duplicates summed (fp32, in file order).  Entry
+ * lines are parsed by `threads` host threads (<= 0: all cores).  The CSR is
+ * held behind the handle: sgnn_host_csr_dims / _export / _free. */
+int sgnn_host_mtx_load(const char* path, int threads, void** out, char* err, size_t err_len, long* err_line);
+void sgnn_host_csr_dims(void* h, uint32_t* n_rows, uint32_t* n_cols, uint64_t* nnz);
+void sgnn_host_csr_export(void* h, uint64_t* rp, uint32_t* ci, float* v);
+void sgnn_host_csr_free(void* h);
+
+/* save_mtx (io.hpp:168-185): coordinate real general, values "%.9g" (fp32
+ * max_digits10), so a load round trip is exact. */
+int sgnn_host_mtx_save(const char* path, uint32_t n_rows, uint32_t n_cols, const uint64_t* rp,
+                       const uint32_t* ci, const float* v, int threads, char* err, size_t err_len);
+
+/* load_features (io.hpp:187-205): header "n k", then n non-empty lines of k
+ * decimals. */
+int sgnn_host_features_load(const char* path, int threads, void** out, char* err, size_t err_len,
+                            long* err_line);
+void sgnn_host_dense_dims(void* h, uint32_t* rows, uint32_t* cols);
+void sgnn_host_dense_export(void* h, float* out);
+void sgnn_host_dense_free(void* h);
+
+/* load_labels (kind 0, io.hpp:243-251) / load_mask (kind 1, :254-262):
+ * header "n", then n integers.  out == NULL: count only (*n). */
+int sgnn_host_int_column_load(const char* path, int kind, uint64_t max_n, uint32_t* out, uint64_t* n,
+                              char* err, size_t err_len, long* err_line);
+
 #ifdef __cplusplus
 }
 #endif

@@ -274,3 +274,85 @@ class Bench:
 
     def __del__(self):
         self.close()
+
+
+# ---- on-disk formats (io.hpp:80-262) through the reference's own loaders ----
+class RefError(Exception):
+    """A reference exception: .status (5 IoError, 6 ParseError), .what, .line."""
+
+    def __init__(self, status, what, line):
+        super().__init__(f"[{status}] {what}")
+        self.status, self.what, self.line = status, what, line
+
+
+def _io_sigs(L):
+    if getattr(L, "_io_ready", False):
+        return L
+    P, s, cp, sz, lp = C.c_void_p, C.c_char_p, C.c_char_p, C.c_size_t, C.POINTER(C.c_long)
+    L.ref_load_mtx.argtypes = [s, C.POINTER(P), cp, sz, lp]
+    L.ref_csr_dims.argtypes = [P, C.POINTER(C.c_uint32), C.POINTER(C.c_uint32), C.POINTER(C.c_uint64)]
+    L.ref_csr_export.argtypes = [P, P, P, P]
+    L.ref_csr_free.argtypes = [P]
+    L.ref_save_mtx.argtypes = [s, C.c_uint32, C.c_uint32, P, P, P, cp, sz]
+    L.ref_load_features.argtypes = [s, C.POINTER(P), cp, sz, lp]
+    L.ref_dense_dims.argtypes = [P, C.POINTER(C.c_uint32), C.POINTER(C.c_uint32)]
+    L.ref_dense_export.argtypes = [P, P]
+    L.ref_dense_free.argtypes = [P]
+    L.ref_load_int_column.argtypes = [s, C.c_int, P, C.POINTER(C.c_uint64), cp, sz, lp]
+    L._io_ready = True
+    return L
+
+
+def _fail(st, err, line):
+    raise RefError(st, err.value.decode(errors="replace"), int(line.value))
+
+
+def load_mtx(path):
+    """(n_rows, n_cols, rp, ci, v) from the reference's load_mtx<float>."""
+    L = _io_sigs(lib())
+    h, err, line = C.c_void_p(), C.create_string_buffer(4096), C.c_long(0)
+    st = L.ref_load_mtx(os.fsencode(path), C.byref(h), err, 4096, C.byref(line))
+    if st:
+        _fail(st, err, line)
+    m, n, nnz = C.c_uint32(), C.c_uint32(), C.c_uint64()
+    L.ref_csr_dims(h, C.byref(m), C.byref(n), C.byref(nnz))
+    rp = np.empty(m.value + 1, np.uint64)
+    ci = np.empty(nnz.value, np.uint32)
+    v = np.empty(nnz.value, np.float32)
+    L.ref_csr_export(h, rp.ctypes.data, ci.ctypes.data, v.ctypes.data)
+    L.ref_csr_free(h)
+    return m.value, n.value, rp, ci, v
+
+
+def save_mtx(path, n_rows, n_cols, rp, ci, v):
+    L = _io_sigs(lib())
+    rp, ci, v = _csr(rp, ci, v, np.float32)
+    err = C.create_string_buffer(4096)
+    st = L.ref_save_mtx(os.fsencode(path), n_rows, n_cols, rp.ctypes.data, ci.ctypes.data, v.ctypes.data, err, 4096)
+    if st:
+        _fail(st, err, C.c_long(0))
+
+
+def load_features(path):
+    L = _io_sigs(lib())
+    h, err, line = C.c_void_p(), C.create_string_buffer(4096), C.c_long(0)
+    st = L.ref_load_features(os.fsencode(path), C.byref(h), err, 4096, C.byref(line))
+    if st:
+        _fail(st, err, line)
+    r, c = C.c_uint32(), C.c_uint32()
+    L.ref_dense_dims(h, C.byref(r), C.byref(c))
+    out = np.empty((r.value, c.value), np.float32)
+    L.ref_dense_export(h, out.ctypes.data)
+    L.ref_dense_free(h)
+    return out
+
+
+def load_int_column(path, kind):
+    L = _io_sigs(lib())
+    err, line, n = C.create_string_buffer(4096), C.c_long(0), C.c_uint64()
+    st = L.ref_load_int_column(os.fsencode(path), kind, None, C.byref(n), err, 4096, C.byref(line))
+    if st:
+        _fail(st, err, line)
+    out = np.empty(n.value, np.uint32)
+    L.ref_load_int_column(os.fsencode(path), kind, out.ctypes.data, C.byref(n), err, 4096, C.byref(line))
+    return out

@@ -370,4 +370,102 @@ void ref_dataset_export(void* h, uint64_t* rp, uint32_t* ci, float* v, float* x,
 }
 void ref_dataset_free(void* h) { delete static_cast<Dataset<float>*>(h); }
 
+// ---- on-disk formats (io.hpp:80-262) ------------------------------------------
+// Each loader returns 0, 5 (IoError) or 6 (ParseError, *line = e.line()), with
+// e.what() copied into err.
+namespace {
+int io_status(const std::exception& e, char* err, size_t err_len, long* line) {
+    if (err && err_len) {
+        std::strncpy(err, e.what(), err_len - 1);
+        err[err_len - 1] = 0;
+    }
+    if (auto* p = dynamic_cast<const ParseError*>(&e)) {
+        if (line) *line = p->line();
+        return 6;
+    }
+    if (line) *line = 0;
+    if (dynamic_cast<const IoError*>(&e)) return 5;
+    return status_of(e);
+}
+}  // namespace
+
+int ref_load_mtx(const char* path, void** out, char* err, size_t err_len, long* line) {
+    try {
+        *out = new CsrMatrix<float>(load_mtx<float>(path));
+        return 0;
+    } catch (const std::exception& e) {
+        *out = nullptr;
+        return io_status(e, err, err_len, line);
+    }
+}
+
+void ref_csr_dims(void* h, uint32_t* m, uint32_t* n, uint64_t* nnz) {
+    auto* a = static_cast<CsrMatrix<float>*>(h);
+    *m = a->n_rows;
+    *n = a->n_cols;
+    *nnz = a->nnz();
+}
+
+void ref_csr_export(void* h, uint64_t* rp, uint32_t* ci, float* v) {
+    auto* a = static_cast<CsrMatrix<float>*>(h);
+    std::memcpy(rp, a->row_ptr.data(), sizeof(uint64_t) * a->row_ptr.size());
+    std::memcpy(ci, a->col_idx.data(), sizeof(uint32_t) * a->col_idx.size());
+    std::memcpy(v, a->values.data(), sizeof(float) * a->values.size());
+}
+
+void ref_csr_free(void* h) { delete static_cast<CsrMatrix<float>*>(h); }
+
+int ref_save_mtx(const char* path, uint32_t m, uint32_t n, const uint64_t* rp, const uint32_t* ci, const float* v,
+                 char* err, size_t err_len) {
+    try {
+        save_mtx(make_csr<float>(m, n, rp, ci, v), path);
+        return 0;
+    } catch (const std::exception& e) {
+        return io_status(e, err, err_len, nullptr);
+    }
+}
+
+int ref_load_features(const char* path, void** out, char* err, size_t err_len, long* line) {
+    try {
+        *out = new DenseMatrix<float>(load_features<float>(path));
+        return 0;
+    } catch (const std::exception& e) {
+        *out = nullptr;
+        return io_status(e, err, err_len, line);
+    }
+}
+
+void ref_dense_dims(void* h, uint32_t* r, uint32_t* c) {
+    auto* d = static_cast<DenseMatrix<float>*>(h);
+    *r = d->n_rows;
+    *c = d->n_cols;
+}
+
+void ref_dense_export(void* h, float* out) {
+    auto* d = static_cast<DenseMatrix<float>*>(h);
+    std::memcpy(out, d->data.data(), sizeof(float) * d->data.size());
+}
+
+void ref_dense_free(void* h) { delete static_cast<DenseMatrix<float>*>(h); }
+
+// kind 0: load_labels, 1: load_mask; out may be NULL (count only)
+int ref_load_int_column(const char* path, int kind, uint32_t* out, uint64_t* n, char* err, size_t err_len,
+                        long* line) {
+    try {
+        if (kind == 0) {
+            auto l = load_labels(path);
+            *n = l.size();
+            if (out) std::memcpy(out, l.data(), sizeof(uint32_t) * l.size());
+        } else {
+            auto m = load_mask(path);
+            *n = m.size();
+            if (out)
+                for (size_t i = 0; i < m.size(); ++i) out[i] = m[i];
+        }
+        return 0;
+    } catch (const std::exception& e) {
+        return io_status(e, err, err_len, line);
+    }
+}
+
 }  // extern "C"

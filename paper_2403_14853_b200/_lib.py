@@ -42,7 +42,11 @@ class IoError(Error):
 
 
 class ParseError(Error):
-    """error.hpp:46-55"""
+    """error.hpp:46-55: what() is "line N: <message>", .line is N."""
+
+    def __init__(self, what: str, line: int = 0):
+        super().__init__(f"line {line}: {what}")
+        self.line = line
 
 
 class InternalError(Error):
@@ -140,6 +144,18 @@ HOST_SIGNATURES = {
     "sgnn_host_rmat_free": (None, [P]),
     "sgnn_host_balanced_row_partition": (None, [P, u32, i32, P]),
     "sgnn_host_partition_block": (u64, [P, P, P, P, i32, i32, u32, P, P, P, i32]),
+    "sgnn_host_mtx_load": (i32, [C.c_char_p, i32, C.POINTER(P), C.c_char_p, C.c_size_t, C.POINTER(C.c_long)]),
+    "sgnn_host_csr_dims": (None, [P, C.POINTER(u32), C.POINTER(u32), C.POINTER(u64)]),
+    "sgnn_host_csr_export": (None, [P, P, P, P]),
+    "sgnn_host_csr_free": (None, [P]),
+    "sgnn_host_mtx_save": (i32, [C.c_char_p, u32, u32, P, P, P, i32, C.c_char_p, C.c_size_t]),
+    "sgnn_host_features_load": (i32, [C.c_char_p, i32, C.POINTER(P), C.c_char_p, C.c_size_t,
+                                      C.POINTER(C.c_long)]),
+    "sgnn_host_dense_dims": (None, [P, C.POINTER(u32), C.POINTER(u32)]),
+    "sgnn_host_dense_export": (None, [P, P]),
+    "sgnn_host_dense_free": (None, [P]),
+    "sgnn_host_int_column_load": (i32, [C.c_char_p, i32, u64, P, C.POINTER(u64), C.c_char_p, C.c_size_t,
+                                        C.POINTER(C.c_long)]),
 }
 
 _lock = threading.Lock()

@@ -22,12 +22,7 @@ PLAN_FIELDS = ("lanes", "vec", "unroll", "path_items", "split_rows_over", "k_til
                "occupancy")
 
 
-class ParseError(ValueError):
-    """ParseError (error.hpp:46-55): carries the 1-based line number."""
-
-    def __init__(self, what, line):
-        super().__init__(f"line {line}: {what}")
-        self.line = line
+from ._lib import IoError, ParseError  # noqa: E402  (error.hpp:40-55)
 
 
 @dataclass
@@ -82,7 +77,7 @@ def load_report(path) -> LoadedReport:
     try:
         lines = open(path).read().split("\n")
     except OSError as ex:
-        raise FileNotFoundError(f"cannot open '{path}'") from ex
+        raise IoError(f"cannot open '{path}'") from ex
     if not lines or lines[0] == "" and len(lines) == 1:
         raise ParseError("empty report file", 1)
     if lines[0] != HEADER:
