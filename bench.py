@@ -54,7 +54,7 @@ def parse():
     p.add_argument("--workload", choices=("cfg2", "cfg3", "cfg4", "cfg5"), default="cfg2",
                    help="cfg2 (default, the headline) | cfg3 GCN layer | cfg4 FusedMM/SDDMM | "
                         "cfg5 row-partitioned GraphSAGE-mean step")
-    p.add_argument("--exchange", choices=("peer", "nccl"), default="peer",
+    p.add_argument("--exchange", choices=("peer", "nccl"), default="nccl",
                    help="cfg5 at N>1: SpMM reads peer feature blocks in place (peer) or NCCL all-gather")
     return p.parse_args()
 
