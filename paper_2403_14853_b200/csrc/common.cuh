@@ -88,5 +88,62 @@ __device__ __forceinline__ uint64_t shfl_u64(unsigned mask, uint64_t v, int src,
 __device__ __forceinline__ uint32_t ld_stream(const uint32_t* p) { return __ldcs(p); }
 __device__ __forceinline__ float ld_stream(const float* p) { return __ldcs(p); }
 
+// Packed fp32 pair arithmetic (FADD2 / FFMA2 on sm_100): each lane of the
+// pair is an ordinary IEEE round-to-nearest add / fma, so results are those
+// of the scalar ops.  (A packed multiply is not used: ptxas contracts
+// mul.rn.f32x2 + add.rn.f32x2 into FFMA2, which would change the rounding.)
+__device__ __forceinline__ void add2_rn(float& a0, float& a1, float b0, float b1) {
+    uint64_t a, b;
+    asm("mov.b64 %0, {%1,%2};" : "=l"(a) : "f"(a0), "f"(a1));
+    asm("mov.b64 %0, {%1,%2};" : "=l"(b) : "f"(b0), "f"(b1));
+    asm("add.rn.f32x2 %0, %1, %2;" : "=l"(a) : "l"(a), "l"(b));
+    asm("mov.b64 {%0,%1}, %2;" : "=f"(a0), "=f"(a1) : "l"(a));
+}
+// (a0, a1) = fma((s, s), (y0, y1), (a0, a1))
+__device__ __forceinline__ void fma2_rn(float& a0, float& a1, float s, float y0, float y1) {
+    uint64_t a, y, ss;
+    asm("mov.b64 %0, {%1,%2};" : "=l"(a) : "f"(a0), "f"(a1));
+    asm("mov.b64 %0, {%1,%2};" : "=l"(y) : "f"(y0), "f"(y1));
+    asm("mov.b64 %0, {%1,%1};" : "=l"(ss) : "f"(s));
+    asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(a) : "l"(ss), "l"(y), "l"(a));
+    asm("mov.b64 {%0,%1}, %2;" : "=f"(a0), "=f"(a1) : "l"(a));
+}
+
+// L2 policy for gathered operand rows (reused across the whole launch):
+// evict-last, so the streamed CSR arrays and the output do not push them out.
+__device__ __forceinline__ uint64_t gather_policy() {
+    uint64_t p = 0;
+#if defined(SGNN_GATHER_EVICT_LAST)
+    asm("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+#endif
+    return p;
+}
+__device__ __forceinline__ float4 ld_gather(const float4* ptr, uint64_t pol) {
+#if defined(SGNN_GATHER_EVICT_LAST)
+    float4 v;
+#if defined(SGNN_GATHER_L1_NO_ALLOCATE)
+    asm("ld.global.nc.L1::no_allocate.L2::cache_hint.v4.f32 {%0,%1,%2,%3}, [%4], %5;"
+        : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "l"(ptr), "l"(pol));
+#else
+    asm("ld.global.nc.L2::cache_hint.v4.f32 {%0,%1,%2,%3}, [%4], %5;"
+        : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "l"(ptr), "l"(pol));
+#endif
+    return v;
+#else
+    (void)pol;
+    return __ldg(ptr);
+#endif
+}
+__device__ __forceinline__ float ld_gather(const float* ptr, uint64_t pol) {
+#if defined(SGNN_GATHER_EVICT_LAST)
+    float v;
+    asm("ld.global.nc.L2::cache_hint.f32 %0, [%1], %2;" : "=f"(v) : "l"(ptr), "l"(pol));
+    return v;
+#else
+    (void)pol;
+    return __ldg(ptr);
+#endif
+}
+
 }  // namespace dev
 }  // namespace sgnn

@@ -97,6 +97,7 @@ __global__ void __launch_bounds__(128) sddmm_kernel(const SddmmArgs a) {
             xrow.load(a.x + uint64_t(r) * a.ld, gl, a.k);
         };
         if (E) load_cv(0);
+        const uint64_t l2pol = dev::gather_policy();
         for (uint32_t base = 0; base < E; base += U) {
             const int n = (E - base) < uint32_t(U) ? int(E - base) : U;
             F yf[U];
@@ -106,8 +107,8 @@ __global__ void __launch_bounds__(128) sddmm_kernel(const SddmmArgs a) {
                 const uint32_t col = __shfl_sync(gmask, cc[u / G], u % G, G);
                 pv[u] = __shfl_sync(gmask, vv[u / G], u % G, G);
                 const float* lrow = reinterpret_cast<const float*>(ylane + uint64_t(col) * ldb);
-                if (full) yf[u].template gather<false>(lrow, nq);
-                else yf[u].template gather<true>(lrow, nq);
+                if (full) yf[u].template gather<false>(lrow, nq, l2pol);
+                else yf[u].template gather<true>(lrow, nq, l2pol);
             }
             if (base + U < E) load_cv(base + U);
             float res[CH];

@@ -81,6 +81,30 @@ struct Reducer {
         if (RED == SGNN_REDUCE_SUM || RED == SGNN_REDUCE_MEAN) return __fmaf_rn(s, y, acc);
         return fold(acc, s, y, first);
     }
+    // Whole-fragment folds: acc[i] = fold(acc[i], s, x[i]) for every i, in
+    // packed pairs where the op allows (same per-element rounding).
+    template <int N>
+    static __device__ __forceinline__ void fold_all(float (&acc)[N], float s, const float (&x)[N], bool first) {
+        if constexpr ((RED == SGNN_REDUCE_SUM || RED == SGNN_REDUCE_MEAN) && N % 2 == 0) {
+#ifndef SGNN_EXPERIMENT_FMA_FOLD
+#pragma unroll
+            for (int i = 0; i < N; i += 2) add2_rn(acc[i], acc[i + 1], __fmul_rn(s, x[i]), __fmul_rn(s, x[i + 1]));
+            return;
+#endif
+        }
+#pragma unroll
+        for (int i = 0; i < N; ++i) acc[i] = fold(acc[i], s, x[i], first);
+    }
+    template <int N>
+    static __device__ __forceinline__ void fold_fused_all(float (&acc)[N], float s, const float (&y)[N], bool first) {
+        if constexpr ((RED == SGNN_REDUCE_SUM || RED == SGNN_REDUCE_MEAN) && N % 2 == 0) {
+#pragma unroll
+            for (int i = 0; i < N; i += 2) fma2_rn(acc[i], acc[i + 1], s, y[i], y[i + 1]);
+        } else {
+#pragma unroll
+            for (int i = 0; i < N; ++i) acc[i] = fold_fused(acc[i], s, y[i], first);
+        }
+    }
     // canonical combine of consecutive segment partials (left to right)
     static __device__ __forceinline__ float combine(float t, float s) {
         if (RED == SGNN_REDUCE_SUM || RED == SGNN_REDUCE_MEAN) return __fadd_rn(t, s);
@@ -133,7 +157,7 @@ struct Frag {
     // lane's first element; blocks beyond nq are skipped (ZERO: zero-filled,
     // needed where all lanes' values are summed, i.e. the FusedMM dot).
     template <bool ZERO>
-    __device__ __forceinline__ void gather(const float* __restrict__ lrow, int nq) {
+    __device__ __forceinline__ void gather(const float* __restrict__ lrow, int nq, uint64_t pol) {
         if constexpr (!ZERO) {
             // Unpredicated: blocks beyond the width re-read block 0 (the lane
             // base is clamped inside the row), their values are never stored.
@@ -141,10 +165,10 @@ struct Frag {
             for (int q = 0; q < V; ++q) {
                 const int qe = (q < nq) ? q : 0;
                 if constexpr (VEC) {
-                    const float4 t = __ldg(reinterpret_cast<const float4*>(lrow + 4 * G * qe));
+                    const float4 t = ld_gather(reinterpret_cast<const float4*>(lrow + 4 * G * qe), pol);
                     v[4 * q + 0] = t.x; v[4 * q + 1] = t.y; v[4 * q + 2] = t.z; v[4 * q + 3] = t.w;
                 } else {
-                    v[q] = __ldg(lrow + G * qe);
+                    v[q] = ld_gather(lrow + G * qe, pol);
                 }
             }
             return;
@@ -153,10 +177,10 @@ struct Frag {
         for (int q = 0; q < V; ++q) {
             if (q < nq) {
                 if constexpr (VEC) {
-                    const float4 t = __ldg(reinterpret_cast<const float4*>(lrow + 4 * G * q));
+                    const float4 t = ld_gather(reinterpret_cast<const float4*>(lrow + 4 * G * q), pol);
                     v[4 * q + 0] = t.x; v[4 * q + 1] = t.y; v[4 * q + 2] = t.z; v[4 * q + 3] = t.w;
                 } else {
-                    v[q] = __ldg(lrow + G * q);
+                    v[q] = ld_gather(lrow + G * q, pol);
                 }
             } else if constexpr (ZERO) {
 #pragma unroll
@@ -319,23 +343,32 @@ __global__ void __launch_bounds__(128, MINB) spmm_worker_kernel(const SpmmArgs a
         }
     };
     const int nq = F::blocks_in(gl, a.width);
+    const uint64_t l2pol = dev::gather_policy();
     const bool full = a.width == uint32_t(F::W * G * V);  // every lane's blocks are in range
 
     for (uint32_t w = (blockIdx.x * blockDim.x + threadIdx.x) / G; w < a.n_workers; w += n_groups) {
         const uint32_t i0 = __ldg(a.wrow + w), i1 = __ldg(a.wrow + w + 1);
-        const uint64_t j0 = __ldg(a.wnz + w), j1 = __ldg(a.wnz + w + 1);
-        const uint32_t E = uint32_t(j1 - j0);  // nonzeros of this worker; hot loop is 32-bit local
+        const uint64_t j0 = __ldg(a.wnz + w);
+        const uint32_t E = uint32_t(__ldg(a.wnz + w + 1) - j0);  // nonzeros of this worker
         uint32_t slot = a.wslot ? __ldg(a.wslot + w) : 0u;
 
-        // row_ptr window: lane gl holds rp[rb + 1 + gl] (row ends of rows rb..rb+G-1)
+        // All row bookkeeping is in 32-bit positions local to the worker
+        // (j0-relative, clamped to E): every row r >= i0 ends at or after j0.
+        // Lane gl of the window holds the local end of row rb + gl.
+        auto window = [&](uint32_t rb_) -> uint32_t {
+            const uint64_t e = __ldg(a.rp + min(rb_ + 1 + uint32_t(gl), a.n_rows));
+            return uint32_t(min(e - j0, uint64_t(E)));
+        };
         uint32_t r = i0;
         uint32_t rb = r;
-        uint64_t rwin = __ldg(a.rp + min(rb + 1 + uint32_t(gl), a.n_rows));
-        uint64_t rstart = __ldg(a.rp + r);
-        uint64_t rend = dev::shfl_u64(gmask, rwin, 0, G);
-        bool inside = (rstart >= j0) && (rend <= j1);
-        // local (j0-relative) row end and segment end, clamped to E
-        uint32_t rend_l = uint32_t(min(rend, j1) - j0);
+        uint32_t rwin = window(rb);
+        // Row i0 may have begun in an earlier worker (plan.cuh: then j0 sits on
+        // one of its segment boundaries); rows i0 < r < i1 lie entirely inside
+        // [j0, j1), row i1 is the head of a row finished elsewhere.
+        const bool head_cut = __ldg(a.rp + i0) < j0;
+        bool inside = !head_cut && r < i1;
+        uint32_t rs_l = 0;                                  // local start of row r
+        uint32_t rend_l = __shfl_sync(gmask, rwin, 0, G);   // local end of row r
         uint32_t seg_l = min(uint32_t(SEG), rend_l);
         uint32_t next_l = 0;  // next local position needing row/segment work (0: settle first)
         bool first = true;
@@ -372,7 +405,7 @@ __global__ void __launch_bounds__(128, MINB) spmm_worker_kernel(const SpmmArgs a
         };
         auto finish_row = [&]() {  // row r has no more nonzeros in this worker
             if (inside) {
-                const uint64_t deg = rend - rstart;
+                const uint64_t deg = rend_l - rs_l;  // the whole row is local
                 float* crow = a.c + uint64_t(r) * a.ldc;
                 if (have_tot) {
                     F t;
@@ -389,15 +422,14 @@ __global__ void __launch_bounds__(128, MINB) spmm_worker_kernel(const SpmmArgs a
         };
         auto advance_row = [&]() {
             ++r;
-            rstart = rend;
+            rs_l = rend_l;
             if (r - rb >= uint32_t(G)) {
                 rb = r;
-                rwin = __ldg(a.rp + min(rb + 1 + uint32_t(gl), a.n_rows));
+                rwin = window(rb);
             }
-            rend = dev::shfl_u64(gmask, rwin, int(r - rb), G);
-            inside = (rstart >= j0) && (rend <= j1);
-            rend_l = uint32_t(min(rend, j1) - j0);
-            seg_l = uint32_t(min(rstart + SEG, min(rend, j1)) - j0);
+            rend_l = __shfl_sync(gmask, rwin, int(r - rb), G);
+            inside = r < i1;
+            seg_l = min(rs_l + uint32_t(SEG), rend_l);
             first = true;
             have_tot = false;
             acc.zero();
@@ -446,8 +478,8 @@ __global__ void __launch_bounds__(128, MINB) spmm_worker_kernel(const SpmmArgs a
                 av[u] = __shfl_sync(gmask, vv[u / G], u % G, G);
                 const float* lrow = row_addr(col);
                 // the FusedMM dot sums all lanes: zero-fill blocks past a partial width
-                if (!is_fused<OP>() || full) xf[u].template gather<false>(lrow, nq);
-                else xf[u].template gather<true>(lrow, nq);
+                if (!is_fused<OP>() || full) xf[u].template gather<false>(lrow, nq, l2pol);
+                else xf[u].template gather<true>(lrow, nq, l2pol);
             }
             if (base + CHUNK < E) load_cv(base + CHUNK);
             auto fold = [&](const F& xv, float pv) {
@@ -456,10 +488,8 @@ __global__ void __launch_bounds__(128, MINB) spmm_worker_kernel(const SpmmArgs a
                     // s_ij = combine(p_ij, <X_i, Y_j>); Y_j is reused below (read once)
                     s = edge_value<OP>(pv, group_dot(xrow, xv, gmask));
                 }
-#pragma unroll
-                for (int i = 0; i < N; ++i)
-                    acc.v[i] = is_fused<OP>() ? R::fold_fused(acc.v[i], s, xv.v[i], first)
-                                              : R::fold(acc.v[i], s, xv.v[i], first);
+                if constexpr (is_fused<OP>()) R::fold_fused_all(acc.v, s, xv.v, first);
+                else R::fold_all(acc.v, s, xv.v, first);
                 first = false;
             };
             if (base + uint32_t(n) <= next_l) {
@@ -485,8 +515,7 @@ __global__ void __launch_bounds__(128, MINB) spmm_worker_kernel(const SpmmArgs a
 #pragma unroll
                     for (int u = 0; u < U; ++u) {
                         if (u < n) {
-#pragma unroll
-                            for (int i = 0; i < N; ++i) acc.v[i] = R::fold_fused(acc.v[i], sv[u], xf[u].v[i], first);
+                            R::fold_fused_all(acc.v, sv[u], xf[u].v, first);
                             first = false;
                         }
                     }
@@ -512,7 +541,7 @@ __global__ void __launch_bounds__(128, MINB) spmm_worker_kernel(const SpmmArgs a
             finish_row();
             advance_row();
         }
-        if (r < a.n_rows && j1 > max(j0, rstart)) store_slot(acc);  // head of a split row
+        if (r < a.n_rows && E > rs_l) store_slot(acc);  // head of a split row
     }
 }
 
