@@ -647,7 +647,7 @@ def run_cfg5(args):
     flops = 3 * 2 * nnz * k  # 2 forward + 1 backward SpMM (gnn.hpp:237,241,290)
     cfg = {"workload": "cfg5: 2-layer GraphSAGE-mean training step, R-MAT 2^22 avg-deg 50 symmetrised + self "
                        "loops (dedup), X N(0,1) 2^22x128, hidden 128, 16 classes, uniform labels",
-           "n_rows": n, "nnz": nnz, "K": k, "parallelism": f"1D row partition x{ws} (nnz-balanced), "
+           "n_rows": n, "nnz": nnz, "K": k, "parallelism": f"1D row partition x{ws} (nnz-balanced), " +
            ("SpMM reads peer feature blocks in place (CUDA IPC over NVLink)" if ws > 1 and args.exchange == "peer"
             else "all-gather of feature blocks"), "partition_bounds": [int(b) for b in ds.part.bounds]}
     line = _base_line(args, ws, flops / ms / 1e6, ms, cfg, {

@@ -233,19 +233,23 @@ constexpr bool is_fused() { return OP == OP_FUSED_MUL || OP == OP_FUSED_SIGMOID;
 // over v (high v bit first), then across lanes xor G/2, G/4, ..., 1.  It is
 // the same tree for every (G, V) layout, so FusedMM/SDDMM results do not
 // depend on the plan.
+// Blocks q >= nq (past the launch width) are zero leaves: masked here, so
+// the operands' out-of-width registers may hold anything.
 template <int G, int V, bool VEC>
-__device__ __forceinline__ float lane_leaf(const Frag<G, V, VEC>& a, const Frag<G, V, VEC>& b) {
+__device__ __forceinline__ float lane_leaf(const Frag<G, V, VEC>& a, const Frag<G, V, VEC>& b, int nq = V) {
     float p[V];
 #pragma unroll
     for (int q = 0; q < V; ++q) {
+        float t;
         if constexpr (VEC) {
-            float t = __fmul_rn(a.v[4 * q], b.v[4 * q]);
+            t = __fmul_rn(a.v[4 * q], b.v[4 * q]);
             t = __fmaf_rn(a.v[4 * q + 1], b.v[4 * q + 1], t);
             t = __fmaf_rn(a.v[4 * q + 2], b.v[4 * q + 2], t);
-            p[q] = __fmaf_rn(a.v[4 * q + 3], b.v[4 * q + 3], t);
+            t = __fmaf_rn(a.v[4 * q + 3], b.v[4 * q + 3], t);
         } else {
-            p[q] = __fmul_rn(a.v[q], b.v[q]);
+            t = __fmul_rn(a.v[q], b.v[q]);
         }
+        p[q] = (q < nq) ? t : 0.0f;
     }
 #pragma unroll
     for (int half = V / 2; half >= 1; half >>= 1)  // v tree, high bit first
@@ -257,8 +261,8 @@ __device__ __forceinline__ float lane_leaf(const Frag<G, V, VEC>& a, const Frag<
 // One dot, every lane of the group gets it.
 template <int G, int V, bool VEC>
 __device__ __forceinline__ float group_dot(const Frag<G, V, VEC>& a, const Frag<G, V, VEC>& b,
-                                           unsigned gmask) {
-    float p = lane_leaf(a, b);
+                                           unsigned gmask, int nq = V) {
+    float p = lane_leaf(a, b, nq);
 #pragma unroll
     for (int s = G / 2; s >= 1; s >>= 1) p = __fadd_rn(p, __shfl_xor_sync(gmask, p, s, G));
     return p;
@@ -271,11 +275,11 @@ __device__ __forceinline__ float group_dot(const Frag<G, V, VEC>& a, const Frag<
 // returns the dot of nonzero gl / (G/U).
 template <int G, int V, int U, bool VEC>
 __device__ __forceinline__ float batch_dots(const Frag<G, V, VEC>& a, const Frag<G, V, VEC> (&b)[U],
-                                            unsigned gmask, int gl) {
+                                            unsigned gmask, int gl, int nq = V) {
     static_assert(U <= G, "batch_dots needs U <= G");
     float p[U];
 #pragma unroll
-    for (int u = 0; u < U; ++u) p[u] = lane_leaf(a, b[u]);
+    for (int u = 0; u < U; ++u) p[u] = lane_leaf(a, b[u], nq);
     int s = G / 2;
 #pragma unroll
     for (int h = U / 2; h >= 1; h >>= 1, s >>= 1) {
@@ -346,11 +350,22 @@ __global__ void __launch_bounds__(128, MINB) spmm_worker_kernel(const SpmmArgs a
     const uint64_t l2pol = dev::gather_policy();
     const bool full = a.width == uint32_t(F::W * G * V);  // every lane's blocks are in range
 
-    for (uint32_t w = (blockIdx.x * blockDim.x + threadIdx.x) / G; w < a.n_workers; w += n_groups) {
-        const uint32_t i0 = __ldg(a.wrow + w), i1 = __ldg(a.wrow + w + 1);
-        const uint64_t j0 = __ldg(a.wnz + w);
-        const uint32_t E = uint32_t(__ldg(a.wnz + w + 1) - j0);  // nonzeros of this worker
-        uint32_t slot = a.wslot ? __ldg(a.wslot + w) : 0u;
+    // LOCK (groups narrower than a warp): the groups of a warp step through
+    // their workers' batches together, so every shuffle of the batch body runs
+    // with the full warp mask (a lane-dependent group mask makes the compiler
+    // guard each shuffle with a convergence check).  A group whose worker is
+    // exhausted idles through the remaining trips of the warp.
+    constexpr bool LOCK = G < 32;
+    constexpr unsigned FULL = 0xffffffffu;
+    const unsigned bmask = LOCK ? FULL : gmask;  // mask of the batch-body shuffles
+    for (uint32_t w = (blockIdx.x * blockDim.x + threadIdx.x) / G;
+         LOCK ? __any_sync(FULL, w < a.n_workers) : (w < a.n_workers); w += n_groups) {
+        const bool wact = w < a.n_workers;
+        const uint32_t wq = wact ? w : a.n_workers - 1;  // idle group: no rows, no nonzeros
+        const uint32_t i0 = __ldg(a.wrow + wq), i1 = wact ? __ldg(a.wrow + wq + 1) : i0;
+        const uint64_t j0 = __ldg(a.wnz + wq);
+        const uint32_t E = wact ? uint32_t(__ldg(a.wnz + wq + 1) - j0) : 0u;  // nonzeros of this worker
+        uint32_t slot = a.wslot ? __ldg(a.wslot + wq) : 0u;
 
         // All row bookkeeping is in 32-bit positions local to the worker
         // (j0-relative, clamped to E): every row r >= i0 ends at or after j0.
@@ -468,49 +483,50 @@ __global__ void __launch_bounds__(128, MINB) spmm_worker_kernel(const SpmmArgs a
             }
         };
         if (E) load_cv(0);
-        for (uint32_t base = 0; base < E; base += CHUNK) {
-            const int n = (E - base) < uint32_t(CHUNK) ? int(E - base) : CHUNK;
-            F xf[U];
-            float av[U];
-#pragma unroll
-            for (int u = 0; u < U; ++u) {  // unconditional gathers (tail lanes read row 0)
-                const uint32_t col = __shfl_sync(gmask, cc[u / G], u % G, G);
-                av[u] = __shfl_sync(gmask, vv[u / G], u % G, G);
-                const float* lrow = row_addr(col);
-                // the FusedMM dot sums all lanes: zero-fill blocks past a partial width
-                if (!is_fused<OP>() || full) xf[u].template gather<false>(lrow, nq, l2pol);
-                else xf[u].template gather<true>(lrow, nq, l2pol);
-            }
-            if (base + CHUNK < E) load_cv(base + CHUNK);
-            auto fold = [&](const F& xv, float pv) {
-                float s = pv;
-                if constexpr (is_fused<OP>()) {
-                    // s_ij = combine(p_ij, <X_i, Y_j>); Y_j is reused below (read once)
-                    s = edge_value<OP>(pv, group_dot(xrow, xv, gmask));
+        if constexpr (LOCK) {
+            // Batches are cut at row / segment ends (settle runs between
+            // batches, group-divergent); the batch body is warp-uniform.
+            uint32_t base = 0;
+            while (__any_sync(FULL, base < E)) {
+                const bool act = base < E;
+                int n = 0;
+                if (act) {
+                    if (base >= next_l) settle(base);
+                    const uint32_t room = next_l - base;
+                    n = room < uint32_t(CHUNK) ? int(room) : CHUNK;
                 }
-                if constexpr (is_fused<OP>()) R::fold_fused_all(acc.v, s, xv.v, first);
-                else R::fold_all(acc.v, s, xv.v, first);
-                first = false;
-            };
-            if (base + uint32_t(n) <= next_l) {
-                // fast path: the whole batch continues the current row segment
+                F xf[U];
+                float av[U];
+                uint32_t colu[U];
+#pragma unroll
+                for (int u = 0; u < U; ++u) {
+                    colu[u] = __shfl_sync(FULL, cc[u / G], u % G, G);
+                    av[u] = __shfl_sync(FULL, vv[u / G], u % G, G);
+                }
+                if (act) {
+#pragma unroll
+                    for (int u = 0; u < U; ++u) xf[u].template gather<false>(row_addr(colu[u]), nq, l2pol);
+                } else {
+#pragma unroll
+                    for (int u = 0; u < U; ++u) xf[u].zero();
+                }
+                const uint32_t nb = base + uint32_t(n);
+                if (act && nb < E) load_cv(nb);
                 if constexpr (is_fused<OP>()) {
                     float sv[U];
                     if constexpr (U <= G) {
-                        // transpose-reduce: lane gl owns the dot of nonzero gl/(G/U);
-                        // the edge op runs once per nonzero, then s is broadcast
                         constexpr int PER = G / U;
                         const int u_own = gl / PER;
                         float pv_own = av[0];
 #pragma unroll
                         for (int u = 1; u < U; ++u)
                             if (u == u_own) pv_own = av[u];
-                        const float s_own = edge_value<OP>(pv_own, batch_dots(xrow, xf, gmask, gl));
+                        const float s_own = edge_value<OP>(pv_own, batch_dots(xrow, xf, FULL, gl, nq));
 #pragma unroll
-                        for (int u = 0; u < U; ++u) sv[u] = __shfl_sync(gmask, s_own, u * PER, G);
+                        for (int u = 0; u < U; ++u) sv[u] = __shfl_sync(FULL, s_own, u * PER, G);
                     } else {
 #pragma unroll
-                        for (int u = 0; u < U; ++u) sv[u] = edge_value<OP>(av[u], group_dot(xrow, xf[u], gmask));
+                        for (int u = 0; u < U; ++u) sv[u] = edge_value<OP>(av[u], group_dot(xrow, xf[u], FULL, nq));
                     }
 #pragma unroll
                     for (int u = 0; u < U; ++u) {
@@ -521,17 +537,81 @@ __global__ void __launch_bounds__(128, MINB) spmm_worker_kernel(const SpmmArgs a
                     }
                 } else {
 #pragma unroll
-                    for (int u = 0; u < U; ++u)
-                        if (u < n) fold(xf[u], av[u]);
+                    for (int u = 0; u < U; ++u) {
+                        if (u < n) {
+                            R::fold_all(acc.v, av[u], xf[u].v, first);
+                            first = false;
+                        }
+                    }
                 }
-            } else {
-                // slow path: row / segment boundaries inside the batch
-#pragma unroll
-                for (int u = 0; u < U; ++u) {
-                    if (u >= n) break;
-                    const uint32_t l = base + uint32_t(u);
-                    if (l >= next_l) settle(l);
-                    fold(xf[u], av[u]);
+                base = nb;
+            }
+        } else {
+            for (uint32_t base = 0; base < E; base += CHUNK) {
+                const int n = (E - base) < uint32_t(CHUNK) ? int(E - base) : CHUNK;
+                F xf[U];
+                float av[U];
+    #pragma unroll
+                for (int u = 0; u < U; ++u) {  // unconditional gathers (tail lanes read row 0)
+                    const uint32_t col = __shfl_sync(gmask, cc[u / G], u % G, G);
+                    av[u] = __shfl_sync(gmask, vv[u / G], u % G, G);
+                    const float* lrow = row_addr(col);
+                    // the FusedMM dot sums all lanes: zero-fill blocks past a partial width
+                    if (!is_fused<OP>() || full) xf[u].template gather<false>(lrow, nq, l2pol);
+                    else xf[u].template gather<true>(lrow, nq, l2pol);
+                }
+                if (base + CHUNK < E) load_cv(base + CHUNK);
+                auto fold = [&](const F& xv, float pv) {
+                    float s = pv;
+                    if constexpr (is_fused<OP>()) {
+                        // s_ij = combine(p_ij, <X_i, Y_j>); Y_j is reused below (read once)
+                        s = edge_value<OP>(pv, group_dot(xrow, xv, gmask));
+                    }
+                    if constexpr (is_fused<OP>()) R::fold_fused_all(acc.v, s, xv.v, first);
+                    else R::fold_all(acc.v, s, xv.v, first);
+                    first = false;
+                };
+                if (base + uint32_t(n) <= next_l) {
+                    // fast path: the whole batch continues the current row segment
+                    if constexpr (is_fused<OP>()) {
+                        float sv[U];
+                        if constexpr (U <= G) {
+                            // transpose-reduce: lane gl owns the dot of nonzero gl/(G/U);
+                            // the edge op runs once per nonzero, then s is broadcast
+                            constexpr int PER = G / U;
+                            const int u_own = gl / PER;
+                            float pv_own = av[0];
+    #pragma unroll
+                            for (int u = 1; u < U; ++u)
+                                if (u == u_own) pv_own = av[u];
+                            const float s_own = edge_value<OP>(pv_own, batch_dots(xrow, xf, gmask, gl));
+    #pragma unroll
+                            for (int u = 0; u < U; ++u) sv[u] = __shfl_sync(gmask, s_own, u * PER, G);
+                        } else {
+    #pragma unroll
+                            for (int u = 0; u < U; ++u) sv[u] = edge_value<OP>(av[u], group_dot(xrow, xf[u], gmask));
+                        }
+    #pragma unroll
+                        for (int u = 0; u < U; ++u) {
+                            if (u < n) {
+                                R::fold_fused_all(acc.v, sv[u], xf[u].v, first);
+                                first = false;
+                            }
+                        }
+                    } else {
+    #pragma unroll
+                        for (int u = 0; u < U; ++u)
+                            if (u < n) fold(xf[u], av[u]);
+                    }
+                } else {
+                    // slow path: row / segment boundaries inside the batch
+    #pragma unroll
+                    for (int u = 0; u < U; ++u) {
+                        if (u >= n) break;
+                        const uint32_t l = base + uint32_t(u);
+                        if (l >= next_l) settle(l);
+                        fold(xf[u], av[u]);
+                    }
                 }
             }
         }

@@ -35,7 +35,7 @@ def time_it(fn, reps=10, flush=None):
 
 def main():
     flush = torch.empty(512 << 20, dtype=torch.uint8, device="cuda")
-    which = sys.argv[1:] or ["cfg1", "cfg2"]
+    which = sys.argv[1:2] or ["cfg1", "cfg2"]
     for name in which:
         t0 = time.time()
         w = getattr(graphs, name)()
@@ -45,8 +45,13 @@ def main():
         out = torch.empty(w.n_rows, w.k, device="cuda")
         by = alg_bytes(w.n_rows, w.nnz, w.k)
         if w.k == 128:
-            variants = [{}, {"occupancy": 5}, {"occupancy": 6}, {"unroll": 4, "occupancy": 6},
-                        {"unroll": 4, "occupancy": 8}, {"unroll": 16}, {"path_items": 512}]
+            variants = [{}, {"occupancy": 6}, {"lanes": 16, "vec": 2, "unroll": 4},
+                        {"lanes": 16, "vec": 2, "unroll": 4, "occupancy": 4},
+                        {"lanes": 16, "vec": 2, "unroll": 4, "occupancy": 6},
+                        {"lanes": 16, "vec": 2, "unroll": 8, "occupancy": 4},
+                        {"lanes": 8, "vec": 4, "unroll": 4, "occupancy": 4}]
+            if len(sys.argv) > 2:
+                variants = [json.loads(v) for v in sys.argv[2:]]
         elif w.k == 64:
             variants = [{}, {"occupancy": 5}, {"occupancy": 6}, {"unroll": 4, "occupancy": 6},
                         {"lanes": 32, "vec": 1, "unroll": 8}, {"path_items": 512}]
