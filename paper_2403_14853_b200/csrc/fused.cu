@@ -64,11 +64,22 @@ __global__ void __launch_bounds__(128) sddmm_kernel(const SddmmArgs a) {
     const uint32_t ldb = uint32_t(a.ld) * 4u;
     const int nq = F::blocks_in(gl, a.k);
     const bool full = a.k == uint32_t(F::W * G * V);
-    for (uint32_t w = (blockIdx.x * blockDim.x + threadIdx.x) / G; w < a.n_workers; w += n_groups) {
+    // LOCK (groups narrower than a warp): the groups of a warp step through
+    // their batches together so the batch-body shuffles use the full warp mask
+    // (see spmm_worker_kernel); batches are cut at row ends, so every batch's
+    // U dots share one X_i.
+    constexpr bool LOCK = G < 32;
+    constexpr unsigned FULL = 0xffffffffu;
+    for (uint32_t w = (blockIdx.x * blockDim.x + threadIdx.x) / G;
+         LOCK ? __any_sync(FULL, w < a.n_workers) : (w < a.n_workers); w += n_groups) {
+        const bool wact = w < a.n_workers;
+        const uint32_t wq = wact ? w : a.n_workers - 1;
         // a plan's split (no search) or an even nnz split (binary search)
-        const uint64_t j0 = a.wnz ? __ldg(a.wnz + w) : uint64_t(w) * a.per_worker;
-        const uint32_t E = a.wnz ? uint32_t(__ldg(a.wnz + w + 1) - j0) : uint32_t(min(a.per_worker, a.nnz - j0));
-        uint32_t r = a.wrow ? __ldg(a.wrow + w) : row_of(a.rp, a.n_rows, j0);
+        const uint64_t j0 = a.wnz ? __ldg(a.wnz + wq) : uint64_t(wq) * a.per_worker;
+        const uint32_t E = !wact ? 0u
+                           : a.wnz ? uint32_t(__ldg(a.wnz + wq + 1) - j0)
+                                   : uint32_t(min(a.per_worker, a.nnz - j0));
+        uint32_t r = a.wrow ? __ldg(a.wrow + wq) : row_of(a.rp, a.n_rows, j0);
         uint32_t rb = r;
         uint64_t rwin = __ldg(a.rp + min(rb + 1 + uint32_t(gl), a.n_rows));
         uint32_t rend_l = uint32_t(min(dev::shfl_u64(gmask, rwin, 0, G), j0 + E) - j0);
@@ -98,55 +109,113 @@ __global__ void __launch_bounds__(128) sddmm_kernel(const SddmmArgs a) {
         };
         if (E) load_cv(0);
         const uint64_t l2pol = dev::gather_policy();
-        for (uint32_t base = 0; base < E; base += U) {
-            const int n = (E - base) < uint32_t(U) ? int(E - base) : U;
-            F yf[U];
-            float pv[U];
+        if constexpr (LOCK) {
+            uint32_t base = 0;
+            while (__any_sync(FULL, base < E)) {
+                const bool act = base < E;
+                int n = 0;
+                if (act) {
+                    if (base >= rend_l) next_row(base);
+                    const uint32_t room = rend_l - base;
+                    n = room < uint32_t(U) ? int(room) : U;
+                }
+                F yf[U];
+                float pv[U];
+                uint32_t colu[U];
 #pragma unroll
-            for (int u = 0; u < U; ++u) {
-                const uint32_t col = __shfl_sync(gmask, cc[u / G], u % G, G);
-                pv[u] = __shfl_sync(gmask, vv[u / G], u % G, G);
-                const float* lrow = reinterpret_cast<const float*>(ylane + uint64_t(col) * ldb);
-                if (full) yf[u].template gather<false>(lrow, nq, l2pol);
-                else yf[u].template gather<true>(lrow, nq, l2pol);
-            }
-            if (base + U < E) load_cv(base + U);
-            float res[CH];
+                for (int u = 0; u < U; ++u) {
+                    colu[u] = __shfl_sync(FULL, cc[u / G], u % G, G);
+                    pv[u] = __shfl_sync(FULL, vv[u / G], u % G, G);
+                }
+                if (act) {
 #pragma unroll
-            for (int h = 0; h < CH; ++h) res[h] = 0.0f;
-            if (base >= rend_l) next_row(base);
-            if (base + uint32_t(n) <= rend_l) {
+                    for (int u = 0; u < U; ++u)
+                        yf[u].template gather<false>(
+                            reinterpret_cast<const float*>(ylane + uint64_t(colu[u]) * ldb), nq, l2pol);
+                } else {
+#pragma unroll
+                    for (int u = 0; u < U; ++u) yf[u].zero();
+                }
+                const uint32_t nb = base + uint32_t(n);
+                if (act && nb < E) load_cv(nb);
+                float res[CH];
+#pragma unroll
+                for (int h = 0; h < CH; ++h) res[h] = 0.0f;
                 if constexpr (U <= G) {
-                    // transpose-reduce: lane gl owns nonzero gl/(G/U); lane u stores nonzero u
                     constexpr int PER = G / U;
                     const int u_own = gl / PER;
                     float pv_own = pv[0];
 #pragma unroll
                     for (int u = 1; u < U; ++u)
                         if (u == u_own) pv_own = pv[u];
-                    const float r_own = __fmul_rn(pv_own, dev::batch_dots(xrow, yf, gmask, gl));  // kernels.hpp:206
-                    res[0] = __shfl_sync(gmask, r_own, (gl * PER) & (G - 1), G);
+                    const float r_own = __fmul_rn(pv_own, dev::batch_dots(xrow, yf, FULL, gl, nq));  // kernels.hpp:206
+                    res[0] = __shfl_sync(FULL, r_own, (gl * PER) & (G - 1), G);
                 } else {
                     float d[U];
 #pragma unroll
-                    for (int u = 0; u < U; ++u) d[u] = dev::group_dot(xrow, yf[u], gmask);
+                    for (int u = 0; u < U; ++u) d[u] = dev::group_dot(xrow, yf[u], FULL, nq);
 #pragma unroll
                     for (int u = 0; u < U; ++u)
                         if (gl == u % G) res[u / G] = __fmul_rn(pv[u], d[u]);  // kernels.hpp:206
                 }
-            } else {
 #pragma unroll
-                for (int u = 0; u < U; ++u) {
-                    if (u >= n) break;
-                    if (base + uint32_t(u) >= rend_l) next_row(base + uint32_t(u));
-                    const float d = dev::group_dot(xrow, yf[u], gmask);
-                    if (gl == u % G) res[u / G] = __fmul_rn(pv[u], d);
+                for (int h = 0; h < CH; ++h) {
+                    const int q = gl + G * h;
+                    if (q < n) __stcs(a.out + j0 + base + uint32_t(q), res[h]);
                 }
+                base = nb;
             }
-#pragma unroll
-            for (int h = 0; h < CH; ++h) {
-                const uint32_t lq = base + uint32_t(gl + G * h);
-                if ((gl + G * h) < U && lq < E) __stcs(a.out + j0 + lq, res[h]);
+        } else {
+            for (uint32_t base = 0; base < E; base += U) {
+                const int n = (E - base) < uint32_t(U) ? int(E - base) : U;
+                F yf[U];
+                float pv[U];
+    #pragma unroll
+                for (int u = 0; u < U; ++u) {
+                    const uint32_t col = __shfl_sync(gmask, cc[u / G], u % G, G);
+                    pv[u] = __shfl_sync(gmask, vv[u / G], u % G, G);
+                    const float* lrow = reinterpret_cast<const float*>(ylane + uint64_t(col) * ldb);
+                    if (full) yf[u].template gather<false>(lrow, nq, l2pol);
+                    else yf[u].template gather<true>(lrow, nq, l2pol);
+                }
+                if (base + U < E) load_cv(base + U);
+                float res[CH];
+    #pragma unroll
+                for (int h = 0; h < CH; ++h) res[h] = 0.0f;
+                if (base >= rend_l) next_row(base);
+                if (base + uint32_t(n) <= rend_l) {
+                    if constexpr (U <= G) {
+                        // transpose-reduce: lane gl owns nonzero gl/(G/U); lane u stores nonzero u
+                        constexpr int PER = G / U;
+                        const int u_own = gl / PER;
+                        float pv_own = pv[0];
+    #pragma unroll
+                        for (int u = 1; u < U; ++u)
+                            if (u == u_own) pv_own = pv[u];
+                        const float r_own = __fmul_rn(pv_own, dev::batch_dots(xrow, yf, gmask, gl));  // kernels.hpp:206
+                        res[0] = __shfl_sync(gmask, r_own, (gl * PER) & (G - 1), G);
+                    } else {
+                        float d[U];
+    #pragma unroll
+                        for (int u = 0; u < U; ++u) d[u] = dev::group_dot(xrow, yf[u], gmask);
+    #pragma unroll
+                        for (int u = 0; u < U; ++u)
+                            if (gl == u % G) res[u / G] = __fmul_rn(pv[u], d[u]);  // kernels.hpp:206
+                    }
+                } else {
+    #pragma unroll
+                    for (int u = 0; u < U; ++u) {
+                        if (u >= n) break;
+                        if (base + uint32_t(u) >= rend_l) next_row(base + uint32_t(u));
+                        const float d = dev::group_dot(xrow, yf[u], gmask);
+                        if (gl == u % G) res[u / G] = __fmul_rn(pv[u], d);
+                    }
+                }
+    #pragma unroll
+                for (int h = 0; h < CH; ++h) {
+                    const uint32_t lq = base + uint32_t(gl + G * h);
+                    if ((gl + G * h) < U && lq < E) __stcs(a.out + j0 + lq, res[h]);
+                }
             }
         }
     }
