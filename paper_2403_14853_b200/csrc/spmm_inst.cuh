@@ -140,6 +140,17 @@ sgnn_status launch_spmm_worker(const SpmmArgs& a, uint32_t block, uint32_t max_b
         if (f.n_fix == 0 || f.width == 0) return SGNN_OK;                             \
         DeviceProps dp;                                                               \
         SGNN_TRY(device_props(&dp));                                                  \
+        const bool v4 = f.width % 4 == 0 && f.ldc % 4 == 0 && f.ld_slot % 4 == 0 &&    \
+                        reinterpret_cast<uintptr_t>(f.c) % 16 == 0 &&                 \
+                        reinterpret_cast<uintptr_t>(f.slots) % 16 == 0;               \
+        if (v4) {                                                                     \
+            const uint64_t items = uint64_t(f.n_fix) * ((f.width + 127) / 128);        \
+            const uint64_t blocks = std::min<uint64_t>(ceil_div_u64(items * 32, 256), \
+                                                       uint64_t(dp.sm_count) * 8);    \
+            dev::spmm_fixup_vec_kernel<RED><<<unsigned(blocks), 256, 0, s>>>(f);      \
+            SGNN_LAUNCH_CHECK();                                                      \
+            return SGNN_OK;                                                           \
+        }                                                                             \
         const uint64_t total = uint64_t(f.n_fix) * f.width;                           \
         const uint64_t blocks = std::min<uint64_t>(ceil_div_u64(total, 256),          \
                                                    uint64_t(dp.sm_count) * 8);        \

@@ -655,6 +655,47 @@ __global__ void __launch_bounds__(256) spmm_fixup_kernel(const FixupArgs f) {
     }
 }
 
+// float4 fixup: one warp per (split row, 128-float chunk), lane l owns
+// floats 4l..4l+3 of the chunk, so each slot row is one coalesced 512-byte
+// read.  Same per-element chain as spmm_fixup_kernel.
+template <int RED>
+__global__ void __launch_bounds__(256) spmm_fixup_vec_kernel(const FixupArgs f) {
+    using R = Reducer<RED>;
+    constexpr uint64_t SEG = SGNN_SEGMENT;
+    const uint32_t lane = threadIdx.x & 31;
+    const uint32_t nchunk = (f.width + 127) / 128;
+    const uint64_t items = uint64_t(f.n_fix) * nchunk;
+    const uint64_t n_warps = (uint64_t(gridDim.x) * blockDim.x) >> 5;
+    auto comb = [](float4 t, const float4& u) {
+        t.x = R::combine(t.x, u.x); t.y = R::combine(t.y, u.y);
+        t.z = R::combine(t.z, u.z); t.w = R::combine(t.w, u.w);
+        return t;
+    };
+    for (uint64_t it = (uint64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5; it < items; it += n_warps) {
+        const uint32_t fi = uint32_t(it / nchunk);
+        const uint32_t k = uint32_t(it % nchunk) * 128 + lane * 4;
+        if (k >= f.width) continue;
+        const uint32_t r = __ldg(f.fix_row + fi);
+        const uint64_t deg = __ldg(f.rp + r + 1) - __ldg(f.rp + r);
+        const uint64_t nseg = (deg + SEG - 1) / SEG;
+        const uint64_t st = f.ld_slot / 4;
+        const float4* s = reinterpret_cast<const float4*>(f.slots + uint64_t(__ldg(f.fix_slot + fi)) * f.ld_slot + k);
+        float4 v = __ldcs(s);
+        uint64_t q = 1;
+        for (; q + 8 <= nseg; q += 8) {
+            float4 b[8];
+#pragma unroll
+            for (int i = 0; i < 8; ++i) b[i] = __ldcs(s + (q + i) * st);
+#pragma unroll
+            for (int i = 0; i < 8; ++i) v = comb(v, b[i]);
+        }
+        for (; q < nseg; ++q) v = comb(v, __ldcs(s + q * st));
+        v.x = R::finish(v.x, deg); v.y = R::finish(v.y, deg);
+        v.z = R::finish(v.z, deg); v.w = R::finish(v.w, deg);
+        __stcs(reinterpret_cast<float4*>(f.c + uint64_t(r) * f.ldc + k), v);
+    }
+}
+
 }  // namespace dev
 
 // Host launcher table (spmm_launch.cu).
