@@ -322,8 +322,9 @@ __global__ void __launch_bounds__(128, MINB) spmm_worker_kernel(const SpmmArgs a
     // first U lanes of the group (CH per lane when U > G), all U row gathers
     // are issued, then consumed in order.  Keeping one batch per loop trip
     // bounds the live registers to U fragments.
-    constexpr int CH = (U + G - 1) / G;
+    constexpr int BATCH = U;
     constexpr int CHUNK = U;
+    constexpr int CH = (CHUNK + G - 1) / G;
     constexpr uint64_t SEG = SGNN_SEGMENT;
 
     const int lane = threadIdx.x & 31;
@@ -493,7 +494,7 @@ __global__ void __launch_bounds__(128, MINB) spmm_worker_kernel(const SpmmArgs a
                 if (act) {
                     if (base >= next_l) settle(base);
                     const uint32_t room = next_l - base;
-                    n = room < uint32_t(CHUNK) ? int(room) : CHUNK;
+                    n = room < uint32_t(BATCH) ? int(room) : BATCH;
                 }
                 F xf[U];
                 float av[U];
@@ -547,8 +548,8 @@ __global__ void __launch_bounds__(128, MINB) spmm_worker_kernel(const SpmmArgs a
                 base = nb;
             }
         } else {
-            for (uint32_t base = 0; base < E; base += CHUNK) {
-                const int n = (E - base) < uint32_t(CHUNK) ? int(E - base) : CHUNK;
+            for (uint32_t base = 0; base < E; base += BATCH) {
+                const int n = (E - base) < uint32_t(BATCH) ? int(E - base) : BATCH;
                 F xf[U];
                 float av[U];
     #pragma unroll
@@ -560,7 +561,7 @@ __global__ void __launch_bounds__(128, MINB) spmm_worker_kernel(const SpmmArgs a
                     if (!is_fused<OP>() || full) xf[u].template gather<false>(lrow, nq, l2pol);
                     else xf[u].template gather<true>(lrow, nq, l2pol);
                 }
-                if (base + CHUNK < E) load_cv(base + CHUNK);
+                if (base + BATCH < E) load_cv(base + BATCH);
                 auto fold = [&](const F& xv, float pv) {
                     float s = pv;
                     if constexpr (is_fused<OP>()) {
