@@ -504,12 +504,11 @@ __global__ void __launch_bounds__(128, MINB) spmm_worker_kernel(const SpmmArgs a
                     colu[u] = __shfl_sync(FULL, cc[u / G], u % G, G);
                     av[u] = __shfl_sync(FULL, vv[u / G], u % G, G);
                 }
+                // an idle group gathers nothing; its fragments are never folded
+                // (n = 0) and its dots stay inside its own lanes
                 if (act) {
 #pragma unroll
                     for (int u = 0; u < U; ++u) xf[u].template gather<false>(row_addr(colu[u]), nq, l2pol);
-                } else {
-#pragma unroll
-                    for (int u = 0; u < U; ++u) xf[u].zero();
                 }
                 const uint32_t nb = base + uint32_t(n);
                 if (act && nb < E) load_cv(nb);
@@ -529,12 +528,26 @@ __global__ void __launch_bounds__(128, MINB) spmm_worker_kernel(const SpmmArgs a
 #pragma unroll
                         for (int u = 0; u < U; ++u) sv[u] = edge_value<OP>(av[u], group_dot(xrow, xf[u], FULL, nq));
                     }
+                    if (n == U) {
 #pragma unroll
-                    for (int u = 0; u < U; ++u) {
-                        if (u < n) {
+                        for (int u = 0; u < U; ++u) {
                             R::fold_fused_all(acc.v, sv[u], xf[u].v, first);
                             first = false;
                         }
+                    } else {
+#pragma unroll
+                        for (int u = 0; u < U; ++u) {
+                            if (u < n) {
+                                R::fold_fused_all(acc.v, sv[u], xf[u].v, first);
+                                first = false;
+                            }
+                        }
+                    }
+                } else if (n == U) {
+#pragma unroll
+                    for (int u = 0; u < U; ++u) {
+                        R::fold_all(acc.v, av[u], xf[u].v, first);
+                        first = false;
                     }
                 } else {
 #pragma unroll
@@ -599,6 +612,10 @@ __global__ void __launch_bounds__(128, MINB) spmm_worker_kernel(const SpmmArgs a
                                 first = false;
                             }
                         }
+                    } else if (n == U) {
+                        // full batch (all but a worker's last): no per-element guards
+    #pragma unroll
+                        for (int u = 0; u < U; ++u) fold(xf[u], av[u]);
                     } else {
     #pragma unroll
                         for (int u = 0; u < U; ++u)
