@@ -16,6 +16,10 @@
 #include "plan.cuh"
 #include "spmm_inst.cuh"
 
+#ifndef SGNN_SDDMM_MINB
+#define SGNN_SDDMM_MINB 7  // register cap for the K=64 SDDMM (cfg4 probe: 7 best of {1, 6, 7, 8})
+#endif
+
 namespace sgnn {
 
 namespace {
@@ -51,8 +55,8 @@ __device__ __forceinline__ uint32_t row_of(const uint64_t* __restrict__ rp, uint
 // (col, val) of the next batch prefetched, one IMAD per gather address, and
 // the U dot products of a batch formed together when the batch stays in one
 // row (independent shuffle trees interleave).
-template <int G, int V, int U, bool VEC>
-__global__ void __launch_bounds__(128) sddmm_kernel(const SddmmArgs a) {
+template <int G, int V, int U, bool VEC, int MINB = 1>
+__global__ void __launch_bounds__(128, MINB) sddmm_kernel(const SddmmArgs a) {
     using F = dev::Frag<G, V, VEC>;
     constexpr int CH = (U + G - 1) / G;
     const int lane = threadIdx.x & 31;
@@ -223,20 +227,20 @@ __global__ void __launch_bounds__(128) sddmm_kernel(const SddmmArgs a) {
 
 using SddmmLaunch = sgnn_status (*)(const SddmmArgs&, cudaStream_t);
 
-template <int G, int V, int U, bool VEC>
+template <int G, int V, int U, bool VEC, int MINB = 1>
 sgnn_status launch_sddmm(const SddmmArgs& a, cudaStream_t s) {
     static int per_sm = -1;
     DeviceProps dp;
     SGNN_TRY(device_props(&dp));
     if (per_sm < 0) {
         int n = 0;
-        SGNN_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, sddmm_kernel<G, V, U, VEC>, 128, 0));
+        SGNN_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, sddmm_kernel<G, V, U, VEC, MINB>, 128, 0));
         per_sm = std::max(n, 1);
     }
     const uint64_t blocks = std::min<uint64_t>(ceil_div_u64(uint64_t(a.n_workers) * G, 128),
                                                uint64_t(dp.sm_count) * per_sm);
     if (blocks == 0) return SGNN_OK;
-    sddmm_kernel<G, V, U, VEC><<<unsigned(blocks), 128, 0, s>>>(a);
+    sddmm_kernel<G, V, U, VEC, MINB><<<unsigned(blocks), 128, 0, s>>>(a);
     SGNN_LAUNCH_CHECK();
     return SGNN_OK;
 }
@@ -332,7 +336,7 @@ sgnn_status run_sddmm(const sgnn_csr* p, const float* x, const float* y, uint32_
     if (vec) {
         if (lanes == 4) fn = &launch_sddmm<4, 1, 8, true>;
         else if (lanes == 8) fn = &launch_sddmm<8, 1, 8, true>;
-        else if (lanes == 16) fn = &launch_sddmm<16, 1, 8, true>;
+        else if (lanes == 16) fn = &launch_sddmm<16, 1, 8, true, SGNN_SDDMM_MINB>;
         else if (vregs == 1) fn = &launch_sddmm<32, 1, 8, true>;
         else if (vregs == 2) fn = &launch_sddmm<32, 2, 4, true>;
         else if (vregs == 4) fn = &launch_sddmm<32, 4, 4, true>;

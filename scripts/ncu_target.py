@@ -1,6 +1,6 @@
 """One call of a hot-path op between cudaProfilerStart/Stop, for
 `ncu --profile-from-start off --set full` captures (profiles/):
-  python scripts/ncu_target.py cfg2_spmm | cfg2_spmm_bwd | cfg4_fused | cfg4_sddmm | cfg3_spmm"""
+  python scripts/ncu_target.py cfg2_spmm | cfg2_spmm_bwd | cfg4_fused | cfg4_sddmm | cfg3_spmm | cfg5_spmm"""
 import sys
 
 import torch
@@ -10,8 +10,8 @@ from paper_2403_14853_b200 import graphs, ops  # noqa: E402
 
 
 def main(which):
-    if which.startswith("cfg2") or which.startswith("cfg3"):
-        w = graphs.cfg2(1) if which.startswith("cfg2") else graphs.cfg3(1)
+    if which.startswith("cfg2") or which.startswith("cfg3") or which.startswith("cfg5"):
+        w = {"cfg2": graphs.cfg2, "cfg3": graphs.cfg3, "cfg5": graphs.cfg5}[which[:4]](1)
         a = ops.CsrMatrix.from_numpy(w.row_ptr, w.col_idx, w.values, w.n_cols)
         if which.endswith("bwd"):
             a = ops.TrainingCache(a).sum_operand()
