@@ -151,6 +151,37 @@ class PartitionedSpmm:
         gathered = exchange.all_gather(pad_block(x_local, self.part.stride))
         return self.compute(gathered, reduce, out)
 
+    # SDDMM / FusedMM shard the same way: X is this rank's rows,
+    # Y the all-gathered feature blocks in the padded owner layout.
+    def fusedmm_gathered(self, x_local, y_gathered, edge_op="mul", reduce="sum", out=None):
+        """fusedmm (kernels.hpp:216-270) of this rank's row block."""
+        if self._compute is not None:
+            return self._compute_fused(x_local, y_gathered, edge_op, reduce)
+        from . import ops
+        return ops.fusedmm(self._a, x_local, y_gathered, edge_op, reduce, out)
+
+    def sddmm_gathered(self, x_local, y_gathered):
+        """sddmm (kernels.hpp:187-210) of this rank's row block: values of the
+        block's nonzeros in CSR order."""
+        if self._compute is not None:
+            return self._compute_fused(x_local, y_gathered, None, None)
+        from . import ops
+        return ops.sddmm(self._a, x_local, y_gathered).values
+
+    def fusedmm(self, x_local, y_local, exchange, edge_op="mul", reduce="sum", out=None):
+        """Row block of fusedmm(A, X, Y): all-gather Y's blocks, then local."""
+        gathered = exchange.all_gather(pad_block(y_local, self.part.stride))
+        return self.fusedmm_gathered(x_local, gathered, edge_op, reduce, out)
+
+    def sddmm(self, x_local, y_local, exchange):
+        gathered = exchange.all_gather(pad_block(y_local, self.part.stride))
+        return self.sddmm_gathered(x_local, gathered)
+
+    def _compute_fused(self, x_local, y_gathered, edge_op, reduce):
+        if not hasattr(self._compute, "fused"):
+            raise TypeError("the injected compute has no fused(local, x, y, edge_op, reduce) entry")
+        return self._compute.fused(self.local, x_local, y_gathered, edge_op, reduce)
+
     def compute_peer(self, parts, reduce="sum", out=None):
         """The local SpMM reading the partition's blocks in place (pointer
         table or tensors, one per rank): bitwise the gathered-buffer result."""

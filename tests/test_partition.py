@@ -331,3 +331,100 @@ def test_two_rank_sage_peer_exchange_matches_reference(cuda):
         assert p.exitcode == 0
     want = load_golden("gnn_planted")["sage-mean_losses"][:6]
     np.testing.assert_allclose(losses, want, rtol=2e-3, atol=1e-5)
+
+
+class _OracleCompute:
+    """Local compute by the oracle (CPU gloo tests): SpMM and FusedMM/SDDMM."""
+
+    def __call__(self, local, gathered, reduce):
+        return _oracle_compute(local, gathered, reduce)
+
+    def fused(self, local, x_local, y_gathered, edge_op, reduce):
+        import torch
+        rp, ci, v = local
+        if edge_op is None:  # sddmm values
+            return torch.from_numpy(port.sddmm(rp, ci, v, x_local.numpy(), y_gathered.numpy(), np.float64))
+        op = {"mul": port.EDGE_MUL, "sigmoid_mul": port.EDGE_SIGMOID_MUL}[edge_op]
+        red = {"sum": 0, "min": 1, "max": 2, "mean": 3}[reduce]
+        return torch.from_numpy(port.fusedmm(rp, ci, v, x_local.numpy(), y_gathered.numpy(), op, red, np.float64))
+
+
+def _fused_worker(rank, world, port_, rp, ci, v, x, y, q):
+    import torch
+    import torch.distributed as dist
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port_))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_2403_14853_b200 import partition
+        pt = partition.make_partition(rp, world)
+        me = partition.PartitionedSpmm(rp, ci, v, pt, rank, x.shape[1], device="cpu", compute=_OracleCompute())
+        r0, r1 = pt.rows(rank)
+        xl = torch.from_numpy(x[r0:r1].astype(np.float64))
+        yl = torch.from_numpy(y[r0:r1].astype(np.float64))
+        ex = partition.NcclExchange()
+        f = me.fusedmm(xl, yl, ex, "sigmoid_mul", "sum").numpy()
+        sd = me.sddmm(xl, yl, ex).numpy()
+        out = [None] * world
+        dist.all_gather_object(out, (f, sd))
+        if rank == 0:
+            q.put(out)
+    finally:
+        dist.destroy_process_group()
+
+
+def test_two_rank_gloo_fusedmm_sddmm_match_single_process():
+    """SDDMM / FusedMM shard like SpMM: X local, Y all-gathered."""
+    import torch.multiprocessing as mp
+    rng = np.random.default_rng(8)
+    n, k = 300, 8
+    rp, ci, v = rand_csr(rng, n, n, 0.04, hub_rows=(2,), empty_frac=0.1)
+    x = rng.normal(0, 0.5, (n, k)).astype(np.float32)
+    y = rng.normal(0, 0.5, (n, k)).astype(np.float32)
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port_ = _free_port()
+    procs = [ctx.Process(target=_fused_worker, args=(r, 2, port_, rp, ci, v, x, y, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    got = q.get(timeout=120)
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    f = np.concatenate([g[0] for g in got])
+    sd = np.concatenate([g[1] for g in got])
+    xd, yd = x.astype(np.float64), y.astype(np.float64)
+    np.testing.assert_array_equal(f, port.fusedmm(rp, ci, v, xd, yd, port.EDGE_SIGMOID_MUL, 0, np.float64))
+    np.testing.assert_array_equal(sd, port.sddmm(rp, ci, v, xd, yd, np.float64))
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("parts", [2, 3, 8])
+def test_loopback_partitioned_fusedmm_sddmm_bitwise(cuda, parts):
+    """Row-partitioned FusedMM / SDDMM (Y all-gathered in the padded owner
+    layout) reproduce the single-GPU results bit for bit (the fused dot and
+    segments are plan-independent)."""
+    import torch
+
+    from paper_2403_14853_b200 import graphs, ops, partition
+    n, k = 1 << 13, 64
+    rp, ci = graphs.rmat(13, n * 16, seed=4, symmetrize=True, self_loops=True)
+    v = graphs.uniform(len(ci), 0.0, 1.0, 2)
+    x = torch.from_numpy(graphs.normal(n * k, 0, 0.1, 3).reshape(n, k)).cuda()
+    y = torch.from_numpy(graphs.normal(n * k, 0, 0.1, 5).reshape(n, k)).cuda()
+    a = ops.CsrMatrix.from_numpy(rp, ci, v, n)
+    want_f = ops.fusedmm(a, x, y, "sigmoid_mul", "sum").cpu().numpy()
+    want_max = ops.fusedmm(a, x, y, "mul", "max").cpu().numpy()
+    want_s = ops.sddmm(a, x, y).values.cpu().numpy()
+    pt = partition.make_partition(rp, parts)
+    ranks = [partition.PartitionedSpmm(rp, ci, v, pt, p, k) for p in range(parts)]
+    gathered = partition.LoopbackExchange().all_gather(
+        [partition.pad_block(y[pt.rows(p)[0]:pt.rows(p)[1]], pt.stride) for p in range(parts)])
+    xs = [x[r.r0:r.r1].contiguous() for r in ranks]
+    got_f = np.concatenate([r.fusedmm_gathered(xl, gathered, "sigmoid_mul", "sum").cpu().numpy()
+                            for r, xl in zip(ranks, xs)])
+    got_max = np.concatenate([r.fusedmm_gathered(xl, gathered, "mul", "max").cpu().numpy()
+                              for r, xl in zip(ranks, xs)])
+    got_s = np.concatenate([r.sddmm_gathered(xl, gathered).cpu().numpy() for r, xl in zip(ranks, xs)])
+    np.testing.assert_array_equal(got_f.view(np.uint32), want_f.view(np.uint32))
+    np.testing.assert_array_equal(got_max.view(np.uint32), want_max.view(np.uint32))
+    np.testing.assert_array_equal(got_s.view(np.uint32), want_s.view(np.uint32))
