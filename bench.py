@@ -315,6 +315,19 @@ def run_ours(args):
     torch.cuda.synchronize()
     warm_ms = s0.elapsed_time(s1) / 10
 
+    # BASELINE cfg2 is "sum/mean": the same step with ReduceOp::Mean (forward
+    # divides by deg; the backward runs on the cached mean operand, Aᵀ with
+    # 1/deg values, gnn.hpp:149-159), reported beside the sum headline
+    atm = cache.mean_operand()
+    plan_bm = ops.Plan(atm, w.k, **params)
+    tm_f = _events_time(lambda: ops.spmm_plan(a, x, "mean", plan_f, c), 10, 3, flush)
+    tm_b = _events_time(lambda: ops.spmm_plan(atm, g, "sum", plan_bm, dx), 10, 3, flush)
+    mean_ms = (sum(tm_f) + sum(tm_b)) / len(tm_f)
+    mean_leg = {"fwd_ms": round(sum(tm_f) / len(tm_f), 4), "bwd_ms": round(sum(tm_b) / len(tm_b), 4),
+                "GFLOP/s": round(flops_step / mean_ms / 1e6, 2),
+                "note": "ReduceOp::Mean step: fwd spmm(A, X, mean) (sum kernels + divide pass), bwd through "
+                        "TrainingCache::mean_operand; L2 flushed between calls"}
+
     # roofline of the SpMM launches (worker + fixup per call)
     bytes_f = spmm_bytes(w.n_rows, w.nnz, w.k)
     bytes_b = spmm_bytes(w.n_cols, w.nnz, w.k)
@@ -343,7 +356,7 @@ def run_ours(args):
                              "frac > 1 and traffic (ncu dram bytes per call, profiles/traffic.json) << algorithmic"},
         "gpu_launches": launches_step * args.steps,
         "fwd_ms": round(sum(fwd) / args.steps, 4), "bwd_ms": round(sum(bwd) / args.steps, 4),
-        "warm_l2_ms_per_step": round(warm_ms, 4), "transpose_ms": round(cache_ms, 3),
+        "warm_l2_ms_per_step": round(warm_ms, 4), "transpose_ms": round(cache_ms, 3), "mean": mean_leg,
         "gen_s": round(gen_s, 2),
     }
     out["clocks"] = clk.summary()
