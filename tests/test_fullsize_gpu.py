@@ -1,4 +1,4 @@
-"""Parity at BASELINE sizes (cfg2 / cfg4): full outputs are checked on a
+"""Parity at BASELINE sizes (cfg2 - cfg5): full outputs are checked on a
 deterministic row sample that includes every hub row (the oracle runs on the
 sampled rows only), the transpose is checked bit-exact in full, and
 size-independent properties (involution, linearity, plan transparency) are
@@ -116,3 +116,52 @@ def test_cfg4_fused_and_sddmm_sampled_rows(cuda):
     want_s = port.sddmm(srp, sci, sv, x[rows], y)
     den = port.sddmm_absdenom(srp, sci, sv, x[rows], y)
     assert (np.abs(s[idx] - want_s) <= 1e-5 * den + 1e-30).all()
+
+
+def test_cfg3_device_normalize_full_bitexact_and_spmm(cuda):
+    """cfg3 at full size: the device normalize_adjacency (sparse.hpp:116-174)
+    of the 48M-nnz symmetrised graph is bitwise the oracle's; the K=256 SpMM
+    on A_hat matches the oracle on sampled rows (every hub row included)."""
+    import torch
+
+    from paper_2403_14853_b200 import graphs, ops
+    rp_a, ci_a = graphs.cfg3_graph(1)
+    va = np.ones(len(ci_a), np.float32)
+    a = ops.CsrMatrix.from_numpy(rp_a, ci_a, va, len(rp_a) - 1)
+    ah = ops.normalize_adjacency(a, True)
+    trp, tci, tv = port.normalize_adjacency(rp_a, ci_a, va, True)
+    grp, gci, gv = ah.to_numpy()
+    np.testing.assert_array_equal(grp, trp)
+    np.testing.assert_array_equal(gci, tci)
+    np.testing.assert_array_equal(gv.view(np.uint32), tv.view(np.uint32))
+    n, k = len(trp) - 1, 256
+    x = graphs.normal(n * k, 0, 1, 1, 31).reshape(n, k)
+    got = ops.spmm(ah, torch.from_numpy(x).cuda(), "sum").cpu().numpy()
+    rows = _sample_rows(trp, 1500)
+    srp, sci, sv = _sub(trp, tci, tv, rows)
+    want = port.spmm(srp, sci, sv.astype(np.float64), x.astype(np.float64), 0)
+    assert_spmm_close(got[rows], want, port.spmm_absdenom(srp, sci, sv, x, 0), what="cfg3 spmm")
+
+
+def test_cfg5_mean_spmm_and_backward_sampled_rows(cuda):
+    """cfg5 at full size (202M nnz, K=128, X 2 GiB): mean SpMM and the
+    backward through the symmetric mean operand on sampled rows."""
+    import torch
+
+    from paper_2403_14853_b200 import graphs, ops, sage_dist
+    w = graphs.cfg5(1)
+    a = ops.CsrMatrix.from_numpy(w.row_ptr, w.col_idx, w.values, w.n_cols)
+    x = graphs.normal(w.n_cols * w.k, 0, 1, 1, 51).reshape(w.n_cols, w.k)
+    xt = torch.from_numpy(x).cuda()
+    got = ops.spmm(a, xt, "mean").cpu().numpy()
+    rows = _sample_rows(w.row_ptr, 1500)
+    srp, sci, sv = _sub(w.row_ptr, w.col_idx, w.values, rows)
+    want = port.spmm(srp, sci, sv.astype(np.float64), x.astype(np.float64), 3)
+    assert_spmm_close(got[rows], want, port.spmm_absdenom(srp, sci, sv, x, 3), what="cfg5 mean")
+    cache = ops.TrainingCache(a, True)
+    dx = cache.spmm_backward(xt, "mean").cpu().numpy()
+    assert cache.counters["transpose_builds"] == 0  # symmetric: no transpose (gnn.hpp:152-153)
+    mv = sage_dist.mean_operand_values(w.row_ptr, w.col_idx, w.values)
+    _, _, smv = _sub(w.row_ptr, w.col_idx, mv, rows)
+    want_b = port.spmm(srp, sci, smv.astype(np.float64), x.astype(np.float64), 0)
+    assert_spmm_close(dx[rows], want_b, port.spmm_absdenom(srp, sci, smv, x, 0), what="cfg5 backward")
