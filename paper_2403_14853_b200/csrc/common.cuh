@@ -75,6 +75,10 @@ sgnn_status check_csr(const sgnn_csr* a, const char* what);
 }  // namespace sgnn
 
 // --------------------------------------------------------------- device side
+#ifndef SGNN_CV_SMEM
+#define SGNN_CV_SMEM 1
+#endif
+
 namespace sgnn {
 namespace dev {
 

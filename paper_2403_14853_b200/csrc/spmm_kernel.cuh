@@ -324,6 +324,10 @@ __global__ void __launch_bounds__(128, MINB) spmm_worker_kernel(const SpmmArgs a
     // bounds the live registers to U fragments.
     constexpr int BATCH = U;
     constexpr int CHUNK = U;
+    // full-warp groups broadcast (col, val) through shared memory instead of
+    // 2 shuffles per nonzero (U even, one chunk element per lane)
+    constexpr bool CV_SMEM = (G == 32) && (U % 2 == 0) && (CHUNK <= 32) && SGNN_CV_SMEM;
+    __shared__ __align__(16) uint2 s_cv[CV_SMEM ? 4 : 1][CV_SMEM ? CHUNK : 2];
     constexpr int CH = (CHUNK + G - 1) / G;
     constexpr uint64_t SEG = SGNN_SEGMENT;
 
@@ -565,11 +569,30 @@ __global__ void __launch_bounds__(128, MINB) spmm_worker_kernel(const SpmmArgs a
                 const int n = (E - base) < uint32_t(BATCH) ? int(E - base) : BATCH;
                 F xf[U];
                 float av[U];
+                uint32_t colu[U];
+                if constexpr (CV_SMEM) {
+                    // (col, val) of the batch broadcast through shared memory:
+                    // one 8-byte store per lane, then two nonzeros per 16-byte load
+                    uint2* cvw = s_cv[threadIdx.x >> 5];
+                    if (gl < CHUNK) cvw[gl] = make_uint2(cc[0], __float_as_uint(vv[0]));
+                    __syncwarp();
+#pragma unroll
+                    for (int u = 0; u < U; u += 2) {
+                        const uint4 t = reinterpret_cast<const uint4*>(cvw)[u / 2];
+                        colu[u] = t.x; av[u] = __uint_as_float(t.y);
+                        colu[u + 1] = t.z; av[u + 1] = __uint_as_float(t.w);
+                    }
+                    __syncwarp();
+                } else {
+#pragma unroll
+                    for (int u = 0; u < U; ++u) {
+                        colu[u] = __shfl_sync(gmask, cc[u / G], u % G, G);
+                        av[u] = __shfl_sync(gmask, vv[u / G], u % G, G);
+                    }
+                }
     #pragma unroll
                 for (int u = 0; u < U; ++u) {  // unconditional gathers (tail lanes read row 0)
-                    const uint32_t col = __shfl_sync(gmask, cc[u / G], u % G, G);
-                    av[u] = __shfl_sync(gmask, vv[u / G], u % G, G);
-                    const float* lrow = row_addr(col);
+                    const float* lrow = row_addr(colu[u]);
                     // the FusedMM dot sums all lanes: zero-fill blocks past a partial width
                     if (!is_fused<OP>() || full) xf[u].template gather<false>(lrow, nq, l2pol);
                     else xf[u].template gather<true>(lrow, nq, l2pol);
