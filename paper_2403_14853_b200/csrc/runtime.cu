@@ -33,6 +33,15 @@ sgnn_status device_props(DeviceProps* out) {
             return fail(SGNN_ERR_CUDA, "this library is built for sm_100a (B200); device has cc " +
                                            std::to_string(p.cc_major) + "." +
                                            std::to_string(p.cc_minor));
+        // Scratch comes from the device's default stream-ordered pool; keep
+        // freed blocks in the pool (no release back to the driver at every
+        // synchronisation), so repeated plan / transpose / cache builds reuse
+        // their workspace instead of re-mapping it.
+        cudaMemPool_t pool;
+        if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+            uint64_t keep = ~0ull;
+            cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
+        }
         cache[dev] = p;
         have[dev] = true;
     }

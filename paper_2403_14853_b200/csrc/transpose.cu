@@ -225,14 +225,19 @@ __global__ void __launch_bounds__(kThreads) symmetric_kernel(const uint64_t* __r
                                                              uint32_t m, uint64_t nnz,
                                                              int* __restrict__ flag) {
     __shared__ uint32_t s_rows[2];
+    __shared__ int s_done;
     const uint64_t base = uint64_t(blockIdx.x) * kTile;
     if (threadIdx.x == 0) {
-        uint32_t lo, hi;
-        tile_rows(rp, m, base, min(base + kTile, nnz) - 1, &lo, &hi);
+        // the answer is already "no" (sparse.hpp:179-192 stops at the first
+        // mismatch too): tiles scheduled after it skip their searches
+        s_done = *reinterpret_cast<volatile int*>(flag) == 0;
+        uint32_t lo = 0, hi = 0;
+        if (!s_done) tile_rows(rp, m, base, min(base + kTile, nnz) - 1, &lo, &hi);
         s_rows[0] = lo;
         s_rows[1] = hi + 1;
     }
     __syncthreads();
+    if (s_done) return;
     bool ok = true;
     for (int r = 0; r < kItems; ++r) {
         const uint64_t e = base + uint64_t(r) * kThreads + threadIdx.x;
