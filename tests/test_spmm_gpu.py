@@ -126,6 +126,28 @@ def test_hub_rows_split_segments(cuda):
         np.testing.assert_array_equal(got.view(np.uint32), base.view(np.uint32), err_msg=str(params))
 
 
+@pytest.mark.parametrize("k", [16, 30, 128])
+def test_single_row_150k_nonzeros(cuda, k):
+    """SURVEY 4 test plan: one row of 150k nonzeros (split over hundreds of
+    workers, 586 canonical segments) among short and empty rows; sum, mean
+    and max within tolerance, sum/max bitwise plan-independent."""
+    rng = np.random.default_rng(11)
+    n_cols = 200_000
+    hub = np.sort(rng.choice(n_cols, 150_000, replace=False)).astype(np.uint32)
+    rows = [hub] + [np.sort(rng.choice(n_cols, int(rng.integers(0, 40)), replace=False)).astype(np.uint32)
+                    for _ in range(300)]
+    rp = np.zeros(len(rows) + 1, np.uint64)
+    rp[1:] = np.cumsum([len(r) for r in rows])
+    ci = np.concatenate(rows)
+    v = rng.uniform(-1, 1, len(ci)).astype(np.float32)
+    x = rng.standard_normal((n_cols, k)).astype(np.float32)
+    for red in ("sum", "mean", "max"):
+        base = check_spmm(rp, ci, v, x, n_cols, red)
+        if red != "mean":
+            got = _run((rp, ci, v), x, red, n_cols, path_items=512)
+            np.testing.assert_array_equal(got.view(np.uint32), base.view(np.uint32))
+
+
 def test_plans_bitwise_transparent(cuda):
     """Dispatch transparency: every plan gives bitwise the same C."""
     rng = np.random.default_rng(3)
