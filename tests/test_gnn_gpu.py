@@ -39,6 +39,27 @@ def test_training_matches_reference(cuda, kind):
     assert abs(out.stats[-1].train_accuracy - g[f"{kind}_accs"][-1]) <= 0.02
 
 
+@pytest.mark.parametrize("kind", ["gcn", "sage-sum", "sage-mean"])
+def test_cuda_graph_training_matches_eager(cuda, kind):
+    """train(cuda_graph=True) replays a captured epoch: final weights bitwise
+    the eager run's, losses / accuracies equal (loss sums may differ in the
+    last bits: masked-select vs masked-zero reduction), and faster epochs."""
+    from paper_2403_14853_b200 import gnn
+    g, a, x, lab, mask, m = _setup(kind)
+    eager = gnn.train(m, a, x, lab, mask, epochs=EPOCHS, lr=LR)
+    w_eager = gnn.flat_weights(m)
+    _, _, _, _, _, m2 = _setup(kind)
+    graphed = gnn.train(m2, a, x, lab, mask, epochs=EPOCHS, lr=LR, cuda_graph=True)
+    np.testing.assert_array_equal(gnn.flat_weights(m2).view(np.uint32), w_eager.view(np.uint32))
+    np.testing.assert_allclose([s.loss for s in graphed.stats], [s.loss for s in eager.stats], rtol=1e-12)
+    assert [s.train_accuracy for s in graphed.stats] == [s.train_accuracy for s in eager.stats]
+    np.testing.assert_allclose([s.loss for s in graphed.stats], g[f"{kind}_losses"], rtol=2e-3, atol=1e-4)
+    t_eager = np.median([s.epoch_seconds for s in eager.stats[2:]])
+    t_graph = np.median([s.epoch_seconds for s in graphed.stats[2:]])
+    print(f"{kind}: eager {t_eager * 1e6:.1f} us/epoch, graphed {t_graph * 1e6:.1f} us/epoch")
+    assert t_graph < t_eager
+
+
 @pytest.mark.parametrize("kind", ["gcn", "sage-mean"])
 def test_cache_and_dispatch_transparency(cuda, kind):
     """use_cache / use_tuned on vs off give bitwise-identical losses."""
