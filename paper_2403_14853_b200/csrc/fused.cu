@@ -126,11 +126,16 @@ __global__ void __launch_bounds__(128, MINB) sddmm_kernel(const SddmmArgs a) {
                 F yf[U];
                 float pv[U];
                 uint32_t colu[U];
+                // with the transpose-reduce a lane needs only the value of the
+                // nonzero it owns (taken before load_cv overwrites vv)
+                constexpr bool ALL_VALS = U > G;
+                float pv_own = 0.0f;
 #pragma unroll
                 for (int u = 0; u < U; ++u) {
                     colu[u] = __shfl_sync(FULL, cc[u / G], u % G, G);
-                    pv[u] = __shfl_sync(FULL, vv[u / G], u % G, G);
+                    if constexpr (ALL_VALS) pv[u] = __shfl_sync(FULL, vv[u / G], u % G, G);
                 }
+                if constexpr (!ALL_VALS) pv_own = __shfl_sync(FULL, vv[0], gl / (G / U), G);
                 if (act) {
 #pragma unroll
                     for (int u = 0; u < U; ++u)
@@ -147,11 +152,6 @@ __global__ void __launch_bounds__(128, MINB) sddmm_kernel(const SddmmArgs a) {
                 for (int h = 0; h < CH; ++h) res[h] = 0.0f;
                 if constexpr (U <= G) {
                     constexpr int PER = G / U;
-                    const int u_own = gl / PER;
-                    float pv_own = pv[0];
-#pragma unroll
-                    for (int u = 1; u < U; ++u)
-                        if (u == u_own) pv_own = pv[u];
                     const float r_own = __fmul_rn(pv_own, dev::batch_dots(xrow, yf, FULL, gl, nq));  // kernels.hpp:206
                     res[0] = __shfl_sync(FULL, r_own, (gl * PER) & (G - 1), G);
                 } else {

@@ -362,7 +362,6 @@ __global__ void __launch_bounds__(128, MINB) spmm_worker_kernel(const SpmmArgs a
     // exhausted idles through the remaining trips of the warp.
     constexpr bool LOCK = G < 32;
     constexpr unsigned FULL = 0xffffffffu;
-    const unsigned bmask = LOCK ? FULL : gmask;  // mask of the batch-body shuffles
     for (uint32_t w = (blockIdx.x * blockDim.x + threadIdx.x) / G;
          LOCK ? __any_sync(FULL, w < a.n_workers) : (w < a.n_workers); w += n_groups) {
         const bool wact = w < a.n_workers;
@@ -503,11 +502,17 @@ __global__ void __launch_bounds__(128, MINB) spmm_worker_kernel(const SpmmArgs a
                 F xf[U];
                 float av[U];
                 uint32_t colu[U];
+                // FusedMM with the transpose-reduce needs only the value of
+                // the nonzero a lane owns (one shuffle, below), not all U
+                constexpr bool ALL_VALS = !is_fused<OP>() || U > G;
 #pragma unroll
                 for (int u = 0; u < U; ++u) {
                     colu[u] = __shfl_sync(FULL, cc[u / G], u % G, G);
-                    av[u] = __shfl_sync(FULL, vv[u / G], u % G, G);
+                    if constexpr (ALL_VALS) av[u] = __shfl_sync(FULL, vv[u / G], u % G, G);
                 }
+                // (taken before load_cv below overwrites vv with the next chunk)
+                float pv_own = 0.0f;
+                if constexpr (!ALL_VALS) pv_own = __shfl_sync(FULL, vv[0], gl / (G / U), G);
                 // an idle group gathers nothing; its fragments are never folded
                 // (n = 0) and its dots stay inside its own lanes
                 if (act) {
@@ -520,11 +525,6 @@ __global__ void __launch_bounds__(128, MINB) spmm_worker_kernel(const SpmmArgs a
                     float sv[U];
                     if constexpr (U <= G) {
                         constexpr int PER = G / U;
-                        const int u_own = gl / PER;
-                        float pv_own = av[0];
-#pragma unroll
-                        for (int u = 1; u < U; ++u)
-                            if (u == u_own) pv_own = av[u];
                         const float s_own = edge_value<OP>(pv_own, batch_dots(xrow, xf, FULL, gl, nq));
 #pragma unroll
                         for (int u = 0; u < U; ++u) sv[u] = __shfl_sync(FULL, s_own, u * PER, G);
