@@ -7,13 +7,15 @@
 // {l + G*v} (scalar path), so one warp instruction gathers a contiguous,
 // coalesced piece of a neighbour row X[col, :].
 //
-// Per nonzero the group broadcasts (col, val) by warp shuffle from a
-// coalesced chunk load, issues U independent row gathers before consuming
-// them (memory-level parallelism), then accumulates in ascending nonzero
-// order with separately rounded multiply and add -- the reference's exact
-// fp32 chain (kernels.hpp:55-58) for every row of <= SGNN_SEGMENT nonzeros.
-// Row ends come from a G-wide window of row_ptr held in registers, so short
-// rows cost no dependent loads.
+// Per batch the group broadcasts the (col, val) pairs of a coalesced chunk
+// load (through shared memory for full-warp groups, by shuffles otherwise),
+// issues U independent row gathers before consuming them (memory-level
+// parallelism), then accumulates in ascending nonzero order with separately
+// rounded multiply and add (FMUL + FADD2) -- the reference's exact fp32 chain
+// (kernels.hpp:55-58) for every row of <= SGNN_SEGMENT nonzeros.  Row ends
+// come from a G-wide window of row_ptr held in registers, so short rows cost
+// no dependent loads.  Groups narrower than a warp run in lockstep (see the
+// LOCK comment in spmm_worker_kernel).
 #pragma once
 
 #include "common.cuh"
