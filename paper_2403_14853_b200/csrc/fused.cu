@@ -16,6 +16,9 @@
 #include "plan.cuh"
 #include "spmm_inst.cuh"
 
+#ifndef SGNN_SDDMM_U16
+#define SGNN_SDDMM_U16 8  // gathers in flight per group of the K=64 SDDMM
+#endif
 #ifndef SGNN_SDDMM_MINB
 #define SGNN_SDDMM_MINB 7  // register cap for the K=64 SDDMM (cfg4 probe: 7 best of {1, 6, 7, 8})
 #endif
@@ -336,7 +339,7 @@ sgnn_status run_sddmm(const sgnn_csr* p, const float* x, const float* y, uint32_
     if (vec) {
         if (lanes == 4) fn = &launch_sddmm<4, 1, 8, true>;
         else if (lanes == 8) fn = &launch_sddmm<8, 1, 8, true>;
-        else if (lanes == 16) fn = &launch_sddmm<16, 1, 8, true, SGNN_SDDMM_MINB>;
+        else if (lanes == 16) fn = &launch_sddmm<16, 1, SGNN_SDDMM_U16, true, SGNN_SDDMM_MINB>;
         else if (vregs == 1) fn = &launch_sddmm<32, 1, 8, true>;
         else if (vregs == 2) fn = &launch_sddmm<32, 2, 4, true>;
         else if (vregs == 4) fn = &launch_sddmm<32, 4, 4, true>;
