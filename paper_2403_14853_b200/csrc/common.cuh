@@ -79,6 +79,10 @@ sgnn_status check_csr(const sgnn_csr* a, const char* what);
 #define SGNN_CV_SMEM 1
 #endif
 
+#ifndef SGNN_FIXUP_LONG
+#define SGNN_FIXUP_LONG 32  // split rows with more segments go to spmm_fixup_long_kernel
+#endif
+
 namespace sgnn {
 namespace dev {
 

@@ -423,6 +423,8 @@ sgnn_status run_fusedmm(const sgnn_csr* p, const float* x, const float* y, uint3
         f.rp = p->row_ptr;
         f.fix_row = plan->fix_row;
         f.fix_slot = plan->fix_slot;
+        f.fix_long = plan->fix_long;
+        f.n_long = plan->n_long;
         f.slots = plan->slots;
         f.c = out;
         f.ldc = k;

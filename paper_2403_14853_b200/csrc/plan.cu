@@ -99,6 +99,21 @@ __global__ void plan_fix_kernel(const uint64_t* __restrict__ rp, uint32_t m, uin
     fix_slot[fixscan[w]] = wslot[w] + first;
 }
 
+// 1 for split rows with more than SGNN_FIXUP_LONG segments (long fixup list)
+__global__ void plan_long_flag_kernel(const uint64_t* __restrict__ rp, const uint32_t* __restrict__ fix_row,
+                                      uint32_t n_fix, uint32_t* __restrict__ flag) {
+    const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n_fix) return;
+    const uint32_t r = fix_row[i];
+    flag[i] = (rp[r + 1] - rp[r] + kSeg - 1) / kSeg > SGNN_FIXUP_LONG ? 1u : 0u;
+}
+
+__global__ void plan_long_scatter_kernel(const uint32_t* __restrict__ flag, const uint32_t* __restrict__ pos,
+                                         uint32_t n_fix, uint32_t* __restrict__ out) {
+    const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n_fix && flag[i]) out[pos[i]] = i;
+}
+
 uint32_t pow2_floor(uint64_t v) {
     uint32_t p = 1;
     while (uint64_t(p) * 2 <= v && p < (1u << 30)) p *= 2;
@@ -269,7 +284,7 @@ sgnn_status build_plan(const sgnn_csr* a, uint32_t k, const sgnn_plan_params* pa
     if (plan->n_fix > 0) {
         // fix arrays + slot workspace
         void* fmem = nullptr;
-        const size_t fbytes = align(sizeof(uint32_t) * plan->n_fix) * 2 +
+        const size_t fbytes = align(sizeof(uint32_t) * plan->n_fix) * 4 +
                               sizeof(float) * size_t(plan->n_slots) * plan->kt;
         ce = cudaMalloc(&fmem, fbytes);
         if (ce != cudaSuccess) {
@@ -280,7 +295,9 @@ sgnn_status build_plan(const sgnn_csr* a, uint32_t k, const sgnn_plan_params* pa
         char* fb = static_cast<char*>(fmem);
         plan->fix_row = reinterpret_cast<uint32_t*>(fb);
         plan->fix_slot = reinterpret_cast<uint32_t*>(fb + align(sizeof(uint32_t) * plan->n_fix));
-        plan->slots = reinterpret_cast<float*>(fb + 2 * align(sizeof(uint32_t) * plan->n_fix));
+        plan->fix_long = reinterpret_cast<uint32_t*>(fb + 2 * align(sizeof(uint32_t) * plan->n_fix));
+        uint32_t* long_pos = reinterpret_cast<uint32_t*>(fb + 3 * align(sizeof(uint32_t) * plan->n_fix));
+        plan->slots = reinterpret_cast<float*>(fb + 4 * align(sizeof(uint32_t) * plan->n_fix));
         plan_fix_kernel<<<unsigned(ceil_div_u64(W, tb)), tb, 0, s>>>(
             a->row_ptr, a->n_rows, W, plan->wrow, plan->wnz, plan->wslot, fscan, plan->fix_row,
             plan->fix_slot);
@@ -289,6 +306,32 @@ sgnn_status build_plan(const sgnn_csr* a, uint32_t k, const sgnn_plan_params* pa
             destroy_plan(plan);
             return fail(SGNN_ERR_CUDA, std::string("plan fix: ") + cudaGetErrorString(ce));
         }
+        // compact the long split rows (their fixup gets a CTA each):
+        // flags -> exclusive scan (scratch) -> scatter of the fix indices
+        const unsigned fb_blocks = unsigned(ceil_div_u64(plan->n_fix, tb));
+        uint32_t* pos = nullptr;
+        st = scratch_alloc(reinterpret_cast<void**>(&pos), sizeof(uint32_t) * plan->n_fix, s);
+        if (st == SGNN_OK) {
+            plan_long_flag_kernel<<<fb_blocks, tb, 0, s>>>(a->row_ptr, plan->fix_row, plan->n_fix, long_pos);
+            st = exclusive_scan_u32(long_pos, pos, plan->n_fix, s);
+        }
+        uint32_t last[2] = {0, 0};
+        if (st == SGNN_OK &&
+            (cudaMemcpyAsync(&last[0], pos + plan->n_fix - 1, sizeof(uint32_t), cudaMemcpyDeviceToHost, s) !=
+                 cudaSuccess ||
+             cudaMemcpyAsync(&last[1], long_pos + plan->n_fix - 1, sizeof(uint32_t), cudaMemcpyDeviceToHost, s) !=
+                 cudaSuccess))
+            st = fail(SGNN_ERR_CUDA, "plan long rows: readback");
+        if (st == SGNN_OK)
+            plan_long_scatter_kernel<<<fb_blocks, tb, 0, s>>>(long_pos, pos, plan->n_fix, plan->fix_long);
+        if (st == SGNN_OK && cudaStreamSynchronize(s) != cudaSuccess)
+            st = fail(SGNN_ERR_CUDA, "plan long rows: sync");
+        scratch_free(pos, s);
+        if (st != SGNN_OK) {
+            destroy_plan(plan);
+            return st;
+        }
+        plan->n_long = last[0] + last[1];
     }
     *out = plan;
     return SGNN_OK;

@@ -36,6 +36,8 @@ struct sgnn_plan_s {
     uint32_t* wslot = nullptr;  // [n_workers+1] exclusive scan of per-worker slot counts
     uint32_t* fix_row = nullptr;   // [n_fix]
     uint32_t* fix_slot = nullptr;  // [n_fix] first slot of the row
+    uint32_t* fix_long = nullptr;  // [n_long] split rows with > SGNN_FIXUP_LONG segments
+    uint32_t n_long = 0;
     float* slots = nullptr;        // [n_slots * kt]
     void* fmem = nullptr;          // allocation holding fix_row/fix_slot/slots
 };

@@ -131,6 +131,8 @@ sgnn_status run_spmm(const sgnn_csr* a, const float* x, uint32_t k, float* c, in
             f.rp = a->row_ptr;
             f.fix_row = plan->fix_row;
             f.fix_slot = plan->fix_slot;
+            f.fix_long = plan->fix_long;
+            f.n_long = plan->n_long;
             f.slots = plan->slots;
             f.c = c + k0;
             f.ldc = k;
@@ -202,6 +204,8 @@ sgnn_status run_spmm_peer(const sgnn_csr* a, const float* const* parts, uint32_t
             f.rp = a->row_ptr;
             f.fix_row = plan->fix_row;
             f.fix_slot = plan->fix_slot;
+            f.fix_long = plan->fix_long;
+            f.n_long = plan->n_long;
             f.slots = plan->slots;
             f.c = c + k0;
             f.ldc = k;

@@ -149,6 +149,10 @@ sgnn_status launch_spmm_worker(const SpmmArgs& a, uint32_t block, uint32_t max_b
                                                        uint64_t(dp.sm_count) * 8);    \
             dev::spmm_fixup_vec_kernel<RED><<<unsigned(blocks), 256, 0, s>>>(f);      \
             SGNN_LAUNCH_CHECK();                                                      \
+            if (f.fix_long && f.n_long) {                                             \
+                dev::spmm_fixup_long_kernel<RED><<<f.n_long, dev::kFixupLongThreads, 0, s>>>(f); \
+                SGNN_LAUNCH_CHECK();                                                  \
+            }                                                                         \
             return SGNN_OK;                                                           \
         }                                                                             \
         const uint64_t total = uint64_t(f.n_fix) * f.width;                           \

@@ -24,6 +24,7 @@ namespace sgnn {
 
 #define SGNN_MAX_PEERS 8
 
+
 struct SpmmArgs {
     const uint64_t* __restrict__ rp;
     const uint32_t* __restrict__ ci;
@@ -58,6 +59,10 @@ struct FixupArgs {
     uint64_t ld_slot;
     uint32_t n_fix;
     uint32_t width;
+    // split rows with > SGNN_FIXUP_LONG segments (indices into fix_row), done
+    // by spmm_fixup_long_kernel; null: all rows by the per-row kernels
+    const uint32_t* __restrict__ fix_long = nullptr;
+    uint32_t n_long = 0;
 };
 
 namespace dev {
@@ -721,6 +726,7 @@ __global__ void __launch_bounds__(256) spmm_fixup_vec_kernel(const FixupArgs f) 
         const uint32_t r = __ldg(f.fix_row + fi);
         const uint64_t deg = __ldg(f.rp + r + 1) - __ldg(f.rp + r);
         const uint64_t nseg = (deg + SEG - 1) / SEG;
+        if (f.fix_long && nseg > SGNN_FIXUP_LONG) continue;  // spmm_fixup_long_kernel's row
         const uint64_t st = f.ld_slot / 4;
         const float4* s = reinterpret_cast<const float4*>(f.slots + uint64_t(__ldg(f.fix_slot + fi)) * f.ld_slot + k);
         float4 v = __ldcs(s);
@@ -736,6 +742,56 @@ __global__ void __launch_bounds__(256) spmm_fixup_vec_kernel(const FixupArgs f) 
         v.x = R::finish(v.x, deg); v.y = R::finish(v.y, deg);
         v.z = R::finish(v.z, deg); v.w = R::finish(v.w, deg);
         __stcs(reinterpret_cast<float4*>(f.c + uint64_t(r) * f.ldc + k), v);
+    }
+}
+
+// Split rows with more than SGNN_FIXUP_LONG segments (hub rows: cfg2's
+// largest has 300): a CTA stages chunks of the row's consecutive slots in
+// shared memory with all its threads, then each thread runs the canonical
+// left-to-right chain over its columns -- instead of one warp walking 300
+// slot loads in dependent batches of 8.
+constexpr int kFixupLongThreads = 256;
+constexpr int kFixupLongBytes = 48 * 1024;
+template <int RED>
+__global__ void __launch_bounds__(kFixupLongThreads) spmm_fixup_long_kernel(const FixupArgs f) {
+    using R = Reducer<RED>;
+    constexpr uint64_t SEG = SGNN_SEGMENT;
+    __shared__ __align__(16) float tile[kFixupLongBytes / 4];
+    const uint32_t w4 = f.width / 4;  // float4 per slot row (width % 4 == 0 here)
+    const uint32_t chunk = max(1u, uint32_t(kFixupLongBytes / 16) / w4);  // slots per staging round
+    for (uint32_t li = blockIdx.x; li < f.n_long; li += gridDim.x) {
+        const uint32_t fi = __ldg(f.fix_long + li);
+        const uint32_t r = __ldg(f.fix_row + fi);
+        const uint64_t deg = __ldg(f.rp + r + 1) - __ldg(f.rp + r);
+        const uint32_t nseg = uint32_t((deg + SEG - 1) / SEG);
+        const float* s0 = f.slots + uint64_t(__ldg(f.fix_slot + fi)) * f.ld_slot;
+        // thread t owns columns t, t + T, ... (< width); its chain in registers
+        constexpr int PER = 1024 / kFixupLongThreads;  // width <= 1024 floats
+        float v[PER];
+        for (uint32_t q0 = 0; q0 < nseg; q0 += chunk) {
+            const uint32_t nq = min(chunk, nseg - q0);
+            __syncthreads();
+            for (uint32_t i = threadIdx.x; i < nq * w4; i += kFixupLongThreads) {
+                const uint32_t q = i / w4, c4 = i % w4;
+                reinterpret_cast<float4*>(tile)[i] =
+                    __ldcs(reinterpret_cast<const float4*>(s0 + uint64_t(q0 + q) * f.ld_slot) + c4);
+            }
+            __syncthreads();
+#pragma unroll
+            for (int j = 0; j < PER; ++j) {
+                const uint32_t k = threadIdx.x + uint32_t(j) * kFixupLongThreads;
+                if (k >= f.width) break;
+                uint32_t q = 0;
+                if (q0 == 0) v[j] = tile[k], q = 1;
+                for (; q < nq; ++q) v[j] = R::combine(v[j], tile[q * f.width + k]);
+            }
+        }
+#pragma unroll
+        for (int j = 0; j < PER; ++j) {
+            const uint32_t k = threadIdx.x + uint32_t(j) * kFixupLongThreads;
+            if (k >= f.width) break;
+            __stcs(f.c + uint64_t(r) * f.ldc + k, R::finish(v[j], deg));
+        }
     }
 }
 
