@@ -41,6 +41,11 @@ METRIC = "SpMM/FusedMM GFLOP/s (2·nnz·K) and % of HBM roofline; GNN epoch time
 FALLBACK_HBM = 6650.0
 
 
+# Pure-gather ceiling on cfg2's own column sequence (512-byte rows, 128 MB
+# table): scripts/probes/gather_probe.cu on the B200, 16 CTAs/SM x U=4 best.
+GATHER_PROBE_CFG2_GBPS = 20201.0
+
+
 def parse():
     p = argparse.ArgumentParser()
     p.add_argument("--gpus", type=int, default=1)
@@ -351,6 +356,15 @@ def run_ours(args):
                      "alg_bytes_per_launch": (bytes_f + bytes_b) // 2,
                      "traffic_GBps_at_measured_time": (round(traffic / ((sum(fwd) + sum(bwd)) / (2 * args.steps)) / 1e6, 1)
                                                        if traffic else None),
+                     "gather": {
+                         "bytes_per_call": w.nnz * w.k * 4,
+                         "achieved_GBps": round(w.nnz * w.k * 4 * 2 * args.steps / (sum(fwd) + sum(bwd)) / 1e6, 1),
+                         "probe_ceiling_GBps": GATHER_PROBE_CFG2_GBPS,
+                         "frac_of_probe": round(w.nnz * w.k * 4 * 2 * args.steps / (sum(fwd) + sum(bwd)) / 1e6
+                                                / GATHER_PROBE_CFG2_GBPS, 4),
+                         "note": "the binding stream: X-row gathers (L2 hit 91%). probe_ceiling = pure gather "
+                                 "of the same column sequence, no values/row ends, best of 6 occupancies x 3 "
+                                 "depths (scripts/probes/gather_probe.cu, DESIGN 3.1)"},
                      "note": "per SpMM call (worker + fixup): achieved = algorithmic bytes (CSR + gathered X rows "
                              "+ output) / event-timed duration; gathers of hub rows hit L2 (ncu: ~91% L2 hit), so "
                              "frac > 1 and traffic (ncu dram bytes per call, profiles/traffic.json) << algorithmic"},
