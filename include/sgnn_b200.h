@@ -107,6 +107,11 @@ const char* sgnn_last_error(void);
 /* Device query used by the tuner (hardware.cpp:8-34 analogue): SM count,
  * L2 bytes, compute capability.  Synchronous. */
 sgnn_status sgnn_device_info(int* sm_count, int* l2_bytes, int* cc_major, int* cc_minor);
+/* Workspace (plan builds, transposes, cache operands' scratch) comes from the
+ * device's default stream-ordered memory pool, which the library sets to keep
+ * freed blocks for reuse.  This returns all but keep_bytes of the pool's
+ * unused memory to the driver (cudaMemPoolTrimTo).  Synchronous. */
+sgnn_status sgnn_release_scratch(size_t keep_bytes);
 
 /* ------------------------------------------------------------------ plans */
 /* Precompute the nnz-balanced work split of A for embedding width K

@@ -98,6 +98,7 @@ SIGNATURES = {
     "sgnn_abi_version": (i32, []),
     "sgnn_last_error": (C.c_char_p, []),
     "sgnn_device_info": (i32, [C.POINTER(i32)] * 4),
+    "sgnn_release_scratch": (i32, [C.c_size_t]),
     "sgnn_plan_create": (i32, [CsrP, u32, C.POINTER(PlanParams), C.POINTER(P), P]),
     "sgnn_plan_destroy": (i32, [P]),
     "sgnn_plan_get_params": (i32, [P, C.POINTER(PlanParams)]),

@@ -71,6 +71,16 @@ sgnn_status sgnn_device_info(int* sm_count, int* l2_bytes, int* cc_major, int* c
     return SGNN_OK;
 }
 
+sgnn_status sgnn_release_scratch(size_t keep_bytes) {
+    int dev = 0;
+    SGNN_CUDA_TRY(cudaGetDevice(&dev));
+    cudaMemPool_t pool;
+    SGNN_CUDA_TRY(cudaDeviceGetDefaultMemPool(&pool, dev));
+    SGNN_CUDA_TRY(cudaDeviceSynchronize());
+    SGNN_CUDA_TRY(cudaMemPoolTrimTo(pool, keep_bytes));
+    return SGNN_OK;
+}
+
 // ------------------------------------------------------------------ plans
 sgnn_status sgnn_plan_create(const sgnn_csr* a, uint32_t k, const sgnn_plan_params* params,
                              sgnn_plan* out, sgnn_stream stream) {

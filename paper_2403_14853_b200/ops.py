@@ -20,7 +20,7 @@ from ._lib import (ConfigError, DispatchError, Error, InternalError, ShapeError,
 __all__ = [
     "CsrMatrix", "KernelKind", "Plan", "TrainingCache", "DispatchGuard", "spmm", "spmm_with",
     "spmm_into", "resolve_kernel", "set_dispatch", "get_dispatch", "transpose", "row_degrees",
-    "is_symmetric", "sddmm", "fusedmm", "specialization_sweep", "spmm_plan",
+    "is_symmetric", "sddmm", "fusedmm", "specialization_sweep", "spmm_plan", "spmm_peer", "release_scratch",
 ]
 
 specialization_sweep = (16, 32, 64, 128, 256, 512, 1024)  # kernels.hpp:27
@@ -349,6 +349,11 @@ def run_tuning(a: CsrMatrix, ks, reps: int = 5, seed: int = 42, graph_id: str = 
         if e.speedup > top.speedup or (e.speedup == top.speedup and e.k < top.k):
             top = e
     return TuningReport(entries, top.k, profile, graph_id, skipped, plans)
+
+
+def release_scratch(keep_bytes: int = 0) -> None:
+    """Return the library's unused workspace to the driver (sgnn_release_scratch)."""
+    check(lib().sgnn_release_scratch(int(keep_bytes)), "release_scratch")
 
 
 def resolve_kernel(k: int, reduce) -> KernelKind:

@@ -60,7 +60,7 @@ def main():
                         {"lanes": 32, "vec": 1, "unroll": 8}, {"lanes": 32, "vec": 1, "unroll": 8, "occupancy": 5}]
         else:
             variants = [{}, {"occupancy": 5}, {"occupancy": 6}, {"unroll": 16}, {"lanes": 4, "vec": 2},
-                        {"path_items": 64}]
+                        {"path_items": 64}, {"path_items": 16}, {"path_items": 8}, {"path_items": 8, "unroll": 4}]
         for red in ("sum", "mean"):
             for v in variants:
                 try:
