@@ -149,3 +149,20 @@ def test_backward_tape_error(cuda):
         cache.spmm_backward(torch.ones(5, 8, device="cuda"))
     with pytest.raises(ops.ShapeError):
         ops.TrainingCache(_dev(np.array([0, 0], np.uint64), np.zeros(0, np.uint32), np.zeros(0, np.float32), 3))
+
+
+def test_release_scratch_after_builds(cuda):
+    """Workspace stays pooled for reuse; sgnn_release_scratch trims it and
+    later builds still work."""
+    import torch
+
+    from paper_2403_14853_b200 import ops
+    rng = np.random.default_rng(2)
+    rp, ci, v = rand_csr(rng, 3000, 2000, 0.01)
+    a = ops.CsrMatrix.from_numpy(rp, ci, v, 2000)
+    t1 = ops.transpose(a)
+    ops.release_scratch(0)
+    t2 = ops.transpose(a)
+    torch.cuda.synchronize()
+    for x, y in zip(t1.to_numpy(), t2.to_numpy()):
+        np.testing.assert_array_equal(x, y)
