@@ -284,6 +284,38 @@ sgnn_status sgnn_fusedmm_plan_f32(const sgnn_csr* p, const float* x, uint32_t x_
                                   const float* y, uint32_t y_rows, uint32_t k, int edge_op,
                                   int reduce, float* out, sgnn_plan plan, sgnn_stream stream);
 
+/* ---------------------------------------------------- GNN training engine
+ * train() of gnn.hpp:414-438 on the device: build_cache (GCN normalizes A),
+ * forward (gnn.hpp:212-256), softmax_xent + masked_accuracy (:318-370),
+ * backward through the TrainingCache (:261-313), sgd_step (:374-386).
+ * Sparse propagation on this library's SpMM, dense products in cuBLAS SGEMM
+ * (fp32, no TF32).  model_kind: 0 GCN, 1 SAGE-sum, 2 SAGE-mean, 3 GIN.
+ * a, x [n x in], labels [n] (u32), mask [n] (u8) are device arrays (copied);
+ * max_epochs sizes the per-epoch statistics.  Synchronous. */
+typedef struct sgnn_gnn_s* sgnn_gnn;
+sgnn_status sgnn_gnn_create(const sgnn_csr* a, int model_kind, uint32_t in_features, uint32_t hidden,
+                            uint32_t classes, const float* x, const uint32_t* labels, const uint8_t* mask,
+                            int use_cache, int add_self_loops, uint32_t max_epochs, sgnn_gnn* out,
+                            sgnn_stream stream);
+/* Weights, row-major: w1 [in x hidden], w2 [hidden x classes], and for SAGE
+ * w1_self / w2_self of the same shapes (NULL otherwise); epsilon for GIN.
+ * Host or device pointers.  Synchronous. */
+sgnn_status sgnn_gnn_set_weights(sgnn_gnn g, const float* w1, const float* w2, const float* w1_self,
+                                 const float* w2_self, float epsilon, sgnn_stream stream);
+sgnn_status sgnn_gnn_get_weights(sgnn_gnn g, float* w1, float* w2, float* w1_self, float* w2_self,
+                                 float* epsilon, sgnn_stream stream);
+/* `epochs` training epochs at learning rate lr.  Per epoch: loss[e] (mean
+ * masked cross-entropy), accuracy[e], seconds[e] (device time); any of them
+ * may be NULL.  cuda_graph != 0: epoch 1 runs eagerly, later epochs replay
+ * its CUDA-graph capture (needs use_cache; operand fetches are then counted
+ * at capture only).  Synchronous. */
+sgnn_status sgnn_gnn_train(sgnn_gnn g, uint32_t epochs, float lr, int cuda_graph, double* loss,
+                           double* accuracy, double* seconds, sgnn_stream stream);
+/* The engine's TrainingCache counters (gnn.hpp:121-123). */
+sgnn_status sgnn_gnn_counters(sgnn_gnn g, uint64_t* transpose_builds, uint64_t* normalize_builds,
+                              uint64_t* cache_hits, int* symmetric);
+sgnn_status sgnn_gnn_destroy(sgnn_gnn g);
+
 #ifdef __cplusplus
 } /* extern "C" */
 #endif

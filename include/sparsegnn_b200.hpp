@@ -24,6 +24,7 @@
 
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cmath>
 #include <cstdint>
 #include <cstring>
@@ -382,5 +383,89 @@ private:
     DeviceCsr a_;
     sgnn_cache h_ = nullptr;
 };
+
+// ------------------------------------------------------ GNN training (gnn.hpp)
+/// EpochStats / TrainOptions / train (gnn.hpp:389-438) over the native engine
+/// (sgnn_gnn_*): the whole epoch runs on the device (SpMM, cuBLAS SGEMM,
+/// device softmax-xent and SGD).  `Model` is the caller's GnnModel-like
+/// object (kind, in_features, hidden, classes, w1, w2, w1_self, w2_self with
+/// a `data` vector, epsilon); its parameters are updated in place, as in the
+/// reference.  `cuda_graph` replays a captured epoch after the first.
+struct EpochStats {
+    int epoch = 0;  // 1-based
+    double loss = 0;
+    double train_accuracy = 0;
+    double epoch_seconds = 0;
+};
+
+struct TrainOptions {
+    int epochs = 100;
+    double lr = 0.05;
+    int threads = 0;  // accepted for signature compatibility; unused on the GPU
+    bool use_tuned = true;
+    bool use_cache = true;
+    bool add_self_loops = true;
+    bool cuda_graph = false;
+};
+
+struct TrainOutput {
+    std::vector<EpochStats> stats;
+    std::uint64_t transpose_builds = 0, normalize_builds = 0, cache_hits = 0;
+    bool symmetric = false;
+};
+
+template <class Model, class Csr, class Dense, class Labels, class Mask>
+TrainOutput train(Model& model, const Csr& a, const Dense& x, const Labels& labels, const Mask& mask,
+                  const TrainOptions& opts = {}) {
+    if (opts.epochs < 1) throw SGNN_B200_ERR(ConfigError)("train: epochs must be >= 1");
+    if (labels.size() != a.n_rows || mask.size() != a.n_rows)
+        throw SGNN_B200_ERR(ShapeError)("train: labels/mask length must equal the node count");
+    const int kind = static_cast<int>(model.kind);
+    const bool self_w = kind == 1 || kind == 2;
+    DeviceCsr da(a);
+    auto dx = internal::upload_dense(x);
+    std::vector<std::uint32_t> lab(labels.begin(), labels.end());
+    std::vector<std::uint8_t> msk(mask.begin(), mask.end());
+    DeviceBuffer<std::uint32_t> dlab(lab.data(), lab.size());
+    DeviceBuffer<std::uint8_t> dmsk(msk.data(), msk.size());
+    const sgnn_csr v = da.view();
+    sgnn_gnn g = nullptr;
+    check(sgnn_gnn_create(&v, kind, model.in_features, model.hidden, model.classes, dx.get(), dlab.get(),
+                          dmsk.get(), opts.use_cache ? 1 : 0, opts.add_self_loops ? 1 : 0,
+                          static_cast<std::uint32_t>(opts.epochs), &g, nullptr));
+    struct Guard {
+        sgnn_gnn g;
+        ~Guard() { sgnn_gnn_destroy(g); }
+    } guard{g};
+    auto f32 = [](const auto& m) { return std::vector<float>(m.data.begin(), m.data.end()); };
+    std::vector<float> w1 = f32(model.w1), w2 = f32(model.w2), w1s, w2s;
+    if (self_w) {
+        w1s = f32(model.w1_self);
+        w2s = f32(model.w2_self);
+    }
+    check(sgnn_gnn_set_weights(g, w1.data(), w2.data(), self_w ? w1s.data() : nullptr,
+                               self_w ? w2s.data() : nullptr, static_cast<float>(model.epsilon), nullptr));
+    const std::size_t e = static_cast<std::size_t>(opts.epochs);
+    std::vector<double> loss(e), acc(e), secs(e);
+    check(sgnn_gnn_train(g, static_cast<std::uint32_t>(opts.epochs), static_cast<float>(opts.lr),
+                         opts.cuda_graph ? 1 : 0, loss.data(), acc.data(), secs.data(), nullptr));
+    float eps = 0.0f;
+    check(sgnn_gnn_get_weights(g, w1.data(), w2.data(), self_w ? w1s.data() : nullptr,
+                               self_w ? w2s.data() : nullptr, &eps, nullptr));
+    auto put = [](auto& m, const std::vector<float>& f) { std::copy(f.begin(), f.end(), m.data.begin()); };
+    put(model.w1, w1);
+    put(model.w2, w2);
+    if (self_w) {
+        put(model.w1_self, w1s);
+        put(model.w2_self, w2s);
+    }
+    model.epsilon = eps;
+    TrainOutput out;
+    for (std::size_t i = 0; i < e; ++i) out.stats.push_back({int(i) + 1, loss[i], acc[i], secs[i]});
+    int sym = 0;
+    check(sgnn_gnn_counters(g, &out.transpose_builds, &out.normalize_builds, &out.cache_hits, &sym));
+    out.symmetric = sym != 0;
+    return out;
+}
 
 }  // namespace sparsegnn_b200

@@ -133,6 +133,12 @@ SIGNATURES = {
     "sgnn_sddmm_plan_f32": (i32, [CsrP, P, u32, P, u32, u32, P, P, P]),
     "sgnn_fusedmm_f32": (i32, [CsrP, P, u32, P, u32, u32, i32, i32, P, P]),
     "sgnn_fusedmm_plan_f32": (i32, [CsrP, P, u32, P, u32, u32, i32, i32, P, P, P]),
+    "sgnn_gnn_create": (i32, [CsrP, i32, u32, u32, u32, P, P, P, i32, i32, u32, C.POINTER(P), P]),
+    "sgnn_gnn_set_weights": (i32, [P, P, P, P, P, C.c_float, P]),
+    "sgnn_gnn_get_weights": (i32, [P, P, P, P, P, C.POINTER(C.c_float), P]),
+    "sgnn_gnn_train": (i32, [P, u32, C.c_float, i32, P, P, P, P]),
+    "sgnn_gnn_counters": (i32, [P, C.POINTER(u64), C.POINTER(u64), C.POINTER(u64), C.POINTER(i32)]),
+    "sgnn_gnn_destroy": (i32, [P]),
 }
 
 HOST_SIGNATURES = {

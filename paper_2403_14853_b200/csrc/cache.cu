@@ -226,6 +226,23 @@ sgnn_status cache_spmm_backward(sgnn_cache_s* c, const float* dc, uint32_t dc_ro
     return run_spmm(&op, dc, k, dx, SGNN_REDUCE_SUM, plan, s);
 }
 
+// dX = spmm(op, dC, Sum) for an operand already fetched from this cache (the
+// GCN backward fetches sum_operand once and applies it twice, gnn.hpp:274-279)
+sgnn_status cache_spmm_with_operand(sgnn_cache_s* c, const sgnn_csr* op, const float* dc, uint32_t k, float* dx,
+                                    cudaStream_t s) {
+    if (k == 0 || op->n_rows == 0) return SGNN_OK;
+    auto key = std::make_pair(op->row_ptr, k);
+    auto it = c->plans.find(key);
+    sgnn_plan_s* plan = nullptr;
+    if (it == c->plans.end()) {
+        SGNN_TRY(build_plan(op, k, nullptr, k % 4 == 0, &plan, s));
+        c->plans[key] = plan;
+    } else {
+        plan = it->second;
+    }
+    return run_spmm(op, dc, k, dx, SGNN_REDUCE_SUM, plan, s);
+}
+
 sgnn_status cache_counters(sgnn_cache_s* c, uint64_t* tb, uint64_t* nb, uint64_t* hits, int* sym) {
     if (tb) *tb = c->transpose_builds;
     if (nb) *nb = c->normalize_builds;

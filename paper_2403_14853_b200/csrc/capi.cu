@@ -380,4 +380,46 @@ void sgnn_set_dispatch(int enabled) {
 
 int sgnn_get_dispatch(void) { return g_tuned_enabled.load(std::memory_order_relaxed) ? 1 : 0; }
 
+// ---------------------------------------------------------- GNN engine
+sgnn_status sgnn_gnn_create(const sgnn_csr* a, int model_kind, uint32_t in_features, uint32_t hidden,
+                            uint32_t classes, const float* x, const uint32_t* labels, const uint8_t* mask,
+                            int use_cache, int add_self_loops, uint32_t max_epochs, sgnn_gnn* out,
+                            sgnn_stream stream) {
+    if (!out) return fail(SGNN_ERR_CONFIG, "gnn_create: null out");
+    *out = nullptr;
+    SGNN_TRY(check_csr(a, "gnn_create"));
+    if (!x || !labels || !mask) return fail(SGNN_ERR_CONFIG, "gnn_create: null features/labels/mask");
+    return gnn_create(a, model_kind, in_features, hidden, classes, x, labels, mask, use_cache, add_self_loops,
+                      max_epochs, out, cs(stream));
+}
+
+sgnn_status sgnn_gnn_set_weights(sgnn_gnn g, const float* w1, const float* w2, const float* w1_self,
+                                 const float* w2_self, float epsilon, sgnn_stream stream) {
+    if (!g) return fail(SGNN_ERR_CONFIG, "gnn: null engine");
+    return gnn_set_weights(g, w1, w2, w1_self, w2_self, epsilon, cs(stream));
+}
+
+sgnn_status sgnn_gnn_get_weights(sgnn_gnn g, float* w1, float* w2, float* w1_self, float* w2_self,
+                                 float* epsilon, sgnn_stream stream) {
+    if (!g) return fail(SGNN_ERR_CONFIG, "gnn: null engine");
+    return gnn_get_weights(g, w1, w2, w1_self, w2_self, epsilon, cs(stream));
+}
+
+sgnn_status sgnn_gnn_train(sgnn_gnn g, uint32_t epochs, float lr, int cuda_graph, double* loss,
+                           double* accuracy, double* seconds, sgnn_stream stream) {
+    if (!g) return fail(SGNN_ERR_CONFIG, "gnn: null engine");
+    return gnn_train(g, epochs, lr, cuda_graph, loss, accuracy, seconds, cs(stream));
+}
+
+sgnn_status sgnn_gnn_counters(sgnn_gnn g, uint64_t* transpose_builds, uint64_t* normalize_builds,
+                              uint64_t* cache_hits, int* symmetric) {
+    if (!g) return fail(SGNN_ERR_CONFIG, "gnn: null engine");
+    return gnn_counters(g, transpose_builds, normalize_builds, cache_hits, symmetric);
+}
+
+sgnn_status sgnn_gnn_destroy(sgnn_gnn g) {
+    gnn_destroy(g);
+    return SGNN_OK;
+}
+
 }  // extern "C"

@@ -1,0 +1,555 @@
+// gnn.cu -- the native GNN training engine: train() of gnn.hpp:414-438 with
+// forward (gnn.hpp:212-256), backward (:261-313), softmax_xent (:318-349),
+// masked_accuracy (:353-370) and sgd_step (:374-386) on the device.  Sparse
+// propagation runs on this library's SpMM through the TrainingCache
+// (cache.cu); the dense products are cuBLAS SGEMMs (fp32, no TF32); the rest
+// are small element-wise kernels below.  An epoch never synchronises with the
+// host (loss / accuracy land in device memory), so it can be captured once
+// and replayed as a CUDA graph.
+#include <cublas_v2.h>
+
+#include <cstring>
+#include <vector>
+
+#include "ops.cuh"
+#include "plan.cuh"
+
+namespace {
+
+constexpr int kGcn = 0, kSageSum = 1, kSageMean = 2, kGin = 3;  // ModelKind order, gnn.hpp:17
+
+__global__ void relu_kernel(const float* __restrict__ x, uint64_t n, float* __restrict__ y) {
+    for (uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += uint64_t(gridDim.x) * blockDim.x)
+        y[i] = x[i] > 0.0f ? x[i] : 0.0f;  // relu (dense.hpp)
+}
+
+// relu_backward: grad where act > 0, else 0
+__global__ void relu_backward_kernel(const float* __restrict__ g, const float* __restrict__ act, uint64_t n,
+                                     float* __restrict__ out) {
+    for (uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += uint64_t(gridDim.x) * blockDim.x)
+        out[i] = act[i] <= 0.0f ? 0.0f : g[i];
+}
+
+// y += x (add_inplace)
+__global__ void add_kernel(float* __restrict__ y, const float* __restrict__ x, uint64_t n) {
+    for (uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += uint64_t(gridDim.x) * blockDim.x)
+        y[i] = __fadd_rn(y[i], x[i]);
+}
+
+// out = (1 + eps) * x + y  (scaled_add with the GIN scale, eps on the device)
+__global__ void scaled_add_kernel(const float* __restrict__ eps, const float* __restrict__ x,
+                                  const float* __restrict__ y, uint64_t n, float* __restrict__ out) {
+    const float s = __fadd_rn(1.0f, *eps);
+    for (uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += uint64_t(gridDim.x) * blockDim.x)
+        out[i] = __fadd_rn(__fmul_rn(s, x[i]), y[i]);
+}
+
+// w -= lr * g
+__global__ void sgd_kernel(float* __restrict__ w, const float* __restrict__ g, uint64_t n, float lr) {
+    for (uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += uint64_t(gridDim.x) * blockDim.x)
+        w[i] = __fsub_rn(w[i], __fmul_rn(lr, g[i]));
+}
+
+// softmax_xent + masked_accuracy, one warp per row: per-row loss (double) and
+// correct flag, gradient rows (zero outside the mask).
+__global__ void softmax_xent_kernel(const float* __restrict__ logits, uint32_t n, uint32_t c,
+                                    const uint32_t* __restrict__ labels, const uint8_t* __restrict__ mask,
+                                    double inv_n, float* __restrict__ grad, double* __restrict__ row_loss,
+                                    uint32_t* __restrict__ row_ok) {
+    const uint32_t lane = threadIdx.x & 31;
+    const uint32_t nw = (gridDim.x * blockDim.x) >> 5;
+    for (uint32_t i = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; i < n; i += nw) {
+        const float* row = logits + uint64_t(i) * c;
+        float* grow = grad + uint64_t(i) * c;
+        if (!mask[i]) {
+            for (uint32_t j = lane; j < c; j += 32) grow[j] = 0.0f;
+            if (lane == 0) {
+                row_loss[i] = 0.0;
+                row_ok[i] = 0;
+            }
+            continue;
+        }
+        double mx = -1.0 / 0.0;
+        uint32_t best = 0;
+        float bestv = -1.0f / 0.0f;
+        for (uint32_t j = lane; j < c; j += 32) {
+            const float v = row[j];
+            mx = fmax(mx, double(v));
+            if (v > bestv) {  // ties: smallest class index (lane order then merge)
+                bestv = v;
+                best = j;
+            }
+        }
+        for (int s = 16; s >= 1; s >>= 1) {
+            mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, s));
+            const float ov = __shfl_xor_sync(0xffffffffu, bestv, s);
+            const uint32_t oj = __shfl_xor_sync(0xffffffffu, best, s);
+            if (ov > bestv || (ov == bestv && oj < best)) {
+                bestv = ov;
+                best = oj;
+            }
+        }
+        double den = 0.0;
+        for (uint32_t j = lane; j < c; j += 32) den += exp(double(row[j]) - mx);
+        for (int s = 16; s >= 1; s >>= 1) den += __shfl_xor_sync(0xffffffffu, den, s);
+        const uint32_t lab = labels[i];
+        for (uint32_t j = lane; j < c; j += 32) {
+            const double p = exp(double(row[j]) - mx) / den;
+            grow[j] = float((p - (j == lab ? 1.0 : 0.0)) * inv_n);
+        }
+        if (lane == 0) {
+            row_loss[i] = (mx + log(den)) - double(row[lab]);
+            row_ok[i] = best == lab ? 1u : 0u;
+        }
+    }
+}
+
+// Sum of the per-row losses / correct flags in a fixed order (one block), and
+// the epoch's stats written to stats[2 * (*epoch)]; epoch counter advanced.
+__global__ void __launch_bounds__(1024) epoch_stats_kernel(const double* __restrict__ row_loss,
+                                                           const uint32_t* __restrict__ row_ok, uint32_t n,
+                                                           double inv_n, double* __restrict__ stats,
+                                                           uint32_t* __restrict__ epoch, uint32_t max_epochs) {
+    __shared__ double sl[1024];
+    __shared__ unsigned long long sc[1024];
+    double l = 0.0;
+    unsigned long long cnt = 0;
+    for (uint32_t i = threadIdx.x; i < n; i += blockDim.x) {
+        l += row_loss[i];
+        cnt += row_ok[i];
+    }
+    sl[threadIdx.x] = l;
+    sc[threadIdx.x] = cnt;
+    __syncthreads();
+    for (uint32_t s = blockDim.x / 2; s >= 1; s >>= 1) {
+        if (threadIdx.x < s) {
+            sl[threadIdx.x] += sl[threadIdx.x + s];
+            sc[threadIdx.x] += sc[threadIdx.x + s];
+        }
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) {
+        const uint32_t e = *epoch;
+        if (e < max_epochs) {
+            stats[2 * e] = sl[0] * inv_n;
+            stats[2 * e + 1] = double(sc[0]) * inv_n;
+        }
+        *epoch = e + 1;
+    }
+}
+
+// GIN: deps += sum(a .* b) in double (dot_all), fixed order (one block)
+__global__ void __launch_bounds__(1024) dot_all_kernel(const float* __restrict__ a, const float* __restrict__ b,
+                                                       uint64_t n, double* __restrict__ acc) {
+    __shared__ double s[1024];
+    double v = 0.0;
+    for (uint64_t i = threadIdx.x; i < n; i += blockDim.x) v += double(a[i]) * double(b[i]);
+    s[threadIdx.x] = v;
+    __syncthreads();
+    for (uint32_t k = blockDim.x / 2; k >= 1; k >>= 1) {
+        if (threadIdx.x < k) s[threadIdx.x] += s[threadIdx.x + k];
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) *acc += s[0];
+}
+
+// GIN: eps -= lr * float(deps); deps reset
+__global__ void eps_step_kernel(float* eps, double* deps, float lr) {
+    *eps = __fsub_rn(*eps, __fmul_rn(lr, float(*deps)));
+    *deps = 0.0;
+}
+
+unsigned grid_for(uint64_t n) {
+    const uint64_t b = (n + 255) / 256;
+    return unsigned(b < 4096 ? (b ? b : 1) : 4096);
+}
+
+}  // namespace
+
+struct sgnn_gnn_s {
+    int kind = kGcn;
+    uint32_t n = 0, in = 0, hid = 0, cls = 0;
+    sgnn_cache_s* cache = nullptr;
+    sgnn_csr a_hat{};
+    cublasHandle_t blas = nullptr;
+    void* blas_ws = nullptr;
+    std::vector<void*> owned;
+    // inputs
+    float* x = nullptr;
+    uint32_t* labels = nullptr;
+    uint8_t* mask = nullptr;
+    uint32_t n_masked = 0;
+    // parameters and their gradients
+    float *w1 = nullptr, *w2 = nullptr, *w1s = nullptr, *w2s = nullptr, *eps = nullptr;
+    float *g1 = nullptr, *g2 = nullptr, *g1s = nullptr, *g2s = nullptr;
+    double* deps = nullptr;
+    // activations / scratch
+    float *a1 = nullptr, *h1 = nullptr, *a2 = nullptr, *z1 = nullptr, *t1 = nullptr, *logits = nullptr,
+          *t2 = nullptr, *grad = nullptr, *d_h = nullptr, *d_h2 = nullptr, *d_c = nullptr;
+    double* row_loss = nullptr;
+    uint32_t* row_ok = nullptr;
+    double* stats = nullptr;  // [2 * max_epochs]
+    uint32_t* epoch = nullptr;
+    uint32_t max_epochs = 0;
+    // forward plans on a_hat, per K
+    std::vector<std::pair<uint32_t, sgnn_plan_s*>> plans;
+    cudaGraphExec_t graph = nullptr;
+    float graph_lr = 0.0f;
+    bool use_cache = true;
+
+    ~sgnn_gnn_s() {
+        if (graph) cudaGraphExecDestroy(graph);
+        for (auto& p : plans) sgnn::destroy_plan(p.second);
+        if (cache) sgnn::cache_destroy(cache);
+        if (blas) cublasDestroy(blas);
+        for (void* p : owned) cudaFree(p);
+    }
+};
+
+namespace sgnn {
+namespace {
+
+template <class T>
+sgnn_status dalloc(sgnn_gnn_s* g, T** p, uint64_t count) {
+    void* m = nullptr;
+    SGNN_CUDA_TRY(cudaMalloc(&m, sizeof(T) * (count ? count : 1)));
+    g->owned.push_back(m);
+    *p = static_cast<T*>(m);
+    return SGNN_OK;
+}
+
+sgnn_status blas_ok(cublasStatus_t st, const char* what) {
+    if (st != CUBLAS_STATUS_SUCCESS) return fail(SGNN_ERR_CUDA, std::string("cuBLAS ") + what + " failed");
+    return SGNN_OK;
+}
+
+// Row-major products through column-major cuBLAS (C^T = B^T A^T etc.).
+// matmul (dense.hpp): C[m,n] = A[m,k] B[k,n]
+sgnn_status mm(sgnn_gnn_s* g, const float* A, const float* B, float* Cm, int m, int k, int n) {
+    const float one = 1.0f, zero = 0.0f;
+    return blas_ok(cublasSgemm(g->blas, CUBLAS_OP_N, CUBLAS_OP_N, n, m, k, &one, B, n, A, k, &zero, Cm, n), "mm");
+}
+// matmul_tn: C[k,n] = A[m,k]^T B[m,n]
+sgnn_status mm_tn(sgnn_gnn_s* g, const float* A, const float* B, float* Cm, int m, int k, int n) {
+    const float one = 1.0f, zero = 0.0f;
+    return blas_ok(cublasSgemm(g->blas, CUBLAS_OP_N, CUBLAS_OP_T, n, k, m, &one, B, n, A, k, &zero, Cm, n), "mm_tn");
+}
+// matmul_nt: C[m,n] = A[m,k] B[n,k]^T
+sgnn_status mm_nt(sgnn_gnn_s* g, const float* A, const float* B, float* Cm, int m, int k, int n) {
+    const float one = 1.0f, zero = 0.0f;
+    return blas_ok(cublasSgemm(g->blas, CUBLAS_OP_T, CUBLAS_OP_N, n, m, k, &one, B, k, A, k, &zero, Cm, n), "mm_nt");
+}
+
+sgnn_status fwd_spmm(sgnn_gnn_s* g, const float* x, uint32_t k, float* out, int reduce, cudaStream_t s) {
+    sgnn_plan_s* plan = nullptr;
+    for (auto& p : g->plans)
+        if (p.first == k) plan = p.second;
+    if (!plan) return fail(SGNN_ERR_INTERNAL, "gnn: no forward plan for K=" + std::to_string(k));
+    return run_spmm(&g->a_hat, x, k, out, reduce, plan, s);
+}
+
+#define LAUNCH_EW(kernel, n, ...)                                              \
+    do {                                                                       \
+        kernel<<<grid_for(n), 256, 0, s>>>(__VA_ARGS__);                       \
+        SGNN_LAUNCH_CHECK();                                                   \
+    } while (0)
+
+// One epoch (gnn.hpp:427-435): forward, softmax_xent, accuracy, backward, sgd.
+sgnn_status epoch(sgnn_gnn_s* g, float lr, cudaStream_t s) {
+    const uint64_t nh = uint64_t(g->n) * g->hid, nc = uint64_t(g->n) * g->cls, ni = uint64_t(g->n) * g->in;
+    const int n = int(g->n), in = int(g->in), hid = int(g->hid), cls = int(g->cls);
+    const int red = g->kind == kSageMean ? SGNN_REDUCE_MEAN : SGNN_REDUCE_SUM;
+    // ---- forward (gnn.hpp:212-256)
+    if (g->kind == kGcn) {
+        SGNN_TRY(mm(g, g->x, g->w1, g->z1, n, in, hid));                 // z1 = X W1
+        SGNN_TRY(fwd_spmm(g, g->z1, g->hid, g->t1, SGNN_REDUCE_SUM, s));  // A_hat z1
+        LAUNCH_EW(relu_kernel, nh, g->t1, nh, g->h1);                     // h1
+        SGNN_TRY(mm(g, g->h1, g->w2, g->t2, n, hid, cls));               // z2 = h1 W2
+        SGNN_TRY(fwd_spmm(g, g->t2, g->cls, g->logits, SGNN_REDUCE_SUM, s));
+    } else if (g->kind == kSageSum || g->kind == kSageMean) {
+        SGNN_TRY(fwd_spmm(g, g->x, g->in, g->a1, red, s));                // a1 = A X
+        SGNN_TRY(mm(g, g->a1, g->w1, g->z1, n, in, hid));
+        SGNN_TRY(mm(g, g->x, g->w1s, g->t1, n, in, hid));
+        LAUNCH_EW(add_kernel, nh, g->z1, g->t1, nh);                       // z1 = a1 W1 + X W1s
+        LAUNCH_EW(relu_kernel, nh, g->z1, nh, g->h1);
+        SGNN_TRY(fwd_spmm(g, g->h1, g->hid, g->a2, red, s));               // a2 = A h1
+        SGNN_TRY(mm(g, g->a2, g->w2, g->logits, n, hid, cls));
+        SGNN_TRY(mm(g, g->h1, g->w2s, g->t2, n, hid, cls));
+        LAUNCH_EW(add_kernel, nc, g->logits, g->t2, nc);
+    } else {  // GIN
+        SGNN_TRY(fwd_spmm(g, g->x, g->in, g->t1, SGNN_REDUCE_SUM, s));
+        LAUNCH_EW(scaled_add_kernel, ni, g->eps, g->x, g->t1, ni, g->a1);  // a1 = (1+eps) X + A X
+        SGNN_TRY(mm(g, g->a1, g->w1, g->z1, n, in, hid));
+        LAUNCH_EW(relu_kernel, nh, g->z1, nh, g->h1);
+        SGNN_TRY(fwd_spmm(g, g->h1, g->hid, g->z1, SGNN_REDUCE_SUM, s));
+        LAUNCH_EW(scaled_add_kernel, nh, g->eps, g->h1, g->z1, nh, g->a2);
+        SGNN_TRY(mm(g, g->a2, g->w2, g->logits, n, hid, cls));
+    }
+    // ---- softmax_xent + masked_accuracy (gnn.hpp:318-370)
+    const double inv_n = 1.0 / double(g->n_masked);
+    softmax_xent_kernel<<<grid_for(uint64_t(g->n) * 32), 256, 0, s>>>(g->logits, g->n, g->cls, g->labels, g->mask,
+                                                                      inv_n, g->grad, g->row_loss, g->row_ok);
+    SGNN_LAUNCH_CHECK();
+    epoch_stats_kernel<<<1, 1024, 0, s>>>(g->row_loss, g->row_ok, g->n, inv_n, g->stats, g->epoch, g->max_epochs);
+    SGNN_LAUNCH_CHECK();
+    // ---- backward (gnn.hpp:261-313)
+    if (g->kind == kGcn) {
+        sgnn_csr at;  // fetched once, applied twice (gnn.hpp:274-279)
+        SGNN_TRY(cache_sum_operand(g->cache, &at, s));
+        SGNN_TRY(cache_spmm_with_operand(g->cache, &at, g->grad, g->cls, g->d_c, s));                 // dz2
+        SGNN_TRY(mm_tn(g, g->h1, g->d_c, g->g2, n, hid, cls));                                        // W2 grad
+        SGNN_TRY(mm_nt(g, g->d_c, g->w2, g->d_h, n, cls, hid));                                       // dh1
+        LAUNCH_EW(relu_backward_kernel, nh, g->d_h, g->h1, nh, g->d_h2);                             // dp1
+        SGNN_TRY(cache_spmm_with_operand(g->cache, &at, g->d_h2, g->hid, g->d_h, s));                 // dz1
+        SGNN_TRY(mm_tn(g, g->x, g->d_h, g->g1, n, in, hid));
+    } else if (g->kind == kSageSum || g->kind == kSageMean) {
+        SGNN_TRY(mm_tn(g, g->a2, g->grad, g->g2, n, hid, cls));
+        SGNN_TRY(mm_tn(g, g->h1, g->grad, g->g2s, n, hid, cls));
+        SGNN_TRY(mm_nt(g, g->grad, g->w2, g->d_h, n, cls, hid));                                      // ds2
+        SGNN_TRY(cache_spmm_backward(g->cache, g->d_h, g->n, g->hid, g->d_h2, red, s));              // dh1
+        SGNN_TRY(mm_nt(g, g->grad, g->w2s, g->d_h, n, cls, hid));
+        LAUNCH_EW(add_kernel, nh, g->d_h2, g->d_h, nh);
+        LAUNCH_EW(relu_backward_kernel, nh, g->d_h2, g->h1, nh, g->d_h);                             // dz1
+        SGNN_TRY(mm_tn(g, g->a1, g->d_h, g->g1, n, in, hid));
+        SGNN_TRY(mm_tn(g, g->x, g->d_h, g->g1s, n, in, hid));
+    } else {  // GIN
+        SGNN_TRY(mm_tn(g, g->a2, g->grad, g->g2, n, hid, cls));
+        SGNN_TRY(mm_nt(g, g->grad, g->w2, g->d_h, n, cls, hid));                                      // dm2
+        dot_all_kernel<<<1, 1024, 0, s>>>(g->d_h, g->h1, nh, g->deps);
+        SGNN_LAUNCH_CHECK();
+        SGNN_TRY(cache_spmm_backward(g->cache, g->d_h, g->n, g->hid, g->d_h2, SGNN_REDUCE_SUM, s));
+        LAUNCH_EW(scaled_add_kernel, nh, g->eps, g->d_h, g->d_h2, nh, g->z1);                        // dh1
+        LAUNCH_EW(relu_backward_kernel, nh, g->z1, g->h1, nh, g->d_h2);                              // dz1
+        SGNN_TRY(mm_tn(g, g->a1, g->d_h2, g->g1, n, in, hid));
+        SGNN_TRY(mm_nt(g, g->d_h2, g->w1, g->t1, n, hid, in));                                        // dm1
+        dot_all_kernel<<<1, 1024, 0, s>>>(g->t1, g->x, ni, g->deps);
+        SGNN_LAUNCH_CHECK();
+    }
+    // ---- sgd_step (gnn.hpp:374-386)
+    LAUNCH_EW(sgd_kernel, uint64_t(in) * hid, g->w1, g->g1, uint64_t(in) * hid, lr);
+    LAUNCH_EW(sgd_kernel, uint64_t(hid) * cls, g->w2, g->g2, uint64_t(hid) * cls, lr);
+    if (g->kind == kSageSum || g->kind == kSageMean) {
+        LAUNCH_EW(sgd_kernel, uint64_t(in) * hid, g->w1s, g->g1s, uint64_t(in) * hid, lr);
+        LAUNCH_EW(sgd_kernel, uint64_t(hid) * cls, g->w2s, g->g2s, uint64_t(hid) * cls, lr);
+    }
+    if (g->kind == kGin) {
+        eps_step_kernel<<<1, 1, 0, s>>>(g->eps, g->deps, lr);
+        SGNN_LAUNCH_CHECK();
+    }
+    return SGNN_OK;
+}
+
+}  // namespace
+
+sgnn_status gnn_create(const sgnn_csr* a, int kind, uint32_t in, uint32_t hidden, uint32_t classes,
+                       const float* x, const uint32_t* labels, const uint8_t* mask, int use_cache,
+                       int add_self_loops, uint32_t max_epochs, sgnn_gnn_s** out, cudaStream_t s) {
+    *out = nullptr;
+    if (kind < kGcn || kind > kGin) return fail(SGNN_ERR_CONFIG, "gnn: unknown model kind");
+    if (in == 0 || hidden == 0 || classes == 0)
+        return fail(SGNN_ERR_CONFIG, "init_model: in_features, hidden, and classes must be positive");
+    if (a->n_rows != a->n_cols)
+        return fail(SGNN_ERR_SHAPE, "build_cache: adjacency is " + std::to_string(a->n_rows) + "x" +
+                                        std::to_string(a->n_cols) + ", expected square");
+    auto* g = new sgnn_gnn_s;
+    g->kind = kind;
+    g->n = a->n_rows;
+    g->in = in;
+    g->hid = hidden;
+    g->cls = classes;
+    g->max_epochs = max_epochs ? max_epochs : 1;
+    g->use_cache = use_cache != 0;
+    auto bail = [&](sgnn_status st) {
+        delete g;
+        return st;
+    };
+    sgnn_status st = cache_create_model(a, kind, use_cache, add_self_loops, &g->cache, s);
+    if (st != SGNN_OK) return bail(st);
+    if ((st = cache_a_hat(g->cache, &g->a_hat)) != SGNN_OK) return bail(st);
+    if (cublasCreate(&g->blas) != CUBLAS_STATUS_SUCCESS) return bail(fail(SGNN_ERR_CUDA, "cuBLAS create failed"));
+    // fp32 products (no TF32); explicit workspace so an epoch can be graph-captured
+    cublasSetMathMode(g->blas, CUBLAS_PEDANTIC_MATH);
+    const size_t ws = size_t(32) << 20;
+    if (cudaMalloc(&g->blas_ws, ws) != cudaSuccess) return bail(fail(SGNN_ERR_NOMEM, "gnn: cuBLAS workspace"));
+    g->owned.push_back(g->blas_ws);
+    cublasSetWorkspace(g->blas, g->blas_ws, ws);
+    cublasSetStream(g->blas, s);
+    const uint64_t n = g->n;
+    const uint64_t wide = std::max<uint64_t>(hidden, in);
+    if ((st = dalloc(g, &g->x, n * in)) != SGNN_OK || (st = dalloc(g, &g->labels, n)) != SGNN_OK ||
+        (st = dalloc(g, &g->mask, n)) != SGNN_OK || (st = dalloc(g, &g->w1, uint64_t(in) * hidden)) != SGNN_OK ||
+        (st = dalloc(g, &g->w2, uint64_t(hidden) * classes)) != SGNN_OK ||
+        (st = dalloc(g, &g->w1s, uint64_t(in) * hidden)) != SGNN_OK ||
+        (st = dalloc(g, &g->w2s, uint64_t(hidden) * classes)) != SGNN_OK || (st = dalloc(g, &g->eps, 1)) != SGNN_OK ||
+        (st = dalloc(g, &g->g1, uint64_t(in) * hidden)) != SGNN_OK ||
+        (st = dalloc(g, &g->g2, uint64_t(hidden) * classes)) != SGNN_OK ||
+        (st = dalloc(g, &g->g1s, uint64_t(in) * hidden)) != SGNN_OK ||
+        (st = dalloc(g, &g->g2s, uint64_t(hidden) * classes)) != SGNN_OK || (st = dalloc(g, &g->deps, 1)) != SGNN_OK ||
+        (st = dalloc(g, &g->a1, n * in)) != SGNN_OK || (st = dalloc(g, &g->h1, n * hidden)) != SGNN_OK ||
+        (st = dalloc(g, &g->a2, n * hidden)) != SGNN_OK || (st = dalloc(g, &g->z1, n * wide)) != SGNN_OK ||
+        (st = dalloc(g, &g->t1, n * wide)) != SGNN_OK || (st = dalloc(g, &g->logits, n * classes)) != SGNN_OK ||
+        (st = dalloc(g, &g->t2, n * classes)) != SGNN_OK || (st = dalloc(g, &g->grad, n * classes)) != SGNN_OK ||
+        (st = dalloc(g, &g->d_h, n * wide)) != SGNN_OK || (st = dalloc(g, &g->d_h2, n * wide)) != SGNN_OK ||
+        (st = dalloc(g, &g->d_c, n * classes)) != SGNN_OK || (st = dalloc(g, &g->row_loss, n)) != SGNN_OK ||
+        (st = dalloc(g, &g->row_ok, n)) != SGNN_OK || (st = dalloc(g, &g->stats, 2ull * g->max_epochs)) != SGNN_OK ||
+        (st = dalloc(g, &g->epoch, 1)) != SGNN_OK)
+        return bail(st);
+    if (cudaMemcpyAsync(g->x, x, sizeof(float) * n * in, cudaMemcpyDeviceToDevice, s) != cudaSuccess ||
+        cudaMemcpyAsync(g->labels, labels, sizeof(uint32_t) * n, cudaMemcpyDeviceToDevice, s) != cudaSuccess ||
+        cudaMemcpyAsync(g->mask, mask, n, cudaMemcpyDeviceToDevice, s) != cudaSuccess ||
+        cudaMemsetAsync(g->eps, 0, sizeof(float), s) != cudaSuccess ||
+        cudaMemsetAsync(g->deps, 0, sizeof(double), s) != cudaSuccess ||
+        cudaMemsetAsync(g->epoch, 0, sizeof(uint32_t), s) != cudaSuccess)
+        return bail(fail(SGNN_ERR_CUDA, "gnn: input upload failed"));
+    // n_masked and the label range check (softmax_xent, gnn.hpp:322-331)
+    std::vector<uint8_t> hm(n);
+    std::vector<uint32_t> hl(n);
+    if (cudaMemcpyAsync(hm.data(), mask, n, cudaMemcpyDeviceToHost, s) != cudaSuccess ||
+        cudaMemcpyAsync(hl.data(), labels, sizeof(uint32_t) * n, cudaMemcpyDeviceToHost, s) != cudaSuccess ||
+        cudaStreamSynchronize(s) != cudaSuccess)
+        return bail(fail(SGNN_ERR_CUDA, "gnn: label readback failed"));
+    for (uint64_t i = 0; i < n; ++i) {
+        if (!hm[i]) continue;
+        ++g->n_masked;
+        if (hl[i] >= classes)
+            return bail(fail(SGNN_ERR_CONFIG, "softmax_xent: label " + std::to_string(hl[i]) + " out of range for " +
+                                                  std::to_string(classes) + " classes"));
+    }
+    if (g->n_masked == 0) return bail(fail(SGNN_ERR_CONFIG, "softmax_xent: mask selects no rows"));
+    // forward plans for the widths this model propagates
+    std::vector<uint32_t> ks;
+    if (kind == kGcn) ks = {hidden, classes};
+    else ks = {in, hidden};
+    for (uint32_t k : ks) {
+        bool have = false;
+        for (auto& p : g->plans) have |= p.first == k;
+        if (have) continue;
+        sgnn_plan_s* p = nullptr;
+        if ((st = build_plan(&g->a_hat, k, nullptr, k % 4 == 0, &p, s)) != SGNN_OK) return bail(st);
+        g->plans.push_back({k, p});
+    }
+    *out = g;
+    return SGNN_OK;
+}
+
+sgnn_status gnn_set_weights(sgnn_gnn_s* g, const float* w1, const float* w2, const float* w1s, const float* w2s,
+                            float eps, cudaStream_t s) {
+    const uint64_t a = uint64_t(g->in) * g->hid, b = uint64_t(g->hid) * g->cls;
+    const bool self = g->kind == kSageSum || g->kind == kSageMean;
+    if (!w1 || !w2 || (self && (!w1s || !w2s))) return fail(SGNN_ERR_CONFIG, "gnn: missing weights");
+    if (cudaMemcpyAsync(g->w1, w1, sizeof(float) * a, cudaMemcpyDefault, s) != cudaSuccess ||
+        cudaMemcpyAsync(g->w2, w2, sizeof(float) * b, cudaMemcpyDefault, s) != cudaSuccess ||
+        (self && (cudaMemcpyAsync(g->w1s, w1s, sizeof(float) * a, cudaMemcpyDefault, s) != cudaSuccess ||
+                  cudaMemcpyAsync(g->w2s, w2s, sizeof(float) * b, cudaMemcpyDefault, s) != cudaSuccess)) ||
+        cudaMemcpyAsync(g->eps, &eps, sizeof(float), cudaMemcpyHostToDevice, s) != cudaSuccess ||
+        cudaStreamSynchronize(s) != cudaSuccess)
+        return fail(SGNN_ERR_CUDA, "gnn: weight upload failed");
+    return SGNN_OK;
+}
+
+sgnn_status gnn_get_weights(sgnn_gnn_s* g, float* w1, float* w2, float* w1s, float* w2s, float* eps,
+                            cudaStream_t s) {
+    const uint64_t a = uint64_t(g->in) * g->hid, b = uint64_t(g->hid) * g->cls;
+    const bool self = g->kind == kSageSum || g->kind == kSageMean;
+    if ((w1 && cudaMemcpyAsync(w1, g->w1, sizeof(float) * a, cudaMemcpyDefault, s) != cudaSuccess) ||
+        (w2 && cudaMemcpyAsync(w2, g->w2, sizeof(float) * b, cudaMemcpyDefault, s) != cudaSuccess) ||
+        (self && w1s && cudaMemcpyAsync(w1s, g->w1s, sizeof(float) * a, cudaMemcpyDefault, s) != cudaSuccess) ||
+        (self && w2s && cudaMemcpyAsync(w2s, g->w2s, sizeof(float) * b, cudaMemcpyDefault, s) != cudaSuccess) ||
+        (eps && cudaMemcpyAsync(eps, g->eps, sizeof(float), cudaMemcpyDeviceToHost, s) != cudaSuccess) ||
+        cudaStreamSynchronize(s) != cudaSuccess)
+        return fail(SGNN_ERR_CUDA, "gnn: weight download failed");
+    return SGNN_OK;
+}
+
+// train (gnn.hpp:414-438): epochs of forward / xent / backward / sgd; stats
+// (loss, accuracy) per epoch and per-epoch device time (CUDA events).
+// cuda_graph: epoch 1 runs eagerly, epochs 2.. replay its capture.
+sgnn_status gnn_train(sgnn_gnn_s* g, uint32_t epochs, float lr, int cuda_graph, double* loss, double* acc,
+                      double* seconds, cudaStream_t s) {
+    if (epochs == 0) return fail(SGNN_ERR_CONFIG, "train: epochs must be >= 1");
+    if (epochs > g->max_epochs) return fail(SGNN_ERR_CONFIG, "train: more epochs than the engine was sized for");
+    // A graph is captured on a stream of our own (capturing the legacy
+    // default stream is not allowed); it is ordered after the caller's
+    // stream and the caller's stream after it.
+    cudaStream_t user = s;
+    cudaStream_t own = nullptr;
+    if (cuda_graph && g->use_cache) {
+        cudaEvent_t ready;
+        SGNN_CUDA_TRY(cudaStreamCreateWithFlags(&own, cudaStreamNonBlocking));
+        SGNN_CUDA_TRY(cudaEventCreateWithFlags(&ready, cudaEventDisableTiming));
+        SGNN_CUDA_TRY(cudaEventRecord(ready, user));
+        SGNN_CUDA_TRY(cudaStreamWaitEvent(own, ready, 0));
+        cudaEventDestroy(ready);
+        s = own;
+    }
+    SGNN_CUDA_TRY(cudaMemsetAsync(g->epoch, 0, sizeof(uint32_t), s));
+    cublasSetStream(g->blas, s);
+    std::vector<cudaEvent_t> ev(epochs + 1);
+    for (auto& e : ev) SGNN_CUDA_TRY(cudaEventCreate(&e));
+    sgnn_status st = SGNN_OK;
+    SGNN_CUDA_TRY(cudaEventRecord(ev[0], s));
+    for (uint32_t e = 0; e < epochs && st == SGNN_OK; ++e) {
+        // replays need every operand resident: with use_cache off the
+        // backward operand is rebuilt (allocated) per fetch, so run eagerly
+        const bool replay = cuda_graph && g->use_cache && e > 0;
+        if (replay && (!g->graph || g->graph_lr != lr)) {
+            if (g->graph) {
+                cudaGraphExecDestroy(g->graph);
+                g->graph = nullptr;
+            }
+            cudaGraph_t cg = nullptr;
+            if (cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal) != cudaSuccess) {
+                st = fail(SGNN_ERR_CUDA, "gnn: graph capture failed to start");
+                break;
+            }
+            const sgnn_status cs = epoch(g, lr, s);
+            const cudaError_t ce = cudaStreamEndCapture(s, &cg);
+            if (cs != SGNN_OK || ce != cudaSuccess) {
+                if (cg) cudaGraphDestroy(cg);
+                st = cs != SGNN_OK ? cs : fail(SGNN_ERR_CUDA, "gnn: graph capture failed");
+                break;
+            }
+            const cudaError_t ie = cudaGraphInstantiate(&g->graph, cg, 0);
+            cudaGraphDestroy(cg);
+            if (ie != cudaSuccess) {
+                st = fail(SGNN_ERR_CUDA, "gnn: graph instantiate failed");
+                break;
+            }
+            g->graph_lr = lr;
+        }
+        if (replay) {
+            if (cudaGraphLaunch(g->graph, s) != cudaSuccess) st = fail(SGNN_ERR_CUDA, "gnn: graph launch failed");
+        } else {
+            st = epoch(g, lr, s);
+        }
+        if (st == SGNN_OK && cudaEventRecord(ev[e + 1], s) != cudaSuccess) st = fail(SGNN_ERR_CUDA, "gnn: event");
+    }
+    if (st == SGNN_OK && cudaStreamSynchronize(s) != cudaSuccess) st = fail(SGNN_ERR_CUDA, "gnn: epoch failed");
+    if (st == SGNN_OK) {
+        std::vector<double> hs(2ull * epochs);
+        if (cudaMemcpy(hs.data(), g->stats, sizeof(double) * hs.size(), cudaMemcpyDeviceToHost) != cudaSuccess)
+            st = fail(SGNN_ERR_CUDA, "gnn: stats readback failed");
+        for (uint32_t e = 0; e < epochs && st == SGNN_OK; ++e) {
+            if (loss) loss[e] = hs[2 * e];
+            if (acc) acc[e] = hs[2 * e + 1];
+            float ms = 0.0f;
+            cudaEventElapsedTime(&ms, ev[e], ev[e + 1]);
+            if (seconds) seconds[e] = double(ms) * 1e-3;
+        }
+    }
+    for (auto& e : ev) cudaEventDestroy(e);
+    if (own) {
+        cudaStreamSynchronize(own);
+        cudaStreamDestroy(own);
+        cublasSetStream(g->blas, user);
+    }
+    return st;
+}
+
+sgnn_status gnn_counters(sgnn_gnn_s* g, uint64_t* tb, uint64_t* nb, uint64_t* hits, int* sym) {
+    return cache_counters(g->cache, tb, nb, hits, sym);
+}
+
+void gnn_destroy(sgnn_gnn_s* g) { delete g; }
+
+}  // namespace sgnn

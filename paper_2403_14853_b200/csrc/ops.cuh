@@ -5,6 +5,7 @@
 
 struct sgnn_plan_s;
 struct sgnn_cache_s;
+struct sgnn_gnn_s;
 
 namespace sgnn {
 
@@ -19,6 +20,8 @@ sgnn_status cache_counters(sgnn_cache_s* c, uint64_t* tb, uint64_t* nb, uint64_t
 sgnn_status cache_create_model(const sgnn_csr* a, int model_kind, int use_cache, int add_loops,
                                sgnn_cache_s** out, cudaStream_t s);
 sgnn_status cache_a_hat(sgnn_cache_s* c, sgnn_csr* out);
+sgnn_status cache_spmm_with_operand(sgnn_cache_s* c, const sgnn_csr* op, const float* dc, uint32_t k, float* dx,
+                                    cudaStream_t s);
 
 // normalize_adjacency (normalize.cu); trp == nullptr -> count only.
 sgnn_status run_normalize(const sgnn_csr* a, int add_loops, uint64_t* out_nnz, uint64_t* trp,
@@ -52,5 +55,18 @@ sgnn_status run_sddmm(const sgnn_csr* p, const float* x, const float* y, uint32_
 sgnn_status run_fusedmm(const sgnn_csr* p, const float* x, const float* y, uint32_t k,
                         int edge_op, int reduce, float* out, const sgnn_plan_s* plan,
                         cudaStream_t s);
+
+// GNN training engine (gnn.cu)
+sgnn_status gnn_create(const sgnn_csr* a, int kind, uint32_t in, uint32_t hidden, uint32_t classes,
+                       const float* x, const uint32_t* labels, const uint8_t* mask, int use_cache,
+                       int add_self_loops, uint32_t max_epochs, sgnn_gnn_s** out, cudaStream_t s);
+sgnn_status gnn_set_weights(sgnn_gnn_s* g, const float* w1, const float* w2, const float* w1s, const float* w2s,
+                            float eps, cudaStream_t s);
+sgnn_status gnn_get_weights(sgnn_gnn_s* g, float* w1, float* w2, float* w1s, float* w2s, float* eps,
+                            cudaStream_t s);
+sgnn_status gnn_train(sgnn_gnn_s* g, uint32_t epochs, float lr, int cuda_graph, double* loss, double* acc,
+                      double* seconds, cudaStream_t s);
+sgnn_status gnn_counters(sgnn_gnn_s* g, uint64_t* tb, uint64_t* nb, uint64_t* hits, int* sym);
+void gnn_destroy(sgnn_gnn_s* g);
 
 }  // namespace sgnn

@@ -321,3 +321,57 @@ def train(model: GnnModel, a: ops.CsrMatrix, x: torch.Tensor, labels: torch.Tens
             torch.cuda.synchronize()
             out.stats.append(EpochStats(epoch, loss, acc, time.perf_counter() - t0))
     return out
+
+
+_KIND_IDS = {"gcn": 0, "sage-sum": 1, "sage-mean": 2, "gin": 3}
+
+
+class NativeTrainOutput:
+    """TrainOutput of the native engine: per-epoch stats and the engine's
+    TrainingCache counters (gnn.hpp:121-123)."""
+
+    def __init__(self, stats, counters):
+        self.stats = stats
+        self.counters = counters
+
+
+def train_native(model: GnnModel, a: ops.CsrMatrix, x: torch.Tensor, labels: torch.Tensor, mask: torch.Tensor,
+                 epochs=100, lr=0.05, use_cache=True, add_self_loops=True, cuda_graph=False) -> NativeTrainOutput:
+    """train (gnn.hpp:414-438) in the native engine (sgnn_gnn_*, csrc/gnn.cu):
+    every epoch runs inside the library (SpMM + cuBLAS + element-wise
+    kernels); model's weights are updated in place at the end."""
+    import ctypes as C
+    from ._lib import check, lib
+    L = lib()
+    xs = x.contiguous()
+    lab = labels.to(torch.int32).contiguous()
+    msk = mask.to(torch.uint8).contiguous()
+    h = C.c_void_p()
+    check(L.sgnn_gnn_create(C.byref(a.c()), _KIND_IDS[model.kind], model.in_features, model.hidden, model.classes,
+                            xs.data_ptr(), lab.data_ptr(), msk.data_ptr(), int(use_cache), int(add_self_loops),
+                            int(epochs), C.byref(h), ops._stream()), "gnn_create")
+    try:
+        self_w = model.has_self_weights
+        w1, w2 = model.w1.contiguous(), model.w2.contiguous()
+        w1s = model.w1_self.contiguous() if self_w else None
+        w2s = model.w2_self.contiguous() if self_w else None
+        check(L.sgnn_gnn_set_weights(h, w1.data_ptr(), w2.data_ptr(), w1s.data_ptr() if self_w else None,
+                                     w2s.data_ptr() if self_w else None, float(model.epsilon), ops._stream()),
+              "gnn_set_weights")
+        loss = (C.c_double * epochs)()
+        acc = (C.c_double * epochs)()
+        sec = (C.c_double * epochs)()
+        check(L.sgnn_gnn_train(h, int(epochs), float(lr), int(cuda_graph), loss, acc, sec, ops._stream()), "train")
+        eps = C.c_float()
+        check(L.sgnn_gnn_get_weights(h, model.w1.data_ptr(), model.w2.data_ptr(),
+                                     model.w1_self.data_ptr() if self_w else None,
+                                     model.w2_self.data_ptr() if self_w else None, C.byref(eps), ops._stream()),
+              "gnn_get_weights")
+        model.epsilon = float(eps.value)
+        t, n, hits, sym = C.c_uint64(), C.c_uint64(), C.c_uint64(), C.c_int()
+        check(L.sgnn_gnn_counters(h, C.byref(t), C.byref(n), C.byref(hits), C.byref(sym)), "gnn_counters")
+        stats = [EpochStats(e + 1, float(loss[e]), float(acc[e]), float(sec[e])) for e in range(epochs)]
+        return NativeTrainOutput(stats, {"transpose_builds": t.value, "normalize_builds": n.value,
+                                         "cache_hits": hits.value, "symmetric": bool(sym.value)})
+    finally:
+        L.sgnn_gnn_destroy(h)

@@ -113,3 +113,36 @@ def test_tape_and_shape_errors(cuda):
     logits, tape = gnn.forward(m, cache, x)
     with pytest.raises(ops.TapeError):
         gnn.backward(m, cache, tape, torch.zeros(10, CLASSES, device="cuda"))
+
+
+@pytest.mark.parametrize("kind", ["gcn", "sage-sum", "sage-mean", "gin"])
+def test_native_engine_matches_reference(cuda, kind):
+    """The native engine (sgnn_gnn_*, csrc/gnn.cu: SpMM + cuBLAS + device
+    softmax-xent / SGD) reproduces the reference's train(): losses, cache
+    counters, final accuracy; weights close to the torch engine's."""
+    from paper_2403_14853_b200 import gnn
+    g, a, x, lab, mask, m = _setup(kind)
+    out = gnn.train_native(m, a, x, lab, mask, epochs=EPOCHS, lr=LR)
+    losses = np.array([s.loss for s in out.stats])
+    np.testing.assert_allclose(losses, g[f"{kind}_losses"], rtol=2e-3, atol=1e-4)
+    c = out.counters
+    assert [c["transpose_builds"], c["normalize_builds"], c["cache_hits"]] == [int(v) for v in g[f"{kind}_counters"]]
+    assert abs(out.stats[-1].train_accuracy - g[f"{kind}_accs"][-1]) <= 0.02
+    _, _, _, _, _, m2 = _setup(kind)
+    gnn.train(m2, a, x, lab, mask, epochs=EPOCHS, lr=LR)
+    np.testing.assert_allclose(gnn.flat_weights(m), gnn.flat_weights(m2), rtol=1e-3, atol=1e-5)
+
+
+@pytest.mark.parametrize("kind", ["gcn", "sage-mean", "gin"])
+def test_native_engine_cuda_graph_bitwise(cuda, kind):
+    """Replaying the captured epoch gives bitwise the eager native run."""
+    from paper_2403_14853_b200 import gnn
+    _, a, x, lab, mask, m = _setup(kind)
+    eager = gnn.train_native(m, a, x, lab, mask, epochs=EPOCHS, lr=LR)
+    _, _, _, _, _, m2 = _setup(kind)
+    graphed = gnn.train_native(m2, a, x, lab, mask, epochs=EPOCHS, lr=LR, cuda_graph=True)
+    np.testing.assert_array_equal(gnn.flat_weights(m2).view(np.uint32), gnn.flat_weights(m).view(np.uint32))
+    assert [s.loss for s in graphed.stats] == [s.loss for s in eager.stats]
+    t_e = np.median([s.epoch_seconds for s in eager.stats[2:]])
+    t_g = np.median([s.epoch_seconds for s in graphed.stats[2:]])
+    print(f"native {kind}: eager {t_e * 1e6:.1f} us/epoch, graphed {t_g * 1e6:.1f} us/epoch")
