@@ -681,6 +681,22 @@ def run_cfg5(args):
         "epoch_ms": round(ms, 3), "loss": loss, "scaling": "strong", "gpu_launches": steps * 12})
     line["steps"] = steps
     line["clocks"] = clk.summary()
+    if ws == 1:
+        # the same epoch in the native engine (csrc/gnn.cu: SpMM + cuBLAS +
+        # device xent/SGD, no torch in the loop), for comparison
+        from paper_2403_14853_b200 import gnn
+        xs = torch.from_numpy(graphs.normal(n * k, 0, 1, args.seed, 51).reshape(n, k)).to(dev)
+        from paper_2403_14853_b200 import ops as _ops
+        ops_csr = _ops.CsrMatrix.from_numpy(w.row_ptr, w.col_idx, w.values, w.n_cols, device=dev)
+        labs = torch.from_numpy(labels_all).to(dev)
+        m = gnn.init_model("sage-mean", k, hidden, classes, seed=args.seed)
+        nat = gnn.train_native(m, ops_csr, xs, labs, torch.ones(n, dtype=torch.uint8, device=dev),
+                               epochs=steps + 1, lr=0.05)
+        nat_ms = float(np.median([s_.epoch_seconds for s_ in nat.stats[1:]])) * 1e3
+        line["native_engine"] = {"epoch_ms": round(nat_ms, 3), "GFLOP/s (3 SpMMs)": round(flops / nat_ms / 1e6, 2),
+                                 "note": "gnn.train_native: the whole SAGE-mean epoch in the library "
+                                         "(median of epochs 2..); the headline is the row-partitioned "
+                                         "torch step, which also runs at N > 1"}
     if dist:
         dist.barrier()
         dist.destroy_process_group()
