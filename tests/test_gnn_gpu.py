@@ -146,3 +146,19 @@ def test_native_engine_cuda_graph_bitwise(cuda, kind):
     t_e = np.median([s.epoch_seconds for s in eager.stats[2:]])
     t_g = np.median([s.epoch_seconds for s in graphed.stats[2:]])
     print(f"native {kind}: eager {t_e * 1e6:.1f} us/epoch, graphed {t_g * 1e6:.1f} us/epoch")
+
+
+def test_native_engine_errors(cuda):
+    """gnn.hpp's error classes through the native engine."""
+    import torch
+
+    from paper_2403_14853_b200 import _lib, gnn, ops
+    g, a, x, lab, mask, m = _setup("gcn")
+    with pytest.raises(_lib.ConfigError):  # label out of range (softmax_xent)
+        gnn.train_native(m, a, x, torch.full_like(lab, CLASSES), mask, epochs=2)
+    with pytest.raises(_lib.ConfigError):  # empty mask
+        gnn.train_native(m, a, x, lab, torch.zeros_like(mask), epochs=2)
+    rect = ops.CsrMatrix.from_numpy(np.array([0, 1], np.uint64), np.array([1], np.uint32),
+                                    np.array([1.0], np.float32), 2)
+    with pytest.raises(_lib.ShapeError):  # build_cache: adjacency must be square
+        gnn.train_native(m, rect, x[:1], lab[:1], mask[:1], epochs=2)
