@@ -197,9 +197,12 @@ def cpu_reference_run(w, x, g, steps, warmup, budget_s=150.0, flavours=None):
     best, best_t = None, None
     for f, b in benches.items():
         for spec in (False, True):
-            t0 = time.perf_counter()
-            b.step(specialized=spec, threads=0)
-            dt = time.perf_counter() - t0
+            dt = None
+            for _ in range(2):  # the first call also pays first-touch page faults
+                t0 = time.perf_counter()
+                b.step(specialized=spec, threads=0)
+                t = time.perf_counter() - t0
+                dt = t if dt is None else min(dt, t)
             if best_t is None or dt < best_t:
                 best, best_t = (f, spec), dt
     est = best_t * (steps + warmup)
