@@ -7,6 +7,7 @@
 #include <random>
 
 #include "sparsegnn_b200.hpp"
+#include "sparsegnn_b200_io.hpp"
 
 extern "C" {
 void orc_spmm_f64(uint32_t, const uint64_t*, const uint32_t*, const double*, const double*, uint32_t,
@@ -231,6 +232,37 @@ int main() {
         EXPECT(m1.w1.data == m2.w1.data && m1.w2.data == m2.w2.data);
         for (std::size_t i = 0; i < r1.stats.size(); ++i) EXPECT(r1.stats[i].loss == r2.stats[i].loss);
         EXPECT(throws<sg::ConfigError>([&] { sg::TrainOptions bad; bad.epochs = 0; sg::train(m1, a, x, labels, mask, bad); }));
+    }
+    // ---- io.hpp drop-in: load_mtx / save_mtx round trip, ParseError lines
+    {
+        const std::string p = "/tmp/sgnn_compat_test.mtx";
+        {
+            FILE* f = std::fopen(p.c_str(), "w");
+            std::fputs("%%MatrixMarket matrix coordinate real symmetric\n% c\n3 3 3\n1 1 2\n3 1 0.5\n3 3 -1\n", f);
+            std::fclose(f);
+        }
+        Csr a = sg::load_mtx<Csr>(p);
+        EXPECT(a.n_rows == 3u && a.n_cols == 3u);
+        EXPECT((a.row_ptr == std::vector<uint64_t>{0, 2, 2, 4}));
+        EXPECT((a.col_idx == std::vector<uint32_t>{0, 2, 0, 2}));
+        EXPECT((a.values == std::vector<float>{2.f, 0.5f, 0.5f, -1.f}));
+        sg::save_mtx(a, p);
+        Csr b = sg::load_mtx<Csr>(p);
+        EXPECT(b.row_ptr == a.row_ptr && b.col_idx == a.col_idx && b.values == a.values);
+        {
+            FILE* f = std::fopen(p.c_str(), "w");
+            std::fputs("%%MatrixMarket matrix coordinate real general\n2 2 2\n1 1 1\n2 x 1\n", f);
+            std::fclose(f);
+        }
+        long line = -1;
+        try {
+            (void)sg::load_mtx<Csr>(p);
+        } catch (const sg::ParseError& e) {
+            line = e.line();
+        }
+        EXPECT(line == 4);
+        EXPECT(throws<sg::IoError>([&] { (void)sg::load_mtx<Csr>("/nonexistent/x.mtx"); }));
+        std::remove(p.c_str());
     }
     std::printf("compat OK\n");
     return 0;
