@@ -132,10 +132,11 @@ void default_params(const sgnn_csr* a, uint32_t k, bool vec_ok, const DeviceProp
         else if (k <= 64) { d.lanes = 16; d.vec = 1; }
         else if (k <= 128) { d.lanes = 32; d.vec = 1; }
         else if (k <= 256) { d.lanes = 32; d.vec = 2; }
+        else if (k <= 512) { d.lanes = 32; d.vec = 2; }  // two 256-wide passes (cfg2 tuner: 1.28x over vec 4)
         else { d.lanes = 32; d.vec = 4; }
-        d.unroll = d.vec >= 4 ? 4 : (d.vec == 2 ? 4 : 8);
+        d.unroll = d.vec >= 4 ? 4 : (d.vec == 2 ? (k > 256 ? 8 : 4) : 8);
         // register cap for 5 resident 128-thread CTAs: best or equal on cfg1-cfg4 probes
-        if (d.vec <= 2 && k > 16) d.occupancy = 5;
+        if (d.vec <= 2 && k > 16 && k <= 256) d.occupancy = 5;
     } else {
         d.lanes = 32;
         d.vec = k <= 32 ? 1 : k <= 64 ? 2 : k <= 128 ? 4 : 8;
@@ -147,7 +148,9 @@ void default_params(const sgnn_csr* a, uint32_t k, bool vec_ok, const DeviceProp
     const uint64_t groups = uint64_t(dp.sm_count > 0 ? dp.sm_count : 148) *
                             uint64_t(dp.max_threads_per_sm > 0 ? dp.max_threads_per_sm : 2048) /
                             d.lanes;
-    uint64_t want = total / (4 * groups);
+    // 4-lane groups (K <= 16) do little work per nonzero: longer paths
+    // (cfg2 tuner: 2 workers per group 1.29x over 4)
+    uint64_t want = total / ((d.lanes <= 4 ? 2 : 4) * groups);
     d.path_items = std::max<uint32_t>(32, std::min<uint32_t>(4096, pow2_floor(std::max<uint64_t>(want, 1))));
     d.split_rows_over = std::max<uint32_t>(d.path_items, SGNN_SEGMENT);
     d.k_tile = 0;
