@@ -132,8 +132,7 @@ void default_params(const sgnn_csr* a, uint32_t k, bool vec_ok, const DeviceProp
         else if (k <= 64) { d.lanes = 16; d.vec = 1; }
         else if (k <= 128) { d.lanes = 32; d.vec = 1; }
         else if (k <= 256) { d.lanes = 32; d.vec = 2; }
-        else if (k <= 512) { d.lanes = 32; d.vec = 2; }  // two 256-wide passes (cfg2 tuner: 1.28x over vec 4)
-        else { d.lanes = 32; d.vec = 4; }
+        else { d.lanes = 32; d.vec = 2; }  // 256-wide passes: cfg2 1.28x (K=512), 1.26x (K=1024) over vec 4
         d.unroll = d.vec >= 4 ? 4 : (d.vec == 2 ? (k > 256 ? 8 : 4) : 8);
         // register cap for 5 resident 128-thread CTAs: best or equal on cfg1-cfg4 probes
         if (d.vec <= 2 && k > 16 && k <= 256) d.occupancy = 5;
