@@ -53,7 +53,9 @@ std::vector<sgnn_plan_params> candidates(const sgnn_csr* a, uint32_t k, const De
         for (const LV& l : all) {
             const uint32_t width = 4 * l.lanes * l.vec;
             // one pass (width covers K, at most 2x wider) or exact K-tiles
-            if ((width >= k && width < 2 * k + 4) || (width < k && k % width == 0 && k / width <= 2))
+            // (up to 8 passes for wide K: 128/256-wide passes win there)
+            const uint32_t max_tiles = k >= 512 ? 8u : 2u;
+            if ((width >= k && width < 2 * k + 4) || (width < k && k % width == 0 && k / width <= max_tiles))
                 layouts.push_back(l);
         }
     } else {
