@@ -86,6 +86,43 @@ sgnn_status check_csr(const sgnn_csr* a, const char* what);
 namespace sgnn {
 namespace dev {
 
+// Worker schedule of a warp running PER consecutive workers at a time (one
+// per lane group).  The first round is static (warp i takes workers
+// i*PER..); later rounds are taken from a counter (ctr[0]) so warps that drew
+// short workers pick up more instead of idling through a static grid stride
+// -- power-law rows make per-worker times uneven.  The last warp to leave
+// zeroes the counters for the next launch on the stream.  ctr == null: the
+// static grid-stride schedule.  Which warp runs a worker never changes its
+// results.
+template <int PER>
+struct WarpSched {
+    uint32_t* ctr;
+    uint32_t first_round;  // workers of the static first round (all warps)
+    uint32_t base;         // first worker of this warp's current set
+    __device__ __forceinline__ explicit WarpSched(uint32_t* c) : ctr(c) {
+        const uint32_t warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+        first_round = ((gridDim.x * blockDim.x) >> 5) * PER;
+        base = warp * PER;
+    }
+    __device__ __forceinline__ void next() {
+        if (ctr) {
+            uint32_t t = 0;
+            if ((threadIdx.x & 31) == 0) t = atomicAdd(ctr, uint32_t(PER));
+            base = first_round + __shfl_sync(0xffffffffu, t, 0);
+        } else {
+            base += first_round;
+        }
+    }
+    __device__ __forceinline__ void finish() {
+        if (ctr && (threadIdx.x & 31) == 0) {
+            if (atomicAdd(ctr + 1, 1u) == first_round / PER - 1) {
+                atomicExch(ctr, 0u);
+                atomicExch(ctr + 1, 0u);
+            }
+        }
+    }
+};
+
 __device__ __forceinline__ uint64_t shfl_u64(unsigned mask, uint64_t v, int src, int width) {
     const uint32_t lo = __shfl_sync(mask, static_cast<uint32_t>(v), src, width);
     const uint32_t hi = __shfl_sync(mask, static_cast<uint32_t>(v >> 32), src, width);

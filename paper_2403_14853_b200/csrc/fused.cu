@@ -42,6 +42,7 @@ struct SddmmArgs {
     uint32_t n_workers;
     uint32_t k;
     uint64_t ld;
+    uint32_t* wctr;  // dynamic worker schedule (plan_counter), null: static
 };
 
 __device__ __forceinline__ uint32_t row_of(const uint64_t* __restrict__ rp, uint32_t m, uint64_t e) {
@@ -65,7 +66,6 @@ __global__ void __launch_bounds__(128, MINB) sddmm_kernel(const SddmmArgs a) {
     const int lane = threadIdx.x & 31;
     const int gl = lane & (G - 1);
     const unsigned gmask = (G == 32) ? 0xffffffffu : (((1u << G) - 1u) << (lane & ~(G - 1)));
-    const uint32_t n_groups = (gridDim.x * blockDim.x) / G;
     const int gl_eff = min(gl, int(a.k / F::W) - 1);
     const char* ylane = reinterpret_cast<const char*>(a.y + F::W * gl_eff);
     const uint32_t ldb = uint32_t(a.ld) * 4u;
@@ -77,8 +77,9 @@ __global__ void __launch_bounds__(128, MINB) sddmm_kernel(const SddmmArgs a) {
     // U dots share one X_i.
     constexpr bool LOCK = G < 32;
     constexpr unsigned FULL = 0xffffffffu;
-    for (uint32_t w = (blockIdx.x * blockDim.x + threadIdx.x) / G;
-         LOCK ? __any_sync(FULL, w < a.n_workers) : (w < a.n_workers); w += n_groups) {
+    dev::WarpSched<32 / G> ws(a.wctr);
+    for (uint32_t w = ws.base + uint32_t(lane / G); LOCK ? __any_sync(FULL, w < a.n_workers) : (w < a.n_workers);
+         ws.next(), w = ws.base + uint32_t(lane / G)) {
         const bool wact = w < a.n_workers;
         const uint32_t wq = wact ? w : a.n_workers - 1;
         // a plan's split (no search) or an even nnz split (binary search)
@@ -226,6 +227,7 @@ __global__ void __launch_bounds__(128, MINB) sddmm_kernel(const SddmmArgs a) {
             }
         }
     }
+    ws.finish();
 }
 
 using SddmmLaunch = sgnn_status (*)(const SddmmArgs&, cudaStream_t);
@@ -330,10 +332,12 @@ sgnn_status run_sddmm(const sgnn_csr* p, const float* x, const float* y, uint32_
     a.n_workers = uint32_t(ceil_div_u64(p->nnz, a.per_worker));
     a.wrow = nullptr;
     a.wnz = nullptr;
+    a.wctr = nullptr;
     if (plan) {  // reuse the plan's nnz-balanced split: worker starts need no row search
         a.wrow = plan->wrow;
         a.wnz = plan->wnz;
         a.n_workers = plan->n_workers;
+        a.wctr = plan_counter(plan, s);
     }
     SddmmLaunch fn = nullptr;
     if (vec) {
@@ -398,7 +402,7 @@ sgnn_status run_fusedmm(const sgnn_csr* p, const float* x, const float* y, uint3
         st = fail(SGNN_ERR_UNSUPPORTED, "fusedmm: no kernel for lanes=" + std::to_string(lanes) +
                                             " vec=" + std::to_string(vregs) + " unroll=" + std::to_string(unroll));
     if (st == SGNN_OK) {
-        SpmmArgs args;
+        SpmmArgs args{};
         args.rp = p->row_ptr;
         args.ci = p->col_idx;
         args.val = p->values;
@@ -416,6 +420,7 @@ sgnn_status run_fusedmm(const sgnn_csr* p, const float* x, const float* y, uint3
         args.ldc = k;
         args.ld_slot = plan->kt;
         args.width = k;
+        args.wctr = plan_counter(plan, s);
         st = launch(args, plan->p.block, 0, s);
     }
     if (st == SGNN_OK && plan->n_fix) {

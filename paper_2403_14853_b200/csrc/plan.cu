@@ -1,5 +1,6 @@
 // plan.cu -- builds the nnz-balanced worker split (see plan.cuh).
 #include <algorithm>
+#include <cstdlib>
 
 #include "plan.cuh"
 
@@ -142,14 +143,16 @@ void default_params(const sgnn_csr* a, uint32_t k, bool vec_ok, const DeviceProp
         d.unroll = d.vec >= 8 ? 2 : 4;
     }
     d.block = 128;
-    // Enough workers for ~4 per resident lane group, so the tail is short.
+    // Workers per resident lane group (warps take workers dynamically, so
+    // shorter workers even out the tail but cost row/segment cuts).  Probes
+    // (scripts/sched_probe.py): full-warp groups 8 per group (cfg2 1.57 ->
+    // 1.55 ms), 16-lane groups 4 (cfg4 FusedMM: 8 is 1.28x slower), 4-lane
+    // groups (K <= 16, little work per nonzero) 2 (cfg2 tuner: 1.29x over 4).
     const uint64_t total = a->nnz + a->n_rows;
     const uint64_t groups = uint64_t(dp.sm_count > 0 ? dp.sm_count : 148) *
                             uint64_t(dp.max_threads_per_sm > 0 ? dp.max_threads_per_sm : 2048) /
                             d.lanes;
-    // 4-lane groups (K <= 16) do little work per nonzero: longer paths
-    // (cfg2 tuner: 2 workers per group 1.29x over 4)
-    uint64_t want = total / ((d.lanes <= 4 ? 2 : 4) * groups);
+    uint64_t want = total / ((d.lanes <= 4 ? 2 : d.lanes == 32 ? 8 : 4) * groups);
     d.path_items = std::max<uint32_t>(32, std::min<uint32_t>(4096, pow2_floor(std::max<uint64_t>(want, 1))));
     d.split_rows_over = std::max<uint32_t>(d.path_items, SGNN_SEGMENT);
     d.k_tile = 0;
@@ -199,6 +202,21 @@ sgnn_status resolve_params(const sgnn_csr* a, uint32_t k, bool vec_ok, const Dev
     return SGNN_OK;
 }
 
+uint32_t* plan_counter(const sgnn_plan_s* p, cudaStream_t s) {
+    static const bool off = std::getenv("SGNN_STATIC_SCHEDULE") != nullptr;  // A/B switch
+    if (off || !p || !p->wctr || s == cudaStreamPerThread) return nullptr;
+    cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+    if (cudaStreamIsCapturing(s, &cs) != cudaSuccess) {
+        (void)cudaGetLastError();
+        return nullptr;
+    }
+    if (cs != cudaStreamCaptureStatusNone) return nullptr;
+    const uintptr_t key = reinterpret_cast<uintptr_t>(s) + 1;
+    uintptr_t owner = p->ctr_owner.load(std::memory_order_acquire);
+    if (owner == 0 && p->ctr_owner.compare_exchange_strong(owner, key, std::memory_order_acq_rel)) return p->wctr;
+    return owner == key ? p->wctr : nullptr;
+}
+
 bool plan_matches(const sgnn_plan_s* p, const sgnn_csr* a, uint32_t k) {
     return p && p->row_ptr == a->row_ptr && p->n_rows == a->n_rows && p->nnz == a->nnz && p->k == k;
 }
@@ -241,7 +259,8 @@ sgnn_status build_plan(const sgnn_csr* a, uint32_t k, const sgnn_plan_params* pa
     const size_t o_wnz = align(o_wrow + sizeof(uint32_t) * (size_t(W) + 1));
     const size_t o_wslot = align(o_wnz + sizeof(uint64_t) * (size_t(W) + 1));
     const size_t o_fscan = align(o_wslot + sizeof(uint32_t) * (size_t(W) + 1));
-    const size_t o_end = align(o_fscan + sizeof(uint32_t) * (size_t(W) + 1));
+    const size_t o_ctr = align(o_fscan + sizeof(uint32_t) * (size_t(W) + 1));
+    const size_t o_end = align(o_ctr + 2 * sizeof(uint32_t));
     cudaError_t ce = cudaMalloc(&plan->mem, o_end);
     if (ce != cudaSuccess) {
         delete plan;
@@ -252,6 +271,12 @@ sgnn_status build_plan(const sgnn_csr* a, uint32_t k, const sgnn_plan_params* pa
     plan->wnz = reinterpret_cast<uint64_t*>(base + o_wnz);
     plan->wslot = reinterpret_cast<uint32_t*>(base + o_wslot);
     uint32_t* fscan = reinterpret_cast<uint32_t*>(base + o_fscan);
+    plan->wctr = reinterpret_cast<uint32_t*>(base + o_ctr);
+    ce = cudaMemsetAsync(plan->wctr, 0, 2 * sizeof(uint32_t), s);  // ordered by the readback sync below
+    if (ce != cudaSuccess) {
+        destroy_plan(plan);
+        return fail(SGNN_ERR_CUDA, std::string("plan counter: ") + cudaGetErrorString(ce));
+    }
 
     const int tb = 256;
     plan_coords_kernel<<<unsigned(ceil_div_u64(uint64_t(W) + 1, tb)), tb, 0, s>>>(

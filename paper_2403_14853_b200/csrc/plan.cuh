@@ -12,6 +12,8 @@
 // rows go to a workspace and a fixup pass adds them left to right.
 #pragma once
 
+#include <atomic>
+
 #include "common.cuh"
 
 struct sgnn_plan_s {
@@ -40,9 +42,21 @@ struct sgnn_plan_s {
     uint32_t n_long = 0;
     float* slots = nullptr;        // [n_slots * kt]
     void* fmem = nullptr;          // allocation holding fix_row/fix_slot/slots
+    // dynamic worker schedule: [0] workers taken past the first round, [1]
+    // warps exited; the last warp of a launch zeroes both (plan_counter)
+    uint32_t* wctr = nullptr;
+    mutable std::atomic<uintptr_t> ctr_owner{0};  // stream key (+1) owning wctr
 };
 
 namespace sgnn {
+
+// The dynamic-schedule counter for a launch with `p` on stream `s`, or null
+// (static grid-stride schedule).  Launches on one stream are ordered, so the
+// counter belongs to the first ordinary stream that launches with the plan;
+// other streams, the per-thread default stream and graph captures take the
+// static schedule (same results: the schedule only decides which warp runs
+// which worker).
+uint32_t* plan_counter(const sgnn_plan_s* p, cudaStream_t s);
 
 // Library defaults for (A, K) (used when params fields are 0).
 void default_params(const sgnn_csr* a, uint32_t k, bool vec_ok, const DeviceProps& dp,

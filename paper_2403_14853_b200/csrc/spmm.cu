@@ -120,6 +120,7 @@ sgnn_status run_spmm(const sgnn_csr* a, const float* x, uint32_t k, float* c, in
             args.wslot = plan->wslot;
             args.n_rows = a->n_rows;
             args.n_workers = plan->n_workers;
+            args.wctr = plan_counter(plan, s);
             args.ldx = k;
             args.ldc = k;
             args.ld_slot = plan->kt;
@@ -193,6 +194,7 @@ sgnn_status run_spmm_peer(const sgnn_csr* a, const float* const* parts, uint32_t
             args.wslot = plan->wslot;
             args.n_rows = a->n_rows;
             args.n_workers = plan->n_workers;
+            args.wctr = plan_counter(plan, s);
             args.ldx = k;
             args.ldc = k;
             args.ld_slot = plan->kt;

@@ -47,6 +47,7 @@ struct SpmmArgs {
     // c & ((1 << part_shift) - 1); block base pointers pre-offset by k0
     const float* xparts[SGNN_MAX_PEERS];
     uint32_t part_shift;
+    uint32_t* wctr;  // dynamic worker schedule (plan_counter), null: static
 };
 
 struct FixupArgs {
@@ -341,7 +342,6 @@ __global__ void __launch_bounds__(128, MINB) spmm_worker_kernel(const SpmmArgs a
     const int lane = threadIdx.x & 31;
     const int gl = lane & (G - 1);
     const unsigned gmask = (G == 32) ? 0xffffffffu : (((1u << G) - 1u) << (lane & ~(G - 1)));
-    const uint32_t n_groups = (gridDim.x * blockDim.x) / G;
     // this lane's slice of any gathered row: byte offset col*ldxb from xlane
     // lanes past the width alias the row's last valid block (always in bounds)
     const int gl_eff = min(gl, int(a.width / F::W) - 1);
@@ -369,8 +369,9 @@ __global__ void __launch_bounds__(128, MINB) spmm_worker_kernel(const SpmmArgs a
     // exhausted idles through the remaining trips of the warp.
     constexpr bool LOCK = G < 32;
     constexpr unsigned FULL = 0xffffffffu;
-    for (uint32_t w = (blockIdx.x * blockDim.x + threadIdx.x) / G;
-         LOCK ? __any_sync(FULL, w < a.n_workers) : (w < a.n_workers); w += n_groups) {
+    dev::WarpSched<32 / G> ws(a.wctr);
+    for (uint32_t w = ws.base + uint32_t(lane / G); LOCK ? __any_sync(FULL, w < a.n_workers) : (w < a.n_workers);
+         ws.next(), w = ws.base + uint32_t(lane / G)) {
         const bool wact = w < a.n_workers;
         const uint32_t wq = wact ? w : a.n_workers - 1;  // idle group: no rows, no nonzeros
         const uint32_t i0 = __ldg(a.wrow + wq), i1 = wact ? __ldg(a.wrow + wq + 1) : i0;
@@ -671,6 +672,7 @@ __global__ void __launch_bounds__(128, MINB) spmm_worker_kernel(const SpmmArgs a
         }
         if (r < a.n_rows && E > rs_l) store_slot(acc);  // head of a split row
     }
+    ws.finish();
 }
 
 // Adds the segment partials of each split row left to right and applies the

@@ -205,3 +205,69 @@ def test_misaligned_operands_use_scalar_path(cuda):
     out = ops.spmm(a, xt, "sum")
     want = port.spmm(rp, ci, v, x, 0, np.float32)
     np.testing.assert_array_equal(out.cpu().numpy().view(np.uint32), want.view(np.uint32))
+
+
+# ---- dynamic worker schedule (common.cuh WarpSched, plan.cu plan_counter) ----
+@pytest.mark.parametrize("k", [64, 256])
+def test_dynamic_schedule_counter_reset_streams_graphs(cuda, k):
+    """Many more workers than resident warps, so warps take workers from the
+    plan's counter.  The counter resets itself at the end of each launch:
+    repeated launches, a launch on a second stream (static schedule), and CUDA
+    graph replays (static) are bitwise the first launch, which matches the
+    oracle.  FusedMM and SDDMM share the counter of the fused plan."""
+    import torch
+    from paper_2403_14853_b200 import graphs
+    ops = _ops()
+    rp, ci = graphs.rmat(15, 16 << 15, seed=5)
+    v = graphs.normal(len(ci), 0, 1, 9)
+    n = len(rp) - 1
+    x = graphs.normal(n * k, 0, 1, 10).reshape(n, k)
+    a = ops.CsrMatrix.from_numpy(rp, ci, v, n)
+    xt = torch.from_numpy(x).cuda()
+    plan = ops.Plan(a, k, path_items=32)
+    assert plan.stats["workers"] > 2 * 148 * 20 * 2  # > 2 rounds of resident worker sets (occupancy 5)
+    first = ops.spmm_plan(a, xt, "sum", plan)
+    want32 = port.spmm(rp, ci, v, x, 0, np.float32)
+    short = _short_rows(rp)
+    np.testing.assert_array_equal(first.cpu().numpy()[short].view(np.uint32), want32[short].view(np.uint32))
+    ref = first.cpu().numpy()
+    out = torch.empty_like(first)
+
+    def again():  # into a NaN-filled output: a skipped worker would show
+        out.fill_(float("nan"))
+        ops.spmm_plan(a, xt, "sum", plan, out)
+        return out.cpu().numpy()
+
+    for _ in range(5):
+        np.testing.assert_array_equal(again(), ref)
+    side = torch.cuda.Stream()
+    side.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.stream(side):
+        out.fill_(float("nan"))
+        ops.spmm_plan(a, xt, "sum", plan, out)
+    torch.cuda.current_stream().wait_stream(side)
+    np.testing.assert_array_equal(out.cpu().numpy(), ref)
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g):
+        ops.spmm_plan(a, xt, "sum", plan, out)
+    for _ in range(3):
+        out.fill_(float("nan"))
+        g.replay()
+        np.testing.assert_array_equal(out.cpu().numpy(), ref)
+    # after the capture, the owning stream still gets the dynamic schedule
+    np.testing.assert_array_equal(again(), ref)
+    # FusedMM / SDDMM over the fused plan's counter
+    if k == 64:
+        y = torch.from_numpy(graphs.normal(n * k, 0, 0.1, 11).reshape(n, k)).cuda()
+        xs = xt * 0.1
+        f0 = ops.fusedmm(a, xs, y, "mul", "sum").cpu().numpy()
+        s0 = ops.sddmm(a, xs, y).values.cpu().numpy()
+        for _ in range(3):
+            out.fill_(float("nan"))
+            ops.fusedmm(a, xs, y, "mul", "sum", out=out)
+            np.testing.assert_array_equal(out.cpu().numpy(), f0)
+            nan = torch.full((len(ci),), float("nan"), device="cuda")
+            del nan  # the caching allocator hands this block to sddmm's output
+            np.testing.assert_array_equal(ops.sddmm(a, xs, y).values.cpu().numpy(), s0)
+        want_s = port.sddmm(rp, ci, v, xs.cpu().numpy().astype(np.float64), y.cpu().numpy().astype(np.float64))
+        np.testing.assert_allclose(s0, want_s, rtol=1e-4, atol=1e-5)
