@@ -134,9 +134,13 @@ void default_params(const sgnn_csr* a, uint32_t k, bool vec_ok, const DeviceProp
         else if (k <= 128) { d.lanes = 32; d.vec = 1; }
         else if (k <= 256) { d.lanes = 32; d.vec = 2; }
         else { d.lanes = 32; d.vec = 2; }  // 256-wide passes: cfg2 1.28x (K=512), 1.26x (K=1024) over vec 4
-        d.unroll = d.vec >= 4 ? 4 : (d.vec == 2 ? (k > 256 ? 8 : 4) : 8);
+        // 8 gathers in flight except with 4 float4 per lane; two float4 per
+        // lane (128 < K <= 256) at the compiler's register allocation: the
+        // tuner's choice on cfg2 K=256 (1.04x) and cfg3 (1.08x over U=4 at
+        // the 5-CTA cap; profiles/r01_tuning_cfg2.csv, r01_tune_cfg35.log)
+        d.unroll = d.vec >= 4 ? 4 : 8;
         // register cap for 5 resident 128-thread CTAs: best or equal on cfg1-cfg4 probes
-        if (d.vec <= 2 && k > 16 && k <= 256) d.occupancy = 5;
+        if (d.vec == 1 && k > 16) d.occupancy = 5;
     } else {
         d.lanes = 32;
         d.vec = k <= 32 ? 1 : k <= 64 ? 2 : k <= 128 ? 4 : 8;
@@ -145,15 +149,18 @@ void default_params(const sgnn_csr* a, uint32_t k, bool vec_ok, const DeviceProp
     d.block = 128;
     // Workers per resident lane group (warps take workers dynamically, so
     // shorter workers even out the tail but cost row/segment cuts).  Probes
-    // (scripts/sched_probe.py): full-warp groups 8 per group (cfg2 1.57 ->
-    // 1.55 ms), 16-lane groups 4 (cfg4 FusedMM: 8 is 1.28x slower), 4-lane
-    // groups (K <= 16, little work per nonzero) 2 (cfg2 tuner: 1.29x over 4).
+    // (scripts/sched_probe.py): 16-lane groups 4 (cfg4 FusedMM: 8 is 1.28x
+    // slower), 4-lane groups (K <= 16, little work per nonzero) 2 (cfg2
+    // tuner: 1.29x over 4); full-warp groups 8, capped below.
     const uint64_t total = a->nnz + a->n_rows;
     const uint64_t groups = uint64_t(dp.sm_count > 0 ? dp.sm_count : 148) *
                             uint64_t(dp.max_threads_per_sm > 0 ? dp.max_threads_per_sm : 2048) /
                             d.lanes;
     uint64_t want = total / ((d.lanes <= 4 ? 2 : d.lanes == 32 ? 8 : 4) * groups);
-    d.path_items = std::max<uint32_t>(32, std::min<uint32_t>(4096, pow2_floor(std::max<uint64_t>(want, 1))));
+    // full-warp groups: at most 1024 rows+nonzeros per worker (cfg5 tuner:
+    // 1.035x over 2048; cfg2 1.55 ms, 8 per group)
+    const uint32_t cap = d.lanes == 32 ? 1024 : 4096;
+    d.path_items = std::max<uint32_t>(32, std::min<uint32_t>(cap, pow2_floor(std::max<uint64_t>(want, 1))));
     d.split_rows_over = std::max<uint32_t>(d.path_items, SGNN_SEGMENT);
     d.k_tile = 0;
     d.scalar = p->scalar;
