@@ -18,22 +18,95 @@ namespace {
 
 constexpr int kGcn = 0, kSageSum = 1, kSageMean = 2, kGin = 3;  // ModelKind order, gnn.hpp:17
 
-__global__ void relu_kernel(const float* __restrict__ x, uint64_t n, float* __restrict__ y) {
-    for (uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += uint64_t(gridDim.x) * blockDim.x)
-        y[i] = x[i] > 0.0f ? x[i] : 0.0f;  // relu (dense.hpp)
+// Element-wise passes over n floats: float4 body (every buffer here is a
+// whole cudaMalloc allocation or a 16-byte aligned offset into one) plus a
+// scalar tail; grid-stride over at most grid_for(n / 4) blocks.
+template <class Op>
+__device__ __forceinline__ void ew_loop(uint64_t n, Op op) {
+    const uint64_t n4 = n / 4, stride = uint64_t(gridDim.x) * blockDim.x;
+    const uint64_t t0 = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    for (uint64_t i = t0; i < n4; i += stride) op.vec(i);
+    for (uint64_t i = 4 * n4 + t0; i < n; i += stride) op.one(i);
 }
 
+// relu (dense.hpp): x > 0 ? x : 0
+__device__ __forceinline__ float relu1(float x) { return x > 0.0f ? x : 0.0f; }
 // relu_backward: grad where act > 0, else 0
+__device__ __forceinline__ float relu_bwd1(float g, float act) { return act <= 0.0f ? 0.0f : g; }
+
+__global__ void relu_kernel(const float* __restrict__ x, uint64_t n, float* __restrict__ y) {
+    struct {
+        const float* x; float* y;
+        __device__ void vec(uint64_t i) const {
+            const float4 a = reinterpret_cast<const float4*>(x)[i];
+            reinterpret_cast<float4*>(y)[i] = make_float4(relu1(a.x), relu1(a.y), relu1(a.z), relu1(a.w));
+        }
+        __device__ void one(uint64_t i) const { y[i] = relu1(x[i]); }
+    } op{x, y};
+    ew_loop(n, op);
+}
+
 __global__ void relu_backward_kernel(const float* __restrict__ g, const float* __restrict__ act, uint64_t n,
                                      float* __restrict__ out) {
-    for (uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += uint64_t(gridDim.x) * blockDim.x)
-        out[i] = act[i] <= 0.0f ? 0.0f : g[i];
+    struct {
+        const float *g, *act; float* out;
+        __device__ void vec(uint64_t i) const {
+            const float4 a = reinterpret_cast<const float4*>(g)[i], h = reinterpret_cast<const float4*>(act)[i];
+            reinterpret_cast<float4*>(out)[i] =
+                make_float4(relu_bwd1(a.x, h.x), relu_bwd1(a.y, h.y), relu_bwd1(a.z, h.z), relu_bwd1(a.w, h.w));
+        }
+        __device__ void one(uint64_t i) const { out[i] = relu_bwd1(g[i], act[i]); }
+    } op{g, act, out};
+    ew_loop(n, op);
 }
 
 // y += x (add_inplace)
 __global__ void add_kernel(float* __restrict__ y, const float* __restrict__ x, uint64_t n) {
-    for (uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += uint64_t(gridDim.x) * blockDim.x)
-        y[i] = __fadd_rn(y[i], x[i]);
+    struct {
+        float* y; const float* x;
+        __device__ void vec(uint64_t i) const {
+            float4 a = reinterpret_cast<float4*>(y)[i];
+            const float4 b = reinterpret_cast<const float4*>(x)[i];
+            a.x = __fadd_rn(a.x, b.x); a.y = __fadd_rn(a.y, b.y); a.z = __fadd_rn(a.z, b.z); a.w = __fadd_rn(a.w, b.w);
+            reinterpret_cast<float4*>(y)[i] = a;
+        }
+        __device__ void one(uint64_t i) const { y[i] = __fadd_rn(y[i], x[i]); }
+    } op{y, x};
+    ew_loop(n, op);
+}
+
+// h = relu(a + b): SAGE's z1 = a1 W1 + X W1s followed by relu (gnn.hpp:238-239)
+// in one pass; z1 itself is not needed later (relu_backward tests h1).
+__global__ void add_relu_kernel(const float* __restrict__ a, const float* __restrict__ b, uint64_t n,
+                                float* __restrict__ h) {
+    struct {
+        const float *a, *b; float* h;
+        __device__ void vec(uint64_t i) const {
+            const float4 u = reinterpret_cast<const float4*>(a)[i], v = reinterpret_cast<const float4*>(b)[i];
+            reinterpret_cast<float4*>(h)[i] = make_float4(relu1(__fadd_rn(u.x, v.x)), relu1(__fadd_rn(u.y, v.y)),
+                                                          relu1(__fadd_rn(u.z, v.z)), relu1(__fadd_rn(u.w, v.w)));
+        }
+        __device__ void one(uint64_t i) const { h[i] = relu1(__fadd_rn(a[i], b[i])); }
+    } op{a, b, h};
+    ew_loop(n, op);
+}
+
+// out = relu_backward(g + u, act): SAGE's dh1 = A^T ds2 + grad W2s^T then
+// dz1 (gnn.hpp:290-292) in one pass.
+__global__ void add_relu_backward_kernel(const float* __restrict__ g, const float* __restrict__ u,
+                                         const float* __restrict__ act, uint64_t n, float* __restrict__ out) {
+    struct {
+        const float *g, *u, *act; float* out;
+        __device__ void vec(uint64_t i) const {
+            const float4 a = reinterpret_cast<const float4*>(g)[i], b = reinterpret_cast<const float4*>(u)[i];
+            const float4 h = reinterpret_cast<const float4*>(act)[i];
+            reinterpret_cast<float4*>(out)[i] =
+                make_float4(relu_bwd1(__fadd_rn(a.x, b.x), h.x), relu_bwd1(__fadd_rn(a.y, b.y), h.y),
+                            relu_bwd1(__fadd_rn(a.z, b.z), h.z), relu_bwd1(__fadd_rn(a.w, b.w), h.w));
+        }
+        __device__ void one(uint64_t i) const { out[i] = relu_bwd1(__fadd_rn(g[i], u[i]), act[i]); }
+    } op{g, u, act, out};
+    ew_loop(n, op);
 }
 
 // out = (1 + eps) * x + y  (scaled_add with the GIN scale, eps on the device)
@@ -50,62 +123,94 @@ __global__ void sgd_kernel(float* __restrict__ w, const float* __restrict__ g, u
         w[i] = __fsub_rn(w[i], __fmul_rn(lr, g[i]));
 }
 
-// softmax_xent + masked_accuracy, one warp per row: per-row loss (double) and
-// correct flag, gradient rows (zero outside the mask).
-__global__ void softmax_xent_kernel(const float* __restrict__ logits, uint32_t n, uint32_t c,
-                                    const uint32_t* __restrict__ labels, const uint8_t* __restrict__ mask,
-                                    double inv_n, float* __restrict__ grad, double* __restrict__ row_loss,
-                                    uint32_t* __restrict__ row_ok) {
-    const uint32_t lane = threadIdx.x & 31;
-    const uint32_t nw = (gridDim.x * blockDim.x) >> 5;
-    for (uint32_t i = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; i < n; i += nw) {
+// softmax_xent + masked_accuracy (gnn.hpp:318-370).  A group of G lanes
+// (G = the power of two >= classes, at most 32) owns a row; lane j holds
+// class j (and j + G, ... when classes > 32).  Per row: the gradient row
+// (zero outside the mask), and the row's loss (double) and correct flag
+// folded into the group's running sums.  Block b covers the contiguous rows
+// [b*rpb, (b+1)*rpb); its groups' sums are added in group order and written
+// to blk_loss[b] / blk_ok[b] -- a fixed order for a given n, so the epoch's
+// loss is deterministic (epoch_stats_kernel adds the block sums).
+constexpr int kSoftmaxThreads = 256;
+template <int G>
+__global__ void __launch_bounds__(kSoftmaxThreads) softmax_xent_kernel(
+    const float* __restrict__ logits, uint32_t n, uint32_t c, const uint32_t* __restrict__ labels,
+    const uint8_t* __restrict__ mask, double inv_n, uint32_t rpb, float* __restrict__ grad,
+    double* __restrict__ blk_loss, uint32_t* __restrict__ blk_ok) {
+    constexpr int NG = kSoftmaxThreads / G;
+    __shared__ double s_loss[NG];
+    __shared__ uint32_t s_ok[NG];
+    const uint32_t gl = threadIdx.x % G, grp = threadIdx.x / G;
+    const unsigned gmask = G == 32 ? 0xffffffffu : (((1u << G) - 1u) << ((threadIdx.x & 31) & ~(G - 1)));
+    const uint32_t r0 = blockIdx.x * rpb, r1 = min(n, r0 + rpb);
+    double lsum = 0.0;
+    uint32_t oks = 0;
+    for (uint32_t i = r0 + grp; i < r1; i += NG) {  // group-uniform trip count
         const float* row = logits + uint64_t(i) * c;
         float* grow = grad + uint64_t(i) * c;
         if (!mask[i]) {
-            for (uint32_t j = lane; j < c; j += 32) grow[j] = 0.0f;
-            if (lane == 0) {
-                row_loss[i] = 0.0;
-                row_ok[i] = 0;
-            }
+            for (uint32_t j = gl; j < c; j += G) grow[j] = 0.0f;
             continue;
         }
-        double mx = -1.0 / 0.0;
+        float mxf = -1.0f / 0.0f, bestv = -1.0f / 0.0f;
         uint32_t best = 0;
-        float bestv = -1.0f / 0.0f;
-        for (uint32_t j = lane; j < c; j += 32) {
+        for (uint32_t j = gl; j < c; j += G) {
             const float v = row[j];
-            mx = fmax(mx, double(v));
-            if (v > bestv) {  // ties: smallest class index (lane order then merge)
+            mxf = fmaxf(mxf, v);
+            if (v > bestv) {  // ties: smallest class index
                 bestv = v;
                 best = j;
             }
         }
-        for (int s = 16; s >= 1; s >>= 1) {
-            mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, s));
-            const float ov = __shfl_xor_sync(0xffffffffu, bestv, s);
-            const uint32_t oj = __shfl_xor_sync(0xffffffffu, best, s);
+#pragma unroll
+        for (int o = G / 2; o >= 1; o >>= 1) {
+            mxf = fmaxf(mxf, __shfl_xor_sync(gmask, mxf, o, G));
+            const float ov = __shfl_xor_sync(gmask, bestv, o, G);
+            const uint32_t oj = __shfl_xor_sync(gmask, best, o, G);
             if (ov > bestv || (ov == bestv && oj < best)) {
                 bestv = ov;
                 best = oj;
             }
         }
-        double den = 0.0;
-        for (uint32_t j = lane; j < c; j += 32) den += exp(double(row[j]) - mx);
-        for (int s = 16; s >= 1; s >>= 1) den += __shfl_xor_sync(0xffffffffu, den, s);
+        const double mx = double(mxf);  // max in double of the float logits
+        double e0 = 0.0, den = 0.0;
+        for (uint32_t j = gl; j < c; j += G) {
+            const double e = exp(double(row[j]) - mx);
+            if (j == gl) e0 = e;
+            den += e;
+        }
+#pragma unroll
+        for (int o = G / 2; o >= 1; o >>= 1) den += __shfl_xor_sync(gmask, den, o, G);
         const uint32_t lab = labels[i];
-        for (uint32_t j = lane; j < c; j += 32) {
-            const double p = exp(double(row[j]) - mx) / den;
+        for (uint32_t j = gl; j < c; j += G) {
+            const double p = (j == gl ? e0 : exp(double(row[j]) - mx)) / den;
             grow[j] = float((p - (j == lab ? 1.0 : 0.0)) * inv_n);
         }
-        if (lane == 0) {
-            row_loss[i] = (mx + log(den)) - double(row[lab]);
-            row_ok[i] = best == lab ? 1u : 0u;
+        if (gl == 0) {
+            lsum += (mx + log(den)) - double(row[lab]);
+            oks += best == lab ? 1u : 0u;
         }
+    }
+    if (gl == 0) {
+        s_loss[grp] = lsum;
+        s_ok[grp] = oks;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double l = 0.0;
+        uint32_t k = 0;
+        for (int q = 0; q < NG; ++q) {
+            l += s_loss[q];
+            k += s_ok[q];
+        }
+        blk_loss[blockIdx.x] = l;
+        blk_ok[blockIdx.x] = k;
     }
 }
 
-// Sum of the per-row losses / correct flags in a fixed order (one block), and
-// the epoch's stats written to stats[2 * (*epoch)]; epoch counter advanced.
+// Sum of the per-block losses / correct counts in a fixed order (one
+// block), and the epoch's stats written to stats[2 * (*epoch)]; epoch
+// counter advanced.
 __global__ void __launch_bounds__(1024) epoch_stats_kernel(const double* __restrict__ row_loss,
                                                            const uint32_t* __restrict__ row_ok, uint32_t n,
                                                            double inv_n, double* __restrict__ stats,
@@ -162,6 +267,17 @@ __global__ void eps_step_kernel(float* eps, double* deps, float lr) {
 unsigned grid_for(uint64_t n) {
     const uint64_t b = (n + 255) / 256;
     return unsigned(b < 4096 ? (b ? b : 1) : 4096);
+}
+
+// softmax_xent launch shape for n rows: rows per block and blocks (a fixed
+// function of n, so the loss reduction order is too)
+void softmax_shape(uint32_t n, uint32_t* rpb, uint32_t* blocks) {
+    const uint32_t want = 2048;  // blocks (~14 per SM)
+    uint32_t r = (n + want - 1) / want;
+    r = r < 1 ? 1 : r;
+    *rpb = r;
+    *blocks = (n + r - 1) / r;
+    if (*blocks == 0) *blocks = 1;
 }
 
 }  // namespace
@@ -253,6 +369,12 @@ sgnn_status fwd_spmm(sgnn_gnn_s* g, const float* x, uint32_t k, float* out, int 
         kernel<<<grid_for(n), 256, 0, s>>>(__VA_ARGS__);                       \
         SGNN_LAUNCH_CHECK();                                                   \
     } while (0)
+// float4 element-wise kernels (ew_loop): a quarter of the threads
+#define LAUNCH_EW4(kernel, n, ...)                                             \
+    do {                                                                       \
+        kernel<<<grid_for(((n) + 3) / 4), 256, 0, s>>>(__VA_ARGS__);           \
+        SGNN_LAUNCH_CHECK();                                                   \
+    } while (0)
 
 // One epoch (gnn.hpp:427-435): forward, softmax_xent, accuracy, backward, sgd.
 sgnn_status epoch(sgnn_gnn_s* g, float lr, cudaStream_t s) {
@@ -263,34 +385,45 @@ sgnn_status epoch(sgnn_gnn_s* g, float lr, cudaStream_t s) {
     if (g->kind == kGcn) {
         SGNN_TRY(mm(g, g->x, g->w1, g->z1, n, in, hid));                 // z1 = X W1
         SGNN_TRY(fwd_spmm(g, g->z1, g->hid, g->t1, SGNN_REDUCE_SUM, s));  // A_hat z1
-        LAUNCH_EW(relu_kernel, nh, g->t1, nh, g->h1);                     // h1
+        LAUNCH_EW4(relu_kernel, nh, g->t1, nh, g->h1);                    // h1
         SGNN_TRY(mm(g, g->h1, g->w2, g->t2, n, hid, cls));               // z2 = h1 W2
         SGNN_TRY(fwd_spmm(g, g->t2, g->cls, g->logits, SGNN_REDUCE_SUM, s));
     } else if (g->kind == kSageSum || g->kind == kSageMean) {
         SGNN_TRY(fwd_spmm(g, g->x, g->in, g->a1, red, s));                // a1 = A X
         SGNN_TRY(mm(g, g->a1, g->w1, g->z1, n, in, hid));
         SGNN_TRY(mm(g, g->x, g->w1s, g->t1, n, in, hid));
-        LAUNCH_EW(add_kernel, nh, g->z1, g->t1, nh);                       // z1 = a1 W1 + X W1s
-        LAUNCH_EW(relu_kernel, nh, g->z1, nh, g->h1);
+        LAUNCH_EW4(add_relu_kernel, nh, g->z1, g->t1, nh, g->h1);          // h1 = relu(a1 W1 + X W1s)
         SGNN_TRY(fwd_spmm(g, g->h1, g->hid, g->a2, red, s));               // a2 = A h1
         SGNN_TRY(mm(g, g->a2, g->w2, g->logits, n, hid, cls));
         SGNN_TRY(mm(g, g->h1, g->w2s, g->t2, n, hid, cls));
-        LAUNCH_EW(add_kernel, nc, g->logits, g->t2, nc);
+        LAUNCH_EW4(add_kernel, nc, g->logits, g->t2, nc);
     } else {  // GIN
         SGNN_TRY(fwd_spmm(g, g->x, g->in, g->t1, SGNN_REDUCE_SUM, s));
         LAUNCH_EW(scaled_add_kernel, ni, g->eps, g->x, g->t1, ni, g->a1);  // a1 = (1+eps) X + A X
         SGNN_TRY(mm(g, g->a1, g->w1, g->z1, n, in, hid));
-        LAUNCH_EW(relu_kernel, nh, g->z1, nh, g->h1);
+        LAUNCH_EW4(relu_kernel, nh, g->z1, nh, g->h1);
         SGNN_TRY(fwd_spmm(g, g->h1, g->hid, g->z1, SGNN_REDUCE_SUM, s));
         LAUNCH_EW(scaled_add_kernel, nh, g->eps, g->h1, g->z1, nh, g->a2);
         SGNN_TRY(mm(g, g->a2, g->w2, g->logits, n, hid, cls));
     }
     // ---- softmax_xent + masked_accuracy (gnn.hpp:318-370)
     const double inv_n = 1.0 / double(g->n_masked);
-    softmax_xent_kernel<<<grid_for(uint64_t(g->n) * 32), 256, 0, s>>>(g->logits, g->n, g->cls, g->labels, g->mask,
-                                                                      inv_n, g->grad, g->row_loss, g->row_ok);
+    uint32_t rpb = 1, nblk = 1;
+    softmax_shape(g->n, &rpb, &nblk);
+    if (g->cls <= 4)
+        softmax_xent_kernel<4><<<nblk, kSoftmaxThreads, 0, s>>>(g->logits, g->n, g->cls, g->labels, g->mask, inv_n,
+                                                                rpb, g->grad, g->row_loss, g->row_ok);
+    else if (g->cls <= 8)
+        softmax_xent_kernel<8><<<nblk, kSoftmaxThreads, 0, s>>>(g->logits, g->n, g->cls, g->labels, g->mask, inv_n,
+                                                                rpb, g->grad, g->row_loss, g->row_ok);
+    else if (g->cls <= 16)
+        softmax_xent_kernel<16><<<nblk, kSoftmaxThreads, 0, s>>>(g->logits, g->n, g->cls, g->labels, g->mask, inv_n,
+                                                                 rpb, g->grad, g->row_loss, g->row_ok);
+    else
+        softmax_xent_kernel<32><<<nblk, kSoftmaxThreads, 0, s>>>(g->logits, g->n, g->cls, g->labels, g->mask, inv_n,
+                                                                 rpb, g->grad, g->row_loss, g->row_ok);
     SGNN_LAUNCH_CHECK();
-    epoch_stats_kernel<<<1, 1024, 0, s>>>(g->row_loss, g->row_ok, g->n, inv_n, g->stats, g->epoch, g->max_epochs);
+    epoch_stats_kernel<<<1, 1024, 0, s>>>(g->row_loss, g->row_ok, nblk, inv_n, g->stats, g->epoch, g->max_epochs);
     SGNN_LAUNCH_CHECK();
     // ---- backward (gnn.hpp:261-313)
     if (g->kind == kGcn) {
@@ -299,7 +432,7 @@ sgnn_status epoch(sgnn_gnn_s* g, float lr, cudaStream_t s) {
         SGNN_TRY(cache_spmm_with_operand(g->cache, &at, g->grad, g->cls, g->d_c, s));                 // dz2
         SGNN_TRY(mm_tn(g, g->h1, g->d_c, g->g2, n, hid, cls));                                        // W2 grad
         SGNN_TRY(mm_nt(g, g->d_c, g->w2, g->d_h, n, cls, hid));                                       // dh1
-        LAUNCH_EW(relu_backward_kernel, nh, g->d_h, g->h1, nh, g->d_h2);                             // dp1
+        LAUNCH_EW4(relu_backward_kernel, nh, g->d_h, g->h1, nh, g->d_h2);                            // dp1
         SGNN_TRY(cache_spmm_with_operand(g->cache, &at, g->d_h2, g->hid, g->d_h, s));                 // dz1
         SGNN_TRY(mm_tn(g, g->x, g->d_h, g->g1, n, in, hid));
     } else if (g->kind == kSageSum || g->kind == kSageMean) {
@@ -308,10 +441,10 @@ sgnn_status epoch(sgnn_gnn_s* g, float lr, cudaStream_t s) {
         SGNN_TRY(mm_nt(g, g->grad, g->w2, g->d_h, n, cls, hid));                                      // ds2
         SGNN_TRY(cache_spmm_backward(g->cache, g->d_h, g->n, g->hid, g->d_h2, red, s));              // dh1
         SGNN_TRY(mm_nt(g, g->grad, g->w2s, g->d_h, n, cls, hid));
-        LAUNCH_EW(add_kernel, nh, g->d_h2, g->d_h, nh);
-        LAUNCH_EW(relu_backward_kernel, nh, g->d_h2, g->h1, nh, g->d_h);                             // dz1
-        SGNN_TRY(mm_tn(g, g->a1, g->d_h, g->g1, n, in, hid));
-        SGNN_TRY(mm_tn(g, g->x, g->d_h, g->g1s, n, in, hid));
+        // dz1 into z1 (free after the forward's add_relu)
+        LAUNCH_EW4(add_relu_backward_kernel, nh, g->d_h2, g->d_h, g->h1, nh, g->z1);
+        SGNN_TRY(mm_tn(g, g->a1, g->z1, g->g1, n, in, hid));
+        SGNN_TRY(mm_tn(g, g->x, g->z1, g->g1s, n, in, hid));
     } else {  // GIN
         SGNN_TRY(mm_tn(g, g->a2, g->grad, g->g2, n, hid, cls));
         SGNN_TRY(mm_nt(g, g->grad, g->w2, g->d_h, n, cls, hid));                                      // dm2
@@ -319,7 +452,7 @@ sgnn_status epoch(sgnn_gnn_s* g, float lr, cudaStream_t s) {
         SGNN_LAUNCH_CHECK();
         SGNN_TRY(cache_spmm_backward(g->cache, g->d_h, g->n, g->hid, g->d_h2, SGNN_REDUCE_SUM, s));
         LAUNCH_EW(scaled_add_kernel, nh, g->eps, g->d_h, g->d_h2, nh, g->z1);                        // dh1
-        LAUNCH_EW(relu_backward_kernel, nh, g->z1, g->h1, nh, g->d_h2);                              // dz1
+        LAUNCH_EW4(relu_backward_kernel, nh, g->z1, g->h1, nh, g->d_h2);                             // dz1
         SGNN_TRY(mm_tn(g, g->a1, g->d_h2, g->g1, n, in, hid));
         SGNN_TRY(mm_nt(g, g->d_h2, g->w1, g->t1, n, hid, in));                                        // dm1
         dot_all_kernel<<<1, 1024, 0, s>>>(g->t1, g->x, ni, g->deps);
