@@ -8,6 +8,8 @@
 // and replayed as a CUDA graph.
 #include <cublas_v2.h>
 
+#include <algorithm>
+#include <cstdlib>
 #include <cstring>
 #include <vector>
 
@@ -243,6 +245,244 @@ __global__ void __launch_bounds__(1024) epoch_stats_kernel(const double* __restr
     }
 }
 
+// ---- SAGE's classes-wide products (hidden h <= 128, h % 4 == 0, classes
+// c <= CP): memory-bound passes of their own instead of cuBLAS calls that
+// run far below HBM speed at this shape.  A warp owns a row; lane l holds
+// hidden features 4l..4l+3 (lanes l >= h/4 idle in the loads).  Each
+// product is rounded on its own and the two are added like the reference
+// (matmul, matmul, add: gnn.hpp:241-244 and :285-292).
+
+// grad[i, 0..CP) (zero past c); float4 loads when rows are 16-byte aligned
+template <int CP>
+__device__ __forceinline__ void load_grad_row(const float* __restrict__ grad, uint32_t i, uint32_t c, float (&g)[CP]) {
+    if (c % 4 == 0) {
+        const float4* r = reinterpret_cast<const float4*>(grad + uint64_t(i) * c);
+#pragma unroll
+        for (int j4 = 0; j4 < CP / 4; ++j4) {
+            const float4 v = 4 * j4 < int(c) ? __ldg(r + j4) : make_float4(0.f, 0.f, 0.f, 0.f);
+            g[4 * j4] = v.x; g[4 * j4 + 1] = v.y; g[4 * j4 + 2] = v.z; g[4 * j4 + 3] = v.w;
+        }
+    } else {
+#pragma unroll
+        for (int j = 0; j < CP; ++j) g[j] = j < int(c) ? __ldg(grad + uint64_t(i) * c + j) : 0.0f;
+    }
+}
+
+// W (row-major h x c) staged in shared memory for lane l's rows 4l..4l+3:
+// float4 (q, j4) of lane l = W[4l + q][4 j4 .. 4 j4 + 3] at index
+// (q * CP/4 + j4) * 32 + l, so a warp's LDS.128 hits consecutive addresses.
+template <int CP>
+__device__ __forceinline__ void stage_w(const float* __restrict__ w, uint32_t h, uint32_t c, float4* sw) {
+    for (uint32_t t = threadIdx.x; t < 4 * (CP / 4) * 32; t += blockDim.x) {
+        const uint32_t l = t % 32, qj = t / 32, q = qj / (CP / 4), j4 = qj % (CP / 4), k = 4 * l + q;
+        float v[4];
+#pragma unroll
+        for (int e = 0; e < 4; ++e) v[e] = (k < h && 4 * j4 + e < c) ? w[k * c + 4 * j4 + e] : 0.0f;
+        sw[t] = make_float4(v[0], v[1], v[2], v[3]);
+    }
+}
+
+// logits[i, :] = [a2 | h1][i, :] . [W2; W2s]: one fp32 accumulation over the
+// concatenated 2h inputs (the usual SAGE concat form of a2 W2 + h1 W2s).
+// A warp takes RU rows at a time (their loads in flight together).
+template <int CP>
+__global__ void __launch_bounds__(256) sage_logits_kernel(const float* __restrict__ a2, const float* __restrict__ h1,
+                                                          const float* __restrict__ w2, const float* __restrict__ w2s,
+                                                          uint32_t n, uint32_t h, uint32_t c,
+                                                          float* __restrict__ logits) {
+    constexpr int RU = 4, J4 = CP / 4;
+    __shared__ float4 sw[2][4 * J4 * 32];
+    stage_w<CP>(w2, h, c, sw[0]);
+    stage_w<CP>(w2s, h, c, sw[1]);
+    __syncthreads();
+    const uint32_t lane = threadIdx.x & 31;
+    const bool act = lane < h / 4;
+    const uint32_t nw = (gridDim.x * blockDim.x) >> 5;
+    for (uint32_t i0 = ((blockIdx.x * blockDim.x + threadIdx.x) >> 5) * RU; i0 < n; i0 += nw * RU) {
+        float4 x[2][RU];
+#pragma unroll
+        for (int r = 0; r < RU; ++r) {
+            const bool ok = act && i0 + r < n;
+            x[0][r] = ok ? __ldg(reinterpret_cast<const float4*>(a2 + uint64_t(i0 + r) * h) + lane) : make_float4(0.f, 0.f, 0.f, 0.f);
+            x[1][r] = ok ? __ldg(reinterpret_cast<const float4*>(h1 + uint64_t(i0 + r) * h) + lane) : make_float4(0.f, 0.f, 0.f, 0.f);
+        }
+        float p[RU][CP];
+#pragma unroll
+        for (int r = 0; r < RU; ++r)
+#pragma unroll
+            for (int j = 0; j < CP; ++j) p[r][j] = 0.0f;
+#pragma unroll
+        for (int m = 0; m < 2; ++m)
+#pragma unroll
+            for (int q = 0; q < 4; ++q)
+#pragma unroll
+                for (int j4 = 0; j4 < J4; ++j4) {
+                    const float4 wv = sw[m][(q * J4 + j4) * 32 + lane];
+#pragma unroll
+                    for (int r = 0; r < RU; ++r) {
+                        const float xv = q == 0 ? x[m][r].x : q == 1 ? x[m][r].y : q == 2 ? x[m][r].z : x[m][r].w;
+                        p[r][4 * j4 + 0] = __fmaf_rn(xv, wv.x, p[r][4 * j4 + 0]);
+                        p[r][4 * j4 + 1] = __fmaf_rn(xv, wv.y, p[r][4 * j4 + 1]);
+                        p[r][4 * j4 + 2] = __fmaf_rn(xv, wv.z, p[r][4 * j4 + 2]);
+                        p[r][4 * j4 + 3] = __fmaf_rn(xv, wv.w, p[r][4 * j4 + 3]);
+                    }
+                }
+        // transpose-reduce each row's CP partials over the warp: lane l ends
+        // with class l / (32 / CP)
+#pragma unroll
+        for (int r = 0; r < RU; ++r) {
+            int sh = 16;
+#pragma unroll
+            for (int half = CP / 2; half >= 1; half >>= 1, sh >>= 1) {
+                const bool up = (lane & sh) != 0;
+#pragma unroll
+                for (int j = 0; j < half; ++j) {
+                    const float send = up ? p[r][j] : p[r][half + j];
+                    const float keep = up ? p[r][half + j] : p[r][j];
+                    p[r][j] = __fadd_rn(keep, __shfl_xor_sync(0xffffffffu, send, sh));
+                }
+            }
+#pragma unroll
+            for (; sh >= 1; sh >>= 1) p[r][0] = __fadd_rn(p[r][0], __shfl_xor_sync(0xffffffffu, p[r][0], sh));
+        }
+        constexpr uint32_t PER = 32 / CP;
+        const uint32_t j = lane / PER;
+        if (lane % PER == 0 && j < c) {
+#pragma unroll
+            for (int r = 0; r < RU; ++r)
+                if (i0 + r < n) logits[uint64_t(i0 + r) * c + j] = p[r][0];
+        }
+    }
+}
+
+// Per-block partial weight gradients of the classes-wide layer:
+// part[b][m][k][j] = sum over block b's rows i of (m ? h1 : a2)[i, k] grad[i, j]
+// (g2 = a2^T grad, g2s = h1^T grad).  Warps 0-3 take a2, warps 4-7 h1; the
+// four warps of a product are combined in warp order.
+template <int CP>
+__global__ void __launch_bounds__(256) sage_wgrad_kernel(const float* __restrict__ a2, const float* __restrict__ h1,
+                                                         const float* __restrict__ grad, uint32_t n, uint32_t h,
+                                                         uint32_t c, uint32_t rpb, float* __restrict__ part) {
+    constexpr int RU = 2;
+    __shared__ __align__(16) float red[2][128 * CP];
+    const uint32_t lane = threadIdx.x & 31, w = threadIdx.x >> 5, m = w >> 2, wm = w & 3;
+    const bool act = lane < h / 4;
+    const float* src = m ? h1 : a2;
+    float acc[4][CP];
+#pragma unroll
+    for (int q = 0; q < 4; ++q)
+#pragma unroll
+        for (int j = 0; j < CP; ++j) acc[q][j] = 0.0f;
+    const uint32_t r0 = blockIdx.x * rpb, r1 = min(n, r0 + rpb);
+    if (act) {
+        for (uint32_t i = r0 + wm * RU; i < r1; i += 4 * RU) {
+            float4 x[RU];
+            float g[RU][CP];
+#pragma unroll
+            for (int r = 0; r < RU; ++r) {
+                const bool ok = i + r < r1;
+                x[r] = ok ? __ldg(reinterpret_cast<const float4*>(src + uint64_t(i + r) * h) + lane)
+                          : make_float4(0.f, 0.f, 0.f, 0.f);
+                load_grad_row<CP>(grad, ok ? i + r : i, c, g[r]);
+            }
+#pragma unroll
+            for (int r = 0; r < RU; ++r) {
+                const float xs[4] = {x[r].x, x[r].y, x[r].z, x[r].w};  // zero past r1
+#pragma unroll
+                for (int q = 0; q < 4; ++q)
+#pragma unroll
+                    for (int j = 0; j < CP; ++j) acc[q][j] = __fmaf_rn(xs[q], g[r][j], acc[q][j]);
+            }
+        }
+    }
+    for (uint32_t step = 0; step < 4; ++step) {
+        if (wm == step && act) {
+#pragma unroll
+            for (int q = 0; q < 4; ++q)
+#pragma unroll
+                for (int j = 0; j < CP; ++j) {
+                    float* r = &red[m][(4 * lane + q) * CP + j];
+                    *r = step == 0 ? acc[q][j] : __fadd_rn(*r, acc[q][j]);
+                }
+        }
+        __syncthreads();
+    }
+    float* out = part + uint64_t(blockIdx.x) * 2 * h * CP;
+    for (uint32_t t = threadIdx.x; t < 2 * h * CP; t += blockDim.x) out[t] = red[t / (h * CP)][t % (h * CP)];
+}
+
+// g2 / g2s (h x c row-major) = sum of the block partials in block order
+template <int CP>
+__global__ void sage_wgrad_finish_kernel(const float* __restrict__ part, uint32_t nblk, uint32_t h, uint32_t c,
+                                         float* __restrict__ g2, float* __restrict__ g2s) {
+    const uint32_t t = blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= 2 * h * CP) return;
+    const uint32_t m = t / (h * CP), kj = t % (h * CP), k = kj / CP, j = kj % CP;
+    if (j >= c) return;
+    float v = 0.0f;
+    for (uint32_t b = 0; b < nblk; ++b) v = __fadd_rn(v, part[uint64_t(b) * 2 * h * CP + t]);
+    (m ? g2s : g2)[k * c + j] = v;
+}
+
+// out[i, k] = grad[i, :] . W[k, :]  (grad W^T, W row-major h x c); with
+// U != null: out[i, k] = relu_backward(U[i, k] + grad[i, :] . W[k, :], act[i, k])
+// -- SAGE's ds2 = grad W2^T, and dz1 from dh1 = A^T ds2 + grad W2s^T
+// (the second product never reaches memory).
+template <int CP>
+__global__ void __launch_bounds__(256) sage_grad_wt_kernel(const float* __restrict__ grad, const float* __restrict__ w,
+                                                           uint32_t n, uint32_t h, uint32_t c,
+                                                           const float* __restrict__ u, const float* __restrict__ act,
+                                                           float* __restrict__ out) {
+    constexpr int RU = 4, J4 = CP / 4;
+    __shared__ float4 sw[4 * J4 * 32];
+    stage_w<CP>(w, h, c, sw);
+    __syncthreads();
+    const uint32_t lane = threadIdx.x & 31;
+    if (lane >= h / 4) return;
+    const uint32_t nw = (gridDim.x * blockDim.x) >> 5;
+    for (uint32_t i0 = ((blockIdx.x * blockDim.x + threadIdx.x) >> 5) * RU; i0 < n; i0 += nw * RU) {
+        float g[RU][CP];
+        float4 uv[RU], hv[RU];
+#pragma unroll
+        for (int r = 0; r < RU; ++r) {
+            const uint32_t i = i0 + r < n ? i0 + r : i0;
+            load_grad_row<CP>(grad, i, c, g[r]);
+            if (u) {
+                uv[r] = __ldg(reinterpret_cast<const float4*>(u + uint64_t(i) * h) + lane);
+                hv[r] = __ldg(reinterpret_cast<const float4*>(act + uint64_t(i) * h) + lane);
+            }
+        }
+        float d[RU][4];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+#pragma unroll
+            for (int j4 = 0; j4 < J4; ++j4) {
+                const float4 wv = sw[(q * J4 + j4) * 32 + lane];
+#pragma unroll
+                for (int r = 0; r < RU; ++r) {
+                    float t = j4 == 0 ? __fmul_rn(g[r][0], wv.x) : __fmaf_rn(g[r][4 * j4], wv.x, d[r][q]);
+                    t = __fmaf_rn(g[r][4 * j4 + 1], wv.y, t);
+                    t = __fmaf_rn(g[r][4 * j4 + 2], wv.z, t);
+                    d[r][q] = __fmaf_rn(g[r][4 * j4 + 3], wv.w, t);
+                }
+            }
+        }
+#pragma unroll
+        for (int r = 0; r < RU; ++r) {
+            if (i0 + r >= n) break;
+            float4* o = reinterpret_cast<float4*>(out + uint64_t(i0 + r) * h) + lane;
+            if (u) {
+                *o = make_float4(relu_bwd1(__fadd_rn(uv[r].x, d[r][0]), hv[r].x),
+                                 relu_bwd1(__fadd_rn(uv[r].y, d[r][1]), hv[r].y),
+                                 relu_bwd1(__fadd_rn(uv[r].z, d[r][2]), hv[r].z),
+                                 relu_bwd1(__fadd_rn(uv[r].w, d[r][3]), hv[r].w));
+            } else {
+                *o = make_float4(d[r][0], d[r][1], d[r][2], d[r][3]);
+            }
+        }
+    }
+}
+
 // GIN: deps += sum(a .* b) in double (dot_all), fixed order (one block)
 __global__ void __launch_bounds__(1024) dot_all_kernel(const float* __restrict__ a, const float* __restrict__ b,
                                                        uint64_t n, double* __restrict__ acc) {
@@ -304,6 +544,10 @@ struct sgnn_gnn_s {
           *t2 = nullptr, *grad = nullptr, *d_h = nullptr, *d_h2 = nullptr, *d_c = nullptr;
     double* row_loss = nullptr;
     uint32_t* row_ok = nullptr;
+    // SAGE classes-wide products in the library's own passes (sage_*_kernel)
+    bool skinny = false;
+    uint32_t wg_rpb = 0, wg_blocks = 0;
+    float* wg_part = nullptr;  // [wg_blocks][2][hid][16]
     double* stats = nullptr;  // [2 * max_epochs]
     uint32_t* epoch = nullptr;
     uint32_t max_epochs = 0;
@@ -369,6 +613,14 @@ sgnn_status fwd_spmm(sgnn_gnn_s* g, const float* x, uint32_t k, float* out, int 
         kernel<<<grid_for(n), 256, 0, s>>>(__VA_ARGS__);                       \
         SGNN_LAUNCH_CHECK();                                                   \
     } while (0)
+// SAGE classes-wide kernels, instantiated for 4, 8 or 16 padded classes
+#define SAGE_CP(kernel, grid, block, args)                                     \
+    do {                                                                       \
+        if (g->cls <= 4) kernel<4><<<(grid), (block), 0, s>>> args;           \
+        else if (g->cls <= 8) kernel<8><<<(grid), (block), 0, s>>> args;      \
+        else kernel<16><<<(grid), (block), 0, s>>> args;                      \
+        SGNN_LAUNCH_CHECK();                                                   \
+    } while (0)
 // float4 element-wise kernels (ew_loop): a quarter of the threads
 #define LAUNCH_EW4(kernel, n, ...)                                             \
     do {                                                                       \
@@ -394,9 +646,14 @@ sgnn_status epoch(sgnn_gnn_s* g, float lr, cudaStream_t s) {
         SGNN_TRY(mm(g, g->x, g->w1s, g->t1, n, in, hid));
         LAUNCH_EW4(add_relu_kernel, nh, g->z1, g->t1, nh, g->h1);          // h1 = relu(a1 W1 + X W1s)
         SGNN_TRY(fwd_spmm(g, g->h1, g->hid, g->a2, red, s));               // a2 = A h1
-        SGNN_TRY(mm(g, g->a2, g->w2, g->logits, n, hid, cls));
-        SGNN_TRY(mm(g, g->h1, g->w2s, g->t2, n, hid, cls));
-        LAUNCH_EW4(add_kernel, nc, g->logits, g->t2, nc);
+        if (g->skinny) {
+            SAGE_CP(sage_logits_kernel, grid_for(uint64_t(g->n) * 32), 256,
+                    (g->a2, g->h1, g->w2, g->w2s, g->n, g->hid, g->cls, g->logits));
+        } else {
+            SGNN_TRY(mm(g, g->a2, g->w2, g->logits, n, hid, cls));
+            SGNN_TRY(mm(g, g->h1, g->w2s, g->t2, n, hid, cls));
+            LAUNCH_EW4(add_kernel, nc, g->logits, g->t2, nc);
+        }
     } else {  // GIN
         SGNN_TRY(fwd_spmm(g, g->x, g->in, g->t1, SGNN_REDUCE_SUM, s));
         LAUNCH_EW(scaled_add_kernel, ni, g->eps, g->x, g->t1, ni, g->a1);  // a1 = (1+eps) X + A X
@@ -436,13 +693,25 @@ sgnn_status epoch(sgnn_gnn_s* g, float lr, cudaStream_t s) {
         SGNN_TRY(cache_spmm_with_operand(g->cache, &at, g->d_h2, g->hid, g->d_h, s));                 // dz1
         SGNN_TRY(mm_tn(g, g->x, g->d_h, g->g1, n, in, hid));
     } else if (g->kind == kSageSum || g->kind == kSageMean) {
-        SGNN_TRY(mm_tn(g, g->a2, g->grad, g->g2, n, hid, cls));
-        SGNN_TRY(mm_tn(g, g->h1, g->grad, g->g2s, n, hid, cls));
-        SGNN_TRY(mm_nt(g, g->grad, g->w2, g->d_h, n, cls, hid));                                      // ds2
-        SGNN_TRY(cache_spmm_backward(g->cache, g->d_h, g->n, g->hid, g->d_h2, red, s));              // dh1
-        SGNN_TRY(mm_nt(g, g->grad, g->w2s, g->d_h, n, cls, hid));
-        // dz1 into z1 (free after the forward's add_relu)
-        LAUNCH_EW4(add_relu_backward_kernel, nh, g->d_h2, g->d_h, g->h1, nh, g->z1);
+        if (g->skinny) {
+            SAGE_CP(sage_wgrad_kernel, g->wg_blocks, 256, (g->a2, g->h1, g->grad, g->n, g->hid, g->cls, g->wg_rpb, g->wg_part));
+            SAGE_CP(sage_wgrad_finish_kernel, unsigned((2 * g->hid * 16 + 127) / 128), 128,
+                    (g->wg_part, g->wg_blocks, g->hid, g->cls, g->g2, g->g2s));
+            SAGE_CP(sage_grad_wt_kernel, grid_for(uint64_t(g->n) * 32), 256,
+                    (g->grad, g->w2, g->n, g->hid, g->cls, nullptr, nullptr, g->d_h));                  // ds2
+            SGNN_TRY(cache_spmm_backward(g->cache, g->d_h, g->n, g->hid, g->d_h2, red, s));          // dh1 (A^T part)
+            // dz1 = relu_backward(dh1 + grad W2s^T, h1) into z1 (free after the forward)
+            SAGE_CP(sage_grad_wt_kernel, grid_for(uint64_t(g->n) * 32), 256,
+                    (g->grad, g->w2s, g->n, g->hid, g->cls, g->d_h2, g->h1, g->z1));
+        } else {
+            SGNN_TRY(mm_tn(g, g->a2, g->grad, g->g2, n, hid, cls));
+            SGNN_TRY(mm_tn(g, g->h1, g->grad, g->g2s, n, hid, cls));
+            SGNN_TRY(mm_nt(g, g->grad, g->w2, g->d_h, n, cls, hid));                                  // ds2
+            SGNN_TRY(cache_spmm_backward(g->cache, g->d_h, g->n, g->hid, g->d_h2, red, s));          // dh1
+            SGNN_TRY(mm_nt(g, g->grad, g->w2s, g->d_h, n, cls, hid));
+            // dz1 into z1 (free after the forward's add_relu)
+            LAUNCH_EW4(add_relu_backward_kernel, nh, g->d_h2, g->d_h, g->h1, nh, g->z1);
+        }
         SGNN_TRY(mm_tn(g, g->a1, g->z1, g->g1, n, in, hid));
         SGNN_TRY(mm_tn(g, g->x, g->z1, g->g1s, n, in, hid));
     } else {  // GIN
@@ -527,6 +796,14 @@ sgnn_status gnn_create(const sgnn_csr* a, int kind, uint32_t in, uint32_t hidden
         (st = dalloc(g, &g->row_ok, n)) != SGNN_OK || (st = dalloc(g, &g->stats, 2ull * g->max_epochs)) != SGNN_OK ||
         (st = dalloc(g, &g->epoch, 1)) != SGNN_OK)
         return bail(st);
+    g->skinny = (kind == kSageSum || kind == kSageMean) && hidden % 4 == 0 && hidden <= 128 && classes <= 16 &&
+                !std::getenv("SGNN_GNN_CUBLAS_SKINNY");  // A/B switch
+    if (g->skinny) {
+        g->wg_blocks = std::min<uint32_t>(592, std::max<uint32_t>(1, g->n));  // 4 per SM
+        g->wg_rpb = (g->n + g->wg_blocks - 1) / g->wg_blocks;
+        g->wg_blocks = (g->n + g->wg_rpb - 1) / g->wg_rpb;
+        if ((st = dalloc(g, &g->wg_part, uint64_t(g->wg_blocks) * 2 * hidden * 16)) != SGNN_OK) return bail(st);
+    }
     if (cudaMemcpyAsync(g->x, x, sizeof(float) * n * in, cudaMemcpyDeviceToDevice, s) != cudaSuccess ||
         cudaMemcpyAsync(g->labels, labels, sizeof(uint32_t) * n, cudaMemcpyDeviceToDevice, s) != cudaSuccess ||
         cudaMemcpyAsync(g->mask, mask, n, cudaMemcpyDeviceToDevice, s) != cudaSuccess ||

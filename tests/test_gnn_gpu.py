@@ -162,3 +162,30 @@ def test_native_engine_errors(cuda):
                                     np.array([1.0], np.float32), 2)
     with pytest.raises(_lib.ShapeError):  # build_cache: adjacency must be square
         gnn.train_native(m, rect, x[:1], lab[:1], mask[:1], epochs=2)
+
+
+@pytest.mark.parametrize("hidden,classes", [(128, 16), (64, 10), (32, 3)])
+def test_native_sage_classes_wide_kernels(cuda, monkeypatch, hidden, classes):
+    """SAGE's classes-wide products (logits, W2/W2s gradients, grad W2^T and
+    the fused grad W2s^T + relu_backward: sage_*_kernel in csrc/gnn.cu) vs
+    the same engine on cuBLAS (SGNN_GNN_CUBLAS_SKINNY): losses and weights
+    agree to fp32 reassociation, on a symmetric graph with hub and empty rows."""
+    import torch
+
+    from paper_2403_14853_b200 import gnn, graphs, ops
+    rp, ci = graphs.rmat(11, 2048 * 8, seed=5, symmetrize=True)
+    n = len(rp) - 1
+    a = ops.CsrMatrix.from_numpy(rp, ci, np.ones(len(ci), np.float32), n)
+    rng = np.random.default_rng(3)
+    x = torch.from_numpy(rng.standard_normal((n, 48)).astype(np.float32)).cuda()
+    lab = torch.from_numpy(rng.integers(0, classes, n)).cuda()
+    mask = torch.from_numpy((rng.random(n) < 0.7).astype(np.uint8)).cuda()
+    runs = []
+    for cublas in (False, True):
+        if cublas:
+            monkeypatch.setenv("SGNN_GNN_CUBLAS_SKINNY", "1")
+        m = gnn.init_model("sage-mean", 48, hidden, classes, seed=2)
+        out = gnn.train_native(m, a, x, lab, mask, epochs=8, lr=0.05)
+        runs.append(([s.loss for s in out.stats], gnn.flat_weights(m)))
+    np.testing.assert_allclose(runs[0][0], runs[1][0], rtol=1e-5)
+    np.testing.assert_allclose(runs[0][1], runs[1][1], rtol=1e-4, atol=1e-6)
