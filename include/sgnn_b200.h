@@ -316,6 +316,38 @@ sgnn_status sgnn_gnn_counters(sgnn_gnn g, uint64_t* transpose_builds, uint64_t* 
                               uint64_t* cache_hits, int* symmetric);
 sgnn_status sgnn_gnn_destroy(sgnn_gnn g);
 
+/* ------------------------------------------------------ SAGE layer glue
+ * The element-wise and classes-wide steps of a SAGE layer pair as device
+ * passes, for hosts that sequence the layers themselves (the row-partitioned
+ * trainer calls them on each rank's rows; the engine above uses the same
+ * kernels).  Forward gnn.hpp:236-244, softmax_xent + masked_accuracy
+ * :318-370, backward :283-292.  Device arrays, row-major, 16-byte aligned;
+ * the classes-wide products need hidden % 4 == 0, hidden <= 128 and
+ * 1 <= classes <= 16 (SGNN_ERR_SHAPE otherwise).  Stream-asynchronous. */
+/* h = relu(a + b) over n elements (z1 = a1 W1 + X W1s, then relu) */
+sgnn_status sgnn_add_relu_f32(const float* a, const float* b, uint64_t n, float* h, sgnn_stream stream);
+/* logits[i, :] = [a2 | h1][i, :] . [w2; w2s]  (a2, h1: n x hidden; w2, w2s:
+ * hidden x classes; one fp32 accumulation over the 2*hidden inputs) */
+sgnn_status sgnn_sage_logits_f32(const float* a2, const float* h1, const float* w2, const float* w2s,
+                                 uint32_t n, uint32_t hidden, uint32_t classes, float* logits,
+                                 sgnn_stream stream);
+/* softmax_xent + masked_accuracy over n rows: grad[i, :] = (softmax - onehot)
+ * * inv_count on masked rows, 0 elsewhere; *loss_sum (double) = sum of the
+ * masked rows' cross-entropy, *correct = masked rows whose argmax (first
+ * index on ties) is the label.  Labels are not range-checked here. */
+sgnn_status sgnn_softmax_xent_f32(const float* logits, uint32_t n, uint32_t classes, const uint32_t* labels,
+                                  const uint8_t* mask, double inv_count, float* grad, double* loss_sum,
+                                  uint32_t* correct, sgnn_stream stream);
+/* g2 = a2^T grad, g2s = h1^T grad  (hidden x classes; block partials added
+ * in a fixed order: deterministic for given n) */
+sgnn_status sgnn_sage_wgrad_f32(const float* a2, const float* h1, const float* grad, uint32_t n,
+                                uint32_t hidden, uint32_t classes, float* g2, float* g2s, sgnn_stream stream);
+/* out = grad w^T (u == act == NULL), or out = relu_backward(u + grad w^T, act):
+ * ds2 = grad W2^T, and dz1 from dh1 = A^T ds2 + grad W2s^T */
+sgnn_status sgnn_sage_grad_wt_f32(const float* grad, const float* w, uint32_t n, uint32_t hidden,
+                                  uint32_t classes, const float* u, const float* act, float* out,
+                                  sgnn_stream stream);
+
 #ifdef __cplusplus
 } /* extern "C" */
 #endif

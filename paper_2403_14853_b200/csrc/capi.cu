@@ -422,4 +422,36 @@ sgnn_status sgnn_gnn_destroy(sgnn_gnn g) {
     return SGNN_OK;
 }
 
+// ---------------------------------------------------------- SAGE glue
+sgnn_status sgnn_add_relu_f32(const float* a, const float* b, uint64_t n, float* h, sgnn_stream stream) {
+    if (n && (!a || !b || !h)) return fail(SGNN_ERR_CONFIG, "add_relu: null array");
+    return glue_add_relu(a, b, n, h, cs(stream));
+}
+
+sgnn_status sgnn_sage_logits_f32(const float* a2, const float* h1, const float* w2, const float* w2s, uint32_t n,
+                                 uint32_t hidden, uint32_t classes, float* logits, sgnn_stream stream) {
+    if (n && (!a2 || !h1 || !w2 || !w2s || !logits)) return fail(SGNN_ERR_CONFIG, "sage_logits: null array");
+    return glue_sage_logits(a2, h1, w2, w2s, n, hidden, classes, logits, cs(stream));
+}
+
+sgnn_status sgnn_softmax_xent_f32(const float* logits, uint32_t n, uint32_t classes, const uint32_t* labels,
+                                  const uint8_t* mask, double inv_count, float* grad, double* loss_sum,
+                                  uint32_t* correct, sgnn_stream stream) {
+    if (!loss_sum || !correct || (n && (!logits || !labels || !mask || !grad)))
+        return fail(SGNN_ERR_CONFIG, "softmax_xent: null array");
+    return glue_softmax_xent(logits, n, classes, labels, mask, inv_count, grad, loss_sum, correct, cs(stream));
+}
+
+sgnn_status sgnn_sage_wgrad_f32(const float* a2, const float* h1, const float* grad, uint32_t n, uint32_t hidden,
+                                uint32_t classes, float* g2, float* g2s, sgnn_stream stream) {
+    if (!g2 || !g2s || (n && (!a2 || !h1 || !grad))) return fail(SGNN_ERR_CONFIG, "sage_wgrad: null array");
+    return glue_sage_wgrad(a2, h1, grad, n, hidden, classes, g2, g2s, cs(stream));
+}
+
+sgnn_status sgnn_sage_grad_wt_f32(const float* grad, const float* w, uint32_t n, uint32_t hidden, uint32_t classes,
+                                  const float* u, const float* act, float* out, sgnn_stream stream) {
+    if (n && (!grad || !w || !out)) return fail(SGNN_ERR_CONFIG, "sage_grad_wt: null array");
+    return glue_sage_grad_wt(grad, w, n, hidden, classes, u, act, out, cs(stream));
+}
+
 }  // extern "C"

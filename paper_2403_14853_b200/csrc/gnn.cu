@@ -245,6 +245,22 @@ __global__ void __launch_bounds__(1024) epoch_stats_kernel(const double* __restr
     }
 }
 
+// Masked loss sum and correct count over the per-block sums, in block order
+// (the ABI's softmax_xent; the engine's epoch_stats_kernel does the same
+// and divides).
+__global__ void softmax_finish_kernel(const double* __restrict__ blk_loss, const uint32_t* __restrict__ blk_ok,
+                                      uint32_t nblk, double* __restrict__ loss_sum, uint32_t* __restrict__ correct) {
+    if (threadIdx.x != 0) return;
+    double l = 0.0;
+    uint32_t k = 0;
+    for (uint32_t b = 0; b < nblk; ++b) {
+        l += blk_loss[b];
+        k += blk_ok[b];
+    }
+    *loss_sum = l;
+    *correct = k;
+}
+
 // ---- SAGE's classes-wide products (hidden h <= 128, h % 4 == 0, classes
 // c <= CP): memory-bound passes of their own instead of cuBLAS calls that
 // run far below HBM speed at this shape.  A warp owns a row; lane l holds
@@ -614,10 +630,10 @@ sgnn_status fwd_spmm(sgnn_gnn_s* g, const float* x, uint32_t k, float* out, int 
         SGNN_LAUNCH_CHECK();                                                   \
     } while (0)
 // SAGE classes-wide kernels, instantiated for 4, 8 or 16 padded classes
-#define SAGE_CP(kernel, grid, block, args)                                     \
+#define SAGE_CP(kernel, cls, grid, block, args)                                \
     do {                                                                       \
-        if (g->cls <= 4) kernel<4><<<(grid), (block), 0, s>>> args;           \
-        else if (g->cls <= 8) kernel<8><<<(grid), (block), 0, s>>> args;      \
+        if ((cls) <= 4) kernel<4><<<(grid), (block), 0, s>>> args;            \
+        else if ((cls) <= 8) kernel<8><<<(grid), (block), 0, s>>> args;       \
         else kernel<16><<<(grid), (block), 0, s>>> args;                      \
         SGNN_LAUNCH_CHECK();                                                   \
     } while (0)
@@ -647,7 +663,7 @@ sgnn_status epoch(sgnn_gnn_s* g, float lr, cudaStream_t s) {
         LAUNCH_EW4(add_relu_kernel, nh, g->z1, g->t1, nh, g->h1);          // h1 = relu(a1 W1 + X W1s)
         SGNN_TRY(fwd_spmm(g, g->h1, g->hid, g->a2, red, s));               // a2 = A h1
         if (g->skinny) {
-            SAGE_CP(sage_logits_kernel, grid_for(uint64_t(g->n) * 32), 256,
+            SAGE_CP(sage_logits_kernel, g->cls, grid_for(uint64_t(g->n) * 32), 256,
                     (g->a2, g->h1, g->w2, g->w2s, g->n, g->hid, g->cls, g->logits));
         } else {
             SGNN_TRY(mm(g, g->a2, g->w2, g->logits, n, hid, cls));
@@ -694,14 +710,14 @@ sgnn_status epoch(sgnn_gnn_s* g, float lr, cudaStream_t s) {
         SGNN_TRY(mm_tn(g, g->x, g->d_h, g->g1, n, in, hid));
     } else if (g->kind == kSageSum || g->kind == kSageMean) {
         if (g->skinny) {
-            SAGE_CP(sage_wgrad_kernel, g->wg_blocks, 256, (g->a2, g->h1, g->grad, g->n, g->hid, g->cls, g->wg_rpb, g->wg_part));
-            SAGE_CP(sage_wgrad_finish_kernel, unsigned((2 * g->hid * 16 + 127) / 128), 128,
+            SAGE_CP(sage_wgrad_kernel, g->cls, g->wg_blocks, 256, (g->a2, g->h1, g->grad, g->n, g->hid, g->cls, g->wg_rpb, g->wg_part));
+            SAGE_CP(sage_wgrad_finish_kernel, g->cls, unsigned((2 * g->hid * 16 + 127) / 128), 128,
                     (g->wg_part, g->wg_blocks, g->hid, g->cls, g->g2, g->g2s));
-            SAGE_CP(sage_grad_wt_kernel, grid_for(uint64_t(g->n) * 32), 256,
+            SAGE_CP(sage_grad_wt_kernel, g->cls, grid_for(uint64_t(g->n) * 32), 256,
                     (g->grad, g->w2, g->n, g->hid, g->cls, nullptr, nullptr, g->d_h));                  // ds2
             SGNN_TRY(cache_spmm_backward(g->cache, g->d_h, g->n, g->hid, g->d_h2, red, s));          // dh1 (A^T part)
             // dz1 = relu_backward(dh1 + grad W2s^T, h1) into z1 (free after the forward)
-            SAGE_CP(sage_grad_wt_kernel, grid_for(uint64_t(g->n) * 32), 256,
+            SAGE_CP(sage_grad_wt_kernel, g->cls, grid_for(uint64_t(g->n) * 32), 256,
                     (g->grad, g->w2s, g->n, g->hid, g->cls, g->d_h2, g->h1, g->z1));
         } else {
             SGNN_TRY(mm_tn(g, g->a2, g->grad, g->g2, n, hid, cls));
@@ -961,5 +977,88 @@ sgnn_status gnn_counters(sgnn_gnn_s* g, uint64_t* tb, uint64_t* nb, uint64_t* hi
 }
 
 void gnn_destroy(sgnn_gnn_s* g) { delete g; }
+
+// ------------------------------------------------------------ SAGE glue (ABI)
+namespace {
+bool sage_shape_ok(uint32_t h, uint32_t c) { return h > 0 && h % 4 == 0 && h <= 128 && c > 0 && c <= 16; }
+sgnn_status sage_shape(uint32_t h, uint32_t c, const char* what) {
+    if (!sage_shape_ok(h, c))
+        return fail(SGNN_ERR_SHAPE, std::string(what) + ": needs hidden % 4 == 0, hidden <= 128, 1 <= classes <= 16 (got " +
+                                        std::to_string(h) + ", " + std::to_string(c) + ")");
+    return SGNN_OK;
+}
+}  // namespace
+
+sgnn_status glue_add_relu(const float* a, const float* b, uint64_t n, float* h, cudaStream_t s) {
+    if (n == 0) return SGNN_OK;
+    LAUNCH_EW4(add_relu_kernel, n, a, b, n, h);
+    return SGNN_OK;
+}
+
+sgnn_status glue_sage_logits(const float* a2, const float* h1, const float* w2, const float* w2s, uint32_t n,
+                             uint32_t h, uint32_t c, float* logits, cudaStream_t s) {
+    SGNN_TRY(sage_shape(h, c, "sage_logits"));
+    if (n == 0) return SGNN_OK;
+    SAGE_CP(sage_logits_kernel, c, grid_for(uint64_t(n) * 32), 256, (a2, h1, w2, w2s, n, h, c, logits));
+    return SGNN_OK;
+}
+
+sgnn_status glue_softmax_xent(const float* logits, uint32_t n, uint32_t c, const uint32_t* labels,
+                              const uint8_t* mask, double inv_count, float* grad, double* loss_sum,
+                              uint32_t* correct, cudaStream_t s) {
+    if (c == 0) return fail(SGNN_ERR_SHAPE, "softmax_xent: classes must be positive");
+    uint32_t rpb = 1, nblk = 1;
+    softmax_shape(n, &rpb, &nblk);
+    void* blk = nullptr;
+    SGNN_TRY(scratch_alloc(&blk, size_t(nblk) * (sizeof(double) + sizeof(uint32_t)), s));
+    double* bl = static_cast<double*>(blk);
+    uint32_t* bo = reinterpret_cast<uint32_t*>(bl + nblk);
+    if (n) {
+        if (c <= 4)
+            softmax_xent_kernel<4><<<nblk, kSoftmaxThreads, 0, s>>>(logits, n, c, labels, mask, inv_count, rpb, grad, bl, bo);
+        else if (c <= 8)
+            softmax_xent_kernel<8><<<nblk, kSoftmaxThreads, 0, s>>>(logits, n, c, labels, mask, inv_count, rpb, grad, bl, bo);
+        else if (c <= 16)
+            softmax_xent_kernel<16><<<nblk, kSoftmaxThreads, 0, s>>>(logits, n, c, labels, mask, inv_count, rpb, grad, bl, bo);
+        else
+            softmax_xent_kernel<32><<<nblk, kSoftmaxThreads, 0, s>>>(logits, n, c, labels, mask, inv_count, rpb, grad, bl, bo);
+    }
+    softmax_finish_kernel<<<1, 32, 0, s>>>(bl, bo, n ? nblk : 0, loss_sum, correct);
+    const cudaError_t e = cudaGetLastError();
+    scratch_free(blk, s);
+    if (e != cudaSuccess) return fail(SGNN_ERR_CUDA, std::string("softmax_xent: ") + cudaGetErrorString(e));
+    return SGNN_OK;
+}
+
+sgnn_status sage_wgrad_launch(const float* a2, const float* h1, const float* grad, uint32_t n, uint32_t h,
+                              uint32_t c, uint32_t rpb, uint32_t nblk, float* part, float* g2, float* g2s,
+                              cudaStream_t s) {
+    SAGE_CP(sage_wgrad_kernel, c, nblk, 256, (a2, h1, grad, n, h, c, rpb, part));
+    SAGE_CP(sage_wgrad_finish_kernel, c, unsigned((2 * h * 16 + 127) / 128), 128, (part, nblk, h, c, g2, g2s));
+    return SGNN_OK;
+}
+
+sgnn_status glue_sage_wgrad(const float* a2, const float* h1, const float* grad, uint32_t n, uint32_t h, uint32_t c,
+                            float* g2, float* g2s, cudaStream_t s) {
+    SGNN_TRY(sage_shape(h, c, "sage_wgrad"));
+    const uint32_t want = std::min<uint32_t>(592, std::max<uint32_t>(1, n));
+    const uint32_t rpb = std::max<uint32_t>(1, (n + want - 1) / want);
+    const uint32_t nblk = std::max<uint32_t>(1, (n + rpb - 1) / rpb);
+    float* part = nullptr;
+    SGNN_TRY(scratch_alloc(reinterpret_cast<void**>(&part), sizeof(float) * nblk * 2 * h * 16, s));
+    const sgnn_status st = sage_wgrad_launch(a2, h1, grad, n, h, c, rpb, nblk, part, g2, g2s, s);
+    scratch_free(part, s);
+    return st;
+}
+
+sgnn_status glue_sage_grad_wt(const float* grad, const float* w, uint32_t n, uint32_t h, uint32_t c, const float* u,
+                              const float* act, float* out, cudaStream_t s) {
+    SGNN_TRY(sage_shape(h, c, "sage_grad_wt"));
+    if ((u == nullptr) != (act == nullptr)) return fail(SGNN_ERR_CONFIG, "sage_grad_wt: u and act go together");
+    if (n == 0) return SGNN_OK;
+    SAGE_CP(sage_grad_wt_kernel, c, grid_for(uint64_t(n) * 32), 256, (grad, w, n, h, c, u, act, out));
+    return SGNN_OK;
+}
+
 
 }  // namespace sgnn

@@ -68,5 +68,16 @@ sgnn_status gnn_train(sgnn_gnn_s* g, uint32_t epochs, float lr, int cuda_graph, 
                       double* seconds, cudaStream_t s);
 sgnn_status gnn_counters(sgnn_gnn_s* g, uint64_t* tb, uint64_t* nb, uint64_t* hits, int* sym);
 void gnn_destroy(sgnn_gnn_s* g);
+// SAGE layer glue (gnn.cu), see sgnn_b200.h
+sgnn_status glue_add_relu(const float* a, const float* b, uint64_t n, float* h, cudaStream_t s);
+sgnn_status glue_sage_logits(const float* a2, const float* h1, const float* w2, const float* w2s, uint32_t n,
+                             uint32_t h, uint32_t c, float* logits, cudaStream_t s);
+sgnn_status glue_softmax_xent(const float* logits, uint32_t n, uint32_t c, const uint32_t* labels,
+                              const uint8_t* mask, double inv_count, float* grad, double* loss_sum,
+                              uint32_t* correct, cudaStream_t s);
+sgnn_status glue_sage_wgrad(const float* a2, const float* h1, const float* grad, uint32_t n, uint32_t h, uint32_t c,
+                            float* g2, float* g2s, cudaStream_t s);
+sgnn_status glue_sage_grad_wt(const float* grad, const float* w, uint32_t n, uint32_t h, uint32_t c, const float* u,
+                              const float* act, float* out, cudaStream_t s);
 
 }  // namespace sgnn

@@ -48,7 +48,7 @@ std::vector<sgnn_plan_params> candidates(const sgnn_csr* a, uint32_t k, const De
     if (vec) {
         const LV all[] = {{4, 1, 8}, {4, 2, 8}, {8, 1, 8}, {8, 2, 4}, {8, 2, 8}, {8, 4, 4},
                           {16, 1, 8}, {16, 2, 4}, {16, 2, 8}, {16, 4, 2}, {16, 4, 4},
-                          {32, 1, 4}, {32, 1, 8}, {32, 2, 4}, {32, 2, 8}, {32, 4, 2},
+                          {32, 1, 4}, {32, 1, 8}, {32, 1, 16}, {32, 2, 4}, {32, 2, 8}, {32, 4, 2},
                           {32, 4, 4}, {32, 8, 2}};
         for (const LV& l : all) {
             const uint32_t width = 4 * l.lanes * l.vec;

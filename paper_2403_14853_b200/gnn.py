@@ -375,3 +375,84 @@ def train_native(model: GnnModel, a: ops.CsrMatrix, x: torch.Tensor, labels: tor
                                          "cache_hits": hits.value, "symmetric": bool(sym.value)})
     finally:
         L.sgnn_gnn_destroy(h)
+
+
+# ---------------------------------------------------------------- SAGE glue
+# The library's SAGE layer-glue passes (sgnn_add_relu_f32, sgnn_sage_*_f32,
+# sgnn_softmax_xent_f32; csrc/gnn.cu) over torch CUDA tensors, for trainers
+# that sequence the layers themselves (sage_dist.DistSage on each rank).
+
+def sage_glue_ok(hidden: int, classes: int) -> bool:
+    """Shapes the classes-wide glue kernels take (hidden % 4 == 0, <= 128;
+    1 <= classes <= 16)."""
+    return hidden > 0 and hidden % 4 == 0 and hidden <= 128 and 1 <= classes <= 16
+
+
+def _ptr(t):
+    return t.data_ptr() if t is not None else None
+
+
+def add_relu(a: torch.Tensor, b: torch.Tensor, out: torch.Tensor | None = None) -> torch.Tensor:
+    """relu(a + b) in one pass (SAGE's z1 = a1 W1 + X W1s, then relu)."""
+    from ._lib import check, lib
+    ops._dense(a, "add_relu a")
+    ops._dense(b, "add_relu b")
+    if a.shape != b.shape:
+        raise ops.ShapeError(f"add_relu: {tuple(a.shape)} vs {tuple(b.shape)}")
+    out = torch.empty_like(a) if out is None else out
+    check(lib().sgnn_add_relu_f32(a.data_ptr(), b.data_ptr(), a.numel(), out.data_ptr(), ops._stream()), "add_relu")
+    return out
+
+
+def sage_logits(a2, h1, w2, w2s, out=None) -> torch.Tensor:
+    """[a2 | h1] . [w2; w2s] (gnn.hpp:241-244)."""
+    from ._lib import check, lib
+    for t, nm in ((a2, "a2"), (h1, "h1"), (w2, "w2"), (w2s, "w2_self")):
+        ops._dense(t, f"sage_logits {nm}")
+    n, h = a2.shape
+    c = w2.shape[1]
+    if h1.shape != a2.shape or w2.shape != (h, c) or w2s.shape != (h, c):
+        raise ops.ShapeError("sage_logits: operand shapes disagree")
+    out = torch.empty(n, c, device=a2.device) if out is None else out
+    check(lib().sgnn_sage_logits_f32(a2.data_ptr(), h1.data_ptr(), w2.data_ptr(), w2s.data_ptr(), n, h, c,
+                                     out.data_ptr(), ops._stream()), "sage_logits")
+    return out
+
+
+def softmax_xent_device(logits, labels_u32, mask_u8, inv_count: float):
+    """softmax_xent + masked_accuracy on the device (gnn.hpp:318-370):
+    (grad, loss_sum double[1], correct int32[1]) -- sums, not means, so
+    ranks can all-reduce them."""
+    from ._lib import check, lib
+    ops._dense(logits, "softmax_xent logits")
+    n, c = logits.shape
+    grad = torch.empty_like(logits)
+    loss = torch.empty(1, dtype=torch.float64, device=logits.device)
+    correct = torch.empty(1, dtype=torch.int32, device=logits.device)
+    check(lib().sgnn_softmax_xent_f32(logits.data_ptr(), n, c, labels_u32.data_ptr(), mask_u8.data_ptr(),
+                                      float(inv_count), grad.data_ptr(), loss.data_ptr(), correct.data_ptr(),
+                                      ops._stream()), "softmax_xent")
+    return grad, loss, correct
+
+
+def sage_wgrad(a2, h1, grad):
+    """(a2^T grad, h1^T grad): the classes-wide layer's weight gradients."""
+    from ._lib import check, lib
+    n, h = a2.shape
+    c = grad.shape[1]
+    g2 = torch.empty(h, c, device=a2.device)
+    g2s = torch.empty(h, c, device=a2.device)
+    check(lib().sgnn_sage_wgrad_f32(a2.data_ptr(), h1.data_ptr(), grad.data_ptr(), n, h, c, g2.data_ptr(),
+                                    g2s.data_ptr(), ops._stream()), "sage_wgrad")
+    return g2, g2s
+
+
+def sage_grad_wt(grad, w, u=None, act=None, out=None):
+    """grad w^T, or relu_backward(u + grad w^T, act) (gnn.hpp:285-292)."""
+    from ._lib import check, lib
+    n, c = grad.shape
+    h = w.shape[0]
+    out = torch.empty(n, h, device=grad.device) if out is None else out
+    check(lib().sgnn_sage_grad_wt_f32(grad.data_ptr(), w.data_ptr(), n, h, c, _ptr(u), _ptr(act), out.data_ptr(),
+                                      ops._stream()), "sage_grad_wt")
+    return out

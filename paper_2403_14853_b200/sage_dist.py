@@ -18,7 +18,7 @@ from dataclasses import dataclass
 import numpy as np
 import torch
 
-from . import partition
+from . import gnn, partition
 
 
 def mean_operand_values(row_ptr, col_idx, values):
@@ -59,9 +59,12 @@ class DistSage:
             row_ptr, col_idx, values, self.part, rank, hidden, device, compute)
         self.bwd = partition.PartitionedSpmm(row_ptr, col_idx, bwd_vals, self.part, rank, hidden, device, compute)
         self.hidden, self.classes = hidden, classes
+        self.use_glue = True  # the library's SAGE glue passes on CUDA tensors (False: torch ops)
 
     def step(self, params: SageParams, x_local, labels_local, mask_local, lr, n_masked_total):
         """One training step; returns the global mean loss."""
+        if self.use_glue and x_local.is_cuda and gnn.sage_glue_ok(self.hidden, self.classes):
+            return self._step_glue(params, x_local, labels_local, mask_local, lr, n_masked_total)
         red = self.reduce
         ex = self.exchange
         # forward (gnn.hpp:236-244)
@@ -98,6 +101,36 @@ class DistSage:
         for p, g, n in zip((params.w1, params.w2, params.w1_self, params.w2_self), (g_w1, g_w2, g_w1s, g_w2s), sizes):
             p -= lr * flat[o:o + n].reshape(g.shape)
             o += n
+        return float(loss_sum[0]) / n_masked_total
+
+
+    def _step_glue(self, params: SageParams, x_local, labels_local, mask_local, lr, n_masked_total):
+        """The same step with the library's SAGE glue passes (csrc/gnn.cu:
+        add+relu, [a2|h1] logits, device softmax_xent, classes-wide weight
+        gradients, grad W2s^T fused into relu_backward) around the
+        partitioned SpMMs and the two big GEMMs per direction."""
+        red = self.reduce
+        ex = self.exchange
+        if getattr(self, "_lab_src", None) is not labels_local:
+            self._lab_src = labels_local
+            self._lab = labels_local.to(torch.int32).contiguous()
+            self._msk = mask_local.to(torch.uint8).contiguous()
+        a1 = self.fwd.forward(x_local, ex, red)
+        h1 = gnn.add_relu(a1 @ params.w1, x_local @ params.w1_self)
+        a2 = self.fwd2.forward(h1, ex, red)
+        logits = gnn.sage_logits(a2, h1, params.w2, params.w2_self)
+        grad, loss_sum, _ = gnn.softmax_xent_device(logits, self._lab, self._msk, 1.0 / n_masked_total)
+        g_w2, g_w2s = gnn.sage_wgrad(a2, h1, grad)
+        ds2 = gnn.sage_grad_wt(grad, params.w2)
+        dz1 = gnn.sage_grad_wt(grad, params.w2_self, u=self.bwd.forward(ds2, ex, "sum"), act=h1)
+        g_w1 = a1.T @ dz1
+        g_w1s = x_local.T @ dz1
+        flat = self.allreduce(torch.cat([g_w1.ravel(), g_w2.ravel(), g_w1s.ravel(), g_w2s.ravel()]))
+        loss_sum = self.allreduce(loss_sum)
+        o = 0
+        for p, g in zip((params.w1, params.w2, params.w1_self, params.w2_self), (g_w1, g_w2, g_w1s, g_w2s)):
+            p -= lr * flat[o:o + g.numel()].reshape(g.shape)
+            o += g.numel()
         return float(loss_sum[0]) / n_masked_total
 
 

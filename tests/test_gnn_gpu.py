@@ -189,3 +189,38 @@ def test_native_sage_classes_wide_kernels(cuda, monkeypatch, hidden, classes):
         runs.append(([s.loss for s in out.stats], gnn.flat_weights(m)))
     np.testing.assert_allclose(runs[0][0], runs[1][0], rtol=1e-5)
     np.testing.assert_allclose(runs[0][1], runs[1][1], rtol=1e-4, atol=1e-6)
+
+
+@pytest.mark.parametrize("hidden,classes", [(128, 16), (64, 10)])
+def test_dist_sage_glue_step_matches_torch_step(cuda, hidden, classes):
+    """The row-partitioned SAGE-mean step (sage_dist.DistSage, one rank) with
+    the library's glue passes vs the same step in torch ops: losses and
+    weights agree to fp32 reassociation."""
+    import torch
+
+    from paper_2403_14853_b200 import graphs, sage_dist
+
+    class Local:  # one rank: the gathered operand is the local block
+        def all_gather(self, block):
+            return block.contiguous()
+
+    rp, ci = graphs.rmat(11, 2048 * 8, seed=9, symmetrize=True, self_loops=True)
+    n = len(rp) - 1
+    v = np.ones(len(ci), np.float32)
+    rng = np.random.default_rng(4)
+    f = 32
+    x = torch.from_numpy(rng.standard_normal((n, f)).astype(np.float32)).cuda()
+    lab = torch.from_numpy(rng.integers(0, classes, n)).cuda()
+    mask = torch.from_numpy((rng.random(n) < 0.8).astype(np.uint8)).cuda()
+    w0 = [torch.from_numpy((0.1 * rng.standard_normal(s)).astype(np.float32)).cuda()
+          for s in ((f, hidden), (hidden, classes), (f, hidden), (hidden, classes))]
+    runs = []
+    for glue in (True, False):
+        ds = sage_dist.DistSage(rp, ci, v, 1, 0, f, hidden, classes, "mean", device="cuda", exchange=Local(),
+                                allreduce=lambda t: t)
+        ds.use_glue = glue
+        params = sage_dist.SageParams(*[w.clone() for w in w0])
+        losses = [ds.step(params, x, lab, mask, 0.05, int(mask.sum())) for _ in range(5)]
+        runs.append((losses, torch.cat([p.ravel() for p in (params.w1, params.w2, params.w1_self, params.w2_self)])))
+    np.testing.assert_allclose(runs[0][0], runs[1][0], rtol=1e-5)
+    np.testing.assert_allclose(runs[0][1].cpu().numpy(), runs[1][1].cpu().numpy(), rtol=1e-4, atol=1e-6)
