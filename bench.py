@@ -681,7 +681,10 @@ def run_cfg5(args):
            ("SpMM reads peer feature blocks in place (CUDA IPC over NVLink)" if ws > 1 and args.exchange == "peer"
             else "all-gather of feature blocks"), "partition_bounds": [int(b) for b in ds.part.bounds]}
     line = _base_line(args, ws, flops / ms / 1e6, ms, cfg, {
-        "epoch_ms": round(ms, 3), "loss": loss, "scaling": "strong", "gpu_launches": steps * 12})
+        # per step: 2 forward SpMMs (worker, 2 fixups, mean divide), 1 backward
+        # SpMM (worker, 2 fixups), 8 glue passes (add_relu, logits, xent + sum,
+        # wgrad + sum, 2 grad_wt)
+        "epoch_ms": round(ms, 3), "loss": loss, "scaling": "strong", "gpu_launches": steps * 19})
     line["steps"] = steps
     line["clocks"] = clk.summary()
     if ws == 1:
