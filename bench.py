@@ -11,7 +11,7 @@ with A^T built once on the device before timing (the cache; its build time
 is reported separately as `transpose_ms`).
 
   value  = 2 * (2*nnz*K) / step time   [GFLOP/s], inputs resident in HBM,
-           L2 flushed (256 MiB write) between steps, device-timed (CUDA events)
+           L2 flushed (256 MiB write + 256 MiB read) between steps, device-timed (CUDA events)
   e2e    = the same metric through the public API with pinned HOST buffers:
            H2D of X and dC, both SpMMs, D2H of C and dX inside the timed region
   roofline = algorithmic bytes of the SpMM launches / their event-timed
@@ -56,8 +56,8 @@ def parse():
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--plan", type=str, default="", help="JSON plan params override")
-    p.add_argument("--workload", choices=("cfg2", "cfg3", "cfg4", "cfg5"), default="cfg2",
-                   help="cfg2 (default, the headline) | cfg3 GCN layer | cfg4 FusedMM/SDDMM | "
+    p.add_argument("--workload", choices=("cfg1", "cfg2", "cfg3", "cfg4", "cfg5"), default="cfg2",
+                   help="cfg2 (default, the headline) | cfg1 small ER SpMM | cfg3 GCN layer | cfg4 FusedMM/SDDMM | "
                         "cfg5 row-partitioned GraphSAGE-mean step")
     p.add_argument("--exchange", choices=("peer", "nccl"), default="nccl",
                    help="cfg5 at N>1: SpMM reads peer feature blocks in place (peer) or NCCL all-gather")
@@ -158,7 +158,7 @@ def config_of(w, extra=None):
     c = {"workload": "cfg2: SpMM fwd + bwd (cached CSC), R-MAT 2^18 avg-deg 256 sampled, dedup",
          "n_rows": w.n_rows, "nnz": w.nnz, "K": w.k, "reduce": "sum", "values": "1.0",
          "X,dC": "N(0,1)", "rmat": "(0.57,0.19,0.19,0.05), no permutation, N*256 samples",
-         "seed": w.seed, "l2": "flushed between steps (256 MiB write), flush not timed"}
+         "seed": w.seed, "l2": "flushed between steps (256 MiB write + 256 MiB read), flush not timed"}
     if extra:
         c.update(extra)
     return c
@@ -258,7 +258,7 @@ def run_ours(args):
     g = torch.from_numpy(g_np).to(dev)
     c = torch.empty(w.n_rows, w.k, device=dev)
     dx = torch.empty(w.n_cols, w.k, device=dev)
-    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+    flush = L2Flush(dev)
     stream = torch.cuda.current_stream()
 
     params = json.loads(args.plan) if args.plan else {}
@@ -498,6 +498,22 @@ def run_reference(args):
     print(json.dumps(out), flush=True)
 
 
+class L2Flush:
+    """Between timed steps: write a 256 MiB buffer (larger than the 126 MB
+    L2), then read another 256 MiB one, so the flush's own dirty lines are
+    written back before the timed region starts instead of inside it (L2
+    then holds clean, unrelated lines)."""
+
+    def __init__(self, device):
+        import torch
+        self.w = torch.empty(256 << 20, dtype=torch.uint8, device=device)
+        self.r = torch.zeros(256 << 20, dtype=torch.uint8, device=device)
+
+    def zero_(self):  # (drop-in for the old `flush.zero_()`)
+        self.w.zero_()
+        self.r.max()
+
+
 # ------------------------------------------------------- secondary workloads
 def _events_time(fn, steps, warmup, flush=None):
     """Per-step CUDA-event times (flush outside the events), ms list."""
@@ -534,6 +550,48 @@ def _base_line(args, ws, value, ms, config, extra):
     return line
 
 
+def run_cfg1(args):
+    """cfg1 (BASELINE configs[0], the reference's CPU-runnable case): one SpMM
+    sum, ER 16384^2 with 16 distinct columns per row, K = 32 -- a 38 MB
+    problem, so launch and memory latency dominate."""
+    import torch
+
+    from paper_2403_14853_b200 import graphs, ops
+    torch.cuda.set_device(0)
+    w = graphs.cfg1(args.seed)
+    m, nnz, k = w.n_rows, w.nnz, w.k
+    a = ops.CsrMatrix.from_numpy(w.row_ptr, w.col_idx, w.values, w.n_cols)
+    x = torch.from_numpy(graphs.uniform(w.n_cols * k, -1.0, 1.0, args.seed, stream=12).reshape(w.n_cols, k)).cuda()
+    c = torch.empty(m, k, device="cuda")
+    plan = ops.Plan(a, k)
+    flush = L2Flush("cuda")
+    with ClockSampler(0) as clk:
+        t = _events_time(lambda: ops.spmm_plan(a, x, "sum", plan, c), max(args.steps, 50), args.warmup, flush)
+    # warm L2, back to back: the launches are queued behind a device-side
+    # sleep so host launch overhead (~20 us through Python) is not timed
+    nw = max(args.steps, 50)
+    torch.cuda.synchronize()
+    torch.cuda._sleep(20_000_000)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(nw):
+        ops.spmm_plan(a, x, "sum", plan, c)
+    e1.record()
+    torch.cuda.synchronize()
+    ms, ms_w = float(np.median(t)), e0.elapsed_time(e1) / nw
+    by = spmm_bytes(m, nnz, k)
+    cfg = {"workload": "cfg1: SpMM sum, ER 16384^2, 16 distinct uniform cols/row, vals U[-1,1], X 16384x32 U[-1,1]",
+           "n_rows": m, "nnz": nnz, "K": k, "l2": "flushed between steps (256 MiB write + 256 MiB read), "
+           "flush not timed; median of the steps", "plan": plan.params}
+    line = _base_line(args, 1, 2 * nnz * k / ms / 1e6, ms, cfg, {
+        "roofline": {"bound": "hbm", "achieved": round(by / ms / 1e6, 1), "unit": "GB/s", "traffic": None,
+                     "alg_bytes_per_step": by},
+        "warm_l2_ms_per_step": round(ms_w, 5), "gpu_launches": max(args.steps, 50)})
+    line["steps"] = max(args.steps, 50)
+    line["clocks"] = clk.summary()
+    print(json.dumps(line), flush=True)
+
+
 def run_cfg4(args):
     """FusedMM (sigmoid edge op, sum) + SDDMM alone on cfg4."""
     import torch
@@ -546,7 +604,7 @@ def run_cfg4(args):
     x = torch.from_numpy(graphs.normal(m * k, 0, 0.1, args.seed, 41).reshape(m, k)).cuda()
     y = torch.from_numpy(graphs.normal(w.n_cols * k, 0, 0.1, args.seed, 42).reshape(w.n_cols, k)).cuda()
     out = torch.empty(m, k, device="cuda")
-    flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
+    flush = L2Flush("cuda")
     plan = p.plan(k, "fused")
     with ClockSampler(0) as clk:
         tf = _events_time(lambda: ops.fusedmm(p, x, y, "sigmoid_mul", "sum", out, plan=plan), args.steps, args.warmup, flush)
@@ -556,7 +614,7 @@ def run_cfg4(args):
     sd_bytes = 8 * (m + 1) + 8 * nnz + 4 * m * k + 4 * nnz * k + 4 * nnz
     cfg = {"workload": "cfg4: FusedMM e_ij = sigmoid(<X_i,Y_j>) a_ij, out = sum_j e_ij Y_j; R-MAT 2^20, N*32 "
                        "samples, dedup", "n_rows": m, "nnz": nnz, "K": k, "a_ij": "U[0,1]", "X,Y": "N(0,0.1)",
-           "l2": "flushed between steps (256 MiB write), flush not timed", "plan": plan.params}
+           "l2": "flushed between steps (256 MiB write + 256 MiB read), flush not timed", "plan": plan.params}
     line = _base_line(args, 1, 2 * nnz * k / mf / 1e6, mf, cfg, {
         "roofline": {"bound": "hbm", "achieved": round(fu_bytes / mf / 1e6, 1), "unit": "GB/s",
                      "traffic": (load_traffic("cfg4") or None), "alg_bytes_per_step": fu_bytes},
@@ -592,7 +650,7 @@ def run_cfg3(args):
     g = torch.from_numpy(graphs.normal(n * k, 0, 1, args.seed, 32).reshape(n, k)).cuda()
     hw = h @ wt
     out = torch.empty(n, k, device="cuda")
-    flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
+    flush = L2Flush("cuda")
     plan = a_hat.plan(k)
 
     def sparse():
@@ -610,7 +668,7 @@ def run_cfg3(args):
     by = 2 * spmm_bytes(n, nnz, k)
     cfg = {"workload": "cfg3: GCN layer fwd+bwd, A_hat = D^-1/2(A+I)D^-1/2 of R-MAT 2^20 avg-deg 50 symmetrised; "
                        "sparse = SpMM(A_hat, HW) + A_hat^T G; dense HW, H^T(A_hat^T G) cuBLAS SGEMM timed apart",
-           "n_rows": n, "nnz": nnz, "K": k, "l2": "flushed between steps, flush not timed", "plan": plan.params}
+           "n_rows": n, "nnz": nnz, "K": k, "l2": "flushed between steps (256 MiB write + 256 MiB read), flush not timed", "plan": plan.params}
     line = _base_line(args, 1, 2 * 2 * nnz * k / ms_sp / 1e6, ms_sp, cfg, {
         "roofline": {"bound": "hbm", "achieved": round(by / ms_sp / 1e6, 1), "unit": "GB/s",
                      "traffic": load_traffic("cfg3"), "alg_bytes_per_step": by},
@@ -723,6 +781,8 @@ def main():
         run_reference(args)
     elif args.workload == "cfg2":
         run_ours(args)
+    elif args.workload == "cfg1":
+        run_cfg1(args)
     elif args.workload == "cfg3":
         run_cfg3(args)
     elif args.workload == "cfg4":
