@@ -316,6 +316,17 @@ sgnn_status sgnn_gnn_counters(sgnn_gnn g, uint64_t* transpose_builds, uint64_t* 
                               uint64_t* cache_hits, int* symmetric);
 sgnn_status sgnn_gnn_destroy(sgnn_gnn g);
 
+/* ------------------------------------------------- dense FP32 products
+ * The GNN layers' tall products on the 5th-gen tensor cores in FP32
+ * emulation (each operand split into three bf16 terms, fp32 accumulation;
+ * max |err| / sum|a*b| ~1e-7, below SGEMM's): op 0: C[m x n] = A[m x k] B[k x n];
+ * op 1: C[k x n] = A[m x k]^T B[m x n] (split over m, deterministic).  Row-
+ * major device arrays, 16-byte aligned, k and n multiples of 4 (SGNN_ERR_
+ * UNSUPPORTED otherwise -- callers then use their own GEMM).  The engine
+ * above uses these for m >= 4096.  Stream-asynchronous. */
+sgnn_status sgnn_dense_mm_f32(int op, uint32_t m, uint32_t n, uint32_t k, const float* a, const float* b, float* c,
+                              sgnn_stream stream);
+
 /* ------------------------------------------------------ SAGE layer glue
  * The element-wise and classes-wide steps of a SAGE layer pair as device
  * passes, for hosts that sequence the layers themselves (the row-partitioned

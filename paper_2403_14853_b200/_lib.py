@@ -139,6 +139,7 @@ SIGNATURES = {
     "sgnn_gnn_train": (i32, [P, u32, C.c_float, i32, P, P, P, P]),
     "sgnn_gnn_counters": (i32, [P, C.POINTER(u64), C.POINTER(u64), C.POINTER(u64), C.POINTER(i32)]),
     "sgnn_gnn_destroy": (i32, [P]),
+    "sgnn_dense_mm_f32": (i32, [i32, u32, u32, u32, P, P, P, P]),
     "sgnn_add_relu_f32": (i32, [P, P, u64, P, P]),
     "sgnn_sage_logits_f32": (i32, [P, P, P, P, u32, u32, u32, P, P]),
     "sgnn_softmax_xent_f32": (i32, [P, u32, u32, P, P, C.c_double, P, P, P, P]),

@@ -1,3 +1,4 @@
+#include <algorithm>
 // capi.cu -- the extern "C" boundary (include/sgnn_b200.h).  Validation and
 // error messages follow the reference operator API (kernels.hpp:131-173).
 #include <atomic>
@@ -419,6 +420,32 @@ sgnn_status sgnn_gnn_counters(sgnn_gnn g, uint64_t* transpose_builds, uint64_t* 
 
 sgnn_status sgnn_gnn_destroy(sgnn_gnn g) {
     gnn_destroy(g);
+    return SGNN_OK;
+}
+
+// ---------------------------------------------------- dense FP32 products
+sgnn_status sgnn_dense_mm_f32(int op, uint32_t m, uint32_t n, uint32_t k, const float* a, const float* b, float* c,
+                              sgnn_stream stream) {
+    if (op != 0 && op != 1) return fail(SGNN_ERR_CONFIG, "dense_mm: op must be 0 (A B) or 1 (A^T B)");
+    if (m == 0 || n == 0 || k == 0) return SGNN_OK;
+    if (!a || !b || !c) return fail(SGNN_ERR_CONFIG, "dense_mm: null array");
+    auto al = [](const void* p) { return reinterpret_cast<uintptr_t>(p) % 16 == 0; };
+    if (k % 4 || n % 4 || !al(a) || !al(b) || !al(c) || m > 0x7fffffffu)
+        return fail(SGNN_ERR_UNSUPPORTED, "dense_mm: needs 16-byte aligned rows (k, n multiples of 4)");
+    const cudaStream_t s = cs(stream);
+    void* ws = nullptr;
+    const size_t ws_bytes = size_t(4) << 20;
+    SGNN_TRY(scratch_alloc(&ws, ws_bytes, s));
+    int rc = 0;
+    if (op == 0) {
+        rc = dense_mm_nn(int(m), int(n), int(k), a, b, c, 0.0f, ws, ws_bytes, s);
+    } else {
+        const int splits = int(std::max<uint32_t>(1, std::min<uint32_t>(148, m / 8192)));
+        rc = dense_mm_tn(int(m), int(n), int(k), a, b, c, splits, ws, ws_bytes, s);
+    }
+    scratch_free(ws, s);
+    if (rc) return fail(SGNN_ERR_UNSUPPORTED, "dense_mm: the tensor-core kernel refused this shape (" + std::to_string(rc) + ")");
+    SGNN_LAUNCH_CHECK();
     return SGNN_OK;
 }
 

@@ -11,6 +11,7 @@
 #include <algorithm>
 #include <cstdlib>
 #include <cstring>
+#include <initializer_list>
 #include <vector>
 
 #include "ops.cuh"
@@ -545,6 +546,8 @@ struct sgnn_gnn_s {
     sgnn_csr a_hat{};
     cublasHandle_t blas = nullptr;
     void* blas_ws = nullptr;
+    size_t blas_ws_bytes = 0;
+    bool dense_tc = true;  // tall products on the tensor cores (mm / mm_tn)
     std::vector<void*> owned;
     // inputs
     float* x = nullptr;
@@ -599,14 +602,32 @@ sgnn_status blas_ok(cublasStatus_t st, const char* what) {
     return SGNN_OK;
 }
 
+// Tall products (all rows of the graph) run on the tensor cores in FP32
+// emulation (dense_common.cuh: 3 bf16 terms per operand, fp32 accumulation,
+// more accurate than SGEMM); the small ones, and any shape the CUTLASS
+// kernels refuse, on cuBLAS SGEMM.
+bool tall_ok(const sgnn_gnn_s* g, int m, int k, int n, std::initializer_list<const void*> ptrs) {
+    if (!g->dense_tc || m < 4096 || k < 32 || n < 32 || k % 4 || n % 4) return false;
+    for (const void* p : ptrs)
+        if (reinterpret_cast<uintptr_t>(p) % 16) return false;
+    return true;
+}
+
 // Row-major products through column-major cuBLAS (C^T = B^T A^T etc.).
 // matmul (dense.hpp): C[m,n] = A[m,k] B[k,n]
-sgnn_status mm(sgnn_gnn_s* g, const float* A, const float* B, float* Cm, int m, int k, int n) {
+sgnn_status mm(sgnn_gnn_s* g, const float* A, const float* B, float* Cm, int m, int k, int n, cudaStream_t s) {
+    if (tall_ok(g, m, k, n, {A, B, Cm}) &&
+        dense_mm_nn(m, n, k, A, B, Cm, 0.0f, g->blas_ws, g->blas_ws_bytes, s) == 0)
+        return SGNN_OK;
     const float one = 1.0f, zero = 0.0f;
     return blas_ok(cublasSgemm(g->blas, CUBLAS_OP_N, CUBLAS_OP_N, n, m, k, &one, B, n, A, k, &zero, Cm, n), "mm");
 }
 // matmul_tn: C[k,n] = A[m,k]^T B[m,n]
-sgnn_status mm_tn(sgnn_gnn_s* g, const float* A, const float* B, float* Cm, int m, int k, int n) {
+sgnn_status mm_tn(sgnn_gnn_s* g, const float* A, const float* B, float* Cm, int m, int k, int n, cudaStream_t s) {
+    if (tall_ok(g, m, k, n, {A, B, Cm})) {
+        const int splits = std::max(1, std::min(148, m / 8192));  // one split per SM at cfg5 sizes
+        if (dense_mm_tn(m, n, k, A, B, Cm, splits, g->blas_ws, g->blas_ws_bytes, s) == 0) return SGNN_OK;
+    }
     const float one = 1.0f, zero = 0.0f;
     return blas_ok(cublasSgemm(g->blas, CUBLAS_OP_N, CUBLAS_OP_T, n, k, m, &one, B, n, A, k, &zero, Cm, n), "mm_tn");
 }
@@ -651,33 +672,33 @@ sgnn_status epoch(sgnn_gnn_s* g, float lr, cudaStream_t s) {
     const int red = g->kind == kSageMean ? SGNN_REDUCE_MEAN : SGNN_REDUCE_SUM;
     // ---- forward (gnn.hpp:212-256)
     if (g->kind == kGcn) {
-        SGNN_TRY(mm(g, g->x, g->w1, g->z1, n, in, hid));                 // z1 = X W1
+        SGNN_TRY(mm(g, g->x, g->w1, g->z1, n, in, hid, s));                 // z1 = X W1
         SGNN_TRY(fwd_spmm(g, g->z1, g->hid, g->t1, SGNN_REDUCE_SUM, s));  // A_hat z1
         LAUNCH_EW4(relu_kernel, nh, g->t1, nh, g->h1);                    // h1
-        SGNN_TRY(mm(g, g->h1, g->w2, g->t2, n, hid, cls));               // z2 = h1 W2
+        SGNN_TRY(mm(g, g->h1, g->w2, g->t2, n, hid, cls, s));               // z2 = h1 W2
         SGNN_TRY(fwd_spmm(g, g->t2, g->cls, g->logits, SGNN_REDUCE_SUM, s));
     } else if (g->kind == kSageSum || g->kind == kSageMean) {
         SGNN_TRY(fwd_spmm(g, g->x, g->in, g->a1, red, s));                // a1 = A X
-        SGNN_TRY(mm(g, g->a1, g->w1, g->z1, n, in, hid));
-        SGNN_TRY(mm(g, g->x, g->w1s, g->t1, n, in, hid));
+        SGNN_TRY(mm(g, g->a1, g->w1, g->z1, n, in, hid, s));
+        SGNN_TRY(mm(g, g->x, g->w1s, g->t1, n, in, hid, s));
         LAUNCH_EW4(add_relu_kernel, nh, g->z1, g->t1, nh, g->h1);          // h1 = relu(a1 W1 + X W1s)
         SGNN_TRY(fwd_spmm(g, g->h1, g->hid, g->a2, red, s));               // a2 = A h1
         if (g->skinny) {
             SAGE_CP(sage_logits_kernel, g->cls, grid_for(uint64_t(g->n) * 32), 256,
                     (g->a2, g->h1, g->w2, g->w2s, g->n, g->hid, g->cls, g->logits));
         } else {
-            SGNN_TRY(mm(g, g->a2, g->w2, g->logits, n, hid, cls));
-            SGNN_TRY(mm(g, g->h1, g->w2s, g->t2, n, hid, cls));
+            SGNN_TRY(mm(g, g->a2, g->w2, g->logits, n, hid, cls, s));
+            SGNN_TRY(mm(g, g->h1, g->w2s, g->t2, n, hid, cls, s));
             LAUNCH_EW4(add_kernel, nc, g->logits, g->t2, nc);
         }
     } else {  // GIN
         SGNN_TRY(fwd_spmm(g, g->x, g->in, g->t1, SGNN_REDUCE_SUM, s));
         LAUNCH_EW(scaled_add_kernel, ni, g->eps, g->x, g->t1, ni, g->a1);  // a1 = (1+eps) X + A X
-        SGNN_TRY(mm(g, g->a1, g->w1, g->z1, n, in, hid));
+        SGNN_TRY(mm(g, g->a1, g->w1, g->z1, n, in, hid, s));
         LAUNCH_EW4(relu_kernel, nh, g->z1, nh, g->h1);
         SGNN_TRY(fwd_spmm(g, g->h1, g->hid, g->z1, SGNN_REDUCE_SUM, s));
         LAUNCH_EW(scaled_add_kernel, nh, g->eps, g->h1, g->z1, nh, g->a2);
-        SGNN_TRY(mm(g, g->a2, g->w2, g->logits, n, hid, cls));
+        SGNN_TRY(mm(g, g->a2, g->w2, g->logits, n, hid, cls, s));
     }
     // ---- softmax_xent + masked_accuracy (gnn.hpp:318-370)
     const double inv_n = 1.0 / double(g->n_masked);
@@ -703,11 +724,11 @@ sgnn_status epoch(sgnn_gnn_s* g, float lr, cudaStream_t s) {
         sgnn_csr at;  // fetched once, applied twice (gnn.hpp:274-279)
         SGNN_TRY(cache_sum_operand(g->cache, &at, s));
         SGNN_TRY(cache_spmm_with_operand(g->cache, &at, g->grad, g->cls, g->d_c, s));                 // dz2
-        SGNN_TRY(mm_tn(g, g->h1, g->d_c, g->g2, n, hid, cls));                                        // W2 grad
+        SGNN_TRY(mm_tn(g, g->h1, g->d_c, g->g2, n, hid, cls, s));                                        // W2 grad
         SGNN_TRY(mm_nt(g, g->d_c, g->w2, g->d_h, n, cls, hid));                                       // dh1
         LAUNCH_EW4(relu_backward_kernel, nh, g->d_h, g->h1, nh, g->d_h2);                            // dp1
         SGNN_TRY(cache_spmm_with_operand(g->cache, &at, g->d_h2, g->hid, g->d_h, s));                 // dz1
-        SGNN_TRY(mm_tn(g, g->x, g->d_h, g->g1, n, in, hid));
+        SGNN_TRY(mm_tn(g, g->x, g->d_h, g->g1, n, in, hid, s));
     } else if (g->kind == kSageSum || g->kind == kSageMean) {
         if (g->skinny) {
             SAGE_CP(sage_wgrad_kernel, g->cls, g->wg_blocks, 256, (g->a2, g->h1, g->grad, g->n, g->hid, g->cls, g->wg_rpb, g->wg_part));
@@ -720,25 +741,25 @@ sgnn_status epoch(sgnn_gnn_s* g, float lr, cudaStream_t s) {
             SAGE_CP(sage_grad_wt_kernel, g->cls, grid_for(uint64_t(g->n) * 32), 256,
                     (g->grad, g->w2s, g->n, g->hid, g->cls, g->d_h2, g->h1, g->z1));
         } else {
-            SGNN_TRY(mm_tn(g, g->a2, g->grad, g->g2, n, hid, cls));
-            SGNN_TRY(mm_tn(g, g->h1, g->grad, g->g2s, n, hid, cls));
+            SGNN_TRY(mm_tn(g, g->a2, g->grad, g->g2, n, hid, cls, s));
+            SGNN_TRY(mm_tn(g, g->h1, g->grad, g->g2s, n, hid, cls, s));
             SGNN_TRY(mm_nt(g, g->grad, g->w2, g->d_h, n, cls, hid));                                  // ds2
             SGNN_TRY(cache_spmm_backward(g->cache, g->d_h, g->n, g->hid, g->d_h2, red, s));          // dh1
             SGNN_TRY(mm_nt(g, g->grad, g->w2s, g->d_h, n, cls, hid));
             // dz1 into z1 (free after the forward's add_relu)
             LAUNCH_EW4(add_relu_backward_kernel, nh, g->d_h2, g->d_h, g->h1, nh, g->z1);
         }
-        SGNN_TRY(mm_tn(g, g->a1, g->z1, g->g1, n, in, hid));
-        SGNN_TRY(mm_tn(g, g->x, g->z1, g->g1s, n, in, hid));
+        SGNN_TRY(mm_tn(g, g->a1, g->z1, g->g1, n, in, hid, s));
+        SGNN_TRY(mm_tn(g, g->x, g->z1, g->g1s, n, in, hid, s));
     } else {  // GIN
-        SGNN_TRY(mm_tn(g, g->a2, g->grad, g->g2, n, hid, cls));
+        SGNN_TRY(mm_tn(g, g->a2, g->grad, g->g2, n, hid, cls, s));
         SGNN_TRY(mm_nt(g, g->grad, g->w2, g->d_h, n, cls, hid));                                      // dm2
         dot_all_kernel<<<1, 1024, 0, s>>>(g->d_h, g->h1, nh, g->deps);
         SGNN_LAUNCH_CHECK();
         SGNN_TRY(cache_spmm_backward(g->cache, g->d_h, g->n, g->hid, g->d_h2, SGNN_REDUCE_SUM, s));
         LAUNCH_EW(scaled_add_kernel, nh, g->eps, g->d_h, g->d_h2, nh, g->z1);                        // dh1
         LAUNCH_EW4(relu_backward_kernel, nh, g->z1, g->h1, nh, g->d_h2);                             // dz1
-        SGNN_TRY(mm_tn(g, g->a1, g->d_h2, g->g1, n, in, hid));
+        SGNN_TRY(mm_tn(g, g->a1, g->d_h2, g->g1, n, in, hid, s));
         SGNN_TRY(mm_nt(g, g->d_h2, g->w1, g->t1, n, hid, in));                                        // dm1
         dot_all_kernel<<<1, 1024, 0, s>>>(g->t1, g->x, ni, g->deps);
         SGNN_LAUNCH_CHECK();
@@ -791,6 +812,8 @@ sgnn_status gnn_create(const sgnn_csr* a, int kind, uint32_t in, uint32_t hidden
     if (cudaMalloc(&g->blas_ws, ws) != cudaSuccess) return bail(fail(SGNN_ERR_NOMEM, "gnn: cuBLAS workspace"));
     g->owned.push_back(g->blas_ws);
     cublasSetWorkspace(g->blas, g->blas_ws, ws);
+    g->blas_ws_bytes = ws;  // shared with the CUTLASS GEMMs (same stream, never concurrent)
+    g->dense_tc = !std::getenv("SGNN_GNN_CUBLAS_DENSE");  // A/B switch
     cublasSetStream(g->blas, s);
     const uint64_t n = g->n;
     const uint64_t wide = std::max<uint64_t>(hidden, in);

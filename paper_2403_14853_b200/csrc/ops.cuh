@@ -68,6 +68,12 @@ sgnn_status gnn_train(sgnn_gnn_s* g, uint32_t epochs, float lr, int cuda_graph, 
                       double* seconds, cudaStream_t s);
 sgnn_status gnn_counters(sgnn_gnn_s* g, uint64_t* tb, uint64_t* nb, uint64_t* hits, int* sym);
 void gnn_destroy(sgnn_gnn_s* g);
+// Tensor-core FP32 GEMMs (dense_nn.cu / dense_tn.cu, dense_common.cuh): 0 on
+// success.  nn: C[m,n] = A[m,k] B[k,n] + beta C; tn: C[k,n] = A[m,k]^T B[m,n].
+int dense_mm_nn(int m, int n, int k, const float* a, const float* b, float* c, float beta, void* ws, size_t ws_bytes,
+                cudaStream_t s);
+int dense_mm_tn(int m, int n, int k, const float* a, const float* b, float* c, int splits, void* ws, size_t ws_bytes,
+                cudaStream_t s);
 // SAGE layer glue (gnn.cu), see sgnn_b200.h
 sgnn_status glue_add_relu(const float* a, const float* b, uint64_t n, float* h, cudaStream_t s);
 sgnn_status glue_sage_logits(const float* a2, const float* h1, const float* w2, const float* w2s, uint32_t n,

@@ -392,6 +392,22 @@ def _ptr(t):
     return t.data_ptr() if t is not None else None
 
 
+def dense_mm(a: torch.Tensor, b: torch.Tensor, transpose_a: bool = False) -> torch.Tensor:
+    """a @ b (or a.T @ b) for the layers' tall products on the tensor cores in
+    FP32 emulation (sgnn_dense_mm_f32); shapes the kernels do not take
+    (unaligned rows, short matrices) use torch's matmul on the same GPU."""
+    from ._lib import lib
+    if a.shape[0] >= 4096 and a.is_cuda and a.is_contiguous() and b.is_contiguous() \
+            and a.dtype == torch.float32 and b.dtype == torch.float32:
+        m, k = a.shape
+        n = b.shape[1]
+        out = torch.empty((k, n) if transpose_a else (m, n), device=a.device)
+        if lib().sgnn_dense_mm_f32(1 if transpose_a else 0, m, n, k, a.data_ptr(), b.data_ptr(), out.data_ptr(),
+                                   ops._stream()) == 0:
+            return out
+    return a.T @ b if transpose_a else a @ b
+
+
 def add_relu(a: torch.Tensor, b: torch.Tensor, out: torch.Tensor | None = None) -> torch.Tensor:
     """relu(a + b) in one pass (SAGE's z1 = a1 W1 + X W1s, then relu)."""
     from ._lib import check, lib

@@ -116,15 +116,15 @@ class DistSage:
             self._lab = labels_local.to(torch.int32).contiguous()
             self._msk = mask_local.to(torch.uint8).contiguous()
         a1 = self.fwd.forward(x_local, ex, red)
-        h1 = gnn.add_relu(a1 @ params.w1, x_local @ params.w1_self)
+        h1 = gnn.add_relu(gnn.dense_mm(a1, params.w1), gnn.dense_mm(x_local, params.w1_self))
         a2 = self.fwd2.forward(h1, ex, red)
         logits = gnn.sage_logits(a2, h1, params.w2, params.w2_self)
         grad, loss_sum, _ = gnn.softmax_xent_device(logits, self._lab, self._msk, 1.0 / n_masked_total)
         g_w2, g_w2s = gnn.sage_wgrad(a2, h1, grad)
         ds2 = gnn.sage_grad_wt(grad, params.w2)
         dz1 = gnn.sage_grad_wt(grad, params.w2_self, u=self.bwd.forward(ds2, ex, "sum"), act=h1)
-        g_w1 = a1.T @ dz1
-        g_w1s = x_local.T @ dz1
+        g_w1 = gnn.dense_mm(a1, dz1, transpose_a=True)
+        g_w1s = gnn.dense_mm(x_local, dz1, transpose_a=True)
         flat = self.allreduce(torch.cat([g_w1.ravel(), g_w2.ravel(), g_w1s.ravel(), g_w2s.ravel()]))
         loss_sum = self.allreduce(loss_sum)
         o = 0

@@ -224,3 +224,53 @@ def test_dist_sage_glue_step_matches_torch_step(cuda, hidden, classes):
         runs.append((losses, torch.cat([p.ravel() for p in (params.w1, params.w2, params.w1_self, params.w2_self)])))
     np.testing.assert_allclose(runs[0][0], runs[1][0], rtol=1e-5)
     np.testing.assert_allclose(runs[0][1].cpu().numpy(), runs[1][1].cpu().numpy(), rtol=1e-4, atol=1e-6)
+
+
+@pytest.mark.parametrize("kind", ["sage-mean", "gcn"])
+def test_native_tensor_core_gemms_match_sgemm(cuda, monkeypatch, kind):
+    """The engine's tall products (X W, A^T G over all rows) on the tensor
+    cores in FP32 emulation (csrc/dense_*.cu) vs the same engine on cuBLAS
+    SGEMM (SGNN_GNN_CUBLAS_DENSE): losses and weights agree to fp32
+    reassociation; the emulated products are checked against fp64 too."""
+    import torch
+
+    from paper_2403_14853_b200 import gnn, graphs, ops
+    rp, ci = graphs.rmat(13, 8192 * 8, seed=6, symmetrize=True)
+    n = len(rp) - 1
+    a = ops.CsrMatrix.from_numpy(rp, ci, np.ones(len(ci), np.float32), n)
+    rng = np.random.default_rng(8)
+    x = torch.from_numpy(rng.standard_normal((n, 64)).astype(np.float32)).cuda()
+    lab = torch.from_numpy(rng.integers(0, 8, n)).cuda()
+    mask = torch.from_numpy((rng.random(n) < 0.6).astype(np.uint8)).cuda()
+    runs = []
+    for cublas in (False, True):
+        if cublas:
+            monkeypatch.setenv("SGNN_GNN_CUBLAS_DENSE", "1")
+        m = gnn.init_model(kind, 64, 128, 8, seed=3)
+        out = gnn.train_native(m, a, x, lab, mask, epochs=6, lr=0.05)
+        runs.append(([s.loss for s in out.stats], gnn.flat_weights(m)))
+    assert not np.array_equal(runs[0][1], runs[1][1])  # two different GEMM paths ran
+    np.testing.assert_allclose(runs[0][0], runs[1][0], rtol=1e-5)
+    np.testing.assert_allclose(runs[0][1], runs[1][1], rtol=1e-4, atol=1e-6)
+
+
+@pytest.mark.parametrize("m,k,n", [(5000, 128, 128), (70000, 64, 96), (4100, 256, 32)])
+def test_dense_mm_tensor_core_fp32(cuda, m, k, n):
+    """sgnn_dense_mm_f32 (tensor-core FP32 emulation) vs fp64: A B and A^T B
+    within 1e-6 of sum|a*b| -- tighter than SGEMM needs -- and deterministic."""
+    import torch
+
+    from paper_2403_14853_b200 import gnn
+    g = torch.Generator(device="cuda").manual_seed(m + k + n)
+    a = torch.randn(m, k, device="cuda", generator=g)
+    b = torch.randn(k, n, device="cuda", generator=g)
+    b2 = torch.randn(m, n, device="cuda", generator=g)
+    c = gnn.dense_mm(a, b)
+    want = a.double() @ b.double()
+    den = a.double().abs() @ b.double().abs()
+    assert ((c.double() - want).abs() <= 1e-6 * den).all()
+    t = gnn.dense_mm(a, b2, transpose_a=True)
+    want = a.double().T @ b2.double()
+    den = a.double().abs().T @ b2.double().abs()
+    assert ((t.double() - want).abs() <= 1e-6 * den).all()
+    assert torch.equal(gnn.dense_mm(a, b2, transpose_a=True).view(torch.int32), t.view(torch.int32))
