@@ -1,3 +1,4 @@
+// Probe driver for fp32emu.cu (tensor-core FP32 GEMM vs cuBLAS SGEMM, 4M x 128 x 128): nvcc ... fp32emu_main.cu fp32emu.o -lcublas
 #include <cstdio>
 #include <cstdlib>
 #include <vector>

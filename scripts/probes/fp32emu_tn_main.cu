@@ -1,3 +1,4 @@
+// Probe driver for fp32emu_tn.cu (split-K A^T B over 4M rows vs cuBLAS SGEMM)
 #include <cstdio>
 #include <cstdlib>
 #include <vector>
