@@ -218,12 +218,18 @@ __global__ void mean_scale_kernel(const uint32_t* __restrict__ ci, const float* 
         vout[e] = __fdiv_rn(vin[e], float(__ldg(deg + __ldg(ci + e))));
 }
 
-// One thread per nonzero (i, j, v): binary-search i in row j; mismatch -> flag 0.
+// is_symmetric with half the searches: only the upper entries (i, j > i)
+// binary-search their mirror (j, i) in row j (value must match); lower
+// entries are only counted.  Every upper entry matched and #upper == #lower
+// <=> the mirror map is a bijection of the off-diagonal entries <=> the
+// reference's check (every entry's mirror exists with an equal value) holds.
+// flag[0] = 0 on a mismatch; cnt[0] / cnt[1] accumulate #upper / #lower.
 __global__ void __launch_bounds__(kThreads) symmetric_kernel(const uint64_t* __restrict__ rp,
                                                              const uint32_t* __restrict__ ci,
                                                              const float* __restrict__ v,
                                                              uint32_t m, uint64_t nnz,
-                                                             int* __restrict__ flag) {
+                                                             int* __restrict__ flag,
+                                                             unsigned long long* __restrict__ cnt) {
     __shared__ uint32_t s_rows[2];
     __shared__ int s_done;
     const uint64_t base = uint64_t(blockIdx.x) * kTile;
@@ -239,11 +245,18 @@ __global__ void __launch_bounds__(kThreads) symmetric_kernel(const uint64_t* __r
     __syncthreads();
     if (s_done) return;
     bool ok = true;
+    uint32_t up = 0, low = 0;
     for (int r = 0; r < kItems; ++r) {
         const uint64_t e = base + uint64_t(r) * kThreads + threadIdx.x;
         if (e >= nnz) break;
         const uint32_t i = find_row(rp, s_rows[0], s_rows[1], e);
         const uint32_t j = __ldg(ci + e);
+        if (j < i) {
+            ++low;
+            continue;
+        }
+        if (j == i) continue;
+        ++up;
         uint64_t lo = __ldg(rp + j), hi = __ldg(rp + j + 1);
         const uint64_t end = hi;
         while (lo < hi) {  // lower_bound of i in row j
@@ -252,6 +265,15 @@ __global__ void __launch_bounds__(kThreads) symmetric_kernel(const uint64_t* __r
             else hi = mid;
         }
         if (lo == end || __ldg(ci + lo) != i || __ldg(v + lo) != __ldg(v + e)) ok = false;
+    }
+    // block sums of the counts (warp reduce, one atomic per warp)
+    for (int o = 16; o >= 1; o >>= 1) {
+        up += __shfl_xor_sync(0xffffffffu, up, o);
+        low += __shfl_xor_sync(0xffffffffu, low, o);
+    }
+    if ((threadIdx.x & 31) == 0) {
+        if (up) atomicAdd(cnt, (unsigned long long)up);
+        if (low) atomicAdd(cnt + 1, (unsigned long long)low);
     }
     if (__syncthreads_or(!ok) && threadIdx.x == 0) atomicExch(flag, 0);
 }
@@ -372,22 +394,26 @@ sgnn_status run_is_symmetric(const sgnn_csr* a, int* out, cudaStream_t s) {
         *out = 1;
         return SGNN_OK;
     }
-    int* flag = nullptr;
-    SGNN_TRY(scratch_alloc(reinterpret_cast<void**>(&flag), sizeof(int), s));
-    const int one = 1;
+    // scratch: flag (int, padded to 8 bytes) | #upper | #lower
+    unsigned long long* buf = nullptr;
+    SGNN_TRY(scratch_alloc(reinterpret_cast<void**>(&buf), 3 * sizeof(unsigned long long), s));
+    int* flag = reinterpret_cast<int*>(buf);
+    const unsigned long long init[3] = {1ull, 0ull, 0ull};  // flag word = 1 (little endian)
     sgnn_status st = SGNN_OK;
-    if (cudaMemcpyAsync(flag, &one, sizeof(int), cudaMemcpyHostToDevice, s) != cudaSuccess)
+    if (cudaMemcpyAsync(buf, init, sizeof(init), cudaMemcpyHostToDevice, s) != cudaSuccess)
         st = fail(SGNN_ERR_CUDA, "is_symmetric: memcpy failed");
     if (st == SGNN_OK) {
         symmetric_kernel<<<unsigned(ceil_div_u64(a->nnz, kTile)), kThreads, 0, s>>>(
-            a->row_ptr, a->col_idx, a->values, a->n_rows, a->nnz, flag);
+            a->row_ptr, a->col_idx, a->values, a->n_rows, a->nnz, flag, buf + 1);
         if (cudaGetLastError() != cudaSuccess) st = fail(SGNN_ERR_CUDA, "is_symmetric: launch failed");
     }
+    unsigned long long res[3] = {0, 0, 0};
     if (st == SGNN_OK &&
-        (cudaMemcpyAsync(out, flag, sizeof(int), cudaMemcpyDeviceToHost, s) != cudaSuccess ||
+        (cudaMemcpyAsync(res, buf, sizeof(res), cudaMemcpyDeviceToHost, s) != cudaSuccess ||
          cudaStreamSynchronize(s) != cudaSuccess))
         st = fail(SGNN_ERR_CUDA, "is_symmetric: readback failed");
-    scratch_free(flag, s);
+    scratch_free(buf, s);
+    if (st == SGNN_OK) *out = (int(res[0] & 0xffffffffu) != 0 && res[1] == res[2]) ? 1 : 0;
     return st;
 }
 

@@ -166,3 +166,35 @@ def test_release_scratch_after_builds(cuda):
     torch.cuda.synchronize()
     for x, y in zip(t1.to_numpy(), t2.to_numpy()):
         np.testing.assert_array_equal(x, y)
+
+
+def test_is_symmetric_upper_lower_counting(cuda):
+    """is_symmetric searches only the upper entries and compares the upper and
+    lower counts: an extra lower entry, a value mismatch, a diagonal-only
+    matrix and symmetric hub matrices all agree with the oracle."""
+    import numpy as np
+
+    from paper_2403_14853_b200 import graphs, ops
+
+    def sym(rp, ci, v, n):
+        got = ops.is_symmetric(ops.CsrMatrix.from_numpy(np.asarray(rp, np.uint64), np.asarray(ci, np.uint32),
+                                                        np.asarray(v, np.float32), n))
+        assert got == port.is_symmetric(np.asarray(rp, np.uint64), np.asarray(ci, np.uint32),
+                                        np.asarray(v, np.float32), n)
+        return got
+    # (0,1),(1,0) mirrored; extra lower (2,0) without (0,2)
+    assert not sym([0, 1, 2, 3], [1, 0, 0], [1, 1, 1], 3)
+    # extra upper (0,2) without (2,0)
+    assert not sym([0, 2, 3, 3], [1, 2, 0], [1, 1, 1], 3)
+    # mirror present, value differs
+    assert not sym([0, 1, 2], [1, 0], [1.0, 2.0], 2)
+    assert sym([0, 1, 2], [1, 0], [2.0, 2.0], 2)
+    assert sym([0, 1, 2, 3], [0, 1, 2], [5, 6, 7], 3)  # diagonal only
+    rp, ci = graphs.rmat(12, 4096 * 16, seed=11, symmetrize=True, self_loops=True)
+    v = np.ones(len(ci), np.float32)
+    assert sym(rp, ci, v, 4096)
+    v2 = v.copy()
+    v2[len(v2) // 2] = 2.0  # one mirror pair now differs
+    assert not sym(rp, ci, v2, 4096)
+    rp2, ci2 = graphs.rmat(12, 4096 * 16, seed=11)
+    assert not sym(rp2, ci2, np.ones(len(ci2), np.float32), 4096)
