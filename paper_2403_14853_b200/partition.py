@@ -87,8 +87,11 @@ def make_partition(row_ptr, n_parts: int, align: int = 1, pow2: bool = False) ->
 
 
 def pad_block(x_local, stride: int):
-    """[rows_p, K] -> [stride, K] (zero padding; padded rows are never read)."""
+    """[rows_p, K] -> [stride, K] (zero padding; padded rows are never read).
+    A block that already has `stride` rows is used as it is (no copy)."""
     import torch
+    if x_local.shape[0] == stride:
+        return x_local.contiguous()
     out = torch.zeros((stride, x_local.shape[1]), dtype=x_local.dtype, device=x_local.device)
     out[: x_local.shape[0]].copy_(x_local)
     return out
