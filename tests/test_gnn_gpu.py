@@ -274,3 +274,25 @@ def test_dense_mm_tensor_core_fp32(cuda, m, k, n):
     den = a.double().abs().T @ b2.double().abs()
     assert ((t.double() - want).abs() <= 1e-6 * den).all()
     assert torch.equal(gnn.dense_mm(a, b2, transpose_a=True).view(torch.int32), t.view(torch.int32))
+
+
+def test_native_cuda_graph_with_tensor_core_gemms(cuda):
+    """CUDA-graph epochs with the tensor-core FP32 products in the captured
+    graph (graph of 8192 nodes: tall products on dense_*.cu) replay bitwise
+    the eager epochs."""
+    import torch
+
+    from paper_2403_14853_b200 import gnn, graphs, ops
+    rp, ci = graphs.rmat(13, 8192 * 8, seed=12, symmetrize=True)
+    n = len(rp) - 1
+    a = ops.CsrMatrix.from_numpy(rp, ci, np.ones(len(ci), np.float32), n)
+    rng = np.random.default_rng(9)
+    x = torch.from_numpy(rng.standard_normal((n, 64)).astype(np.float32)).cuda()
+    lab = torch.from_numpy(rng.integers(0, 8, n)).cuda()
+    mask = torch.from_numpy((rng.random(n) < 0.6).astype(np.uint8)).cuda()
+    m1 = gnn.init_model("sage-mean", 64, 128, 8, seed=4)
+    eager = gnn.train_native(m1, a, x, lab, mask, epochs=5, lr=0.05)
+    m2 = gnn.init_model("sage-mean", 64, 128, 8, seed=4)
+    graphed = gnn.train_native(m2, a, x, lab, mask, epochs=5, lr=0.05, cuda_graph=True)
+    np.testing.assert_array_equal(gnn.flat_weights(m2).view(np.uint32), gnn.flat_weights(m1).view(np.uint32))
+    assert [s.loss for s in graphed.stats] == [s.loss for s in eager.stats]
