@@ -208,7 +208,7 @@ def cpu_reference_run(w, x, g, steps, warmup, budget_s=150.0, flavours=None):
     for f, b in benches.items():
         for spec in (False, True):
             dt = None
-            for _ in range(2):  # the first call also pays first-touch page faults
+            for _ in range(3):  # the first call also pays first-touch page faults; min of 3 (noisy hosts)
                 t0 = time.perf_counter()
                 b.step(specialized=spec, threads=0)
                 t = time.perf_counter() - t0
