@@ -755,8 +755,8 @@ def run_cfg5(args):
     line = _base_line(args, ws, flops / ms / 1e6, ms, cfg, {
         # per step: 2 forward SpMMs (worker, 2 fixups, mean divide), 1 backward
         # SpMM (worker, 2 fixups), 8 glue passes (add_relu, logits, xent + sum,
-        # wgrad + sum, 2 grad_wt)
-        "epoch_ms": round(ms, 3), "loss": loss, "scaling": "strong", "gpu_launches": steps * 19})
+        # wgrad + sum, 2 grad_wt), 4 tensor-core FP32 products (2 X W, 2 A^T B)
+        "epoch_ms": round(ms, 3), "loss": loss, "scaling": "strong", "gpu_launches": steps * 23})
     line["steps"] = steps
     line["clocks"] = clk.summary()
     if ws == 1:
