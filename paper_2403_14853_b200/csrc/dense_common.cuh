@@ -27,17 +27,20 @@ using ClusterShape = Shape<_1, _1, _1>;
 // The kernel for given operand layouts and tile scheduler, spelled out at
 // namespace scope in each translation unit (SGNN_DENSE_GEMM) -- nvcc's host
 // pass rejects these builder chains as member aliases of a class template.
-#define SGNN_DENSE_GEMM(NAME, LAYOUT_A, LAYOUT_B, SCHEDULER)                                                     \
+#define SGNN_DENSE_GEMM(NAME, LAYOUT_A, LAYOUT_B, SCHEDULER) \
+    SGNN_DENSE_GEMM_CFG(NAME, LAYOUT_A, LAYOUT_B, SCHEDULER, sgnn::dense::TileShape, sgnn::dense::ClusterShape, \
+                        cutlass::epilogue::TmaWarpSpecialized1Sm, cutlass::gemm::KernelTmaWarpSpecialized1SmFastFP32Sm100)
+#define SGNN_DENSE_GEMM_CFG(NAME, LAYOUT_A, LAYOUT_B, SCHEDULER, TILE, CLUSTER, EPI_SCHED, MMA_SCHED)              \
     using NAME##_Epilogue = typename cutlass::epilogue::collective::CollectiveBuilder<                          \
-        cutlass::arch::Sm100, cutlass::arch::OpClassTensorOp, sgnn::dense::TileShape, sgnn::dense::ClusterShape,   \
+        cutlass::arch::Sm100, cutlass::arch::OpClassTensorOp, TILE, CLUSTER,                                      \
         cutlass::epilogue::collective::EpilogueTileAuto, float, float, float, cutlass::layout::RowMajor, 4, float, \
-        cutlass::layout::RowMajor, 4, cutlass::epilogue::TmaWarpSpecialized1Sm>::CollectiveOp;                   \
+        cutlass::layout::RowMajor, 4, EPI_SCHED>::CollectiveOp;                                                   \
     using NAME##_Mainloop = typename cutlass::gemm::collective::CollectiveBuilder<                              \
         cutlass::arch::Sm100, cutlass::arch::OpClassTensorOp, float, LAYOUT_A, 4, float, LAYOUT_B, 4, float,      \
-        sgnn::dense::TileShape, sgnn::dense::ClusterShape,                                                        \
+        TILE, CLUSTER,                                                                                            \
         cutlass::gemm::collective::StageCountAutoCarveout<static_cast<int>(                                       \
             sizeof(typename NAME##_Epilogue::SharedStorage))>,                                                    \
-        cutlass::gemm::KernelTmaWarpSpecialized1SmFastFP32Sm100>::CollectiveOp;                                   \
+        MMA_SCHED>::CollectiveOp;                                                                                 \
     using NAME = cutlass::gemm::device::GemmUniversalAdapter<cutlass::gemm::kernel::GemmUniversal<                \
         cute::Shape<int, int, int, int>, NAME##_Mainloop, NAME##_Epilogue, SCHEDULER>>;
 

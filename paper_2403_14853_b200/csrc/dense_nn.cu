@@ -2,7 +2,13 @@
 // (dense_common.cuh): the engine's X W products.
 #include "dense_common.cuh"
 
-SGNN_DENSE_GEMM(SgnnGemmNN, cutlass::layout::RowMajor, cutlass::layout::RowMajor, void)
+#define COMMA ,
+
+// 256 x 128 tiles on SM pairs (cta_group::2): 1.64 vs 1.73 ms for 1SM 128 x 128
+// on 4M x 128 x 128 (scripts/probes/fp32emu*.cu)
+SGNN_DENSE_GEMM_CFG(SgnnGemmNN, cutlass::layout::RowMajor, cutlass::layout::RowMajor, void,
+                    cute::Shape<cute::_256 COMMA cute::_128 COMMA cute::_16>, cute::Shape<cute::_2 COMMA cute::_1 COMMA cute::_1>,
+                    cutlass::epilogue::TmaWarpSpecialized2Sm, cutlass::gemm::KernelTmaWarpSpecialized2SmFastFP32Sm100)
 
 namespace sgnn {
 int dense_mm_nn(int m, int n, int k, const float* a, const float* b, float* c, float beta, void* ws, size_t ws_bytes,
