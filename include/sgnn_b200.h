@@ -316,6 +316,86 @@ sgnn_status sgnn_gnn_counters(sgnn_gnn g, uint64_t* transpose_builds, uint64_t* 
                               uint64_t* cache_hits, int* symmetric);
 sgnn_status sgnn_gnn_destroy(sgnn_gnn g);
 
+/* ------------------------------------- multi-GPU: communicator + row-partitioned trainer
+ * The 1D row partition of SURVEY 8e for the partitioned config (BASELINE
+ * cfg5, 2-layer GraphSAGE): the reference's thread fan-out over contiguous
+ * row chunks (parallel.hpp:28-65, balanced_row_partition) lifted to GPUs, and
+ * train() (gnn.hpp:414-438) for SAGE-sum / SAGE-mean on each rank's rows.
+ *
+ * Communicator: one process per GPU, NCCL (ncclCommInitRank on the calling
+ * thread's current device; libnccl.so.2 is loaded at run time -- the one the
+ * process already has, e.g. torch's, else the system's).  Rank 0 makes the
+ * 128-byte id, the host distributes it (any channel), every rank inits.
+ * A *loopback* communicator runs P virtual ranks in one process on one
+ * stream, phase by phase (device copies instead of NCCL): the partition and
+ * exchange logic and each rank's share of the work, measured on one GPU.
+ * NULL comm = one rank, no exchange.  Synchronous. */
+typedef struct sgnn_comm_s* sgnn_comm;
+#define SGNN_COMM_ID_BYTES 128
+sgnn_status sgnn_comm_get_unique_id(void* id /* SGNN_COMM_ID_BYTES */);
+sgnn_status sgnn_comm_init_rank(const void* id, int nranks, int rank, sgnn_comm* out);
+sgnn_status sgnn_comm_init_loopback(int nranks, sgnn_comm* out);
+/* kind: 0 NCCL, 1 loopback */
+sgnn_status sgnn_comm_info(sgnn_comm c, int* nranks, int* rank, int* kind);
+sgnn_status sgnn_comm_destroy(sgnn_comm c);
+
+/* Rank `rank` (NCCL: the communicator's own rank, argument ignored) of the
+ * row-partitioned trainer.  bounds (host, P+1 entries, bounds[0] = 0,
+ * bounds[P] = n): rank r owns rows [bounds[r], bounds[r+1]).  block: those
+ * rows of A as a device CSR with GLOBAL column ids (rows x n; borrowed -- it
+ * must outlive the engine).  bwd_block: NULL for a symmetric A (the backward
+ * operand is A's own rows, gnn.hpp:133-136,152-153), else the same rows of
+ * A^T (borrowed); for SAGE-mean the engine scales its values by 1/deg of the
+ * column (gnn.hpp:158-159) with the all-gathered global degrees.
+ * model_kind 1 SAGE-sum, 2 SAGE-mean (others SGNN_ERR_UNSUPPORTED); needs
+ * in % 4 == 0, hidden % 4 == 0, hidden <= 128, classes <= 16.  x_local
+ * [rows x in], labels_local [rows] (u32), mask_local [rows] (u8): host or
+ * device, copied.  Labels are range-checked here (ConfigError, gnn.hpp:327);
+ * a rank that fails must abort the job (its peers would wait).  Weights are
+ * zero until sgnn_dist_set_weights.  Synchronous. */
+typedef struct sgnn_dist_s* sgnn_dist;
+sgnn_status sgnn_dist_create(sgnn_comm comm, int rank, const uint32_t* bounds, const sgnn_csr* block,
+                             const sgnn_csr* bwd_block, int model_kind, uint32_t in_features, uint32_t hidden,
+                             uint32_t classes, const float* x_local, const uint32_t* labels_local,
+                             const uint8_t* mask_local, uint32_t max_epochs, sgnn_dist* out, sgnn_stream stream);
+/* w1, w1_self [in x hidden], w2, w2_self [hidden x classes], row-major, host
+ * or device; identical on every rank.  Synchronous. */
+sgnn_status sgnn_dist_set_weights(sgnn_dist g, const float* w1, const float* w2, const float* w1_self,
+                                  const float* w2_self, sgnn_stream stream);
+sgnn_status sgnn_dist_get_weights(sgnn_dist g, float* w1, float* w2, float* w1_self, float* w2_self,
+                                  sgnn_stream stream);
+/* New features for the rank's rows (host or device pointer, copied into the
+ * gathered feature buffer and re-exchanged at the next epoch).  borrow != 0
+ * with one rank: the epochs read x_local in place (16-byte aligned; it must
+ * stay valid and unchanged until the next call).  Stream-asynchronous. */
+sgnn_status sgnn_dist_set_features(sgnn_dist g, const float* x_local, int borrow, sgnn_stream stream);
+/* `epochs` training epochs at learning rate lr (forward, softmax_xent +
+ * masked_accuracy, backward, sgd_step; the loss is the global masked mean).
+ * NCCL / one rank: engines = {own engine}; loopback: all P engines, in rank
+ * order.  The first call also runs the one-time collective setup (global
+ * degrees, mean operand values, the global masked-row count; synchronous
+ * once).  Stream-asynchronous otherwise (no host sync per epoch). */
+sgnn_status sgnn_dist_epochs(sgnn_dist* engines, int n_engines, uint32_t epochs, float lr, sgnn_stream stream);
+/* Statistics of epochs [first, first+count) since the last reset:
+ * loss[i], accuracy[i], and times[i*SGNN_DIST_TIMES + j] in device ms:
+ * j=0 epoch, 1 the three SpMMs, 2 this rank's compute phases, 3 exchanges
+ * (incl. waiting for peers), 4/5/6 the layer-1 / layer-2 / backward SpMM.
+ * Any output may be NULL.  Synchronizes the stream. */
+#define SGNN_DIST_TIMES 7
+sgnn_status sgnn_dist_stats(sgnn_dist g, uint32_t first, uint32_t count, double* loss, double* accuracy,
+                            double* times, sgnn_stream stream);
+/* (loss, accuracy) pairs of epochs [first, first+count) copied to dst
+ * (host or device, 2*count doubles), stream-asynchronous: the per-step
+ * result read of a pipelined caller. */
+sgnn_status sgnn_dist_stats_copy(sgnn_dist g, uint32_t first, uint32_t count, double* dst, sgnn_stream stream);
+/* Restart the epoch counter (statistics slots) at 0. */
+sgnn_status sgnn_dist_reset(sgnn_dist g);
+/* The rank's first row, row count, block nnz, global masked count (after the
+ * first epoch) and the device address of its rows of the feature buffer. */
+sgnn_status sgnn_dist_info(sgnn_dist g, uint32_t* row0, uint32_t* rows, uint64_t* nnz, uint64_t* n_masked,
+                           float** x_local);
+sgnn_status sgnn_dist_destroy(sgnn_dist g);
+
 /* ------------------------------------------------- dense FP32 products
  * The GNN layers' tall products on the 5th-gen tensor cores in FP32
  * emulation (each operand split into three bf16 terms, fp32 accumulation;

@@ -47,6 +47,14 @@ void sgnn_host_rmat_free(void* h);
 void sgnn_host_balanced_row_partition(const uint64_t* rp, uint32_t n_rows, int n_chunks,
                                       uint32_t* bounds);
 
+/* The same rule with cost(i) = nnz(rows < i) + row_weight * i: the GPU row
+ * partition weights the row-proportional work of a training step (dense
+ * products, element-wise passes: ~30x a nonzero's SpMM work on the cfg5
+ * step) against the nonzeros.  row_weight = 1 reproduces
+ * sgnn_host_balanced_row_partition exactly. */
+void sgnn_host_weighted_row_partition(const uint64_t* rp, uint32_t n_rows, int n_chunks, uint32_t row_weight,
+                                      uint32_t* bounds);
+
 /* Row block `part` of a square CSR A (n x n) split at `bounds` (n_parts+1
  * entries, e.g. from sgnn_host_balanced_row_partition), with every column id
  * remapped to the padded owner layout used by the multi-GPU exchange:

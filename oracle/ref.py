@@ -76,6 +76,19 @@ def lib(flavour: str = "O2"):
     L.ref_bench_out.restype = C.POINTER(C.c_float)
     L.ref_bench_free.argtypes = [C.c_void_p]
     L.ref_hw_cores.restype = C.c_int
+    L.ref_trainer_create.argtypes = [C.c_int, C.c_uint32, u64p, u32p, f32p, C.c_uint32, f32p, u32p,
+                                     np.ctypeslib.ndpointer(np.uint8, flags="C_CONTIGUOUS"), C.c_uint32,
+                                     C.c_uint32, f32p, C.c_double, C.c_int]
+    L.ref_trainer_create.restype = C.c_void_p
+    L.ref_trainer_epoch.argtypes = [C.c_void_p, C.POINTER(C.c_double), C.POINTER(C.c_double)]
+    L.ref_trainer_free.argtypes = [C.c_void_p]
+    L.ref_sage_sample_create.argtypes = [C.c_int, C.c_uint32, C.c_uint32, C.c_uint32, u64p, u32p, f32p, u64p, u32p,
+                                         f32p, f32p, f32p, f32p, u32p,
+                                         np.ctypeslib.ndpointer(np.uint8, flags="C_CONTIGUOUS"), C.c_uint32,
+                                         C.c_uint32, f32p, C.c_double, C.c_int]
+    L.ref_sage_sample_create.restype = C.c_void_p
+    L.ref_sage_sample_epoch.argtypes = [C.c_void_p, C.POINTER(C.c_double)]
+    L.ref_sage_sample_free.argtypes = [C.c_void_p]
     _LIBS[flavour] = L
     return L
 
@@ -246,6 +259,71 @@ def train(kind, rp, ci, v, x, labels, mask, hidden, classes, w_init, epochs, lr,
                        hidden, classes, np.ascontiguousarray(w_init, np.float32), epochs, lr,
                        int(use_cache), threads, losses, accs, w_out, cnt))
     return losses, accs, w_out, dict(zip(("transpose_builds", "normalize_builds", "cache_hits"), (int(c) for c in cnt)))
+
+
+class Trainer:
+    """The reference's train() (gnn.hpp:414-438), one epoch-loop iteration per
+    `epoch()` call (bench.py's GNN-epoch reference arm).  build_cache runs in
+    the constructor, outside any timed region."""
+
+    def __init__(self, kind, rp, ci, v, x, labels, mask, hidden, classes, w_init, lr=0.05, threads=0,
+                 flavour="O2"):
+        self.L = lib(flavour)
+        rp, ci, v = _csr(rp, ci, v, np.float32)
+        n, in_f = x.shape
+        self.h = self.L.ref_trainer_create(MODEL_KINDS[kind], n, rp, ci, v, in_f, np.ascontiguousarray(x, np.float32),
+                                           np.ascontiguousarray(labels, np.uint32),
+                                           np.ascontiguousarray(mask, np.uint8), hidden, classes,
+                                           np.ascontiguousarray(w_init, np.float32), lr, threads)
+        if not self.h:
+            raise RuntimeError("ref_trainer_create failed")
+
+    def epoch(self):
+        loss, acc = C.c_double(), C.c_double()
+        _check(self.L.ref_trainer_epoch(self.h, C.byref(loss), C.byref(acc)))
+        return loss.value, acc.value
+
+    def close(self):
+        if getattr(self, "h", None):
+            self.L.ref_trainer_free(self.h)
+            self.h = None
+
+    def __del__(self):
+        self.close()
+
+
+class SageSample:
+    """A row sample R of the SAGE epoch on the reference's own functions
+    (ref_shim.cpp ref_sage_sample_*): rows R of A_hat and of the backward
+    operand (|R| x n), full-height X and stand-in operands, |R|-row dense work."""
+
+    def __init__(self, kind, n, a_r, m_r, x, x_r, stand_in, labels_r, mask_r, hidden, classes, w_init, lr=0.05,
+                 threads=0, flavour="O2"):
+        self.L = lib(flavour)
+        rpa, cia, va = _csr(*a_r, np.float32)
+        rpm, cim, vm = _csr(*m_r, np.float32)
+        self.rows = len(rpa) - 1
+        self.h = self.L.ref_sage_sample_create(
+            MODEL_KINDS[kind], n, x.shape[1], self.rows, rpa, cia, va, rpm, cim, vm,
+            np.ascontiguousarray(x, np.float32), np.ascontiguousarray(x_r, np.float32),
+            np.ascontiguousarray(stand_in, np.float32), np.ascontiguousarray(labels_r, np.uint32),
+            np.ascontiguousarray(mask_r, np.uint8), hidden, classes, np.ascontiguousarray(w_init, np.float32), lr,
+            threads)
+        if not self.h:
+            raise RuntimeError("ref_sage_sample_create failed")
+
+    def epoch(self):
+        loss = C.c_double()
+        _check(self.L.ref_sage_sample_epoch(self.h, C.byref(loss)))
+        return loss.value
+
+    def close(self):
+        if getattr(self, "h", None):
+            self.L.ref_sage_sample_free(self.h)
+            self.h = None
+
+    def __del__(self):
+        self.close()
 
 
 class Bench:

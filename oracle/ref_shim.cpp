@@ -259,6 +259,157 @@ void ref_bench_free(void* h) { delete static_cast<RefBench*>(h); }
 
 int ref_hw_cores() { return detect_hardware().cores; }
 
+// ---- bench arm for the GNN epoch: train() (gnn.hpp:414-438) split so that
+// each call runs exactly one iteration of its epoch loop (gnn.hpp:427-435:
+// forward, softmax_xent, masked_accuracy, backward, sgd_step).  The one-time
+// part of train() -- build_cache (gnn.hpp:423) -- runs in create, outside the
+// timed region, like the reference's own per-epoch clock (gnn.hpp:428,434).
+struct RefTrainer {
+    GnnModel<float> model;
+    TrainingCache<float> cache;
+    DenseMatrix<float> x;
+    std::vector<index_t> labels;
+    std::vector<std::uint8_t> mask;
+    float lr = 0.05f;
+    int threads = 0;
+    bool use_tuned = true;
+};
+
+void* ref_trainer_create(int kind, uint32_t n, const uint64_t* rp, const uint32_t* ci, const float* v,
+                         uint32_t in, const float* x, const uint32_t* labels, const uint8_t* mask,
+                         uint32_t hidden, uint32_t classes, const float* w_init, double lr, int threads) {
+    try {
+        auto* t = new RefTrainer{init_model<float>(static_cast<ModelKind>(kind), in, hidden, classes, 1)};
+        size_t o = 0;
+        auto get = [&](DenseMatrix<float>& w) {
+            std::memcpy(w.data.data(), w_init + o, sizeof(float) * w.data.size());
+            o += w.data.size();
+        };
+        get(t->model.w1);
+        get(t->model.w2);
+        if (t->model.has_self_weights()) {
+            get(t->model.w1_self);
+            get(t->model.w2_self);
+        }
+        {
+            CsrMatrix<float> a = make_csr<float>(n, n, rp, ci, v);
+            t->cache = build_cache(t->model.kind, a, true, true);  // TrainOptions defaults
+        }
+        t->x = make_dense<float>(n, in, x);
+        t->labels.assign(labels, labels + n);
+        t->mask.assign(mask, mask + n);
+        t->lr = static_cast<float>(lr);
+        t->threads = threads;
+        return t;
+    } catch (const std::exception&) {
+        return nullptr;
+    }
+}
+
+int ref_trainer_epoch(void* h, double* loss, double* acc) {
+    GUARD_BEGIN
+    auto* t = static_cast<RefTrainer*>(h);
+    DispatchGuard dispatch(t->use_tuned);
+    auto [logits, tape] = forward(t->model, t->cache, t->x, t->threads);
+    auto [l, grad] = softmax_xent(logits, std::span<const index_t>(t->labels), std::span<const std::uint8_t>(t->mask));
+    const double a = masked_accuracy(logits, std::span<const index_t>(t->labels), std::span<const std::uint8_t>(t->mask));
+    Gradients<float> grads = backward(t->model, t->cache, tape, grad, t->threads);
+    sgd_step(t->model, grads, t->lr);
+    if (loss) *loss = l;
+    if (acc) *acc = a;
+    GUARD_END
+}
+
+void ref_trainer_free(void* h) { delete static_cast<RefTrainer*>(h); }
+
+// ---- a ROW SAMPLE of the SAGE epoch: the same sequence of reference calls
+// as forward + softmax_xent + masked_accuracy + backward + sgd_step for
+// SAGE (gnn.hpp:234-244, :318-370, :283-296, :374-386), restricted to a row
+// set R: every row-proportional operand has |R| rows and the three SpMMs
+// run over rows R of A_hat / of the backward operand (|R| x n, all columns),
+// gathering from full-height [n x K] operands.  The layer-2 and backward
+// SpMM operands (h1, ds2 of ALL rows, which a sample cannot compute) are
+// full-height stand-ins of the same shape.  Work (and time) scales with |R|
+// and nnz(R): the bounded CPU baseline for an epoch that takes minutes.
+struct RefSageSample {
+    GnnModel<float> model;
+    CsrMatrix<float> a_r, m_r;
+    DenseMatrix<float> x, x_r, h_full, ds_full;
+    std::vector<index_t> labels;
+    std::vector<std::uint8_t> mask;
+    float lr = 0.05f;
+    int threads = 0;
+};
+
+void* ref_sage_sample_create(int kind, uint32_t n, uint32_t in, uint32_t n_r, const uint64_t* rp_a,
+                             const uint32_t* ci_a, const float* v_a, const uint64_t* rp_m, const uint32_t* ci_m,
+                             const float* v_m, const float* x, const float* x_r, const float* stand_in,
+                             const uint32_t* labels_r, const uint8_t* mask_r, uint32_t hidden, uint32_t classes,
+                             const float* w_init, double lr, int threads) {
+    try {
+        auto* t = new RefSageSample{init_model<float>(static_cast<ModelKind>(kind), in, hidden, classes, 1)};
+        size_t o = 0;
+        auto get = [&](DenseMatrix<float>& w) {
+            std::memcpy(w.data.data(), w_init + o, sizeof(float) * w.data.size());
+            o += w.data.size();
+        };
+        get(t->model.w1);
+        get(t->model.w2);
+        get(t->model.w1_self);
+        get(t->model.w2_self);
+        t->a_r = make_csr<float>(n_r, n, rp_a, ci_a, v_a);
+        t->m_r = make_csr<float>(n_r, n, rp_m, ci_m, v_m);
+        t->x = make_dense<float>(n, in, x);
+        t->x_r = make_dense<float>(n_r, in, x_r);
+        t->h_full = make_dense<float>(n, hidden, stand_in);
+        t->ds_full = make_dense<float>(n, hidden, stand_in);
+        t->labels.assign(labels_r, labels_r + n_r);
+        t->mask.assign(mask_r, mask_r + n_r);
+        t->lr = static_cast<float>(lr);
+        t->threads = threads;
+        return t;
+    } catch (const std::exception&) {
+        return nullptr;
+    }
+}
+
+int ref_sage_sample_epoch(void* h, double* loss) {
+    GUARD_BEGIN
+    auto* t = static_cast<RefSageSample*>(h);
+    const GnnModel<float>& m = t->model;
+    const ReduceOp red = m.propagate_reduce();
+    const int th = t->threads;
+    const std::span<const index_t> lab(t->labels);
+    const std::span<const std::uint8_t> msk(t->mask);
+    // forward (gnn.hpp:236-244)
+    DenseMatrix<float> a1 = spmm(t->a_r, t->x, red, th);
+    DenseMatrix<float> z1 = matmul(a1, m.w1, th);
+    add_inplace(z1, matmul(t->x_r, m.w1_self, th));
+    DenseMatrix<float> h1 = relu(z1);
+    DenseMatrix<float> a2 = spmm(t->a_r, t->h_full, red, th);
+    DenseMatrix<float> logits = matmul(a2, m.w2, th);
+    add_inplace(logits, matmul(h1, m.w2_self, th));
+    // softmax_xent + masked_accuracy (gnn.hpp:318-370)
+    auto [l, grad] = softmax_xent(logits, lab, msk);
+    (void)masked_accuracy(logits, lab, msk);
+    // backward (gnn.hpp:283-296)
+    Gradients<float> g;
+    g.w2 = matmul_tn(a2, grad, th);
+    g.w2_self = matmul_tn(h1, grad, th);
+    DenseMatrix<float> ds2 = matmul_nt(grad, m.w2, th);
+    DenseMatrix<float> dh1 = spmm(t->m_r, t->ds_full, ReduceOp::Sum, th);
+    add_inplace(dh1, matmul_nt(grad, m.w2_self, th));
+    DenseMatrix<float> dz1 = relu_backward(dh1, h1);
+    g.w1 = matmul_tn(a1, dz1, th);
+    g.w1_self = matmul_tn(t->x_r, dz1, th);
+    sgd_step(t->model, g, t->lr);
+    (void)ds2;  // its full-height counterpart is the stand-in ds_full
+    if (loss) *loss = l;
+    GUARD_END
+}
+
+void ref_sage_sample_free(void* h) { delete static_cast<RefSageSample*>(h); }
+
 // load_report (src/report.cpp:76-145): parses `path` with the reference's own
 // loader; returns 0 and best_k / #entries / #skipped, or a status (6 = ParseError).
 int ref_load_report(const char* path, uint32_t* best_k, uint32_t* n_entries, uint32_t* n_skipped) {

@@ -139,6 +139,21 @@ SIGNATURES = {
     "sgnn_gnn_train": (i32, [P, u32, C.c_float, i32, P, P, P, P]),
     "sgnn_gnn_counters": (i32, [P, C.POINTER(u64), C.POINTER(u64), C.POINTER(u64), C.POINTER(i32)]),
     "sgnn_gnn_destroy": (i32, [P]),
+    "sgnn_comm_get_unique_id": (i32, [P]),
+    "sgnn_comm_init_rank": (i32, [P, i32, i32, C.POINTER(P)]),
+    "sgnn_comm_init_loopback": (i32, [i32, C.POINTER(P)]),
+    "sgnn_comm_info": (i32, [P, C.POINTER(i32), C.POINTER(i32), C.POINTER(i32)]),
+    "sgnn_comm_destroy": (i32, [P]),
+    "sgnn_dist_create": (i32, [P, i32, P, CsrP, CsrP, i32, u32, u32, u32, P, P, P, u32, C.POINTER(P), P]),
+    "sgnn_dist_set_weights": (i32, [P, P, P, P, P, P]),
+    "sgnn_dist_get_weights": (i32, [P, P, P, P, P, P]),
+    "sgnn_dist_set_features": (i32, [P, P, i32, P]),
+    "sgnn_dist_epochs": (i32, [P, i32, u32, C.c_float, P]),
+    "sgnn_dist_stats": (i32, [P, u32, u32, P, P, P, P]),
+    "sgnn_dist_stats_copy": (i32, [P, u32, u32, P, P]),
+    "sgnn_dist_reset": (i32, [P]),
+    "sgnn_dist_info": (i32, [P, C.POINTER(u32), C.POINTER(u32), C.POINTER(u64), C.POINTER(u64), C.POINTER(P)]),
+    "sgnn_dist_destroy": (i32, [P]),
     "sgnn_dense_mm_f32": (i32, [i32, u32, u32, u32, P, P, P, P]),
     "sgnn_add_relu_f32": (i32, [P, P, u64, P, P]),
     "sgnn_sage_logits_f32": (i32, [P, P, P, P, u32, u32, u32, P, P]),
@@ -156,6 +171,7 @@ HOST_SIGNATURES = {
     "sgnn_host_rmat_export": (None, [P, P, P]),
     "sgnn_host_rmat_free": (None, [P]),
     "sgnn_host_balanced_row_partition": (None, [P, u32, i32, P]),
+    "sgnn_host_weighted_row_partition": (None, [P, u32, i32, u32, P]),
     "sgnn_host_partition_block": (u64, [P, P, P, P, i32, i32, u32, P, P, P, i32]),
     "sgnn_host_mtx_load": (i32, [C.c_char_p, i32, C.POINTER(P), C.c_char_p, C.c_size_t, C.POINTER(C.c_long)]),
     "sgnn_host_csr_dims": (None, [P, C.POINTER(u32), C.POINTER(u32), C.POINTER(u64)]),

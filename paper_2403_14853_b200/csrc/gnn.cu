@@ -1053,6 +1053,31 @@ sgnn_status glue_softmax_xent(const float* logits, uint32_t n, uint32_t c, const
     return SGNN_OK;
 }
 
+uint32_t softmax_block_count(uint32_t n) {
+    uint32_t rpb = 1, nblk = 1;
+    softmax_shape(n, &rpb, &nblk);
+    return nblk;
+}
+
+sgnn_status softmax_xent_partials(const float* logits, uint32_t n, uint32_t c, const uint32_t* labels,
+                                  const uint8_t* mask, double inv_count, float* grad, double* blk_loss,
+                                  uint32_t* blk_ok, cudaStream_t s) {
+    if (c == 0 || c > 32) return fail(SGNN_ERR_SHAPE, "softmax_xent: 1..32 classes");
+    if (n == 0) return SGNN_OK;
+    uint32_t rpb = 1, nblk = 1;
+    softmax_shape(n, &rpb, &nblk);
+    if (c <= 4)
+        softmax_xent_kernel<4><<<nblk, kSoftmaxThreads, 0, s>>>(logits, n, c, labels, mask, inv_count, rpb, grad, blk_loss, blk_ok);
+    else if (c <= 8)
+        softmax_xent_kernel<8><<<nblk, kSoftmaxThreads, 0, s>>>(logits, n, c, labels, mask, inv_count, rpb, grad, blk_loss, blk_ok);
+    else if (c <= 16)
+        softmax_xent_kernel<16><<<nblk, kSoftmaxThreads, 0, s>>>(logits, n, c, labels, mask, inv_count, rpb, grad, blk_loss, blk_ok);
+    else
+        softmax_xent_kernel<32><<<nblk, kSoftmaxThreads, 0, s>>>(logits, n, c, labels, mask, inv_count, rpb, grad, blk_loss, blk_ok);
+    SGNN_LAUNCH_CHECK();
+    return SGNN_OK;
+}
+
 sgnn_status sage_wgrad_launch(const float* a2, const float* h1, const float* grad, uint32_t n, uint32_t h,
                               uint32_t c, uint32_t rpb, uint32_t nblk, float* part, float* g2, float* g2s,
                               cudaStream_t s) {

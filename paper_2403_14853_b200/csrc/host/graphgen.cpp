@@ -213,6 +213,30 @@ void sgnn_host_balanced_row_partition(const uint64_t* rp, uint32_t n_rows, int n
     }
 }
 
+void sgnn_host_weighted_row_partition(const uint64_t* rp, uint32_t n_rows, int n_chunks, uint32_t row_weight,
+                                      uint32_t* bounds) {
+    // cost(i) = rp[i] + w * i, monotone in i: bound c is the first row whose
+    // cost reaches c/n_chunks of the total (w = 1: balanced_row_partition's
+    // rule and result, parallel.hpp:28-41); binary search per bound.
+    const uint64_t w = row_weight;
+    auto cost = [&](uint32_t i) { return rp[i] + w * uint64_t(i); };
+    for (int c = 0; c <= n_chunks; ++c) bounds[c] = n_rows;
+    bounds[0] = 0;
+    const uint64_t total = cost(n_rows);
+    uint32_t lo_row = 0;
+    for (int c = 1; c < n_chunks; ++c) {
+        const uint64_t target = total * uint64_t(c) / uint64_t(n_chunks);
+        uint32_t lo = lo_row, hi = n_rows;  // first i in [lo, n_rows] with cost(i) >= target
+        while (lo < hi) {
+            const uint32_t mid = lo + (hi - lo) / 2;
+            if (cost(mid) < target) lo = mid + 1;
+            else hi = mid;
+        }
+        bounds[c] = lo;
+        lo_row = lo;
+    }
+}
+
 uint64_t sgnn_host_partition_block(const uint64_t* rp, const uint32_t* ci, const float* v,
                                    const uint32_t* bounds, int n_parts, int part, uint32_t stride,
                                    uint64_t* out_rp, uint32_t* out_ci, float* out_v, int threads) {

@@ -85,5 +85,14 @@ sgnn_status glue_sage_wgrad(const float* a2, const float* h1, const float* grad,
                             float* g2, float* g2s, cudaStream_t s);
 sgnn_status glue_sage_grad_wt(const float* grad, const float* w, uint32_t n, uint32_t h, uint32_t c, const float* u,
                               const float* act, float* out, cudaStream_t s);
+// softmax_xent into caller-owned per-block partials (fixed block shape for n)
+uint32_t softmax_block_count(uint32_t n);
+sgnn_status softmax_xent_partials(const float* logits, uint32_t n, uint32_t c, const uint32_t* labels,
+                                  const uint8_t* mask, double inv_count, float* grad, double* blk_loss,
+                                  uint32_t* blk_ok, cudaStream_t s);
+// SAGE classes-wide weight gradients into caller-owned partials [nblk][2][h][16]
+sgnn_status sage_wgrad_launch(const float* a2, const float* h1, const float* grad, uint32_t n, uint32_t h,
+                              uint32_t c, uint32_t rpb, uint32_t nblk, float* part, float* g2, float* g2s,
+                              cudaStream_t s);
 
 }  // namespace sgnn

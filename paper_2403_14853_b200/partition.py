@@ -1,28 +1,30 @@
 """1D row partition of a square graph over GPUs.
 
 Rank p owns the contiguous row block [b_p, b_{p+1}) chosen by the reference's
-cost rule (nnz + rows, parallel.hpp:28-41, `balanced_row_partition`), the
-matching feature rows X[b_p:b_{p+1}] and the output rows C[b_p:b_{p+1}].  The
-only exchange is an all-gather of the feature blocks: every block is padded to
-`stride` rows so the gathered buffer is [P*stride, K], and the block's column
-ids are remapped once (host, `sgnn_host_partition_block`) to that padded
-layout -- col' = owner*stride + (col - b_owner) -- so the unchanged SpMM
-kernel reads the gathered buffer directly.  The remap is monotone, so every
-row is accumulated in the same order as on one GPU: the P-GPU result is
-bitwise the 1-GPU result.
+cost rule (parallel.hpp:28-41, `balanced_row_partition`) with the rows
+weighted (`row_weight`, dist.row_partition), the matching feature rows
+X[b_p:b_{p+1}] and the output rows C[b_p:b_{p+1}].  The only exchange is an
+all-gather-v of the feature blocks into a full-height [n, K] buffer -- rank
+q's rows land at rows b_q.., so the gathered buffer IS X in its own row order,
+the block keeps its global column ids and the unchanged SpMM kernel reads it
+directly.  Every row is accumulated in the same order as on one GPU: the
+P-GPU result is bitwise the 1-GPU result.  (The native trainer,
+csrc/dist.cu / dist.py, does the same exchange with grouped ncclSend/Recv;
+this module is the torch.distributed mirror used by the gloo tests.)
 
 Exchanges:
-  PeerBlocks        no copy at all: every rank's padded block lives in its own
-                    cudaMalloc allocation, mapped into every other rank with
-                    CUDA IPC (NVLink/NVSwitch peer memory on the B200 box); the
-                    SpMM kernel (sgnn_spmm_peer_f32) gathers X rows straight
-                    from the owner's HBM, so the all-gather is fused into the
-                    SpMM's own gather loop.  A pow2 stride turns the owner
-                    lookup into a shift and a mask.
-  NcclExchange      torch.distributed all_gather_into_tensor (NCCL over NVLink
-                    on the B200 box; gloo on CPU for tests)
+  NcclExchange      torch.distributed point-to-point all-gather-v (NCCL over
+                    NVLink on the B200 box; gloo on CPU for tests)
   LoopbackExchange  P virtual partitions in one process (device copies) -- the
                     SURVEY 4.5 test mode for partition/reassembly logic on one GPU
+  PeerBlocks        no copy at all: every rank's block lives in its own
+                    cudaMalloc allocation, mapped into every other rank with
+                    CUDA IPC (NVLink/NVSwitch peer memory); the SpMM kernel
+                    (sgnn_spmm_peer_f32) gathers X rows straight from the
+                    owner's HBM.  This path needs the *padded* layout: blocks
+                    of a pow2 stride, columns remapped once to
+                    col' = owner*stride + local (sgnn_host_partition_block),
+                    so the owner lookup is a shift and a mask.
 """
 from __future__ import annotations
 
@@ -36,8 +38,17 @@ from . import _lib, graphs
 @dataclass
 class RowPartition:
     bounds: np.ndarray  # u32[P+1]
-    stride: int         # padded rows per block (>= max block size)
+    stride: int         # padded rows per block (>= max block size); 0 = unpadded
     n: int
+
+    @property
+    def padded(self) -> bool:
+        return self.stride > 0
+
+    @property
+    def n_gathered(self) -> int:
+        """Rows of the gathered operand: n (unpadded) or P * stride."""
+        return self.parts * self.stride if self.padded else self.n
 
     @property
     def parts(self) -> int:
@@ -54,8 +65,14 @@ class RowPartition:
         return int(self.bounds[p]), int(self.bounds[p + 1])
 
     def block(self, row_ptr, col_idx, values, p: int, threads: int = 0):
-        """Rank p's CSR block with columns remapped to the padded layout."""
+        """Rank p's CSR block: global column ids (unpadded), or columns
+        remapped to the padded owner layout."""
         r0, r1 = self.rows(p)
+        if not self.padded:
+            rp = np.asarray(row_ptr, np.uint64)
+            e0, e1 = int(rp[r0]), int(rp[r1])
+            return ((rp[r0:r1 + 1] - rp[r0]).astype(np.uint64), np.ascontiguousarray(np.asarray(col_idx)[e0:e1], np.uint32),
+                    np.ascontiguousarray(np.asarray(values)[e0:e1], np.float32) if values is not None else None)
         rp = np.ascontiguousarray(row_ptr, np.uint64)
         ci = np.ascontiguousarray(col_idx, np.uint32)
         v = np.ascontiguousarray(values, np.float32) if values is not None else None
@@ -72,12 +89,24 @@ class RowPartition:
         return out_rp, out_ci, out_v
 
 
-def make_partition(row_ptr, n_parts: int, align: int = 1, pow2: bool = False) -> RowPartition:
-    """balanced_row_partition (parallel.hpp:28-41) at GPU granularity.
-    pow2=True rounds the block stride up to a power of two (the peer path
-    splits a remapped column into (owner, row) with a shift and a mask)."""
+def make_partition(row_ptr, n_parts: int, align: int = 1, pow2: bool = False, padded: bool | None = None,
+                   row_weight: int = 1) -> RowPartition:
+    """balanced_row_partition (parallel.hpp:28-41) at GPU granularity, with
+    cost nnz + row_weight * rows (row_weight = 1: the reference's rule).
+    Unpadded by default; padded=True (implied by pow2=True, the peer path)
+    pads every block to `stride` rows, rounded up to a power of two with pow2
+    (the peer SpMM splits a remapped column into (owner, row) with a shift)."""
     rp = np.ascontiguousarray(row_ptr, np.uint64)
-    bounds = graphs.balanced_row_partition(rp, n_parts)
+    padded = pow2 if padded is None else padded
+    if row_weight == 1:
+        bounds = graphs.balanced_row_partition(rp, n_parts)
+    else:
+        out = np.empty(n_parts + 1, np.uint32)
+        _lib.host().sgnn_host_weighted_row_partition(rp.ctypes.data, len(rp) - 1, n_parts, int(row_weight),
+                                                     out.ctypes.data)
+        bounds = out
+    if not padded:
+        return RowPartition(bounds, 0, len(rp) - 1)
     sizes = np.diff(bounds.astype(np.int64))
     stride = int(max(1, sizes.max() if len(sizes) else 1))
     stride = (stride + align - 1) // align * align
@@ -90,7 +119,7 @@ def pad_block(x_local, stride: int):
     """[rows_p, K] -> [stride, K] (zero padding; padded rows are never read).
     A block that already has `stride` rows is used as it is (no copy)."""
     import torch
-    if x_local.shape[0] == stride:
+    if stride == 0 or x_local.shape[0] == stride:  # unpadded layout: the block as it is
         return x_local.contiguous()
     out = torch.zeros((stride, x_local.shape[1]), dtype=x_local.dtype, device=x_local.device)
     out[: x_local.shape[0]].copy_(x_local)
@@ -98,12 +127,39 @@ def pad_block(x_local, stride: int):
 
 
 class NcclExchange:
-    """All-gather of the padded feature blocks through torch.distributed
-    (NCCL on GPUs; gloo on CPU tensors)."""
+    """All-gather of the feature blocks through torch.distributed (NCCL on
+    GPUs; gloo on CPU tensors): all_gather_v for the unpadded layout,
+    all_gather for the padded one."""
 
     def __init__(self, group=None):
         import torch.distributed as dist
         self.dist, self.group = dist, group
+
+    def all_gather_v(self, block, bounds):
+        """Rank q's rows [bounds[q], bounds[q+1]) to every rank: a full-height
+        [n, K] buffer (point-to-point, each rank receives only the others'
+        rows)."""
+        import torch
+        ws = self.dist.get_world_size(self.group)
+        if ws == 1:
+            return block.contiguous()
+        me = self.dist.get_rank(self.group)
+        b = [int(v) for v in bounds]
+        out = torch.empty((b[-1], block.shape[1]), dtype=block.dtype, device=block.device)
+        out[b[me]:b[me + 1]].copy_(block)
+        src = out[b[me]:b[me + 1]]
+        ops = []
+        for q in range(ws):
+            if q == me:
+                continue
+            if b[me + 1] > b[me]:
+                ops.append(self.dist.P2POp(self.dist.isend, src, q, self.group))
+            if b[q + 1] > b[q]:
+                ops.append(self.dist.P2POp(self.dist.irecv, out[b[q]:b[q + 1]], q, self.group))
+        if ops:
+            for r in self.dist.batch_isend_irecv(ops):
+                r.wait()
+        return out
 
     def all_gather(self, block):
         import torch
@@ -122,6 +178,10 @@ class LoopbackExchange:
         import torch
         return torch.cat([b.contiguous() for b in blocks], dim=0)
 
+    def all_gather_v(self, blocks, bounds):
+        import torch
+        return torch.cat([b.contiguous() for b in blocks], dim=0)
+
 
 class PartitionedSpmm:
     """Rank-local forward of C[rows_p] = reduce_j A[rows_p, j] X[j] with the
@@ -133,7 +193,7 @@ class PartitionedSpmm:
         self.part, self.rank, self.k = part, rank, int(k)
         self.r0, self.r1 = part.rows(rank)
         self.local = part.block(row_ptr, col_idx, values, rank)
-        self.n_gathered = part.parts * part.stride
+        self.n_gathered = part.n_gathered
         self.device = device
         self._compute = compute
         self._plan = None
@@ -153,8 +213,13 @@ class PartitionedSpmm:
         """x_local: this rank's feature rows [r1-r0, K]."""
         if isinstance(exchange, PeerExchange):
             return self.forward_peer(x_local, exchange.blocks_for(self.part.stride, x_local.shape[1]), reduce, out)
-        gathered = exchange.all_gather(pad_block(x_local, self.part.stride))
-        return self.compute(gathered, reduce, out)
+        return self.compute(self.gather(x_local, exchange), reduce, out)
+
+    def gather(self, local, exchange):
+        """The full operand from this rank's rows of it."""
+        if self.part.padded:
+            return exchange.all_gather(pad_block(local, self.part.stride))
+        return exchange.all_gather_v(local, self.part.bounds)
 
     # SDDMM / FusedMM shard the same way (SURVEY 8e): X is this rank's rows,
     # Y the all-gathered feature blocks in the padded owner layout.
@@ -175,12 +240,10 @@ class PartitionedSpmm:
 
     def fusedmm(self, x_local, y_local, exchange, edge_op="mul", reduce="sum", out=None):
         """Row block of fusedmm(A, X, Y): all-gather Y's blocks, then local."""
-        gathered = exchange.all_gather(pad_block(y_local, self.part.stride))
-        return self.fusedmm_gathered(x_local, gathered, edge_op, reduce, out)
+        return self.fusedmm_gathered(x_local, self.gather(y_local, exchange), edge_op, reduce, out)
 
     def sddmm(self, x_local, y_local, exchange):
-        gathered = exchange.all_gather(pad_block(y_local, self.part.stride))
-        return self.sddmm_gathered(x_local, gathered)
+        return self.sddmm_gathered(x_local, self.gather(y_local, exchange))
 
     def _compute_fused(self, x_local, y_gathered, edge_op, reduce):
         if not hasattr(self._compute, "fused"):

@@ -40,15 +40,16 @@ class DistSage:
     """One rank of the partitioned SAGE (sum or mean) trainer."""
 
     def __init__(self, row_ptr, col_idx, values, n_parts, rank, k_in, hidden, classes, reduce="mean",
-                 device="cuda", exchange=None, allreduce=None, compute=None, symmetric=True):
+                 device="cuda", exchange=None, allreduce=None, compute=None, symmetric=True, row_weight=1):
         if not symmetric:
             raise NotImplementedError("the partitioned backward uses the symmetric short-circuit "
                                       "(gnn.hpp:152-153); cfg5 is symmetric")
         self.reduce = reduce
         self.exchange = exchange or partition.NcclExchange()
-        # the peer path splits remapped columns with a shift: pow2 block stride
-        self.part = partition.make_partition(row_ptr, n_parts,
-                                             pow2=isinstance(self.exchange, partition.PeerExchange))
+        # unpadded all-gather-v layout (global column ids); the peer path
+        # splits remapped columns with a shift: padded pow2 block stride
+        peer = isinstance(self.exchange, partition.PeerExchange)
+        self.part = partition.make_partition(row_ptr, n_parts, pow2=peer, row_weight=row_weight)
         self.rank = rank
         self.r0, self.r1 = self.part.rows(rank)
         self.device = device
@@ -111,15 +112,17 @@ class DistSage:
         partitioned SpMMs and the two big GEMMs per direction."""
         red = self.reduce
         ex = self.exchange
-        if getattr(self, "_lab_src", None) is not labels_local:
-            self._lab_src = labels_local
-            self._lab = labels_local.to(torch.int32).contiguous()
-            self._msk = mask_local.to(torch.uint8).contiguous()
+        # converted on every call (one cheap cast each): a cache keyed on the
+        # labels alone would reuse a stale mask (train vs validation masks)
+        lab = labels_local.to(torch.int32).contiguous()
+        msk = mask_local.to(torch.uint8).contiguous()
+        if lab.numel() and (int(lab.min()) < 0 or int(lab.max()) >= self.classes):
+            raise partition._lib.ConfigError(f"softmax_xent: label out of range for {self.classes} classes")
         a1 = self.fwd.forward(x_local, ex, red)
         h1 = gnn.add_relu(gnn.dense_mm(a1, params.w1), gnn.dense_mm(x_local, params.w1_self))
         a2 = self.fwd2.forward(h1, ex, red)
         logits = gnn.sage_logits(a2, h1, params.w2, params.w2_self)
-        grad, loss_sum, _ = gnn.softmax_xent_device(logits, self._lab, self._msk, 1.0 / n_masked_total)
+        grad, loss_sum, _ = gnn.softmax_xent_device(logits, lab, msk, 1.0 / n_masked_total)
         g_w2, g_w2s = gnn.sage_wgrad(a2, h1, grad)
         ds2 = gnn.sage_grad_wt(grad, params.w2)
         dz1 = gnn.sage_grad_wt(grad, params.w2_self, u=self.bwd.forward(ds2, ex, "sum"), act=h1)

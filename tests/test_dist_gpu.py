@@ -1,0 +1,181 @@
+"""The row-partitioned SAGE trainer (csrc/dist.cu, sgnn_dist_* / dist.py):
+one rank against the reference's own training runs and bitwise against the
+single-GPU native engine; P loopback ranks (the partition + exchange logic on
+one GPU) against one rank and against the reference, for symmetric and
+non-symmetric graphs; errors.  SURVEY 8e; train() = gnn.hpp:414-438."""
+import numpy as np
+import pytest
+
+from conftest import load_golden, rand_csr
+
+pytestmark = pytest.mark.gpu
+
+HIDDEN, CLASSES, LR, EPOCHS = 32, 4, 0.05, 30
+
+
+def _golden():
+    g = load_golden("gnn_planted")
+    return g, g["row_ptr"], g["col_idx"], g["values"], g["x"], g["labels"], g["mask"]
+
+
+def _split(w0, f, h, c):
+    o, out = 0, []
+    for r, cc in ((f, h), (h, c), (f, h), (h, c)):
+        out.append(np.ascontiguousarray(w0[o:o + r * cc].reshape(r, cc)))
+        o += r * cc
+    return out
+
+
+def _run(comm_p, rp, ci, v, x, lab, mask, kind, w0, epochs, row_weight=30, symmetric=None):
+    from paper_2403_14853_b200 import dist
+    f = x.shape[1]
+    ws = _split(w0, f, HIDDEN, CLASSES)
+    if comm_p == 1:
+        eng = dist.DistSage.from_graph(None, rp, ci, v, x, lab, mask, HIDDEN, CLASSES, kind, max_epochs=epochs,
+                                       symmetric=symmetric)
+        eng.set_weights(*ws)
+        eng.epochs(epochs, LR)
+        loss, acc, times = eng.stats()
+        return loss, acc, [t.cpu().numpy() for t in eng.get_weights()], times, [eng]
+    comm = dist.Comm.loopback(comm_p)
+    bounds = dist.row_partition(rp, comm_p, row_weight)
+    engs = [dist.DistSage.from_graph(comm, rp, ci, v, x, lab, mask, HIDDEN, CLASSES, kind, rank=r, bounds=bounds,
+                                     max_epochs=epochs, symmetric=symmetric) for r in range(comm_p)]
+    for e in engs:
+        e.set_weights(*ws)
+    dist.DistSage.epochs_group(engs, epochs, LR)
+    loss, acc, times = engs[0].stats()
+    wts = [t.cpu().numpy() for t in engs[0].get_weights()]
+    for e in engs[1:]:  # every rank holds the same all-reduced weights
+        for a, b in zip(wts, e.get_weights()):
+            np.testing.assert_array_equal(a.view(np.uint32), b.cpu().numpy().view(np.uint32))
+        np.testing.assert_array_equal(e.stats()[0], loss)
+    engs_keep = engs + [comm]
+    return loss, acc, wts, times, engs_keep
+
+
+@pytest.mark.parametrize("kind", ["sage-sum", "sage-mean"])
+def test_one_rank_matches_reference_training(cuda, kind):
+    g, rp, ci, v, x, lab, mask = _golden()
+    loss, acc, _, times, _ = _run(1, rp, ci, v, x, lab, mask, kind, g[f"{kind}_w0"], EPOCHS)
+    np.testing.assert_allclose(loss, g[f"{kind}_losses"], rtol=2e-3, atol=1e-4)
+    assert abs(acc[-1] - g[f"{kind}_accs"][-1]) <= 0.02
+    assert (times[:, 0] > 0).all() and (times[:, 1] > 0).all() and (times[:, 3] >= 0).all()
+
+
+@pytest.mark.parametrize("kind", ["sage-sum", "sage-mean"])
+def test_one_rank_weights_bitwise_native_engine(cuda, kind):
+    """The trainer at one rank runs the native engine's kernels in the same
+    order: final weights bit-identical to gnn.train_native's."""
+    import torch
+
+    from paper_2403_14853_b200 import gnn, ops
+    g, rp, ci, v, x, lab, mask = _golden()
+    loss, _, wts, _, _ = _run(1, rp, ci, v, x, lab, mask, kind, g[f"{kind}_w0"], 12)
+    m = gnn.model_from_flat(kind, x.shape[1], HIDDEN, CLASSES, g[f"{kind}_w0"])
+    a = ops.CsrMatrix.from_numpy(rp, ci, v, len(rp) - 1)
+    nat = gnn.train_native(m, a, torch.from_numpy(x).cuda(), torch.from_numpy(lab.astype(np.int64)).cuda(),
+                           torch.from_numpy(mask).cuda(), epochs=12, lr=LR)
+    for got, want in zip(wts, (m.w1, m.w2, m.w1_self, m.w2_self)):
+        np.testing.assert_array_equal(got.view(np.uint32), want.cpu().numpy().view(np.uint32))
+    np.testing.assert_allclose(loss, [s.loss for s in nat.stats], rtol=1e-12)
+
+
+@pytest.mark.parametrize("parts", [2, 3, 5])
+@pytest.mark.parametrize("kind", ["sage-sum", "sage-mean"])
+def test_loopback_partition_matches_one_rank(cuda, parts, kind):
+    """P virtual ranks: every SpMM row is bitwise the 1-GPU one, the weight
+    gradients are sums of per-rank partials (fp32 reassociation only)."""
+    g, rp, ci, v, x, lab, mask = _golden()
+    l1, a1, w1, _, _ = _run(1, rp, ci, v, x, lab, mask, kind, g[f"{kind}_w0"], 10)
+    lp, ap, wp, times, _ = _run(parts, rp, ci, v, x, lab, mask, kind, g[f"{kind}_w0"], 10, row_weight=1)
+    np.testing.assert_allclose(lp, l1, rtol=1e-5)
+    for a, b in zip(wp, w1):
+        np.testing.assert_allclose(a, b, rtol=1e-4, atol=1e-6)
+    np.testing.assert_allclose(lp, g[f"{kind}_losses"][:10], rtol=2e-3, atol=1e-4)
+    assert (times[:, 3] > 0).all()  # the exchanges ran
+
+
+def test_loopback_empty_rank_and_weighted_partition(cuda):
+    """More ranks than the graph's balance needs (an empty row block) and
+    the nnz + 30 rows cost: still the reference's losses."""
+    from paper_2403_14853_b200 import dist
+    g, rp, ci, v, x, lab, mask = _golden()
+    n = len(rp) - 1
+    bounds = np.array([0, 0, 150, n, n], np.uint32)  # ranks 0 and 3 own no rows
+    comm = dist.Comm.loopback(4)
+    ws = _split(g["sage-mean_w0"], x.shape[1], HIDDEN, CLASSES)
+    engs = [dist.DistSage.from_graph(comm, rp, ci, v, x, lab, mask, HIDDEN, CLASSES, "sage-mean", rank=r,
+                                     bounds=bounds, max_epochs=8) for r in range(4)]
+    for e in engs:
+        e.set_weights(*ws)
+    dist.DistSage.epochs_group(engs, 8, LR)
+    np.testing.assert_allclose(engs[2].stats()[0], g["sage-mean_losses"][:8], rtol=2e-3, atol=1e-4)
+    assert engs[0].rows == 0 and engs[3].rows == 0 and engs[0].n_masked == int(mask.sum())
+
+
+@pytest.mark.parametrize("parts", [1, 3])
+def test_non_symmetric_graph_uses_transpose_block(cuda, parts):
+    """A non-symmetric A: the backward operand is rows of A^T (mean: scaled
+    by 1/deg of the column on the device), gnn.hpp:127-172; losses match the
+    reference's train() on the same graph (oracle/_ref)."""
+    from oracle import ref
+    rng = np.random.default_rng(11)
+    n, f = 300, 16
+    rp, ci, v = rand_csr(rng, n, n, 0.03, hub_rows=(2,), value="positive")
+    x = rng.normal(0, 1, (n, f)).astype(np.float32)
+    lab = rng.integers(0, CLASSES, n).astype(np.uint32)
+    mask = (rng.random(n) < 0.7).astype(np.uint8)
+    w0 = ref.init_model("sage-mean", f, HIDDEN, CLASSES, 5)
+    want, _, _, _ = ref.train("sage-mean", rp, ci, v, x, lab, mask, HIDDEN, CLASSES, w0, 10, LR)
+    loss, _, _, _, _ = _run(parts, rp, ci, v, x, lab, mask, "sage-mean", w0, 10, row_weight=1)
+    np.testing.assert_allclose(loss, want, rtol=2e-3, atol=1e-4)
+
+
+def test_set_features_borrow_and_copy(cuda):
+    """New features mid-training: borrowed in place (1 rank) or copied and
+    re-gathered (loopback) give the same epochs as a fresh engine."""
+    import torch
+
+    from paper_2403_14853_b200 import dist
+    g, rp, ci, v, x, lab, mask = _golden()
+    x2 = (x * 0.5 + 0.1).astype(np.float32)
+    w0 = g["sage-mean_w0"]
+    ref_loss, _, _, _, _ = _run(1, rp, ci, v, x2, lab, mask, "sage-mean", w0, 4)
+    eng = dist.DistSage.from_graph(None, rp, ci, v, x, lab, mask, HIDDEN, CLASSES, "sage-mean", max_epochs=8)
+    eng.set_weights(*_split(w0, x.shape[1], HIDDEN, CLASSES))
+    xt = torch.from_numpy(x2).cuda()
+    eng.set_features(xt, borrow=True)
+    eng.epochs(4, LR)
+    np.testing.assert_array_equal(eng.stats()[0], ref_loss)
+    comm = dist.Comm.loopback(2)
+    b = dist.row_partition(rp, 2, 1)
+    engs = [dist.DistSage.from_graph(comm, rp, ci, v, x, lab, mask, HIDDEN, CLASSES, "sage-mean", rank=r, bounds=b,
+                                     max_epochs=8) for r in range(2)]
+    for e in engs:
+        e.set_weights(*_split(w0, x.shape[1], HIDDEN, CLASSES))
+        e.set_features(torch.from_numpy(x2[e.r0:e.r0 + e.rows]).cuda())
+    dist.DistSage.epochs_group(engs, 4, LR)
+    np.testing.assert_allclose(engs[0].stats()[0], ref_loss, rtol=1e-5)
+
+
+def test_errors(cuda):
+    from paper_2403_14853_b200 import _lib, dist, ops
+    g, rp, ci, v, x, lab, mask = _golden()
+    n = len(rp) - 1
+    with pytest.raises(_lib.UnsupportedError):
+        dist.DistSage.from_graph(None, rp, ci, v, x, lab, mask, HIDDEN, CLASSES, "gcn")
+    bad = lab.copy()
+    bad[3] = CLASSES
+    with pytest.raises(ops.ConfigError, match="out of range"):
+        dist.DistSage.from_graph(None, rp, ci, v, x, bad, mask, HIDDEN, CLASSES, "sage-mean")
+    comm = dist.Comm.loopback(2)
+    with pytest.raises(ops.ConfigError):  # non-monotone bounds
+        dist.DistSage.from_graph(comm, rp, ci, v, x, lab, mask, HIDDEN, CLASSES, "sage-mean", rank=0,
+                                 bounds=np.array([0, n, n - 5], np.uint32))
+    e0 = dist.DistSage.from_graph(comm, rp, ci, v, x, lab, mask, HIDDEN, CLASSES, "sage-mean", rank=0,
+                                  bounds=dist.row_partition(rp, 2, 1), max_epochs=2)
+    with pytest.raises(ops.ConfigError):  # loopback needs all ranks
+        e0.epochs(1, LR)
+    with pytest.raises(ops.ConfigError):
+        e0.stats(0, 1)  # not run yet

@@ -29,12 +29,14 @@ def _oracle_compute(local, gathered, reduce):
 
 
 def test_partition_blocks_cover_and_remap():
+    """Padded owner layout (the peer path): blocks cover the graph, the remap
+    is invertible and keeps every row strictly increasing."""
     from paper_2403_14853_b200 import partition
     rng = np.random.default_rng(0)
     n = 500
     rp, ci, v = rand_csr(rng, n, n, 0.02, hub_rows=(0, 7), empty_frac=0.1)
     for parts in (1, 2, 3, 8):
-        pt = partition.make_partition(rp, parts)
+        pt = partition.make_partition(rp, parts, padded=True)
         np.testing.assert_array_equal(pt.bounds, port.balanced_row_partition(rp, parts))
         assert pt.stride >= max(np.diff(pt.bounds.astype(np.int64)))
         total = 0
@@ -53,28 +55,66 @@ def test_partition_blocks_cover_and_remap():
         assert total == len(ci)
 
 
-def _worker(rank, world, port_, rp, ci, v, x, reduce, q):
+def test_unpadded_partition_keeps_global_columns():
+    """Default (all-gather-v) layout: no padding, blocks are plain row slices
+    with global column ids; the gathered operand has exactly n rows."""
+    from paper_2403_14853_b200 import partition
+    rng = np.random.default_rng(1)
+    n = 700
+    rp, ci, v = rand_csr(rng, n, n, 0.02, hub_rows=(0, 3), empty_frac=0.1)
+    for parts in (1, 2, 5, 8):
+        for w in (1, 30):
+            pt = partition.make_partition(rp, parts, row_weight=w)
+            assert not pt.padded and pt.n_gathered == n
+            if w == 1:
+                np.testing.assert_array_equal(pt.bounds, port.balanced_row_partition(rp, parts))
+            cat = [pt.block(rp, ci, v, p) for p in range(parts)]
+            np.testing.assert_array_equal(np.concatenate([c[1] for c in cat]), ci)
+            np.testing.assert_array_equal(np.concatenate([c[2] for c in cat]), v)
+            for p, (lrp, _, _) in enumerate(cat):
+                r0, r1 = pt.rows(p)
+                np.testing.assert_array_equal(lrp, rp[r0:r1 + 1] - rp[r0])
+
+
+@pytest.mark.parametrize("parts", [2, 3, 4, 8])
+def test_weighted_row_partition_balances_cost(parts):
+    """sgnn_host_weighted_row_partition: w = 1 is balanced_row_partition
+    exactly; any w gives contiguous blocks whose cost nnz + w*rows is within
+    one row's cost of the even share."""
+    from paper_2403_14853_b200 import dist, graphs
+    rp, _ = graphs.rmat(13, (1 << 13) * 20, seed=2, symmetrize=True, self_loops=True)
+    np.testing.assert_array_equal(dist.row_partition(rp, parts, 1), port.balanced_row_partition(rp, parts))
+    for w in (1, 7, 30, 1000):
+        b = dist.row_partition(rp, parts, w).astype(np.int64)
+        assert b[0] == 0 and b[-1] == len(rp) - 1 and (np.diff(b) >= 0).all()
+        cost = rp.astype(np.int64) + w * np.arange(len(rp))
+        total = int(cost[-1])
+        for c in range(1, parts):
+            target = total * c // parts
+            assert cost[b[c]] >= target and (b[c] == 0 or cost[b[c] - 1] < target)
+
+
+def _worker(rank, world, port_, rp, ci, v, x, reduce, q, row_weight=1):
     import torch
     import torch.distributed as dist
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port_))
     dist.init_process_group("gloo", rank=rank, world_size=world)
     try:
         from paper_2403_14853_b200 import partition
-        pt = partition.make_partition(rp, world)
+        pt = partition.make_partition(rp, world, row_weight=row_weight)
         ps = partition.PartitionedSpmm(rp, ci, v, pt, rank, x.shape[1], device="cpu", compute=_oracle_compute)
         r0, r1 = pt.rows(rank)
         c_local = ps.forward(torch.from_numpy(x[r0:r1].copy()), partition.NcclExchange(), reduce)
-        # reassemble on every rank through the same padded all-gather
-        full = partition.NcclExchange().all_gather(partition.pad_block(c_local, pt.stride))
+        # reassemble on every rank through the same all-gather-v (uneven blocks)
+        full = partition.NcclExchange().all_gather_v(c_local, pt.bounds)
         if rank == 0:
-            rows = [full[p * pt.stride: p * pt.stride + (pt.rows(p)[1] - pt.rows(p)[0])] for p in range(world)]
-            q.put(torch.cat(rows).numpy())
+            q.put(full.numpy())
     finally:
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("reduce", ["sum", "mean", "max"])
-def test_two_rank_gloo_matches_single_process(reduce):
+@pytest.mark.parametrize("reduce,world,row_weight", [("sum", 2, 1), ("mean", 2, 30), ("max", 2, 1), ("sum", 3, 30)])
+def test_two_rank_gloo_matches_single_process(reduce, world, row_weight):
     import torch.multiprocessing as mp
     rng = np.random.default_rng(3)
     n = 400
@@ -83,7 +123,8 @@ def test_two_rank_gloo_matches_single_process(reduce):
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port_ = _free_port()
-    procs = [ctx.Process(target=_worker, args=(r, 2, port_, rp, ci, v, x, reduce, q)) for r in range(2)]
+    procs = [ctx.Process(target=_worker, args=(r, world, port_, rp, ci, v, x, reduce, q, row_weight))
+             for r in range(world)]
     for p in procs:
         p.start()
     got = q.get(timeout=120)
