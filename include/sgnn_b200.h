@@ -197,6 +197,14 @@ sgnn_status sgnn_ipc_get_handle(void* dev_ptr, void* handle64);
 sgnn_status sgnn_ipc_open_handle(const void* handle64, void** dev_ptr);
 sgnn_status sgnn_ipc_close_handle(void* dev_ptr);
 
+/* Built-in self-test of the mean epilogue's division (the exact
+ * reciprocal-and-round path that replaces __fdiv_rn inside the SpMM kernels,
+ * kernels.hpp:60-63): every degree in [d0, d1) x `samples` values (specials,
+ * random bit patterns over all exponents) compared bitwise with IEEE
+ * division.  *mismatches = 0 on success.  Synchronous. */
+sgnn_status sgnn_selftest_count_division(uint64_t d0, uint64_t d1, uint32_t samples, uint64_t seed,
+                                         uint64_t* mismatches, uint64_t* first_deg, uint32_t* first_sample);
+
 /* ------------------------------------------------------------- transpose */
 /* transpose(a) (sparse.hpp:72-89): CSR(A) -> CSR(A^T), bit-exact with the
  * reference's stable counting sort (rows ascending within each column).

@@ -116,6 +116,7 @@ SIGNATURES = {
     "sgnn_resolve_kernel": (i32, [u32, i32, C.POINTER(u32)]),
     "sgnn_set_dispatch": (None, [i32]),
     "sgnn_get_dispatch": (i32, []),
+    "sgnn_selftest_count_division": (i32, [u64, u64, u32, u64, C.POINTER(u64), C.POINTER(u64), C.POINTER(u32)]),
     "sgnn_transpose_workspace": (i32, [CsrP, C.POINTER(C.c_size_t)]),
     "sgnn_csr_transpose": (i32, [CsrP, P, P, P, P, C.c_size_t, P]),
     "sgnn_row_degrees": (i32, [CsrP, P, P]),

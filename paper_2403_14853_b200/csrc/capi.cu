@@ -2,6 +2,7 @@
 // capi.cu -- the extern "C" boundary (include/sgnn_b200.h).  Validation and
 // error messages follow the reference operator API (kernels.hpp:131-173).
 #include <atomic>
+#include <initializer_list>
 #include <cstring>
 #include <new>
 
@@ -34,6 +35,13 @@ const char* reduce_name(int r) {
 }
 
 cudaStream_t cs(sgnn_stream s) { return reinterpret_cast<cudaStream_t>(s); }
+
+// the glue passes issue float4 loads: every (non-null) array 16-byte aligned
+bool aligned16(std::initializer_list<const void*> ps) {
+    for (const void* p : ps)
+        if (reinterpret_cast<uintptr_t>(p) % 16) return false;
+    return true;
+}
 
 sgnn_status spmm_shapes(const sgnn_csr* a, uint32_t x_rows, uint32_t k) {
     if (a->n_cols != x_rows)  // check_spmm_shapes, kernels.hpp:131-136
@@ -423,6 +431,12 @@ sgnn_status sgnn_gnn_destroy(sgnn_gnn g) {
     return SGNN_OK;
 }
 
+sgnn_status sgnn_selftest_count_division(uint64_t d0, uint64_t d1, uint32_t samples, uint64_t seed,
+                                         uint64_t* mismatches, uint64_t* first_deg, uint32_t* first_sample) {
+    if (!mismatches) return fail(SGNN_ERR_CONFIG, "selftest: null out");
+    return selftest_count_division(d0, d1, samples, seed, mismatches, first_deg, first_sample);
+}
+
 // ---------------------------------------------------- dense FP32 products
 sgnn_status sgnn_dense_mm_f32(int op, uint32_t m, uint32_t n, uint32_t k, const float* a, const float* b, float* c,
                               sgnn_stream stream) {
@@ -433,17 +447,16 @@ sgnn_status sgnn_dense_mm_f32(int op, uint32_t m, uint32_t n, uint32_t k, const 
     if (k % 4 || n % 4 || !al(a) || !al(b) || !al(c) || m > 0x7fffffffu)
         return fail(SGNN_ERR_UNSUPPORTED, "dense_mm: needs 16-byte aligned rows (k, n multiples of 4)");
     const cudaStream_t s = cs(stream);
+    const int splits = int(std::max<uint32_t>(1, std::min<uint32_t>(148, m / 8192)));
+    size_t ws_bytes = 0;  // exactly what the kernel asks for this shape
+    int rc = op == 0 ? dense_mm_nn_workspace(int(m), int(n), int(k), &ws_bytes)
+                     : dense_mm_tn_workspace(int(m), int(n), int(k), splits, &ws_bytes);
+    if (rc) return fail(SGNN_ERR_UNSUPPORTED, "dense_mm: the tensor-core kernel refused this shape (" + std::to_string(rc) + ")");
     void* ws = nullptr;
-    const size_t ws_bytes = size_t(4) << 20;
-    SGNN_TRY(scratch_alloc(&ws, ws_bytes, s));
-    int rc = 0;
-    if (op == 0) {
-        rc = dense_mm_nn(int(m), int(n), int(k), a, b, c, 0.0f, ws, ws_bytes, s);
-    } else {
-        const int splits = int(std::max<uint32_t>(1, std::min<uint32_t>(148, m / 8192)));
-        rc = dense_mm_tn(int(m), int(n), int(k), a, b, c, splits, ws, ws_bytes, s);
-    }
-    scratch_free(ws, s);
+    if (ws_bytes) SGNN_TRY(scratch_alloc(&ws, ws_bytes, s));
+    rc = op == 0 ? dense_mm_nn(int(m), int(n), int(k), a, b, c, 0.0f, ws, ws_bytes, s)
+                 : dense_mm_tn(int(m), int(n), int(k), a, b, c, splits, ws, ws_bytes, s);
+    if (ws) scratch_free(ws, s);
     if (rc) return fail(SGNN_ERR_UNSUPPORTED, "dense_mm: the tensor-core kernel refused this shape (" + std::to_string(rc) + ")");
     SGNN_LAUNCH_CHECK();
     return SGNN_OK;
@@ -452,12 +465,14 @@ sgnn_status sgnn_dense_mm_f32(int op, uint32_t m, uint32_t n, uint32_t k, const 
 // ---------------------------------------------------------- SAGE glue
 sgnn_status sgnn_add_relu_f32(const float* a, const float* b, uint64_t n, float* h, sgnn_stream stream) {
     if (n && (!a || !b || !h)) return fail(SGNN_ERR_CONFIG, "add_relu: null array");
+    if (!aligned16({a, b, h})) return fail(SGNN_ERR_UNSUPPORTED, "add_relu: arrays must be 16-byte aligned");
     return glue_add_relu(a, b, n, h, cs(stream));
 }
 
 sgnn_status sgnn_sage_logits_f32(const float* a2, const float* h1, const float* w2, const float* w2s, uint32_t n,
                                  uint32_t hidden, uint32_t classes, float* logits, sgnn_stream stream) {
     if (n && (!a2 || !h1 || !w2 || !w2s || !logits)) return fail(SGNN_ERR_CONFIG, "sage_logits: null array");
+    if (!aligned16({a2, h1})) return fail(SGNN_ERR_UNSUPPORTED, "sage_logits: a2 / h1 must be 16-byte aligned");
     return glue_sage_logits(a2, h1, w2, w2s, n, hidden, classes, logits, cs(stream));
 }
 
@@ -472,12 +487,14 @@ sgnn_status sgnn_softmax_xent_f32(const float* logits, uint32_t n, uint32_t clas
 sgnn_status sgnn_sage_wgrad_f32(const float* a2, const float* h1, const float* grad, uint32_t n, uint32_t hidden,
                                 uint32_t classes, float* g2, float* g2s, sgnn_stream stream) {
     if (!g2 || !g2s || (n && (!a2 || !h1 || !grad))) return fail(SGNN_ERR_CONFIG, "sage_wgrad: null array");
+    if (!aligned16({a2, h1, grad})) return fail(SGNN_ERR_UNSUPPORTED, "sage_wgrad: arrays must be 16-byte aligned");
     return glue_sage_wgrad(a2, h1, grad, n, hidden, classes, g2, g2s, cs(stream));
 }
 
 sgnn_status sgnn_sage_grad_wt_f32(const float* grad, const float* w, uint32_t n, uint32_t hidden, uint32_t classes,
                                   const float* u, const float* act, float* out, sgnn_stream stream) {
     if (n && (!grad || !w || !out)) return fail(SGNN_ERR_CONFIG, "sage_grad_wt: null array");
+    if (!aligned16({grad, u, act, out})) return fail(SGNN_ERR_UNSUPPORTED, "sage_grad_wt: arrays must be 16-byte aligned");
     return glue_sage_grad_wt(grad, w, n, hidden, classes, u, act, out, cs(stream));
 }
 

@@ -46,9 +46,11 @@ using ClusterShape = Shape<_1, _1, _1>;
 
 // C[m x n] (row-major) = A' B' + beta C with A' m x k, B' k x n in the
 // kernel's layouts; splits > 1: deterministic split-K.  0 on success.
+// ws == nullptr && ws_bytes == 0: only query -- *ws_needed gets the
+// workspace size (return 1 when the kernel cannot take the shape).
 template <class Gemm, bool SPLITK>
 int run_gemm(int m, int n, int k, const float* a, const float* b, float* c, float beta, int splits, void* ws,
-             size_t ws_bytes, cudaStream_t s) {
+             size_t ws_bytes, cudaStream_t s, size_t* ws_needed = nullptr) {
     using Kernel = typename Gemm::GemmKernel;
     using SA = typename Kernel::StrideA;
     using SB = typename Kernel::StrideB;
@@ -67,6 +69,10 @@ int run_gemm(int m, int n, int k, const float* a, const float* b, float* c, floa
     }
     Gemm gemm;
     if (gemm.can_implement(args) != cutlass::Status::kSuccess) return 1;
+    if (ws_needed) {
+        *ws_needed = Gemm::get_workspace_size(args);
+        if (!ws && !ws_bytes) return 0;
+    }
     if (Gemm::get_workspace_size(args) > ws_bytes) return 2;
     if (gemm.initialize(args, ws, s) != cutlass::Status::kSuccess) return 3;
     if (gemm.run(s) != cutlass::Status::kSuccess) return 4;

@@ -15,4 +15,7 @@ int dense_mm_nn(int m, int n, int k, const float* a, const float* b, float* c, f
                 cudaStream_t s) {
     return dense::run_gemm<SgnnGemmNN, false>(m, n, k, a, b, c, beta, 1, ws, ws_bytes, s);
 }
+int dense_mm_nn_workspace(int m, int n, int k, size_t* bytes) {
+    return dense::run_gemm<SgnnGemmNN, false>(m, n, k, nullptr, nullptr, nullptr, 0.0f, 1, nullptr, 0, nullptr, bytes);
+}
 }  // namespace sgnn

@@ -11,4 +11,8 @@ int dense_mm_tn(int m, int n, int k, const float* a, const float* b, float* c, i
                 cudaStream_t s) {
     return dense::run_gemm<SgnnGemmTN, true>(k, n, m, a, b, c, 0.0f, splits, ws, ws_bytes, s);
 }
+int dense_mm_tn_workspace(int m, int n, int k, int splits, size_t* bytes) {
+    return dense::run_gemm<SgnnGemmTN, true>(k, n, m, nullptr, nullptr, nullptr, 0.0f, splits, nullptr, 0, nullptr,
+                                             bytes);
+}
 }  // namespace sgnn

@@ -37,6 +37,8 @@ sgnn_status run_spmm_peer(const sgnn_csr* a, const float* const* parts, uint32_t
 sgnn_status run_mean_divide(const uint64_t* rp, uint32_t m, float* c, uint64_t ldc, uint32_t k,
                             cudaStream_t s);
 
+sgnn_status selftest_count_division(uint64_t d0, uint64_t d1, uint32_t samples, uint64_t seed, uint64_t* mismatches,
+                                    uint64_t* first_deg, uint32_t* first_bits);
 sgnn_status run_transpose(const sgnn_csr* a, uint64_t* trp, uint32_t* tci, float* tv, void* ws,
                           size_t ws_bytes, cudaStream_t s);
 size_t transpose_workspace_bytes(const sgnn_csr* a);
@@ -74,6 +76,9 @@ int dense_mm_nn(int m, int n, int k, const float* a, const float* b, float* c, f
                 cudaStream_t s);
 int dense_mm_tn(int m, int n, int k, const float* a, const float* b, float* c, int splits, void* ws, size_t ws_bytes,
                 cudaStream_t s);
+// workspace bytes the products need for this shape (nonzero return: shape refused)
+int dense_mm_nn_workspace(int m, int n, int k, size_t* bytes);
+int dense_mm_tn_workspace(int m, int n, int k, int splits, size_t* bytes);
 // SAGE layer glue (gnn.cu), see sgnn_b200.h
 sgnn_status glue_add_relu(const float* a, const float* b, uint64_t n, float* h, cudaStream_t s);
 sgnn_status glue_sage_logits(const float* a2, const float* h1, const float* w2, const float* w2s, uint32_t n,

@@ -1,10 +1,10 @@
 // spmm.cu -- host driver of the SpMM worker + fixup kernels (K-tile passes),
 // and the Mean epilogue.
 //
-// Mean (kernels.hpp:60-63) is the Sum kernels followed by one divide pass
-// over C: the IEEE-exact division (__fdiv_rn) carries a slow-path subroutine
-// call whose register cost would otherwise be paid inside the gather loop.
-// The quotient is the same: (canonical sum) / deg.
+// Mean (kernels.hpp:60-63): the mean kernels divide by the row's nonzero
+// count where the row is stored (dev::div_by_count, bit-identical to
+// __fdiv_rn without its slow-path call); layouts without a mean kernel, the
+// peer path and FusedMM run the Sum kernels and one divide pass over C.
 #include <algorithm>
 
 #include "ops.cuh"
@@ -43,6 +43,58 @@ __global__ void __launch_bounds__(256) mean_divide_kernel(const uint64_t* __rest
 
 }  // namespace
 
+// Self-test of the mean epilogue's division (dev::div_by_count) against
+// __fdiv_rn: degrees [d0, d1) x `samples` values per degree (a counter-hashed
+// mix of random bit patterns -- every exponent, subnormals, signs -- and the
+// specials 0, -0, +-inf, NaN, +-FLT_MAX, +-FLT_MIN, +-denorm_min).
+__global__ void count_division_check_kernel(uint64_t d0, uint64_t d1, uint32_t samples, uint64_t seed,
+                                            unsigned long long* bad, unsigned long long* first_bad) {
+    const uint64_t n = (d1 - d0) * samples;
+    for (uint64_t t = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; t < n; t += uint64_t(gridDim.x) * blockDim.x) {
+        const uint64_t deg = d0 + t / samples;
+        const uint32_t j = uint32_t(t % samples);
+        uint32_t bits;
+        constexpr uint32_t kSpecial[] = {0x00000000u, 0x80000000u, 0x7f800000u, 0xff800000u, 0x7fc00000u,
+                                         0x7f7fffffu, 0xff7fffffu, 0x00800000u, 0x80800000u, 0x00000001u,
+                                         0x80000001u, 0x3f800000u, 0x007fffffu};
+        if (j < sizeof(kSpecial) / sizeof(kSpecial[0])) {
+            bits = kSpecial[j];
+        } else {
+            uint64_t z = seed + t * 0x9E3779B97F4A7C15ull;
+            z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+            z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+            z ^= z >> 31;
+            bits = uint32_t(z);
+            if (j & 1) bits = (bits & 0x807fffffu) | (uint32_t(96 + (z >> 40) % 64) << 23);  // |v| ~ 2^-31..2^32
+        }
+        const float v = __uint_as_float(bits);
+        const float want = __fdiv_rn(v, float(deg));
+        const float got = dev::div_by_count(v, dev::recip_count(deg));
+        const bool same = __float_as_uint(want) == __float_as_uint(got) || (want != want && got != got);
+        if (!same) {
+            atomicAdd(bad, 1ull);
+            atomicMin(first_bad, (unsigned long long)t);
+        }
+    }
+}
+
+sgnn_status selftest_count_division(uint64_t d0, uint64_t d1, uint32_t samples, uint64_t seed, uint64_t* mismatches,
+                                    uint64_t* first_deg, uint32_t* first_bits) {
+    if (d0 == 0 || d1 <= d0 || samples == 0) return fail(SGNN_ERR_CONFIG, "selftest: need 0 < d0 < d1, samples > 0");
+    unsigned long long* buf = nullptr;
+    SGNN_CUDA_TRY(cudaMalloc(&buf, 2 * sizeof(unsigned long long)));
+    unsigned long long h[2] = {0ull, ~0ull};
+    cudaMemcpy(buf, h, sizeof(h), cudaMemcpyHostToDevice);
+    count_division_check_kernel<<<148 * 16, 256>>>(d0, d1, samples, seed, buf, buf + 1);
+    const cudaError_t e = cudaMemcpy(h, buf, sizeof(h), cudaMemcpyDeviceToHost);
+    cudaFree(buf);
+    if (e != cudaSuccess) return fail(SGNN_ERR_CUDA, std::string("selftest: ") + cudaGetErrorString(e));
+    *mismatches = h[0];
+    if (first_deg) *first_deg = h[0] ? d0 + h[1] / samples : 0;
+    if (first_bits) *first_bits = h[0] ? uint32_t(h[1] % samples) : 0;
+    return SGNN_OK;
+}
+
 sgnn_status run_mean_divide(const uint64_t* rp, uint32_t m, float* c, uint64_t ldc, uint32_t k,
                             cudaStream_t s) {
     if (m == 0 || k == 0) return SGNN_OK;
@@ -57,8 +109,8 @@ sgnn_status run_mean_divide(const uint64_t* rp, uint32_t m, float* c, uint64_t l
 
 SpmmLauncher find_spmm_launcher(bool vec, int lanes, int vregs, int unroll, int reduce, int occ) {
     switch (reduce) {
-        case SGNN_REDUCE_SUM:
-        case SGNN_REDUCE_MEAN: return spmm_lookup_sum(vec, lanes, vregs, unroll, occ);
+        case SGNN_REDUCE_SUM: return spmm_lookup_sum(vec, lanes, vregs, unroll, occ);
+        case SGNN_REDUCE_MEAN: return spmm_lookup_mean(vec, lanes, vregs, unroll, occ);
         case SGNN_REDUCE_MIN: return spmm_lookup_min(vec, lanes, vregs, unroll, occ);
         case SGNN_REDUCE_MAX: return spmm_lookup_max(vec, lanes, vregs, unroll, occ);
     }
@@ -67,8 +119,8 @@ SpmmLauncher find_spmm_launcher(bool vec, int lanes, int vregs, int unroll, int 
 
 sgnn_status launch_spmm_fixup(const FixupArgs& f, int reduce, cudaStream_t s) {
     switch (reduce) {
-        case SGNN_REDUCE_SUM:
-        case SGNN_REDUCE_MEAN: return spmm_lookup_sum_fixup(f, s);
+        case SGNN_REDUCE_SUM: return spmm_lookup_sum_fixup(f, s);
+        case SGNN_REDUCE_MEAN: return spmm_lookup_mean_fixup(f, s);
         case SGNN_REDUCE_MIN: return spmm_lookup_min_fixup(f, s);
         case SGNN_REDUCE_MAX: return spmm_lookup_max_fixup(f, s);
     }
@@ -98,6 +150,14 @@ sgnn_status run_spmm(const sgnn_csr* a, const float* x, uint32_t k, float* c, in
     const int occ = vec ? int(plan->p.occupancy) : 1;
     SpmmLauncher launch = find_spmm_launcher(vec, lanes, vregs, unroll, reduce, occ);
     if (!launch && occ > 1) launch = find_spmm_launcher(vec, lanes, vregs, unroll, reduce, 1);
+    // mean: the divide happens in the row epilogue of the mean kernels; a
+    // layout without one runs the sum kernels and the divide pass
+    int kred = reduce;
+    if (!launch && reduce == SGNN_REDUCE_MEAN) {
+        kred = SGNN_REDUCE_SUM;
+        launch = find_spmm_launcher(vec, lanes, vregs, unroll, kred, occ);
+        if (!launch && occ > 1) launch = find_spmm_launcher(vec, lanes, vregs, unroll, kred, 1);
+    }
     if (!launch)
         return fail(SGNN_ERR_UNSUPPORTED, "spmm: no kernel compiled for lanes=" +
                                               std::to_string(lanes) + " vec=" +
@@ -140,10 +200,10 @@ sgnn_status run_spmm(const sgnn_csr* a, const float* x, uint32_t k, float* c, in
             f.ld_slot = plan->kt;
             f.n_fix = plan->n_fix;
             f.width = kp;
-            SGNN_TRY(launch_spmm_fixup(f, reduce, s));
+            SGNN_TRY(launch_spmm_fixup(f, kred, s));
         }
     }
-    if (reduce == SGNN_REDUCE_MEAN) SGNN_TRY(run_mean_divide(a->row_ptr, a->n_rows, c, k, k, s));
+    if (reduce == SGNN_REDUCE_MEAN && kred != reduce) SGNN_TRY(run_mean_divide(a->row_ptr, a->n_rows, c, k, k, s));
     return SGNN_OK;
 }
 

@@ -190,8 +190,11 @@ sgnn_status launch_spmm_worker(const SpmmArgs& a, uint32_t block, uint32_t max_b
         return nullptr;                                                               \
     }
 
-// Mean runs the Sum kernels plus run_mean_divide (spmm.cu).
+// Mean has kernels of its own (the divide in the row epilogue); layouts
+// without one run the Sum kernels plus run_mean_divide (spmm.cu).
 SpmmLauncher spmm_lookup_sum(bool, int, int, int, int);
+SpmmLauncher spmm_lookup_mean(bool, int, int, int, int);
+sgnn_status spmm_lookup_mean_fixup(const FixupArgs&, cudaStream_t);
 SpmmLauncher spmm_peer_lookup_sum(bool, int, int, int, int);
 SpmmLauncher spmm_lookup_min(bool, int, int, int, int);
 SpmmLauncher spmm_lookup_max(bool, int, int, int, int);

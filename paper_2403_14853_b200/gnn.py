@@ -397,15 +397,31 @@ def dense_mm(a: torch.Tensor, b: torch.Tensor, transpose_a: bool = False) -> tor
     FP32 emulation (sgnn_dense_mm_f32); shapes the kernels do not take
     (unaligned rows, short matrices) use torch's matmul on the same GPU."""
     from ._lib import lib
+    if a.dim() != 2 or b.dim() != 2:
+        raise ops.ShapeError(f"dense_mm: expected 2-D operands, got {tuple(a.shape)} and {tuple(b.shape)}")
+    inner = a.shape[0] if transpose_a else a.shape[1]
+    if b.shape[0] != inner:
+        raise ops.ShapeError(f"dense_mm: {'A^T' if transpose_a else 'A'} is {tuple(a.T.shape if transpose_a else a.shape)}"
+                             f" but B is {tuple(b.shape)}")
+    if a.device != b.device:
+        raise ops.ConfigError(f"dense_mm: operands on {a.device} and {b.device}")
     if a.shape[0] >= 4096 and a.is_cuda and a.is_contiguous() and b.is_contiguous() \
             and a.dtype == torch.float32 and b.dtype == torch.float32:
         m, k = a.shape
         n = b.shape[1]
         out = torch.empty((k, n) if transpose_a else (m, n), device=a.device)
-        if lib().sgnn_dense_mm_f32(1 if transpose_a else 0, m, n, k, a.data_ptr(), b.data_ptr(), out.data_ptr(),
-                                   ops._stream()) == 0:
+        st = lib().sgnn_dense_mm_f32(1 if transpose_a else 0, m, n, k, a.data_ptr(), b.data_ptr(), out.data_ptr(),
+                                     ops._stream())
+        if st == 0:
             return out
+        if st != _lib_status_unsupported():
+            from ._lib import check
+            check(st, "dense_mm")
     return a.T @ b if transpose_a else a @ b
+
+
+def _lib_status_unsupported() -> int:
+    return 10  # SGNN_ERR_UNSUPPORTED: a shape the tensor-core kernels do not take
 
 
 def add_relu(a: torch.Tensor, b: torch.Tensor, out: torch.Tensor | None = None) -> torch.Tensor:
@@ -442,6 +458,12 @@ def softmax_xent_device(logits, labels_u32, mask_u8, inv_count: float):
     from ._lib import check, lib
     ops._dense(logits, "softmax_xent logits")
     n, c = logits.shape
+    if labels_u32.dtype not in (torch.int32, torch.uint32) or labels_u32.numel() != n or not labels_u32.is_contiguous():
+        raise ops.ConfigError("softmax_xent: labels must be a contiguous 32-bit integer tensor of one entry per row")
+    if mask_u8.dtype != torch.uint8 or mask_u8.numel() != n or not mask_u8.is_contiguous():
+        raise ops.ConfigError("softmax_xent: mask must be a contiguous uint8 tensor of one entry per row")
+    if n and (int(labels_u32.min()) < 0 or int(labels_u32.max()) >= c):  # gnn.hpp:327
+        raise ops.ConfigError(f"softmax_xent: label out of range for {c} classes")
     grad = torch.empty_like(logits)
     loss = torch.empty(1, dtype=torch.float64, device=logits.device)
     correct = torch.empty(1, dtype=torch.int32, device=logits.device)
@@ -454,8 +476,12 @@ def softmax_xent_device(logits, labels_u32, mask_u8, inv_count: float):
 def sage_wgrad(a2, h1, grad):
     """(a2^T grad, h1^T grad): the classes-wide layer's weight gradients."""
     from ._lib import check, lib
+    for t, nm in ((a2, "a2"), (h1, "h1"), (grad, "grad")):
+        ops._dense(t, f"sage_wgrad {nm}")
     n, h = a2.shape
     c = grad.shape[1]
+    if h1.shape != a2.shape or grad.shape[0] != n:
+        raise ops.ShapeError("sage_wgrad: operand shapes disagree")
     g2 = torch.empty(h, c, device=a2.device)
     g2s = torch.empty(h, c, device=a2.device)
     check(lib().sgnn_sage_wgrad_f32(a2.data_ptr(), h1.data_ptr(), grad.data_ptr(), n, h, c, g2.data_ptr(),
@@ -466,8 +492,19 @@ def sage_wgrad(a2, h1, grad):
 def sage_grad_wt(grad, w, u=None, act=None, out=None):
     """grad w^T, or relu_backward(u + grad w^T, act) (gnn.hpp:285-292)."""
     from ._lib import check, lib
+    ops._dense(grad, "sage_grad_wt grad")
+    ops._dense(w, "sage_grad_wt w")
     n, c = grad.shape
     h = w.shape[0]
+    if w.shape[1] != c:
+        raise ops.ShapeError(f"sage_grad_wt: w is {tuple(w.shape)}, grad has {c} columns")
+    if (u is None) != (act is None):
+        raise ops.ConfigError("sage_grad_wt: u and act go together")
+    for t, nm in ((u, "u"), (act, "act")):
+        if t is not None:
+            ops._dense(t, f"sage_grad_wt {nm}")
+            if t.shape != (n, h):
+                raise ops.ShapeError(f"sage_grad_wt: {nm} is {tuple(t.shape)}, expected {(n, h)}")
     out = torch.empty(n, h, device=grad.device) if out is None else out
     check(lib().sgnn_sage_grad_wt_f32(grad.data_ptr(), w.data_ptr(), n, h, c, _ptr(u), _ptr(act), out.data_ptr(),
                                       ops._stream()), "sage_grad_wt")

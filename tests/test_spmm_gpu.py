@@ -271,3 +271,42 @@ def test_dynamic_schedule_counter_reset_streams_graphs(cuda, k):
             np.testing.assert_array_equal(ops.sddmm(a, xs, y).values.cpu().numpy(), s0)
         want_s = port.sddmm(rp, ci, v, xs.cpu().numpy().astype(np.float64), y.cpu().numpy().astype(np.float64))
         np.testing.assert_allclose(s0, want_s, rtol=1e-4, atol=1e-5)
+
+
+@pytest.mark.parametrize("d0,d1,samples", [(1, 1 << 18, 512), ((1 << 24) - 4096, (1 << 24) + 4096, 4096),
+                                           ((1 << 31) - 2048, (1 << 31), 4096)])
+def test_mean_division_selftest(cuda, d0, d1, samples):
+    """The mean epilogue's division (reciprocal in double + one rounding,
+    common.cuh div_by_count) is bitwise IEEE __fdiv_rn for every degree in
+    the range and every value class (specials, subnormals, all exponents)."""
+    import ctypes as C
+
+    from paper_2403_14853_b200 import _lib
+    bad, fd, fs = C.c_uint64(), C.c_uint64(), C.c_uint32()
+    _lib.check(_lib.lib().sgnn_selftest_count_division(d0, d1, samples, 1234, C.byref(bad), C.byref(fd),
+                                                       C.byref(fs)), "selftest")
+    assert bad.value == 0, f"{bad.value} mismatches, first at degree {fd.value} sample {fs.value}"
+
+
+@pytest.mark.parametrize("k", [128, 64, 30])
+def test_mean_epilogue_bitwise_sum_over_degree(cuda, k):
+    """spmm(A, X, mean) == spmm(A, X, sum) / deg with IEEE division, bit for
+    bit: rows split across workers, hub rows through the fixup kernels, tiny
+    and signed-zero values (the divide moved into the kernels' row epilogue)."""
+    import torch
+    ops = _ops()
+    rng = np.random.default_rng(17)
+    n = 3000
+    rp, ci, v = rand_csr(rng, n, n, 0.01, hub_rows=(0, 5, 77), hub_density=0.7, empty_frac=0.05)
+    x = rng.normal(0, 1, (n, k)).astype(np.float32)
+    x[::7] *= np.float32(1e-38)  # subnormal-range sums
+    x[3] = -0.0
+    a = ops.CsrMatrix.from_numpy(rp, ci, v, n)
+    xt = torch.from_numpy(x).cuda()
+    for params in ({}, {"lanes": 16, "split_rows_over": 256}, {"lanes": 32, "vec": 2, "unroll": 4}):
+        plan = ops.Plan(a, k, **params) if params else None
+        s = ops.spmm_plan(a, xt, "sum", plan) if plan else ops.spmm(a, xt, "sum")
+        m = ops.spmm_plan(a, xt, "mean", plan) if plan else ops.spmm(a, xt, "mean")
+        deg = torch.from_numpy(np.diff(rp.astype(np.int64)).astype(np.float32)).cuda()[:, None]
+        want = torch.where(deg > 0, s / torch.clamp(deg, min=1.0), torch.zeros_like(s))
+        np.testing.assert_array_equal(m.cpu().numpy().view(np.uint32), want.cpu().numpy().view(np.uint32))
