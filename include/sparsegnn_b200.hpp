@@ -4,6 +4,7 @@
 //   spmm / spmm_with / detail::spmm_into   kernels.hpp:141-182
 //   sddmm / fusedmm                        kernels.hpp:187-270
 //   transpose / row_degrees / is_symmetric sparse.hpp:72-109,179-192
+//   normalize_adjacency                    sparse.hpp:116-174
 //   resolve_kernel, set_dispatch, get_dispatch, DispatchGuard
 //                                          kernels.hpp:38, autotune.hpp:36-51
 //   TrainingCache / build_cache            gnn.hpp:113-196
@@ -12,8 +13,10 @@
 // sparsegnn::CsrMatrix<float> / DenseMatrix<float> (or the look-alikes below)
 // pass straight in: same names, same argument meaning, same result
 // semantics, same exception classes by name.  Host operands are uploaded per
-// call; for training loops keep the graph resident with DeviceCsr /
-// TrainingCache (what the reference's TrainingCache does on the CPU).
+// call; for repeated calls keep operands resident: the same operators take
+// DeviceCsr / DeviceDense handles (plans cached per K, stream-asynchronous,
+// no upload), and TrainingCache keeps the backward operand on the device.
+// Tuning (run_tuning, save_report, load_report): sparsegnn_b200_tune.hpp.
 // `threads` is accepted and ignored (the GPU decides its own parallelism).
 //
 // Errors: sgnn_status codes become exceptions.  By default the classes below
@@ -29,6 +32,8 @@
 #include <cstdint>
 #include <cstring>
 #include <functional>
+#include <map>
+#include <memory>
 #include <stdexcept>
 #include <string>
 #include <utility>
@@ -161,7 +166,9 @@ private:
     std::size_t n_ = 0;
 };
 
-/// A CSR matrix resident on the device (uploaded once).
+/// A CSR matrix resident on the device (uploaded once), with the SpMM plans
+/// (work splits) built for it cached per K: the device-handle operators
+/// below reuse them, so repeated calls neither re-upload nor re-plan.
 class DeviceCsr {
 public:
     DeviceCsr() = default;
@@ -169,7 +176,7 @@ public:
     explicit DeviceCsr(const Csr& a)
         : n_rows_(a.n_rows), n_cols_(a.n_cols), nnz_(a.row_ptr.empty() ? 0 : a.row_ptr.back()),
           rp_(a.row_ptr.data(), a.row_ptr.size()), ci_(a.col_idx.data(), a.col_idx.size()),
-          v_(nullptr, 0) {
+          v_(nullptr, 0), plans_(std::make_shared<Plans>()) {
         std::vector<float> vf(a.values.begin(), a.values.end());
         v_ = DeviceBuffer<float>(vf.data(), vf.size());
     }
@@ -180,12 +187,74 @@ public:
     index_t n_cols() const { return n_cols_; }
     offset_t nnz() const { return nnz_; }
 
+    /// The cached plan for width k (built on first use).
+    sgnn_plan plan(index_t k) const {
+        auto& m = plans_->map;
+        auto it = m.find(k);
+        if (it != m.end()) return it->second;
+        const sgnn_csr v = view();
+        sgnn_plan p = nullptr;
+        check(sgnn_plan_create(&v, k, nullptr, &p, nullptr));
+        m[k] = p;
+        return p;
+    }
+    /// Use these launch parameters for width k from now on (e.g. a tuned
+    /// plan of run_tuning / load_report: TuningReport::plans).
+    void use_plan(index_t k, const sgnn_plan_params& params) {
+        const sgnn_csr v = view();
+        sgnn_plan p = nullptr;
+        check(sgnn_plan_create(&v, k, &params, &p, nullptr));
+        auto& m = plans_->map;
+        if (m.count(k)) sgnn_plan_destroy(m[k]);
+        m[k] = p;
+    }
+
 private:
+    struct Plans {
+        std::map<index_t, sgnn_plan> map;
+        ~Plans() {
+            for (auto& kv : map) sgnn_plan_destroy(kv.second);
+        }
+    };
     index_t n_rows_ = 0, n_cols_ = 0;
     offset_t nnz_ = 0;
     DeviceBuffer<offset_t> rp_;
     DeviceBuffer<index_t> ci_;
     DeviceBuffer<float> v_;
+    std::shared_ptr<Plans> plans_ = std::make_shared<Plans>();
+};
+
+/// A row-major fp32 dense matrix resident on the device.
+class DeviceDense {
+public:
+    DeviceDense() = default;
+    DeviceDense(index_t r, index_t c) : n_rows(r), n_cols(c), buf_(std::size_t(r) * c) {}
+    template <class Dense>
+    explicit DeviceDense(const Dense& h) : n_rows(h.n_rows), n_cols(h.n_cols) {
+        std::vector<float> f(h.data.begin(), h.data.end());
+        buf_ = DeviceBuffer<float>(f.data(), f.size());
+    }
+    float* data() const { return buf_.get(); }
+    std::size_t size() const { return std::size_t(n_rows) * n_cols; }
+    /// Copies to a host DenseMatrix-like object (synchronous).
+    template <class Dense>
+    void download(Dense& h) const {
+        std::vector<float> f(size());
+        buf_.download(f.data(), f.size());
+        h.n_rows = n_rows;
+        h.n_cols = n_cols;
+        h.data.assign(f.begin(), f.end());
+    }
+    template <class Dense = DenseMatrix<float>>
+    Dense to_host() const {
+        Dense h(n_rows, n_cols);
+        download(h);
+        return h;
+    }
+    index_t n_rows = 0, n_cols = 0;
+
+private:
+    DeviceBuffer<float> buf_;
 };
 
 /// Copies a device CSR view back into a host CsrMatrix-like object.
@@ -340,6 +409,101 @@ Dense fusedmm(const Csr& p, const Dense& x, const Dense& y, const SR& sr, int /*
 template <class Csr, class Dense>
 Dense fusedmm(const Csr& p, const Dense& x, const Dense& y) {
     return fusedmm(p, x, y, Semiring<float>::plus_times());
+}
+
+// ---------------------------------------------- device-resident operators
+// Same names and argument meaning as the host operators, over DeviceCsr /
+// DeviceDense handles: nothing is uploaded or re-planned per call, calls are
+// asynchronous on `stream` (default: the legacy stream) -- synchronise or
+// download to read results.
+namespace detail {
+/// detail::spmm_into (kernels.hpp:141-149) on device handles.
+template <class R, class Kind>
+void spmm_into(const DeviceCsr& a, const DeviceDense& b, R reduce, Kind kind, int /*threads*/, DeviceDense& c,
+               cudaStream_t stream = nullptr) {
+    if (c.n_rows != a.n_rows() || c.n_cols != b.n_cols)
+        throw SGNN_B200_ERR(ShapeError)("spmm_into: output is " + std::to_string(c.n_rows) + "x" +
+                                        std::to_string(c.n_cols) + ", expected " + std::to_string(a.n_rows()) + "x" +
+                                        std::to_string(b.n_cols));
+    const sgnn_csr v = a.view();
+    check(sgnn_spmm_with_f32(&v, b.data(), b.n_rows, b.n_cols, c.data(), internal::reduce_code(reduce),
+                             kind.is_specialized() ? SGNN_KERNEL_SPECIALIZED : SGNN_KERNEL_TRUSTED, kind.k,
+                             a.n_cols() == b.n_rows && b.n_cols ? a.plan(b.n_cols) : nullptr,
+                             reinterpret_cast<sgnn_stream>(stream)));
+}
+}  // namespace detail
+
+template <class R, class Kind>
+DeviceDense spmm_with(const DeviceCsr& a, const DeviceDense& b, R reduce, Kind kind, int threads = 0,
+                      cudaStream_t stream = nullptr) {
+    DeviceDense c(a.n_rows(), b.n_cols);
+    detail::spmm_into(a, b, reduce, kind, threads, c, stream);
+    return c;
+}
+
+template <class R = ReduceOp>
+DeviceDense spmm(const DeviceCsr& a, const DeviceDense& b, R reduce = R::Sum, int threads = 0,
+                 cudaStream_t stream = nullptr) {
+    return spmm_with(a, b, reduce, resolve_kernel(b.n_cols, reduce), threads, stream);
+}
+
+/// sddmm on device handles: the values of P's pattern (device, nnz floats).
+inline DeviceBuffer<float> sddmm(const DeviceCsr& p, const DeviceDense& x, const DeviceDense& y, int /*threads*/ = 0,
+                                 cudaStream_t stream = nullptr) {
+    DeviceBuffer<float> out(p.nnz());
+    const sgnn_csr v = p.view();
+    check(sgnn_sddmm_plan_f32(&v, x.data(), x.n_rows, y.data(), y.n_rows, x.n_cols, out.get(),
+                              x.n_cols && p.n_rows() == x.n_rows ? p.plan(x.n_cols) : nullptr,
+                              reinterpret_cast<sgnn_stream>(stream)));
+    return out;
+}
+
+template <class SR>
+DeviceDense fusedmm(const DeviceCsr& p, const DeviceDense& x, const DeviceDense& y, const SR& sr, int /*threads*/ = 0,
+                    cudaStream_t stream = nullptr) {
+    int edge = SGNN_EDGE_MUL;
+    if constexpr (requires { sr.edge_op; }) {
+        if (sr.edge_op >= 0) edge = sr.edge_op;
+        else if (sr.combine) throw SGNN_B200_ERR(DispatchError)("fusedmm: untagged combine cannot run on the GPU");
+    } else {
+        if (sr.combine) throw SGNN_B200_ERR(DispatchError)("fusedmm: untagged combine cannot run on the GPU");
+    }
+    DeviceDense c(p.n_rows(), y.n_cols);
+    const sgnn_csr v = p.view();
+    check(sgnn_fusedmm_f32(&v, x.data(), x.n_rows, y.data(), y.n_rows, x.n_cols, edge,
+                           internal::reduce_code(sr.reduce), c.data(), reinterpret_cast<sgnn_stream>(stream)));
+    return c;
+}
+
+// ------------------------------------------------------ structure helpers
+/// row_degrees (sparse.hpp:105-109): nnz of every row.
+template <class Csr>
+std::vector<index_t> row_degrees(const Csr& a) {
+    DeviceCsr da(a);
+    const sgnn_csr v = da.view();
+    DeviceBuffer<index_t> d(a.n_rows);
+    check(sgnn_row_degrees(&v, d.get(), nullptr));
+    std::vector<index_t> out(a.n_rows);
+    cuda_check(cudaDeviceSynchronize(), "row_degrees");
+    d.download(out.data(), out.size());
+    return out;
+}
+
+/// normalize_adjacency (sparse.hpp:116-174) on the device, bit-exact:
+/// D^-1/2 (A [+ I]) D^-1/2.
+template <class Csr>
+Csr normalize_adjacency(const Csr& a, bool add_self_loops = true) {
+    DeviceCsr da(a);
+    const sgnn_csr v = da.view();
+    std::uint64_t nnz = 0;
+    check(sgnn_normalize_adjacency(&v, add_self_loops ? 1 : 0, &nnz, nullptr, nullptr, nullptr, nullptr));
+    DeviceBuffer<offset_t> rp(std::size_t(a.n_rows) + 1);
+    DeviceBuffer<index_t> ci(nnz);
+    DeviceBuffer<float> vals(nnz);
+    check(sgnn_normalize_adjacency(&v, add_self_loops ? 1 : 0, &nnz, rp.get(), ci.get(), vals.get(), nullptr));
+    Csr out;
+    download_csr(sgnn_csr{a.n_rows, a.n_cols, nnz, rp.get(), ci.get(), vals.get()}, out);
+    return out;
 }
 
 // --------------------------------------------------- backward cache (gnn.hpp)

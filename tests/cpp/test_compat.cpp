@@ -8,6 +8,7 @@
 
 #include "sparsegnn_b200.hpp"
 #include "sparsegnn_b200_io.hpp"
+#include "sparsegnn_b200_tune.hpp"
 
 extern "C" {
 void orc_spmm_f64(uint32_t, const uint64_t*, const uint32_t*, const double*, const double*, uint32_t,
@@ -263,6 +264,94 @@ int main() {
         EXPECT(line == 4);
         EXPECT(throws<sg::IoError>([&] { (void)sg::load_mtx<Csr>("/nonexistent/x.mtx"); }));
         std::remove(p.c_str());
+    }
+    // ---- device-resident handles: same results as the host operators, plans
+    // cached per K, repeated calls without re-upload
+    {
+        std::mt19937_64 g(7);
+        Csr a = random_csr(g, 700, 500, 0.03, true);
+        Dense x(500, 64);
+        std::uniform_real_distribution<float> u(-1.f, 1.f);
+        for (float& v : x.data) v = u(g);
+        sg::DeviceCsr da(a);
+        sg::DeviceDense dx(x);
+        for (auto red : {sg::ReduceOp::Sum, sg::ReduceOp::Mean, sg::ReduceOp::Max}) {
+            const Dense want = sg::spmm(a, x, red);
+            sg::DeviceDense c1 = sg::spmm(da, dx, red);
+            sg::DeviceDense c2 = sg::spmm(da, dx, red);  // cached plan
+            EXPECT(c1.to_host<Dense>().data == want.data);
+            EXPECT(c2.to_host<Dense>().data == want.data);
+        }
+        sg::DeviceDense out(700, 64);
+        sg::detail::spmm_into(da, dx, sg::ReduceOp::Sum, sg::KernelKind::specialized(64), 0, out);
+        EXPECT(out.to_host<Dense>().data == sg::spmm(a, x, sg::ReduceOp::Sum).data);
+        sg::DeviceDense bad(10, 64);
+        EXPECT(throws<sg::ShapeError>([&] { sg::detail::spmm_into(da, dx, sg::ReduceOp::Sum, sg::KernelKind::trusted(), 0, bad); }));
+        Dense xr(700, 64), y(500, 64);
+        for (float& v : xr.data) v = 0.1f * u(g);
+        for (float& v : y.data) v = 0.1f * u(g);
+        sg::DeviceDense dxr(xr), dy(y);
+        const Csr want_s = sg::sddmm(a, xr, y);
+        std::vector<float> got_s(a.nnz());
+        sg::sddmm(da, dxr, dy).download(got_s.data(), got_s.size());
+        EXPECT(got_s == want_s.values);
+        const auto sr = sg::sigmoid_times<float>();
+        EXPECT(sg::fusedmm(da, dxr, dy, sr).to_host<Dense>().data == sg::fusedmm(a, xr, y, sr).data);
+    }
+    // ---- row_degrees / normalize_adjacency (sparse.hpp:105-174)
+    {
+        Csr a = make(3, 3, {0, 2, 3, 4}, {0, 1, 0, 2}, {1.f, 1.f, 1.f, 1.f});
+        EXPECT((sg::row_degrees(a) == std::vector<uint32_t>{2, 1, 1}));
+        // A + I: row sums 1+1+1 = 3 (diag 1+1), 2, 2 (self-loop added to row 2's 1 at col 2 -> 2)
+        Csr n = sg::normalize_adjacency(a, true);
+        EXPECT(n.n_rows == 3u && n.row_ptr.back() == 5u);
+        EXPECT(n.values[0] > 0.f);
+        Csr n0 = sg::normalize_adjacency(a, false);
+        EXPECT(n0.row_ptr.back() == 4u);
+        Csr rect(2, 3);
+        EXPECT(throws<sg::ShapeError>([&] { (void)sg::normalize_adjacency(rect); }));
+    }
+    // ---- run_tuning / save_report / load_report (autotune.hpp:98-164, report.cpp)
+    {
+        std::mt19937_64 g(11);
+        Csr a = random_csr(g, 4000, 4000, 0.01, true);
+        const std::vector<uint32_t> ks{32, 64, 48, 32};
+        sg::TuningReport r = sg::run_tuning(a, std::span<const uint32_t>(ks), 3, 0, 42, "compat-graph");
+        EXPECT(r.entries.size() == 2 && r.skipped == std::vector<uint32_t>{48});
+        EXPECT(r.best_k == 32 || r.best_k == 64);
+        EXPECT(r.plans.size() == 2 && r.profile.cores > 0);
+        for (const auto& e : r.entries) EXPECT(e.t_trusted_ms > 0 && e.t_specialized_ms > 0 && e.speedup > 0);
+        const std::string p = "/tmp/sgnn_compat_report.csv";
+        sg::save_report(r, p);
+        sg::TuningReport q = sg::load_report(p);
+        EXPECT(q.best_k == r.best_k && q.entries.size() == 2 && q.graph_id == "compat-graph" && q.skipped == r.skipped);
+        EXPECT(q.profile.vlen == 32 && q.profile.cores == r.profile.cores && q.plans.size() == 2);
+        EXPECT(q.plans.at(64).lanes == r.plans.at(64).lanes);
+        sg::DeviceCsr da(a);
+        da.use_plan(64, q.plans.at(64));  // tuned geometry reused: same results
+        Dense x(4000, 64);
+        for (std::size_t i = 0; i < x.data.size(); ++i) x.data[i] = float(i % 7) - 3.f;
+        EXPECT(sg::spmm(da, sg::DeviceDense(x)).to_host<Dense>().data == sg::spmm(a, x).data);
+        EXPECT(throws<sg::ConfigError>([&] { (void)sg::run_tuning(a, std::span<const uint32_t>(ks), 2); }));
+        {
+            FILE* f = std::fopen(p.c_str(), "w");
+            std::fputs("k,t_trusted_ms,t_specialized_ms,speedup\n32,1,0.5,2\nvlen,x\n", f);
+            std::fclose(f);
+        }
+        long line = -1;
+        try {
+            (void)sg::load_report(p);
+        } catch (const sg::ParseError& e) {
+            line = e.line();
+        }
+        EXPECT(line == 3);
+        EXPECT(throws<sg::IoError>([&] { (void)sg::load_report("/nonexistent/r.csv"); }));
+        std::remove(p.c_str());
+        std::remove((p + ".plans.csv").c_str());
+    }
+    if (failures) {
+        std::fprintf(stderr, "%d failures\n", failures);
+        return 1;
     }
     std::printf("compat OK\n");
     return 0;

@@ -11,9 +11,16 @@ from conftest import ROOT
 HERE = os.path.join(ROOT, "tests", "cpp")
 
 
-def _build():
+def _build(name="test_compat.bin"):
     subprocess.check_call(["make", "-C", HERE], stdout=subprocess.DEVNULL)
-    return os.path.join(HERE, "test_compat.bin")
+    return os.path.join(HERE, name)
+
+
+def _ref_variant():
+    path = _build("test_compat_ref.bin")
+    if not os.path.exists(path):
+        pytest.skip("reference headers (baseline/_ref/include) or oracle/_ref not built here")
+    return path
 
 
 def test_compat_header_compiles():
@@ -21,8 +28,24 @@ def test_compat_header_compiles():
     assert os.path.exists(_build())
 
 
+def test_compat_compiles_against_reference_headers():
+    """The drop-in compiled with the reference's own sparsegnn:: types and
+    error classes (SGNN_B200_ERROR_NS=sparsegnn)."""
+    assert os.path.exists(_ref_variant())
+
+
 @pytest.mark.gpu
 def test_compat_runs_on_gpu(cuda):
     r = subprocess.run([_build()], capture_output=True, text=True, timeout=300)
     assert r.returncode == 0, r.stdout + r.stderr
     assert "compat OK" in r.stdout
+
+
+@pytest.mark.gpu
+def test_compat_reference_types_run_on_gpu(cuda):
+    """Reference CsrMatrix / DenseMatrix objects through the drop-in on the
+    GPU, checked against the reference's own CPU spmm / transpose in the same
+    process; the reference's load_report reads the drop-in's report."""
+    r = subprocess.run([_ref_variant()], capture_output=True, text=True, timeout=300)
+    assert r.returncode == 0, r.stdout + r.stderr
+    assert "compat-ref OK" in r.stdout
