@@ -386,8 +386,9 @@ sgnn_status sgnn_dist_set_features(sgnn_dist g, const float* x_local, int borrow
 sgnn_status sgnn_dist_epochs(sgnn_dist* engines, int n_engines, uint32_t epochs, float lr, sgnn_stream stream);
 /* Statistics of epochs [first, first+count) since the last reset:
  * loss[i], accuracy[i], and times[i*SGNN_DIST_TIMES + j] in device ms:
- * j=0 epoch, 1 the three SpMMs, 2 this rank's compute phases, 3 exchanges
- * (incl. waiting for peers), 4/5/6 the layer-1 / layer-2 / backward SpMM.
+ * j=0 epoch, 1 the three SpMMs, 2 this rank's compute phases, 3 = epoch - compute
+ * (exchanges and waiting for peers; loopback: also the other virtual ranks'
+ * phases), 4/5/6 the layer-1 / layer-2 / backward SpMM.
  * Any output may be NULL.  Synchronizes the stream. */
 #define SGNN_DIST_TIMES 7
 sgnn_status sgnn_dist_stats(sgnn_dist g, uint32_t first, uint32_t count, double* loss, double* accuracy,

@@ -126,16 +126,30 @@ __global__ void add_into_kernel(T* __restrict__ dst, const T* __restrict__ src, 
 
 // (loss_sum, correct) of this rank's rows from softmax_xent's per-block
 // partials, in block order (deterministic for a given partition)
-__global__ void rank_stats_kernel(const double* __restrict__ blk_loss, const uint32_t* __restrict__ blk_ok,
-                                  uint32_t nblk, double* __restrict__ out) {
-    if (threadIdx.x != 0) return;
+// (one block of 256: strided partial sums, then a fixed tree)
+__global__ void __launch_bounds__(256) rank_stats_kernel(const double* __restrict__ blk_loss,
+                                                         const uint32_t* __restrict__ blk_ok, uint32_t nblk,
+                                                         double* __restrict__ out) {
+    __shared__ double sl[256], sk[256];
     double l = 0.0, k = 0.0;
-    for (uint32_t b = 0; b < nblk; ++b) {
+    for (uint32_t b = threadIdx.x; b < nblk; b += 256) {
         l += blk_loss[b];
         k += double(blk_ok[b]);
     }
-    out[0] = l;
-    out[1] = k;
+    sl[threadIdx.x] = l;
+    sk[threadIdx.x] = k;
+    __syncthreads();
+    for (uint32_t h = 128; h >= 1; h >>= 1) {
+        if (threadIdx.x < h) {
+            sl[threadIdx.x] += sl[threadIdx.x + h];
+            sk[threadIdx.x] += sk[threadIdx.x + h];
+        }
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) {
+        out[0] = sl[0];
+        out[1] = sk[0];
+    }
 }
 
 __global__ void epoch_record_kernel(const double* __restrict__ red, double inv_n, double* __restrict__ stats) {
@@ -172,9 +186,9 @@ struct sgnn_comm_s {
 };
 
 // ------------------------------------------------------------------- engine
-enum Mark {  // per-epoch event markers
-    M_BEGIN, M_X, M_SPMM1_0, M_SPMM1_1, M_PH0, M_EX1, M_SPMM2_0, M_SPMM2_1, M_PH1, M_EX2, M_SPMMB_0, M_SPMMB_1,
-    M_PH2, M_EX3, M_END, M_COUNT
+enum Mark {  // per-epoch event markers (P*_S / P*_E: a compute phase of this rank)
+    M_BEGIN, M_X, M_P0_S, M_SPMM1_0, M_SPMM1_1, M_P0_E, M_EX1, M_P1_S, M_SPMM2_0, M_SPMM2_1, M_P1_E, M_EX2, M_P2_S,
+    M_SPMMB_0, M_SPMMB_1, M_P2_E, M_EX3, M_P3_S, M_END, M_COUNT
 };
 
 struct sgnn_dist_s {
@@ -407,13 +421,14 @@ sgnn_status prepare(sgnn_dist_s* const* gs, int ng, cudaStream_t s) {
 // phase 0: a1 = A_r X, h1_r = relu(a1 W1 + X_r W1s)
 sgnn_status phase0(sgnn_dist_s* g, uint32_t e, cudaStream_t s) {
     const int red = g->kind == kSageMean ? SGNN_REDUCE_MEAN : SGNN_REDUCE_SUM;
+    DIST_MARK(g, M_P0_S);
     DIST_MARK(g, M_SPMM1_0);
     if (g->rows) SGNN_TRY(sgnn::run_spmm(&g->fwd, g->x_operand(), g->in, g->a1, red, g->plan_in, s));
     DIST_MARK(g, M_SPMM1_1);
     SGNN_TRY(mm(g, g->a1, g->wpack + g->off_w1, g->z1, g->rows, g->in, g->hid, s));
     SGNN_TRY(mm(g, g->x_rows(), g->wpack + g->off_w1s, g->t1, g->rows, g->in, g->hid, s));
     SGNN_TRY(sgnn::glue_add_relu(g->z1, g->t1, uint64_t(g->rows) * g->hid, g->h1_full + uint64_t(g->r0) * g->hid, s));
-    DIST_MARK(g, M_PH0);
+    DIST_MARK(g, M_P0_E);
     return SGNN_OK;
 }
 
@@ -421,6 +436,7 @@ sgnn_status phase0(sgnn_dist_s* g, uint32_t e, cudaStream_t s) {
 sgnn_status phase1(sgnn_dist_s* g, uint32_t e, cudaStream_t s) {
     const int red = g->kind == kSageMean ? SGNN_REDUCE_MEAN : SGNN_REDUCE_SUM;
     const float* h1r = g->h1_full + uint64_t(g->r0) * g->hid;
+    DIST_MARK(g, M_P1_S);
     DIST_MARK(g, M_SPMM2_0);
     if (g->rows) SGNN_TRY(sgnn::run_spmm(&g->fwd, g->h1_full, g->hid, g->a2, red, g->plan_hid, s));
     DIST_MARK(g, M_SPMM2_1);
@@ -428,7 +444,7 @@ sgnn_status phase1(sgnn_dist_s* g, uint32_t e, cudaStream_t s) {
                                     g->logits, s));
     SGNN_TRY(sgnn::softmax_xent_partials(g->logits, g->rows, g->cls, g->labels, g->mask, g->inv_n, g->grad,
                                          g->blk_loss, g->blk_ok, s));
-    rank_stats_kernel<<<1, 32, 0, s>>>(g->blk_loss, g->blk_ok, g->rows ? g->sm_blocks : 0, g->red);
+    rank_stats_kernel<<<1, 256, 0, s>>>(g->blk_loss, g->blk_ok, g->rows ? g->sm_blocks : 0, g->red);
     SGNN_LAUNCH_CHECK();
     if (g->rows) {
         SGNN_TRY(sgnn::sage_wgrad_launch(g->a2, h1r, g->grad, g->rows, g->hid, g->cls, g->wg_rpb, g->wg_blocks,
@@ -439,25 +455,27 @@ sgnn_status phase1(sgnn_dist_s* g, uint32_t e, cudaStream_t s) {
     }
     SGNN_TRY(sgnn::glue_sage_grad_wt(g->grad, g->wpack + g->off_w2, g->rows, g->hid, g->cls, nullptr, nullptr,
                                      g->ds2_full + uint64_t(g->r0) * g->hid, s));
-    DIST_MARK(g, M_PH1);
+    DIST_MARK(g, M_P1_E);
     return SGNN_OK;
 }
 
 // phase 2: dh1 = M_r ds2, dz1 = relu_backward(dh1 + grad W2s^T, h1), W1 / W1s gradients
 sgnn_status phase2(sgnn_dist_s* g, uint32_t e, cudaStream_t s) {
     const float* h1r = g->h1_full + uint64_t(g->r0) * g->hid;
+    DIST_MARK(g, M_P2_S);
     DIST_MARK(g, M_SPMMB_0);
     if (g->rows) SGNN_TRY(sgnn::run_spmm(&g->bwd, g->ds2_full, g->hid, g->dh1, SGNN_REDUCE_SUM, g->plan_bwd, s));
     DIST_MARK(g, M_SPMMB_1);
     SGNN_TRY(sgnn::glue_sage_grad_wt(g->grad, g->wpack + g->off_w2s, g->rows, g->hid, g->cls, g->dh1, h1r, g->z1, s));
     SGNN_TRY(mm_tn(g, g->a1, g->z1, g->gpack + g->off_w1, g->rows, g->in, g->hid, s));
     SGNN_TRY(mm_tn(g, g->x_rows(), g->z1, g->gpack + g->off_w1s, g->rows, g->in, g->hid, s));
-    DIST_MARK(g, M_PH2);
+    DIST_MARK(g, M_P2_E);
     return SGNN_OK;
 }
 
 // phase 3: sgd_step on every weight, epoch statistics
 sgnn_status phase3(sgnn_dist_s* g, uint32_t e, float lr, cudaStream_t s) {
+    DIST_MARK(g, M_P3_S);
     pack_sgd_kernel<<<ew_grid(g->pack_n), 256, 0, s>>>(g->wpack, g->gpack, g->pack_n, lr);
     epoch_record_kernel<<<1, 1, 0, s>>>(g->red, g->inv_n, g->stats + 2 * uint64_t(e));
     SGNN_LAUNCH_CHECK();
@@ -785,8 +803,8 @@ sgnn_status sgnn_dist_stats(sgnn_dist g, uint32_t first, uint32_t count, double*
             double* t = times + size_t(i) * SGNN_DIST_TIMES;
             t[0] = el(M_BEGIN, M_END);                                                    // epoch
             t[1] = el(M_SPMM1_0, M_SPMM1_1) + el(M_SPMM2_0, M_SPMM2_1) + el(M_SPMMB_0, M_SPMMB_1);  // 3 SpMMs
-            t[2] = el(M_X, M_PH0) + el(M_EX1, M_PH1) + el(M_EX2, M_PH2) + el(M_EX3, M_END);  // this rank's compute
-            t[3] = el(M_BEGIN, M_X) + el(M_PH0, M_EX1) + el(M_PH1, M_EX2) + el(M_PH2, M_EX3);  // exchanges (+ waits)
+            t[2] = el(M_P0_S, M_P0_E) + el(M_P1_S, M_P1_E) + el(M_P2_S, M_P2_E) + el(M_P3_S, M_END);  // own compute
+            t[3] = t[0] - t[2];  // exchanges + waiting for peers (loopback: + the other ranks' phases)
             t[4] = el(M_SPMM1_0, M_SPMM1_1);
             t[5] = el(M_SPMM2_0, M_SPMM2_1);
             t[6] = el(M_SPMMB_0, M_SPMMB_1);

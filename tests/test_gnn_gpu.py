@@ -204,6 +204,9 @@ def test_dist_sage_glue_step_matches_torch_step(cuda, hidden, classes):
         def all_gather(self, block):
             return block.contiguous()
 
+        def all_gather_v(self, block, bounds):
+            return block.contiguous()
+
     rp, ci = graphs.rmat(11, 2048 * 8, seed=9, symmetrize=True, self_loops=True)
     n = len(rp) - 1
     v = np.ones(len(ci), np.float32)
