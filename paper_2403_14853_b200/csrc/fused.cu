@@ -436,7 +436,8 @@ sgnn_status run_fusedmm(const sgnn_csr* p, const float* x, const float* y, uint3
         f.ld_slot = plan->kt;
         f.n_fix = plan->n_fix;
         f.width = k;
-        st = launch_spmm_fixup(f, reduce, s);
+        // the fused kernels of mean are the sum kernels; the divide is the pass below
+        st = launch_spmm_fixup(f, reduce == SGNN_REDUCE_MEAN ? SGNN_REDUCE_SUM : reduce, s);
     }
     if (st == SGNN_OK && reduce == SGNN_REDUCE_MEAN)  // kernels.hpp:263-266
         st = run_mean_divide(p->row_ptr, p->n_rows, out, k, k, s);
