@@ -25,6 +25,11 @@
 
 namespace sgnn {
 
+// fused_tma.cu: the TMA-gather (warp-specialised) kernels for K = 64 / 128
+sgnn_status run_fused_tma(const sgnn_csr* p, const float* x, const float* y, uint32_t k, int op, int reduce,
+                          float* out, const sgnn_plan_s* plan, cudaStream_t s, bool* ran);
+int tma_op_sddmm();
+
 namespace {
 
 struct SddmmArgs {
@@ -334,6 +339,11 @@ sgnn_status run_sddmm(const sgnn_csr* p, const float* x, const float* y, uint32_
     a.wnz = nullptr;
     a.wctr = nullptr;
     if (plan) {  // reuse the plan's nnz-balanced split: worker starts need no row search
+        if (vec && p->n_cols) {
+            bool ran = false;
+            SGNN_TRY(run_fused_tma(p, x, y, k, tma_op_sddmm(), SGNN_REDUCE_SUM, out, plan, s, &ran));
+            if (ran) return SGNN_OK;
+        }
         a.wrow = plan->wrow;
         a.wnz = plan->wnz;
         a.n_workers = plan->n_workers;
@@ -397,11 +407,17 @@ sgnn_status run_fusedmm(const sgnn_csr* p, const float* x, const float* y, uint3
     }
     if (plan->n_slots && plan->kt < k)  // the dot needs all of K: slots must be K wide
         st = fail(SGNN_ERR_DISPATCH, "fusedmm: plan workspace is narrower than K; build the plan with k_tile=K");
-    SpmmLauncher launch = st == SGNN_OK ? find_fused_launcher(vec, lanes, vregs, unroll, edge_op, reduce) : nullptr;
-    if (st == SGNN_OK && !launch)
+    bool tma_ran = false;
+    if (st == SGNN_OK && vec && p->n_cols) {
+        const int op = edge_op == SGNN_EDGE_SIGMOID_MUL ? dev::OP_FUSED_SIGMOID : dev::OP_FUSED_MUL;
+        st = run_fused_tma(p, x, y, k, op, reduce, out, plan, s, &tma_ran);
+    }
+    SpmmLauncher launch = st == SGNN_OK && !tma_ran ? find_fused_launcher(vec, lanes, vregs, unroll, edge_op, reduce)
+                                                    : nullptr;
+    if (st == SGNN_OK && !tma_ran && !launch)
         st = fail(SGNN_ERR_UNSUPPORTED, "fusedmm: no kernel for lanes=" + std::to_string(lanes) +
                                             " vec=" + std::to_string(vregs) + " unroll=" + std::to_string(unroll));
-    if (st == SGNN_OK) {
+    if (st == SGNN_OK && !tma_ran) {
         SpmmArgs args{};
         args.rp = p->row_ptr;
         args.ci = p->col_idx;

@@ -4,11 +4,12 @@
 //
 // The stable placement is an LSD radix sort of the nonzeros keyed by column
 // (2 passes of <= 11-bit digits for up to 2^22 columns), carrying (row, value)
-// as payload.  Within a tile, ranks are made stable with a warp-level
-// multisplit (__match_any_sync) processed in index order, so the output is
-// exactly the counting-sort order.  The row id of a nonzero is found in the
-// first pass by binary search inside the tile's row range, so no expanded
-// row array is materialised.
+// as payload.  Each tile of 4096 nonzeros is ranked warp by warp with
+// __match_any_sync in index order, staged in shared memory in digit order and
+// written out as contiguous runs per digit, so the output is exactly the
+// counting-sort order.  The first pass derives the row of every nonzero from
+// the row starts inside its tile (marks + a block scan), so no expanded row
+// array is read and no per-nonzero search is made.
 //
 // Also: row_degrees (sparse.hpp:105-109), is_symmetric (sparse.hpp:179-192)
 // and the mean-operand value scaling (gnn.hpp:158-159).
@@ -24,7 +25,7 @@ constexpr int kThreads = 256;
 constexpr int kWarps = kThreads / 32;
 constexpr int kItems = 16;                          // per thread per tile
 constexpr uint64_t kTile = uint64_t(kThreads) * kItems;  // 4096 nonzeros
-constexpr int kMaxDigitBits = 11;
+constexpr int kMaxDigitBits = 11;  // <= 2048 bins (the downsweep's u16 warp counters, 8 bins per thread)
 
 struct RadixPlan {
     int passes = 1;
@@ -122,8 +123,22 @@ __global__ void __launch_bounds__(kThreads) radix_upsweep_kernel(const uint32_t*
     for (uint32_t d = threadIdx.x; d < bins; d += kThreads) hist[uint64_t(d) * tiles + blockIdx.x] = sh[d];
 }
 
-// Stable scatter of one tile.  FIRST: payload rows are computed by binary
-// search (pass 1); otherwise read from rows_in.  LAST: keys are not written.
+// Stable scatter of one tile (4096 nonzeros in index order), staged through
+// shared memory so the global writes are contiguous runs per digit:
+//   A. warp w ranks its 512 consecutive items (16 rounds of 32, lane order =
+//      index order) with __match_any_sync against warp-private u16 digit
+//      counters -- no block barrier per round;
+//   B. per digit, exclusive offsets over the warps and the tile's digit
+//      starts (one block scan);
+//   C. every item lands in the tile's digit-sorted order in shared memory;
+//   D. consecutive threads write consecutive staged items: within a digit
+//      they go to consecutive global positions.
+// The order is the stable counting sort's (index order within a digit).
+// FIRST: rows come from the CSR itself -- each row start inside the tile
+// marks its position, an inclusive scan of the marks gives every item's row
+// (empty rows included); LAST: keys are not written.
+constexpr int kDownSmemFixed = 3 * kThreads * kItems * 4;  // staged keys, rows, vals
+
 template <bool FIRST, bool LAST, bool VALS>
 __global__ void __launch_bounds__(kThreads) radix_downsweep_kernel(
     const uint32_t* __restrict__ keys_in, const uint32_t* __restrict__ rows_in,
@@ -131,53 +146,148 @@ __global__ void __launch_bounds__(kThreads) radix_downsweep_kernel(
     uint32_t* __restrict__ rows_out, float* __restrict__ vals_out, uint64_t n, int shift,
     uint32_t mask, uint64_t tiles, const uint32_t* __restrict__ hist_scan,
     const uint64_t* __restrict__ rp, uint32_t m) {
-    extern __shared__ uint32_t sh[];
+    constexpr int T = kThreads * kItems;  // 4096
+    constexpr int WI = T / kWarps;        // 512 items per warp
+    extern __shared__ __align__(16) uint32_t sh[];
     const uint32_t bins = mask + 1;
-    uint32_t* cnt = sh;               // [bins]
-    uint32_t* whist = sh + bins;      // [kWarps][bins]
-    __shared__ uint32_t s_rows[2];
+    uint32_t* skey = sh;                    // [T]
+    uint32_t* srow = sh + T;                // [T] (FIRST: row marks, then rows)
+    float* sval = reinterpret_cast<float*>(sh + 2 * T);  // [T]
+    uint32_t* sgoff = sh + 3 * T;           // [bins] global offset - tile digit start
+    uint32_t* sdst = sgoff + bins;          // [bins] tile digit start
+    uint16_t* wcnt = reinterpret_cast<uint16_t*>(sdst + bins);  // [kWarps][bins]
+    __shared__ uint32_t s_scan[kThreads];
+    __shared__ uint32_t s_r0;
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-    for (uint32_t d = threadIdx.x; d < bins * (kWarps + 1); d += kThreads) sh[d] = 0;
-    const uint64_t base = uint64_t(blockIdx.x) * kTile;
-    if (FIRST && threadIdx.x == 0) {
-        uint32_t lo, hi;
-        tile_rows(rp, m, base, min(base + kTile, n) - 1, &lo, &hi);
-        s_rows[0] = lo;
-        s_rows[1] = hi + 1;
+    const uint64_t base = uint64_t(blockIdx.x) * T;
+    const uint32_t cnt = uint32_t(min(uint64_t(T), n - base));
+    for (uint32_t d = threadIdx.x; d < bins * kWarps / 2; d += kThreads) reinterpret_cast<uint32_t*>(wcnt)[d] = 0;
+    if (FIRST) {
+        for (int i = threadIdx.x; i < T; i += kThreads) srow[i] = 0;
+        if (threadIdx.x == 0) {
+            uint32_t lo = 0, hi = m;  // row of the tile's first item
+            while (hi - lo > 1) {
+                const uint32_t mid = lo + (hi - lo) / 2;
+                if (__ldg(rp + mid) <= base) lo = mid;
+                else hi = mid;
+            }
+            s_r0 = lo;
+        }
+        __syncthreads();
+        // mark every row start strictly inside the tile (empty rows stack up)
+        const uint32_t r0 = s_r0;
+        for (uint32_t r = r0 + 1 + threadIdx.x; r <= m; r += kThreads) {
+            const uint64_t st = __ldg(rp + r);
+            if (st >= base + cnt) break;
+            atomicAdd(srow + (st - base), 1u);
+        }
+        __syncthreads();
+        // inclusive scan of the marks: item i's row = r0 + marks(<= i)
+        uint32_t loc[kItems], acc = 0;
+#pragma unroll
+        for (int q = 0; q < kItems; ++q) {
+            acc += srow[threadIdx.x * kItems + q];
+            loc[q] = acc;
+        }
+        s_scan[threadIdx.x] = acc;
+        __syncthreads();
+        for (int off = 1; off < kThreads; off <<= 1) {
+            const uint32_t v = threadIdx.x >= off ? s_scan[threadIdx.x - off] : 0u;
+            __syncthreads();
+            s_scan[threadIdx.x] += v;
+            __syncthreads();
+        }
+        const uint32_t pre = r0 + (threadIdx.x ? s_scan[threadIdx.x - 1] : 0u);
+#pragma unroll
+        for (int q = 0; q < kItems; ++q) srow[threadIdx.x * kItems + q] = pre + loc[q];
     }
     __syncthreads();
+    // A. warp-local stable ranks
     const unsigned lt = (1u << lane) - 1u;
-    for (int r = 0; r < kItems; ++r) {
-        const uint64_t idx = base + uint64_t(r) * kThreads + threadIdx.x;
-        const bool valid = idx < n;
-        uint32_t key = 0, row = 0;
-        float val = 0.0f;
+    uint32_t pk[kItems];  // digit << 16 | rank within the warp's digit
+    uint32_t kk[kItems], rr[kItems];
+    float vv[kItems];
+    uint16_t* mycnt = wcnt + wid * bins;
+#pragma unroll
+    for (int q = 0; q < kItems; ++q) {
+        const uint32_t li = uint32_t(wid * WI + q * 32 + lane);
+        const bool valid = li < cnt;
+        const uint64_t idx = base + li;
+        uint32_t key = 0;
         if (valid) {
-            key = FIRST ? __ldcs(keys_in + idx) : __ldcs(keys_in + idx);
-            if (FIRST) row = find_row(rp, s_rows[0], s_rows[1], idx);
-            else row = __ldcs(rows_in + idx);
-            if (VALS) val = __ldcs(vals_in + idx);
+            key = __ldcs(keys_in + idx);
+            rr[q] = FIRST ? srow[li] : __ldcs(rows_in + idx);
+            vv[q] = VALS ? __ldcs(vals_in + idx) : 0.0f;
+        } else {
+            rr[q] = 0;
+            vv[q] = 0.0f;
         }
+        kk[q] = key;
         const uint32_t d = (key >> shift) & mask;
         const unsigned peers = __match_any_sync(0xffffffffu, valid ? d : 0xffffffffu);
-        const uint32_t rank = __popc(peers & lt);
-        const bool leader = (peers & lt) == 0;
-        if (valid && leader) whist[wid * bins + d] = __popc(peers);
-        __syncthreads();
-        if (valid) {
-            uint32_t pos = cnt[d] + rank;
-            for (int w = 0; w < wid; ++w) pos += whist[w * bins + d];
-            const uint64_t dst = uint64_t(__ldg(hist_scan + uint64_t(d) * tiles + blockIdx.x)) + pos;
-            if (!LAST) keys_out[dst] = key;
-            rows_out[dst] = row;
-            if (VALS) vals_out[dst] = val;
+        const uint32_t before = mycnt[d];
+        __syncwarp();
+        if (valid && (peers & lt) == 0) mycnt[d] = uint16_t(before + __popc(peers));
+        __syncwarp();
+        pk[q] = valid ? (d << 16) | (before + __popc(peers & lt)) : 0xffffffffu;
+    }
+    __syncthreads();
+    // B. per digit: exclusive offsets over the warps, tile totals, block scan
+    constexpr int BPT = 2048 / kThreads;  // bins per thread (bins <= 2048)
+    uint32_t tot[BPT];
+    uint32_t run = 0;
+#pragma unroll
+    for (int b = 0; b < BPT; ++b) {
+        const uint32_t d = threadIdx.x * BPT + b;
+        uint32_t t = 0;
+        if (d < bins) {
+#pragma unroll
+            for (int w = 0; w < kWarps; ++w) {
+                const uint32_t c = wcnt[w * bins + d];
+                wcnt[w * bins + d] = uint16_t(t);
+                t += c;
+            }
         }
+        tot[b] = t;
+        run += t;
+    }
+    s_scan[threadIdx.x] = run;
+    __syncthreads();
+    for (int off = 1; off < kThreads; off <<= 1) {
+        const uint32_t v = threadIdx.x >= off ? s_scan[threadIdx.x - off] : 0u;
         __syncthreads();
-        if (valid && leader) {
-            atomicAdd(cnt + d, __popc(peers));
-            whist[wid * bins + d] = 0;
+        s_scan[threadIdx.x] += v;
+        __syncthreads();
+    }
+    uint32_t start = threadIdx.x ? s_scan[threadIdx.x - 1] : 0u;
+#pragma unroll
+    for (int b = 0; b < BPT; ++b) {
+        const uint32_t d = threadIdx.x * BPT + b;
+        if (d < bins) {
+            sdst[d] = start;
+            sgoff[d] = __ldg(hist_scan + uint64_t(d) * tiles + blockIdx.x) - start;
         }
-        __syncthreads();
+        start += tot[b];
+    }
+    __syncthreads();
+    // C. stage in the tile's digit-sorted order
+#pragma unroll
+    for (int q = 0; q < kItems; ++q) {
+        if (pk[q] == 0xffffffffu) continue;
+        const uint32_t d = pk[q] >> 16;
+        const uint32_t slot = sdst[d] + wcnt[wid * bins + d] + (pk[q] & 0xffffu);
+        skey[slot] = kk[q];
+        srow[slot] = rr[q];
+        if (VALS) sval[slot] = vv[q];
+    }
+    __syncthreads();
+    // D. contiguous runs per digit to global memory
+    for (uint32_t k = threadIdx.x; k < cnt; k += kThreads) {
+        const uint32_t key = skey[k];
+        const uint64_t dst = uint64_t(sgoff[(key >> shift) & mask]) + k;
+        if (!LAST) keys_out[dst] = key;
+        rows_out[dst] = srow[k];
+        if (VALS) vals_out[dst] = sval[k];
     }
 }
 
@@ -186,7 +296,8 @@ sgnn_status launch_down(const uint32_t* ki, const uint32_t* ri, const float* vi,
                         uint32_t* ro, float* vo, uint64_t n, int shift, uint32_t mask,
                         uint64_t tiles, const uint32_t* hs, const uint64_t* rp, uint32_t m,
                         cudaStream_t s) {
-    const size_t smem = sizeof(uint32_t) * size_t(mask + 1) * (kWarps + 1);
+    const size_t bins = size_t(mask) + 1;
+    const size_t smem = kDownSmemFixed + 2 * 4 * bins + 2 * kWarps * bins;
     auto k = radix_downsweep_kernel<FIRST, LAST, VALS>;
     SGNN_CUDA_TRY(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
     k<<<unsigned(tiles), kThreads, smem, s>>>(ki, ri, vi, ko, ro, vo, n, shift, mask, tiles, hs, rp, m);

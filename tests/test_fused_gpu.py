@@ -164,3 +164,44 @@ def test_errors(cuda):
         ops.fusedmm(p, torch.ones(1, 4, device="cuda"), torch.ones(3, 4, device="cuda"))
     with pytest.raises(ops.DispatchError):
         ops.fusedmm(p, torch.ones(1, 4, device="cuda"), torch.ones(2, 4, device="cuda"), edge_op=lambda a, b: a)
+
+
+@pytest.mark.parametrize("k", [64, 128])
+def test_tma_pipeline_bitwise_register_kernels(cuda, k, monkeypatch):
+    """The warp-specialised TMA-gather kernels (fused_tma.cu: tile::gather4
+    into mbarrier-paced shared-memory rings, K = 64 / 128) give bit for bit
+    the register-gather kernels' FusedMM (both edge ops, sum and mean) and
+    SDDMM, for every ring depth and work split: split hub rows (segment
+    slots + fixup), empty rows, workers of only empty rows."""
+    from paper_2403_14853_b200 import graphs
+    ops = _ops()
+    rng = np.random.default_rng(5)
+    n = 1 << 13
+    rp, ci = graphs.rmat(13, n * 12, seed=3)
+    deg = np.diff(rp.astype(np.int64))
+    v = rng.uniform(0, 1, len(ci)).astype(np.float32)
+    x = rng.normal(0, 0.1, (n, k)).astype(np.float32)
+    y = rng.normal(0, 0.1, (n, k)).astype(np.float32)
+    assert (deg == 0).any() and deg.max() > 1000
+    p = ops.CsrMatrix.from_numpy(rp, ci, v, n)
+    xt, yt = _t(x), _t(y)
+    cases = [("sigmoid_mul", "sum"), ("mul", "sum"), ("sigmoid_mul", "mean")]
+    for pi in (64, 512):
+        plan = ops.Plan(p, k, **{**_fused_layout_kw(k), "path_items": pi})
+        monkeypatch.setenv("SGNN_NO_TMA_FUSED", "1")
+        want = {c: ops.fusedmm(p, xt, yt, *c, plan=plan).cpu().numpy() for c in cases}
+        want_s = ops.sddmm(p, xt, yt).values.cpu().numpy()
+        monkeypatch.delenv("SGNN_NO_TMA_FUSED")
+        for depth in ("2", "3", "4"):
+            monkeypatch.setenv("SGNN_TMA_DEPTH", depth)
+            for c in cases:
+                got = ops.fusedmm(p, xt, yt, *c, plan=plan).cpu().numpy()
+                np.testing.assert_array_equal(got.view(np.uint32), want[c].view(np.uint32), err_msg=f"{c} {pi} {depth}")
+            got_s = ops.sddmm(p, xt, yt).values.cpu().numpy()
+            np.testing.assert_array_equal(got_s.view(np.uint32), want_s.view(np.uint32), err_msg=f"sddmm {depth}")
+    check_fused(rp, ci, v, n, x, y, "sigmoid_mul", "sum")
+    check_sddmm(rp, ci, v, n, x, y)
+
+
+def _fused_layout_kw(k):
+    return {"lanes": 16 if k == 64 else 32, "vec": 1, "unroll": 8, "k_tile": k}
