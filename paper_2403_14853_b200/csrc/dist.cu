@@ -16,8 +16,8 @@
 //   [X all-gather, when features changed]
 //   phase 0  a1 = A_r X (mean), h1_r = relu(a1 W1 + X_r W1s)      (gnn.hpp:237-240)
 //   exch     all-gather h1
-//   phase 1  a2 = A_r h1, logits, softmax_xent + accuracy, W2/W2s gradients,
-//            ds2_r = grad W2^T                                     (:241-244, :318-370, :283-289)
+//   phase 1  a2 = A_r h1; logits, softmax_xent + accuracy and ds2_r = grad W2^T
+//            in one pass (sage_head_kernel); W2/W2s gradients     (:241-244, :318-370, :283-289)
 //   exch     all-gather ds2
 //   phase 2  dh1 = M_r ds2 (M = mean/sum backward operand rows), dz1 =
 //            relu_backward(dh1 + grad W2s^T), W1/W1s gradients    (:290-296)
@@ -440,10 +440,10 @@ sgnn_status phase1(sgnn_dist_s* g, uint32_t e, cudaStream_t s) {
     DIST_MARK(g, M_SPMM2_0);
     if (g->rows) SGNN_TRY(sgnn::run_spmm(&g->fwd, g->h1_full, g->hid, g->a2, red, g->plan_hid, s));
     DIST_MARK(g, M_SPMM2_1);
-    SGNN_TRY(sgnn::glue_sage_logits(g->a2, h1r, g->wpack + g->off_w2, g->wpack + g->off_w2s, g->rows, g->hid, g->cls,
-                                    g->logits, s));
-    SGNN_TRY(sgnn::softmax_xent_partials(g->logits, g->rows, g->cls, g->labels, g->mask, g->inv_n, g->grad,
-                                         g->blk_loss, g->blk_ok, s));
+    // logits, softmax_xent + accuracy, grad, ds2_r = grad W2^T in one pass
+    SGNN_TRY(sgnn::sage_head_partials(g->a2, h1r, g->wpack + g->off_w2, g->wpack + g->off_w2s, g->rows, g->hid,
+                                      g->cls, g->labels, g->mask, g->inv_n, g->grad,
+                                      g->ds2_full + uint64_t(g->r0) * g->hid, g->blk_loss, g->blk_ok, s));
     rank_stats_kernel<<<1, 256, 0, s>>>(g->blk_loss, g->blk_ok, g->rows ? g->sm_blocks : 0, g->red);
     SGNN_LAUNCH_CHECK();
     if (g->rows) {
@@ -453,8 +453,6 @@ sgnn_status phase1(sgnn_dist_s* g, uint32_t e, cudaStream_t s) {
         SGNN_CUDA_TRY(cudaMemsetAsync(g->gpack + g->off_w2, 0, sizeof(float) * (g->off_w1s - g->off_w2), s));
         SGNN_CUDA_TRY(cudaMemsetAsync(g->gpack + g->off_w2s, 0, sizeof(float) * (g->pack_n - g->off_w2s), s));
     }
-    SGNN_TRY(sgnn::glue_sage_grad_wt(g->grad, g->wpack + g->off_w2, g->rows, g->hid, g->cls, nullptr, nullptr,
-                                     g->ds2_full + uint64_t(g->r0) * g->hid, s));
     DIST_MARK(g, M_P1_E);
     return SGNN_OK;
 }

@@ -193,37 +193,36 @@ __global__ void __launch_bounds__(32 * (NCW + 1)) fused_tma_kernel(const TmaArgs
         };
 #pragma unroll
         for (int q = 0; q < PF; ++q) gen(q);
-        for (uint32_t it = 0;; ++it) {
-            const uint32_t s = it % D;
-            if (it >= uint32_t(D)) mbar_wait(empty + c * D + s, ((it / D) - 1) & 1);
-            uint32_t* h = hdr + (c * D + s) * 2;
-            h[0] = hw[0];
-            h[1] = hc[0];
-            float* sv = svals + (c * D + s) * U;
+        // emit item q (loaded PF emits ago), then refill lookahead slot q: the
+        // slots rotate by unrolling (no register copies, which would stall on
+        // the loads still in flight)
+        uint32_t it = 0;
+        bool fin = false;
+        while (!fin) {
 #pragma unroll
-            for (int t = 0; t < U; ++t) sv[t] = vs[0][t];
-            uint64_t* fb = full + c * D + s;
-            if (hw[0] != kSentinel && hn[0]) {
-                float* dst = sdata + (size_t(c) * D + s) * (U * K);
-                mbar_arrive_tx(fb, uint32_t(L::kStageBytes));
-                tma_gather4(dst, &tmap, fb, cs[0][0], cs[0][1], cs[0][2], cs[0][3]);
-                tma_gather4(dst + 4 * K, &tmap, fb, cs[0][4], cs[0][5], cs[0][6], cs[0][7]);
-            } else {
-                mbar_arrive(fb);
-            }
-            if (hw[0] == kSentinel) break;
+            for (int q = 0; q < PF; ++q) {
+                if (fin) break;
+                const uint32_t s = it % D;
+                if (it >= uint32_t(D)) mbar_wait(empty + c * D + s, ((it / D) - 1) & 1);
+                uint32_t* h = hdr + (c * D + s) * 2;
+                h[0] = hw[q];
+                h[1] = hc[q];
+                float* sv = svals + (c * D + s) * U;
 #pragma unroll
-            for (int q = 0; q + 1 < PF; ++q) {
-                hw[q] = hw[q + 1];
-                hc[q] = hc[q + 1];
-                hn[q] = hn[q + 1];
-#pragma unroll
-                for (int t = 0; t < U; ++t) {
-                    cs[q][t] = cs[q + 1][t];
-                    vs[q][t] = vs[q + 1][t];
+                for (int t = 0; t < U; ++t) sv[t] = vs[q][t];
+                uint64_t* fb = full + c * D + s;
+                if (hw[q] != kSentinel && hn[q]) {
+                    float* dst = sdata + (size_t(c) * D + s) * (U * K);
+                    mbar_arrive_tx(fb, uint32_t(L::kStageBytes));
+                    tma_gather4(dst, &tmap, fb, cs[q][0], cs[q][1], cs[q][2], cs[q][3]);
+                    tma_gather4(dst + 4 * K, &tmap, fb, cs[q][4], cs[q][5], cs[q][6], cs[q][7]);
+                } else {
+                    mbar_arrive(fb);
                 }
+                ++it;
+                if (hw[q] == kSentinel) fin = true;
+                else gen(q);
             }
-            gen(PF - 1);
         }
         if (a.wctr && atomicAdd(a.wctr + 1, 1u) == first_round - 1) {  // last slot out resets the schedule
             atomicExch(a.wctr, 0u);

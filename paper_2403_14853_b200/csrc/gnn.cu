@@ -405,10 +405,12 @@ __global__ void __launch_bounds__(256) sage_wgrad_kernel(const float* __restrict
 #pragma unroll
             for (int r = 0; r < RU; ++r) {
                 const float xs[4] = {x[r].x, x[r].y, x[r].z, x[r].w};  // zero past r1
+                // packed FFMA2 over class pairs: each half an ordinary fma
 #pragma unroll
                 for (int q = 0; q < 4; ++q)
 #pragma unroll
-                    for (int j = 0; j < CP; ++j) acc[q][j] = __fmaf_rn(xs[q], g[r][j], acc[q][j]);
+                    for (int j = 0; j < CP; j += 2)
+                        sgnn::dev::fma2_rn(acc[q][j], acc[q][j + 1], xs[q], g[r][j], g[r][j + 1]);
             }
         }
     }
@@ -497,6 +499,172 @@ __global__ void __launch_bounds__(256) sage_grad_wt_kernel(const float* __restri
                 *o = make_float4(d[r][0], d[r][1], d[r][2], d[r][3]);
             }
         }
+    }
+}
+
+// SAGE's layer-2 head in one pass over a2 and h1 (gnn.hpp:241-244,
+// :318-370, :283-287).  A warp takes R = 32 / CP rows at a time: lane l
+// accumulates the logit partials of all R x CP (row, class) pairs over its
+// features (sage_logits_kernel's FMA chains), and one 32-value
+// transpose-reduce (lane offsets 16, 8, 4, 2, 1 -- the same lane tree as
+// sage_logits_kernel) leaves lane l with the logit of row l / CP, class
+// l % CP.  Each CP-lane group then runs softmax_xent + masked_accuracy for
+// its row exactly as softmax_xent_kernel<G = CP> (same double arithmetic,
+// butterfly and tie rule), writes the gradient row and forms ds2 = grad W2^T
+// with sage_grad_wt_kernel's FMA chain (lane gl: feature blocks gl + CP b).
+// grad and ds2 are bitwise the three-kernel sequence's; a2 / h1 are read
+// once and the logits never reach memory.  Block b owns rows [b*rpb,
+// (b+1)*rpb); loss / correct sums go to blk_loss[b] / blk_ok[b] in a fixed
+// order.
+template <int CP>
+__global__ void __launch_bounds__(256) sage_head_kernel(
+    const float* __restrict__ a2, const float* __restrict__ h1, const float* __restrict__ w2,
+    const float* __restrict__ w2s, uint32_t n, uint32_t h, uint32_t c, const uint32_t* __restrict__ labels,
+    const uint8_t* __restrict__ mask, double inv_n, uint32_t rpb, float* __restrict__ grad,
+    float* __restrict__ ds2, double* __restrict__ blk_loss, uint32_t* __restrict__ blk_ok) {
+    constexpr int R = 32 / CP, J4 = CP / 4, NB = 32 / CP;  // rows per warp step; feature blocks per lane
+    constexpr unsigned FULL = 0xffffffffu;
+    __shared__ float4 sw[2][4 * J4 * 32];
+    __shared__ double s_loss[8];
+    __shared__ uint32_t s_ok[8];
+    stage_w<CP>(w2, h, c, sw[0]);
+    stage_w<CP>(w2s, h, c, sw[1]);
+    __syncthreads();
+    const uint32_t lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    const bool act = lane < h / 4;
+    const uint32_t gl = lane % CP, grp = lane / CP;  // class / row-of-step after the reduce
+    const uint32_t r0 = blockIdx.x * rpb, r1 = min(n, r0 + rpb);
+    double lsum = 0.0;
+    uint32_t oks = 0;
+    for (uint32_t i0 = r0 + wid * R; i0 < r1; i0 += 8 * R) {
+        float v;
+        {
+            float4 x[2][R];
+#pragma unroll
+            for (int r = 0; r < R; ++r) {
+                const bool ok = act && i0 + r < r1;
+                x[0][r] = ok ? __ldg(reinterpret_cast<const float4*>(a2 + uint64_t(i0 + r) * h) + lane) : make_float4(0.f, 0.f, 0.f, 0.f);
+                x[1][r] = ok ? __ldg(reinterpret_cast<const float4*>(h1 + uint64_t(i0 + r) * h) + lane) : make_float4(0.f, 0.f, 0.f, 0.f);
+            }
+            float p[32];  // p[r * CP + j]
+#pragma unroll
+            for (int t = 0; t < 32; ++t) p[t] = 0.0f;
+#pragma unroll
+            for (int m = 0; m < 2; ++m)
+#pragma unroll
+                for (int q = 0; q < 4; ++q)
+#pragma unroll
+                    for (int j4 = 0; j4 < J4; ++j4) {
+                        const float4 wv = sw[m][(q * J4 + j4) * 32 + lane];
+#pragma unroll
+                        for (int r = 0; r < R; ++r) {
+                            const float xv = q == 0 ? x[m][r].x : q == 1 ? x[m][r].y : q == 2 ? x[m][r].z : x[m][r].w;
+                            float* pr = p + r * CP + 4 * j4;
+                            pr[0] = __fmaf_rn(xv, wv.x, pr[0]);
+                            pr[1] = __fmaf_rn(xv, wv.y, pr[1]);
+                            pr[2] = __fmaf_rn(xv, wv.z, pr[2]);
+                            pr[3] = __fmaf_rn(xv, wv.w, pr[3]);
+                        }
+                    }
+            // 32-value transpose-reduce: lane l ends with index l
+#pragma unroll
+            for (int sh = 16; sh >= 1; sh >>= 1) {
+                const bool up = (lane & sh) != 0;
+#pragma unroll
+                for (int t = 0; t < sh; ++t) {
+                    const float send = up ? p[t] : p[sh + t];
+                    const float keep = up ? p[sh + t] : p[t];
+                    p[t] = __fadd_rn(keep, __shfl_xor_sync(FULL, send, sh));
+                }
+            }
+            v = p[0];
+        }
+        const uint32_t i = i0 + grp;
+        const bool row_ok = i < r1;
+        const unsigned gmask = CP == 32 ? FULL : (((1u << CP) - 1u) << (lane & ~(CP - 1)));
+        const bool cl = gl < c;
+        float g = 0.0f;
+        if (row_ok && mask[i]) {  // group-uniform
+            float mxf = -1.0f / 0.0f, bestv = -1.0f / 0.0f;
+            uint32_t best = 0;
+            if (cl) {
+                mxf = fmaxf(mxf, v);
+                if (v > bestv) {
+                    bestv = v;
+                    best = gl;
+                }
+            }
+#pragma unroll
+            for (int o = CP / 2; o >= 1; o >>= 1) {
+                mxf = fmaxf(mxf, __shfl_xor_sync(gmask, mxf, o, CP));
+                const float ov = __shfl_xor_sync(gmask, bestv, o, CP);
+                const uint32_t oj = __shfl_xor_sync(gmask, best, o, CP);
+                if (ov > bestv || (ov == bestv && oj < best)) {
+                    bestv = ov;
+                    best = oj;
+                }
+            }
+            const double mx = double(mxf);
+            const double e = cl ? exp(double(v) - mx) : 0.0;
+            double den = e;
+#pragma unroll
+            for (int o = CP / 2; o >= 1; o >>= 1) den += __shfl_xor_sync(gmask, den, o, CP);
+            const uint32_t lab = labels[i];
+            const float vlab = __shfl_sync(gmask, v, int(lab), CP);
+            if (cl) g = float((e / den - (gl == lab ? 1.0 : 0.0)) * inv_n);
+            if (gl == 0) {
+                lsum += (mx + log(den)) - double(vlab);
+                oks += best == lab ? 1u : 0u;
+            }
+        }
+        if (row_ok && cl) grad[uint64_t(i) * c + gl] = g;
+        // ds2[i, k] = sum_j grad[i, j] W2[k, j] (sage_grad_wt_kernel's chain)
+        float gj[CP];
+#pragma unroll
+        for (int j = 0; j < CP; ++j) gj[j] = __shfl_sync(FULL, g, j, CP);
+        if (row_ok) {
+#pragma unroll
+            for (int b = 0; b < NB; ++b) {
+                const uint32_t fb = gl + CP * b;  // feature block: features 4 fb .. 4 fb + 3
+                if (fb >= h / 4) break;
+                float d[4];
+#pragma unroll
+                for (int q = 0; q < 4; ++q) {
+#pragma unroll
+                    for (int j4 = 0; j4 < J4; ++j4) {
+                        const float4 wv = sw[0][(q * J4 + j4) * 32 + fb];
+                        float t = j4 == 0 ? __fmul_rn(gj[0], wv.x) : __fmaf_rn(gj[4 * j4], wv.x, d[q]);
+                        t = __fmaf_rn(gj[4 * j4 + 1], wv.y, t);
+                        t = __fmaf_rn(gj[4 * j4 + 2], wv.z, t);
+                        d[q] = __fmaf_rn(gj[4 * j4 + 3], wv.w, t);
+                    }
+                }
+                reinterpret_cast<float4*>(ds2 + uint64_t(i) * h)[fb] = make_float4(d[0], d[1], d[2], d[3]);
+            }
+        }
+    }
+    // per warp: the groups' sums in group order (lane gl == 0 of each group)
+    double wl = 0.0;
+    uint32_t wk = 0;
+#pragma unroll
+    for (int q = 0; q < R; ++q) {
+        wl += __shfl_sync(FULL, lsum, q * CP);
+        wk += __shfl_sync(FULL, oks, q * CP);
+    }
+    if (lane == 0) {
+        s_loss[wid] = wl;
+        s_ok[wid] = wk;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double l = 0.0;
+        uint32_t k = 0;
+        for (int q = 0; q < 8; ++q) {
+            l += s_loss[q];
+            k += s_ok[q];
+        }
+        blk_loss[blockIdx.x] = l;
+        blk_ok[blockIdx.x] = k;
     }
 }
 
@@ -684,8 +852,13 @@ sgnn_status epoch(sgnn_gnn_s* g, float lr, cudaStream_t s) {
         LAUNCH_EW4(add_relu_kernel, nh, g->z1, g->t1, nh, g->h1);          // h1 = relu(a1 W1 + X W1s)
         SGNN_TRY(fwd_spmm(g, g->h1, g->hid, g->a2, red, s));               // a2 = A h1
         if (g->skinny) {
-            SAGE_CP(sage_logits_kernel, g->cls, grid_for(uint64_t(g->n) * 32), 256,
-                    (g->a2, g->h1, g->w2, g->w2s, g->n, g->hid, g->cls, g->logits));
+            // logits + softmax_xent + accuracy + ds2 = grad W2^T in one pass
+            // (sage_head_kernel); the loss partials feed epoch_stats below
+            uint32_t rpb = 1, nblk = 1;
+            softmax_shape(g->n, &rpb, &nblk);
+            SAGE_CP(sage_head_kernel, g->cls, nblk, 256,
+                    (g->a2, g->h1, g->w2, g->w2s, g->n, g->hid, g->cls, g->labels, g->mask,
+                     1.0 / double(g->n_masked), rpb, g->grad, g->d_h, g->row_loss, g->row_ok));
         } else {
             SGNN_TRY(mm(g, g->a2, g->w2, g->logits, n, hid, cls, s));
             SGNN_TRY(mm(g, g->h1, g->w2s, g->t2, n, hid, cls, s));
@@ -704,7 +877,9 @@ sgnn_status epoch(sgnn_gnn_s* g, float lr, cudaStream_t s) {
     const double inv_n = 1.0 / double(g->n_masked);
     uint32_t rpb = 1, nblk = 1;
     softmax_shape(g->n, &rpb, &nblk);
-    if (g->cls <= 4)
+    if (g->skinny) {
+        // (done by sage_head_kernel in the forward)
+    } else if (g->cls <= 4)
         softmax_xent_kernel<4><<<nblk, kSoftmaxThreads, 0, s>>>(g->logits, g->n, g->cls, g->labels, g->mask, inv_n,
                                                                 rpb, g->grad, g->row_loss, g->row_ok);
     else if (g->cls <= 8)
@@ -734,8 +909,7 @@ sgnn_status epoch(sgnn_gnn_s* g, float lr, cudaStream_t s) {
             SAGE_CP(sage_wgrad_kernel, g->cls, g->wg_blocks, 256, (g->a2, g->h1, g->grad, g->n, g->hid, g->cls, g->wg_rpb, g->wg_part));
             SAGE_CP(sage_wgrad_finish_kernel, g->cls, unsigned((2 * g->hid * 16 + 127) / 128), 128,
                     (g->wg_part, g->wg_blocks, g->hid, g->cls, g->g2, g->g2s));
-            SAGE_CP(sage_grad_wt_kernel, g->cls, grid_for(uint64_t(g->n) * 32), 256,
-                    (g->grad, g->w2, g->n, g->hid, g->cls, nullptr, nullptr, g->d_h));                  // ds2
+            // ds2 = grad W2^T is already in d_h (sage_head_kernel)
             SGNN_TRY(cache_spmm_backward(g->cache, g->d_h, g->n, g->hid, g->d_h2, red, s));          // dh1 (A^T part)
             // dz1 = relu_backward(dh1 + grad W2s^T, h1) into z1 (free after the forward)
             SAGE_CP(sage_grad_wt_kernel, g->cls, grid_for(uint64_t(g->n) * 32), 256,
@@ -1075,6 +1249,18 @@ sgnn_status softmax_xent_partials(const float* logits, uint32_t n, uint32_t c, c
     else
         softmax_xent_kernel<32><<<nblk, kSoftmaxThreads, 0, s>>>(logits, n, c, labels, mask, inv_count, rpb, grad, blk_loss, blk_ok);
     SGNN_LAUNCH_CHECK();
+    return SGNN_OK;
+}
+
+sgnn_status sage_head_partials(const float* a2, const float* h1, const float* w2, const float* w2s, uint32_t n,
+                               uint32_t h, uint32_t c, const uint32_t* labels, const uint8_t* mask, double inv_count,
+                               float* grad, float* ds2, double* blk_loss, uint32_t* blk_ok, cudaStream_t s) {
+    SGNN_TRY(sage_shape(h, c, "sage_head"));
+    if (n == 0) return SGNN_OK;
+    uint32_t rpb = 1, nblk = 1;
+    softmax_shape(n, &rpb, &nblk);
+    SAGE_CP(sage_head_kernel, c, nblk, 256,
+            (a2, h1, w2, w2s, n, h, c, labels, mask, inv_count, rpb, grad, ds2, blk_loss, blk_ok));
     return SGNN_OK;
 }
 

@@ -95,6 +95,11 @@ uint32_t softmax_block_count(uint32_t n);
 sgnn_status softmax_xent_partials(const float* logits, uint32_t n, uint32_t c, const uint32_t* labels,
                                   const uint8_t* mask, double inv_count, float* grad, double* blk_loss,
                                   uint32_t* blk_ok, cudaStream_t s);
+// SAGE layer-2 head in one pass: logits, softmax_xent + accuracy (per-block
+// partials as softmax_xent_partials), grad rows, ds2 = grad W2^T
+sgnn_status sage_head_partials(const float* a2, const float* h1, const float* w2, const float* w2s, uint32_t n,
+                               uint32_t h, uint32_t c, const uint32_t* labels, const uint8_t* mask, double inv_count,
+                               float* grad, float* ds2, double* blk_loss, uint32_t* blk_ok, cudaStream_t s);
 // SAGE classes-wide weight gradients into caller-owned partials [nblk][2][h][16]
 sgnn_status sage_wgrad_launch(const float* a2, const float* h1, const float* grad, uint32_t n, uint32_t h,
                               uint32_t c, uint32_t rpb, uint32_t nblk, float* part, float* g2, float* g2s,
