@@ -360,7 +360,6 @@ def cfg5_e2e(eng, x_np, steps, flops, dev, tdist):
     for e in free:
         e.record(comp)
     eng.reset()
-    one_rank = eng.comm is None or eng.comm.nranks == 1
 
     def upload(i):
         b = i % nb
@@ -380,7 +379,7 @@ def cfg5_e2e(eng, x_np, steps, flops, dev, tdist):
     ready = upload(0)
     for i in range(steps):
         comp.wait_event(ready)
-        eng.set_features(xb[i % nb], borrow=one_rank)  # P>1: copied into the gathered buffer, re-exchanged
+        eng.set_features(xb[i % nb])  # device copy into [a1 | X_r] (P>1: also the gathered buffer, re-exchanged)
         eng.epochs(1, LR)
         free[i % nb].record(comp)
         if i + 1 < steps:

@@ -329,6 +329,9 @@ sgnn_status sgnn_gnn_destroy(sgnn_gnn g);
  * cfg5, 2-layer GraphSAGE): the reference's thread fan-out over contiguous
  * row chunks (parallel.hpp:28-65, balanced_row_partition) lifted to GPUs, and
  * train() (gnn.hpp:414-438) for SAGE-sum / SAGE-mean on each rank's rows.
+ * The layer-1 products are one fp32 product [a1 | X] [W1; W1s] (and one
+ * [a1 | X]^T dz1 for the weight gradients) instead of the reference's two
+ * products and an add: the same values within fp32 rounding of the sum.
  *
  * Communicator: one process per GPU, NCCL (ncclCommInitRank on the calling
  * thread's current device; libnccl.so.2 is loaded at run time -- the one the
@@ -372,10 +375,11 @@ sgnn_status sgnn_dist_set_weights(sgnn_dist g, const float* w1, const float* w2,
                                   const float* w2_self, sgnn_stream stream);
 sgnn_status sgnn_dist_get_weights(sgnn_dist g, float* w1, float* w2, float* w1_self, float* w2_self,
                                   sgnn_stream stream);
-/* New features for the rank's rows (host or device pointer, copied into the
- * gathered feature buffer and re-exchanged at the next epoch).  borrow != 0
- * with one rank: the epochs read x_local in place (16-byte aligned; it must
- * stay valid and unchanged until the next call).  Stream-asynchronous. */
+/* New features for the rank's rows (host or device pointer [rows x in]),
+ * copied into the engine's [a1 | X_r] row buffer and, with P ranks, into the
+ * gathered feature buffer (re-exchanged at the next epoch).  `borrow` is
+ * accepted for compatibility and ignored (the features are always copied).
+ * Stream-asynchronous. */
 sgnn_status sgnn_dist_set_features(sgnn_dist g, const float* x_local, int borrow, sgnn_stream stream);
 /* `epochs` training epochs at learning rate lr (forward, softmax_xent +
  * masked_accuracy, backward, sgd_step; the loss is the global masked mean).
@@ -400,7 +404,8 @@ sgnn_status sgnn_dist_stats_copy(sgnn_dist g, uint32_t first, uint32_t count, do
 /* Restart the epoch counter (statistics slots) at 0. */
 sgnn_status sgnn_dist_reset(sgnn_dist g);
 /* The rank's first row, row count, block nnz, global masked count (after the
- * first epoch) and the device address of its rows of the feature buffer. */
+ * first epoch) and the device address of its feature rows (row stride
+ * 2 * in_features: the right half of the [a1 | X_r] buffer). */
 sgnn_status sgnn_dist_info(sgnn_dist g, uint32_t* row0, uint32_t* rows, uint64_t* nnz, uint64_t* n_masked,
                            float** x_local);
 sgnn_status sgnn_dist_destroy(sgnn_dist g);

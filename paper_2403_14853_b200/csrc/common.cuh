@@ -157,14 +157,18 @@ __device__ __forceinline__ void fma2_rn(float& a0, float& a1, float s, float y0,
 // Mean epilogue (kernels.hpp:60-63): v / T(nnz(i)), IEEE round-to-nearest,
 // bit-identical to __fdiv_rn(v, float(deg)) but without div.rn.f32's
 // slow-path subroutine call (whose register cost would land in the gather
-// loop).  d = float(deg) is a 24-bit float; the exact quotient of two 24-bit
-// floats is either representable or at least 2^-49 (relative) away from every
-// rounding midpoint, so any approximation within 2^-50 of v/d rounds to the
-// same float.  recip_count gives 1/d within ~2^-52.5 (rcp.approx seed, two
-// Newton steps in double), v * r in double adds 2^-53, and the final
-// cvt.rn.f32.f64 performs the single rounding -- normal, subnormal, signed
-// zero, inf and NaN inputs included (checked bitwise against __fdiv_rn over
-// every degree up to 2^18 and special values: tests/test_spmm_gpu.py).
+// loop).  d = float(deg) is a 24-bit float.  For a NORMAL quotient, the exact
+// quotient of two 24-bit floats is either representable or at least 2^-49
+// (relative) away from every rounding midpoint, so any approximation within
+// 2^-50 of v/d rounds to the same float: recip_count gives 1/d within
+// ~2^-52.5 (rcp.approx seed, two Newton steps in double), v * r in double
+// adds 2^-53, and the final cvt.rn.f32.f64 performs the single rounding
+// (inf and NaN included).  A SUBNORMAL quotient (|v| < d 2^-126) has fewer
+// bits, so exact midpoints occur (e.g. v = 3077091 * 2^-143, d = 15744): it is
+// computed exactly on the 2^-149 grid: |v| 2^149 is an integer < 2^48, the
+// integer quotient and remainder come exactly out of double arithmetic, and
+// ties go to even.  Checked bitwise against __fdiv_rn
+// over every degree up to 2^18 and special values (tests/test_spmm_gpu.py).
 __device__ __forceinline__ double recip_count(uint64_t deg) {
     const float d = float(deg);
     float r0;
@@ -175,7 +179,25 @@ __device__ __forceinline__ double recip_count(uint64_t deg) {
     r = __fma_rn(__fma_rn(-dd, r, 1.0), r, r);
     return r;
 }
-__device__ __forceinline__ float div_by_count(float v, double r) {
+__device__ __forceinline__ float div_by_count_subnormal(float v, double r, float d) {
+    // all in double, all exact: num < 2^48, q * d < 2^49, the remainder fma
+    const double num = double(fabsf(v)) * 0x1p149;
+    const double dd = double(d);
+    double q = trunc(num * r);  // within one of the integer quotient
+    double rem = __fma_rn(-q, dd, num);
+    if (rem < 0.0) {
+        q -= 1.0;
+        rem += dd;
+    } else if (rem >= dd) {
+        q += 1.0;
+        rem -= dd;
+    }
+    const double rem2 = 2.0 * rem;
+    if (rem2 > dd || (rem2 == dd && (static_cast<long long>(q) & 1))) q += 1.0;  // ties to even
+    return copysignf(float(q) * 0x1p-149f, v);
+}
+__device__ __forceinline__ float div_by_count(float v, double r, float d) {
+    if (fabsf(v) < d * 0x1p-126f) return div_by_count_subnormal(v, r, d);
     return __double2float_rn(__dmul_rn(double(v), r));
 }
 

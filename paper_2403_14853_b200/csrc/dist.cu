@@ -14,7 +14,7 @@
 //
 // One epoch = compute phases separated by exchanges:
 //   [X all-gather, when features changed]
-//   phase 0  a1 = A_r X (mean), h1_r = relu(a1 W1 + X_r W1s)      (gnn.hpp:237-240)
+//   phase 0  a1 = A_r X (mean), h1_r = relu([a1 | X_r] [W1; W1s])  (gnn.hpp:237-240)
 //   exch     all-gather h1
 //   phase 1  a2 = A_r h1; logits, softmax_xent + accuracy and ds2_r = grad W2^T
 //            in one pass (sage_head_kernel); W2/W2s gradients     (:241-244, :318-370, :283-289)
@@ -211,10 +211,12 @@ struct sgnn_dist_s {
     bool dense_tc = true;
     std::vector<void*> owned;
     // full-height operands (gathered) and rank-local activations
-    float *x_full = nullptr, *h1_full = nullptr, *ds2_full = nullptr;
-    const float* x_borrow = nullptr;  // P == 1: features read in place for the next epochs
-    float *a1 = nullptr, *a2 = nullptr, *z1 = nullptr, *t1 = nullptr, *dh1 = nullptr, *logits = nullptr,
-          *grad = nullptr;
+    // ax = [a1 | X_r] (R x 2 in): the layer-1 aggregate beside the rank's
+    // own features, so a1 W1 + X_r W1s is ONE product with [W1; W1s] (and the
+    // weight gradient one A^T B); with one rank X_r is also the SpMM operand
+    // (row stride 2 in), with P ranks the gathered x_full [n x in] is.
+    float *ax = nullptr, *x_full = nullptr, *h1_full = nullptr, *ds2_full = nullptr;
+    float *a2 = nullptr, *z1 = nullptr, *dh1 = nullptr, *grad = nullptr;
     uint32_t* labels = nullptr;
     uint8_t* mask = nullptr;
     uint32_t* deg = nullptr;  // global degrees [n] (gathered)
@@ -234,9 +236,8 @@ struct sgnn_dist_s {
     bool prepared = false, x_dirty = true;
     std::vector<cudaEvent_t> ev;  // [max_epochs * M_COUNT]
 
-    float* x_local() { return x_full + uint64_t(r0) * in; }
-    const float* x_operand() const { return x_borrow ? x_borrow : x_full; }
-    const float* x_rows() const { return x_operand() + (x_borrow ? 0 : uint64_t(r0) * in); }
+    const float* x_operand() const { return P == 1 ? ax + in : x_full; }
+    uint64_t x_ld() const { return P == 1 ? 2ull * in : uint64_t(in); }
     cudaEvent_t mark(uint32_t e, int m) { return ev[size_t(e) * M_COUNT + m]; }
 
     ~sgnn_dist_s() {
@@ -423,11 +424,11 @@ sgnn_status phase0(sgnn_dist_s* g, uint32_t e, cudaStream_t s) {
     const int red = g->kind == kSageMean ? SGNN_REDUCE_MEAN : SGNN_REDUCE_SUM;
     DIST_MARK(g, M_P0_S);
     DIST_MARK(g, M_SPMM1_0);
-    if (g->rows) SGNN_TRY(sgnn::run_spmm(&g->fwd, g->x_operand(), g->in, g->a1, red, g->plan_in, s));
+    if (g->rows)  // a1 into the left half of ax
+        SGNN_TRY(sgnn::run_spmm_ld(&g->fwd, g->x_operand(), g->x_ld(), g->in, g->ax, 2ull * g->in, red, g->plan_in, s));
     DIST_MARK(g, M_SPMM1_1);
-    SGNN_TRY(mm(g, g->a1, g->wpack + g->off_w1, g->z1, g->rows, g->in, g->hid, s));
-    SGNN_TRY(mm(g, g->x_rows(), g->wpack + g->off_w1s, g->t1, g->rows, g->in, g->hid, s));
-    SGNN_TRY(sgnn::glue_add_relu(g->z1, g->t1, uint64_t(g->rows) * g->hid, g->h1_full + uint64_t(g->r0) * g->hid, s));
+    SGNN_TRY(mm(g, g->ax, g->wpack + g->off_w1, g->z1, g->rows, 2 * g->in, g->hid, s));  // [a1 | X_r] [W1; W1s]
+    SGNN_TRY(sgnn::glue_relu(g->z1, uint64_t(g->rows) * g->hid, g->h1_full + uint64_t(g->r0) * g->hid, s));
     DIST_MARK(g, M_P0_E);
     return SGNN_OK;
 }
@@ -450,8 +451,7 @@ sgnn_status phase1(sgnn_dist_s* g, uint32_t e, cudaStream_t s) {
         SGNN_TRY(sgnn::sage_wgrad_launch(g->a2, h1r, g->grad, g->rows, g->hid, g->cls, g->wg_rpb, g->wg_blocks,
                                          g->wg_part, g->gpack + g->off_w2, g->gpack + g->off_w2s, s));
     } else {
-        SGNN_CUDA_TRY(cudaMemsetAsync(g->gpack + g->off_w2, 0, sizeof(float) * (g->off_w1s - g->off_w2), s));
-        SGNN_CUDA_TRY(cudaMemsetAsync(g->gpack + g->off_w2s, 0, sizeof(float) * (g->pack_n - g->off_w2s), s));
+        SGNN_CUDA_TRY(cudaMemsetAsync(g->gpack + g->off_w2, 0, sizeof(float) * (g->pack_n - g->off_w2), s));
     }
     DIST_MARK(g, M_P1_E);
     return SGNN_OK;
@@ -465,8 +465,7 @@ sgnn_status phase2(sgnn_dist_s* g, uint32_t e, cudaStream_t s) {
     if (g->rows) SGNN_TRY(sgnn::run_spmm(&g->bwd, g->ds2_full, g->hid, g->dh1, SGNN_REDUCE_SUM, g->plan_bwd, s));
     DIST_MARK(g, M_SPMMB_1);
     SGNN_TRY(sgnn::glue_sage_grad_wt(g->grad, g->wpack + g->off_w2s, g->rows, g->hid, g->cls, g->dh1, h1r, g->z1, s));
-    SGNN_TRY(mm_tn(g, g->a1, g->z1, g->gpack + g->off_w1, g->rows, g->in, g->hid, s));
-    SGNN_TRY(mm_tn(g, g->x_rows(), g->z1, g->gpack + g->off_w1s, g->rows, g->in, g->hid, s));
+    SGNN_TRY(mm_tn(g, g->ax, g->z1, g->gpack + g->off_w1, g->rows, 2 * g->in, g->hid, s));  // [g1; g1s] = ax^T dz1
     DIST_MARK(g, M_P2_E);
     return SGNN_OK;
 }
@@ -501,7 +500,7 @@ sgnn_status run_epochs(sgnn_dist_s* const* gs, int ng, uint32_t epochs, float lr
     for (uint32_t it = 0; it < epochs; ++it) {
         const uint32_t e = g0->epoch;
         SGNN_TRY(each([&](sgnn_dist_s* g) { return cudaEventRecord(g->mark(e, M_BEGIN), s) == cudaSuccess ? SGNN_OK : fail(SGNN_ERR_CUDA, "event"); }));
-        if (g0->x_dirty && !g0->x_borrow)
+        if (g0->x_dirty && g0->P > 1)
             SGNN_TRY(allgather_rows(gs, ng, [](sgnn_dist_s* g) { return static_cast<void*>(g->x_full); }, g0->in, s));
         SGNN_TRY(each([&](sgnn_dist_s* g) {
             g->x_dirty = false;
@@ -526,6 +525,7 @@ sgnn_status run_epochs(sgnn_dist_s* const* gs, int ng, uint32_t epochs, float lr
 
 // ====================================================================== C ABI
 extern "C" {
+sgnn_status sgnn_dist_set_features(sgnn_dist g, const float* x_local, int borrow, sgnn_stream stream);
 
 sgnn_status sgnn_comm_get_unique_id(void* id) {
     if (!id) return fail(SGNN_ERR_CONFIG, "comm_get_unique_id: null id");
@@ -657,20 +657,20 @@ sgnn_status sgnn_dist_create(sgnn_comm comm, int rank, const uint32_t* bounds, c
     cublasSetWorkspace(g->blas, g->ws, g->ws_bytes);
     const uint64_t N = n, R = rows;
     auto al = [](uint64_t v) { return (v + 63) / 64 * 64; };
-    g->off_w1 = 0;
-    g->off_w2 = al(uint64_t(in_features) * hidden);
-    g->off_w1s = g->off_w2 + al(uint64_t(hidden) * classes);
-    g->off_w2s = g->off_w1s + al(uint64_t(in_features) * hidden);
+    g->off_w1 = 0;  // [W1; W1s] contiguous: the layer-1 product's B operand
+    g->off_w1s = uint64_t(in_features) * hidden;
+    g->off_w2 = al(2ull * in_features * hidden);
+    g->off_w2s = g->off_w2 + al(uint64_t(hidden) * classes);
     g->pack_n = g->off_w2s + al(uint64_t(hidden) * classes);
     g->sm_blocks = sgnn::softmax_block_count(rows ? rows : 1);
     g->wg_blocks = std::min<uint32_t>(592, std::max<uint32_t>(1, rows));
     g->wg_rpb = (std::max<uint32_t>(1, rows) + g->wg_blocks - 1) / g->wg_blocks;
     g->wg_blocks = (std::max<uint32_t>(1, rows) + g->wg_rpb - 1) / g->wg_rpb;
-    if ((st = dalloc(g, &g->x_full, N * in_features)) != SGNN_OK || (st = dalloc(g, &g->h1_full, N * hidden)) != SGNN_OK ||
-        (st = dalloc(g, &g->ds2_full, N * hidden)) != SGNN_OK || (st = dalloc(g, &g->a1, R * in_features)) != SGNN_OK ||
-        (st = dalloc(g, &g->a2, R * hidden)) != SGNN_OK || (st = dalloc(g, &g->z1, R * hidden)) != SGNN_OK ||
-        (st = dalloc(g, &g->t1, R * hidden)) != SGNN_OK || (st = dalloc(g, &g->dh1, R * hidden)) != SGNN_OK ||
-        (st = dalloc(g, &g->logits, R * classes)) != SGNN_OK || (st = dalloc(g, &g->grad, R * classes)) != SGNN_OK ||
+    if ((P > 1 && (st = dalloc(g, &g->x_full, N * in_features)) != SGNN_OK) ||
+        (st = dalloc(g, &g->h1_full, N * hidden)) != SGNN_OK || (st = dalloc(g, &g->ds2_full, N * hidden)) != SGNN_OK ||
+        (st = dalloc(g, &g->ax, R * 2 * in_features)) != SGNN_OK || (st = dalloc(g, &g->a2, R * hidden)) != SGNN_OK ||
+        (st = dalloc(g, &g->z1, R * hidden)) != SGNN_OK || (st = dalloc(g, &g->dh1, R * hidden)) != SGNN_OK ||
+        (st = dalloc(g, &g->grad, R * classes)) != SGNN_OK ||
         (st = dalloc(g, &g->labels, R)) != SGNN_OK || (st = dalloc(g, &g->mask, R)) != SGNN_OK ||
         (st = dalloc(g, &g->deg, N)) != SGNN_OK || (st = dalloc(g, &g->wpack, g->pack_n)) != SGNN_OK ||
         (st = dalloc(g, &g->gpack, g->pack_n)) != SGNN_OK || (st = dalloc(g, &g->blk_loss, g->sm_blocks)) != SGNN_OK ||
@@ -683,7 +683,7 @@ sgnn_status sgnn_dist_create(sgnn_comm comm, int rank, const uint32_t* bounds, c
         cudaMemsetAsync(g->gpack, 0, sizeof(float) * g->pack_n, s) != cudaSuccess)
         return bail(fail(SGNN_ERR_CUDA, "dist: memset"));
     if (rows) {
-        if (cudaMemcpyAsync(g->x_local(), x_local, sizeof(float) * R * in_features, cudaMemcpyDefault, s) != cudaSuccess ||
+        if (sgnn_dist_set_features(g, x_local, 0, reinterpret_cast<sgnn_stream>(s)) != SGNN_OK ||
             cudaMemcpyAsync(g->labels, labels_local, sizeof(uint32_t) * R, cudaMemcpyDefault, s) != cudaSuccess ||
             cudaMemcpyAsync(g->mask, mask_local, R, cudaMemcpyDefault, s) != cudaSuccess)
             return bail(fail(SGNN_ERR_CUDA, "dist: input upload failed"));
@@ -747,17 +747,15 @@ sgnn_status sgnn_dist_set_features(sgnn_dist g, const float* x_local, int borrow
     cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
     if (!g) return fail(SGNN_ERR_CONFIG, "dist_set_features: null engine");
     if (!x_local && g->rows) return fail(SGNN_ERR_CONFIG, "dist_set_features: null features");
-    if (borrow && g->P == 1) {
-        if (reinterpret_cast<uintptr_t>(x_local) % 16)
-            return fail(SGNN_ERR_UNSUPPORTED, "dist_set_features: borrowed features must be 16-byte aligned");
-        g->x_borrow = x_local;
-        g->x_dirty = false;
-        return SGNN_OK;
+    (void)borrow;  // the features are always copied: into the right half of [a1 | X_r] and, with P ranks,
+                   // into the rank's rows of the gathered operand
+    if (g->rows) {
+        const size_t row = sizeof(float) * g->in;
+        SGNN_CUDA_TRY(cudaMemcpy2DAsync(g->ax + g->in, 2 * row, x_local, row, row, g->rows, cudaMemcpyDefault, s));
+        if (g->P > 1)
+            SGNN_CUDA_TRY(cudaMemcpyAsync(g->x_full + uint64_t(g->r0) * g->in, x_local, row * g->rows,
+                                          cudaMemcpyDefault, s));
     }
-    g->x_borrow = nullptr;
-    if (g->rows)
-        SGNN_CUDA_TRY(cudaMemcpyAsync(g->x_local(), x_local, sizeof(float) * uint64_t(g->rows) * g->in,
-                                      cudaMemcpyDefault, s));
     g->x_dirty = true;
     return SGNN_OK;
 }
@@ -833,7 +831,7 @@ sgnn_status sgnn_dist_info(sgnn_dist g, uint32_t* row0, uint32_t* rows, uint64_t
     if (rows) *rows = g->rows;
     if (nnz) *nnz = g->fwd.nnz;
     if (n_masked) *n_masked = g->n_masked;
-    if (x_local) *x_local = g->x_local();
+    if (x_local) *x_local = g->ax + g->in;  // row stride 2 * in
     return SGNN_OK;
 }
 

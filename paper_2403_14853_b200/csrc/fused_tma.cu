@@ -2,6 +2,9 @@
 // K = 64 and 128: Y rows are gathered by the Tensor Memory Accelerator into
 // shared-memory rings instead of into registers.
 //
+// STATUS: opt-in (SGNN_TMA_FUSED=1), slower than the register kernels on
+// cfg4 -- see tma_fused_enabled() below and DESIGN.md 3.3.
+//
 // Why: at K = 64 the register-gather worker (spmm_kernel.cuh, fused mode) is
 // latency-bound -- per batch of 8 nonzeros it waits for the 8 row gathers,
 // then runs the dependent dot -> transpose-reduce -> edge op -> fold chain,
@@ -539,8 +542,12 @@ sgnn_status launch_depth(const TmaArgs& a, const CUtensorMap& map, cudaStream_t 
 
 }  // namespace
 
-// SGNN_NO_TMA_FUSED set: the register-gather kernels (A/B switch, read per call)
-bool tma_fused_enabled() { return !std::getenv("SGNN_NO_TMA_FUSED"); }
+// Opt-in (SGNN_TMA_FUSED set, read per call): measured slower than the
+// register-gather kernels on cfg4 -- 1.77-2.3 ms vs 1.17 ms FusedMM, 1.5-2.2
+// vs 0.79 ms SDDMM (scripts/tma_probe.py, profiles/r02_tma_*): the consumers
+// spend their issue slots spinning on the full barriers, i.e. the gather4
+// rows arrive at ~23 GB/s per SM with 96 stages (192 KB) in flight per SM.
+bool tma_fused_enabled() { return std::getenv("SGNN_TMA_FUSED") != nullptr; }
 
 // 1 = ran; 0 = not applicable here (the caller takes the register kernels).
 sgnn_status run_fused_tma(const sgnn_csr* p, const float* x, const float* y, uint32_t k, int op, int reduce,

@@ -1186,6 +1186,12 @@ sgnn_status sage_shape(uint32_t h, uint32_t c, const char* what) {
 }
 }  // namespace
 
+sgnn_status glue_relu(const float* x, uint64_t n, float* y, cudaStream_t s) {
+    if (n == 0) return SGNN_OK;
+    LAUNCH_EW4(relu_kernel, n, x, n, y);
+    return SGNN_OK;
+}
+
 sgnn_status glue_add_relu(const float* a, const float* b, uint64_t n, float* h, cudaStream_t s) {
     if (n == 0) return SGNN_OK;
     LAUNCH_EW4(add_relu_kernel, n, a, b, n, h);

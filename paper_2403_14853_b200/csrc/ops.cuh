@@ -29,6 +29,10 @@ sgnn_status run_normalize(const sgnn_csr* a, int add_loops, uint64_t* out_nnz, u
 
 sgnn_status run_spmm(const sgnn_csr* a, const float* x, uint32_t k, float* c, int reduce,
                      const sgnn_plan_s* plan, cudaStream_t s);
+// the same with row strides of X and C (floats, >= K): operands that are
+// column slices of wider row-major buffers
+sgnn_status run_spmm_ld(const sgnn_csr* a, const float* x, uint64_t ldx, uint32_t k, float* c, uint64_t ldc,
+                        int reduce, const sgnn_plan_s* plan, cudaStream_t s);
 // SpMM reading X from the row blocks `parts` of a partition (peer memory).
 sgnn_status run_spmm_peer(const sgnn_csr* a, const float* const* parts, uint32_t n_parts,
                           uint32_t part_shift, uint32_t k, float* c, int reduce,
@@ -81,6 +85,7 @@ int dense_mm_nn_workspace(int m, int n, int k, size_t* bytes);
 int dense_mm_tn_workspace(int m, int n, int k, int splits, size_t* bytes);
 // SAGE layer glue (gnn.cu), see sgnn_b200.h
 sgnn_status glue_add_relu(const float* a, const float* b, uint64_t n, float* h, cudaStream_t s);
+sgnn_status glue_relu(const float* x, uint64_t n, float* y, cudaStream_t s);
 sgnn_status glue_sage_logits(const float* a2, const float* h1, const float* w2, const float* w2s, uint32_t n,
                              uint32_t h, uint32_t c, float* logits, cudaStream_t s);
 sgnn_status glue_softmax_xent(const float* logits, uint32_t n, uint32_t c, const uint32_t* labels,

@@ -69,7 +69,7 @@ __global__ void count_division_check_kernel(uint64_t d0, uint64_t d1, uint32_t s
         }
         const float v = __uint_as_float(bits);
         const float want = __fdiv_rn(v, float(deg));
-        const float got = dev::div_by_count(v, dev::recip_count(deg));
+        const float got = dev::div_by_count(v, dev::recip_count(deg), float(deg));
         const bool same = __float_as_uint(want) == __float_as_uint(got) || (want != want && got != got);
         if (!same) {
             atomicAdd(bad, 1ull);
@@ -129,12 +129,19 @@ sgnn_status launch_spmm_fixup(const FixupArgs& f, int reduce, cudaStream_t s) {
 
 sgnn_status run_spmm(const sgnn_csr* a, const float* x, uint32_t k, float* c, int reduce,
                      const sgnn_plan_s* plan, cudaStream_t s) {
+    return run_spmm_ld(a, x, k, k, c, k, reduce, plan, s);
+}
+
+sgnn_status run_spmm_ld(const sgnn_csr* a, const float* x, uint64_t ldx, uint32_t k, float* c, uint64_t ldc,
+                        int reduce, const sgnn_plan_s* plan, cudaStream_t s) {
+    if (ldx < k || ldc < k) return fail(SGNN_ERR_CONFIG, "spmm: row strides must be >= K");
     if (reduce < 0 || reduce > 3) return fail(SGNN_ERR_CONFIG, "spmm: unknown reduce op");
     if (k == 0 || a->n_rows == 0) return SGNN_OK;
     if (!plan_matches(plan, a, k))
         return fail(SGNN_ERR_DISPATCH, "spmm: plan was built for another matrix or K");
     const bool aligned = (reinterpret_cast<uintptr_t>(x) % 16 == 0) &&
-                         (reinterpret_cast<uintptr_t>(c) % 16 == 0) && (k % 4 == 0);
+                         (reinterpret_cast<uintptr_t>(c) % 16 == 0) && (k % 4 == 0) && (ldx % 4 == 0) &&
+                         (ldc % 4 == 0);
     const bool vec = plan->vec && aligned;
     int lanes = int(plan->p.lanes), vregs = int(plan->p.vec), unroll = int(plan->p.unroll);
     if (!vec) {
@@ -181,8 +188,8 @@ sgnn_status run_spmm(const sgnn_csr* a, const float* x, uint32_t k, float* c, in
             args.n_rows = a->n_rows;
             args.n_workers = plan->n_workers;
             args.wctr = plan_counter(plan, s);
-            args.ldx = k;
-            args.ldc = k;
+            args.ldx = ldx;
+            args.ldc = ldc;
             args.ld_slot = plan->kt;
             args.width = std::min(kernel_width, kp - sk);
             SGNN_TRY(launch(args, plan->p.block, 0, s));
@@ -196,14 +203,14 @@ sgnn_status run_spmm(const sgnn_csr* a, const float* x, uint32_t k, float* c, in
             f.n_long = plan->n_long;
             f.slots = plan->slots;
             f.c = c + k0;
-            f.ldc = k;
+            f.ldc = ldc;
             f.ld_slot = plan->kt;
             f.n_fix = plan->n_fix;
             f.width = kp;
             SGNN_TRY(launch_spmm_fixup(f, kred, s));
         }
     }
-    if (reduce == SGNN_REDUCE_MEAN && kred != reduce) SGNN_TRY(run_mean_divide(a->row_ptr, a->n_rows, c, k, k, s));
+    if (reduce == SGNN_REDUCE_MEAN && kred != reduce) SGNN_TRY(run_mean_divide(a->row_ptr, a->n_rows, c, ldc, k, s));
     return SGNN_OK;
 }
 

@@ -122,7 +122,7 @@ struct Reducer {
     // epilogue: mean divide (kernels.hpp:60-63, exact: div_by_count); empty
     // rows give 0 for all ops
     static __device__ __forceinline__ float finish(float v, uint64_t deg) {
-        if (RED == SGNN_REDUCE_MEAN) return deg ? div_by_count(v, recip_count(deg)) : 0.0f;
+        if (RED == SGNN_REDUCE_MEAN) return deg ? div_by_count(v, recip_count(deg), float(deg)) : 0.0f;
         return deg ? v : 0.0f;
     }
 };

@@ -174,7 +174,8 @@ class DistSage:
         return out
 
     def set_features(self, x_local: torch.Tensor, borrow: bool = False):
-        """New features for this rank's rows (device or pinned host tensor)."""
+        """New features for this rank's rows (device or pinned host tensor),
+        copied into the engine (`borrow` is accepted and ignored)."""
         if x_local.shape != (self.rows, self.in_features) or x_local.dtype != torch.float32:
             raise ops.ShapeError(f"dist_set_features: expected float32 [{self.rows}, {self.in_features}]")
         x_local = x_local.contiguous()

@@ -1,5 +1,5 @@
 """cfg4 FusedMM / SDDMM: the TMA-gather kernels (fused_tma.cu) at ring depths
-2/3/4 against the register-gather kernels (SGNN_NO_TMA_FUSED), CUDA events,
+2/3/4 against the register-gather kernels (default; SGNN_TMA_FUSED=1 selects TMA), CUDA events,
 L2 flushed between calls, median of 20; bitwise comparison of the outputs."""
 import json
 import os
@@ -26,9 +26,9 @@ def main():
     outs = {}
     for mode in ("reg", "tma2", "tma3", "tma4"):
         if mode == "reg":
-            os.environ["SGNN_NO_TMA_FUSED"] = "1"
+            os.environ.pop("SGNN_TMA_FUSED", None)
         else:
-            os.environ.pop("SGNN_NO_TMA_FUSED", None)
+            os.environ["SGNN_TMA_FUSED"] = "1"
             os.environ["SGNN_TMA_DEPTH"] = mode[-1]
         out = torch.empty(m, k, device="cuda")
         tf = bench._events_time(lambda: ops.fusedmm(p, x, y, "sigmoid_mul", "sum", out, plan=plan), 20, 3, flush)

@@ -1,5 +1,5 @@
 """The row-partitioned SAGE trainer (csrc/dist.cu, sgnn_dist_* / dist.py):
-one rank against the reference's own training runs and bitwise against the
+one rank against the reference's own training runs and against the
 single-GPU native engine; P loopback ranks (the partition + exchange logic on
 one GPU) against one rank and against the reference, for symmetric and
 non-symmetric graphs; errors.  SURVEY 8e; train() = gnn.hpp:414-438."""
@@ -64,9 +64,11 @@ def test_one_rank_matches_reference_training(cuda, kind):
 
 
 @pytest.mark.parametrize("kind", ["sage-sum", "sage-mean"])
-def test_one_rank_weights_bitwise_native_engine(cuda, kind):
-    """The trainer at one rank runs the native engine's kernels in the same
-    order: final weights bit-identical to gnn.train_native's."""
+def test_one_rank_matches_native_engine(cuda, kind):
+    """The trainer at one rank against the native engine (gnn.train_native):
+    the same SpMM / head / gradient kernels; only the layer-1 products differ
+    ([a1 | X] [W1; W1s] as one product here, two products + add there), so
+    the weights agree to fp32 rounding of that sum."""
     import torch
 
     from paper_2403_14853_b200 import gnn, ops
@@ -77,8 +79,8 @@ def test_one_rank_weights_bitwise_native_engine(cuda, kind):
     nat = gnn.train_native(m, a, torch.from_numpy(x).cuda(), torch.from_numpy(lab.astype(np.int64)).cuda(),
                            torch.from_numpy(mask).cuda(), epochs=12, lr=LR)
     for got, want in zip(wts, (m.w1, m.w2, m.w1_self, m.w2_self)):
-        np.testing.assert_array_equal(got.view(np.uint32), want.cpu().numpy().view(np.uint32))
-    np.testing.assert_allclose(loss, [s.loss for s in nat.stats], rtol=1e-12)
+        np.testing.assert_allclose(got, want.cpu().numpy(), rtol=1e-4, atol=1e-6)
+    np.testing.assert_allclose(loss, [s.loss for s in nat.stats], rtol=1e-6)
 
 
 @pytest.mark.parametrize("parts", [2, 3, 5])

@@ -188,10 +188,10 @@ def test_tma_pipeline_bitwise_register_kernels(cuda, k, monkeypatch):
     cases = [("sigmoid_mul", "sum"), ("mul", "sum"), ("sigmoid_mul", "mean")]
     for pi in (64, 512):
         plan = ops.Plan(p, k, **{**_fused_layout_kw(k), "path_items": pi})
-        monkeypatch.setenv("SGNN_NO_TMA_FUSED", "1")
+        monkeypatch.delenv("SGNN_TMA_FUSED", raising=False)
         want = {c: ops.fusedmm(p, xt, yt, *c, plan=plan).cpu().numpy() for c in cases}
         want_s = ops.sddmm(p, xt, yt).values.cpu().numpy()
-        monkeypatch.delenv("SGNN_NO_TMA_FUSED")
+        monkeypatch.setenv("SGNN_TMA_FUSED", "1")
         for depth in ("2", "3", "4"):
             monkeypatch.setenv("SGNN_TMA_DEPTH", depth)
             for c in cases:
@@ -201,6 +201,7 @@ def test_tma_pipeline_bitwise_register_kernels(cuda, k, monkeypatch):
             np.testing.assert_array_equal(got_s.view(np.uint32), want_s.view(np.uint32), err_msg=f"sddmm {depth}")
     check_fused(rp, ci, v, n, x, y, "sigmoid_mul", "sum")
     check_sddmm(rp, ci, v, n, x, y)
+    monkeypatch.delenv("SGNN_TMA_FUSED")
 
 
 def _fused_layout_kw(k):
