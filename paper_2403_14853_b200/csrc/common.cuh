@@ -196,9 +196,16 @@ __device__ __forceinline__ float div_by_count_subnormal(float v, double r, float
     if (rem2 > dd || (rem2 == dd && (static_cast<long long>(q) & 1))) q += 1.0;  // ties to even
     return copysignf(float(q) * 0x1p-149f, v);
 }
-__device__ __forceinline__ float div_by_count(float v, double r, float d) {
-    if (fabsf(v) < d * 0x1p-126f) return div_by_count_subnormal(v, r, d);
+// nonzero v whose quotient by d is subnormal (zero takes the normal path)
+__device__ __forceinline__ bool count_quotient_subnormal(float v, float d) {
+    return fabsf(v) < d * 0x1p-126f && v != 0.0f;
+}
+__device__ __forceinline__ float div_by_count_normal(float v, double r) {
     return __double2float_rn(__dmul_rn(double(v), r));
+}
+__device__ __forceinline__ float div_by_count(float v, double r, float d) {
+    if (count_quotient_subnormal(v, d)) return div_by_count_subnormal(v, r, d);
+    return div_by_count_normal(v, r);
 }
 
 // L2 policy for gathered operand rows (reused across the whole launch):

@@ -125,6 +125,29 @@ struct Reducer {
         if (RED == SGNN_REDUCE_MEAN) return deg ? div_by_count(v, recip_count(deg), float(deg)) : 0.0f;
         return deg ? v : 0.0f;
     }
+    // the same over a row fragment: one reciprocal per row, and the exact
+    // subnormal-quotient path behind one (rarely taken) branch per row, so
+    // the common case never executes it predicated
+    template <int N>
+    static __device__ __forceinline__ void finish_frag(float (&v)[N], uint64_t deg) {
+        if (RED != SGNN_REDUCE_MEAN || !deg) {
+#pragma unroll
+            for (int i = 0; i < N; ++i) v[i] = deg ? v[i] : 0.0f;
+            return;
+        }
+        const double r = recip_count(deg);
+        const float d = float(deg);
+        bool exact = false;
+#pragma unroll
+        for (int i = 0; i < N; ++i) exact |= count_quotient_subnormal(v[i], d);
+        if (__builtin_expect(exact, 0)) {
+#pragma unroll
+            for (int i = 0; i < N; ++i) v[i] = div_by_count(v[i], r, d);
+        } else {
+#pragma unroll
+            for (int i = 0; i < N; ++i) v[i] = div_by_count_normal(v[i], r);
+        }
+    }
 };
 
 template <int G, int V, bool VEC>
@@ -441,8 +464,7 @@ __global__ void __launch_bounds__(128, MINB) spmm_worker_kernel(const SpmmArgs a
 #pragma unroll
                     for (int i = 0; i < N; ++i) acc.v[i] = R::combine(t.v[i], acc.v[i]);
                 }
-#pragma unroll
-                for (int i = 0; i < N; ++i) acc.v[i] = R::finish(acc.v[i], deg);
+                R::finish_frag(acc.v, deg);
                 acc.store(crow, gl, a.width);
             } else {
                 store_slot(acc);
