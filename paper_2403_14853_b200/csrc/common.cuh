@@ -208,6 +208,12 @@ __device__ __forceinline__ float div_by_count(float v, double r, float d) {
     return div_by_count_normal(v, r);
 }
 
+// (a0, a1) = fma((s, s), (w0, w1), (a0, a1)): the same as fma2_rn, named for
+// call sites where the pair runs over outputs (w0, w1 from two rows of W)
+__device__ __forceinline__ void fma2s_rn(float& a0, float& a1, float s, float w0, float w1) {
+    fma2_rn(a0, a1, s, w0, w1);
+}
+
 // L2 policy for gathered operand rows (reused across the whole launch):
 // evict-last, so the streamed CSR arrays and the output do not push them out.
 __device__ __forceinline__ uint64_t gather_policy() {

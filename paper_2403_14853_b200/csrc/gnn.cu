@@ -285,6 +285,17 @@ __device__ __forceinline__ void load_grad_row(const float* __restrict__ grad, ui
     }
 }
 
+// the same row from a shared-memory copy (c % 4 == 0)
+template <int CP>
+__device__ __forceinline__ void load_grad_row_smem(const float* grad, uint32_t i, uint32_t c, float (&g)[CP]) {
+    const float4* r = reinterpret_cast<const float4*>(grad + uint64_t(i) * c);
+#pragma unroll
+    for (int j4 = 0; j4 < CP / 4; ++j4) {
+        const float4 v = 4 * j4 < int(c) ? r[j4] : make_float4(0.f, 0.f, 0.f, 0.f);
+        g[4 * j4] = v.x; g[4 * j4 + 1] = v.y; g[4 * j4 + 2] = v.z; g[4 * j4 + 3] = v.w;
+    }
+}
+
 // W (row-major h x c) staged in shared memory for lane l's rows 4l..4l+3:
 // float4 (q, j4) of lane l = W[4l + q][4 j4 .. 4 j4 + 3] at index
 // (q * CP/4 + j4) * 32 + l, so a warp's LDS.128 hits consecutive addresses.
@@ -374,46 +385,103 @@ __global__ void __launch_bounds__(256) sage_logits_kernel(const float* __restric
 
 // Per-block partial weight gradients of the classes-wide layer:
 // part[b][m][k][j] = sum over block b's rows i of (m ? h1 : a2)[i, k] grad[i, j]
-// (g2 = a2^T grad, g2s = h1^T grad).  Warps 0-3 take a2, warps 4-7 h1; the
-// four warps of a product are combined in warp order.
+// (g2 = a2^T grad, g2s = h1^T grad).  Warps 0-3 take a2, warps 4-7 h1 (warp
+// wm of a product: rows r0 + 2 wm + 8 t, +1); the four warps of a product are
+// combined in warp order.  The a2 / h1 rows arrive in shared memory by bulk
+// copies (cp.async.bulk, one elected thread, mbarrier completion) of
+// kWgChunk-row chunks, kWgStages in flight, so the streaming read is not
+// limited by the registers of loads in flight (126 registers capped this
+// kernel at 16 warps/SM with 2 rows in flight each: 2.7 TB/s).  Bitwise the
+// register-load version (same rows per warp, same FFMA2 order).
+constexpr int kWgChunk = 32, kWgStages = 3;
 template <int CP>
 __global__ void __launch_bounds__(256) sage_wgrad_kernel(const float* __restrict__ a2, const float* __restrict__ h1,
                                                          const float* __restrict__ grad, uint32_t n, uint32_t h,
                                                          uint32_t c, uint32_t rpb, float* __restrict__ part) {
     constexpr int RU = 2;
-    __shared__ __align__(16) float red[2][128 * CP];
+    extern __shared__ __align__(128) float wsm[];  // [stages][2][kWgChunk][h] | [stages][kWgChunk][c]; then red
+    __shared__ __align__(8) uint64_t full[kWgStages];
     const uint32_t lane = threadIdx.x & 31, w = threadIdx.x >> 5, m = w >> 2, wm = w & 3;
     const bool act = lane < h / 4;
-    const float* src = m ? h1 : a2;
+    const uint32_t r0 = min(n, blockIdx.x * rpb), r1 = min(n, r0 + rpb);
+    const uint32_t nch = (r1 - r0 + kWgChunk - 1) / kWgChunk;
+    const size_t stage_floats = size_t(2) * kWgChunk * h;
+    const bool sgrad = c % 4 == 0;  // grad rows staged too (16-byte multiples)
+    float* gsm = wsm + kWgStages * stage_floats;  // [stages][kWgChunk][c]
+    auto smem_u32 = [](const void* p) { return static_cast<uint32_t>(__cvta_generic_to_shared(p)); };
+    if (threadIdx.x == 0) {
+        for (int q = 0; q < kWgStages; ++q)
+            asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(full + q)) : "memory");
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+    auto issue = [&](uint32_t q) {  // chunk q -> stage q % kWgStages (thread 0)
+        const uint32_t s = q % kWgStages, row = r0 + q * kWgChunk;
+        const uint32_t rows = min(uint32_t(kWgChunk), r1 - row);
+        const uint32_t bytes = rows * h * 4;
+        float* dst = wsm + s * stage_floats;
+        const uint32_t bar = smem_u32(full + s);
+        const uint32_t gbytes = sgrad ? rows * c * 4 : 0u;
+        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(2 * bytes + gbytes)
+                     : "memory");
+        if (sgrad)
+            asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                             smem_u32(gsm + size_t(s) * kWgChunk * c)),
+                         "l"(grad + uint64_t(row) * c), "r"(gbytes), "r"(bar)
+                         : "memory");
+        asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                         smem_u32(dst)),
+                     "l"(a2 + uint64_t(row) * h), "r"(bytes), "r"(bar)
+                     : "memory");
+        asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                         smem_u32(dst + kWgChunk * h)),
+                     "l"(h1 + uint64_t(row) * h), "r"(bytes), "r"(bar)
+                     : "memory");
+    };
+    if (threadIdx.x == 0)
+        for (uint32_t q = 0; q < min(nch, uint32_t(kWgStages)); ++q) issue(q);
     float acc[4][CP];
 #pragma unroll
     for (int q = 0; q < 4; ++q)
 #pragma unroll
         for (int j = 0; j < CP; ++j) acc[q][j] = 0.0f;
-    const uint32_t r0 = blockIdx.x * rpb, r1 = min(n, r0 + rpb);
-    if (act) {
-        for (uint32_t i = r0 + wm * RU; i < r1; i += 4 * RU) {
-            float4 x[RU];
-            float g[RU][CP];
+    for (uint32_t q = 0; q < nch; ++q) {
+        const uint32_t s = q % kWgStages, row = r0 + q * kWgChunk;
+        const uint32_t rows = min(uint32_t(kWgChunk), r1 - row);
+        asm volatile(
+            "{\n.reg .pred p;\nWAIT_%=:\nmbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n@!p bra WAIT_%=;\n}\n" ::"r"(
+                smem_u32(full + s)),
+            "r"((q / kWgStages) & 1)
+            : "memory");
+        const float* src = wsm + s * stage_floats + size_t(m) * kWgChunk * h;
+        if (act) {
+            for (uint32_t lr = wm * RU; lr < rows; lr += 4 * RU) {
+                float4 x[RU];
+                float g[RU][CP];
 #pragma unroll
-            for (int r = 0; r < RU; ++r) {
-                const bool ok = i + r < r1;
-                x[r] = ok ? __ldg(reinterpret_cast<const float4*>(src + uint64_t(i + r) * h) + lane)
-                          : make_float4(0.f, 0.f, 0.f, 0.f);
-                load_grad_row<CP>(grad, ok ? i + r : i, c, g[r]);
-            }
+                for (int r = 0; r < RU; ++r) {
+                    const bool ok = lr + r < rows;
+                    x[r] = ok ? reinterpret_cast<const float4*>(src + size_t(lr + r) * h)[lane]
+                              : make_float4(0.f, 0.f, 0.f, 0.f);
+                    if (sgrad) load_grad_row_smem<CP>(gsm + size_t(s) * kWgChunk * c, ok ? lr + r : lr, c, g[r]);
+                    else load_grad_row<CP>(grad, ok ? row + lr + r : row + lr, c, g[r]);
+                }
 #pragma unroll
-            for (int r = 0; r < RU; ++r) {
-                const float xs[4] = {x[r].x, x[r].y, x[r].z, x[r].w};  // zero past r1
-                // packed FFMA2 over class pairs: each half an ordinary fma
+                for (int r = 0; r < RU; ++r) {
+                    const float xs[4] = {x[r].x, x[r].y, x[r].z, x[r].w};  // zero past the block's rows
+                    // packed FFMA2 over class pairs: each half an ordinary fma
 #pragma unroll
-                for (int q = 0; q < 4; ++q)
+                    for (int qq = 0; qq < 4; ++qq)
 #pragma unroll
-                    for (int j = 0; j < CP; j += 2)
-                        sgnn::dev::fma2_rn(acc[q][j], acc[q][j + 1], xs[q], g[r][j], g[r][j + 1]);
+                        for (int j = 0; j < CP; j += 2)
+                            sgnn::dev::fma2_rn(acc[qq][j], acc[qq][j + 1], xs[qq], g[r][j], g[r][j + 1]);
+                }
             }
         }
+        __syncthreads();  // stage s consumed by every warp
+        if (threadIdx.x == 0 && q + kWgStages < nch) issue(q + kWgStages);
     }
+    float(*red)[128 * CP] = reinterpret_cast<float(*)[128 * CP]>(wsm);  // stages are free now
     for (uint32_t step = 0; step < 4; ++step) {
         if (wm == step && act) {
 #pragma unroll
@@ -428,6 +496,11 @@ __global__ void __launch_bounds__(256) sage_wgrad_kernel(const float* __restrict
     }
     float* out = part + uint64_t(blockIdx.x) * 2 * h * CP;
     for (uint32_t t = threadIdx.x; t < 2 * h * CP; t += blockDim.x) out[t] = red[t / (h * CP)][t % (h * CP)];
+}
+
+size_t sage_wgrad_smem(uint32_t h, uint32_t c, int cp) {
+    return std::max(size_t(kWgStages) * kWgChunk * (2 * h + (c % 4 == 0 ? c : 0)), size_t(2) * 128 * cp) *
+           sizeof(float);
 }
 
 // g2 / g2s (h x c row-major) = sum of the block partials in block order
@@ -560,10 +633,9 @@ __global__ void __launch_bounds__(256) sage_head_kernel(
                         for (int r = 0; r < R; ++r) {
                             const float xv = q == 0 ? x[m][r].x : q == 1 ? x[m][r].y : q == 2 ? x[m][r].z : x[m][r].w;
                             float* pr = p + r * CP + 4 * j4;
-                            pr[0] = __fmaf_rn(xv, wv.x, pr[0]);
-                            pr[1] = __fmaf_rn(xv, wv.y, pr[1]);
-                            pr[2] = __fmaf_rn(xv, wv.z, pr[2]);
-                            pr[3] = __fmaf_rn(xv, wv.w, pr[3]);
+                            // packed FFMA2 over class pairs (each half an ordinary fma)
+                            sgnn::dev::fma2_rn(pr[0], pr[1], xv, wv.x, wv.y);
+                            sgnn::dev::fma2_rn(pr[2], pr[3], xv, wv.z, wv.w);
                         }
                     }
             // 32-value transpose-reduce: lane l ends with index l
@@ -627,16 +699,24 @@ __global__ void __launch_bounds__(256) sage_head_kernel(
             for (int b = 0; b < NB; ++b) {
                 const uint32_t fb = gl + CP * b;  // feature block: features 4 fb .. 4 fb + 3
                 if (fb >= h / 4) break;
+                // features (4 fb + q, 4 fb + q + 1) as packed pairs: each half
+                // is sage_grad_wt_kernel's chain (mul, then fmas in class order)
                 float d[4];
 #pragma unroll
-                for (int q = 0; q < 4; ++q) {
+                for (int q = 0; q < 4; q += 2) {
 #pragma unroll
                     for (int j4 = 0; j4 < J4; ++j4) {
-                        const float4 wv = sw[0][(q * J4 + j4) * 32 + fb];
-                        float t = j4 == 0 ? __fmul_rn(gj[0], wv.x) : __fmaf_rn(gj[4 * j4], wv.x, d[q]);
-                        t = __fmaf_rn(gj[4 * j4 + 1], wv.y, t);
-                        t = __fmaf_rn(gj[4 * j4 + 2], wv.z, t);
-                        d[q] = __fmaf_rn(gj[4 * j4 + 3], wv.w, t);
+                        const float4 wa = sw[0][(q * J4 + j4) * 32 + fb];
+                        const float4 wb = sw[0][((q + 1) * J4 + j4) * 32 + fb];
+                        if (j4 == 0) {
+                            d[q] = __fmul_rn(gj[0], wa.x);
+                            d[q + 1] = __fmul_rn(gj[0], wb.x);
+                        } else {
+                            sgnn::dev::fma2s_rn(d[q], d[q + 1], gj[4 * j4], wa.x, wb.x);
+                        }
+                        sgnn::dev::fma2s_rn(d[q], d[q + 1], gj[4 * j4 + 1], wa.y, wb.y);
+                        sgnn::dev::fma2s_rn(d[q], d[q + 1], gj[4 * j4 + 2], wa.z, wb.z);
+                        sgnn::dev::fma2s_rn(d[q], d[q + 1], gj[4 * j4 + 3], wa.w, wb.w);
                     }
                 }
                 reinterpret_cast<float4*>(ds2 + uint64_t(i) * h)[fb] = make_float4(d[0], d[1], d[2], d[3]);
@@ -906,9 +986,8 @@ sgnn_status epoch(sgnn_gnn_s* g, float lr, cudaStream_t s) {
         SGNN_TRY(mm_tn(g, g->x, g->d_h, g->g1, n, in, hid, s));
     } else if (g->kind == kSageSum || g->kind == kSageMean) {
         if (g->skinny) {
-            SAGE_CP(sage_wgrad_kernel, g->cls, g->wg_blocks, 256, (g->a2, g->h1, g->grad, g->n, g->hid, g->cls, g->wg_rpb, g->wg_part));
-            SAGE_CP(sage_wgrad_finish_kernel, g->cls, unsigned((2 * g->hid * 16 + 127) / 128), 128,
-                    (g->wg_part, g->wg_blocks, g->hid, g->cls, g->g2, g->g2s));
+            SGNN_TRY(sage_wgrad_launch(g->a2, g->h1, g->grad, g->n, g->hid, g->cls, g->wg_rpb, g->wg_blocks, g->wg_part,
+                                       g->g2, g->g2s, s));
             // ds2 = grad W2^T is already in d_h (sage_head_kernel)
             SGNN_TRY(cache_spmm_backward(g->cache, g->d_h, g->n, g->hid, g->d_h2, red, s));          // dh1 (A^T part)
             // dz1 = relu_backward(dh1 + grad W2s^T, h1) into z1 (free after the forward)
@@ -1270,10 +1349,22 @@ sgnn_status sage_head_partials(const float* a2, const float* h1, const float* w2
     return SGNN_OK;
 }
 
+template <int CP>
+sgnn_status wgrad_launch_cp(const float* a2, const float* h1, const float* grad, uint32_t n, uint32_t h, uint32_t c,
+                            uint32_t rpb, uint32_t nblk, float* part, cudaStream_t s) {
+    const size_t smem = sage_wgrad_smem(h, c, CP);
+    SGNN_CUDA_TRY(cudaFuncSetAttribute(sage_wgrad_kernel<CP>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+    sage_wgrad_kernel<CP><<<nblk, 256, smem, s>>>(a2, h1, grad, n, h, c, rpb, part);
+    SGNN_LAUNCH_CHECK();
+    return SGNN_OK;
+}
+
 sgnn_status sage_wgrad_launch(const float* a2, const float* h1, const float* grad, uint32_t n, uint32_t h,
                               uint32_t c, uint32_t rpb, uint32_t nblk, float* part, float* g2, float* g2s,
                               cudaStream_t s) {
-    SAGE_CP(sage_wgrad_kernel, c, nblk, 256, (a2, h1, grad, n, h, c, rpb, part));
+    if (c <= 4) SGNN_TRY(wgrad_launch_cp<4>(a2, h1, grad, n, h, c, rpb, nblk, part, s));
+    else if (c <= 8) SGNN_TRY(wgrad_launch_cp<8>(a2, h1, grad, n, h, c, rpb, nblk, part, s));
+    else SGNN_TRY(wgrad_launch_cp<16>(a2, h1, grad, n, h, c, rpb, nblk, part, s));
     SAGE_CP(sage_wgrad_finish_kernel, c, unsigned((2 * h * 16 + 127) / 128), 128, (part, nblk, h, c, g2, g2s));
     return SGNN_OK;
 }
