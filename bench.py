@@ -301,6 +301,8 @@ def run_cfg5(args):
         "epoch_ms": round(epoch_ms, 4), "epoch_ms_mean": round(total_max / K, 4),
         "spmm_ms": round(float(np.median(sp_max)), 4), "compute_ms": round(float(np.median(comp_max)), 4),
         "exchange_ms": round(float(np.median(ex_max)), 4),
+        "dense_ms": round(float(np.median(times[:, 7])), 4),
+        "sparse_gflops": round(flops / (float(np.median(sp_max)) * 1e-3) / 1e9, 2),
         "loss_first_last": [round(float(loss[0]), 6), round(float(loss[-1]), 6)],
         "accuracy_last": round(float(acc[-1]), 6),
         "roofline": roof,

@@ -392,9 +392,11 @@ sgnn_status sgnn_dist_epochs(sgnn_dist* engines, int n_engines, uint32_t epochs,
  * loss[i], accuracy[i], and times[i*SGNN_DIST_TIMES + j] in device ms:
  * j=0 epoch, 1 the three SpMMs, 2 this rank's compute phases, 3 = epoch - compute
  * (exchanges and waiting for peers; loopback: also the other virtual ranks'
- * phases), 4/5/6 the layer-1 / layer-2 / backward SpMM.
- * Any output may be NULL.  Synchronizes the stream. */
-#define SGNN_DIST_TIMES 7
+ * phases), 4/5/6 the layer-1 / layer-2 / backward SpMM, 7 the two dense
+ * products ([a1 | X] [W1; W1s] and its weight gradient; timed apart from
+ * the sparse path as BASELINE asks).  Any output may be NULL.  Synchronizes
+ * the stream. */
+#define SGNN_DIST_TIMES 8
 sgnn_status sgnn_dist_stats(sgnn_dist g, uint32_t first, uint32_t count, double* loss, double* accuracy,
                             double* times, sgnn_stream stream);
 /* (loss, accuracy) pairs of epochs [first, first+count) copied to dst

@@ -187,8 +187,8 @@ struct sgnn_comm_s {
 
 // ------------------------------------------------------------------- engine
 enum Mark {  // per-epoch event markers (P*_S / P*_E: a compute phase of this rank)
-    M_BEGIN, M_X, M_P0_S, M_SPMM1_0, M_SPMM1_1, M_P0_E, M_EX1, M_P1_S, M_SPMM2_0, M_SPMM2_1, M_P1_E, M_EX2, M_P2_S,
-    M_SPMMB_0, M_SPMMB_1, M_P2_E, M_EX3, M_P3_S, M_END, M_COUNT
+    M_BEGIN, M_X, M_P0_S, M_SPMM1_0, M_SPMM1_1, M_GEMM1_1, M_P0_E, M_EX1, M_P1_S, M_SPMM2_0, M_SPMM2_1, M_P1_E, M_EX2,
+    M_P2_S, M_SPMMB_0, M_SPMMB_1, M_GEMM2_0, M_P2_E, M_EX3, M_P3_S, M_END, M_COUNT
 };
 
 struct sgnn_dist_s {
@@ -428,6 +428,7 @@ sgnn_status phase0(sgnn_dist_s* g, uint32_t e, cudaStream_t s) {
         SGNN_TRY(sgnn::run_spmm_ld(&g->fwd, g->x_operand(), g->x_ld(), g->in, g->ax, 2ull * g->in, red, g->plan_in, s));
     DIST_MARK(g, M_SPMM1_1);
     SGNN_TRY(mm(g, g->ax, g->wpack + g->off_w1, g->z1, g->rows, 2 * g->in, g->hid, s));  // [a1 | X_r] [W1; W1s]
+    DIST_MARK(g, M_GEMM1_1);
     SGNN_TRY(sgnn::glue_relu(g->z1, uint64_t(g->rows) * g->hid, g->h1_full + uint64_t(g->r0) * g->hid, s));
     DIST_MARK(g, M_P0_E);
     return SGNN_OK;
@@ -465,6 +466,7 @@ sgnn_status phase2(sgnn_dist_s* g, uint32_t e, cudaStream_t s) {
     if (g->rows) SGNN_TRY(sgnn::run_spmm(&g->bwd, g->ds2_full, g->hid, g->dh1, SGNN_REDUCE_SUM, g->plan_bwd, s));
     DIST_MARK(g, M_SPMMB_1);
     SGNN_TRY(sgnn::glue_sage_grad_wt(g->grad, g->wpack + g->off_w2s, g->rows, g->hid, g->cls, g->dh1, h1r, g->z1, s));
+    DIST_MARK(g, M_GEMM2_0);
     SGNN_TRY(mm_tn(g, g->ax, g->z1, g->gpack + g->off_w1, g->rows, 2 * g->in, g->hid, s));  // [g1; g1s] = ax^T dz1
     DIST_MARK(g, M_P2_E);
     return SGNN_OK;
@@ -804,6 +806,7 @@ sgnn_status sgnn_dist_stats(sgnn_dist g, uint32_t first, uint32_t count, double*
             t[4] = el(M_SPMM1_0, M_SPMM1_1);
             t[5] = el(M_SPMM2_0, M_SPMM2_1);
             t[6] = el(M_SPMMB_0, M_SPMMB_1);
+            t[7] = el(M_SPMM1_1, M_GEMM1_1) + el(M_GEMM2_0, M_P2_E);  // the two dense products
         }
     }
     return SGNN_OK;

@@ -27,7 +27,7 @@ from . import _lib, graphs, ops
 from ._lib import check, lib
 
 KIND_IDS = {"sage-sum": 1, "sage-mean": 2}
-TIME_FIELDS = ("epoch_ms", "spmm_ms", "compute_ms", "exchange_ms", "spmm1_ms", "spmm2_ms", "spmm_bwd_ms")
+TIME_FIELDS = ("epoch_ms", "spmm_ms", "compute_ms", "exchange_ms", "spmm1_ms", "spmm2_ms", "spmm_bwd_ms", "dense_ms")
 ROW_WEIGHT = 30  # GPU partition cost: nnz + ROW_WEIGHT * rows (DESIGN 6)
 
 
@@ -198,7 +198,7 @@ class DistSage:
             e.epochs_run += n
 
     def stats(self, first: int = 0, count: int | None = None):
-        """(loss[], accuracy[], times[count x 7]) of epochs [first, first+count)."""
+        """(loss[], accuracy[], times[count x 8]) of epochs [first, first+count)."""
         count = self.epochs_run - first if count is None else count
         loss = np.zeros(count)
         acc = np.zeros(count)
