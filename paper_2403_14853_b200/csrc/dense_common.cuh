@@ -23,6 +23,10 @@ namespace dense {
 using namespace cute;
 using TileShape = Shape<_128, _128, _16>;
 using ClusterShape = Shape<_1, _1, _1>;
+using Tile2Sm = Shape<_256, _128, _16>;     // 256 x 128 tiles on SM pairs (cta_group::2)
+using Cluster2Sm = Shape<_2, _1, _1>;
+using LinComb = cutlass::epilogue::fusion::LinearCombination<float, float, float, float>;
+using LinCombRelu = cutlass::epilogue::fusion::LinCombEltAct<cutlass::epilogue::thread::ReLu, float, float, float, float>;
 
 // The kernel for given operand layouts and tile scheduler, spelled out at
 // namespace scope in each translation unit (SGNN_DENSE_GEMM) -- nvcc's host
@@ -31,10 +35,15 @@ using ClusterShape = Shape<_1, _1, _1>;
     SGNN_DENSE_GEMM_CFG(NAME, LAYOUT_A, LAYOUT_B, SCHEDULER, sgnn::dense::TileShape, sgnn::dense::ClusterShape, \
                         cutlass::epilogue::TmaWarpSpecialized1Sm, cutlass::gemm::KernelTmaWarpSpecialized1SmFastFP32Sm100)
 #define SGNN_DENSE_GEMM_CFG(NAME, LAYOUT_A, LAYOUT_B, SCHEDULER, TILE, CLUSTER, EPI_SCHED, MMA_SCHED)              \
+    SGNN_DENSE_GEMM_FUSED(NAME, LAYOUT_A, LAYOUT_B, SCHEDULER, TILE, CLUSTER, EPI_SCHED, MMA_SCHED,               \
+                          sgnn::dense::LinComb)
+// (FUSION: the epilogue's per-element op, e.g. LinCombEltAct<ReLu, ...> to
+// write relu(A B) directly)
+#define SGNN_DENSE_GEMM_FUSED(NAME, LAYOUT_A, LAYOUT_B, SCHEDULER, TILE, CLUSTER, EPI_SCHED, MMA_SCHED, FUSION)    \
     using NAME##_Epilogue = typename cutlass::epilogue::collective::CollectiveBuilder<                          \
         cutlass::arch::Sm100, cutlass::arch::OpClassTensorOp, TILE, CLUSTER,                                      \
         cutlass::epilogue::collective::EpilogueTileAuto, float, float, float, cutlass::layout::RowMajor, 4, float, \
-        cutlass::layout::RowMajor, 4, EPI_SCHED>::CollectiveOp;                                                   \
+        cutlass::layout::RowMajor, 4, EPI_SCHED, FUSION>::CollectiveOp;                                           \
     using NAME##_Mainloop = typename cutlass::gemm::collective::CollectiveBuilder<                              \
         cutlass::arch::Sm100, cutlass::arch::OpClassTensorOp, float, LAYOUT_A, 4, float, LAYOUT_B, 4, float,      \
         TILE, CLUSTER,                                                                                            \

@@ -9,6 +9,7 @@
 namespace sgnn {
 int dense_mm_nn(int, int, int, const float*, const float*, float*, float, void*, size_t, cudaStream_t) { return 1; }
 int dense_mm_tn(int, int, int, const float*, const float*, float*, int, void*, size_t, cudaStream_t) { return 1; }
+int dense_mm_nn_relu(int, int, int, const float*, const float*, float*, void*, size_t, cudaStream_t) { return 1; }
 int dense_mm_nn_workspace(int, int, int, size_t*) { return 1; }
 int dense_mm_tn_workspace(int, int, int, int, size_t*) { return 1; }
 }  // namespace sgnn

@@ -427,9 +427,16 @@ sgnn_status phase0(sgnn_dist_s* g, uint32_t e, cudaStream_t s) {
     if (g->rows)  // a1 into the left half of ax
         SGNN_TRY(sgnn::run_spmm_ld(&g->fwd, g->x_operand(), g->x_ld(), g->in, g->ax, 2ull * g->in, red, g->plan_in, s));
     DIST_MARK(g, M_SPMM1_1);
-    SGNN_TRY(mm(g, g->ax, g->wpack + g->off_w1, g->z1, g->rows, 2 * g->in, g->hid, s));  // [a1 | X_r] [W1; W1s]
+    // h1_r = relu([a1 | X_r] [W1; W1s]): relu in the product's epilogue, or a separate pass
+    float* h1r = g->h1_full + uint64_t(g->r0) * g->hid;
+    const float* w1cat = g->wpack + g->off_w1;
+    if (!(tall_ok(g, g->rows, 2 * g->in, g->hid, {g->ax, w1cat, h1r}) &&
+          sgnn::dense_mm_nn_relu(int(g->rows), int(g->hid), int(2 * g->in), g->ax, w1cat, h1r, g->ws, g->ws_bytes,
+                                 s) == 0)) {
+        SGNN_TRY(mm(g, g->ax, w1cat, g->z1, g->rows, 2 * g->in, g->hid, s));
+        SGNN_TRY(sgnn::glue_relu(g->z1, uint64_t(g->rows) * g->hid, h1r, s));
+    }
     DIST_MARK(g, M_GEMM1_1);
-    SGNN_TRY(sgnn::glue_relu(g->z1, uint64_t(g->rows) * g->hid, g->h1_full + uint64_t(g->r0) * g->hid, s));
     DIST_MARK(g, M_P0_E);
     return SGNN_OK;
 }

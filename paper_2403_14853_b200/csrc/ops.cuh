@@ -80,6 +80,9 @@ int dense_mm_nn(int m, int n, int k, const float* a, const float* b, float* c, f
                 cudaStream_t s);
 int dense_mm_tn(int m, int n, int k, const float* a, const float* b, float* c, int splits, void* ws, size_t ws_bytes,
                 cudaStream_t s);
+// C = relu(A B) (the activation in the product's epilogue)
+int dense_mm_nn_relu(int m, int n, int k, const float* a, const float* b, float* c, void* ws, size_t ws_bytes,
+                     cudaStream_t s);
 // workspace bytes the products need for this shape (nonzero return: shape refused)
 int dense_mm_nn_workspace(int m, int n, int k, size_t* bytes);
 int dense_mm_tn_workspace(int m, int n, int k, int splits, size_t* bytes);
