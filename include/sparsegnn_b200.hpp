@@ -40,6 +40,7 @@
 #include <vector>
 
 #include "sgnn_b200.h"
+#include "sgnn_host.h"
 
 namespace sparsegnn_b200 {
 
@@ -631,5 +632,115 @@ TrainOutput train(Model& model, const Csr& a, const Dense& x, const Labels& labe
     out.symmetric = sym != 0;
     return out;
 }
+
+// ------------------------------------------- multi-GPU: row-partitioned SAGE
+/// The communicator of the row partition (sgnn_comm_*): one process per GPU
+/// over NCCL (the 128-byte id from rank 0 travels over the caller's channel),
+/// or P virtual ranks in one process (loopback).
+class Comm {
+public:
+    static std::vector<std::uint8_t> unique_id() {
+        std::vector<std::uint8_t> id(SGNN_COMM_ID_BYTES);
+        check(sgnn_comm_get_unique_id(id.data()));
+        return id;
+    }
+    static Comm nccl(const std::vector<std::uint8_t>& id, int nranks, int rank) {
+        Comm c;
+        check(sgnn_comm_init_rank(id.data(), nranks, rank, &c.h_));
+        return c;
+    }
+    static Comm loopback(int nranks) {
+        Comm c;
+        check(sgnn_comm_init_loopback(nranks, &c.h_));
+        return c;
+    }
+    Comm() = default;
+    Comm(Comm&& o) noexcept : h_(o.h_) { o.h_ = nullptr; }
+    Comm& operator=(Comm&& o) noexcept {
+        std::swap(h_, o.h_);
+        return *this;
+    }
+    ~Comm() { if (h_) sgnn_comm_destroy(h_); }
+    sgnn_comm get() const { return h_; }
+
+private:
+    sgnn_comm h_ = nullptr;
+};
+
+/// Contiguous row bounds of equal nnz + row_weight * rows cost
+/// (balanced_row_partition, parallel.hpp:28-41, at GPU granularity).
+template <class Csr>
+std::vector<std::uint32_t> row_partition(const Csr& a, int parts, std::uint32_t row_weight = 30) {
+    std::vector<std::uint32_t> b(std::size_t(parts) + 1);
+    sgnn_host_weighted_row_partition(a.row_ptr.data(), a.n_rows, parts, row_weight, b.data());
+    return b;
+}
+
+/// One rank of the row-partitioned SAGE trainer (train(), gnn.hpp:414-438,
+/// on rows [bounds[rank], bounds[rank+1]) of a symmetric A): the rank's
+/// block is uploaded from the caller's host CSR and features.
+class PartitionedSage {
+public:
+    template <class Csr, class Dense, class Labels, class Mask>
+    PartitionedSage(const Comm* comm, int rank, const std::vector<std::uint32_t>& bounds, const Csr& a, const Dense& x,
+                    const Labels& labels, const Mask& mask, int model_kind /* 1 sum, 2 mean */, index_t hidden,
+                    index_t classes, std::uint32_t max_epochs = 128)
+        : r0_(bounds.at(std::size_t(rank))), rows_(bounds.at(std::size_t(rank) + 1) - r0_) {
+        const offset_t e0 = a.row_ptr[r0_], e1 = a.row_ptr[r0_ + rows_];
+        std::vector<offset_t> rp(rows_ + 1);
+        for (index_t i = 0; i <= rows_; ++i) rp[i] = a.row_ptr[r0_ + i] - e0;
+        std::vector<float> v(a.values.begin() + std::ptrdiff_t(e0), a.values.begin() + std::ptrdiff_t(e1));
+        rp_ = DeviceBuffer<offset_t>(rp.data(), rp.size());
+        ci_ = DeviceBuffer<index_t>(a.col_idx.data() + e0, std::size_t(e1 - e0));
+        v_ = DeviceBuffer<float>(v.data(), v.size());
+        const sgnn_csr blk{rows_, a.n_cols, e1 - e0, rp_.get(), ci_.get(), v_.get()};
+        std::vector<float> xr(x.data.begin() + std::ptrdiff_t(std::size_t(r0_) * x.n_cols),
+                              x.data.begin() + std::ptrdiff_t(std::size_t(r0_ + rows_) * x.n_cols));
+        std::vector<std::uint32_t> lab(labels.begin() + r0_, labels.begin() + r0_ + rows_);
+        std::vector<std::uint8_t> msk(mask.begin() + r0_, mask.begin() + r0_ + rows_);
+        check(sgnn_dist_create(comm ? comm->get() : nullptr, rank, bounds.data(), &blk, nullptr, model_kind, x.n_cols,
+                               hidden, classes, xr.data(), lab.data(), msk.data(), max_epochs, &h_, nullptr));
+    }
+    ~PartitionedSage() { if (h_) sgnn_dist_destroy(h_); }
+    PartitionedSage(const PartitionedSage&) = delete;
+    PartitionedSage& operator=(const PartitionedSage&) = delete;
+
+    /// Weights in the model's layout (w1, w2, w1_self, w2_self with `data`).
+    template <class Model>
+    void set_weights(const Model& m) {
+        auto f = [](const auto& w) { return std::vector<float>(w.data.begin(), w.data.end()); };
+        const auto w1 = f(m.w1), w2 = f(m.w2), w1s = f(m.w1_self), w2s = f(m.w2_self);
+        check(sgnn_dist_set_weights(h_, w1.data(), w2.data(), w1s.data(), w2s.data(), nullptr));
+    }
+    /// `epochs` epochs on this rank alone (NCCL rank or one rank).
+    void epochs(std::uint32_t n, float lr) {
+        sgnn_dist g = h_;
+        check(sgnn_dist_epochs(&g, 1, n, lr, nullptr));
+        run_ += n;
+    }
+    /// Loopback: all P ranks of one communicator, in rank order.
+    static void epochs_group(std::vector<PartitionedSage*>& ranks, std::uint32_t n, float lr) {
+        std::vector<sgnn_dist> hs;
+        for (auto* r : ranks) hs.push_back(r->h_);
+        check(sgnn_dist_epochs(hs.data(), int(hs.size()), n, lr, nullptr));
+        for (auto* r : ranks) r->run_ += n;
+    }
+    /// Per-epoch loss (the global masked mean) of the epochs run so far.
+    std::vector<double> losses() const {
+        std::vector<double> l(run_);
+        if (run_) check(sgnn_dist_stats(h_, 0, run_, l.data(), nullptr, nullptr, nullptr));
+        return l;
+    }
+    index_t row0() const { return r0_; }
+    index_t rows() const { return rows_; }
+
+private:
+    index_t r0_ = 0, rows_ = 0;
+    DeviceBuffer<offset_t> rp_;
+    DeviceBuffer<index_t> ci_;
+    DeviceBuffer<float> v_;
+    sgnn_dist h_ = nullptr;
+    std::uint32_t run_ = 0;
+};
 
 }  // namespace sparsegnn_b200

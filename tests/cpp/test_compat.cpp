@@ -2,6 +2,7 @@
 // the reference's operator API is used, checked against the SPEC known
 // answers and the CPU oracle (oracle/liboracle.so, test infrastructure).
 // Run by tests/test_cpp_compat.py on the GPU box.
+#include <cmath>
 #include <cstdio>
 #include <cstdlib>
 #include <random>
@@ -233,6 +234,30 @@ int main() {
         EXPECT(m1.w1.data == m2.w1.data && m1.w2.data == m2.w2.data);
         for (std::size_t i = 0; i < r1.stats.size(); ++i) EXPECT(r1.stats[i].loss == r2.stats[i].loss);
         EXPECT(throws<sg::ConfigError>([&] { sg::TrainOptions bad; bad.epochs = 0; sg::train(m1, a, x, labels, mask, bad); }));
+        // ---- the row-partitioned SAGE-mean trainer from C++ (sgnn_dist_*):
+        // one rank vs two loopback ranks of a balanced_row_partition
+        struct SModel {
+            Dense w1, w2, w1_self, w2_self;
+        } sm{Dense(f, hid), Dense(hid, cls), Dense(f, hid), Dense(hid, cls)};
+        std::mt19937_64 gs(11);
+        std::uniform_real_distribution<float> us(-0.4f, 0.4f);
+        for (Dense* w : {&sm.w1, &sm.w2, &sm.w1_self, &sm.w2_self})
+            for (auto& v : w->data) v = us(gs);
+        sg::PartitionedSage one(nullptr, 0, {0u, n}, a, x, labels, mask, 2, hid, cls, 32);
+        one.set_weights(sm);
+        one.epochs(15, 0.5f);
+        sg::Comm comm = sg::Comm::loopback(2);
+        const std::vector<uint32_t> b = sg::row_partition(a, 2, 1);
+        sg::PartitionedSage p0(&comm, 0, b, a, x, labels, mask, 2, hid, cls, 32);
+        sg::PartitionedSage p1(&comm, 1, b, a, x, labels, mask, 2, hid, cls, 32);
+        p0.set_weights(sm);
+        p1.set_weights(sm);
+        std::vector<sg::PartitionedSage*> ranks{&p0, &p1};
+        sg::PartitionedSage::epochs_group(ranks, 15, 0.5f);
+        const auto l1 = one.losses(), l2 = p0.losses();
+        EXPECT(l1.size() == 15u && l2.size() == 15u && l1.back() < l1.front());
+        EXPECT(p0.rows() + p1.rows() == n && p1.row0() == p0.rows());
+        for (std::size_t i = 0; i < l1.size() && i < l2.size(); ++i) EXPECT(std::fabs(l1[i] - l2[i]) <= 1e-5 * std::fabs(l1[i]));
     }
     // ---- io.hpp drop-in: load_mtx / save_mtx round trip, ParseError lines
     {
