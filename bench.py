@@ -522,7 +522,7 @@ def run_loopback_cfg5(args):
     spmm = np.array([np.median(e.stats(W, K)[2][:, 1]) for e in engs])
     loss = engs[0].stats(W, K)[0]
     rows = np.diff(bounds.astype(np.int64))
-    recv = [(w.n_rows - int(r)) * 128 * 4 * 2 for r in rows]  # h1 + ds2 all-gathers per epoch (X gathered once)
+    recv = [(w.n_rows - int(r)) * (128 + 16) * 4 for r in rows]  # h1 + grad all-gathers per epoch (X gathered once)
     print(json.dumps({"loopback_ranks": P, "row_weight": args.row_weight, "bounds": [int(b) for b in bounds],
                       "rank_compute_ms": [round(float(c), 3) for c in comp],
                       "rank_spmm_ms": [round(float(c), 3) for c in spmm],

@@ -18,8 +18,9 @@
 //   exch     all-gather h1
 //   phase 1  a2 = A_r h1; logits, softmax_xent + accuracy and ds2_r = grad W2^T
 //            in one pass (sage_head_kernel); W2/W2s gradients     (:241-244, :318-370, :283-289)
-//   exch     all-gather ds2
-//   phase 2  dh1 = M_r ds2 (M = mean/sum backward operand rows), dz1 =
+//   exch     all-gather grad (16 floats a row, not ds2's 128)
+//   phase 2  the other ranks' ds2 rows = their grad rows W2^T (bitwise the
+//            owners'), dh1 = M_r ds2 (M = mean/sum backward operand rows), dz1 =
 //            relu_backward(dh1 + grad W2s^T), W1/W1s gradients    (:290-296)
 //   exch     all-reduce gradients + (loss, correct)
 //   phase 3  sgd_step (:374-386), epoch stats
@@ -216,7 +217,9 @@ struct sgnn_dist_s {
     // weight gradient one A^T B); with one rank X_r is also the SpMM operand
     // (row stride 2 in), with P ranks the gathered x_full [n x in] is.
     float *ax = nullptr, *x_full = nullptr, *h1_full = nullptr, *ds2_full = nullptr;
-    float *a2 = nullptr, *z1 = nullptr, *dh1 = nullptr, *grad = nullptr;
+    float *a2 = nullptr, *z1 = nullptr, *dh1 = nullptr;
+    float* grad_full = nullptr;  // [n x classes]: the rank's rows at r0, the others gathered
+    float* grad() const { return grad_full + uint64_t(r0) * cls; }
     uint32_t* labels = nullptr;
     uint8_t* mask = nullptr;
     uint32_t* deg = nullptr;  // global degrees [n] (gathered)
@@ -451,12 +454,12 @@ sgnn_status phase1(sgnn_dist_s* g, uint32_t e, cudaStream_t s) {
     DIST_MARK(g, M_SPMM2_1);
     // logits, softmax_xent + accuracy, grad, ds2_r = grad W2^T in one pass
     SGNN_TRY(sgnn::sage_head_partials(g->a2, h1r, g->wpack + g->off_w2, g->wpack + g->off_w2s, g->rows, g->hid,
-                                      g->cls, g->labels, g->mask, g->inv_n, g->grad,
+                                      g->cls, g->labels, g->mask, g->inv_n, g->grad(),
                                       g->ds2_full + uint64_t(g->r0) * g->hid, g->blk_loss, g->blk_ok, s));
     rank_stats_kernel<<<1, 256, 0, s>>>(g->blk_loss, g->blk_ok, g->rows ? g->sm_blocks : 0, g->red);
     SGNN_LAUNCH_CHECK();
     if (g->rows) {
-        SGNN_TRY(sgnn::sage_wgrad_launch(g->a2, h1r, g->grad, g->rows, g->hid, g->cls, g->wg_rpb, g->wg_blocks,
+        SGNN_TRY(sgnn::sage_wgrad_launch(g->a2, h1r, g->grad(), g->rows, g->hid, g->cls, g->wg_rpb, g->wg_blocks,
                                          g->wg_part, g->gpack + g->off_w2, g->gpack + g->off_w2s, s));
     } else {
         SGNN_CUDA_TRY(cudaMemsetAsync(g->gpack + g->off_w2, 0, sizeof(float) * (g->pack_n - g->off_w2), s));
@@ -469,10 +472,20 @@ sgnn_status phase1(sgnn_dist_s* g, uint32_t e, cudaStream_t s) {
 sgnn_status phase2(sgnn_dist_s* g, uint32_t e, cudaStream_t s) {
     const float* h1r = g->h1_full + uint64_t(g->r0) * g->hid;
     DIST_MARK(g, M_P2_S);
+    if (g->P > 1) {
+        // the other ranks' ds2 rows from their gathered gradient rows (16
+        // floats a row on the wire instead of 128): the head's own chain
+        // (sage_grad_wt_kernel), so every ds2 row is bitwise the owner's
+        const uint64_t r1 = uint64_t(g->r0) + g->rows;
+        SGNN_TRY(sgnn::glue_sage_grad_wt(g->grad_full, g->wpack + g->off_w2, g->r0, g->hid, g->cls, nullptr, nullptr,
+                                         g->ds2_full, s));
+        SGNN_TRY(sgnn::glue_sage_grad_wt(g->grad_full + r1 * g->cls, g->wpack + g->off_w2, uint32_t(g->n - r1), g->hid,
+                                         g->cls, nullptr, nullptr, g->ds2_full + r1 * g->hid, s));
+    }
     DIST_MARK(g, M_SPMMB_0);
     if (g->rows) SGNN_TRY(sgnn::run_spmm(&g->bwd, g->ds2_full, g->hid, g->dh1, SGNN_REDUCE_SUM, g->plan_bwd, s));
     DIST_MARK(g, M_SPMMB_1);
-    SGNN_TRY(sgnn::glue_sage_grad_wt(g->grad, g->wpack + g->off_w2s, g->rows, g->hid, g->cls, g->dh1, h1r, g->z1, s));
+    SGNN_TRY(sgnn::glue_sage_grad_wt(g->grad(), g->wpack + g->off_w2s, g->rows, g->hid, g->cls, g->dh1, h1r, g->z1, s));
     DIST_MARK(g, M_GEMM2_0);
     SGNN_TRY(mm_tn(g, g->ax, g->z1, g->gpack + g->off_w1, g->rows, 2 * g->in, g->hid, s));  // [g1; g1s] = ax^T dz1
     DIST_MARK(g, M_P2_E);
@@ -519,7 +532,7 @@ sgnn_status run_epochs(sgnn_dist_s* const* gs, int ng, uint32_t epochs, float lr
         SGNN_TRY(allgather_rows(gs, ng, [](sgnn_dist_s* g) { return static_cast<void*>(g->h1_full); }, g0->hid, s));
         SGNN_TRY(each([&](sgnn_dist_s* g) { return cudaEventRecord(g->mark(e, M_EX1), s) == cudaSuccess ? SGNN_OK : fail(SGNN_ERR_CUDA, "event"); }));
         SGNN_TRY(each([&](sgnn_dist_s* g) { return phase1(g, e, s); }));
-        SGNN_TRY(allgather_rows(gs, ng, [](sgnn_dist_s* g) { return static_cast<void*>(g->ds2_full); }, g0->hid, s));
+        SGNN_TRY(allgather_rows(gs, ng, [](sgnn_dist_s* g) { return static_cast<void*>(g->grad_full); }, g0->cls, s));
         SGNN_TRY(each([&](sgnn_dist_s* g) { return cudaEventRecord(g->mark(e, M_EX2), s) == cudaSuccess ? SGNN_OK : fail(SGNN_ERR_CUDA, "event"); }));
         SGNN_TRY(each([&](sgnn_dist_s* g) { return phase2(g, e, s); }));
         SGNN_TRY(allreduce_grads(gs, ng, s));
@@ -679,7 +692,7 @@ sgnn_status sgnn_dist_create(sgnn_comm comm, int rank, const uint32_t* bounds, c
         (st = dalloc(g, &g->h1_full, N * hidden)) != SGNN_OK || (st = dalloc(g, &g->ds2_full, N * hidden)) != SGNN_OK ||
         (st = dalloc(g, &g->ax, R * 2 * in_features)) != SGNN_OK || (st = dalloc(g, &g->a2, R * hidden)) != SGNN_OK ||
         (st = dalloc(g, &g->z1, R * hidden)) != SGNN_OK || (st = dalloc(g, &g->dh1, R * hidden)) != SGNN_OK ||
-        (st = dalloc(g, &g->grad, R * classes)) != SGNN_OK ||
+        (st = dalloc(g, &g->grad_full, N * classes)) != SGNN_OK ||
         (st = dalloc(g, &g->labels, R)) != SGNN_OK || (st = dalloc(g, &g->mask, R)) != SGNN_OK ||
         (st = dalloc(g, &g->deg, N)) != SGNN_OK || (st = dalloc(g, &g->wpack, g->pack_n)) != SGNN_OK ||
         (st = dalloc(g, &g->gpack, g->pack_n)) != SGNN_OK || (st = dalloc(g, &g->blk_loss, g->sm_blocks)) != SGNN_OK ||
