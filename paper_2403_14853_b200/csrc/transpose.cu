@@ -208,21 +208,21 @@ __global__ void __launch_bounds__(kThreads) radix_downsweep_kernel(
     uint32_t kk[kItems], rr[kItems];
     float vv[kItems];
     uint16_t* mycnt = wcnt + wid * bins;
+    // every item's loads first (all in flight together), then the ranking
 #pragma unroll
     for (int q = 0; q < kItems; ++q) {
         const uint32_t li = uint32_t(wid * WI + q * 32 + lane);
         const bool valid = li < cnt;
         const uint64_t idx = base + li;
-        uint32_t key = 0;
-        if (valid) {
-            key = __ldcs(keys_in + idx);
-            rr[q] = FIRST ? srow[li] : __ldcs(rows_in + idx);
-            vv[q] = VALS ? __ldcs(vals_in + idx) : 0.0f;
-        } else {
-            rr[q] = 0;
-            vv[q] = 0.0f;
-        }
-        kk[q] = key;
+        kk[q] = valid ? __ldcs(keys_in + idx) : 0u;
+        rr[q] = valid ? (FIRST ? srow[li] : __ldcs(rows_in + idx)) : 0u;
+        vv[q] = valid && VALS ? __ldcs(vals_in + idx) : 0.0f;
+    }
+#pragma unroll
+    for (int q = 0; q < kItems; ++q) {
+        const uint32_t li = uint32_t(wid * WI + q * 32 + lane);
+        const bool valid = li < cnt;
+        const uint32_t key = kk[q];
         const uint32_t d = (key >> shift) & mask;
         const unsigned peers = __match_any_sync(0xffffffffu, valid ? d : 0xffffffffu);
         const uint32_t before = mycnt[d];
