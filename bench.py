@@ -306,7 +306,7 @@ def run_cfg5(args):
         "loss_first_last": [round(float(loss[0]), 6), round(float(loss[-1]), 6)],
         "accuracy_last": round(float(acc[-1]), 6),
         "roofline": roof,
-        "gpu_launches": K * CFG5_LAUNCHES_PER_EPOCH,
+        "gpu_launches": K * (CFG5_LAUNCHES_PER_EPOCH + (2 if ws > 1 else 0)),
         "gen_s": round(gen_s, 2), "setup_s": round(setup_s, 2),
     }
     out["clocks"] = clk.summary()
@@ -330,10 +330,11 @@ def run_cfg5(args):
         print(json.dumps(out), flush=True)
 
 
-# our kernels launched per cfg5 epoch at N=1 (ncu launch list, profiles/r02_cfg5_launches.json):
-# 3 SpMMs (worker + 2 fixups each, mean divides on the two forward ones), 2+2 tensor-core
-# products, add_relu, logits, softmax, stats, wgrad (2), grad_wt (2), sgd, epoch record
-CFG5_LAUNCHES_PER_EPOCH = 24
+# our kernels launched per cfg5 epoch at N=1 (ncu launch list, profiles/r02o_cfg5_launches.json):
+# 3 SpMMs (worker + 2 fixups each; the mean divide is in the epilogue), 2 tensor-core
+# products (relu in the first one's epilogue), head, rank stats, wgrad + finish,
+# relu-backward, sgd, epoch record; at N > 1 also the two remote-row ds2 passes
+CFG5_LAUNCHES_PER_EPOCH = 18
 
 
 def _nvml_index(local):
