@@ -1,15 +1,20 @@
 // transpose.cu -- on-device CSR -> CSC (= CSR of A^T), bit-exact with the
-// reference's serial counting sort (sparse.hpp:72-89): column histogram ->
-// exclusive scan -> placement in ascending original row within each column.
+// reference's serial counting sort (sparse.hpp:72-89): placement in
+// ascending original row within each column, t_row_ptr = the column starts.
 //
 // The stable placement is an LSD radix sort of the nonzeros keyed by column
 // (2 passes of <= 11-bit digits for up to 2^22 columns), carrying (row, value)
-// as payload.  Each tile of 4096 nonzeros is ranked warp by warp with
-// __match_any_sync in index order, staged in shared memory in digit order and
-// written out as contiguous runs per digit, so the output is exactly the
-// counting-sort order.  The first pass derives the row of every nonzero from
-// the row starts inside its tile (marks + a block scan), so no expanded row
-// array is read and no per-nonzero search is made.
+// as payload.  Each tile of 4096 nonzeros is ranked warp by warp in index
+// order (digit peers from one ballot per digit bit, the warp's running digit
+// counts advanced by one shared-memory atomic per peer group), staged in
+// shared memory in digit order and written out as contiguous runs per digit,
+// so the output is exactly the counting-sort order.  The first pass derives
+// the row of every nonzero from the row starts inside its tile (marks + a
+// block scan, the tile's first row precomputed for all tiles at once), so no
+// expanded row array is read and no per-nonzero search is made.  The column
+// starts come from the sorted keys at the end (one boundary pass), not from a
+// column histogram: hub columns made the histogram's global atomics the
+// single slowest step (0.52 ms of 2.5 ms on cfg2).
 //
 // Also: row_degrees (sparse.hpp:105-109), is_symmetric (sparse.hpp:179-192)
 // and the mean-operand value scaling (gnn.hpp:158-159).
@@ -25,7 +30,8 @@ constexpr int kThreads = 256;
 constexpr int kWarps = kThreads / 32;
 constexpr int kItems = 16;                          // per thread per tile
 constexpr uint64_t kTile = uint64_t(kThreads) * kItems;  // 4096 nonzeros
-constexpr int kMaxDigitBits = 11;  // <= 2048 bins (the downsweep's u16 warp counters, 8 bins per thread)
+constexpr int kMaxDigitBits = 11;  // <= 2048 bins (u16 warp counters, <= 8 bins per thread)
+constexpr unsigned kFull = 0xffffffffu;
 
 struct RadixPlan {
     int passes = 1;
@@ -53,8 +59,8 @@ struct Workspace {
     uint32_t* keys_b;
     uint32_t* rows_a;
     float* vals_a;
-    uint32_t* hist;    // bins * tiles (+1 for the scan total)
-    uint32_t* counts;  // n_cols
+    uint32_t* hist;       // bins * tiles (+1 for the scan total)
+    uint32_t* tile_row0;  // tiles: row holding each tile's first nonzero
     size_t bytes;
 };
 
@@ -75,16 +81,9 @@ Workspace carve(void* base, const sgnn_csr* a, const RadixPlan& rp) {
     w.rows_a = reinterpret_cast<uint32_t*>(take(4 * nnz));
     w.vals_a = reinterpret_cast<float*>(take(4 * nnz));
     w.hist = reinterpret_cast<uint32_t*>(take(4 * (size_t(rp.bins) * rp.tiles + 1)));
-    w.counts = reinterpret_cast<uint32_t*>(take(4 * (size_t(a->n_cols) + 1)));
+    w.tile_row0 = reinterpret_cast<uint32_t*>(take(4 * (size_t(rp.tiles) + 1)));
     w.bytes = off;
     return w;
-}
-
-__global__ void col_histogram_kernel(const uint32_t* __restrict__ ci, uint64_t nnz,
-                                     uint32_t* __restrict__ counts) {
-    for (uint64_t e = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; e < nnz;
-         e += uint64_t(gridDim.x) * blockDim.x)
-        atomicAdd(counts + __ldcs(ci + e), 1u);
 }
 
 // Largest r in [lo, hi) with rp[r] <= idx (the row holding nonzero idx).
@@ -106,6 +105,38 @@ __device__ __forceinline__ void tile_rows(const uint64_t* __restrict__ rp, uint3
     *r_hi = find_row(rp, *r_lo, m, last);
 }
 
+// tile_row0[t] = the row holding nonzero t * kTile (the largest r with
+// rp[r] <= t * kTile): each nonempty row names the tiles starting inside it.
+__global__ void tile_row0_kernel(const uint64_t* __restrict__ rp, uint32_t m,
+                                 uint32_t* __restrict__ out) {
+    for (uint32_t r = blockIdx.x * blockDim.x + threadIdx.x; r < m; r += gridDim.x * blockDim.x) {
+        const uint64_t s = __ldg(rp + r), e = __ldg(rp + r + 1);
+        for (uint64_t t = (s + kTile - 1) / kTile; t * kTile < e; ++t) out[t] = r;
+    }
+}
+
+// t_row_ptr from the sorted column keys: position p starts every column in
+// (keys[p-1], keys[p]] (empty columns included); p = nnz closes the rest.
+// Four positions per thread (one 16-byte load where aligned).
+__global__ void col_starts_kernel(const uint32_t* __restrict__ keys, uint64_t nnz, uint32_t n_cols,
+                                  uint64_t* __restrict__ trp) {
+    const uint64_t p0 = (uint64_t(blockIdx.x) * blockDim.x + threadIdx.x) * 4;
+    if (p0 > nnz) return;
+    int64_t k[5];
+    k[0] = p0 ? int64_t(__ldg(keys + p0 - 1)) : -1;
+    if (p0 + 4 <= nnz && (reinterpret_cast<uintptr_t>(keys + p0) & 15) == 0) {
+        const uint4 v = __ldg(reinterpret_cast<const uint4*>(keys + p0));
+        k[1] = v.x; k[2] = v.y; k[3] = v.z; k[4] = v.w;
+    } else {
+#pragma unroll
+        for (int i = 0; i < 4; ++i)
+            k[i + 1] = p0 + i < nnz ? int64_t(__ldg(keys + p0 + i)) : (p0 + i == nnz ? int64_t(n_cols) : k[i]);
+    }
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+        for (int64_t c = k[i] + 1; c <= k[i + 1]; ++c) trp[c] = p0 + i;
+}
+
 __global__ void __launch_bounds__(kThreads) radix_upsweep_kernel(const uint32_t* __restrict__ keys,
                                                                  uint64_t n, int shift,
                                                                  uint32_t mask, uint64_t tiles,
@@ -113,21 +144,48 @@ __global__ void __launch_bounds__(kThreads) radix_upsweep_kernel(const uint32_t*
     extern __shared__ uint32_t sh[];
     const uint32_t bins = mask + 1;
     for (uint32_t d = threadIdx.x; d < bins; d += kThreads) sh[d] = 0;
-    __syncthreads();
     const uint64_t base = uint64_t(blockIdx.x) * kTile;
-    for (int r = 0; r < kItems; ++r) {
+    uint32_t k[kItems];
+#pragma unroll
+    for (int r = 0; r < kItems; ++r) {  // all loads in flight before the first atomic
         const uint64_t idx = base + uint64_t(r) * kThreads + threadIdx.x;
-        if (idx < n) atomicAdd(sh + ((__ldg(keys + idx) >> shift) & mask), 1u);
+        k[r] = idx < n ? __ldcs(keys + idx) : 0xffffffffu;
     }
     __syncthreads();
+#pragma unroll
+    for (int r = 0; r < kItems; ++r)
+        if (base + uint64_t(r) * kThreads + threadIdx.x < n) atomicAdd(sh + ((k[r] >> shift) & mask), 1u);
+    __syncthreads();
     for (uint32_t d = threadIdx.x; d < bins; d += kThreads) hist[uint64_t(d) * tiles + blockIdx.x] = sh[d];
+}
+
+// Exclusive scan of one value per thread over the block (warp shuffles, one
+// barrier); `s_warp` holds kWarps entries and must not be reused before the
+// next barrier.
+__device__ __forceinline__ uint32_t block_exclusive_scan(uint32_t v, uint32_t* s_warp) {
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    uint32_t x = v;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t y = __shfl_up_sync(kFull, x, o);
+        if (lane >= o) x += y;
+    }
+    if (lane == 31) s_warp[wid] = x;
+    __syncthreads();
+    uint32_t pre = 0;
+#pragma unroll
+    for (int w = 0; w < kWarps; ++w) pre += (w < wid) ? s_warp[w] : 0u;
+    return pre + x - v;
 }
 
 // Stable scatter of one tile (4096 nonzeros in index order), staged through
 // shared memory so the global writes are contiguous runs per digit:
 //   A. warp w ranks its 512 consecutive items (16 rounds of 32, lane order =
-//      index order) with __match_any_sync against warp-private u16 digit
-//      counters -- no block barrier per round;
+//      index order): the lanes sharing a digit come from one ballot per digit
+//      bit, the group's lowest lane advances the warp's counter for that digit
+//      with one shared atomic (u16 counters packed in pairs) and broadcasts
+//      the old count -- no per-round barrier, and the 16 rounds' atomics
+//      pipeline (same-warp shared atomics to one address stay in order);
 //   B. per digit, exclusive offsets over the warps and the tile's digit
 //      starts (one block scan);
 //   C. every item lands in the tile's digit-sorted order in shared memory;
@@ -136,46 +194,69 @@ __global__ void __launch_bounds__(kThreads) radix_upsweep_kernel(const uint32_t*
 // The order is the stable counting sort's (index order within a digit).
 // FIRST: rows come from the CSR itself -- each row start inside the tile
 // marks its position, an inclusive scan of the marks gives every item's row
-// (empty rows included); LAST: keys are not written.
+// (empty rows included).
 constexpr int kDownSmemFixed = 3 * kThreads * kItems * 4;  // staged keys, rows, vals
 
-template <bool FIRST, bool LAST, bool VALS>
-__global__ void __launch_bounds__(kThreads) radix_downsweep_kernel(
+template <bool FIRST, bool VALS>
+__global__ void __launch_bounds__(kThreads, 3) radix_downsweep_kernel(
     const uint32_t* __restrict__ keys_in, const uint32_t* __restrict__ rows_in,
     const float* __restrict__ vals_in, uint32_t* __restrict__ keys_out,
     uint32_t* __restrict__ rows_out, float* __restrict__ vals_out, uint64_t n, int shift,
-    uint32_t mask, uint64_t tiles, const uint32_t* __restrict__ hist_scan,
-    const uint64_t* __restrict__ rp, uint32_t m) {
+    int dbits, uint64_t tiles, const uint32_t* __restrict__ hist_scan,
+    const uint64_t* __restrict__ rp, uint32_t m, const uint32_t* __restrict__ tile_row0) {
     constexpr int T = kThreads * kItems;  // 4096
     constexpr int WI = T / kWarps;        // 512 items per warp
     extern __shared__ __align__(16) uint32_t sh[];
-    const uint32_t bins = mask + 1;
+    const uint32_t bins = 1u << dbits;
+    const uint32_t mask = bins - 1;
+    // bins per thread for the digit bookkeeping (1 when bins < kThreads)
+    const uint32_t bpt = bins >= uint32_t(kThreads) ? bins / kThreads : 1u;
     uint32_t* skey = sh;                    // [T]
     uint32_t* srow = sh + T;                // [T] (FIRST: row marks, then rows)
     float* sval = reinterpret_cast<float*>(sh + 2 * T);  // [T]
     uint32_t* sgoff = sh + 3 * T;           // [bins] global offset - tile digit start
     uint32_t* sdst = sgoff + bins;          // [bins] tile digit start
-    uint16_t* wcnt = reinterpret_cast<uint16_t*>(sdst + bins);  // [kWarps][bins]
-    __shared__ uint32_t s_scan[kThreads];
-    __shared__ uint32_t s_r0;
+    uint32_t* wcnt = sdst + bins;           // [kWarps][bins / 2]: u16 counters in pairs
+    uint16_t* wc16 = reinterpret_cast<uint16_t*>(wcnt);  // [kWarps][bins]
+    __shared__ uint32_t s_warp[2][kWarps];
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
     const uint64_t base = uint64_t(blockIdx.x) * T;
     const uint32_t cnt = uint32_t(min(uint64_t(T), n - base));
-    for (uint32_t d = threadIdx.x; d < bins * kWarps / 2; d += kThreads) reinterpret_cast<uint32_t*>(wcnt)[d] = 0;
+    const uint32_t cwords = bins >= 2 ? bins / 2 : 1;
+    for (uint32_t d = threadIdx.x; d < kWarps * cwords; d += kThreads) wcnt[d] = 0;
+    uint32_t r0 = 0;
     if (FIRST) {
+        r0 = __ldg(tile_row0 + blockIdx.x);
         for (int i = threadIdx.x; i < T; i += kThreads) srow[i] = 0;
-        if (threadIdx.x == 0) {
-            uint32_t lo = 0, hi = m;  // row of the tile's first item
-            while (hi - lo > 1) {
-                const uint32_t mid = lo + (hi - lo) / 2;
-                if (__ldg(rp + mid) <= base) lo = mid;
-                else hi = mid;
-            }
-            s_r0 = lo;
+    }
+    // every load of the tile in flight together: items, the tile's global
+    // digit offsets, (FIRST) the row starts inside the tile
+    uint32_t kk[kItems], rr[kItems];
+    float vv[kItems];
+#pragma unroll
+    for (int q = 0; q < kItems; ++q) {
+        const uint32_t li = uint32_t(wid * WI + q * 32 + lane);
+        const bool valid = li < cnt;
+        const uint64_t idx = base + li;
+        kk[q] = valid ? __ldcs(keys_in + idx) : 0u;
+        rr[q] = valid && !FIRST ? __ldcs(rows_in + idx) : 0u;
+        vv[q] = valid && VALS ? __ldcs(vals_in + idx) : 0.0f;
+    }
+    // the tile's global digit offsets go straight to shared memory (cp.async:
+    // no registers held while they are in flight)
+    for (uint32_t b = 0; b < bpt; ++b) {
+        const uint32_t d = threadIdx.x * bpt + b;
+        if (d < bins) {
+            const uint32_t dst = static_cast<uint32_t>(__cvta_generic_to_shared(sgoff + d));
+            asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(dst),
+                         "l"(hist_scan + uint64_t(d) * tiles + blockIdx.x)
+                         : "memory");
         }
-        __syncthreads();
+    }
+    asm volatile("cp.async.commit_group;" ::: "memory");
+    if (FIRST) {
+        __syncthreads();  // marks zeroed
         // mark every row start strictly inside the tile (empty rows stack up)
-        const uint32_t r0 = s_r0;
         for (uint32_t r = r0 + 1 + threadIdx.x; r <= m; r += kThreads) {
             const uint64_t st = __ldg(rp + r);
             if (st >= base + cnt) break;
@@ -189,85 +270,64 @@ __global__ void __launch_bounds__(kThreads) radix_downsweep_kernel(
             acc += srow[threadIdx.x * kItems + q];
             loc[q] = acc;
         }
-        s_scan[threadIdx.x] = acc;
-        __syncthreads();
-        for (int off = 1; off < kThreads; off <<= 1) {
-            const uint32_t v = threadIdx.x >= off ? s_scan[threadIdx.x - off] : 0u;
-            __syncthreads();
-            s_scan[threadIdx.x] += v;
-            __syncthreads();
-        }
-        const uint32_t pre = r0 + (threadIdx.x ? s_scan[threadIdx.x - 1] : 0u);
+        const uint32_t pre = r0 + block_exclusive_scan(acc, s_warp[0]);
 #pragma unroll
         for (int q = 0; q < kItems; ++q) srow[threadIdx.x * kItems + q] = pre + loc[q];
+        __syncthreads();
+#pragma unroll
+        for (int q = 0; q < kItems; ++q) rr[q] = srow[wid * WI + q * 32 + lane];
     }
-    __syncthreads();
+    __syncthreads();  // counters zeroed (and FIRST: srow read before staging reuses it)
     // A. warp-local stable ranks
     const unsigned lt = (1u << lane) - 1u;
+    uint32_t* mycnt = wcnt + wid * cwords;
     uint32_t pk[kItems];  // digit << 16 | rank within the warp's digit
-    uint32_t kk[kItems], rr[kItems];
-    float vv[kItems];
-    uint16_t* mycnt = wcnt + wid * bins;
-    // every item's loads first (all in flight together), then the ranking
 #pragma unroll
     for (int q = 0; q < kItems; ++q) {
         const uint32_t li = uint32_t(wid * WI + q * 32 + lane);
         const bool valid = li < cnt;
-        const uint64_t idx = base + li;
-        kk[q] = valid ? __ldcs(keys_in + idx) : 0u;
-        rr[q] = valid ? (FIRST ? srow[li] : __ldcs(rows_in + idx)) : 0u;
-        vv[q] = valid && VALS ? __ldcs(vals_in + idx) : 0.0f;
-    }
-#pragma unroll
-    for (int q = 0; q < kItems; ++q) {
-        const uint32_t li = uint32_t(wid * WI + q * 32 + lane);
-        const bool valid = li < cnt;
-        const uint32_t key = kk[q];
-        const uint32_t d = (key >> shift) & mask;
-        const unsigned peers = __match_any_sync(0xffffffffu, valid ? d : 0xffffffffu);
-        const uint32_t before = mycnt[d];
-        __syncwarp();
-        if (valid && (peers & lt) == 0) mycnt[d] = uint16_t(before + __popc(peers));
-        __syncwarp();
-        pk[q] = valid ? (d << 16) | (before + __popc(peers & lt)) : 0xffffffffu;
+        const uint32_t d = (kk[q] >> shift) & mask;
+        unsigned peers = __ballot_sync(kFull, valid);
+        for (int b = 0; b < dbits; ++b) {
+            const bool bit = (d >> b) & 1u;
+            const unsigned bal = __ballot_sync(kFull, bit);
+            peers &= bit ? bal : ~bal;
+        }
+        const int leader = valid ? __ffs(peers) - 1 : lane;
+        const uint32_t hsh = (d & 1u) * 16u;
+        uint32_t old = 0;
+        if (valid && leader == lane) old = atomicAdd(mycnt + (d >> 1), uint32_t(__popc(peers)) << hsh);
+        old = __shfl_sync(kFull, old, leader);
+        pk[q] = valid ? (d << 16) | (((old >> hsh) & 0xffffu) + __popc(peers & lt)) : 0xffffffffu;
     }
     __syncthreads();
-    // B. per digit: exclusive offsets over the warps, tile totals, block scan
-    constexpr int BPT = 2048 / kThreads;  // bins per thread (bins <= 2048)
-    uint32_t tot[BPT];
+    // B. per digit: exclusive offsets over the warps, tile totals (parked in
+    // sdst), block scan, then the tile's digit starts
+    asm volatile("cp.async.wait_all;" ::: "memory");
     uint32_t run = 0;
-#pragma unroll
-    for (int b = 0; b < BPT; ++b) {
-        const uint32_t d = threadIdx.x * BPT + b;
-        uint32_t t = 0;
+    for (uint32_t b = 0; b < bpt; ++b) {
+        const uint32_t d = threadIdx.x * bpt + b;
         if (d < bins) {
+            uint32_t t = 0;
 #pragma unroll
             for (int w = 0; w < kWarps; ++w) {
-                const uint32_t c = wcnt[w * bins + d];
-                wcnt[w * bins + d] = uint16_t(t);
+                const uint32_t c = wc16[w * bins + d];
+                wc16[w * bins + d] = uint16_t(t);
                 t += c;
             }
+            sdst[d] = t;
+            run += t;
         }
-        tot[b] = t;
-        run += t;
     }
-    s_scan[threadIdx.x] = run;
-    __syncthreads();
-    for (int off = 1; off < kThreads; off <<= 1) {
-        const uint32_t v = threadIdx.x >= off ? s_scan[threadIdx.x - off] : 0u;
-        __syncthreads();
-        s_scan[threadIdx.x] += v;
-        __syncthreads();
-    }
-    uint32_t start = threadIdx.x ? s_scan[threadIdx.x - 1] : 0u;
-#pragma unroll
-    for (int b = 0; b < BPT; ++b) {
-        const uint32_t d = threadIdx.x * BPT + b;
+    uint32_t start = block_exclusive_scan(run, s_warp[1]);
+    for (uint32_t b = 0; b < bpt; ++b) {
+        const uint32_t d = threadIdx.x * bpt + b;
         if (d < bins) {
+            const uint32_t t = sdst[d];
             sdst[d] = start;
-            sgoff[d] = __ldg(hist_scan + uint64_t(d) * tiles + blockIdx.x) - start;
+            sgoff[d] -= start;
+            start += t;
         }
-        start += tot[b];
     }
     __syncthreads();
     // C. stage in the tile's digit-sorted order
@@ -275,7 +335,7 @@ __global__ void __launch_bounds__(kThreads) radix_downsweep_kernel(
     for (int q = 0; q < kItems; ++q) {
         if (pk[q] == 0xffffffffu) continue;
         const uint32_t d = pk[q] >> 16;
-        const uint32_t slot = sdst[d] + wcnt[wid * bins + d] + (pk[q] & 0xffffu);
+        const uint32_t slot = sdst[d] + wc16[wid * bins + d] + (pk[q] & 0xffffu);
         skey[slot] = kk[q];
         srow[slot] = rr[q];
         if (VALS) sval[slot] = vv[q];
@@ -285,34 +345,25 @@ __global__ void __launch_bounds__(kThreads) radix_downsweep_kernel(
     for (uint32_t k = threadIdx.x; k < cnt; k += kThreads) {
         const uint32_t key = skey[k];
         const uint64_t dst = uint64_t(sgoff[(key >> shift) & mask]) + k;
-        if (!LAST) keys_out[dst] = key;
+        keys_out[dst] = key;
         rows_out[dst] = srow[k];
         if (VALS) vals_out[dst] = sval[k];
     }
 }
 
-template <bool FIRST, bool LAST, bool VALS>
-sgnn_status launch_down(const uint32_t* ki, const uint32_t* ri, const float* vi, uint32_t* ko,
-                        uint32_t* ro, float* vo, uint64_t n, int shift, uint32_t mask,
-                        uint64_t tiles, const uint32_t* hs, const uint64_t* rp, uint32_t m,
+template <bool FIRST>
+sgnn_status launch_down(bool vals, const uint32_t* ki, const uint32_t* ri, const float* vi, uint32_t* ko,
+                        uint32_t* ro, float* vo, uint64_t n, int shift, int dbits, uint64_t tiles,
+                        const uint32_t* hs, const uint64_t* rp, uint32_t m, const uint32_t* tr0,
                         cudaStream_t s) {
-    const size_t bins = size_t(mask) + 1;
-    const size_t smem = kDownSmemFixed + 2 * 4 * bins + 2 * kWarps * bins;
-    auto k = radix_downsweep_kernel<FIRST, LAST, VALS>;
+    const size_t bins = size_t(1) << dbits;
+    const size_t smem = kDownSmemFixed + 2 * 4 * bins + 4 * kWarps * std::max<size_t>(1, bins / 2);
+    auto k = vals ? radix_downsweep_kernel<FIRST, true> : radix_downsweep_kernel<FIRST, false>;
     SGNN_CUDA_TRY(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
-    k<<<unsigned(tiles), kThreads, smem, s>>>(ki, ri, vi, ko, ro, vo, n, shift, mask, tiles, hs, rp, m);
+    SGNN_CUDA_TRY(cudaFuncSetAttribute(k, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
+    k<<<unsigned(tiles), kThreads, smem, s>>>(ki, ri, vi, ko, ro, vo, n, shift, dbits, tiles, hs, rp, m, tr0);
     SGNN_LAUNCH_CHECK();
     return SGNN_OK;
-}
-
-template <bool FIRST, bool LAST>
-sgnn_status launch_down_v(bool vals, const uint32_t* ki, const uint32_t* ri, const float* vi,
-                          uint32_t* ko, uint32_t* ro, float* vo, uint64_t n, int shift,
-                          uint32_t mask, uint64_t tiles, const uint32_t* hs, const uint64_t* rp,
-                          uint32_t m, cudaStream_t s) {
-    if (vals)
-        return launch_down<FIRST, LAST, true>(ki, ri, vi, ko, ro, vo, n, shift, mask, tiles, hs, rp, m, s);
-    return launch_down<FIRST, LAST, false>(ki, ri, vi, ko, ro, vo, n, shift, mask, tiles, hs, rp, m, s);
 }
 
 __global__ void row_degrees_kernel(const uint64_t* __restrict__ rp, uint32_t m,
@@ -401,6 +452,11 @@ sgnn_status run_transpose(const sgnn_csr* a, uint64_t* trp, uint32_t* tci, float
     DeviceProps dp;
     SGNN_TRY(device_props(&dp));
     const RadixPlan plan = radix_plan(a->n_cols, a->nnz);
+    if (a->nnz == 0) {  // every column empty
+        col_starts_kernel<<<1, 32, 0, s>>>(nullptr, 0, a->n_cols, trp);
+        SGNN_LAUNCH_CHECK();
+        return SGNN_OK;
+    }
     const size_t need = carve(nullptr, a, plan).bytes;
     void* own = nullptr;
     if (!ws) {
@@ -413,30 +469,24 @@ sgnn_status run_transpose(const sgnn_csr* a, uint64_t* trp, uint32_t* tci, float
     Workspace w = carve(ws, a, plan);
     sgnn_status st = SGNN_OK;
     do {
-        // 1. column histogram -> t_row_ptr (sparse.hpp:75-76)
-        if (cudaMemsetAsync(w.counts, 0, sizeof(uint32_t) * (size_t(a->n_cols) + 1), s) != cudaSuccess) {
-            st = fail(SGNN_ERR_CUDA, "transpose: memset failed");
-            break;
-        }
-        if (a->nnz) {
-            const uint64_t blocks = std::min<uint64_t>(ceil_div_u64(a->nnz, 256), uint64_t(dp.sm_count) * 16);
-            col_histogram_kernel<<<unsigned(blocks), 256, 0, s>>>(a->col_idx, a->nnz, w.counts);
+        // the row of every tile's first nonzero (the first pass's row recovery)
+        {
+            const uint64_t blocks = std::min<uint64_t>(ceil_div_u64(a->n_rows, 256), uint64_t(dp.sm_count) * 16);
+            tile_row0_kernel<<<unsigned(std::max<uint64_t>(blocks, 1)), 256, 0, s>>>(a->row_ptr, a->n_rows,
+                                                                                    w.tile_row0);
             if (cudaGetLastError() != cudaSuccess) {
-                st = fail(SGNN_ERR_CUDA, "transpose: histogram launch failed");
+                st = fail(SGNN_ERR_CUDA, "transpose: tile_row0 launch failed");
                 break;
             }
         }
-        st = exclusive_scan_u32_to_u64(w.counts, trp, a->n_cols, s);
-        if (st != SGNN_OK || a->nnz == 0) break;
-
-        // 2. stable LSD radix passes (sparse.hpp:80-86 placement order)
+        // stable LSD radix passes (sparse.hpp:80-86 placement order)
         const bool vals = tv != nullptr;
         const uint32_t mask = plan.bins - 1;
         const uint32_t* keys_src = a->col_idx;
         const uint32_t* rows_src = nullptr;
         const float* vals_src = a->values;
         for (int p = 0; p < plan.passes && st == SGNN_OK; ++p) {
-            const bool first = p == 0, last = p == plan.passes - 1;
+            const bool first = p == 0;
             // the last pass lands in (tci, tv); earlier passes alternate with set A
             const bool to_out = ((plan.passes - 1 - p) % 2) == 0;
             uint32_t* keys_dst = (p % 2 == 0) ? w.keys_a : w.keys_b;
@@ -452,26 +502,21 @@ sgnn_status run_transpose(const sgnn_csr* a, uint64_t* trp, uint32_t* tci, float
             }
             st = exclusive_scan_u32(w.hist, w.hist, uint64_t(plan.bins) * plan.tiles, s);
             if (st != SGNN_OK) break;
-            if (first && last)
-                st = launch_down_v<true, true>(vals, keys_src, rows_src, vals_src, keys_dst, rows_dst,
-                                               vals_dst, a->nnz, shift, mask, plan.tiles, w.hist,
-                                               a->row_ptr, a->n_rows, s);
-            else if (first)
-                st = launch_down_v<true, false>(vals, keys_src, rows_src, vals_src, keys_dst, rows_dst,
-                                                vals_dst, a->nnz, shift, mask, plan.tiles, w.hist,
-                                                a->row_ptr, a->n_rows, s);
-            else if (last)
-                st = launch_down_v<false, true>(vals, keys_src, rows_src, vals_src, keys_dst, rows_dst,
-                                                vals_dst, a->nnz, shift, mask, plan.tiles, w.hist,
-                                                a->row_ptr, a->n_rows, s);
+            if (first)
+                st = launch_down<true>(vals, keys_src, rows_src, vals_src, keys_dst, rows_dst, vals_dst, a->nnz,
+                                       shift, plan.dbits, plan.tiles, w.hist, a->row_ptr, a->n_rows, w.tile_row0, s);
             else
-                st = launch_down_v<false, false>(vals, keys_src, rows_src, vals_src, keys_dst, rows_dst,
-                                                 vals_dst, a->nnz, shift, mask, plan.tiles, w.hist,
-                                                 a->row_ptr, a->n_rows, s);
+                st = launch_down<false>(vals, keys_src, rows_src, vals_src, keys_dst, rows_dst, vals_dst, a->nnz,
+                                        shift, plan.dbits, plan.tiles, w.hist, a->row_ptr, a->n_rows, w.tile_row0, s);
             keys_src = keys_dst;
             rows_src = rows_dst;
             vals_src = vals_dst;
         }
+        if (st != SGNN_OK) break;
+        // t_row_ptr from the sorted keys (sparse.hpp:75-76's histogram + scan)
+        const uint64_t blocks = ceil_div_u64(ceil_div_u64(a->nnz + 1, 4), 256);
+        col_starts_kernel<<<unsigned(blocks), 256, 0, s>>>(keys_src, a->nnz, a->n_cols, trp);
+        if (cudaGetLastError() != cudaSuccess) st = fail(SGNN_ERR_CUDA, "transpose: column-start launch failed");
     } while (false);
     if (own) scratch_free(own, s);
     return st;
