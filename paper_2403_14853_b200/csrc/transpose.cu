@@ -182,10 +182,13 @@ __device__ __forceinline__ uint32_t block_exclusive_scan(uint32_t v, uint32_t* s
 // shared memory so the global writes are contiguous runs per digit:
 //   A. warp w ranks its 512 consecutive items (16 rounds of 32, lane order =
 //      index order): the lanes sharing a digit come from one ballot per digit
-//      bit, the group's lowest lane advances the warp's counter for that digit
-//      with one shared atomic (u16 counters packed in pairs) and broadcasts
-//      the old count -- no per-round barrier, and the 16 rounds' atomics
-//      pipeline (same-warp shared atomics to one address stay in order);
+//      bit (unrolled: the digit width is a template parameter), the group's
+//      lowest lane advances the warp's counter for that digit with one shared
+//      atomic (u16 counters packed in pairs) and broadcasts the old count --
+//      no block barrier, and the rounds' atomics pipeline (same-warp shared
+//      atomics to one address stay in order).  Measured on cfg2 against this:
+//      __match_any_sync (throughput-bound, +40 %), per-warp shared peer masks
+//      built with atomicOr (a longer dependent chain per round, +12 %);
 //   B. per digit, exclusive offsets over the warps and the tile's digit
 //      starts (one block scan);
 //   C. every item lands in the tile's digit-sorted order in shared memory;
@@ -197,7 +200,7 @@ __device__ __forceinline__ uint32_t block_exclusive_scan(uint32_t v, uint32_t* s
 // (empty rows included).
 constexpr int kDownSmemFixed = 3 * kThreads * kItems * 4;  // staged keys, rows, vals
 
-template <bool FIRST, bool VALS>
+template <bool FIRST, bool VALS, int DB>
 __global__ void __launch_bounds__(kThreads, 3) radix_downsweep_kernel(
     const uint32_t* __restrict__ keys_in, const uint32_t* __restrict__ rows_in,
     const float* __restrict__ vals_in, uint32_t* __restrict__ keys_out,
@@ -207,13 +210,16 @@ __global__ void __launch_bounds__(kThreads, 3) radix_downsweep_kernel(
     constexpr int T = kThreads * kItems;  // 4096
     constexpr int WI = T / kWarps;        // 512 items per warp
     extern __shared__ __align__(16) uint32_t sh[];
-    const uint32_t bins = 1u << dbits;
-    const uint32_t mask = bins - 1;
+    static_assert(DB >= 1 && DB <= kMaxDigitBits, "digit width");
+    (void)dbits;
+    constexpr uint32_t bins = 1u << DB;
+    constexpr uint32_t mask = bins - 1;
     // bins per thread for the digit bookkeeping (1 when bins < kThreads)
-    const uint32_t bpt = bins >= uint32_t(kThreads) ? bins / kThreads : 1u;
+    constexpr uint32_t bpt = bins >= uint32_t(kThreads) ? bins / kThreads : 1u;
+    constexpr uint32_t cwords = bins / 2;
     uint32_t* skey = sh;                    // [T]
-    uint32_t* srow = sh + T;                // [T] (FIRST: row marks, then rows)
-    float* sval = reinterpret_cast<float*>(sh + 2 * T);  // [T]
+    float* sval = reinterpret_cast<float*>(sh + T);  // [T]
+    uint32_t* srow = sh + 2 * T;            // [T] (FIRST: row marks, then rows)
     uint32_t* sgoff = sh + 3 * T;           // [bins] global offset - tile digit start
     uint32_t* sdst = sgoff + bins;          // [bins] tile digit start
     uint32_t* wcnt = sdst + bins;           // [kWarps][bins / 2]: u16 counters in pairs
@@ -222,7 +228,6 @@ __global__ void __launch_bounds__(kThreads, 3) radix_downsweep_kernel(
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
     const uint64_t base = uint64_t(blockIdx.x) * T;
     const uint32_t cnt = uint32_t(min(uint64_t(T), n - base));
-    const uint32_t cwords = bins >= 2 ? bins / 2 : 1;
     for (uint32_t d = threadIdx.x; d < kWarps * cwords; d += kThreads) wcnt[d] = 0;
     uint32_t r0 = 0;
     if (FIRST) {
@@ -288,7 +293,8 @@ __global__ void __launch_bounds__(kThreads, 3) radix_downsweep_kernel(
         const bool valid = li < cnt;
         const uint32_t d = (kk[q] >> shift) & mask;
         unsigned peers = __ballot_sync(kFull, valid);
-        for (int b = 0; b < dbits; ++b) {
+#pragma unroll
+        for (int b = 0; b < DB; ++b) {
             const bool bit = (d >> b) & 1u;
             const unsigned bal = __ballot_sync(kFull, bit);
             peers &= bit ? bal : ~bal;
@@ -351,19 +357,35 @@ __global__ void __launch_bounds__(kThreads, 3) radix_downsweep_kernel(
     }
 }
 
+template <bool FIRST, int DB>
+sgnn_status launch_down_db(bool vals, const uint32_t* ki, const uint32_t* ri, const float* vi, uint32_t* ko,
+                           uint32_t* ro, float* vo, uint64_t n, int shift, uint64_t tiles, const uint32_t* hs,
+                           const uint64_t* rp, uint32_t m, const uint32_t* tr0, cudaStream_t s) {
+    constexpr size_t bins = size_t(1) << DB;
+    const size_t smem = kDownSmemFixed + 2 * 4 * bins + 4 * kWarps * (bins / 2);
+    auto k = vals ? radix_downsweep_kernel<FIRST, true, DB> : radix_downsweep_kernel<FIRST, false, DB>;
+    SGNN_CUDA_TRY(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+    SGNN_CUDA_TRY(cudaFuncSetAttribute(k, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
+    k<<<unsigned(tiles), kThreads, smem, s>>>(ki, ri, vi, ko, ro, vo, n, shift, DB, tiles, hs, rp, m, tr0);
+    SGNN_LAUNCH_CHECK();
+    return SGNN_OK;
+}
+
+// the digit width is a template parameter: the ranking's ballots unroll
 template <bool FIRST>
 sgnn_status launch_down(bool vals, const uint32_t* ki, const uint32_t* ri, const float* vi, uint32_t* ko,
                         uint32_t* ro, float* vo, uint64_t n, int shift, int dbits, uint64_t tiles,
                         const uint32_t* hs, const uint64_t* rp, uint32_t m, const uint32_t* tr0,
                         cudaStream_t s) {
-    const size_t bins = size_t(1) << dbits;
-    const size_t smem = kDownSmemFixed + 2 * 4 * bins + 4 * kWarps * std::max<size_t>(1, bins / 2);
-    auto k = vals ? radix_downsweep_kernel<FIRST, true> : radix_downsweep_kernel<FIRST, false>;
-    SGNN_CUDA_TRY(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
-    SGNN_CUDA_TRY(cudaFuncSetAttribute(k, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
-    k<<<unsigned(tiles), kThreads, smem, s>>>(ki, ri, vi, ko, ro, vo, n, shift, dbits, tiles, hs, rp, m, tr0);
-    SGNN_LAUNCH_CHECK();
-    return SGNN_OK;
+#define SGNN_DOWN_CASE(D) \
+    case D: return launch_down_db<FIRST, D>(vals, ki, ri, vi, ko, ro, vo, n, shift, tiles, hs, rp, m, tr0, s);
+    switch (dbits) {
+        SGNN_DOWN_CASE(1) SGNN_DOWN_CASE(2) SGNN_DOWN_CASE(3) SGNN_DOWN_CASE(4) SGNN_DOWN_CASE(5)
+        SGNN_DOWN_CASE(6) SGNN_DOWN_CASE(7) SGNN_DOWN_CASE(8) SGNN_DOWN_CASE(9) SGNN_DOWN_CASE(10)
+        SGNN_DOWN_CASE(11)
+    }
+#undef SGNN_DOWN_CASE
+    return fail(SGNN_ERR_INTERNAL, "transpose: digit width out of range");
 }
 
 __global__ void row_degrees_kernel(const uint64_t* __restrict__ rp, uint32_t m,
