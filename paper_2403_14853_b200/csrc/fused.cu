@@ -11,6 +11,7 @@
 // (the reference reads it twice, kernels.hpp:238,244), with the plan's
 // nnz-balanced split, canonical segments and fixup for hub rows.
 #include <algorithm>
+#include <cstdlib>
 
 #include "ops.cuh"
 #include "plan.cuh"
@@ -235,6 +236,130 @@ __global__ void __launch_bounds__(128, MINB) sddmm_kernel(const SddmmArgs a) {
     ws.finish();
 }
 
+// Full-width float4 SDDMM for K = 4 G (one float4 of every row per lane,
+// G < 32 lanes per nonzero, 32 / G groups per warp in lockstep): the same
+// work split, batches and dot tree as sddmm_kernel's LOCK path -- so bitwise
+// the same results -- with the per-batch overhead cut, since these shapes are
+// bound by instruction issue, not by memory (profiles/r02_cfg4_k64_probes):
+// (col, val) arrive in G-wide windows (one load per lane per G nonzeros, the
+// next window prefetched when the next batch would leave this one), a gather
+// address is one mad.wide, no lane masking of the dot (every lane's float4 is
+// inside K), idle groups gather nothing, and the row advance is warp-uniform
+// and skips up to G rows per step with one ballot over the row-end window.
+template <int G, int U, int MINB>
+__global__ void __launch_bounds__(128, MINB) sddmm_lock_kernel(const SddmmArgs a) {
+    static_assert(G < 32 && U <= G, "lockstep groups, one owned dot per lane");
+    using F = dev::Frag<G, 1, true>;
+    constexpr unsigned FULL = 0xffffffffu;
+    constexpr int PER = G / U;
+    const int lane = threadIdx.x & 31;
+    const int gl = lane & (G - 1), gbase = lane & ~(G - 1);
+    const unsigned gbits = (G == 32) ? FULL : ((1u << G) - 1u);
+    const char* ylane = reinterpret_cast<const char*>(a.y + 4 * gl);
+    const uint32_t ldb = uint32_t(a.ld) * 4u;
+    const uint64_t l2pol = dev::gather_policy();
+    dev::WarpSched<32 / G> ws(a.wctr);
+    for (uint32_t w = ws.base + uint32_t(lane / G); __any_sync(FULL, w < a.n_workers);
+         ws.next(), w = ws.base + uint32_t(lane / G)) {
+        const bool wact = w < a.n_workers;
+        const uint32_t wq = wact ? w : a.n_workers - 1;
+        const uint64_t j0 = a.wnz ? __ldg(a.wnz + wq) : uint64_t(wq) * a.per_worker;
+        const uint32_t E = !wact ? 0u
+                           : a.wnz ? uint32_t(__ldg(a.wnz + wq + 1) - j0)
+                                   : uint32_t(min(a.per_worker, a.nnz - j0));
+        uint32_t r = a.wrow ? __ldg(a.wrow + wq) : row_of(a.rp, a.n_rows, j0);
+        // lane gl of the window: worker-local end of row rb + gl (clamped to E)
+        auto window = [&](uint32_t rb_) -> uint32_t {
+            const uint64_t e = __ldg(a.rp + min(rb_ + 1 + uint32_t(gl), a.n_rows));
+            return uint32_t(min(e - j0, uint64_t(E)));
+        };
+        uint32_t rb = r;
+        uint32_t rwin = window(rb);
+        uint32_t rend_l = __shfl_sync(FULL, rwin, gbase);
+        F xrow;
+        xrow.load(a.x + uint64_t(r) * a.ld, gl, a.k);
+        // (col, val) window: lane gl holds nonzero wb + gl
+        uint32_t wb = 0, cw = 0;
+        float vw = 0.0f;
+        auto load_window = [&](uint32_t at) {
+            wb = at;
+            const bool ok = at + uint32_t(gl) < E;
+            cw = ok ? dev::ld_stream(a.ci + j0 + at + gl) : 0u;  // 0: a safe dummy row
+            vw = ok ? dev::ld_stream(a.val + j0 + at + gl) : 0.0f;
+        };
+        if (E) load_window(0);
+        uint32_t base = 0;
+        while (__any_sync(FULL, base < E)) {
+            const bool act = base < E;
+            // row advance: the first row of the window ending after `base`
+            // (rows before it end at or before base), else the next window
+            while (true) {
+                const bool need = act && base >= rend_l;
+                if (!__any_sync(FULL, need)) break;
+                const unsigned later = (__ballot_sync(FULL, rwin > base) >> gbase) & gbits;
+                const bool found = need && later != 0u;
+                if (found) r = rb + uint32_t(__ffs(later) - 1);
+                if (need && !found) {
+                    rb += G;
+                    rwin = window(rb);
+                }
+                const uint32_t t = __shfl_sync(FULL, rwin, gbase + int(r - rb) * int(found));
+                if (found) {
+                    rend_l = t;
+                    xrow.load(a.x + uint64_t(r) * a.ld, gl, a.k);
+                }
+            }
+            int n = 0;
+            if (act) {
+                const uint32_t room = rend_l - base;
+                n = room < uint32_t(U) ? int(room) : U;
+            }
+            // an active group's batch lies inside the window (base - wb <= G - U);
+            // an idle group's shuffles read anything and gather nothing
+            const int s0 = gbase + int(base - wb);
+            uint32_t colu[U];
+#pragma unroll
+            for (int u = 0; u < U; ++u) colu[u] = __shfl_sync(FULL, cw, s0 + u);
+            const float pv_own = __shfl_sync(FULL, vw, s0 + gl / PER);
+            F yf[U];
+            if (act) {
+#pragma unroll
+                for (int u = 0; u < U; ++u) {
+                    const char* p;
+                    asm("mad.wide.u32 %0, %1, %2, %3;" : "=l"(p) : "r"(colu[u]), "r"(ldb), "l"(ylane));
+                    const float4 t = dev::ld_gather(reinterpret_cast<const float4*>(p), l2pol);
+                    yf[u].v[0] = t.x; yf[u].v[1] = t.y; yf[u].v[2] = t.z; yf[u].v[3] = t.w;
+                }
+            }
+            const uint32_t nb = base + uint32_t(n);
+            if (act && nb < E && nb + uint32_t(U) > wb + uint32_t(G)) load_window(nb);
+            const float r_own = __fmul_rn(pv_own, dev::batch_dots(xrow, yf, FULL, gl));  // kernels.hpp:206
+            const float res = __shfl_sync(FULL, r_own, gbase + ((gl * PER) & (G - 1)));
+            if (gl < n) __stcs(a.out + j0 + base + uint32_t(gl), res);
+            base = nb;
+        }
+    }
+    ws.finish();
+}
+
+template <int G, int U, int MINB>
+sgnn_status launch_sddmm_lock(const SddmmArgs& a, cudaStream_t s) {
+    static int per_sm = -1;
+    DeviceProps dp;
+    SGNN_TRY(device_props(&dp));
+    if (per_sm < 0) {
+        int n = 0;
+        SGNN_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, sddmm_lock_kernel<G, U, MINB>, 128, 0));
+        per_sm = std::max(n, 1);
+    }
+    const uint64_t blocks = std::min<uint64_t>(ceil_div_u64(uint64_t(a.n_workers) * G, 128),
+                                               uint64_t(dp.sm_count) * per_sm);
+    if (blocks == 0) return SGNN_OK;
+    sddmm_lock_kernel<G, U, MINB><<<unsigned(blocks), 128, 0, s>>>(a);
+    SGNN_LAUNCH_CHECK();
+    return SGNN_OK;
+}
+
 using SddmmLaunch = sgnn_status (*)(const SddmmArgs&, cudaStream_t);
 
 template <int G, int V, int U, bool VEC, int MINB = 1>
@@ -350,6 +475,11 @@ sgnn_status run_sddmm(const sgnn_csr* p, const float* x, const float* y, uint32_
         a.wctr = plan_counter(plan, s);
     }
     SddmmLaunch fn = nullptr;
+    static const bool generic = std::getenv("SGNN_SDDMM_GENERIC") != nullptr;  // A/B switch
+    // full-width lockstep kernels (cfg4: 0.79 -> 0.70 ms; register caps 6 / 7 / 8: 0.78 / 0.70 / 0.70,
+    // a two-batch software pipeline at 4-5 CTAs/SM: 0.89-0.93)
+    if (vec && !generic && k == 64 && lanes == 16 && vregs == 1) return launch_sddmm_lock<16, 8, 7>(a, s);
+    if (vec && !generic && k == 32 && lanes == 8 && vregs == 1) return launch_sddmm_lock<8, 8, 1>(a, s);
     if (vec) {
         if (lanes == 4) fn = &launch_sddmm<4, 1, 8, true>;
         else if (lanes == 8) fn = &launch_sddmm<8, 1, 8, true>;
