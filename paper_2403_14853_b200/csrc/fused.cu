@@ -475,7 +475,7 @@ sgnn_status run_sddmm(const sgnn_csr* p, const float* x, const float* y, uint32_
         a.wctr = plan_counter(plan, s);
     }
     SddmmLaunch fn = nullptr;
-    static const bool generic = std::getenv("SGNN_SDDMM_GENERIC") != nullptr;  // A/B switch
+    const bool generic = std::getenv("SGNN_SDDMM_GENERIC") != nullptr;  // A/B switch (tests)
     // full-width lockstep kernels (cfg4: 0.79 -> 0.70 ms; register caps 6 / 7 / 8: 0.78 / 0.70 / 0.70,
     // a two-batch software pipeline at 4-5 CTAs/SM: 0.89-0.93)
     if (vec && !generic && k == 64 && lanes == 16 && vregs == 1) return launch_sddmm_lock<16, 8, 7>(a, s);

@@ -26,6 +26,10 @@ def main():
         r = ops.sddmm(p, x, y)
         print(json.dumps({"op": "sddmm", "ms": round(ms, 4), "sum": float(r.values.double().sum())}))
         return
+    if sys.argv[1:] == ["fused"]:
+        ms = t(lambda: ops.fusedmm(p, x, y, "sigmoid_mul", "sum", out), flush)
+        print(json.dumps({"op": "fusedmm sigmoid sum", "ms": round(ms, 4), "sum": float(out.double().sum())}))
+        return
     ref = ops.fusedmm(p, x, y, "sigmoid_mul", "sum", out.clone())
     for lv in ((16, 1, 8, 5), (16, 1, 8, 6), (16, 1, 16, 1), (16, 1, 16, 4), (16, 1, 16, 5)):
         for pi in (128, 256):

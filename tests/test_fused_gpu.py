@@ -206,3 +206,29 @@ def test_tma_pipeline_bitwise_register_kernels(cuda, k, monkeypatch):
 
 def _fused_layout_kw(k):
     return {"lanes": 16 if k == 64 else 32, "vec": 1, "unroll": 8, "k_tile": k}
+
+
+@pytest.mark.parametrize("k", [32, 64])
+def test_sddmm_lockstep_kernel_bitwise_generic(cuda, k, monkeypatch):
+    """The full-width lockstep SDDMM (sddmm_lock_kernel, K = 32 / 64) gives bit
+    for bit the generic kernel's results (same split, batches and dot tree):
+    hub rows over many (col, val) windows, runs of empty rows longer than the
+    row-end window, single-nonzero rows."""
+    from paper_2403_14853_b200 import graphs
+    ops = _ops()
+    rng = np.random.default_rng(11)
+    n = 1 << 13
+    rp, ci = graphs.rmat(13, n * 10, seed=4)
+    deg = np.diff(rp.astype(np.int64))
+    assert (deg == 0).sum() > 100 and (deg == 1).any() and deg.max() > 1000
+    v = rng.uniform(-1, 1, len(ci)).astype(np.float32)
+    x = rng.normal(0, 0.1, (n, k)).astype(np.float32)
+    y = rng.normal(0, 0.1, (n, k)).astype(np.float32)
+    p = ops.CsrMatrix.from_numpy(rp, ci, v, n)
+    xt, yt = _t(x), _t(y)
+    got = ops.sddmm(p, xt, yt).values.cpu().numpy()
+    monkeypatch.setenv("SGNN_SDDMM_GENERIC", "1")
+    want = ops.sddmm(p, xt, yt).values.cpu().numpy()
+    monkeypatch.delenv("SGNN_SDDMM_GENERIC")
+    np.testing.assert_array_equal(got.view(np.uint32), want.view(np.uint32))
+    check_sddmm(rp, ci, v, n, x, y)
