@@ -198,3 +198,45 @@ def test_is_symmetric_upper_lower_counting(cuda):
     assert not sym(rp, ci, v2, 4096)
     rp2, ci2 = graphs.rmat(12, 4096 * 16, seed=11)
     assert not sym(rp2, ci2, np.ones(len(ci2), np.float32), 4096)
+
+
+@pytest.mark.parametrize("shape,hub,empty", [((3000, (1 << 23) + 3), 0, 0.1),   # 24-bit columns: 3 passes of 8 bits
+                                             ((20000, 1 << 18), 50000, 0.6),    # hub row over ~12 tiles, long empty runs
+                                             ((9000, 2047), 0, 0.0)])           # 11 bits: one pass, 2048 bins
+def test_transpose_pass_counts_hubs_and_no_values(cuda, shape, hub, empty):
+    """The radix plan's pass counts / digit widths (1 and 3 passes), a hub row
+    spanning many 4096-nonzero tiles next to runs of empty rows longer than a
+    tile (the tile-row precomputation), and the structure-only call (null
+    values) -- all bit-exact with the reference's counting sort."""
+    import ctypes as C
+
+    import torch
+    from paper_2403_14853_b200._lib import check, lib
+    ops = _ops()
+    m, n = shape
+    rng = np.random.default_rng(m + n)
+    cnt = rng.binomial(min(n, 40), 0.5, size=m)
+    cnt[rng.random(m) < empty] = 0
+    rows = [np.unique(rng.integers(0, n, size=int(c))) for c in cnt]  # sorted, distinct
+    cnt = np.array([len(r) for r in rows], np.int64)
+    rp = np.zeros(m + 1, np.uint64)
+    rp[1:] = np.cumsum(cnt)
+    ci = np.concatenate(rows).astype(np.uint32)
+    v = rng.uniform(-1, 1, len(ci)).astype(np.float32)
+    if hub:
+        cnt = np.diff(rp.astype(np.int64))
+        cnt[0] = hub
+        rows = [np.sort(rng.choice(n, size=int(c), replace=False)) if c else np.zeros(0, np.int64) for c in cnt]
+        rp = np.zeros(m + 1, np.uint64)
+        rp[1:] = np.cumsum(cnt)
+        ci = np.concatenate(rows).astype(np.uint32)
+        v = rng.uniform(-1, 1, len(ci)).astype(np.float32)
+    a = _dev(rp, ci, v, n)
+    want = port.transpose(rp, ci, v, n)
+    _assert_csr_equal(ops.transpose(a).to_numpy(), want)
+    trp = torch.empty(n + 1, dtype=torch.int64, device="cuda")
+    tci = torch.empty(len(ci), dtype=torch.int32, device="cuda")
+    check(lib().sgnn_csr_transpose(C.byref(a.c()), trp.data_ptr(), tci.data_ptr(), None, None, 0, ops._stream()),
+          "transpose")
+    np.testing.assert_array_equal(trp.cpu().numpy().view(np.uint64), want[0])
+    np.testing.assert_array_equal(tci.cpu().numpy().view(np.uint32), want[1])
