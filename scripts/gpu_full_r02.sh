@@ -18,3 +18,6 @@ timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 300 --c
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:spmm_worker_kernel --launch-skip 3 --launch-count 1 -f -o $O/cfg5_spmm_mean python bench.py --steps 2 --warmup 3 --no-e2e --no-cpu-baseline > $O/ncu_cfg5.log 2>&1
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:radix_downsweep --launch-count 2 -f -o $O/cfg2_transpose python bench.py --workload cfg2 --steps 2 --warmup 3 --no-e2e --no-cpu-baseline > $O/ncu_tr.log 2>&1
 ls -la $O
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:sddmm_lock --launch-skip 3 --launch-count 1 -f -o $O/cfg4_sddmm python scripts/fused_u16_probe.py sddmm > $O/ncu_sd.log 2>&1
+timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file $O/tr_launches.csv python scripts/transpose_probe.py 2 > $O/ncu_trl.log 2>&1
+ls -la $O
