@@ -130,21 +130,53 @@ __global__ void __launch_bounds__(kScanThreads) scan_down_kernel(const TIn* in, 
                                                                  uint64_t n,
                                                                  const TOut* __restrict__ offsets) {
     const uint64_t base = uint64_t(blockIdx.x) * kScanTile + uint64_t(threadIdx.x) * kScanItems;
+    // a thread's 8 consecutive items move as 16-byte vectors when the whole
+    // run is in range and aligned (a scalar blocked load touches 8 sectors
+    // per warp instruction)
+    const bool vin = sizeof(TIn) == 4 && base + kScanItems <= n &&
+                     (reinterpret_cast<uintptr_t>(in + base) & 15) == 0;
+    const bool vout = base + kScanItems <= n && (reinterpret_cast<uintptr_t>(out + base) & 15) == 0 &&
+                      (sizeof(TOut) == 4 || sizeof(TOut) == 8);
     TOut vals[kScanItems];
     TOut s = 0;
+    if (vin) {
+        static_assert(kScanItems == 8, "two 16-byte vectors per thread");
+        const uint4 a = *reinterpret_cast<const uint4*>(in + base);
+        const uint4 b = *reinterpret_cast<const uint4*>(in + base + 4);
+        const uint32_t w[8] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w};
 #pragma unroll
-    for (int i = 0; i < kScanItems; ++i) {
-        const uint64_t idx = base + i;
-        vals[i] = idx < n ? TOut(in[idx]) : TOut(0);
-        s += vals[i];
+        for (int i = 0; i < kScanItems; ++i) {
+            vals[i] = TOut(w[i]);
+            s += vals[i];
+        }
+    } else {
+#pragma unroll
+        for (int i = 0; i < kScanItems; ++i) {
+            const uint64_t idx = base + i;
+            vals[i] = idx < n ? TOut(in[idx]) : TOut(0);
+            s += vals[i];
+        }
     }
     TOut total;
     TOut run = block_exclusive(s, &total) + (offsets ? offsets[blockIdx.x] : TOut(0));
+    if (vout) {
+        TOut o[kScanItems];
 #pragma unroll
-    for (int i = 0; i < kScanItems; ++i) {
-        const uint64_t idx = base + i;
-        if (idx < n) out[idx] = run;
-        run += vals[i];
+        for (int i = 0; i < kScanItems; ++i) {
+            o[i] = run;
+            run += vals[i];
+        }
+        uint4* dst = reinterpret_cast<uint4*>(out + base);
+        constexpr int NV = int(kScanItems * sizeof(TOut) / 16);
+#pragma unroll
+        for (int q = 0; q < NV; ++q) dst[q] = reinterpret_cast<const uint4*>(o)[q];
+    } else {
+#pragma unroll
+        for (int i = 0; i < kScanItems; ++i) {
+            const uint64_t idx = base + i;
+            if (idx < n) out[idx] = run;
+            run += vals[i];
+        }
     }
     // the thread owning the last element writes the grand total to out[n]
     if (n > 0 && base <= n - 1 && n - 1 < base + kScanItems) out[n] = run;

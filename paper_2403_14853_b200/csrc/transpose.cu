@@ -33,11 +33,14 @@ constexpr uint64_t kTile = uint64_t(kThreads) * kItems;  // 4096 nonzeros
 constexpr int kMaxDigitBits = 11;  // <= 2048 bins (u16 warp counters, <= 8 bins per thread)
 constexpr unsigned kFull = 0xffffffffu;
 
+constexpr int kUpTiles = kWarps;  // tiles per upsweep CTA (one per warp): a 32-byte sector per digit
+
 struct RadixPlan {
     int passes = 1;
     int dbits = 1;
     uint32_t bins = 2;
     uint64_t tiles = 0;
+    uint64_t tstride = 0;  // tiles rounded up to kUpTiles: the [digit][tile] count rows
 };
 
 RadixPlan radix_plan(uint32_t n_cols, uint64_t nnz) {
@@ -51,6 +54,7 @@ RadixPlan radix_plan(uint32_t n_cols, uint64_t nnz) {
     r.dbits = std::max(1, (nbits + r.passes - 1) / r.passes);
     r.bins = 1u << r.dbits;
     r.tiles = ceil_div_u64(nnz, kTile);
+    r.tstride = ceil_div_u64(r.tiles, kUpTiles) * kUpTiles;
     return r;
 }
 
@@ -80,7 +84,7 @@ Workspace carve(void* base, const sgnn_csr* a, const RadixPlan& rp) {
     w.keys_b = reinterpret_cast<uint32_t*>(take(4 * nnz));
     w.rows_a = reinterpret_cast<uint32_t*>(take(4 * nnz));
     w.vals_a = reinterpret_cast<float*>(take(4 * nnz));
-    w.hist = reinterpret_cast<uint32_t*>(take(4 * (size_t(rp.bins) * rp.tiles + 1)));
+    w.hist = reinterpret_cast<uint32_t*>(take(4 * (size_t(rp.bins) * rp.tstride + 1)));
     w.tile_row0 = reinterpret_cast<uint32_t*>(take(4 * (size_t(rp.tiles) + 1)));
     w.bytes = off;
     return w;
@@ -137,26 +141,41 @@ __global__ void col_starts_kernel(const uint32_t* __restrict__ keys, uint64_t nn
         for (int64_t c = k[i] + 1; c <= k[i + 1]; ++c) trp[c] = p0 + i;
 }
 
+// Per-tile digit counts, hist[d * tstride + t]: warp w of CTA b counts tile
+// b * kUpTiles + w into its own shared histogram (16 loads per lane in flight
+// before their shared atomics), then each digit's kUpTiles counts leave as one
+// aligned 32-byte sector (one tile per CTA wrote a 4-byte partial sector per
+// digit: 512 scattered writes per 4096 nonzeros).
 __global__ void __launch_bounds__(kThreads) radix_upsweep_kernel(const uint32_t* __restrict__ keys,
                                                                  uint64_t n, int shift,
-                                                                 uint32_t mask, uint64_t tiles,
+                                                                 uint32_t mask, uint64_t tstride,
                                                                  uint32_t* __restrict__ hist) {
-    extern __shared__ uint32_t sh[];
+    static_assert(kUpTiles == 8, "two 16-byte stores per digit");
+    extern __shared__ uint32_t sh[];  // [kUpTiles][bins]
     const uint32_t bins = mask + 1;
-    for (uint32_t d = threadIdx.x; d < bins; d += kThreads) sh[d] = 0;
-    const uint64_t base = uint64_t(blockIdx.x) * kTile;
-    uint32_t k[kItems];
+    for (uint32_t d = threadIdx.x; d < kUpTiles * bins; d += kThreads) sh[d] = 0;
+    __syncthreads();
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    uint32_t* wh = sh + wid * bins;
+    const uint64_t base = (uint64_t(blockIdx.x) * kUpTiles + wid) * kTile;
+    constexpr int R = 16;
+    for (int r0 = 0; r0 < int(kTile / 32); r0 += R) {
+        uint32_t k[R];
 #pragma unroll
-    for (int r = 0; r < kItems; ++r) {  // all loads in flight before the first atomic
-        const uint64_t idx = base + uint64_t(r) * kThreads + threadIdx.x;
-        k[r] = idx < n ? __ldcs(keys + idx) : 0xffffffffu;
+        for (int q = 0; q < R; ++q) {
+            const uint64_t idx = base + uint64_t(r0 + q) * 32 + lane;
+            k[q] = idx < n ? __ldcs(keys + idx) : 0u;
+        }
+#pragma unroll
+        for (int q = 0; q < R; ++q)
+            if (base + uint64_t(r0 + q) * 32 + lane < n) atomicAdd(wh + ((k[q] >> shift) & mask), 1u);
     }
     __syncthreads();
-#pragma unroll
-    for (int r = 0; r < kItems; ++r)
-        if (base + uint64_t(r) * kThreads + threadIdx.x < n) atomicAdd(sh + ((k[r] >> shift) & mask), 1u);
-    __syncthreads();
-    for (uint32_t d = threadIdx.x; d < bins; d += kThreads) hist[uint64_t(d) * tiles + blockIdx.x] = sh[d];
+    for (uint32_t d = threadIdx.x; d < bins; d += kThreads) {
+        uint4* dst = reinterpret_cast<uint4*>(hist + uint64_t(d) * tstride + uint64_t(blockIdx.x) * kUpTiles);
+        dst[0] = make_uint4(sh[d], sh[bins + d], sh[2 * bins + d], sh[3 * bins + d]);
+        dst[1] = make_uint4(sh[4 * bins + d], sh[5 * bins + d], sh[6 * bins + d], sh[7 * bins + d]);
+    }
 }
 
 // Exclusive scan of one value per thread over the block (warp shuffles, one
@@ -205,7 +224,7 @@ __global__ void __launch_bounds__(kThreads, 3) radix_downsweep_kernel(
     const uint32_t* __restrict__ keys_in, const uint32_t* __restrict__ rows_in,
     const float* __restrict__ vals_in, uint32_t* __restrict__ keys_out,
     uint32_t* __restrict__ rows_out, float* __restrict__ vals_out, uint64_t n, int shift,
-    int dbits, uint64_t tiles, const uint32_t* __restrict__ hist_scan,
+    int dbits, uint64_t tstride, const uint32_t* __restrict__ hist_scan,
     const uint64_t* __restrict__ rp, uint32_t m, const uint32_t* __restrict__ tile_row0) {
     constexpr int T = kThreads * kItems;  // 4096
     constexpr int WI = T / kWarps;        // 512 items per warp
@@ -254,7 +273,7 @@ __global__ void __launch_bounds__(kThreads, 3) radix_downsweep_kernel(
         if (d < bins) {
             const uint32_t dst = static_cast<uint32_t>(__cvta_generic_to_shared(sgoff + d));
             asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(dst),
-                         "l"(hist_scan + uint64_t(d) * tiles + blockIdx.x)
+                         "l"(hist_scan + uint64_t(d) * tstride + blockIdx.x)
                          : "memory");
         }
     }
@@ -359,14 +378,15 @@ __global__ void __launch_bounds__(kThreads, 3) radix_downsweep_kernel(
 
 template <bool FIRST, int DB>
 sgnn_status launch_down_db(bool vals, const uint32_t* ki, const uint32_t* ri, const float* vi, uint32_t* ko,
-                           uint32_t* ro, float* vo, uint64_t n, int shift, uint64_t tiles, const uint32_t* hs,
+                           uint32_t* ro, float* vo, uint64_t n, int shift, uint64_t tiles, uint64_t tstride,
+                           const uint32_t* hs,
                            const uint64_t* rp, uint32_t m, const uint32_t* tr0, cudaStream_t s) {
     constexpr size_t bins = size_t(1) << DB;
     const size_t smem = kDownSmemFixed + 2 * 4 * bins + 4 * kWarps * (bins / 2);
     auto k = vals ? radix_downsweep_kernel<FIRST, true, DB> : radix_downsweep_kernel<FIRST, false, DB>;
     SGNN_CUDA_TRY(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
     SGNN_CUDA_TRY(cudaFuncSetAttribute(k, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
-    k<<<unsigned(tiles), kThreads, smem, s>>>(ki, ri, vi, ko, ro, vo, n, shift, DB, tiles, hs, rp, m, tr0);
+    k<<<unsigned(tiles), kThreads, smem, s>>>(ki, ri, vi, ko, ro, vo, n, shift, DB, tstride, hs, rp, m, tr0);
     SGNN_LAUNCH_CHECK();
     return SGNN_OK;
 }
@@ -375,10 +395,10 @@ sgnn_status launch_down_db(bool vals, const uint32_t* ki, const uint32_t* ri, co
 template <bool FIRST>
 sgnn_status launch_down(bool vals, const uint32_t* ki, const uint32_t* ri, const float* vi, uint32_t* ko,
                         uint32_t* ro, float* vo, uint64_t n, int shift, int dbits, uint64_t tiles,
-                        const uint32_t* hs, const uint64_t* rp, uint32_t m, const uint32_t* tr0,
+                        uint64_t tstride, const uint32_t* hs, const uint64_t* rp, uint32_t m, const uint32_t* tr0,
                         cudaStream_t s) {
 #define SGNN_DOWN_CASE(D) \
-    case D: return launch_down_db<FIRST, D>(vals, ki, ri, vi, ko, ro, vo, n, shift, tiles, hs, rp, m, tr0, s);
+    case D: return launch_down_db<FIRST, D>(vals, ki, ri, vi, ko, ro, vo, n, shift, tiles, tstride, hs, rp, m, tr0, s);
     switch (dbits) {
         SGNN_DOWN_CASE(1) SGNN_DOWN_CASE(2) SGNN_DOWN_CASE(3) SGNN_DOWN_CASE(4) SGNN_DOWN_CASE(5)
         SGNN_DOWN_CASE(6) SGNN_DOWN_CASE(7) SGNN_DOWN_CASE(8) SGNN_DOWN_CASE(9) SGNN_DOWN_CASE(10)
@@ -515,21 +535,26 @@ sgnn_status run_transpose(const sgnn_csr* a, uint64_t* trp, uint32_t* tci, float
             uint32_t* rows_dst = to_out ? tci : w.rows_a;
             float* vals_dst = to_out ? tv : w.vals_a;
             const int shift = p * plan.dbits;
-            const size_t up_smem = sizeof(uint32_t) * plan.bins;
-            radix_upsweep_kernel<<<unsigned(plan.tiles), kThreads, up_smem, s>>>(
-                keys_src, a->nnz, shift, mask, plan.tiles, w.hist);
+            const size_t up_smem = sizeof(uint32_t) * plan.bins * kUpTiles;
+            if (cudaFuncSetAttribute(radix_upsweep_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     int(up_smem)) != cudaSuccess) {
+                st = fail(SGNN_ERR_CUDA, "transpose: upsweep attribute failed");
+                break;
+            }
+            radix_upsweep_kernel<<<unsigned(plan.tstride / kUpTiles), kThreads, up_smem, s>>>(
+                keys_src, a->nnz, shift, mask, plan.tstride, w.hist);
             if (cudaGetLastError() != cudaSuccess) {
                 st = fail(SGNN_ERR_CUDA, "transpose: upsweep launch failed");
                 break;
             }
-            st = exclusive_scan_u32(w.hist, w.hist, uint64_t(plan.bins) * plan.tiles, s);
+            st = exclusive_scan_u32(w.hist, w.hist, uint64_t(plan.bins) * plan.tstride, s);
             if (st != SGNN_OK) break;
             if (first)
                 st = launch_down<true>(vals, keys_src, rows_src, vals_src, keys_dst, rows_dst, vals_dst, a->nnz,
-                                       shift, plan.dbits, plan.tiles, w.hist, a->row_ptr, a->n_rows, w.tile_row0, s);
+                                       shift, plan.dbits, plan.tiles, plan.tstride, w.hist, a->row_ptr, a->n_rows, w.tile_row0, s);
             else
                 st = launch_down<false>(vals, keys_src, rows_src, vals_src, keys_dst, rows_dst, vals_dst, a->nnz,
-                                        shift, plan.dbits, plan.tiles, w.hist, a->row_ptr, a->n_rows, w.tile_row0, s);
+                                        shift, plan.dbits, plan.tiles, plan.tstride, w.hist, a->row_ptr, a->n_rows, w.tile_row0, s);
             keys_src = keys_dst;
             rows_src = rows_dst;
             vals_src = vals_dst;
