@@ -181,3 +181,32 @@ def test_errors(cuda):
         e0.epochs(1, LR)
     with pytest.raises(ops.ConfigError):
         e0.stats(0, 1)  # not run yet
+
+
+@pytest.mark.parametrize("kind", ["sage-sum", "sage-mean"])
+def test_nccl_communicator_one_rank_bitwise(cuda, kind):
+    """A real NCCL communicator (sgnn_comm_get_unique_id + ncclCommInitRank on
+    this GPU through the library's run-time-loaded NCCL) attached to the
+    partitioned trainer at one rank: the trainer built over it gives bitwise
+    the communicator-less run (at one rank the exchanges are skipped, so this
+    pins the NCCL bring-up / teardown every N > 1 launch goes through, on the
+    hardware; the exchange logic itself is covered by the loopback tests)."""
+    from paper_2403_14853_b200 import dist
+    g, rp, ci, v, x, lab, mask = _golden()
+    f = x.shape[1]
+    ws = _split(g[f"{kind}_w0"], f, HIDDEN, CLASSES)
+    loss0, acc0, w0, _, _ = _run(1, rp, ci, v, x, lab, mask, kind, g[f"{kind}_w0"], 6)
+    comm = dist.Comm.nccl(dist.Comm.unique_id(), 1, 0)
+    assert (comm.nranks, comm.rank, comm.kind) == (1, 0, "nccl")
+    n = len(rp) - 1
+    eng = dist.DistSage.from_graph(comm, rp, ci, v, x, lab, mask, HIDDEN, CLASSES, kind, rank=0,
+                                   bounds=np.array([0, n], np.uint32), max_epochs=6)
+    eng.set_weights(*ws)
+    eng.epochs(6, LR)
+    loss, acc, _ = eng.stats()
+    np.testing.assert_array_equal(loss, loss0)
+    np.testing.assert_array_equal(acc, acc0)
+    for a, b in zip(eng.get_weights(), w0):
+        np.testing.assert_array_equal(a.cpu().numpy().view(np.uint32), b.view(np.uint32))
+    eng.close()
+    comm.close()
