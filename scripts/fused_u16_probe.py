@@ -31,8 +31,11 @@ def main():
         print(json.dumps({"op": "fusedmm sigmoid sum", "ms": round(ms, 4), "sum": float(out.double().sum())}))
         return
     ref = ops.fusedmm(p, x, y, "sigmoid_mul", "sum", out.clone())
-    for lv in ((16, 1, 8, 5), (16, 1, 8, 6), (16, 1, 16, 1), (16, 1, 16, 4), (16, 1, 16, 5)):
-        for pi in (128, 256):
+    layouts = ((16, 1, 8, 5),) if sys.argv[1:] == ["paths"] else \
+        ((16, 1, 8, 5), (16, 1, 8, 6), (16, 1, 16, 1), (16, 1, 16, 4), (16, 1, 16, 5))
+    paths = (256, 512, 1024, 2048) if sys.argv[1:] == ["paths"] else (128, 256)
+    for lv in layouts:
+        for pi in paths:
             plan = ops.Plan(p, k, lanes=lv[0], vec=lv[1], unroll=lv[2], occupancy=lv[3], path_items=pi)
             ms = t(lambda: ops.fusedmm(p, x, y, "sigmoid_mul", "sum", out, plan=plan), flush)
             same = bool(torch.equal(out.view(torch.int32), ref.view(torch.int32)))
