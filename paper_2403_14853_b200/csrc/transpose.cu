@@ -236,9 +236,15 @@ __global__ void __launch_bounds__(kThreads, 3) radix_downsweep_kernel(
     // bins per thread for the digit bookkeeping (1 when bins < kThreads)
     constexpr uint32_t bpt = bins >= uint32_t(kThreads) ? bins / kThreads : 1u;
     constexpr uint32_t cwords = bins / 2;
-    uint32_t* skey = sh;                    // [T]
-    float* sval = reinterpret_cast<float*>(sh + T);  // [T]
-    uint32_t* srow = sh + 2 * T;            // [T] (FIRST: row marks, then rows)
+    uint32_t* skey = sh;                    // [T] (FIRST: first the row marks, then the rows)
+    // staged (row, value) pairs as one 8-byte store / load per item (not in
+    // the first pass: the extra registers spill there); else rows and values
+    // apart
+    constexpr bool PACK = VALS && !FIRST;
+    uint2* srv = reinterpret_cast<uint2*>(sh + T);   // [T] PACK
+    uint32_t* srow = sh + T;                          // [T] otherwise
+    float* sval = reinterpret_cast<float*>(sh + 2 * T);
+    uint32_t* smark = skey;
     uint32_t* sgoff = sh + 3 * T;           // [bins] global offset - tile digit start
     uint32_t* sdst = sgoff + bins;          // [bins] tile digit start
     uint32_t* wcnt = sdst + bins;           // [kWarps][bins / 2]: u16 counters in pairs
@@ -251,7 +257,7 @@ __global__ void __launch_bounds__(kThreads, 3) radix_downsweep_kernel(
     uint32_t r0 = 0;
     if (FIRST) {
         r0 = __ldg(tile_row0 + blockIdx.x);
-        for (int i = threadIdx.x; i < T; i += kThreads) srow[i] = 0;
+        for (int i = threadIdx.x; i < T; i += kThreads) smark[i] = 0;
     }
     // every load of the tile in flight together: items, the tile's global
     // digit offsets, (FIRST) the row starts inside the tile
@@ -284,24 +290,24 @@ __global__ void __launch_bounds__(kThreads, 3) radix_downsweep_kernel(
         for (uint32_t r = r0 + 1 + threadIdx.x; r <= m; r += kThreads) {
             const uint64_t st = __ldg(rp + r);
             if (st >= base + cnt) break;
-            atomicAdd(srow + (st - base), 1u);
+            atomicAdd(smark + (st - base), 1u);
         }
         __syncthreads();
         // inclusive scan of the marks: item i's row = r0 + marks(<= i)
         uint32_t loc[kItems], acc = 0;
 #pragma unroll
         for (int q = 0; q < kItems; ++q) {
-            acc += srow[threadIdx.x * kItems + q];
+            acc += smark[threadIdx.x * kItems + q];
             loc[q] = acc;
         }
         const uint32_t pre = r0 + block_exclusive_scan(acc, s_warp[0]);
 #pragma unroll
-        for (int q = 0; q < kItems; ++q) srow[threadIdx.x * kItems + q] = pre + loc[q];
+        for (int q = 0; q < kItems; ++q) smark[threadIdx.x * kItems + q] = pre + loc[q];
         __syncthreads();
 #pragma unroll
-        for (int q = 0; q < kItems; ++q) rr[q] = srow[wid * WI + q * 32 + lane];
+        for (int q = 0; q < kItems; ++q) rr[q] = smark[wid * WI + q * 32 + lane];
     }
-    __syncthreads();  // counters zeroed (and FIRST: srow read before staging reuses it)
+    __syncthreads();  // counters zeroed (and FIRST: the rows read before staging reuses skey)
     // A. warp-local stable ranks
     const unsigned lt = (1u << lane) - 1u;
     uint32_t* mycnt = wcnt + wid * cwords;
@@ -330,8 +336,26 @@ __global__ void __launch_bounds__(kThreads, 3) radix_downsweep_kernel(
     // sdst), block scan, then the tile's digit starts
     asm volatile("cp.async.wait_all;" ::: "memory");
     uint32_t run = 0;
-    for (uint32_t b = 0; b < bpt; ++b) {
-        const uint32_t d = threadIdx.x * bpt + b;
+    if constexpr (bpt >= 2) {
+        // a thread's digits are whole counter words: both halves per access
+        constexpr uint32_t wpt = bpt / 2;
+#pragma unroll
+        for (uint32_t b = 0; b < wpt; ++b) {
+            const uint32_t wi = threadIdx.x * wpt + b;  // digits 2 wi, 2 wi + 1
+            uint32_t tlo = 0, thi = 0;
+#pragma unroll
+            for (int w = 0; w < kWarps; ++w) {
+                const uint32_t c = wcnt[w * cwords + wi];
+                wcnt[w * cwords + wi] = tlo | (thi << 16);
+                tlo += c & 0xffffu;
+                thi += c >> 16;
+            }
+            sdst[2 * wi] = tlo;
+            sdst[2 * wi + 1] = thi;
+            run += tlo + thi;
+        }
+    } else {
+        const uint32_t d = threadIdx.x;
         if (d < bins) {
             uint32_t t = 0;
 #pragma unroll
@@ -362,8 +386,12 @@ __global__ void __launch_bounds__(kThreads, 3) radix_downsweep_kernel(
         const uint32_t d = pk[q] >> 16;
         const uint32_t slot = sdst[d] + wc16[wid * bins + d] + (pk[q] & 0xffffu);
         skey[slot] = kk[q];
-        srow[slot] = rr[q];
-        if (VALS) sval[slot] = vv[q];
+        if (PACK) {
+            srv[slot] = make_uint2(rr[q], __float_as_uint(vv[q]));
+        } else {
+            srow[slot] = rr[q];
+            if (VALS) sval[slot] = vv[q];
+        }
     }
     __syncthreads();
     // D. contiguous runs per digit to global memory
@@ -371,8 +399,14 @@ __global__ void __launch_bounds__(kThreads, 3) radix_downsweep_kernel(
         const uint32_t key = skey[k];
         const uint64_t dst = uint64_t(sgoff[(key >> shift) & mask]) + k;
         keys_out[dst] = key;
-        rows_out[dst] = srow[k];
-        if (VALS) vals_out[dst] = sval[k];
+        if (PACK) {
+            const uint2 rv = srv[k];
+            rows_out[dst] = rv.x;
+            vals_out[dst] = __uint_as_float(rv.y);
+        } else {
+            rows_out[dst] = srow[k];
+            if (VALS) vals_out[dst] = sval[k];
+        }
     }
 }
 
