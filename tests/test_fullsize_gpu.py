@@ -1,8 +1,9 @@
-"""Parity at BASELINE sizes (cfg2 - cfg5): full outputs are checked on a
-deterministic row sample that includes every hub row (the oracle runs on the
-sampled rows only), the transpose is checked bit-exact in full, and
-size-independent properties (involution, linearity, plan transparency) are
-checked on the whole matrices."""
+"""Parity at BASELINE sizes (cfg2 - cfg5): the oracle on a deterministic row
+sample that includes every hub row (with the bit-exact checks the contract
+promises on those rows), every row of cfg2 / cfg3 / cfg5's SpMMs against an
+independent fp64 SpMM and every row of cfg4 against the oracle, the
+transpose bit-exact in full, and size-independent properties (involution,
+linearity, plan transparency) on the whole matrices."""
 import numpy as np
 import pytest
 
@@ -195,3 +196,99 @@ def test_cfg5_mean_spmm_and_backward_sampled_rows(cuda):
     _, _, smv = _sub(w.row_ptr, w.col_idx, mv, rows)
     want_b = port.spmm(srp, sci, smv.astype(np.float64), x.astype(np.float64), 0)
     assert_spmm_close(dx[rows], want_b, port.spmm_absdenom(srp, sci, smv, x, 0), what="cfg5 backward")
+
+
+def _all_rows_fp64(rp, ci, v, n_cols, xt, reduce_mean=False):
+    """Every row of A X in fp64 by an independent implementation (cuSPARSE
+    through torch.sparse, test infrastructure only) and the tolerance
+    denominators sum_j |a_ij x_jk| (/ deg for mean), on the device."""
+    import torch
+    n = len(rp) - 1
+    crow = torch.from_numpy(rp.astype(np.int64)).cuda()
+    col = torch.from_numpy(ci.astype(np.int64)).cuda()
+    vals = torch.from_numpy(v.astype(np.float64)).cuda()
+    x64 = xt.double()
+    a64 = torch.sparse_csr_tensor(crow, col, vals, (n, n_cols))
+    ref = a64.matmul(x64)
+    den = torch.sparse_csr_tensor(crow, col, vals.abs(), (n, n_cols)).matmul(x64.abs())
+    del x64
+    if reduce_mean:
+        deg = torch.diff(crow).double().clamp_min(1).unsqueeze(1)
+        ref, den = ref / deg, den / deg
+    return ref, den
+
+
+def _assert_all_rows(got, ref, den, what):
+    err = (got.double() - ref).abs()
+    bad = err > 1e-5 * den + 1e-30
+    assert not bool(bad.any()), f"{what}: {int(bad.sum())} outputs out of tolerance, max err/den " \
+                                f"{float((err / den.clamp_min(1e-300)).max()):.3g}"
+
+
+def test_all_rows_fullsize_vs_independent_fp64(cuda):
+    """Every output row at BASELINE sizes, not a sample: cfg2 SpMM sum / mean
+    and its backward through the cached CSC, cfg3's K=256 SpMM on the device
+    normalized adjacency, cfg5's mean SpMM and its backward through the
+    symmetric mean operand -- against an independent fp64 SpMM (cuSPARSE via
+    torch.sparse) within the oracle's tolerance 1e-5 * sum_j |a_ij x_jk|."""
+    import torch
+
+    from paper_2403_14853_b200 import graphs, ops, sage_dist
+    # cfg2
+    w = graphs.cfg2()
+    x = torch.from_numpy(graphs.normal(w.n_cols * w.k, 0, 1, 1, 21).reshape(w.n_cols, w.k)).cuda()
+    a = ops.CsrMatrix.from_numpy(w.row_ptr, w.col_idx, w.values, w.n_cols)
+    for red in ("sum", "mean"):
+        ref, den = _all_rows_fp64(w.row_ptr, w.col_idx, w.values, w.n_cols, x, red == "mean")
+        _assert_all_rows(ops.spmm(a, x, red), ref, den, f"cfg2 {red}")
+    t = ops.transpose(a)
+    trp, tci, tv = t.to_numpy()
+    dc = torch.from_numpy(graphs.normal(w.n_rows * w.k, 0, 1, 1, 22).reshape(w.n_rows, w.k)).cuda()
+    ref, den = _all_rows_fp64(trp, tci, tv, w.n_rows, dc)
+    _assert_all_rows(ops.TrainingCache(a, True).spmm_backward(dc, "sum"), ref, den, "cfg2 backward")
+    del a, t, x, dc, ref, den
+    # cfg3: A_hat (device-normalized) x H, K = 256
+    rp_a, ci_a = graphs.cfg3_graph(1)
+    a = ops.CsrMatrix.from_numpy(rp_a, ci_a, np.ones(len(ci_a), np.float32), len(rp_a) - 1)
+    ah = ops.normalize_adjacency(a, True)
+    hrp, hci, hv = ah.to_numpy()
+    n = len(hrp) - 1
+    h = torch.from_numpy(graphs.normal(n * 256, 0, 1, 1, 31).reshape(n, 256)).cuda()
+    ref, den = _all_rows_fp64(hrp, hci, hv, n, h)
+    _assert_all_rows(ops.spmm(ah, h, "sum"), ref, den, "cfg3 A_hat H")
+    del a, ah, h, ref, den
+    # cfg5: mean forward and the backward through the mean operand
+    w = graphs.cfg5(1)
+    a = ops.CsrMatrix.from_numpy(w.row_ptr, w.col_idx, w.values, w.n_cols)
+    x = torch.from_numpy(graphs.normal(w.n_cols * w.k, 0, 1, 1, 51).reshape(w.n_cols, w.k)).cuda()
+    ref, den = _all_rows_fp64(w.row_ptr, w.col_idx, w.values, w.n_cols, x, True)
+    _assert_all_rows(ops.spmm(a, x, "mean"), ref, den, "cfg5 mean")
+    del ref, den
+    mv = sage_dist.mean_operand_values(w.row_ptr, w.col_idx, w.values)
+    ref, den = _all_rows_fp64(w.row_ptr, w.col_idx, mv, w.n_cols, x)
+    _assert_all_rows(ops.TrainingCache(a, True).spmm_backward(x, "mean"), ref, den, "cfg5 backward")
+
+
+def test_cfg4_all_rows_vs_oracle(cuda):
+    """cfg4 at full size, every row / nonzero (not a sample): FusedMM
+    sigmoid_mul-sum and SDDMM against the oracle's fp64 results (~30 s of
+    oracle time), within 1e-5 of sum_j |s_ij y_jk| / |p_e| sum_k |x_ik y_jk|."""
+    import torch
+
+    from paper_2403_14853_b200 import graphs, ops
+    w = graphs.cfg4()
+    m, k = w.n_rows, w.k
+    x = graphs.normal(m * k, 0, 0.1, 1, 41).reshape(m, k)
+    y = graphs.normal(w.n_cols * k, 0, 0.1, 1, 42).reshape(w.n_cols, k)
+    p = ops.CsrMatrix.from_numpy(w.row_ptr, w.col_idx, w.values, w.n_cols)
+    xt, yt = torch.from_numpy(x).cuda(), torch.from_numpy(y).cuda()
+    got = ops.fusedmm(p, xt, yt, "sigmoid_mul", "sum").cpu().numpy()
+    want = port.fusedmm(w.row_ptr, w.col_idx, w.values, x, y, 1, 0)
+    assert_spmm_close(got, want, port.fusedmm_absdenom(w.row_ptr, w.col_idx, w.values, x, y, 1, 0),
+                      what="cfg4 fusedmm all rows")
+    del got, want
+    s = ops.sddmm(p, xt, yt).values.cpu().numpy()
+    want_s = port.sddmm(w.row_ptr, w.col_idx, w.values, x, y)
+    den = port.sddmm_absdenom(w.row_ptr, w.col_idx, w.values, x, y)
+    err = np.abs(s.astype(np.float64) - want_s)
+    assert (err <= 1e-5 * den + 1e-30).all(), f"cfg4 sddmm all nonzeros: max err/den {np.max(err / np.maximum(den, 1e-30))}"
