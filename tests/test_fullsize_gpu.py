@@ -329,3 +329,31 @@ def test_short_rows_bitwise_reference_fp32_full_size(cuda):
         assert short.mean() > (0.85 if name == "cfg2" else 0.95)
         np.testing.assert_array_equal(got[short].view(np.uint32), want[short].view(np.uint32),
                                       err_msg=f"{name} {red}")
+
+
+def test_cfg5_transpose_of_symmetric_is_identity(cuda):
+    """cfg5's symmetric 202M-nonzero graph (2^22 columns: two 11-bit radix
+    passes, 2048 bins, 49k tiles): the device transpose returns A itself, bit
+    for bit (sparse.hpp:72-89 on a symmetric matrix), and the symmetry probe
+    agrees."""
+    import torch
+
+    from paper_2403_14853_b200 import graphs, ops
+    w = graphs.cfg5(1)
+    v = graphs.uniform(len(w.col_idx), 0.0, 1.0, 1, stream=55)
+    # symmetric values: v_ij = v_ji from the unordered pair's lower entry
+    rows = np.repeat(np.arange(w.n_rows, dtype=np.int64), np.diff(w.row_ptr.astype(np.int64)))
+    cols = w.col_idx.astype(np.int64)
+    key = np.minimum(rows, cols) * w.n_cols + np.maximum(rows, cols)
+    order = np.argsort(key, kind="stable")
+    first = np.ones(len(key), bool)
+    first[1:] = key[order][1:] != key[order][:-1]
+    rep = np.maximum.accumulate(np.where(first, np.arange(len(key)), 0))
+    vs = np.empty_like(v)
+    vs[order] = v[order][rep]
+    a = ops.CsrMatrix.from_numpy(w.row_ptr, w.col_idx, vs, w.n_cols)
+    assert ops.is_symmetric(a)
+    t = ops.transpose(a)
+    torch.cuda.synchronize()
+    assert torch.equal(t.row_ptr, a.row_ptr) and torch.equal(t.col_idx, a.col_idx)
+    assert torch.equal(t.values.view(torch.int32), a.values.view(torch.int32))
