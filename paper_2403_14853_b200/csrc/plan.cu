@@ -156,7 +156,11 @@ void default_params(const sgnn_csr* a, uint32_t k, bool vec_ok, const DeviceProp
     const uint64_t groups = uint64_t(dp.sm_count > 0 ? dp.sm_count : 148) *
                             uint64_t(dp.max_threads_per_sm > 0 ? dp.max_threads_per_sm : 2048) /
                             d.lanes;
-    uint64_t want = total / ((d.lanes <= 4 ? 2 : d.lanes == 32 ? 8 : 4) * groups);
+    // full-warp groups: 8 workers per group at one float4 per lane, 4 at two
+    // or more (twice the work per nonzero: cfg3 K=256 tuner, 1024 items
+    // 1.08x over 512)
+    const uint64_t per_group = d.lanes <= 4 ? 2 : d.lanes == 32 ? (d.vec >= 2 ? 4 : 8) : 4;
+    uint64_t want = total / (per_group * groups);
     // full-warp groups: at most 1024 rows+nonzeros per worker (cfg5 tuner:
     // 1.035x over 2048; cfg2 1.55 ms, 8 per group)
     const uint32_t cap = d.lanes == 32 ? 1024 : 4096;
