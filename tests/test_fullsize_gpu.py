@@ -331,6 +331,31 @@ def test_short_rows_bitwise_reference_fp32_full_size(cuda):
                                       err_msg=f"{name} {red}")
 
 
+def test_cfg2_min_max_all_rows_and_backward_short_rows_bitwise(cuda):
+    """cfg2 at full size: min / max SpMM on every row bitwise the reference's
+    fp32 kernel (order-free reductions: no segment caveat), and the backward
+    through the cached CSC bitwise the reference's fp32 kernel on A^T for
+    every column of A with <= 256 nonzeros."""
+    import torch
+
+    from paper_2403_14853_b200 import graphs, ops
+    w = graphs.cfg2()
+    x = graphs.normal(w.n_cols * w.k, 0, 1, 1, 21).reshape(w.n_cols, w.k)
+    a = ops.CsrMatrix.from_numpy(w.row_ptr, w.col_idx, w.values, w.n_cols)
+    xt = torch.from_numpy(x).cuda()
+    for red, r in (("min", 1), ("max", 2)):
+        got = ops.spmm(a, xt, red).cpu().numpy()
+        want = _oracle_spmm_parallel(w.row_ptr, w.col_idx, w.values, x, r, np.float32)
+        np.testing.assert_array_equal(got.view(np.uint32), want.view(np.uint32), err_msg=f"cfg2 {red}")
+    dc = graphs.normal(w.n_rows * w.k, 0, 1, 1, 22).reshape(w.n_rows, w.k)
+    got = ops.TrainingCache(a, True).spmm_backward(torch.from_numpy(dc).cuda(), "sum").cpu().numpy()
+    trp, tci, tv = port.transpose(w.row_ptr, w.col_idx, w.values, w.n_cols)
+    want = _oracle_spmm_parallel(trp, tci, tv, dc, 0, np.float32)
+    short = np.diff(trp.astype(np.int64)) <= 256
+    assert short.mean() > 0.5
+    np.testing.assert_array_equal(got[short].view(np.uint32), want[short].view(np.uint32), err_msg="cfg2 backward")
+
+
 def test_cfg5_transpose_of_symmetric_is_identity(cuda):
     """cfg5's symmetric 202M-nonzero graph (2^22 columns: two 11-bit radix
     passes, 2048 bins, 49k tiles): the device transpose returns A itself, bit
