@@ -269,10 +269,27 @@ def test_all_rows_fullsize_vs_independent_fp64(cuda):
     _assert_all_rows(ops.TrainingCache(a, True).spmm_backward(x, "mean"), ref, den, "cfg5 backward")
 
 
+def _oracle_rows_parallel(fn, rp, ci, v, x, *args, parts=16):
+    """An oracle row function (port.fusedmm / fusedmm_absdenom, X row-aligned)
+    over row blocks on host threads, concatenated."""
+    from concurrent.futures import ThreadPoolExecutor
+    n = len(rp) - 1
+    cuts = np.linspace(0, n, parts + 1).astype(np.int64)
+
+    def block(i):
+        r0, r1 = int(cuts[i]), int(cuts[i + 1])
+        j0, j1 = int(rp[r0]), int(rp[r1])
+        brp = (rp[r0:r1 + 1].astype(np.int64) - j0).astype(np.uint64)
+        return fn(brp, ci[j0:j1], v[j0:j1], x[r0:r1], *args)
+
+    with ThreadPoolExecutor(parts) as ex:
+        return np.concatenate(list(ex.map(block, range(parts))))
+
+
 def test_cfg4_all_rows_vs_oracle(cuda):
-    """cfg4 at full size, every row / nonzero (not a sample): FusedMM
-    sigmoid_mul-sum and SDDMM against the oracle's fp64 results (~30 s of
-    oracle time), within 1e-5 of sum_j |s_ij y_jk| / |p_e| sum_k |x_ik y_jk|."""
+    """cfg4 at full size, every row / nonzero (not a sample): FusedMM with both
+    edge ops and all four reductions, and SDDMM, against the oracle's fp64
+    results, within 1e-5 of sum_j |s_ij y_jk| / |p_e| sum_k |x_ik y_jk|."""
     import torch
 
     from paper_2403_14853_b200 import graphs, ops
@@ -282,11 +299,12 @@ def test_cfg4_all_rows_vs_oracle(cuda):
     y = graphs.normal(w.n_cols * k, 0, 0.1, 1, 42).reshape(w.n_cols, k)
     p = ops.CsrMatrix.from_numpy(w.row_ptr, w.col_idx, w.values, w.n_cols)
     xt, yt = torch.from_numpy(x).cuda(), torch.from_numpy(y).cuda()
-    got = ops.fusedmm(p, xt, yt, "sigmoid_mul", "sum").cpu().numpy()
-    want = port.fusedmm(w.row_ptr, w.col_idx, w.values, x, y, 1, 0)
-    assert_spmm_close(got, want, port.fusedmm_absdenom(w.row_ptr, w.col_idx, w.values, x, y, 1, 0),
-                      what="cfg4 fusedmm all rows")
-    del got, want
+    for edge, eop in (("sigmoid_mul", 1), ("mul", 0)):
+        for red, rcode in (("sum", 0), ("mean", 3), ("max", 2), ("min", 1)):
+            got = ops.fusedmm(p, xt, yt, edge, red).cpu().numpy()
+            want = _oracle_rows_parallel(port.fusedmm, w.row_ptr, w.col_idx, w.values, x, y, eop, rcode)
+            den = _oracle_rows_parallel(port.fusedmm_absdenom, w.row_ptr, w.col_idx, w.values, x, y, eop, rcode)
+            assert_spmm_close(got, want, den, what=f"cfg4 fusedmm {edge} {red} all rows")
     s = ops.sddmm(p, xt, yt).values.cpu().numpy()
     want_s = port.sddmm(w.row_ptr, w.col_idx, w.values, x, y)
     den = port.sddmm_absdenom(w.row_ptr, w.col_idx, w.values, x, y)
