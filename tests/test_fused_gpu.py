@@ -232,3 +232,36 @@ def test_sddmm_lockstep_kernel_bitwise_generic(cuda, k, monkeypatch):
     monkeypatch.delenv("SGNN_SDDMM_GENERIC")
     np.testing.assert_array_equal(got.view(np.uint32), want.view(np.uint32))
     check_sddmm(rp, ci, v, n, x, y)
+
+
+@pytest.mark.parametrize("parts", [2, 5])
+def test_row_partitioned_fusedmm_sddmm_bitwise(cuda, parts):
+    """SDDMM / FusedMM shard like the SpMM -- each rank holds a
+    contiguous row block of P (global column ids, dist.row_partition's cost)
+    and its rows of X, with Y all-gathered; the concatenated block results are
+    bitwise the single-GPU ones (every row's chain, segments and dot tree
+    depend only on the row), for both edge ops and all four reductions."""
+    from paper_2403_14853_b200 import dist, graphs
+    ops = _ops()
+    rng = np.random.default_rng(parts)
+    n, k = 1 << 12, 64
+    rp, ci = graphs.rmat(12, n * 16, seed=6)
+    v = rng.uniform(0, 1, len(ci)).astype(np.float32)
+    x = rng.normal(0, 0.1, (n, k)).astype(np.float32)
+    y = rng.normal(0, 0.1, (n, k)).astype(np.float32)
+    p = ops.CsrMatrix.from_numpy(rp, ci, v, n)
+    xt, yt = _t(x), _t(y)
+    bounds = dist.row_partition(rp, parts)
+    blocks = [dist.row_block(rp, ci, v, int(bounds[r]), int(bounds[r + 1])) for r in range(parts)]
+    for edge in ("sigmoid_mul", "mul"):
+        for red in ("sum", "mean", "min", "max"):
+            full = ops.fusedmm(p, xt, yt, edge, red).cpu().numpy()
+            got = np.concatenate([ops.fusedmm(ops.CsrMatrix.from_numpy(b[0], b[1], b[2], n),
+                                              xt[int(bounds[r]):int(bounds[r + 1])].contiguous(), yt, edge, red)
+                                  .cpu().numpy() for r, b in enumerate(blocks)])
+            np.testing.assert_array_equal(got.view(np.uint32), full.view(np.uint32), err_msg=f"{edge} {red}")
+    full = ops.sddmm(p, xt, yt).values.cpu().numpy()
+    got = np.concatenate([ops.sddmm(ops.CsrMatrix.from_numpy(b[0], b[1], b[2], n),
+                                    xt[int(bounds[r]):int(bounds[r + 1])].contiguous(), yt).values.cpu().numpy()
+                          for r, b in enumerate(blocks)])
+    np.testing.assert_array_equal(got.view(np.uint32), full.view(np.uint32))
