@@ -121,7 +121,11 @@ __global__ void tile_row0_kernel(const uint64_t* __restrict__ rp, uint32_t m,
 
 // t_row_ptr from the sorted column keys: position p starts every column in
 // (keys[p-1], keys[p]] (empty columns included); p = nnz closes the rest.
-// Four positions per thread (one 16-byte load where aligned).
+// Four positions per thread (one 16-byte load where aligned).  Runs of more
+// than kGapRun empty columns are left (only their last column, the
+// nonempty one, is written) to col_gaps_kernel, so no thread walks a long run.
+constexpr int64_t kGapRun = 64;
+constexpr uint64_t kUnset = ~0ull;
 __global__ void col_starts_kernel(const uint32_t* __restrict__ keys, uint64_t nnz, uint32_t n_cols,
                                   uint64_t* __restrict__ trp) {
     const uint64_t p0 = (uint64_t(blockIdx.x) * blockDim.x + threadIdx.x) * 4;
@@ -137,8 +141,27 @@ __global__ void col_starts_kernel(const uint32_t* __restrict__ keys, uint64_t nn
             k[i + 1] = p0 + i < nnz ? int64_t(__ldg(keys + p0 + i)) : (p0 + i == nnz ? int64_t(n_cols) : k[i]);
     }
 #pragma unroll
-    for (int i = 0; i < 4; ++i)
-        for (int64_t c = k[i] + 1; c <= k[i + 1]; ++c) trp[c] = p0 + i;
+    for (int i = 0; i < 4; ++i) {
+        const int64_t lo = k[i + 1] - k[i] > kGapRun ? k[i + 1] : k[i] + 1;
+        for (int64_t c = lo; c <= k[i + 1]; ++c) trp[c] = p0 + i;
+    }
+}
+
+// The columns col_starts_kernel left unset (inside long empty runs): the
+// first position whose key is >= c (binary search of the sorted keys).
+__global__ void col_gaps_kernel(const uint32_t* __restrict__ keys, uint64_t nnz, uint32_t n_cols,
+                                uint64_t* __restrict__ trp) {
+    for (uint64_t c = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; c < n_cols;
+         c += uint64_t(gridDim.x) * blockDim.x) {
+        if (trp[c] != kUnset) continue;
+        uint64_t lo = 0, hi = nnz;
+        while (lo < hi) {
+            const uint64_t mid = lo + (hi - lo) / 2;
+            if (__ldg(keys + mid) < c) lo = mid + 1;
+            else hi = mid;
+        }
+        trp[c] = lo;
+    }
 }
 
 // Per-tile digit counts, hist[d * tstride + t]: warp w of CTA b counts tile
@@ -529,8 +552,7 @@ sgnn_status run_transpose(const sgnn_csr* a, uint64_t* trp, uint32_t* tci, float
     SGNN_TRY(device_props(&dp));
     const RadixPlan plan = radix_plan(a->n_cols, a->nnz);
     if (a->nnz == 0) {  // every column empty
-        col_starts_kernel<<<1, 32, 0, s>>>(nullptr, 0, a->n_cols, trp);
-        SGNN_LAUNCH_CHECK();
+        SGNN_CUDA_TRY(cudaMemsetAsync(trp, 0, sizeof(uint64_t) * (size_t(a->n_cols) + 1), s));
         return SGNN_OK;
     }
     const size_t need = carve(nullptr, a, plan).bytes;
@@ -595,8 +617,14 @@ sgnn_status run_transpose(const sgnn_csr* a, uint64_t* trp, uint32_t* tci, float
         }
         if (st != SGNN_OK) break;
         // t_row_ptr from the sorted keys (sparse.hpp:75-76's histogram + scan)
+        if (cudaMemsetAsync(trp, 0xff, sizeof(uint64_t) * size_t(a->n_cols), s) != cudaSuccess) {
+            st = fail(SGNN_ERR_CUDA, "transpose: memset failed");
+            break;
+        }
         const uint64_t blocks = ceil_div_u64(ceil_div_u64(a->nnz + 1, 4), 256);
         col_starts_kernel<<<unsigned(blocks), 256, 0, s>>>(keys_src, a->nnz, a->n_cols, trp);
+        const uint64_t gblocks = std::min<uint64_t>(ceil_div_u64(a->n_cols, 256), uint64_t(dp.sm_count) * 16);
+        if (a->n_cols) col_gaps_kernel<<<unsigned(gblocks), 256, 0, s>>>(keys_src, a->nnz, a->n_cols, trp);
         if (cudaGetLastError() != cudaSuccess) st = fail(SGNN_ERR_CUDA, "transpose: column-start launch failed");
     } while (false);
     if (own) scratch_free(own, s);
