@@ -54,6 +54,15 @@ __global__ void plan_coords_kernel(const uint64_t* __restrict__ rp, uint32_t m, 
 }
 
 // Per worker: number of segment partials it emits and whether a split row starts in it.
+// longest row of the matrix (clamped to u32), for the short-row kernel
+__global__ void row_max_degree_kernel(const uint64_t* __restrict__ rp, uint32_t m, uint32_t* __restrict__ out) {
+    uint32_t best = 0;
+    for (uint32_t r = blockIdx.x * blockDim.x + threadIdx.x; r < m; r += gridDim.x * blockDim.x)
+        best = max(best, uint32_t(min(rp[r + 1] - rp[r], uint64_t(0xffffffffu))));
+    for (int o = 16; o >= 1; o >>= 1) best = max(best, __shfl_xor_sync(0xffffffffu, best, o));
+    if ((threadIdx.x & 31) == 0 && best) atomicMax(out, best);
+}
+
 __global__ void plan_count_kernel(const uint64_t* __restrict__ rp, uint32_t m, uint32_t n_workers,
                                   const uint32_t* __restrict__ wrow,
                                   const uint64_t* __restrict__ wnz, uint32_t* __restrict__ nslot,
@@ -271,7 +280,8 @@ sgnn_status build_plan(const sgnn_csr* a, uint32_t k, const sgnn_plan_params* pa
     const size_t o_wslot = align(o_wnz + sizeof(uint64_t) * (size_t(W) + 1));
     const size_t o_fscan = align(o_wslot + sizeof(uint32_t) * (size_t(W) + 1));
     const size_t o_ctr = align(o_fscan + sizeof(uint32_t) * (size_t(W) + 1));
-    const size_t o_end = align(o_ctr + 2 * sizeof(uint32_t));
+    const size_t o_maxd = align(o_ctr + 2 * sizeof(uint32_t));
+    const size_t o_end = align(o_maxd + sizeof(uint32_t));
     cudaError_t ce = cudaMalloc(&plan->mem, o_end);
     if (ce != cudaSuccess) {
         delete plan;
@@ -283,13 +293,17 @@ sgnn_status build_plan(const sgnn_csr* a, uint32_t k, const sgnn_plan_params* pa
     plan->wslot = reinterpret_cast<uint32_t*>(base + o_wslot);
     uint32_t* fscan = reinterpret_cast<uint32_t*>(base + o_fscan);
     plan->wctr = reinterpret_cast<uint32_t*>(base + o_ctr);
-    ce = cudaMemsetAsync(plan->wctr, 0, 2 * sizeof(uint32_t), s);  // ordered by the readback sync below
+    uint32_t* maxd = reinterpret_cast<uint32_t*>(base + o_maxd);
+    ce = cudaMemsetAsync(plan->wctr, 0, o_end - o_ctr, s);  // counters + max degree; ordered by the readback sync below
     if (ce != cudaSuccess) {
         destroy_plan(plan);
         return fail(SGNN_ERR_CUDA, std::string("plan counter: ") + cudaGetErrorString(ce));
     }
 
     const int tb = 256;
+    if (a->n_rows)
+        row_max_degree_kernel<<<unsigned(std::min<uint64_t>(ceil_div_u64(a->n_rows, tb), uint64_t(dp.sm_count) * 8)), tb,
+                                0, s>>>(a->row_ptr, a->n_rows, maxd);
     plan_coords_kernel<<<unsigned(ceil_div_u64(uint64_t(W) + 1, tb)), tb, 0, s>>>(
         a->row_ptr, a->n_rows, a->nnz, plan->p.path_items, plan->split_T, W, plan->wrow, plan->wnz);
     ce = cudaGetLastError();
@@ -308,10 +322,11 @@ sgnn_status build_plan(const sgnn_csr* a, uint32_t k, const sgnn_plan_params* pa
         destroy_plan(plan);
         return st;
     }
-    uint32_t counts[2] = {0, 0};
+    uint32_t counts[3] = {0, 0, 0};
     ce = cudaMemcpyAsync(&counts[0], plan->wslot + W, sizeof(uint32_t), cudaMemcpyDeviceToHost, s);
     if (ce == cudaSuccess)
         ce = cudaMemcpyAsync(&counts[1], fscan + W, sizeof(uint32_t), cudaMemcpyDeviceToHost, s);
+    if (ce == cudaSuccess) ce = cudaMemcpyAsync(&counts[2], maxd, sizeof(uint32_t), cudaMemcpyDeviceToHost, s);
     if (ce == cudaSuccess) ce = cudaStreamSynchronize(s);
     if (ce != cudaSuccess) {
         destroy_plan(plan);
@@ -319,6 +334,7 @@ sgnn_status build_plan(const sgnn_csr* a, uint32_t k, const sgnn_plan_params* pa
     }
     plan->n_slots = counts[0];
     plan->n_fix = counts[1];
+    plan->max_deg = counts[2];
     if (plan->n_fix > 0) {
         // fix arrays + slot workspace
         void* fmem = nullptr;

@@ -30,6 +30,7 @@ struct sgnn_plan_s {
     uint32_t n_workers = 0;
     uint32_t n_slots = 0;   // segment partials of split rows (per pass)
     uint32_t n_fix = 0;     // split rows
+    uint32_t max_deg = 0;   // longest row (clamped to u32)
 
     // device arrays (one allocation)
     void* mem = nullptr;

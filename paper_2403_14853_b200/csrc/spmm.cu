@@ -6,6 +6,7 @@
 // __fdiv_rn without its slow-path call); layouts without a mean kernel, the
 // peer path and FusedMM run the Sum kernels and one divide pass over C.
 #include <algorithm>
+#include <cstdlib>
 
 #include "ops.cuh"
 #include "plan.cuh"
@@ -39,6 +40,44 @@ __global__ void __launch_bounds__(256) mean_divide_kernel(const uint64_t* __rest
             for (uint32_t q = lane; q < k; q += 32) row[q] = __fdiv_rn(row[q], d);
         }
     }
+}
+
+template <int G, int RED>
+sgnn_status launch_short_rows(const SpmmArgs& a, cudaStream_t s) {
+    static int per_sm = -1;
+    DeviceProps dp;
+    SGNN_TRY(device_props(&dp));
+    if (per_sm < 0) {
+        int n = 0;
+        SGNN_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, dev::spmm_short_rows_kernel<G, 8, RED>, 128, 0));
+        per_sm = std::max(n, 1);
+    }
+    const uint64_t blocks = std::min<uint64_t>(ceil_div_u64(uint64_t(a.n_rows) * G, 128), uint64_t(dp.sm_count) * per_sm);
+    if (blocks == 0) return SGNN_OK;
+    dev::spmm_short_rows_kernel<G, 8, RED><<<unsigned(blocks), 128, 0, s>>>(a);
+    SGNN_LAUNCH_CHECK();
+    return SGNN_OK;
+}
+
+template <int RED>
+sgnn_status short_rows_red(int lanes, const SpmmArgs& a, cudaStream_t s) {
+    switch (lanes) {
+        case 4: return launch_short_rows<4, RED>(a, s);
+        case 8: return launch_short_rows<8, RED>(a, s);
+        case 16: return launch_short_rows<16, RED>(a, s);
+        case 32: return launch_short_rows<32, RED>(a, s);
+    }
+    return fail(SGNN_ERR_UNSUPPORTED, "short rows: lanes");
+}
+
+sgnn_status run_short_rows(int lanes, int reduce, const SpmmArgs& a, cudaStream_t s) {
+    switch (reduce) {
+        case SGNN_REDUCE_SUM: return short_rows_red<SGNN_REDUCE_SUM>(lanes, a, s);
+        case SGNN_REDUCE_MEAN: return short_rows_red<SGNN_REDUCE_MEAN>(lanes, a, s);
+        case SGNN_REDUCE_MIN: return short_rows_red<SGNN_REDUCE_MIN>(lanes, a, s);
+        case SGNN_REDUCE_MAX: return short_rows_red<SGNN_REDUCE_MAX>(lanes, a, s);
+    }
+    return fail(SGNN_ERR_CONFIG, "unknown reduce op");
 }
 
 }  // namespace
@@ -171,6 +210,29 @@ sgnn_status run_spmm_ld(const sgnn_csr* a, const float* x, uint64_t ldx, uint32_
                                               std::to_string(vregs) + " unroll=" +
                                               std::to_string(unroll));
     const uint32_t kernel_width = uint32_t((vec ? 4 : 1) * lanes * vregs);
+    // Small short-row matrices (every row <= 2 G nonzeros, every row's group
+    // resident at once): the short-row kernel -- three dependent loads per row
+    // instead of the worker's metadata / row window / (col, val) / gather
+    // chain (cfg1: 14.4 -> 10.2 us, bitwise the same).  Larger ones keep the
+    // worker (equal or faster once rows outnumber the resident groups).
+    DeviceProps dp;
+    SGNN_TRY(device_props(&dp));
+    const uint64_t resident = uint64_t(dp.sm_count) * uint64_t(dp.max_threads_per_sm > 0 ? dp.max_threads_per_sm : 2048);
+    const bool no_short = std::getenv("SGNN_NO_SHORT_ROWS") != nullptr;  // A/B switch (tests)
+    if (!no_short && vec && vregs == 1 && plan->kt == k && kernel_width >= k && plan->n_fix == 0 &&
+        plan->max_deg <= uint32_t(2 * lanes) && uint64_t(a->n_rows) * lanes <= resident) {
+        SpmmArgs args{};
+        args.rp = a->row_ptr;
+        args.ci = a->col_idx;
+        args.val = a->values;
+        args.x = x;
+        args.c = c;
+        args.n_rows = a->n_rows;
+        args.ldx = ldx;
+        args.ldc = ldc;
+        args.width = k;
+        return run_short_rows(lanes, reduce, args, s);
+    }
 
     for (uint32_t k0 = 0; k0 < k; k0 += plan->kt) {
         const uint32_t kp = std::min(plan->kt, k - k0);

@@ -820,6 +820,70 @@ __global__ void __launch_bounds__(kFixupLongThreads) spmm_fixup_long_kernel(cons
     }
 }
 
+// Short-row SpMM (every row <= 2 G nonzeros, no split rows): one G-lane
+// group per row, rows strided over the groups, no plan metadata and no
+// worker schedule -- a row costs three dependent loads (row_ptr, its (col,
+// val) pairs in one G-wide load each, its gathers).  The fold is the worker's
+// (ascending nonzero order, the same Reducer), so results are bitwise the
+// worker kernel's.  Groups narrower than a warp step together (full-mask
+// shuffles); a group with a shorter row idles through the extra trips.
+template <int G, int U, int RED>
+__global__ void __launch_bounds__(128) spmm_short_rows_kernel(const SpmmArgs a) {
+    using F = Frag<G, 1, true>;
+    using R = Reducer<RED>;
+    constexpr unsigned FULL = 0xffffffffu;
+    const int lane = threadIdx.x & 31, gl = lane & (G - 1), gbase = lane & ~(G - 1);
+    const uint32_t ngroups = (gridDim.x * blockDim.x) / G;
+    const uint32_t g0 = (blockIdx.x * blockDim.x + threadIdx.x) / G;
+    const int gl_eff = min(gl, int(a.width / 4) - 1);
+    const char* xlane = reinterpret_cast<const char*>(a.x + 4 * gl_eff);
+    const uint32_t ldxb = uint32_t(a.ldx) * 4u;
+    const uint64_t l2pol = gather_policy();
+    // every group of a warp runs the same number of row trips
+    const uint32_t wfirst = g0 - uint32_t(lane / G);
+    const uint32_t trips = wfirst < a.n_rows ? (a.n_rows - wfirst + ngroups - 1) / ngroups : 0u;
+    for (uint32_t t = 0; t < trips; ++t) {
+        const uint32_t r = g0 + t * ngroups;
+        const bool act = r < a.n_rows;
+        uint64_t j = 0;
+        uint32_t deg = 0;
+        if (act) {
+            j = __ldg(a.rp + r);
+            deg = uint32_t(__ldg(a.rp + r + 1) - j);
+        }
+        const uint32_t c0 = uint32_t(gl) < deg ? ld_stream(a.ci + j + gl) : 0u;  // 0: a safe dummy row
+        const float v0 = uint32_t(gl) < deg ? ld_stream(a.val + j + gl) : 0.0f;
+        const uint32_t c1 = uint32_t(gl + G) < deg ? ld_stream(a.ci + j + G + gl) : 0u;
+        const float v1 = uint32_t(gl + G) < deg ? ld_stream(a.val + j + G + gl) : 0.0f;
+        F acc;
+        acc.zero();
+        bool first = true;
+        for (uint32_t b = 0; __any_sync(FULL, b < deg); b += U) {
+            F xf[U];
+            float av[U];
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+                const uint32_t p = b + uint32_t(u);  // the same position in every lane of the group
+                const int src = gbase + int(p & (G - 1));
+                const uint32_t col = __shfl_sync(FULL, p < uint32_t(G) ? c0 : c1, src);
+                av[u] = __shfl_sync(FULL, p < uint32_t(G) ? v0 : v1, src);
+                xf[u].template gather<false>(reinterpret_cast<const float*>(xlane + uint64_t(col) * ldxb), 1, l2pol);
+            }
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+                if (b + uint32_t(u) < deg) {
+                    R::fold_all(acc.v, av[u], xf[u].v, first);
+                    first = false;
+                }
+            }
+        }
+        if (act) {
+            R::finish_frag(acc.v, deg);
+            acc.store(a.c + uint64_t(r) * a.ldc, gl, a.width);
+        }
+    }
+}
+
 }  // namespace dev
 
 // Host launcher table (spmm_launch.cu).

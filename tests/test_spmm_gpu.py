@@ -312,3 +312,36 @@ def test_mean_epilogue_bitwise_sum_over_degree(cuda, k):
         deg = torch.from_numpy(np.diff(rp.astype(np.int64)).astype(np.float32)).cuda()[:, None]
         want = torch.where(deg > 0, s / torch.clamp(deg, min=1.0), torch.zeros_like(s))
         np.testing.assert_array_equal(m.cpu().numpy().view(np.uint32), want.cpu().numpy().view(np.uint32))
+
+
+@pytest.mark.parametrize("k", [16, 20, 32, 64, 128])
+def test_short_row_kernel_bitwise_worker(cuda, k, monkeypatch):
+    """Small matrices whose rows all fit 2 G nonzeros take the short-row
+    kernel (one group per row, no plan metadata); its results are bitwise the
+    worker kernel's (SGNN_NO_SHORT_ROWS) and the reference's fp32 kernel, for
+    every reduction, empty rows, a partial width (K = 20) and rows of exactly
+    2 G nonzeros."""
+    import torch
+    ops = _ops()
+    rng = np.random.default_rng(k)
+    m, n = 3000, 5000
+    lanes = 4 if k <= 16 else 8 if k <= 32 else 16 if k <= 64 else 32
+    cnt = rng.integers(0, 2 * lanes + 1, m)
+    cnt[rng.random(m) < 0.2] = 0
+    cnt[:5] = 2 * lanes
+    rows = [np.sort(rng.choice(n, size=int(c), replace=False)) for c in cnt]
+    rp = np.zeros(m + 1, np.uint64)
+    rp[1:] = np.cumsum(cnt)
+    ci = np.concatenate(rows).astype(np.uint32)
+    v = rng.uniform(-1, 1, len(ci)).astype(np.float32)
+    x = rng.uniform(-1, 1, (n, k)).astype(np.float32)
+    a = ops.CsrMatrix.from_numpy(rp, ci, v, n)
+    xt = torch.from_numpy(x).cuda()
+    for red, r in REDS.items():
+        got = ops.spmm(a, xt, red).cpu().numpy()
+        monkeypatch.setenv("SGNN_NO_SHORT_ROWS", "1")
+        want = ops.spmm(a, xt, red).cpu().numpy()
+        monkeypatch.delenv("SGNN_NO_SHORT_ROWS")
+        np.testing.assert_array_equal(got.view(np.uint32), want.view(np.uint32), err_msg=red)
+        w32 = port.spmm(rp, ci, v, x, r, np.float32)
+        np.testing.assert_array_equal(got.view(np.uint32), w32.view(np.uint32), err_msg=f"{red} vs fp32 reference")
