@@ -51,6 +51,22 @@ def _dense(t: torch.Tensor, what: str) -> torch.Tensor:
     return t
 
 
+def _on(a: "CsrMatrix", what: str, *ts: torch.Tensor) -> None:
+    """Every dense operand on the sparse operand's device (a kernel would
+    otherwise read another device's pointers)."""
+    dev = a.row_ptr.device
+    for t in ts:
+        if t.device != dev:
+            raise ConfigError(f"{what}: operand on {t.device}, sparse operand on {dev}")
+
+
+def _out(out: torch.Tensor, shape, what: str) -> torch.Tensor:
+    _dense(out, f"{what} out")
+    if tuple(out.shape) != tuple(shape):
+        raise ShapeError(f"{what}: output is {tuple(out.shape)}, expected {tuple(shape)}")
+    return out
+
+
 class CsrMatrix:
     """CsrMatrix<float> on the device (types.hpp:26-79): row_ptr u64 (stored
     as int64), col_idx u32 (stored as int32), values f32."""
@@ -178,9 +194,8 @@ def spmm_into(a: CsrMatrix, b: torch.Tensor, reduce, kind: KernelKind, out: torc
               plan: Plan | None = None) -> torch.Tensor:
     """detail::spmm_into (kernels.hpp:141-149) plus spmm_with's checks (:157-169)."""
     _dense(b, "spmm")
-    _dense(out, "spmm out")
-    if out.shape[0] != a.n_rows or out.shape[1] != b.shape[1]:
-        raise ShapeError(f"spmm: output is {tuple(out.shape)}, expected ({a.n_rows}, {b.shape[1]})")
+    _out(out, (a.n_rows, b.shape[1]), "spmm")
+    _on(a, "spmm", b, out)
     red = _reduce(reduce)
     if a.n_cols != b.shape[0]:  # check_spmm_shapes, kernels.hpp:131-136
         raise ShapeError(f"spmm: sparse operand is {a.n_rows}x{a.n_cols} but dense operand is "
@@ -223,6 +238,8 @@ def spmm_plan(a: CsrMatrix, b: torch.Tensor, reduce="sum", plan: Plan | None = N
     _dense(b, "spmm")
     if out is None:
         out = torch.empty((a.n_rows, b.shape[1]), dtype=torch.float32, device=b.device)
+    _out(out, (a.n_rows, b.shape[1]), "spmm")
+    _on(a, "spmm", b, out)
     check(lib().sgnn_spmm_f32(C.byref(a.c()), b.data_ptr(), b.shape[0], b.shape[1], out.data_ptr(),
                               _reduce(reduce), plan.handle if plan is not None else None, _stream()), "spmm")
     return out
@@ -534,6 +551,7 @@ def sddmm(p: CsrMatrix, x: torch.Tensor, y: torch.Tensor) -> CsrMatrix:
     """sddmm (kernels.hpp:187-210): P's pattern with values p_e * <X_i, Y_j>."""
     _dense(x, "sddmm X")
     _dense(y, "sddmm Y")
+    _on(p, "sddmm", x, y)
     if p.n_rows != x.shape[0] or p.n_cols != y.shape[0] or x.shape[1] != y.shape[1]:
         raise ShapeError(f"sddmm: pattern {p.n_rows}x{p.n_cols} needs X with {p.n_rows} rows and Y with "
                          f"{p.n_cols} rows of equal width; got X {x.shape[0]}x{x.shape[1]}, "
@@ -571,6 +589,8 @@ def fusedmm(p: CsrMatrix, x: torch.Tensor, y: torch.Tensor, edge_op="mul", reduc
                          f"{x.shape[0]}x{x.shape[1]}, Y {y.shape[0]}x{y.shape[1]})")
     if out is None:
         out = torch.empty((p.n_rows, y.shape[1]), dtype=torch.float32, device=x.device)
+    _out(out, (p.n_rows, y.shape[1]), "fusedmm")
+    _on(p, "fusedmm", x, y, out)
     if plan is None and p.n_rows and x.shape[1] and x.shape[1] <= 1024 and (x.shape[1] % 4 == 0 or x.shape[1] <= 256):
         plan = p.plan(x.shape[1], "fused")  # cached split (built once per matrix and K)
     if plan is not None:

@@ -265,3 +265,23 @@ def test_row_partitioned_fusedmm_sddmm_bitwise(cuda, parts):
                                     xt[int(bounds[r]):int(bounds[r + 1])].contiguous(), yt).values.cpu().numpy()
                           for r, b in enumerate(blocks)])
     np.testing.assert_array_equal(got.view(np.uint32), full.view(np.uint32))
+
+
+def test_output_operand_checks(cuda):
+    """Caller-supplied outputs are validated before any launch (shape, dtype,
+    layout): ShapeError / ConfigError, as the reference's shape checks."""
+    import torch
+    ops = _ops()
+    p = ops.CsrMatrix.from_numpy(np.array([0, 1, 2], np.uint64), np.array([0, 1], np.uint32),
+                                 np.ones(2, np.float32), 2)
+    x = torch.ones(2, 4, device="cuda")
+    with pytest.raises(ops.ShapeError):
+        ops.fusedmm(p, x, x, out=torch.empty(3, 4, device="cuda"))
+    with pytest.raises(ops.ConfigError):
+        ops.fusedmm(p, x, x, out=torch.empty(2, 4, device="cuda", dtype=torch.float64))
+    with pytest.raises(ops.ShapeError):
+        ops.spmm(p, x, "sum", out=torch.empty(2, 5, device="cuda"))
+    with pytest.raises(ops.ConfigError):
+        ops.spmm_plan(p, x, "sum", out=torch.empty(4, 2, device="cuda").t())
+    np.testing.assert_array_equal(ops.fusedmm(p, x, x, out=torch.empty(2, 4, device="cuda")).cpu().numpy(),
+                                  ops.fusedmm(p, x, x).cpu().numpy())
