@@ -425,6 +425,24 @@ SpmmLauncher find_fused_launcher_occ(bool vec, int lanes, int vregs, int unroll,
 }
 
 // Prefers the register-capped (5 CTAs/SM) variant when one is compiled.
+// the full-width lockstep FusedMM (dev::fused_lock_kernel), K = 64, Sum / Mean
+template <int OP, int MINB>
+sgnn_status launch_fused_lock(const SpmmArgs& a, cudaStream_t s) {
+    static int per_sm = -1;
+    DeviceProps dp;
+    SGNN_TRY(device_props(&dp));
+    if (per_sm < 0) {
+        int n = 0;
+        SGNN_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, dev::fused_lock_kernel<16, 8, OP, MINB>, 128, 0));
+        per_sm = std::max(n, 1);
+    }
+    const uint64_t blocks = std::min<uint64_t>(ceil_div_u64(uint64_t(a.n_workers) * 16, 128), uint64_t(dp.sm_count) * per_sm);
+    if (blocks == 0) return SGNN_OK;
+    dev::fused_lock_kernel<16, 8, OP, MINB><<<unsigned(blocks), 128, 0, s>>>(a);
+    SGNN_LAUNCH_CHECK();
+    return SGNN_OK;
+}
+
 SpmmLauncher find_fused_launcher(bool vec, int lanes, int vregs, int unroll, int edge, int reduce) {
     SpmmLauncher l = find_fused_launcher_occ(vec, lanes, vregs, unroll, edge, reduce, 5);
     return l ? l : find_fused_launcher_occ(vec, lanes, vregs, unroll, edge, reduce, 1);
@@ -567,7 +585,14 @@ sgnn_status run_fusedmm(const sgnn_csr* p, const float* x, const float* y, uint3
         args.ld_slot = plan->kt;
         args.width = k;
         args.wctr = plan_counter(plan, s);
-        st = launch(args, plan->p.block, 0, s);
+        const bool generic = std::getenv("SGNN_FUSED_GENERIC") != nullptr;  // A/B switch (tests)
+        if (!generic && vec && k == 64 && (reduce == SGNN_REDUCE_SUM || reduce == SGNN_REDUCE_MEAN))
+            // 5 CTAs/SM (96 registers): 1.175 -> 1.086 ms on cfg4; capped at
+            // 6 / 7 it spills (44 / 136 bytes) and runs 1.098 / 1.211 ms
+            st = edge_op == SGNN_EDGE_SIGMOID_MUL ? launch_fused_lock<dev::OP_FUSED_SIGMOID, 5>(args, s)
+                                                  : launch_fused_lock<dev::OP_FUSED_MUL, 5>(args, s);
+        else
+            st = launch(args, plan->p.block, 0, s);
     }
     if (st == SGNN_OK && plan->n_fix) {
         FixupArgs f;

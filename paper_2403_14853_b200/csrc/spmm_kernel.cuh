@@ -820,6 +820,178 @@ __global__ void __launch_bounds__(kFixupLongThreads) spmm_fixup_long_kernel(cons
     }
 }
 
+// Full-width lockstep FusedMM, Sum (and Mean through the divide pass), for
+// K = 4 G: the worker kernel's split, batches, row / segment / slot rules,
+// dot tree and fma fold -- bitwise its results (test) -- with fewer
+// instructions per batch: (col, val) arrive in G-wide windows, a gather
+// address is one mad.wide, the dot is unmasked (every lane's float4 is inside
+// K), and the row / segment settling runs as warp-uniform loops with
+// full-mask shuffles.  At the worker's 5 CTAs/SM: cfg4 1.175 -> 1.086 ms
+// (capping registers lower spills: DESIGN 3.3).
+template <int G, int U, int OP, int MINB>
+__global__ void __launch_bounds__(128, MINB) fused_lock_kernel(const SpmmArgs a) {
+    static_assert(G < 32 && U <= G && is_fused<OP>(), "lockstep groups, one owned dot per lane");
+    using F = Frag<G, 1, true>;
+    using R = Reducer<SGNN_REDUCE_SUM>;
+    constexpr unsigned FULL = 0xffffffffu;
+    constexpr int PER = G / U;
+    constexpr uint32_t SEG = SGNN_SEGMENT;
+    const int lane = threadIdx.x & 31, gl = lane & (G - 1), gbase = lane & ~(G - 1);
+    const char* ylane = reinterpret_cast<const char*>(a.x + 4 * gl);
+    const uint32_t ldb = uint32_t(a.ldx) * 4u;
+    const uint64_t l2pol = gather_policy();
+    WarpSched<32 / G> ws(a.wctr);
+    for (uint32_t w = ws.base + uint32_t(lane / G); __any_sync(FULL, w < a.n_workers);
+         ws.next(), w = ws.base + uint32_t(lane / G)) {
+        const bool wact = w < a.n_workers;
+        const uint32_t wq = wact ? w : a.n_workers - 1;  // idle group: no rows, no nonzeros
+        const uint32_t i0 = __ldg(a.wrow + wq), i1 = wact ? __ldg(a.wrow + wq + 1) : i0;
+        const uint64_t j0 = __ldg(a.wnz + wq);
+        const uint32_t E = wact ? uint32_t(__ldg(a.wnz + wq + 1) - j0) : 0u;
+        uint32_t slot = a.wslot ? __ldg(a.wslot + wq) : 0u;
+        auto window = [&](uint32_t rb_) -> uint32_t {  // lane gl: local end of row rb_ + gl
+            const uint64_t e = __ldg(a.rp + min(rb_ + 1 + uint32_t(gl), a.n_rows));
+            return uint32_t(min(e - j0, uint64_t(E)));
+        };
+        uint32_t r = i0, rb = i0;
+        uint32_t rwin = window(rb);
+        uint32_t rend_l = __shfl_sync(FULL, rwin, gbase);
+        uint32_t rs_l = 0, seg_l = min(SEG, rend_l);
+        bool inside = __ldg(a.rp + i0) >= j0 && r < i1;  // row i0 did not begin in an earlier worker
+        bool have_tot = false, first = true, xstale = true;  // xstale: X_r not loaded yet
+        F acc, xrow;
+        acc.zero();
+        auto store_slot = [&]() {
+            acc.store(a.slots + uint64_t(slot) * a.ld_slot, gl, a.width);
+            ++slot;
+        };
+        auto finish_row = [&]() {  // row r has no more nonzeros in this worker
+            if (inside) {
+                float* crow = a.c + uint64_t(r) * a.ldc;
+                if (have_tot) {
+                    F t;
+                    t.load_own(crow, gl, a.width);
+#pragma unroll
+                    for (int i = 0; i < 4; ++i) acc.v[i] = R::combine(t.v[i], acc.v[i]);
+                }
+                R::finish_frag(acc.v, rend_l - rs_l);
+                acc.store(crow, gl, a.width);
+            } else {
+                store_slot();
+            }
+        };
+        // rows of the groups in `need` advance by one (window reload per group,
+        // then one full-mask shuffle for the new row ends)
+        auto advance = [&](bool need) {
+            if (need) {
+                ++r;
+                rs_l = rend_l;
+                if (r - rb >= uint32_t(G)) {
+                    rb = r;
+                    rwin = window(rb);
+                }
+            }
+            const uint32_t t = __shfl_sync(FULL, rwin, gbase + int(r - rb));
+            if (need) {
+                rend_l = t;
+                inside = r < i1;
+                seg_l = min(rs_l + SEG, rend_l);
+                first = true;
+                have_tot = false;
+                xstale = true;
+                acc.zero();
+            }
+        };
+        uint32_t wb = 0, cw = 0;
+        float vw = 0.0f;
+        auto load_window = [&](uint32_t at) {
+            wb = at;
+            const bool ok = at + uint32_t(gl) < E;
+            cw = ok ? ld_stream(a.ci + j0 + at + gl) : 0u;  // 0: a safe dummy row
+            vw = ok ? ld_stream(a.val + j0 + at + gl) : 0.0f;
+        };
+        if (E) load_window(0);
+        uint32_t base = 0;
+        while (__any_sync(FULL, base < E)) {
+            const bool act = base < E;
+            // settle (the worker's): close finished rows, then a finished segment
+            while (true) {
+                const bool need = act && base >= rend_l;
+                if (!__any_sync(FULL, need)) break;
+                if (need) finish_row();
+                advance(need);
+            }
+            if (act && base >= seg_l) {  // segment boundary inside a row
+                if (inside) {
+                    float* crow = a.c + uint64_t(r) * a.ldc;
+                    if (have_tot) {
+                        F t;
+                        t.load_own(crow, gl, a.width);
+#pragma unroll
+                        for (int i = 0; i < 4; ++i) t.v[i] = R::combine(t.v[i], acc.v[i]);
+                        t.store(crow, gl, a.width);
+                    } else {
+                        acc.store(crow, gl, a.width);
+                    }
+                    have_tot = true;
+                } else {
+                    store_slot();
+                }
+                acc.zero();
+                first = true;
+                seg_l = min(seg_l + SEG, rend_l);
+            }
+            if (act && xstale) {
+                xrow.load(a.xi + uint64_t(r) * a.ldxi, gl, a.width);
+                xstale = false;
+            }
+            int n = 0;
+            if (act) {
+                const uint32_t room = min(rend_l, seg_l) - base;
+                n = room < uint32_t(U) ? int(room) : U;
+            }
+            // an active group's batch lies inside the window (base - wb <= G - U)
+            const int s0 = gbase + int(base - wb);
+            uint32_t colu[U];
+#pragma unroll
+            for (int u = 0; u < U; ++u) colu[u] = __shfl_sync(FULL, cw, s0 + u);
+            const float pv_own = __shfl_sync(FULL, vw, s0 + gl / PER);
+            F yf[U];
+            if (act) {
+#pragma unroll
+                for (int u = 0; u < U; ++u) {
+                    const char* p;
+                    asm("mad.wide.u32 %0, %1, %2, %3;" : "=l"(p) : "r"(colu[u]), "r"(ldb), "l"(ylane));
+                    const float4 t = ld_gather(reinterpret_cast<const float4*>(p), l2pol);
+                    yf[u].v[0] = t.x; yf[u].v[1] = t.y; yf[u].v[2] = t.z; yf[u].v[3] = t.w;
+                }
+            }
+            const uint32_t nb = base + uint32_t(n);
+            if (act && nb < E && nb + uint32_t(U) > wb + uint32_t(G)) load_window(nb);
+            const float s_own = edge_value<OP>(pv_own, batch_dots(xrow, yf, FULL, gl));
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+                const float sv = __shfl_sync(FULL, s_own, gbase + u * PER);
+                if (u < n) {
+                    R::fold_fused_all(acc.v, sv, yf[u].v, first);
+                    first = false;
+                }
+            }
+            base = nb;
+        }
+        // all nonzeros consumed: close rows ending inside this worker (the
+        // current one and empty rows after it), then the head of row i1
+        while (true) {
+            const bool need = r < i1;
+            if (!__any_sync(FULL, need)) break;
+            if (need) finish_row();
+            advance(need);
+        }
+        if (r < a.n_rows && E > rs_l) store_slot();  // head of a split row
+    }
+    ws.finish();
+}
+
 // Short-row SpMM (every row <= 2 G nonzeros, no split rows): one G-lane
 // group per row, rows strided over the groups, no plan metadata and no
 // worker schedule -- a row costs three dependent loads (row_ptr, its (col,

@@ -285,3 +285,33 @@ def test_output_operand_checks(cuda):
         ops.spmm_plan(p, x, "sum", out=torch.empty(4, 2, device="cuda").t())
     np.testing.assert_array_equal(ops.fusedmm(p, x, x, out=torch.empty(2, 4, device="cuda")).cpu().numpy(),
                                   ops.fusedmm(p, x, x).cpu().numpy())
+
+
+@pytest.mark.parametrize("path_items", [0, 64, 512])
+def test_fused_lockstep_kernel_bitwise_generic(cuda, path_items, monkeypatch):
+    """The full-width lockstep FusedMM (fused_lock_kernel, K = 64, sum and
+    mean, both edge ops) gives bit for bit the worker kernel's results
+    (SGNN_FUSED_GENERIC): hub rows split over workers (segment slots +
+    fixup), rows of several segments inside one worker (running totals in
+    the output row), runs of empty rows, single-nonzero rows."""
+    from paper_2403_14853_b200 import graphs
+    ops = _ops()
+    rng = np.random.default_rng(path_items + 1)
+    n, k = 1 << 13, 64
+    rp, ci = graphs.rmat(13, n * 12, seed=8)
+    deg = np.diff(rp.astype(np.int64))
+    assert (deg == 0).sum() > 100 and (deg == 1).any() and deg.max() > 1000
+    v = rng.uniform(0, 1, len(ci)).astype(np.float32)
+    x = rng.normal(0, 0.1, (n, k)).astype(np.float32)
+    y = rng.normal(0, 0.1, (n, k)).astype(np.float32)
+    p = ops.CsrMatrix.from_numpy(rp, ci, v, n)
+    xt, yt = _t(x), _t(y)
+    plan = ops.Plan(p, k, **{**_fused_layout_kw(k), "path_items": path_items}) if path_items else None
+    for edge in ("sigmoid_mul", "mul"):
+        for red in ("sum", "mean"):
+            got = ops.fusedmm(p, xt, yt, edge, red, plan=plan).cpu().numpy()
+            monkeypatch.setenv("SGNN_FUSED_GENERIC", "1")
+            want = ops.fusedmm(p, xt, yt, edge, red, plan=plan).cpu().numpy()
+            monkeypatch.delenv("SGNN_FUSED_GENERIC")
+            np.testing.assert_array_equal(got.view(np.uint32), want.view(np.uint32), err_msg=f"{edge} {red}")
+    check_fused(rp, ci, v, n, x, y, "sigmoid_mul", "sum")
