@@ -609,7 +609,18 @@ __global__ void __launch_bounds__(256) sage_head_kernel(
     const uint32_t r0 = blockIdx.x * rpb, r1 = min(n, r0 + rpb);
     double lsum = 0.0;
     uint32_t oks = 0;
-    for (uint32_t i0 = r0 + wid * R; i0 < r1; i0 += 8 * R) {
+    // the per-row log(den) is batched: a group's lane (step % CP) keeps the
+    // row's (mx, den, label logit), and every CP steps all lanes take their
+    // log at once (one log sequence per CP rows instead of one per row)
+    uint32_t step = 0;
+    double p_mx = 0.0, p_den = 1.0;
+    float p_vlab = 0.0f;
+    bool p_has = false;
+    auto flush = [&]() {
+        if (p_has) lsum += (p_mx + log(p_den)) - double(p_vlab);
+        p_has = false;
+    };
+    for (uint32_t i0 = r0 + wid * R; i0 < r1; i0 += 8 * R, ++step) {
         float v;
         {
             float4 x[2][R];
@@ -684,11 +695,15 @@ __global__ void __launch_bounds__(256) sage_head_kernel(
             const uint32_t lab = labels[i];
             const float vlab = __shfl_sync(gmask, v, int(lab), CP);
             if (cl) g = float((e / den - (gl == lab ? 1.0 : 0.0)) * inv_n);
-            if (gl == 0) {
-                lsum += (mx + log(den)) - double(vlab);
-                oks += best == lab ? 1u : 0u;
+            if (gl == step % CP) {
+                p_mx = mx;
+                p_den = den;
+                p_vlab = vlab;
+                p_has = true;
             }
+            if (gl == 0) oks += best == lab ? 1u : 0u;
         }
+        if (step % CP == CP - 1) flush();
         if (row_ok && cl) grad[uint64_t(i) * c + gl] = g;
         // ds2[i, k] = sum_j grad[i, j] W2[k, j] (sage_grad_wt_kernel's chain)
         float gj[CP];
@@ -723,14 +738,15 @@ __global__ void __launch_bounds__(256) sage_head_kernel(
             }
         }
     }
-    // per warp: the groups' sums in group order (lane gl == 0 of each group)
-    double wl = 0.0;
+    flush();
+    // per warp: the lanes' loss partials by a fixed butterfly, the groups'
+    // correct counts (lane gl == 0 of each group)
+    double wl = lsum;
+#pragma unroll
+    for (int o = 16; o >= 1; o >>= 1) wl += __shfl_xor_sync(FULL, wl, o);
     uint32_t wk = 0;
 #pragma unroll
-    for (int q = 0; q < R; ++q) {
-        wl += __shfl_sync(FULL, lsum, q * CP);
-        wk += __shfl_sync(FULL, oks, q * CP);
-    }
+    for (int q = 0; q < R; ++q) wk += __shfl_sync(FULL, oks, q * CP);
     if (lane == 0) {
         s_loss[wid] = wl;
         s_ok[wid] = wk;

@@ -54,7 +54,10 @@ def _dense(t: torch.Tensor, what: str) -> torch.Tensor:
 def _on(a: "CsrMatrix", what: str, *ts: torch.Tensor) -> None:
     """Every dense operand on the sparse operand's device (a kernel would
     otherwise read another device's pointers)."""
-    dev = a.row_ptr.device
+    rp = getattr(a, "row_ptr", None)  # (a TrainingCache view holds raw device pointers only)
+    if rp is None:
+        return
+    dev = rp.device
     for t in ts:
         if t.device != dev:
             raise ConfigError(f"{what}: operand on {t.device}, sparse operand on {dev}")
