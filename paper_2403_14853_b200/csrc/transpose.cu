@@ -242,8 +242,10 @@ __device__ __forceinline__ uint32_t block_exclusive_scan(uint32_t v, uint32_t* s
 // (empty rows included).
 constexpr int kDownSmemFixed = 3 * kThreads * kItems * 4;  // staged keys, rows, vals
 
+// 3 CTAs/SM up to 10-bit digits; 11-bit digits need 96 KB of shared memory,
+// so 2 fit and the register cap of 3 would only force spills
 template <bool FIRST, bool VALS, int DB>
-__global__ void __launch_bounds__(kThreads, 3) radix_downsweep_kernel(
+__global__ void __launch_bounds__(kThreads, DB >= 11 ? 2 : 3) radix_downsweep_kernel(
     const uint32_t* __restrict__ keys_in, const uint32_t* __restrict__ rows_in,
     const float* __restrict__ vals_in, uint32_t* __restrict__ keys_out,
     uint32_t* __restrict__ rows_out, float* __restrict__ vals_out, uint64_t n, int shift,

@@ -14,7 +14,7 @@ from paper_2403_14853_b200 import graphs, ops  # noqa: E402
 
 def main():
     reps = int(sys.argv[1]) if len(sys.argv) > 1 else 10
-    w = graphs.cfg2(1)
+    w = graphs.cfg5(1) if len(sys.argv) > 2 and sys.argv[2] == "cfg5" else graphs.cfg2(1)
     a = ops.CsrMatrix.from_numpy(w.row_ptr, w.col_idx, w.values, w.n_cols)
     t = ops.transpose(a)  # warm the workspace pool
     times = []
