@@ -3,7 +3,7 @@
 // ascending original row within each column, t_row_ptr = the column starts.
 //
 // The stable placement is an LSD radix sort of the nonzeros keyed by column
-// (2 passes of <= 11-bit digits for up to 2^22 columns), carrying (row, value)
+// (passes of <= 9-bit digits: 2 up to 2^18 columns, 3 up to 2^27), carrying (row, value)
 // as payload.  Each tile of 4096 nonzeros is ranked warp by warp in index
 // order (digit peers from one ballot per digit bit, the warp's running digit
 // counts advanced by one shared-memory atomic per peer group), staged in
@@ -19,6 +19,7 @@
 // Also: row_degrees (sparse.hpp:105-109), is_symmetric (sparse.hpp:179-192)
 // and the mean-operand value scaling (gnn.hpp:158-159).
 #include <algorithm>
+#include <cstdlib>
 
 #include "ops.cuh"
 
@@ -30,7 +31,11 @@ constexpr int kThreads = 256;
 constexpr int kWarps = kThreads / 32;
 constexpr int kItems = 16;                          // per thread per tile
 constexpr uint64_t kTile = uint64_t(kThreads) * kItems;  // 4096 nonzeros
-constexpr int kMaxDigitBits = 11;  // <= 2048 bins (u16 warp counters, <= 8 bins per thread)
+// <= 512 bins: 22-bit columns (cfg5) as 3 passes of 8 bits run 5.7 ms
+// against 9.0 ms as 2 passes of 11 (2048-bin bookkeeping, 2 CTAs/SM), 20-bit
+// (cfg4) 0.95 vs 1.02 ms as 3 x 7 against 2 x 10; 18-bit cfg2 keeps 2 x 9
+// (1.22 ms; 3 x 6: 1.30)
+constexpr int kMaxDigitBits = 9;
 constexpr unsigned kFull = 0xffffffffu;
 
 constexpr int kUpTiles = kWarps;  // tiles per upsweep CTA (one per warp): a 32-byte sector per digit
@@ -242,10 +247,8 @@ __device__ __forceinline__ uint32_t block_exclusive_scan(uint32_t v, uint32_t* s
 // (empty rows included).
 constexpr int kDownSmemFixed = 3 * kThreads * kItems * 4;  // staged keys, rows, vals
 
-// 3 CTAs/SM up to 10-bit digits; 11-bit digits need 96 KB of shared memory,
-// so 2 fit and the register cap of 3 would only force spills
 template <bool FIRST, bool VALS, int DB>
-__global__ void __launch_bounds__(kThreads, DB >= 11 ? 2 : 3) radix_downsweep_kernel(
+__global__ void __launch_bounds__(kThreads, 3) radix_downsweep_kernel(
     const uint32_t* __restrict__ keys_in, const uint32_t* __restrict__ rows_in,
     const float* __restrict__ vals_in, uint32_t* __restrict__ keys_out,
     uint32_t* __restrict__ rows_out, float* __restrict__ vals_out, uint64_t n, int shift,
@@ -460,8 +463,7 @@ sgnn_status launch_down(bool vals, const uint32_t* ki, const uint32_t* ri, const
     case D: return launch_down_db<FIRST, D>(vals, ki, ri, vi, ko, ro, vo, n, shift, tiles, tstride, hs, rp, m, tr0, s);
     switch (dbits) {
         SGNN_DOWN_CASE(1) SGNN_DOWN_CASE(2) SGNN_DOWN_CASE(3) SGNN_DOWN_CASE(4) SGNN_DOWN_CASE(5)
-        SGNN_DOWN_CASE(6) SGNN_DOWN_CASE(7) SGNN_DOWN_CASE(8) SGNN_DOWN_CASE(9) SGNN_DOWN_CASE(10)
-        SGNN_DOWN_CASE(11)
+        SGNN_DOWN_CASE(6) SGNN_DOWN_CASE(7) SGNN_DOWN_CASE(8) SGNN_DOWN_CASE(9)
     }
 #undef SGNN_DOWN_CASE
     return fail(SGNN_ERR_INTERNAL, "transpose: digit width out of range");

@@ -14,7 +14,8 @@ from paper_2403_14853_b200 import graphs, ops  # noqa: E402
 
 def main():
     reps = int(sys.argv[1]) if len(sys.argv) > 1 else 10
-    w = graphs.cfg5(1) if len(sys.argv) > 2 and sys.argv[2] == "cfg5" else graphs.cfg2(1)
+    which = sys.argv[2] if len(sys.argv) > 2 else "cfg2"
+    w = {"cfg2": graphs.cfg2, "cfg4": graphs.cfg4, "cfg5": graphs.cfg5}[which](1)
     a = ops.CsrMatrix.from_numpy(w.row_ptr, w.col_idx, w.values, w.n_cols)
     t = ops.transpose(a)  # warm the workspace pool
     times = []

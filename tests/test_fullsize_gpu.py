@@ -375,8 +375,8 @@ def test_cfg2_min_max_all_rows_and_backward_short_rows_bitwise(cuda):
 
 
 def test_cfg5_transpose_of_symmetric_is_identity(cuda):
-    """cfg5's symmetric 202M-nonzero graph (2^22 columns: two 11-bit radix
-    passes, 2048 bins, 49k tiles): the device transpose returns A itself, bit
+    """cfg5's symmetric 202M-nonzero graph (2^22 columns: three 8-bit radix
+    passes, 49k tiles): the device transpose returns A itself, bit
     for bit (sparse.hpp:72-89 on a symmetric matrix), and the symmetry probe
     agrees."""
     import torch

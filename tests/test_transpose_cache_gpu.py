@@ -202,7 +202,8 @@ def test_is_symmetric_upper_lower_counting(cuda):
 
 @pytest.mark.parametrize("shape,hub,empty", [((3000, (1 << 23) + 3), 0, 0.1),   # 24-bit columns: 3 passes of 8 bits
                                              ((20000, 1 << 18), 50000, 0.6),    # hub row over ~12 tiles, long empty runs
-                                             ((9000, 2047), 0, 0.0)])           # 11 bits: one pass, 2048 bins
+                                             ((9000, 2047), 0, 0.0),            # 11 bits: two 6-bit passes
+                                             ((9000, 500), 0, 0.0)])            # 9 bits: one pass, 512 bins
 def test_transpose_pass_counts_hubs_and_no_values(cuda, shape, hub, empty):
     """The radix plan's pass counts / digit widths (1 and 3 passes), a hub row
     spanning many 4096-nonzero tiles next to runs of empty rows longer than a
