@@ -433,12 +433,12 @@ sgnn_status launch_fused_lock(const SpmmArgs& a, cudaStream_t s) {
     SGNN_TRY(device_props(&dp));
     if (per_sm < 0) {
         int n = 0;
-        SGNN_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, dev::fused_lock_kernel<16, 8, OP, MINB>, 128, 0));
+        SGNN_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, dev::lock_worker_kernel<16, 8, OP, SGNN_REDUCE_SUM, MINB>, 128, 0));
         per_sm = std::max(n, 1);
     }
     const uint64_t blocks = std::min<uint64_t>(ceil_div_u64(uint64_t(a.n_workers) * 16, 128), uint64_t(dp.sm_count) * per_sm);
     if (blocks == 0) return SGNN_OK;
-    dev::fused_lock_kernel<16, 8, OP, MINB><<<unsigned(blocks), 128, 0, s>>>(a);
+    dev::lock_worker_kernel<16, 8, OP, SGNN_REDUCE_SUM, MINB><<<unsigned(blocks), 128, 0, s>>>(a);
     SGNN_LAUNCH_CHECK();
     return SGNN_OK;
 }

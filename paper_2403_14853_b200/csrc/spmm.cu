@@ -42,6 +42,42 @@ __global__ void __launch_bounds__(256) mean_divide_kernel(const uint64_t* __rest
     }
 }
 
+// The lockstep worker (dev::lock_worker_kernel) for 8- and 16-lane groups
+template <int G, int RED>
+sgnn_status launch_spmm_lock(const SpmmArgs& a, uint32_t block, cudaStream_t s) {
+    constexpr int MINB = 5;
+    static int per_sm = -1;
+    DeviceProps dp;
+    SGNN_TRY(device_props(&dp));
+    if (per_sm < 0) {
+        int n = 0;
+        SGNN_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(
+            &n, dev::lock_worker_kernel<G, 8, dev::OP_SPMM, RED, MINB>, 128, 0));
+        per_sm = std::max(n, 1);
+    }
+    (void)block;
+    const uint64_t blocks = std::min<uint64_t>(ceil_div_u64(uint64_t(a.n_workers) * G, 128), uint64_t(dp.sm_count) * per_sm);
+    if (blocks == 0) return SGNN_OK;
+    dev::lock_worker_kernel<G, 8, dev::OP_SPMM, RED, MINB><<<unsigned(blocks), 128, 0, s>>>(a);
+    SGNN_LAUNCH_CHECK();
+    return SGNN_OK;
+}
+
+template <int RED>
+sgnn_status spmm_lock_red(int lanes, const SpmmArgs& a, uint32_t block, cudaStream_t s) {
+    return lanes == 8 ? launch_spmm_lock<8, RED>(a, block, s) : launch_spmm_lock<16, RED>(a, block, s);
+}
+
+sgnn_status run_spmm_lock(int lanes, int reduce, const SpmmArgs& a, uint32_t block, cudaStream_t s) {
+    switch (reduce) {
+        case SGNN_REDUCE_SUM: return spmm_lock_red<SGNN_REDUCE_SUM>(lanes, a, block, s);
+        case SGNN_REDUCE_MEAN: return spmm_lock_red<SGNN_REDUCE_MEAN>(lanes, a, block, s);
+        case SGNN_REDUCE_MIN: return spmm_lock_red<SGNN_REDUCE_MIN>(lanes, a, block, s);
+        case SGNN_REDUCE_MAX: return spmm_lock_red<SGNN_REDUCE_MAX>(lanes, a, block, s);
+    }
+    return fail(SGNN_ERR_CONFIG, "unknown reduce op");
+}
+
 template <int G, int RED>
 sgnn_status launch_short_rows(const SpmmArgs& a, cudaStream_t s) {
     static int per_sm = -1;
@@ -254,7 +290,12 @@ sgnn_status run_spmm_ld(const sgnn_csr* a, const float* x, uint64_t ldx, uint32_
             args.ldc = ldc;
             args.ld_slot = plan->kt;
             args.width = std::min(kernel_width, kp - sk);
-            SGNN_TRY(launch(args, plan->p.block, 0, s));
+            // 8- / 16-lane groups at one float4 per lane: the lockstep worker
+            // (same results; fewer instructions per batch)
+            const bool lock = vec && vregs == 1 && unroll == 8 && (lanes == 8 || lanes == 16) &&
+                              !std::getenv("SGNN_LOCK_GENERIC");  // A/B switch (tests)
+            if (lock) SGNN_TRY(run_spmm_lock(lanes, kred, args, plan->p.block, s));
+            else SGNN_TRY(launch(args, plan->p.block, 0, s));
         }
         if (plan->n_fix) {
             FixupArgs f;

@@ -820,24 +820,27 @@ __global__ void __launch_bounds__(kFixupLongThreads) spmm_fixup_long_kernel(cons
     }
 }
 
-// Full-width lockstep FusedMM, Sum (and Mean through the divide pass), for
-// K = 4 G: the worker kernel's split, batches, row / segment / slot rules,
+// Lockstep worker for one float4 per lane (K <= 4 G, G < 32): FusedMM
+// (Sum; Mean through the divide pass) and SpMM (every reduction): the
+// worker kernel's split, batches, row / segment / slot rules,
 // dot tree and fma fold -- bitwise its results (test) -- with fewer
 // instructions per batch: (col, val) arrive in G-wide windows, a gather
 // address is one mad.wide, the dot is unmasked (every lane's float4 is inside
 // K), and the row / segment settling runs as warp-uniform loops with
 // full-mask shuffles.  At the worker's 5 CTAs/SM: cfg4 1.175 -> 1.086 ms
 // (capping registers lower spills: DESIGN 3.3).
-template <int G, int U, int OP, int MINB>
-__global__ void __launch_bounds__(128, MINB) fused_lock_kernel(const SpmmArgs a) {
-    static_assert(G < 32 && U <= G && is_fused<OP>(), "lockstep groups, one owned dot per lane");
+template <int G, int U, int OP, int RED, int MINB>
+__global__ void __launch_bounds__(128, MINB) lock_worker_kernel(const SpmmArgs a) {
+    static_assert(G < 32 && U <= G && (OP == OP_SPMM || is_fused<OP>()), "lockstep groups");
+    static_assert(!is_fused<OP>() || RED == SGNN_REDUCE_SUM, "FusedMM: sum kernels (mean: divide pass)");
     using F = Frag<G, 1, true>;
-    using R = Reducer<SGNN_REDUCE_SUM>;
+    using R = Reducer<RED>;
     constexpr unsigned FULL = 0xffffffffu;
     constexpr int PER = G / U;
     constexpr uint32_t SEG = SGNN_SEGMENT;
     const int lane = threadIdx.x & 31, gl = lane & (G - 1), gbase = lane & ~(G - 1);
-    const char* ylane = reinterpret_cast<const char*>(a.x + 4 * gl);
+    // lanes past the width alias the row's last valid float4 (always in bounds)
+    const char* ylane = reinterpret_cast<const char*>(a.x + 4 * min(gl, int(a.width / 4) - 1));
     const uint32_t ldb = uint32_t(a.ldx) * 4u;
     const uint64_t l2pol = gather_policy();
     WarpSched<32 / G> ws(a.wctr);
@@ -941,9 +944,11 @@ __global__ void __launch_bounds__(128, MINB) fused_lock_kernel(const SpmmArgs a)
                 first = true;
                 seg_l = min(seg_l + SEG, rend_l);
             }
-            if (act && xstale) {
-                xrow.load(a.xi + uint64_t(r) * a.ldxi, gl, a.width);
-                xstale = false;
+            if constexpr (is_fused<OP>()) {
+                if (act && xstale) {
+                    xrow.load(a.xi + uint64_t(r) * a.ldxi, gl, a.width);
+                    xstale = false;
+                }
             }
             int n = 0;
             if (act) {
@@ -955,7 +960,13 @@ __global__ void __launch_bounds__(128, MINB) fused_lock_kernel(const SpmmArgs a)
             uint32_t colu[U];
 #pragma unroll
             for (int u = 0; u < U; ++u) colu[u] = __shfl_sync(FULL, cw, s0 + u);
-            const float pv_own = __shfl_sync(FULL, vw, s0 + gl / PER);
+            float pv_own = 0.0f, av[U];
+            if constexpr (is_fused<OP>()) {
+                pv_own = __shfl_sync(FULL, vw, s0 + gl / PER);
+            } else {
+#pragma unroll
+                for (int u = 0; u < U; ++u) av[u] = __shfl_sync(FULL, vw, s0 + u);
+            }
             F yf[U];
             if (act) {
 #pragma unroll
@@ -968,13 +979,23 @@ __global__ void __launch_bounds__(128, MINB) fused_lock_kernel(const SpmmArgs a)
             }
             const uint32_t nb = base + uint32_t(n);
             if (act && nb < E && nb + uint32_t(U) > wb + uint32_t(G)) load_window(nb);
-            const float s_own = edge_value<OP>(pv_own, batch_dots(xrow, yf, FULL, gl));
+            if constexpr (is_fused<OP>()) {
+                const float s_own = edge_value<OP>(pv_own, batch_dots(xrow, yf, FULL, gl));
 #pragma unroll
-            for (int u = 0; u < U; ++u) {
-                const float sv = __shfl_sync(FULL, s_own, gbase + u * PER);
-                if (u < n) {
-                    R::fold_fused_all(acc.v, sv, yf[u].v, first);
-                    first = false;
+                for (int u = 0; u < U; ++u) {
+                    const float sv = __shfl_sync(FULL, s_own, gbase + u * PER);
+                    if (u < n) {
+                        R::fold_fused_all(acc.v, sv, yf[u].v, first);
+                        first = false;
+                    }
+                }
+            } else {
+#pragma unroll
+                for (int u = 0; u < U; ++u) {
+                    if (u < n) {
+                        R::fold_all(acc.v, av[u], yf[u].v, first);
+                        first = false;
+                    }
                 }
             }
             base = nb;

@@ -345,3 +345,37 @@ def test_short_row_kernel_bitwise_worker(cuda, k, monkeypatch):
         np.testing.assert_array_equal(got.view(np.uint32), want.view(np.uint32), err_msg=red)
         w32 = port.spmm(rp, ci, v, x, r, np.float32)
         np.testing.assert_array_equal(got.view(np.uint32), w32.view(np.uint32), err_msg=f"{red} vs fp32 reference")
+
+
+@pytest.mark.parametrize("k", [20, 32, 64])
+@pytest.mark.parametrize("path_items", [0, 64])
+def test_lockstep_worker_bitwise_generic(cuda, k, path_items, monkeypatch):
+    """8- / 16-lane groups at one float4 per lane run the lockstep worker
+    (lock_worker_kernel); it gives bit for bit the generic worker's results
+    (SGNN_LOCK_GENERIC) for every reduction: hub rows split over workers
+    (slots + fixup), multi-segment rows inside a worker, empty-row runs, a
+    partial width (K = 20), and the reference's fp32 kernel on short rows."""
+    import torch
+
+    from paper_2403_14853_b200 import graphs
+    ops = _ops()
+    rng = np.random.default_rng(k + path_items)
+    n = 1 << 13
+    rp, ci = graphs.rmat(13, n * 12, seed=9)
+    deg = np.diff(rp.astype(np.int64))
+    assert (deg == 0).sum() > 100 and deg.max() > 1000
+    v = rng.uniform(-1, 1, len(ci)).astype(np.float32)
+    x = rng.uniform(-1, 1, (n, k)).astype(np.float32)
+    a = ops.CsrMatrix.from_numpy(rp, ci, v, n)
+    xt = torch.from_numpy(x).cuda()
+    plan = ops.Plan(a, k, path_items=path_items) if path_items else None
+    for red, r in REDS.items():
+        got = (ops.spmm_plan(a, xt, red, plan) if plan else ops.spmm(a, xt, red)).cpu().numpy()
+        monkeypatch.setenv("SGNN_LOCK_GENERIC", "1")
+        want = (ops.spmm_plan(a, xt, red, plan) if plan else ops.spmm(a, xt, red)).cpu().numpy()
+        monkeypatch.delenv("SGNN_LOCK_GENERIC")
+        np.testing.assert_array_equal(got.view(np.uint32), want.view(np.uint32), err_msg=red)
+        short = deg <= 256
+        w32 = port.spmm(rp, ci, v, x, r, np.float32)
+        np.testing.assert_array_equal(got[short].view(np.uint32), w32[short].view(np.uint32),
+                                      err_msg=f"{red} vs fp32 reference")
