@@ -21,11 +21,34 @@ import torch
 from . import gnn, partition
 
 
-def mean_operand_values(row_ptr, col_idx, values):
-    """Values of TrainingCache::mean_operand for a symmetric graph
-    (gnn.hpp:152-159): v / deg[col], IEEE fp32 divide."""
-    deg = np.diff(np.asarray(row_ptr, np.uint64).astype(np.int64)).astype(np.float32)
+def mean_operand_values(row_ptr, col_idx, values, degrees=None):
+    """Values of TrainingCache::mean_operand (gnn.hpp:152-159): v / deg[col],
+    IEEE fp32 divide.  `degrees` are a_hat's row degrees (default: those of
+    row_ptr, the symmetric short-circuit where the operand is a_hat itself)."""
+    deg = np.diff(np.asarray(row_ptr, np.uint64).astype(np.int64)) if degrees is None else np.asarray(degrees)
+    deg = deg.astype(np.float32)
     return (np.asarray(values, np.float32) / deg[np.asarray(col_idx, np.int64)]).astype(np.float32)
+
+
+def transpose_host(row_ptr, col_idx, values, n_cols):
+    """transpose (sparse.hpp:72-89) on the host: column histogram, prefix sum,
+    placement in ascending original row (a stable sort by column)."""
+    rp = np.asarray(row_ptr, np.uint64).astype(np.int64)
+    ci = np.asarray(col_idx, np.int64)
+    rows = np.repeat(np.arange(len(rp) - 1, dtype=np.int64), np.diff(rp))
+    order = np.argsort(ci, kind="stable")
+    t_rp = np.zeros(n_cols + 1, np.uint64)
+    t_rp[1:] = np.cumsum(np.bincount(ci, minlength=n_cols)).astype(np.uint64)
+    return t_rp, rows[order].astype(np.uint32), np.asarray(values, np.float32)[order]
+
+
+def is_symmetric_host(row_ptr, col_idx, values):
+    """is_symmetric (sparse.hpp:179-192): A equals its transpose, structure
+    and values."""
+    n = len(row_ptr) - 1
+    t_rp, t_ci, t_v = transpose_host(row_ptr, col_idx, values, n)
+    return (np.array_equal(t_rp, np.asarray(row_ptr, np.uint64)) and np.array_equal(t_ci, np.asarray(col_idx, np.uint32))
+            and np.array_equal(t_v, np.asarray(values, np.float32)))
 
 
 @dataclass
@@ -40,10 +63,13 @@ class DistSage:
     """One rank of the partitioned SAGE (sum or mean) trainer."""
 
     def __init__(self, row_ptr, col_idx, values, n_parts, rank, k_in, hidden, classes, reduce="mean",
-                 device="cuda", exchange=None, allreduce=None, compute=None, symmetric=True, row_weight=1):
-        if not symmetric:
-            raise NotImplementedError("the partitioned backward uses the symmetric short-circuit "
-                                      "(gnn.hpp:152-153); cfg5 is symmetric")
+                 device="cuda", exchange=None, allreduce=None, compute=None, symmetric=None, row_weight=1):
+        """`symmetric`: None probes the graph like build_cache (gnn.hpp:194);
+        a non-symmetric A runs its backward over rows of A^T (gnn.hpp:127-144,
+        :149-160), partitioned at the same row bounds as A."""
+        if symmetric is None:
+            symmetric = is_symmetric_host(row_ptr, col_idx, values)
+        self.symmetric = bool(symmetric)
         self.reduce = reduce
         self.exchange = exchange or partition.NcclExchange()
         # unpadded all-gather-v layout (global column ids); the peer path
@@ -54,11 +80,18 @@ class DistSage:
         self.r0, self.r1 = self.part.rows(rank)
         self.device = device
         self.allreduce = allreduce or _nccl_allreduce
-        bwd_vals = mean_operand_values(row_ptr, col_idx, values) if reduce == "mean" else values
+        if self.symmetric:  # the operand is a_hat itself (mean: columns scaled in place)
+            b_rp, b_ci = row_ptr, col_idx
+            bwd_vals = mean_operand_values(row_ptr, col_idx, values) if reduce == "mean" else values
+        else:  # rows of A^T; mean: scaled by the degree of the original row, now the column
+            b_rp, b_ci, bwd_vals = transpose_host(row_ptr, col_idx, values, len(row_ptr) - 1)
+            if reduce == "mean":
+                bwd_vals = mean_operand_values(b_rp, b_ci, bwd_vals, degrees=np.diff(
+                    np.asarray(row_ptr, np.uint64).astype(np.int64)))
         self.fwd = partition.PartitionedSpmm(row_ptr, col_idx, values, self.part, rank, k_in, device, compute)
         self.fwd2 = self.fwd if hidden == k_in else partition.PartitionedSpmm(
             row_ptr, col_idx, values, self.part, rank, hidden, device, compute)
-        self.bwd = partition.PartitionedSpmm(row_ptr, col_idx, bwd_vals, self.part, rank, hidden, device, compute)
+        self.bwd = partition.PartitionedSpmm(b_rp, b_ci, bwd_vals, self.part, rank, hidden, device, compute)
         self.hidden, self.classes = hidden, classes
         self.use_glue = True  # the library's SAGE glue passes on CUDA tensors (False: torch ops)
 

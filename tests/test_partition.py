@@ -189,6 +189,74 @@ def test_two_rank_sage_mean_step_matches_reference():
     np.testing.assert_allclose(losses, want, rtol=2e-3, atol=1e-5)
 
 
+def _nonsym_case():
+    rng = np.random.default_rng(11)
+    n, f = 300, 16
+    rp, ci, v = rand_csr(rng, n, n, 0.03, hub_rows=(2,), value="positive")
+    x = rng.normal(0, 1, (n, f)).astype(np.float32)
+    lab = rng.integers(0, 4, n).astype(np.uint32)
+    mask = (rng.random(n) < 0.7).astype(np.uint8)
+    return rp, ci, v, x, lab, mask
+
+
+def _nonsym_worker(rank, world, port_, q, kind, w0):
+    import torch
+    import torch.distributed as dist
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port_))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_2403_14853_b200 import partition, sage_dist
+        rp, ci, v, x, lab, mask = _nonsym_case()
+        n, f = x.shape
+        hidden, classes = 32, 4
+        ds = sage_dist.DistSage(rp, ci, v, world, rank, f, hidden, classes, kind.split("-")[1], device="cpu",
+                                exchange=partition.NcclExchange(), compute=_oracle_compute)
+        assert not ds.symmetric  # probed like build_cache (gnn.hpp:194)
+        o = [0]
+
+        def take(r, c):
+            t = torch.from_numpy(w0[o[0]:o[0] + r * c].reshape(r, c).copy())
+            o[0] += r * c
+            return t
+        params = sage_dist.SageParams(take(f, hidden), take(hidden, classes), take(f, hidden), take(hidden, classes))
+        r0, r1 = ds.r0, ds.r1
+        losses = [ds.step(params, torch.from_numpy(x[r0:r1].copy()), torch.from_numpy(lab[r0:r1].astype(np.int64)),
+                          torch.from_numpy(mask[r0:r1].copy()), 0.05, int(mask.sum())) for _ in range(8)]
+        if rank == 0:
+            q.put(losses)
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("kind", ["sage-mean", "sage-sum"])
+def test_two_rank_non_symmetric_backward_matches_reference(kind):
+    """A non-symmetric A (gloo, 2 ranks, oracle SpMM): the backward runs over
+    rows of A^T (mean: scaled by the original row's degree), gnn.hpp:127-160;
+    losses match the reference's own train() on the same graph (oracle/_ref)."""
+    import torch.multiprocessing as mp
+
+    from oracle import ref
+    from paper_2403_14853_b200 import sage_dist
+    rp, ci, v, x, lab, mask = _nonsym_case()
+    # the host transpose is the reference's, bit for bit
+    t = sage_dist.transpose_host(rp, ci, v, x.shape[0])
+    for a, b in zip(t, port.transpose(rp, ci, v, x.shape[0])):
+        np.testing.assert_array_equal(np.asarray(a), np.asarray(b))
+    w0 = ref.init_model(kind, x.shape[1], 32, 4, 5)
+    want, _, _, _ = ref.train(kind, rp, ci, v, x, lab, mask, 32, 4, w0, 8, 0.05)
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port_ = _free_port()
+    procs = [ctx.Process(target=_nonsym_worker, args=(r, 2, port_, q, kind, w0)) for r in range(2)]
+    for p in procs:
+        p.start()
+    losses = q.get(timeout=180)
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    np.testing.assert_allclose(losses, want, rtol=2e-3, atol=1e-5)
+
+
 @pytest.mark.gpu
 @pytest.mark.parametrize("parts", [1, 2, 3, 8])
 def test_loopback_partition_bitwise_equals_single_gpu(cuda, parts):
