@@ -589,13 +589,16 @@ __global__ void __launch_bounds__(256) sage_grad_wt_kernel(const float* __restri
 // once and the logits never reach memory.  Block b owns rows [b*rpb,
 // (b+1)*rpb); loss / correct sums go to blk_loss[b] / blk_ok[b] in a fixed
 // order.
-template <int CP>
+template <int CP, int H>
 __global__ void __launch_bounds__(256) sage_head_kernel(
     const float* __restrict__ a2, const float* __restrict__ h1, const float* __restrict__ w2,
     const float* __restrict__ w2s, uint32_t n, uint32_t h, uint32_t c, const uint32_t* __restrict__ labels,
     const uint8_t* __restrict__ mask, double inv_n, uint32_t rpb, float* __restrict__ grad,
     float* __restrict__ ds2, double* __restrict__ blk_loss, uint32_t* __restrict__ blk_ok) {
-    constexpr int R = 32 / CP, J4 = CP / 4, NB = 32 / CP;  // rows per warp step; feature blocks per lane
+    // H sub-steps of R rows share every weight fragment read from shared
+    // memory (the pass is bound by those reads: 4 J4 + 4 J4 NB 16-byte loads
+    // per lane and step), each row's arithmetic unchanged
+    constexpr int R = 32 / CP, J4 = CP / 4, NB = 32 / CP;  // rows per warp sub-step; feature blocks per lane
     constexpr unsigned FULL = 0xffffffffu;
     __shared__ float4 sw[2][4 * J4 * 32];
     __shared__ double s_loss[8];
@@ -605,14 +608,14 @@ __global__ void __launch_bounds__(256) sage_head_kernel(
     __syncthreads();
     const uint32_t lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
     const bool act = lane < h / 4;
-    const uint32_t gl = lane % CP, grp = lane / CP;  // class / row-of-step after the reduce
+    const uint32_t gl = lane % CP, grp = lane / CP;  // class / row-of-sub-step after the reduce
     const uint32_t r0 = blockIdx.x * rpb, r1 = min(n, r0 + rpb);
     double lsum = 0.0;
     uint32_t oks = 0;
-    // the per-row log(den) is batched: a group's lane (step % CP) keeps the
-    // row's (mx, den, label logit), and every CP steps all lanes take their
-    // log at once (one log sequence per CP rows instead of one per row)
-    uint32_t step = 0;
+    // the per-row log(den) is batched: a group's lane (sub % CP) keeps the
+    // row's (mx, den, label logit), and every CP sub-steps all lanes take
+    // their log at once (one log sequence per CP rows instead of one per row)
+    uint32_t sub = 0;
     double p_mx = 0.0, p_den = 1.0;
     float p_vlab = 0.0f;
     bool p_has = false;
@@ -620,19 +623,21 @@ __global__ void __launch_bounds__(256) sage_head_kernel(
         if (p_has) lsum += (p_mx + log(p_den)) - double(p_vlab);
         p_has = false;
     };
-    for (uint32_t i0 = r0 + wid * R; i0 < r1; i0 += 8 * R, ++step) {
-        float v;
+    for (uint32_t i0 = r0 + wid * (R * H); i0 < r1; i0 += 8 * R * H) {
+        float v[H];
         {
-            float4 x[2][R];
+            float4 x[2][R * H];
 #pragma unroll
-            for (int r = 0; r < R; ++r) {
+            for (int r = 0; r < R * H; ++r) {
                 const bool ok = act && i0 + r < r1;
                 x[0][r] = ok ? __ldg(reinterpret_cast<const float4*>(a2 + uint64_t(i0 + r) * h) + lane) : make_float4(0.f, 0.f, 0.f, 0.f);
                 x[1][r] = ok ? __ldg(reinterpret_cast<const float4*>(h1 + uint64_t(i0 + r) * h) + lane) : make_float4(0.f, 0.f, 0.f, 0.f);
             }
-            float p[32];  // p[r * CP + j]
+            float p[H][32];  // p[hh][r * CP + j]
 #pragma unroll
-            for (int t = 0; t < 32; ++t) p[t] = 0.0f;
+            for (int hh = 0; hh < H; ++hh)
+#pragma unroll
+                for (int t = 0; t < 32; ++t) p[hh][t] = 0.0f;
 #pragma unroll
             for (int m = 0; m < 2; ++m)
 #pragma unroll
@@ -641,100 +646,118 @@ __global__ void __launch_bounds__(256) sage_head_kernel(
                     for (int j4 = 0; j4 < J4; ++j4) {
                         const float4 wv = sw[m][(q * J4 + j4) * 32 + lane];
 #pragma unroll
-                        for (int r = 0; r < R; ++r) {
-                            const float xv = q == 0 ? x[m][r].x : q == 1 ? x[m][r].y : q == 2 ? x[m][r].z : x[m][r].w;
-                            float* pr = p + r * CP + 4 * j4;
-                            // packed FFMA2 over class pairs (each half an ordinary fma)
-                            sgnn::dev::fma2_rn(pr[0], pr[1], xv, wv.x, wv.y);
-                            sgnn::dev::fma2_rn(pr[2], pr[3], xv, wv.z, wv.w);
-                        }
+                        for (int hh = 0; hh < H; ++hh)
+#pragma unroll
+                            for (int r = 0; r < R; ++r) {
+                                const float4 xr = x[m][hh * R + r];
+                                const float xv = q == 0 ? xr.x : q == 1 ? xr.y : q == 2 ? xr.z : xr.w;
+                                float* pr = p[hh] + r * CP + 4 * j4;
+                                // packed FFMA2 over class pairs (each half an ordinary fma)
+                                sgnn::dev::fma2_rn(pr[0], pr[1], xv, wv.x, wv.y);
+                                sgnn::dev::fma2_rn(pr[2], pr[3], xv, wv.z, wv.w);
+                            }
                     }
-            // 32-value transpose-reduce: lane l ends with index l
+            // 32-value transpose-reduce per sub-step: lane l ends with index l
 #pragma unroll
-            for (int sh = 16; sh >= 1; sh >>= 1) {
-                const bool up = (lane & sh) != 0;
+            for (int hh = 0; hh < H; ++hh) {
 #pragma unroll
-                for (int t = 0; t < sh; ++t) {
-                    const float send = up ? p[t] : p[sh + t];
-                    const float keep = up ? p[sh + t] : p[t];
-                    p[t] = __fadd_rn(keep, __shfl_xor_sync(FULL, send, sh));
+                for (int sh = 16; sh >= 1; sh >>= 1) {
+                    const bool up = (lane & sh) != 0;
+#pragma unroll
+                    for (int t = 0; t < sh; ++t) {
+                        const float send = up ? p[hh][t] : p[hh][sh + t];
+                        const float keep = up ? p[hh][sh + t] : p[hh][t];
+                        p[hh][t] = __fadd_rn(keep, __shfl_xor_sync(FULL, send, sh));
+                    }
                 }
+                v[hh] = p[hh][0];
             }
-            v = p[0];
         }
-        const uint32_t i = i0 + grp;
-        const bool row_ok = i < r1;
         const unsigned gmask = CP == 32 ? FULL : (((1u << CP) - 1u) << (lane & ~(CP - 1)));
         const bool cl = gl < c;
-        float g = 0.0f;
-        if (row_ok && mask[i]) {  // group-uniform
-            float mxf = -1.0f / 0.0f, bestv = -1.0f / 0.0f;
-            uint32_t best = 0;
-            if (cl) {
-                mxf = fmaxf(mxf, v);
-                if (v > bestv) {
-                    bestv = v;
-                    best = gl;
-                }
-            }
+        float g[H];
 #pragma unroll
-            for (int o = CP / 2; o >= 1; o >>= 1) {
-                mxf = fmaxf(mxf, __shfl_xor_sync(gmask, mxf, o, CP));
-                const float ov = __shfl_xor_sync(gmask, bestv, o, CP);
-                const uint32_t oj = __shfl_xor_sync(gmask, best, o, CP);
-                if (ov > bestv || (ov == bestv && oj < best)) {
-                    bestv = ov;
-                    best = oj;
-                }
-            }
-            const double mx = double(mxf);
-            const double e = cl ? exp(double(v) - mx) : 0.0;
-            double den = e;
-#pragma unroll
-            for (int o = CP / 2; o >= 1; o >>= 1) den += __shfl_xor_sync(gmask, den, o, CP);
-            const uint32_t lab = labels[i];
-            const float vlab = __shfl_sync(gmask, v, int(lab), CP);
-            if (cl) g = float((e / den - (gl == lab ? 1.0 : 0.0)) * inv_n);
-            if (gl == step % CP) {
-                p_mx = mx;
-                p_den = den;
-                p_vlab = vlab;
-                p_has = true;
-            }
-            if (gl == 0) oks += best == lab ? 1u : 0u;
-        }
-        if (step % CP == CP - 1) flush();
-        if (row_ok && cl) grad[uint64_t(i) * c + gl] = g;
-        // ds2[i, k] = sum_j grad[i, j] W2[k, j] (sage_grad_wt_kernel's chain)
-        float gj[CP];
-#pragma unroll
-        for (int j = 0; j < CP; ++j) gj[j] = __shfl_sync(FULL, g, j, CP);
-        if (row_ok) {
-#pragma unroll
-            for (int b = 0; b < NB; ++b) {
-                const uint32_t fb = gl + CP * b;  // feature block: features 4 fb .. 4 fb + 3
-                if (fb >= h / 4) break;
-                // features (4 fb + q, 4 fb + q + 1) as packed pairs: each half
-                // is sage_grad_wt_kernel's chain (mul, then fmas in class order)
-                float d[4];
-#pragma unroll
-                for (int q = 0; q < 4; q += 2) {
-#pragma unroll
-                    for (int j4 = 0; j4 < J4; ++j4) {
-                        const float4 wa = sw[0][(q * J4 + j4) * 32 + fb];
-                        const float4 wb = sw[0][((q + 1) * J4 + j4) * 32 + fb];
-                        if (j4 == 0) {
-                            d[q] = __fmul_rn(gj[0], wa.x);
-                            d[q + 1] = __fmul_rn(gj[0], wb.x);
-                        } else {
-                            sgnn::dev::fma2s_rn(d[q], d[q + 1], gj[4 * j4], wa.x, wb.x);
-                        }
-                        sgnn::dev::fma2s_rn(d[q], d[q + 1], gj[4 * j4 + 1], wa.y, wb.y);
-                        sgnn::dev::fma2s_rn(d[q], d[q + 1], gj[4 * j4 + 2], wa.z, wb.z);
-                        sgnn::dev::fma2s_rn(d[q], d[q + 1], gj[4 * j4 + 3], wa.w, wb.w);
+        for (int hh = 0; hh < H; ++hh, ++sub) {
+            const uint32_t i = i0 + hh * R + grp;
+            const bool row_ok = i < r1;
+            g[hh] = 0.0f;
+            if (row_ok && mask[i]) {  // group-uniform
+                float mxf = -1.0f / 0.0f, bestv = -1.0f / 0.0f;
+                uint32_t best = 0;
+                if (cl) {
+                    mxf = fmaxf(mxf, v[hh]);
+                    if (v[hh] > bestv) {
+                        bestv = v[hh];
+                        best = gl;
                     }
                 }
-                reinterpret_cast<float4*>(ds2 + uint64_t(i) * h)[fb] = make_float4(d[0], d[1], d[2], d[3]);
+#pragma unroll
+                for (int o = CP / 2; o >= 1; o >>= 1) {
+                    mxf = fmaxf(mxf, __shfl_xor_sync(gmask, mxf, o, CP));
+                    const float ov = __shfl_xor_sync(gmask, bestv, o, CP);
+                    const uint32_t oj = __shfl_xor_sync(gmask, best, o, CP);
+                    if (ov > bestv || (ov == bestv && oj < best)) {
+                        bestv = ov;
+                        best = oj;
+                    }
+                }
+                const double mx = double(mxf);
+                const double e = cl ? exp(double(v[hh]) - mx) : 0.0;
+                double den = e;
+#pragma unroll
+                for (int o = CP / 2; o >= 1; o >>= 1) den += __shfl_xor_sync(gmask, den, o, CP);
+                const uint32_t lab = labels[i];
+                const float vlab = __shfl_sync(gmask, v[hh], int(lab), CP);
+                if (cl) g[hh] = float((e / den - (gl == lab ? 1.0 : 0.0)) * inv_n);
+                if (gl == sub % CP) {
+                    p_mx = mx;
+                    p_den = den;
+                    p_vlab = vlab;
+                    p_has = true;
+                }
+                if (gl == 0) oks += best == lab ? 1u : 0u;
+            }
+            if (sub % CP == CP - 1) flush();
+            if (row_ok && cl) grad[uint64_t(i) * c + gl] = g[hh];
+        }
+        // ds2[i, k] = sum_j grad[i, j] W2[k, j] (sage_grad_wt_kernel's chain)
+        float gj[H][CP];
+#pragma unroll
+        for (int hh = 0; hh < H; ++hh)
+#pragma unroll
+            for (int j = 0; j < CP; ++j) gj[hh][j] = __shfl_sync(FULL, g[hh], j, CP);
+#pragma unroll
+        for (int b = 0; b < NB; ++b) {
+            const uint32_t fb = gl + CP * b;  // feature block: features 4 fb .. 4 fb + 3
+            if (fb >= h / 4) break;
+            // features (4 fb + q, 4 fb + q + 1) as packed pairs: each half
+            // is sage_grad_wt_kernel's chain (mul, then fmas in class order)
+            float d[H][4];
+#pragma unroll
+            for (int q = 0; q < 4; q += 2) {
+#pragma unroll
+                for (int j4 = 0; j4 < J4; ++j4) {
+                    const float4 wa = sw[0][(q * J4 + j4) * 32 + fb];
+                    const float4 wb = sw[0][((q + 1) * J4 + j4) * 32 + fb];
+#pragma unroll
+                    for (int hh = 0; hh < H; ++hh) {
+                        if (j4 == 0) {
+                            d[hh][q] = __fmul_rn(gj[hh][0], wa.x);
+                            d[hh][q + 1] = __fmul_rn(gj[hh][0], wb.x);
+                        } else {
+                            sgnn::dev::fma2s_rn(d[hh][q], d[hh][q + 1], gj[hh][4 * j4], wa.x, wb.x);
+                        }
+                        sgnn::dev::fma2s_rn(d[hh][q], d[hh][q + 1], gj[hh][4 * j4 + 1], wa.y, wb.y);
+                        sgnn::dev::fma2s_rn(d[hh][q], d[hh][q + 1], gj[hh][4 * j4 + 2], wa.z, wb.z);
+                        sgnn::dev::fma2s_rn(d[hh][q], d[hh][q + 1], gj[hh][4 * j4 + 3], wa.w, wb.w);
+                    }
+                }
+            }
+#pragma unroll
+            for (int hh = 0; hh < H; ++hh) {
+                const uint32_t i = i0 + hh * R + grp;
+                if (i < r1)
+                    reinterpret_cast<float4*>(ds2 + uint64_t(i) * h)[fb] = make_float4(d[hh][0], d[hh][1], d[hh][2], d[hh][3]);
             }
         }
     }
@@ -792,6 +815,15 @@ unsigned grid_for(uint64_t n) {
 
 // softmax_xent launch shape for n rows: rows per block and blocks (a fixed
 // function of n, so the loss reduction order is too)
+int head_substeps() {
+    static const int h = [] {
+        const char* e = std::getenv("SGNN_HEAD_H");
+        const int v = e ? std::atoi(e) : 2;
+        return (v == 1 || v == 4) ? v : 2;
+    }();
+    return h;
+}
+
 void softmax_shape(uint32_t n, uint32_t* rpb, uint32_t* blocks) {
     const uint32_t want = 2048;  // blocks (~14 per SM)
     uint32_t r = (n + want - 1) / want;
@@ -922,6 +954,21 @@ sgnn_status fwd_spmm(sgnn_gnn_s* g, const float* x, uint32_t k, float* out, int 
         else kernel<16><<<(grid), (block), 0, s>>> args;                      \
         SGNN_LAUNCH_CHECK();                                                   \
     } while (0)
+// the fused head: H sub-steps per warp step (SGNN_HEAD_H = 1 / 2 / 4: A/B switch)
+#define SAGE_HEAD_H(CPV, hsel, grid, args)                                                      \
+    do {                                                                                        \
+        if ((hsel) == 1) sage_head_kernel<CPV, 1><<<(grid), 256, 0, s>>> args;                  \
+        else if ((hsel) == 4) sage_head_kernel<CPV, 4><<<(grid), 256, 0, s>>> args;             \
+        else sage_head_kernel<CPV, 2><<<(grid), 256, 0, s>>> args;                              \
+    } while (0)
+#define SAGE_HEAD(cls, grid, args)                                             \
+    do {                                                                       \
+        const int hsel_ = head_substeps();                                     \
+        if ((cls) <= 4) SAGE_HEAD_H(4, hsel_, grid, args);                     \
+        else if ((cls) <= 8) SAGE_HEAD_H(8, hsel_, grid, args);                \
+        else SAGE_HEAD_H(16, hsel_, grid, args);                               \
+        SGNN_LAUNCH_CHECK();                                                   \
+    } while (0)
 // float4 element-wise kernels (ew_loop): a quarter of the threads
 #define LAUNCH_EW4(kernel, n, ...)                                             \
     do {                                                                       \
@@ -952,7 +999,7 @@ sgnn_status epoch(sgnn_gnn_s* g, float lr, cudaStream_t s) {
             // (sage_head_kernel); the loss partials feed epoch_stats below
             uint32_t rpb = 1, nblk = 1;
             softmax_shape(g->n, &rpb, &nblk);
-            SAGE_CP(sage_head_kernel, g->cls, nblk, 256,
+            SAGE_HEAD(g->cls, nblk,
                     (g->a2, g->h1, g->w2, g->w2s, g->n, g->hid, g->cls, g->labels, g->mask,
                      1.0 / double(g->n_masked), rpb, g->grad, g->d_h, g->row_loss, g->row_ok));
         } else {
@@ -1360,7 +1407,7 @@ sgnn_status sage_head_partials(const float* a2, const float* h1, const float* w2
     if (n == 0) return SGNN_OK;
     uint32_t rpb = 1, nblk = 1;
     softmax_shape(n, &rpb, &nblk);
-    SAGE_CP(sage_head_kernel, c, nblk, 256,
+    SAGE_HEAD(c, nblk,
             (a2, h1, w2, w2s, n, h, c, labels, mask, inv_count, rpb, grad, ds2, blk_loss, blk_ok));
     return SGNN_OK;
 }
