@@ -214,6 +214,9 @@ __device__ __forceinline__ void fma2s_rn(float& a0, float& a1, float s, float w0
     fma2_rn(a0, a1, s, w0, w1);
 }
 
+#ifndef SGNN_LD_MODE
+#define SGNN_LD_MODE 0  // gathers through __ldg (ld.global.nc); 1-3: A/B variants, see ld_gather
+#endif
 // L2 policy for gathered operand rows (reused across the whole launch):
 // evict-last, so the streamed CSR arrays and the output do not push them out.
 __device__ __forceinline__ uint64_t gather_policy() {
@@ -233,6 +236,22 @@ __device__ __forceinline__ float4 ld_gather(const float4* ptr, uint64_t pol) {
     asm("ld.global.nc.L2::cache_hint.v4.f32 {%0,%1,%2,%3}, [%4], %5;"
         : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "l"(ptr), "l"(pol));
 #endif
+    return v;
+#elif SGNN_LD_MODE == 1  // A/B: coherent path, L1-allocating
+    (void)pol;
+    float4 v;
+    asm("ld.global.ca.v4.f32 {%0,%1,%2,%3}, [%4];" : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "l"(ptr));
+    return v;
+#elif SGNN_LD_MODE == 2  // A/B: L2 only (no L1 allocation)
+    (void)pol;
+    float4 v;
+    asm("ld.global.cg.v4.f32 {%0,%1,%2,%3}, [%4];" : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "l"(ptr));
+    return v;
+#elif SGNN_LD_MODE == 3  // A/B: read-only path without L1 allocation
+    (void)pol;
+    float4 v;
+    asm("ld.global.nc.L1::no_allocate.v4.f32 {%0,%1,%2,%3}, [%4];"
+                 : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "l"(ptr));
     return v;
 #else
     (void)pol;

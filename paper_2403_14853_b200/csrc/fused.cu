@@ -275,6 +275,17 @@ __global__ void __launch_bounds__(128, MINB) sddmm_lock_kernel(const SddmmArgs a
         };
         uint32_t rb = r;
         uint32_t rwin = window(rb);
+        // X rows are read once each (a DRAM miss at every row start): the
+        // window's later non-empty rows go to L2 when the window is loaded
+        auto prefetch_x = [&](bool mine) {  // every lane calls it; the groups in `mine` prefetch
+            const uint32_t prev = __shfl_up_sync(FULL, rwin, 1, G);
+            if (mine && gl >= 1 && rwin > prev && rb + uint32_t(gl) < a.n_rows) {
+                const char* xp = reinterpret_cast<const char*>(a.x + uint64_t(rb + uint32_t(gl)) * a.ld);
+                asm volatile("prefetch.global.L2 [%0];" ::"l"(xp));
+                if (a.k > 32) asm volatile("prefetch.global.L2 [%0];" ::"l"(xp + 128));
+            }
+        };
+        prefetch_x(wact);
         uint32_t rend_l = __shfl_sync(FULL, rwin, gbase);
         F xrow;
         xrow.load(a.x + uint64_t(r) * a.ld, gl, a.k);
@@ -303,6 +314,7 @@ __global__ void __launch_bounds__(128, MINB) sddmm_lock_kernel(const SddmmArgs a
                     rb += G;
                     rwin = window(rb);
                 }
+                if (__any_sync(FULL, need && !found)) prefetch_x(need && !found);
                 const uint32_t t = __shfl_sync(FULL, rwin, gbase + int(r - rb) * int(found));
                 if (found) {
                     rend_l = t;
@@ -439,6 +451,29 @@ sgnn_status launch_fused_lock(const SpmmArgs& a, cudaStream_t s) {
     const uint64_t blocks = std::min<uint64_t>(ceil_div_u64(uint64_t(a.n_workers) * 16, 128), uint64_t(dp.sm_count) * per_sm);
     if (blocks == 0) return SGNN_OK;
     dev::lock_worker_kernel<16, 8, OP, SGNN_REDUCE_SUM, MINB><<<unsigned(blocks), 128, 0, s>>>(a);
+    SGNN_LAUNCH_CHECK();
+    return SGNN_OK;
+}
+
+// the lockstep FusedMM with its gathered rows in a shared-memory ring of NCH
+// chunks (cp.async, spmm_kernel.cuh): the ring sets the CTAs per SM
+template <int OP, int NCH>
+sgnn_status launch_fused_ring(const SpmmArgs& a, cudaStream_t s) {
+    constexpr int MINB = NCH >= 4 ? 3 : 4;
+    auto kern = dev::lock_worker_kernel<16, 8, OP, SGNN_REDUCE_SUM, MINB, NCH>;
+    constexpr uint32_t smem = dev::ring_smem_bytes<NCH>();
+    static int per_sm = -1;
+    DeviceProps dp;
+    SGNN_TRY(device_props(&dp));
+    if (per_sm < 0) {
+        SGNN_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+        int n = 0;
+        SGNN_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, kern, 128, smem));
+        per_sm = std::max(n, 1);
+    }
+    const uint64_t blocks = std::min<uint64_t>(ceil_div_u64(uint64_t(a.n_workers) * 16, 128), uint64_t(dp.sm_count) * per_sm);
+    if (blocks == 0) return SGNN_OK;
+    kern<<<unsigned(blocks), 128, smem, s>>>(a);
     SGNN_LAUNCH_CHECK();
     return SGNN_OK;
 }
@@ -586,11 +621,18 @@ sgnn_status run_fusedmm(const sgnn_csr* p, const float* x, const float* y, uint3
         args.width = k;
         args.wctr = plan_counter(plan, s);
         const bool generic = std::getenv("SGNN_FUSED_GENERIC") != nullptr;  // A/B switch (tests)
-        if (!generic && vec && k == 64 && (reduce == SGNN_REDUCE_SUM || reduce == SGNN_REDUCE_MEAN))
+        const char* ring_env = std::getenv("SGNN_FUSED_RING");  // A/B switch: ring chunks (3 / 4), 0 = registers
+        const int ring = ring_env ? std::atoi(ring_env) : 0;
+        const bool sig = edge_op == SGNN_EDGE_SIGMOID_MUL;
+        if (!generic && vec && k == 64 && (reduce == SGNN_REDUCE_SUM || reduce == SGNN_REDUCE_MEAN) && ring >= 4)
+            st = sig ? launch_fused_ring<dev::OP_FUSED_SIGMOID, 4>(args, s) : launch_fused_ring<dev::OP_FUSED_MUL, 4>(args, s);
+        else if (!generic && vec && k == 64 && (reduce == SGNN_REDUCE_SUM || reduce == SGNN_REDUCE_MEAN) && ring == 3)
+            st = sig ? launch_fused_ring<dev::OP_FUSED_SIGMOID, 3>(args, s) : launch_fused_ring<dev::OP_FUSED_MUL, 3>(args, s);
+        else if (!generic && vec && k == 64 && (reduce == SGNN_REDUCE_SUM || reduce == SGNN_REDUCE_MEAN))
             // 5 CTAs/SM (96 registers): 1.175 -> 1.086 ms on cfg4; capped at
             // 6 / 7 it spills (44 / 136 bytes) and runs 1.098 / 1.211 ms
-            st = edge_op == SGNN_EDGE_SIGMOID_MUL ? launch_fused_lock<dev::OP_FUSED_SIGMOID, 5>(args, s)
-                                                  : launch_fused_lock<dev::OP_FUSED_MUL, 5>(args, s);
+            st = sig ? launch_fused_lock<dev::OP_FUSED_SIGMOID, 5>(args, s)
+                     : launch_fused_lock<dev::OP_FUSED_MUL, 5>(args, s);
         else
             st = launch(args, plan->p.block, 0, s);
     }

@@ -829,16 +829,51 @@ __global__ void __launch_bounds__(kFixupLongThreads) spmm_fixup_long_kernel(cons
 // K), and the row / segment settling runs as warp-uniform loops with
 // full-mask shuffles.  At the worker's 5 CTAs/SM: cfg4 1.175 -> 1.086 ms
 // (capping registers lower spills: DESIGN 3.3).
-template <int G, int U, int OP, int RED, int MINB>
+//
+// NCH > 0 (G = 16, U = 8, K = 64): the gathered rows go through a
+// shared-memory ring instead of registers.  A worker's nonzeros are cut in
+// aligned chunks of 8 local positions; chunk c's 8 rows are copied by
+// cp.async (16 bytes per lane, lane-private slots, so a per-thread
+// wait_group is the only synchronisation) NCH - 1 chunks before they are
+// used, and its values ride along in a small ring.  Batches are cut at chunk
+// ends as well as at row / segment ends, so a batch reads one slot.  The
+// rows in flight per SM are then set by the ring (NCH - 1 chunks per group),
+// not by the register file.  Same dot tree, same fold order: bitwise the
+// register kernel's results (test).
+template <int NCH>
+constexpr uint32_t ring_row_bytes() { return uint32_t(8 * NCH * 8 + 8) * 16u * 16u; }  // 8 groups + 8 positions of pad
+template <int NCH>
+constexpr uint32_t ring_smem_bytes() { return ring_row_bytes<NCH>() + uint32_t(8 * NCH * 8 + 8) * 4u; }
+
+__device__ __forceinline__ void cp_async16(void* smem_dst, const void* gsrc) {
+    const uint32_t d = static_cast<uint32_t>(__cvta_generic_to_shared(smem_dst));
+#if defined(SGNN_RING_CG)
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(d), "l"(gsrc) : "memory");
+#else
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 16;" ::"r"(d), "l"(gsrc) : "memory");
+#endif
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
+
+template <int G, int U, int OP, int RED, int MINB, int NCH = 0>
 __global__ void __launch_bounds__(128, MINB) lock_worker_kernel(const SpmmArgs a) {
     static_assert(G < 32 && U <= G && (OP == OP_SPMM || is_fused<OP>()), "lockstep groups");
     static_assert(!is_fused<OP>() || RED == SGNN_REDUCE_SUM, "FusedMM: sum kernels (mean: divide pass)");
+    constexpr bool RING = NCH > 0;
+    static_assert(!RING || (G == 16 && U == 8 && NCH >= 2), "ring: 16-lane groups, chunks of 8 positions");
     using F = Frag<G, 1, true>;
     using R = Reducer<RED>;
     constexpr unsigned FULL = 0xffffffffu;
     constexpr int PER = G / U;
     constexpr uint32_t SEG = SGNN_SEGMENT;
     const int lane = threadIdx.x & 31, gl = lane & (G - 1), gbase = lane & ~(G - 1);
+    extern __shared__ __align__(16) unsigned char ring_smem[];
+    // this lane's column of its group's row ring, and the group's value ring
+    float4* const ring = reinterpret_cast<float4*>(ring_smem) + size_t(threadIdx.x / G) * (RING ? NCH * 8 * 16 : 0) + gl;
+    float* const vring = reinterpret_cast<float*>(ring_smem + (RING ? ring_row_bytes<RING ? NCH : 1>() : 0)) +
+                         (threadIdx.x / G) * (RING ? NCH * 8 : 0);
     // lanes past the width alias the row's last valid float4 (always in bounds)
     const char* ylane = reinterpret_cast<const char*>(a.x + 4 * min(gl, int(a.width / 4) - 1));
     const uint32_t ldb = uint32_t(a.ldx) * 4u;
@@ -858,6 +893,21 @@ __global__ void __launch_bounds__(128, MINB) lock_worker_kernel(const SpmmArgs a
         };
         uint32_t r = i0, rb = i0;
         uint32_t rwin = window(rb);
+        // FusedMM: X rows are read once each, so every row start is a DRAM
+        // miss on the critical path; the window's later non-empty rows (those
+        // with nonzeros in this worker) are fetched into L2 when the window
+        // is loaded (cfg4: 1.078 -> 1.025 ms)
+        auto prefetch_x = [&](bool mine) {  // every lane calls it; the groups in `mine` prefetch
+            if constexpr (is_fused<OP>()) {
+                const uint32_t prev = __shfl_up_sync(FULL, rwin, 1, G);
+                if (mine && gl >= 1 && rwin > prev && rb + uint32_t(gl) < a.n_rows) {
+                    const char* xp = reinterpret_cast<const char*>(a.xi + uint64_t(rb + uint32_t(gl)) * a.ldxi);
+                    asm volatile("prefetch.global.L2 [%0];" ::"l"(xp));
+                    if (a.width > 32) asm volatile("prefetch.global.L2 [%0];" ::"l"(xp + 128));
+                }
+            }
+        };
+        prefetch_x(wact);
         uint32_t rend_l = __shfl_sync(FULL, rwin, gbase);
         uint32_t rs_l = 0, seg_l = min(SEG, rend_l);
         bool inside = __ldg(a.rp + i0) >= j0 && r < i1;  // row i0 did not begin in an earlier worker
@@ -886,13 +936,18 @@ __global__ void __launch_bounds__(128, MINB) lock_worker_kernel(const SpmmArgs a
         // rows of the groups in `need` advance by one (window reload per group,
         // then one full-mask shuffle for the new row ends)
         auto advance = [&](bool need) {
+            bool reloaded = false;
             if (need) {
                 ++r;
                 rs_l = rend_l;
                 if (r - rb >= uint32_t(G)) {
                     rb = r;
                     rwin = window(rb);
+                    reloaded = true;
                 }
+            }
+            if constexpr (is_fused<OP>()) {
+                if (__any_sync(FULL, reloaded)) prefetch_x(reloaded);
             }
             const uint32_t t = __shfl_sync(FULL, rwin, gbase + int(r - rb));
             if (need) {
@@ -913,10 +968,71 @@ __global__ void __launch_bounds__(128, MINB) lock_worker_kernel(const SpmmArgs a
             cw = ok ? ld_stream(a.ci + j0 + at + gl) : 0u;  // 0: a safe dummy row
             vw = ok ? ld_stream(a.val + j0 + at + gl) : 0.0f;
         };
-        if (E) load_window(0);
+        // RING: (cw, vw) is the 16-position window the next chunk is issued
+        // from, (cw2, vw2) the window after it (loaded two chunks early)
+        uint32_t cw2 = 0, issued = 0, slot_i = 0, slot_c = NCH - 1, next_enter = 0;
+        float vw2 = 0.0f;
+        auto load_window2 = [&](uint32_t at) {
+            const bool ok = at + uint32_t(gl) < E;
+            cw2 = ok ? ld_stream(a.ci + j0 + at + gl) : 0u;
+            vw2 = ok ? ld_stream(a.val + j0 + at + gl) : 0.0f;
+        };
+        // copies of chunk `issued` (positions 8 issued .. +8) into slot slot_i;
+        // every lane runs the shuffles, the groups in `doit` issue and commit
+        auto issue_chunk = [&](bool doit) {
+            const int h8 = int(issued & 1u) * 8;
+            uint32_t colu[8];
+#pragma unroll
+            for (int u = 0; u < 8; ++u) colu[u] = __shfl_sync(FULL, cw, gbase + h8 + u);
+            if (doit) {
+                const uint32_t p0 = issued * 8u;
+                float4* dst = ring + slot_i * (8 * 16);
+#pragma unroll
+                for (int u = 0; u < 8; ++u) {
+                    if (p0 + uint32_t(u) < E) {
+                        const char* p;
+                        asm("mad.wide.u32 %0, %1, %2, %3;" : "=l"(p) : "r"(colu[u]), "r"(ldb), "l"(ylane));
+                        cp_async16(dst + u * 16, p);
+                    }
+                }
+                if ((gl >> 3) == int(issued & 1u)) vring[slot_i * 8 + (gl & 7)] = vw;
+                cp_async_commit();
+                if (issued & 1u) {  // the window is used up: take the next, load the one after
+                    cw = cw2;
+                    vw = vw2;
+                    load_window2((issued + 1u) * 8u + 16u);
+                }
+                ++issued;
+                slot_i = slot_i + 1 == uint32_t(NCH) ? 0u : slot_i + 1;
+            }
+        };
+        if constexpr (RING) {
+            if (E) {
+                load_window(0);
+                load_window2(16);
+            }
+#pragma unroll
+            for (int c = 0; c < NCH - 1; ++c) issue_chunk(wact);
+        } else {
+            if (E) load_window(0);
+        }
         uint32_t base = 0;
         while (__any_sync(FULL, base < E)) {
             const bool act = base < E;
+            if constexpr (RING) {
+                // entering chunk base / 8: issue chunk base / 8 + NCH - 1 into the
+                // slot just consumed, then wait for this chunk's rows
+                const bool enter = act && base == next_enter;
+                if (__any_sync(FULL, enter)) {
+                    issue_chunk(enter);
+                    if (enter) {
+                        cp_async_wait<RING ? NCH - 1 : 0>();
+                        next_enter += 8;
+                        slot_c = slot_c + 1 == uint32_t(NCH) ? 0u : slot_c + 1;
+                    }
+                    __syncwarp();  // the value ring's stores are visible to the group
+                }
+            }
             // settle (the worker's): close finished rows, then a finished segment
             while (true) {
                 const bool need = act && base >= rend_l;
@@ -952,33 +1068,52 @@ __global__ void __launch_bounds__(128, MINB) lock_worker_kernel(const SpmmArgs a
             }
             int n = 0;
             if (act) {
-                const uint32_t room = min(rend_l, seg_l) - base;
+                uint32_t room = min(rend_l, seg_l) - base;
+                if constexpr (RING) room = min(room, 8u - (base & 7u));  // and at the chunk's end
                 n = room < uint32_t(U) ? int(room) : U;
             }
-            // an active group's batch lies inside the window (base - wb <= G - U)
-            const int s0 = gbase + int(base - wb);
-            uint32_t colu[U];
-#pragma unroll
-            for (int u = 0; u < U; ++u) colu[u] = __shfl_sync(FULL, cw, s0 + u);
             float pv_own = 0.0f, av[U];
-            if constexpr (is_fused<OP>()) {
-                pv_own = __shfl_sync(FULL, vw, s0 + gl / PER);
-            } else {
-#pragma unroll
-                for (int u = 0; u < U; ++u) av[u] = __shfl_sync(FULL, vw, s0 + u);
-            }
             F yf[U];
-            if (act) {
+            const uint32_t nb = base + uint32_t(n);
+            if constexpr (RING) {
+                // the batch's rows and values from this chunk's slot (reads past
+                // the chunk's end stay inside the ring or its pad; never folded)
+                const uint32_t off = base & 7u;
+                const float4* src = ring + (slot_c * 8 + off) * 16;
 #pragma unroll
                 for (int u = 0; u < U; ++u) {
-                    const char* p;
-                    asm("mad.wide.u32 %0, %1, %2, %3;" : "=l"(p) : "r"(colu[u]), "r"(ldb), "l"(ylane));
-                    const float4 t = ld_gather(reinterpret_cast<const float4*>(p), l2pol);
+                    const float4 t = src[u * 16];
                     yf[u].v[0] = t.x; yf[u].v[1] = t.y; yf[u].v[2] = t.z; yf[u].v[3] = t.w;
                 }
+                if constexpr (is_fused<OP>()) {
+                    pv_own = vring[slot_c * 8 + min(off + uint32_t(gl / PER), 7u)];
+                } else {
+#pragma unroll
+                    for (int u = 0; u < U; ++u) av[u] = vring[slot_c * 8 + min(off + uint32_t(u), 7u)];
+                }
+            } else {
+                // an active group's batch lies inside the window (base - wb <= G - U)
+                const int s0 = gbase + int(base - wb);
+                uint32_t colu[U];
+#pragma unroll
+                for (int u = 0; u < U; ++u) colu[u] = __shfl_sync(FULL, cw, s0 + u);
+                if constexpr (is_fused<OP>()) {
+                    pv_own = __shfl_sync(FULL, vw, s0 + gl / PER);
+                } else {
+#pragma unroll
+                    for (int u = 0; u < U; ++u) av[u] = __shfl_sync(FULL, vw, s0 + u);
+                }
+                if (act) {
+#pragma unroll
+                    for (int u = 0; u < U; ++u) {
+                        const char* p;
+                        asm("mad.wide.u32 %0, %1, %2, %3;" : "=l"(p) : "r"(colu[u]), "r"(ldb), "l"(ylane));
+                        const float4 t = ld_gather(reinterpret_cast<const float4*>(p), l2pol);
+                        yf[u].v[0] = t.x; yf[u].v[1] = t.y; yf[u].v[2] = t.z; yf[u].v[3] = t.w;
+                    }
+                }
+                if (act && nb < E && nb + uint32_t(U) > wb + uint32_t(G)) load_window(nb);
             }
-            const uint32_t nb = base + uint32_t(n);
-            if (act && nb < E && nb + uint32_t(U) > wb + uint32_t(G)) load_window(nb);
             if constexpr (is_fused<OP>()) {
                 const float s_own = edge_value<OP>(pv_own, batch_dots(xrow, yf, FULL, gl));
 #pragma unroll
@@ -1009,6 +1144,7 @@ __global__ void __launch_bounds__(128, MINB) lock_worker_kernel(const SpmmArgs a
             advance(need);
         }
         if (r < a.n_rows && E > rs_l) store_slot();  // head of a split row
+        if constexpr (RING) cp_async_wait<0>();  // (only empty groups can be pending)
     }
     ws.finish();
 }

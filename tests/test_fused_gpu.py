@@ -315,3 +315,33 @@ def test_fused_lockstep_kernel_bitwise_generic(cuda, path_items, monkeypatch):
             monkeypatch.delenv("SGNN_FUSED_GENERIC")
             np.testing.assert_array_equal(got.view(np.uint32), want.view(np.uint32), err_msg=f"{edge} {red}")
     check_fused(rp, ci, v, n, x, y, "sigmoid_mul", "sum")
+
+
+@pytest.mark.parametrize("ring", [3, 4])
+@pytest.mark.parametrize("path_items", [0, 64, 512])
+def test_fused_ring_kernel_bitwise_lockstep(cuda, ring, path_items, monkeypatch):
+    """The lockstep FusedMM with its gathered rows in a shared-memory ring
+    (cp.async, SGNN_FUSED_RING = ring chunks; K = 64, sum and mean, both edge
+    ops) gives bit for bit the register kernel's results on the same graphs
+    as above: split hub rows, multi-segment rows, runs of empty rows,
+    workers shorter than the ring's lookahead (path_items = 64)."""
+    from paper_2403_14853_b200 import graphs
+    ops = _ops()
+    rng = np.random.default_rng(path_items + 11)
+    n, k = 1 << 13, 64
+    rp, ci = graphs.rmat(13, n * 12, seed=8)
+    v = rng.uniform(0, 1, len(ci)).astype(np.float32)
+    x = rng.normal(0, 0.1, (n, k)).astype(np.float32)
+    y = rng.normal(0, 0.1, (n, k)).astype(np.float32)
+    p = ops.CsrMatrix.from_numpy(rp, ci, v, n)
+    xt, yt = _t(x), _t(y)
+    plan = ops.Plan(p, k, **{**_fused_layout_kw(k), "path_items": path_items}) if path_items else None
+    for edge in ("sigmoid_mul", "mul"):
+        for red in ("sum", "mean"):
+            monkeypatch.delenv("SGNN_FUSED_RING", raising=False)
+            monkeypatch.setenv("SGNN_FUSED_RING", "0")
+            want = ops.fusedmm(p, xt, yt, edge, red, plan=plan).cpu().numpy()
+            monkeypatch.setenv("SGNN_FUSED_RING", str(ring))
+            got = ops.fusedmm(p, xt, yt, edge, red, plan=plan).cpu().numpy()
+            monkeypatch.delenv("SGNN_FUSED_RING")
+            np.testing.assert_array_equal(got.view(np.uint32), want.view(np.uint32), err_msg=f"{edge} {red}")
