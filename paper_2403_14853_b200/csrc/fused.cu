@@ -457,9 +457,8 @@ sgnn_status launch_fused_lock(const SpmmArgs& a, cudaStream_t s) {
 
 // the lockstep FusedMM with its gathered rows in a shared-memory ring of NCH
 // chunks (cp.async, spmm_kernel.cuh): the ring sets the CTAs per SM
-template <int OP, int NCH>
+template <int OP, int NCH, int MINB = (NCH >= 4 ? 3 : NCH == 3 ? 4 : 5)>
 sgnn_status launch_fused_ring(const SpmmArgs& a, cudaStream_t s) {
-    constexpr int MINB = NCH >= 4 ? 3 : 4;
     auto kern = dev::lock_worker_kernel<16, 8, OP, SGNN_REDUCE_SUM, MINB, NCH>;
     constexpr uint32_t smem = dev::ring_smem_bytes<NCH>();
     static int per_sm = -1;
@@ -621,11 +620,13 @@ sgnn_status run_fusedmm(const sgnn_csr* p, const float* x, const float* y, uint3
         args.width = k;
         args.wctr = plan_counter(plan, s);
         const bool generic = std::getenv("SGNN_FUSED_GENERIC") != nullptr;  // A/B switch (tests)
-        const char* ring_env = std::getenv("SGNN_FUSED_RING");  // A/B switch: ring chunks (3 / 4), 0 = registers
+        const char* ring_env = std::getenv("SGNN_FUSED_RING");  // A/B switch: ring chunks (2 / 3 / 4), else registers
         const int ring = ring_env ? std::atoi(ring_env) : 0;
         const bool sig = edge_op == SGNN_EDGE_SIGMOID_MUL;
-        if (!generic && vec && k == 64 && (reduce == SGNN_REDUCE_SUM || reduce == SGNN_REDUCE_MEAN) && ring >= 4)
+        if (!generic && vec && k == 64 && (reduce == SGNN_REDUCE_SUM || reduce == SGNN_REDUCE_MEAN) && ring == 4)
             st = sig ? launch_fused_ring<dev::OP_FUSED_SIGMOID, 4>(args, s) : launch_fused_ring<dev::OP_FUSED_MUL, 4>(args, s);
+        else if (!generic && vec && k == 64 && (reduce == SGNN_REDUCE_SUM || reduce == SGNN_REDUCE_MEAN) && ring == 2)
+            st = sig ? launch_fused_ring<dev::OP_FUSED_SIGMOID, 2>(args, s) : launch_fused_ring<dev::OP_FUSED_MUL, 2>(args, s);
         else if (!generic && vec && k == 64 && (reduce == SGNN_REDUCE_SUM || reduce == SGNN_REDUCE_MEAN) && ring == 3)
             st = sig ? launch_fused_ring<dev::OP_FUSED_SIGMOID, 3>(args, s) : launch_fused_ring<dev::OP_FUSED_MUL, 3>(args, s);
         else if (!generic && vec && k == 64 && (reduce == SGNN_REDUCE_SUM || reduce == SGNN_REDUCE_MEAN))

@@ -317,7 +317,7 @@ def test_fused_lockstep_kernel_bitwise_generic(cuda, path_items, monkeypatch):
     check_fused(rp, ci, v, n, x, y, "sigmoid_mul", "sum")
 
 
-@pytest.mark.parametrize("ring", [3, 4])
+@pytest.mark.parametrize("ring", [2, 3, 4])
 @pytest.mark.parametrize("path_items", [0, 64, 512])
 def test_fused_ring_kernel_bitwise_lockstep(cuda, ring, path_items, monkeypatch):
     """The lockstep FusedMM with its gathered rows in a shared-memory ring
